@@ -1,0 +1,242 @@
+/*
+ * sparsekit_b200.h — C ABI of libsparsekit_b200.so, the B200 (sm_100a) native
+ * implementation of the RecIS dynamic-embedding hot path.
+ *
+ * The reference (`sparsekit`, /root/reference/pkg/src/sparsekit) is a Python
+ * package with no FFI; each entry point below names the reference function it
+ * replaces (file:line).  The Python package `paper_2509_20883_b200` binds these
+ * with ctypes and keeps the reference's Python API on top.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors)
+ *    unless the parameter name ends in `_host`.  Sizes are int64_t.
+ *  - `stream` is a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
+ *    work is stream-ordered.  Calls that must report a data-dependent error
+ *    (ValueError / IndexError in the reference) synchronize `stream` once.
+ *  - Return value: SKB_OK or an SKB_E_* status; skb_last_error() gives the
+ *    thread-local message and skb_last_error_arg() the offending value (first
+ *    bad offset, duplicate id, ...).  The Python layer maps SKB_E_VALUE ->
+ *    ValueError, SKB_E_INDEX -> IndexError, SKB_E_KEY -> KeyError.
+ *  - Floating point rows/state are float32; ids/offsets/steps are int64.
+ *  - A table handle is single-writer: one stream at a time may mutate it
+ *    (embedding.py:10-11).  Distinct handles may run concurrently.
+ */
+#ifndef SPARSEKIT_B200_H
+#define SPARSEKIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SKB_OK 0
+#define SKB_E_VALUE 1       /* reference raises ValueError  */
+#define SKB_E_INDEX 2       /* reference raises IndexError  */
+#define SKB_E_KEY 3         /* reference raises KeyError    */
+#define SKB_E_CUDA 4        /* CUDA runtime failure          */
+#define SKB_E_NOMEM 5       /* device allocation failure     */
+#define SKB_E_ARG 6         /* bad argument at the C boundary */
+#define SKB_E_UNSUPPORTED 7
+
+typedef struct skb_table* skb_table_t;
+
+/* Host-computed float32 Adam scalars, exactly as optim.py:69-75 forms them
+ * (bias corrections use Python double pow, then round to float32). */
+typedef struct {
+  float lr, beta1, beta2, eps;
+  float one_minus_beta1, one_minus_beta2; /* float32(1) - float32(beta) */
+  float bc1, bc2;                         /* float32(1 - beta**t)       */
+  float lr_wd;                            /* float32(lr) * float32(wd)  */
+  int32_t decoupled_decay;                /* variant == adamw and wd != 0 */
+} skb_adam_t;
+
+/* ---- library ---------------------------------------------------------- */
+const char* skb_version(void);
+const char* skb_last_error(void);
+int64_t skb_last_error_arg(void);
+int skb_device_sm_count(int device, int* out_host);
+
+/* ---- L0 hashing: hashing.py:35-40, sharding.py:41-43, sharding.py:170-178 */
+/* out[i] = int64(mix64(u64(ids[i])))                       hashing.py:35-40 */
+int skb_mix64(const int64_t* ids, int64_t n, int64_t* out, void* stream);
+/* out[i] = mix64(ids[i]) % S  (unsigned)        ShardPlan.shard_of sharding.py:41-43 */
+int skb_shard_of(const int64_t* ids, int64_t n, int64_t num_shards, int64_t* out, void* stream);
+/* out[i] = int64(mix64(u64(ids[i]) ^ salt))     LogicalTable.keys_for sharding.py:170-178 */
+int skb_keys_for(const int64_t* ids, int64_t n, uint64_t salt, int64_t* out, void* stream);
+/* FNV-1a 64 of one host byte string (member salts)           hashing.py:43-48 */
+uint64_t skb_fnv1a64_host(const uint8_t* bytes_host, int64_t len);
+/* out[i] = FNV-1a64(blob[offs[i]:offs[i+1]]) as int64   fnv1a64_batch hashing.py:51-71,
+ * hash_feature features.py:30-38 */
+int skb_fnv1a64_strings(const uint8_t* blob, const int64_t* str_offs, int64_t n, int64_t* out,
+                        void* stream);
+/* out[i] = FNV-1a64(LE8(x[i]) || LE8(y[i]))                fnv1a64_pairs hashing.py:74-86 */
+int skb_fnv1a64_pairs(const int64_t* x, const int64_t* y, int64_t n, int64_t* out, void* stream);
+
+/* ---- L3 dedup + owner partition: unique_partition sharding.py:74-100 ---- */
+/* uniq_out[n]: per-shard unique ids in global first-occurrence order, shard 0
+ * first, then shard 1, ...; shard_counts_out[S] (device) their counts;
+ * inv_shard[n], inv_pos[n] the inverse routing index (PartitionResult). */
+int skb_unique_partition(const int64_t* ids, int64_t n, int64_t num_shards, int64_t* uniq_out,
+                         int64_t* shard_counts_out, int64_t* inv_shard, int64_t* inv_pos,
+                         void* stream);
+/* out[i,:] = rows_cat[shard_base[inv_shard[i]] + inv_pos[i], :]
+ *                                          PartitionResult.restore sharding.py:58-66 */
+int skb_partition_restore(const float* rows_cat, int64_t dim, const int64_t* shard_base,
+                          const int64_t* inv_shard, const int64_t* inv_pos, int64_t n, float* out,
+                          void* stream);
+
+/* ---- L2 dynamic embedding table: EmbeddingTable embedding.py:151-308 --- */
+/* EmbeddingTable(name, dim, seed, block_size, evict_threshold) embedding.py:157-171;
+ * evict_threshold < 0 means None.  capacity_hint pre-sizes the row arena. */
+int skb_table_create(int64_t dim, int64_t seed, int64_t block_size, int64_t evict_threshold,
+                     int64_t capacity_hint, skb_table_t* out_host);
+/* initial_rows embedding.py:24-36: out[n, dim] float32, keyed by (seed, id, column) */
+int skb_initial_rows(int64_t seed, const int64_t* ids, int64_t n, int64_t dim, float* out,
+                     void* stream);
+int skb_table_destroy(skb_table_t t);
+/* stats_host[0..5] = {num_rows (len(idmap)), allocated, free_count,
+ *   capacity (block-granular, BlockStore.capacity embedding.py:83-85),
+ *   arena_rows (physical rows reserved), idmap_capacity}.  Synchronizes. */
+int skb_table_stats(skb_table_t t, int64_t* stats_host, void* stream);
+/* lookup_or_insert embedding.py:185-223: offsets_out[i] = slot of ids[i];
+ * unknown ids are admitted in input order (free list LIFO, then sequential),
+ * initialised with initial_rows (embedding.py:24-36), zero m/v; last_step of
+ * every returned slot = step.  Duplicate ids -> SKB_E_VALUE. */
+int skb_table_lookup_or_insert(skb_table_t t, const int64_t* ids, int64_t n, int64_t step,
+                               int64_t* offsets_out, void* stream);
+/* Trusted variant for callers whose ids are unique by construction
+ * (unique_partition output, all_to_all_lookup sharding.py:248-251): no
+ * duplicate check, no synchronization. */
+int skb_table_admit_unique(skb_table_t t, const int64_t* ids, int64_t n, int64_t step,
+                           int64_t* offsets_out, void* stream);
+/* Trusted gather / Adam for offsets produced by admission on the same stream
+ * (all_to_all_lookup / all_to_all_grad_update inner steps): no checks, no sync. */
+int skb_table_gather_unchecked(skb_table_t t, const int64_t* offsets, int64_t n, float* rows_out,
+                               void* stream);
+int skb_sparse_adam_step_unchecked(skb_table_t t, const int64_t* offsets, int64_t n,
+                                   const float* grads, const skb_adam_t* scalars_host, void* stream);
+/* gather embedding.py:233-238 (liveness checked -> SKB_E_INDEX, arg = first bad offset) */
+int skb_table_gather(skb_table_t t, const int64_t* offsets, int64_t n, float* rows_out,
+                     void* stream);
+/* scatter_update embedding.py:240-250 (distinct -> SKB_E_VALUE, live -> SKB_E_INDEX) */
+int skb_table_scatter_update(skb_table_t t, const int64_t* offsets, int64_t n, const float* rows,
+                             void* stream);
+/* evict embedding.py:252-274: stale slots join the free list in insertion order */
+int skb_table_evict(skb_table_t t, int64_t current_step, int64_t* n_evicted_host, void* stream);
+/* export_rows embedding.py:276-284 into caller buffers of >= num_rows entries,
+ * rows sorted by id; n_out_host receives the row count. */
+int skb_table_export(skb_table_t t, int64_t* ids, float* w, float* m, float* v, int64_t* last_step,
+                     int64_t capacity, int64_t* n_out_host, void* stream);
+/* restore_rows embedding.py:286-308 (id already present -> SKB_E_VALUE, arg = id) */
+int skb_table_restore(skb_table_t t, const int64_t* ids, int64_t n, const float* w, const float* m,
+                      const float* v, const int64_t* last_step, void* stream);
+/* BlockStore row/state access by slot (no liveness check), which: 0=w,1=m,2=v
+ *   read / read_state embedding.py:113-126, write / write_state embedding.py:117-131 */
+int skb_table_read_rows(skb_table_t t, const int64_t* offsets, int64_t n, int32_t which, float* out,
+                        void* stream);
+int skb_table_write_rows(skb_table_t t, const int64_t* offsets, int64_t n, int32_t which,
+                         const float* rows, void* stream);
+/* read_last_step / write_last_step embedding.py:133-140 (vals == NULL -> scalar) */
+int skb_table_read_last_step(skb_table_t t, const int64_t* offsets, int64_t n, int64_t* out,
+                             void* stream);
+int skb_table_write_last_step(skb_table_t t, const int64_t* offsets, int64_t n,
+                              const int64_t* vals, int64_t scalar, void* stream);
+/* clear_aux embedding.py:142-148 */
+int skb_table_clear_aux(skb_table_t t, const int64_t* offsets, int64_t n, void* stream);
+/* BlockStore.ensure_capacity embedding.py:87-92 (block-granular) */
+int skb_table_ensure_capacity(skb_table_t t, int64_t slots, void* stream);
+/* IDMap embedding.py:39-61: get (slot or -1), put, remove (-> SKB_E_KEY), free list */
+int skb_table_idmap_get(skb_table_t t, const int64_t* ids, int64_t n, int64_t* slots_out,
+                        void* stream);
+int skb_table_idmap_put(skb_table_t t, int64_t id, int64_t slot, void* stream);
+int skb_table_idmap_remove(skb_table_t t, int64_t id, int64_t* slot_out_host, void* stream);
+/* free_list copy (bottom .. top), n_out_host <= capacity */
+int skb_table_free_list(skb_table_t t, int64_t* out, int64_t capacity, int64_t* n_out_host,
+                        void* stream);
+/* items(): (id, slot) pairs in dict insertion order */
+int skb_table_items(skb_table_t t, int64_t* ids, int64_t* slots, int64_t capacity,
+                    int64_t* n_out_host, void* stream);
+
+/* ---- L2 sparse optimizer: sparse_adam_step optim.py:42-83 --------------- */
+/* distinct offsets (else SKB_E_VALUE); grads [n, dim]; one lazy Adam/AdamW step */
+int skb_sparse_adam_step(skb_table_t t, const int64_t* offsets, int64_t n, const float* grads,
+                         const skb_adam_t* scalars_host, void* stream);
+
+/* ---- L2 ragged pooling: segments.py:61-116 ------------------------------ */
+/* strategy: 0 = sequential (np.add.reduceat: first + numpy pairwise),
+ *           1 = scatter (np.add.at left fold from +0); mode: 0 = sum, 1 = mean.
+ * offsets must be valid (see skb_validate_offsets).          segment_reduce */
+int skb_segment_reduce(const float* rows, int64_t n, int64_t dim, const int64_t* offsets,
+                       int64_t num_segments, int32_t mode, int32_t strategy, float* out,
+                       void* stream);
+/* segment_tile segments.py:94-116 -> out [num_segments, k*dim] */
+int skb_segment_tile(const float* rows, int64_t n, int64_t dim, const int64_t* offsets,
+                     int64_t num_segments, int64_t k, float pad, float* out, void* stream);
+/* _check_segments segments.py:25-33 / _check_offsets ragged.py:32-42 on device:
+ * SKB_E_VALUE if offsets[0] != 0, decreasing, or offsets[len-1] != n_expected */
+int skb_validate_offsets(const int64_t* offsets, int64_t len, int64_t n_expected, void* stream);
+/* np.add.at(g, inverse, grads) left fold by unique index (sharding.py:283-290) */
+int skb_grad_fold(const float* grads, int64_t n, int64_t dim, const int64_t* inverse,
+                  int64_t num_unique, float* out, void* stream);
+
+/* ---- fused step (request-merged logical table; SURVEY §8b additions) ----
+ * Forward = keys_for + unique/admission (lookup_or_insert order) + gather +
+ * pooling of every bag, one logical table, one call.  The per-position grads
+ * of the reference pipeline (train.py:181-186) are dpooled[bag] (sum) or
+ * dpooled[bag] / float32(len) (mean); backward folds them per unique row in
+ * input order and applies Adam/AdamW — bit-identical to
+ * all_to_all_lookup + segment_reduce + all_to_all_grad_update on S = 1.
+ *   ids[N]           raw feature ids, members concatenated (train.py:137-140)
+ *   member_pos[F+1]  (host) position range of each member
+ *   salts[F]         (host) fnv1a64(member) salts (namespaced) — ignored if !namespaced
+ *   bag_offs[G+1]    (device) bag offsets over positions (members' bags concatenated)
+ *   member_bag[F+1]  (host) bag range of each member
+ *   mode             0 sum / 1 mean; strategy per member: 0 sequential / 1 scatter */
+int skb_fused_forward(skb_table_t t, const int64_t* ids, int64_t n, const int64_t* member_pos_host,
+                      const uint64_t* salts_host, int32_t num_members, int32_t namespaced,
+                      const int64_t* bag_offs, int64_t num_bags, const int64_t* member_bag_host,
+                      const int32_t* strategy_host, int32_t mode, int64_t step, float* pooled_out,
+                      void* stream);
+/* Backward of the most recent skb_fused_forward on this table. */
+int skb_fused_backward(skb_table_t t, const float* dpooled, const skb_adam_t* scalars_host,
+                       void* stream);
+/* Number of unique rows the last fused forward touched (synchronizes). */
+int skb_fused_last_unique(skb_table_t t, int64_t* n_unique_host, int64_t* n_new_host, void* stream);
+
+/* ---- feature engine: features.py ---------------------------------------- */
+/* bucketize / fused_bucketize features.py:41-53,165-177: columns concatenated,
+ * col_offs[C+1], edges_cat with edge_offs[C+1]; NaN -> SKB_E_VALUE */
+int skb_bucketize_multi(const float* values, const int64_t* col_offs, int64_t num_cols,
+                        const float* edges_cat, const int64_t* edge_offs, int64_t* out,
+                        int64_t n_total, void* stream);
+/* mod_transform / fused_mod features.py:56-62,180-189 (moduli > 0 checked on host) */
+int skb_mod_multi(const int64_t* values, const int64_t* col_offs, int64_t num_cols,
+                  const int64_t* moduli, int64_t* out, int64_t n_total, void* stream);
+/* cross features.py:65-89: out_offs[rows+1] computed here; out sized by caller
+ * from out_offs[rows] (use skb_cross_offsets first). */
+int skb_cross_offsets(const int64_t* a_offs, const int64_t* b_offs, int64_t rows,
+                      int64_t* out_offs, void* stream);
+int skb_cross(const int64_t* a_vals, const int64_t* a_offs, const int64_t* b_vals,
+              const int64_t* b_offs, int64_t rows, const int64_t* out_offs, int64_t total,
+              int64_t* out, void* stream);
+/* RaggedTensor.truncate ragged.py:139-163: new offsets + element gather index */
+int skb_ragged_truncate(const int64_t* offs, int64_t rows, int64_t max_len, int32_t tail,
+                        int64_t* new_offs, int64_t* src_index, void* stream);
+
+/* out[i] = src[idx[i]] for elements of elem_bytes (1, 4 or 8) — ragged value
+ * selection (truncate ragged.py:139-163, row_ranges ragged.py:18-29) */
+int skb_gather_elems(const void* src, int64_t elem_bytes, const int64_t* idx, int64_t n, void* out,
+                     void* stream);
+/* RaggedTensor.pad_to_dense ragged.py:165-188: dense [rows, max_len, width]
+ * elements of elem_bytes*width bytes, pad pattern pad_host (elem_bytes bytes),
+ * mask [rows, max_len] uint8.  Row longer than max_len -> SKB_E_VALUE. */
+int skb_ragged_pad_dense(const void* values, int64_t elem_bytes, int64_t width, const int64_t* offs,
+                         int64_t rows, int64_t max_len, const void* pad_host, void* out,
+                         uint8_t* mask, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSEKIT_B200_H */

@@ -1,0 +1,196 @@
+"""ctypes binding of libsparsekit_b200.so (the C ABI in include/sparsekit_b200.h).
+
+There is no CPU fallback: importing a compute entry point without the built
+library or without a CUDA device raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsparsekit_b200.so")
+
+SKB_OK, SKB_E_VALUE, SKB_E_INDEX, SKB_E_KEY, SKB_E_CUDA, SKB_E_NOMEM, SKB_E_ARG, SKB_E_UNSUPPORTED = range(8)
+
+_i64, _u64, _i32, _p = ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, ctypes.c_void_p
+
+
+class AdamScalars(ctypes.Structure):
+    """skb_adam_t (host-computed float32 scalars, optim.py:69-75)."""
+    _fields_ = [("lr", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float),
+                ("eps", ctypes.c_float), ("one_minus_beta1", ctypes.c_float),
+                ("one_minus_beta2", ctypes.c_float), ("bc1", ctypes.c_float), ("bc2", ctypes.c_float),
+                ("lr_wd", ctypes.c_float), ("decoupled_decay", ctypes.c_int32)]
+
+
+# name -> argtypes (restype int unless noted)
+_SIGS = {
+    "skb_version": ([], ctypes.c_char_p),
+    "skb_last_error": ([], ctypes.c_char_p),
+    "skb_last_error_arg": ([], _i64),
+    "skb_device_sm_count": ([ctypes.c_int, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "skb_mix64": ([_p, _i64, _p, _p], ctypes.c_int),
+    "skb_shard_of": ([_p, _i64, _i64, _p, _p], ctypes.c_int),
+    "skb_keys_for": ([_p, _i64, _u64, _p, _p], ctypes.c_int),
+    "skb_fnv1a64_host": ([ctypes.c_char_p, _i64], _u64),
+    "skb_fnv1a64_strings": ([_p, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_fnv1a64_pairs": ([_p, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_unique_partition": ([_p, _i64, _i64, _p, _p, _p, _p, _p], ctypes.c_int),
+    "skb_partition_restore": ([_p, _i64, _p, _p, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_table_create": ([_i64, _i64, _i64, _i64, _i64, ctypes.POINTER(_p)], ctypes.c_int),
+    "skb_table_destroy": ([_p], ctypes.c_int),
+    "skb_initial_rows": ([_i64, _p, _i64, _i64, _p, _p], ctypes.c_int),
+    "skb_table_stats": ([_p, ctypes.POINTER(_i64), _p], ctypes.c_int),
+    "skb_table_lookup_or_insert": ([_p, _p, _i64, _i64, _p, _p], ctypes.c_int),
+    "skb_table_admit_unique": ([_p, _p, _i64, _i64, _p, _p], ctypes.c_int),
+    "skb_table_gather": ([_p, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_table_gather_unchecked": ([_p, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_sparse_adam_step_unchecked": ([_p, _p, _i64, _p, ctypes.POINTER(AdamScalars), _p], ctypes.c_int),
+    "skb_table_scatter_update": ([_p, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_table_evict": ([_p, _i64, ctypes.POINTER(_i64), _p], ctypes.c_int),
+    "skb_table_export": ([_p, _p, _p, _p, _p, _p, _i64, ctypes.POINTER(_i64), _p], ctypes.c_int),
+    "skb_table_restore": ([_p, _p, _i64, _p, _p, _p, _p, _p], ctypes.c_int),
+    "skb_table_read_rows": ([_p, _p, _i64, _i32, _p, _p], ctypes.c_int),
+    "skb_table_write_rows": ([_p, _p, _i64, _i32, _p, _p], ctypes.c_int),
+    "skb_table_read_last_step": ([_p, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_table_write_last_step": ([_p, _p, _i64, _p, _i64, _p], ctypes.c_int),
+    "skb_table_clear_aux": ([_p, _p, _i64, _p], ctypes.c_int),
+    "skb_table_ensure_capacity": ([_p, _i64, _p], ctypes.c_int),
+    "skb_table_idmap_get": ([_p, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_table_idmap_put": ([_p, _i64, _i64, _p], ctypes.c_int),
+    "skb_table_idmap_remove": ([_p, _i64, ctypes.POINTER(_i64), _p], ctypes.c_int),
+    "skb_table_free_list": ([_p, _p, _i64, ctypes.POINTER(_i64), _p], ctypes.c_int),
+    "skb_table_items": ([_p, _p, _p, _i64, ctypes.POINTER(_i64), _p], ctypes.c_int),
+    "skb_sparse_adam_step": ([_p, _p, _i64, _p, ctypes.POINTER(AdamScalars), _p], ctypes.c_int),
+    "skb_segment_reduce": ([_p, _i64, _i64, _p, _i64, _i32, _i32, _p, _p], ctypes.c_int),
+    "skb_segment_tile": ([_p, _i64, _i64, _p, _i64, _i64, ctypes.c_float, _p, _p], ctypes.c_int),
+    "skb_validate_offsets": ([_p, _i64, _i64, _p], ctypes.c_int),
+    "skb_grad_fold": ([_p, _i64, _i64, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_fused_forward": ([_p, _p, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_u64), _i32, _i32, _p, _i64,
+                           ctypes.POINTER(_i64), ctypes.POINTER(_i32), _i32, _i64, _p, _p], ctypes.c_int),
+    "skb_fused_backward": ([_p, _p, ctypes.POINTER(AdamScalars), _p], ctypes.c_int),
+    "skb_fused_last_unique": ([_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p], ctypes.c_int),
+    "skb_bucketize_multi": ([_p, _p, _i64, _p, _p, _p, _i64, _p], ctypes.c_int),
+    "skb_mod_multi": ([_p, _p, _i64, _p, _p, _i64, _p], ctypes.c_int),
+    "skb_cross_offsets": ([_p, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_cross": ([_p, _p, _p, _p, _i64, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_ragged_truncate": ([_p, _i64, _i64, _i32, _p, _p, _p], ctypes.c_int),
+    "skb_gather_elems": ([_p, _i64, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_ragged_pad_dense": ([_p, _i64, _i64, _p, _i64, _i64, _p, _p, _p, _p], ctypes.c_int),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """dlopen the library and bind every declared symbol (no CUDA calls)."""
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+def lib():
+    """The bound library; requires a CUDA device (fails loudly otherwise)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                import torch
+                if not torch.cuda.is_available():
+                    raise RuntimeError("paper_2509_20883_b200 needs a CUDA device (sm_100a); no CPU fallback")
+                _lib = load_library()
+    return _lib
+
+
+_EXC = {SKB_E_VALUE: ValueError, SKB_E_INDEX: IndexError, SKB_E_KEY: KeyError,
+        SKB_E_ARG: ValueError, SKB_E_UNSUPPORTED: NotImplementedError, SKB_E_NOMEM: MemoryError}
+
+
+def check(status: int) -> None:
+    if status == SKB_OK:
+        return
+    msg = _lib.skb_last_error().decode("utf-8", "replace")
+    if status == SKB_E_KEY:
+        raise KeyError(int(_lib.skb_last_error_arg()))
+    raise _EXC.get(status, RuntimeError)(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args))
+
+
+# ---------------------------------------------------------------------------
+# tensor plumbing (torch is the device-memory / stream provider)
+# ---------------------------------------------------------------------------
+
+def torch():
+    import torch as _t
+    return _t
+
+
+def ctypes_byref(x):
+    return ctypes.byref(x)
+
+
+def stream_ptr(device=None):
+    t = torch()
+    return ctypes.c_void_p(t.cuda.current_stream(device).cuda_stream)
+
+
+def ptr(x):
+    return ctypes.c_void_p(x.data_ptr()) if x is not None and x.numel() else ctypes.c_void_p(
+        x.data_ptr() if x is not None else 0)
+
+
+_NP2T = {np.dtype(np.int64): "int64", np.dtype(np.float32): "float32", np.dtype(np.uint8): "uint8",
+         np.dtype(np.int32): "int32", np.dtype(np.float64): "float64"}
+
+
+def is_torch(x) -> bool:
+    t = torch()
+    return isinstance(x, t.Tensor)
+
+
+def to_dev(x, dtype: str, device=None):
+    """numpy/list/torch -> contiguous CUDA tensor of `dtype` (a copy only if needed)."""
+    t = torch()
+    tdt = getattr(t, dtype)
+    dev = t.device("cuda", t.cuda.current_device()) if device is None else t.device(device)
+    if isinstance(x, t.Tensor):
+        if x.dtype != tdt:
+            x = x.to(tdt)
+        if x.device != dev:
+            x = x.to(dev)
+        return x.contiguous()
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.dtype(dtype)))
+    if not a.flags.writeable:
+        a = a.copy()
+    return t.from_numpy(a).to(dev)
+
+
+def empty(shape, dtype: str, device=None):
+    t = torch()
+    dev = t.device("cuda", t.cuda.current_device()) if device is None else t.device(device)
+    return t.empty(shape, dtype=getattr(t, dtype), device=dev)
+
+
+def out_like(result, as_numpy: bool):
+    """Return numpy when the caller passed numpy (drop-in), else the CUDA tensor."""
+    if as_numpy:
+        return result.cpu().numpy()
+    return result

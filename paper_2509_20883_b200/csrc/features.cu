@@ -1,0 +1,80 @@
+// features.cu — multi-column feature-engine kernels (features.py:41-62,
+// 165-189).  One launch covers every column of a FusedPlan: a per-element
+// column lookup (binary search over the column offsets, L1-resident) selects
+// the column's edges / modulus — the GPU form of "many small kernels fused
+// into one dispatch" (PAPER §2.2.2).
+#include "common.cuh"
+
+namespace skb {
+
+__device__ __forceinline__ int64_t column_of(const int64_t* __restrict__ col_offs, int64_t C, int64_t i) {
+  int64_t lo = 0, hi = C;  // col_offs[lo] <= i < col_offs[lo+1]
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (col_offs[mid] <= i) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// bin = #{edges e : e <= v} (np.searchsorted side="right"); NaN flagged
+__global__ void k_bucketize(const float* __restrict__ vals, const int64_t* __restrict__ col_offs, int64_t C,
+                            const float* __restrict__ edges, const int64_t* __restrict__ edge_offs, int64_t n,
+                            int64_t* __restrict__ out, unsigned long long* nan_flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float v = vals[i];
+    if (v != v) {
+      atomicMin(nan_flag, (unsigned long long)i);
+      out[i] = 0;
+      continue;
+    }
+    int64_t c = C == 1 ? 0 : column_of(col_offs, C, i);
+    int64_t eb = edge_offs[c], ee = edge_offs[c + 1];
+    int64_t lo = eb, hi = ee;  // first edge > v
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (__ldg(edges + mid) <= v) lo = mid + 1; else hi = mid;
+    }
+    out[i] = lo - eb;
+  }
+}
+
+// non-negative remainder (np.remainder with m > 0)
+__global__ void k_mod(const int64_t* __restrict__ vals, const int64_t* __restrict__ col_offs, int64_t C,
+                      const int64_t* __restrict__ moduli, int64_t n, int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = C == 1 ? 0 : column_of(col_offs, C, i);
+    int64_t m = moduli[c];
+    int64_t r = vals[i] % m;
+    out[i] = r < 0 ? r + m : r;
+  }
+}
+
+}  // namespace skb
+
+using namespace skb;
+
+extern "C" {
+
+int skb_bucketize_multi(const float* values, const int64_t* col_offs, int64_t num_cols, const float* edges_cat,
+                        const int64_t* edge_offs, int64_t* out, int64_t n_total, void* stream) {
+  SKB_API_BEGIN
+  cudaStream_t s = as_stream(stream);
+  if (n_total <= 0) return SKB_OK;
+  DevFlag f(s);
+  k_bucketize<<<grid_for(n_total, 256), 256, 0, s>>>(values, col_offs, num_cols, edges_cat, edge_offs, n_total, out,
+                                                     f.ptr());
+  SKB_LAUNCH_CHECK();
+  if (f.read() >= 0) raise(SKB_E_VALUE, 0, "bucketize input contains NaN");
+  SKB_API_END
+}
+
+int skb_mod_multi(const int64_t* values, const int64_t* col_offs, int64_t num_cols, const int64_t* moduli,
+                  int64_t* out, int64_t n_total, void* stream) {
+  SKB_API_BEGIN
+  if (n_total <= 0) return SKB_OK;
+  k_mod<<<grid_for(n_total, 256), 256, 0, as_stream(stream)>>>(values, col_offs, num_cols, moduli, n_total, out);
+  SKB_LAUNCH_CHECK();
+  SKB_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,23 @@
+// partition.cuh — dedup / partition / fold building blocks shared across TUs.
+#pragma once
+#include "common.cuh"
+
+namespace skb {
+
+// First-occurrence dedup of ids[0:n) on a scratch open-addressing table.
+struct DedupResult {
+  int64_t cap = 0;   // power of two; entry `cap` is the side slot for kEmptyKey
+  Scratch table;     // HEntry[cap+1]: {key, first position}
+  Scratch hslot;     // int64[n]: table index of each position's key
+  Scratch fpos;      // int64[n]: first-occurrence positions, ascending (U valid)
+  Scratch d_u;       // int64: U (device)
+};
+void dedup_first_occurrence(const int64_t* ids, int64_t n, DedupResult& r, cudaStream_t s);
+
+void unique_partition(const int64_t* ids, int64_t n, int64_t S, int64_t* uniq, int64_t* counts,
+                      int64_t* inv_shard, int64_t* inv_pos, cudaStream_t s);
+
+void grad_fold(const float* grads, int64_t n, int D, const int64_t* inverse, int64_t U, float* out,
+               cudaStream_t s);
+
+}  // namespace skb

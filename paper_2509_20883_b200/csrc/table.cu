@@ -1,0 +1,932 @@
+// table.cu — GPU dynamic embedding table: admission / lookup with the
+// reference's exact slot assignment, gather / scatter, eviction in dict
+// insertion order, export / restore, BlockStore accessors, sparse Adam.
+//
+// Admission (embedding.py:185-223) runs as probe -> exclusive scan of the
+// miss flags -> insert: the k-th unknown id (input order) gets
+// free_list[F-1-k] if k < F else allocated + k - F, so offsets are identical
+// to the reference's dict loop while every id is handled by its own thread.
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "partition.cuh"
+#include "rows.cuh"
+#include "table.cuh"
+
+namespace skb {
+
+Table* table_from(skb_table_t h) {
+  if (!h) raise(SKB_E_ARG, 0, "null table handle");
+  return reinterpret_cast<Table*>(h);
+}
+
+// ---------------------------------------------------------------------------
+// growth
+// ---------------------------------------------------------------------------
+template <class T>
+static void grow_array(T*& p, int64_t old_n, int64_t new_n, cudaStream_t s) {
+  T* q = nullptr;
+  SKB_CUDA(cudaMallocAsync(&q, sizeof(T) * new_n, s));
+  if (old_n) SKB_CUDA(cudaMemcpyAsync(q, p, sizeof(T) * old_n, cudaMemcpyDeviceToDevice, s));
+  SKB_CUDA(cudaMemsetAsync(q + old_n, 0, sizeof(T) * (new_n - old_n), s));
+  if (p) SKB_CUDA(cudaFreeAsync(p, s));
+  p = q;
+}
+
+static void grow_arena(Table* t, int64_t new_rows, cudaStream_t s) {
+  if (new_rows <= t->arena_rows) return;
+  const int64_t old = t->arena_rows;
+  grow_array(t->arena, old * t->row_stride(), new_rows * t->row_stride(), s);
+  grow_array(t->last_step, old, new_rows, s);
+  grow_array(t->live, old, new_rows, s);
+  grow_array(t->slot_key, old, new_rows, s);
+  grow_array(t->ins_seq, old, new_rows, s);
+  grow_array(t->free_list, old, new_rows, s);
+  t->arena_rows = new_rows;
+}
+
+__global__ void k_rehash(const HEntry* __restrict__ old, int64_t old_cap, HEntry* nt, uint64_t mask, int64_t cap) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= old_cap; i += (int64_t)gridDim.x * blockDim.x) {
+    HEntry e = old[i];
+    if (i == old_cap) {
+      nt[cap].val = e.val;  // side slot travels as-is
+    } else if (e.key != kEmptyKey) {
+      idmap_insert(nt, mask, cap, e.key, e.val);
+    }
+  }
+}
+
+static void rehash(Table* t, int64_t new_cap, cudaStream_t s) {
+  HEntry* nt = nullptr;
+  SKB_CUDA(cudaMallocAsync(&nt, sizeof(HEntry) * (new_cap + 1), s));
+  ht_fill(nt, new_cap + 1, -1, s);
+  if (t->idmap) {
+    k_rehash<<<grid_for(t->idmap_cap + 1, 256), 256, 0, s>>>(t->idmap, t->idmap_cap, nt, (uint64_t)(new_cap - 1),
+                                                             new_cap);
+    SKB_LAUNCH_CHECK();
+    SKB_CUDA(cudaFreeAsync(t->idmap, s));
+  }
+  t->idmap = nt;
+  t->idmap_cap = new_cap;
+}
+
+void table_refresh(Table* t, cudaStream_t s) {
+  SKB_CUDA(cudaMemcpyAsync(t->snap_host, t->counters, sizeof(int64_t) * C_N, cudaMemcpyDeviceToHost, s));
+  SKB_CUDA(cudaStreamSynchronize(s));
+  for (int i = 0; i < C_N; ++i) t->known[i] = t->snap_host[i];
+  t->pending_adds = 0;
+  t->snap_pending = false;
+}
+
+static void harvest_snapshot(Table* t) {
+  if (!t->snap_pending) return;
+  if (cudaEventQuery(t->snap_ev) != cudaSuccess) {
+    cudaGetLastError();  // clear cudaErrorNotReady
+    return;
+  }
+  for (int i = 0; i < C_N; ++i) t->known[i] = t->snap_host[i];
+  t->snap_pending = false;
+  // pending_adds already excludes ops enqueued before the snapshot
+}
+
+void table_reserve(Table* t, int64_t n, cudaStream_t s) {
+  harvest_snapshot(t);
+  int64_t ub_alloc = t->known[C_ALLOC] + t->pending_adds + n;
+  int64_t ub_rows = t->known[C_ROWS] + t->pending_adds + n;
+  bool arena_ok = ub_alloc <= t->arena_rows;
+  bool map_ok = ub_rows * 10 < t->idmap_cap * 9;  // hard bound: never fill the probe table
+  if (arena_ok && map_ok) return;
+  table_refresh(t, s);
+  int64_t need_alloc = t->known[C_ALLOC] + n;
+  int64_t need_rows = t->known[C_ROWS] + n;
+  if (need_alloc > t->arena_rows) {
+    int64_t nr = t->arena_rows + t->arena_rows / 2;
+    if (nr < need_alloc) nr = need_alloc;
+    if (nr < 1024) nr = 1024;
+    grow_arena(t, nr, s);
+  }
+  if (need_rows * 2 > t->idmap_cap) rehash(t, next_pow2(need_rows * 3), s);
+}
+
+void table_note_inserts(Table* t, int64_t n, cudaStream_t s) {
+  t->pending_adds += n;
+  if (!t->snap_pending) {
+    SKB_CUDA(cudaMemcpyAsync(t->snap_host, t->counters, sizeof(int64_t) * C_N, cudaMemcpyDeviceToHost, s));
+    SKB_CUDA(cudaEventRecord(t->snap_ev, s));
+    t->snap_pending = true;
+    t->pending_adds = 0;  // ops before this point are covered by the snapshot
+  }
+}
+
+// ---------------------------------------------------------------------------
+// admission
+// ---------------------------------------------------------------------------
+__global__ void k_probe(const int64_t* __restrict__ ids, int64_t n, const HEntry* __restrict__ map, uint64_t mask,
+                        int64_t cap, int64_t step, int64_t* __restrict__ offsets, int32_t* __restrict__ miss,
+                        int64_t* __restrict__ last_step) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    long long s = idmap_find(map, mask, cap, ids[i]);
+    miss[i] = s < 0 ? 1 : 0;
+    if (s >= 0) {
+      offsets[i] = s;
+      last_step[s] = step;
+    }
+  }
+}
+
+// One thread per (miss position, 4-column chunk): the slot formula needs no
+// coordination, chunk 0 also publishes the key and the per-slot metadata.
+__global__ void k_admit(const int64_t* __restrict__ ids, int64_t n, const int32_t* __restrict__ miss,
+                        const int64_t* __restrict__ rank, const int64_t* __restrict__ counters,
+                        const int64_t* __restrict__ free_list, HEntry* map, uint64_t mask, int64_t cap, int64_t step,
+                        int D, uint64_t seed_mix, double scale, float* __restrict__ arena,
+                        int64_t* __restrict__ last_step, uint8_t* __restrict__ live, int64_t* __restrict__ slot_key,
+                        int64_t* __restrict__ ins_seq, int64_t* __restrict__ offsets) {
+  const int chunks = (D + 3) / 4;
+  const int64_t total = n * chunks;
+  const int64_t A = counters[C_ALLOC], F = counters[C_FREE], seq = counters[C_SEQ];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / chunks;
+    if (!miss[i]) continue;
+    int ch = (int)(t - i * chunks);
+    int64_t k = rank[i];
+    int64_t slot = assign_slot(k, F, A, free_list);
+    long long key = ids[i];
+    if (ch == 0) {
+      idmap_insert(map, mask, cap, key, slot);
+      offsets[i] = slot;
+      last_step[slot] = step;
+      live[slot] = 1;
+      slot_key[slot] = key;
+      ins_seq[slot] = seq + k;
+    }
+    uint64_t base = mix64((uint64_t)key ^ seed_mix);
+    float* row = arena + slot * (int64_t)(3 * D);
+    for (int c = ch * 4; c < ch * 4 + 4 && c < D; ++c) {
+      row[c] = init_value(base, c, scale);
+      row[D + c] = 0.f;
+      row[2 * D + c] = 0.f;
+    }
+  }
+}
+
+__global__ void k_finish_admit(int64_t* counters, const int64_t* __restrict__ total_new) {
+  int64_t K = *total_new, F = counters[C_FREE];
+  int64_t take = K < F ? K : F;
+  counters[C_FREE] = F - take;
+  counters[C_ALLOC] += K - take;
+  counters[C_ROWS] += K;
+  counters[C_SEQ] += K;
+}
+
+// duplicate detector: first position whose id occurred earlier
+__global__ void k_dup_flag(const HEntry* t, const int64_t* __restrict__ hslot, int64_t n,
+                           unsigned long long* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (t[hslot[i]].val != i) atomicMin(flag, (unsigned long long)i);
+}
+
+// returns the first position i such that ids[i] repeats an earlier id, or -1
+static int64_t first_duplicate(const int64_t* ids, int64_t n, cudaStream_t s) {
+  if (n < 2) return -1;
+  DedupResult r;
+  dedup_first_occurrence(ids, n, r, s);
+  DevFlag f(s);
+  k_dup_flag<<<grid_for(n, 256), 256, 0, s>>>(r.table.as<HEntry>(), r.hslot.as<int64_t>(), n, f.ptr());
+  SKB_LAUNCH_CHECK();
+  return f.read();
+}
+
+static int64_t read_i64(const int64_t* dptr, cudaStream_t s) {
+  int64_t v = 0;
+  SKB_CUDA(cudaMemcpyAsync(&v, dptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  SKB_CUDA(cudaStreamSynchronize(s));
+  return v;
+}
+
+void table_admit(Table* t, const int64_t* ids, int64_t n, int64_t step, int64_t* offsets, cudaStream_t s) {
+  table_reserve(t, n, s);
+  Scratch miss(sizeof(int32_t) * n, s), rank(sizeof(int64_t) * n, s), total(sizeof(int64_t), s);
+  const uint64_t mask = (uint64_t)(t->idmap_cap - 1);
+  k_probe<<<grid_for(n, 256), 256, 0, s>>>(ids, n, t->idmap, mask, t->idmap_cap, step, offsets, miss.as<int32_t>(),
+                                          t->last_step);
+  SKB_LAUNCH_CHECK();
+  scan_exclusive_i32_to_i64(miss.as<int32_t>(), rank.as<int64_t>(), n, total.as<int64_t>(), s);
+  const int chunks = (int)((t->dim + 3) / 4);
+  k_admit<<<grid_for(n * chunks, 256), 256, 0, s>>>(ids, n, miss.as<int32_t>(), rank.as<int64_t>(), t->counters,
+                                                   t->free_list, t->idmap, mask, t->idmap_cap, step, (int)t->dim,
+                                                   t->seed_mix, t->init_scale, t->arena, t->last_step, t->live,
+                                                   t->slot_key, t->ins_seq, offsets);
+  SKB_LAUNCH_CHECK();
+  k_finish_admit<<<1, 1, 0, s>>>(t->counters, total.as<int64_t>());
+  SKB_LAUNCH_CHECK();
+  table_note_inserts(t, n, s);
+}
+
+// ---------------------------------------------------------------------------
+// gather / scatter with liveness checks (embedding.py:225-250)
+// ---------------------------------------------------------------------------
+__global__ void k_check_live(const int64_t* __restrict__ offs, int64_t n, const uint8_t* __restrict__ live,
+                             int64_t limit, unsigned long long* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t o = offs[i];
+    if (o < 0 || o >= limit || !live[o]) atomicMin(flag, (unsigned long long)i);
+  }
+}
+
+__global__ void k_check_range(const int64_t* __restrict__ offs, int64_t n, int64_t limit, unsigned long long* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t o = offs[i];
+    if (o < 0 || o >= limit) atomicMin(flag, (unsigned long long)i);
+  }
+}
+
+static void check_live(Table* t, const int64_t* offs, int64_t n, const char* op, cudaStream_t s) {
+  DevFlag f(s);
+  k_check_live<<<grid_for(n, 256), 256, 0, s>>>(offs, n, t->live, t->arena_rows, f.ptr());
+  SKB_LAUNCH_CHECK();
+  int64_t bad = f.read();
+  if (bad >= 0) {
+    int64_t o = read_i64(offs + bad, s);
+    raise(SKB_E_INDEX, o, "%s: offset %lld is not a live slot", op, (long long)o);
+  }
+}
+
+static int64_t reported_capacity(Table* t) {
+  int64_t hw = t->known[C_ALLOC] > t->ensured_slots ? t->known[C_ALLOC] : t->ensured_slots;
+  return (hw + t->block_size - 1) / t->block_size * t->block_size;
+}
+
+static void check_range(Table* t, const int64_t* offs, int64_t n, cudaStream_t s) {
+  table_refresh(t, s);
+  int64_t lim = reported_capacity(t);
+  if (lim > t->arena_rows) lim = t->arena_rows;
+  DevFlag f(s);
+  k_check_range<<<grid_for(n, 256), 256, 0, s>>>(offs, n, lim, f.ptr());
+  SKB_LAUNCH_CHECK();
+  int64_t bad = f.read();
+  if (bad >= 0) {
+    int64_t o = read_i64(offs + bad, s);
+    raise(SKB_E_INDEX, o, "offset %lld is outside the store capacity %lld", (long long)o, (long long)lim);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// eviction (embedding.py:252-274)
+// ---------------------------------------------------------------------------
+__global__ void k_stale(const uint8_t* __restrict__ live, const int64_t* __restrict__ last, int64_t rows, int64_t step,
+                        int64_t thr, uint8_t* __restrict__ flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = (live[i] && (step - last[i]) > thr) ? 1 : 0;
+}
+
+__global__ void k_gather_i64(const int64_t* __restrict__ src, const int64_t* __restrict__ idx, int64_t n,
+                             int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = src[idx[i]];
+}
+
+__global__ void k_evict_apply(const int64_t* __restrict__ slots, int64_t E, int D, int64_t* counters,
+                              int64_t* __restrict__ free_list, uint8_t* __restrict__ live,
+                              int64_t* __restrict__ last, float* __restrict__ arena) {
+  const int64_t F = counters[C_FREE];
+  const int64_t total = E * D;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j = t / D;
+    int c = (int)(t - j * D);
+    int64_t s = slots[j];
+    float* row = arena + s * (int64_t)(3 * D);
+    row[D + c] = 0.f;
+    row[2 * D + c] = 0.f;
+    if (c == 0) {
+      free_list[F + j] = s;
+      live[s] = 0;
+      last[s] = 0;
+    }
+  }
+}
+
+__global__ void k_evict_counters(int64_t* counters, int64_t E) {
+  counters[C_FREE] += E;
+  counters[C_ROWS] -= E;
+}
+
+// keep only entries whose slot is still live (rebuild instead of tombstones)
+__global__ void k_rebuild_live(const HEntry* __restrict__ old, int64_t cap, const uint8_t* __restrict__ live,
+                               HEntry* nt) {
+  const uint64_t mask = (uint64_t)(cap - 1);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= cap; i += (int64_t)gridDim.x * blockDim.x) {
+    HEntry e = old[i];
+    if (i == cap) {
+      nt[cap].val = (e.val >= 0 && live[e.val]) ? e.val : -1;
+    } else if (e.key != kEmptyKey && live[e.val]) {
+      idmap_insert(nt, mask, cap, e.key, e.val);
+    }
+  }
+}
+
+int64_t table_evict(Table* t, int64_t step, cudaStream_t s) {
+  if (t->evict_threshold < 0 || t->arena_rows == 0) return 0;
+  const int64_t R = t->arena_rows;
+  Scratch flags(R, s), stale(sizeof(int64_t) * R, s), cnt(sizeof(int64_t), s);
+  k_stale<<<grid_for(R, 256), 256, 0, s>>>(t->live, t->last_step, R, step, t->evict_threshold, flags.as<uint8_t>());
+  SKB_LAUNCH_CHECK();
+  select_flagged_index(flags.as<uint8_t>(), R, stale.as<int64_t>(), cnt.as<int64_t>(), s);
+  int64_t E = read_i64(cnt.as<int64_t>(), s);
+  if (E == 0) return 0;
+  Scratch seq(sizeof(int64_t) * E, s), seq2(sizeof(int64_t) * E, s), slots2(sizeof(int64_t) * E, s);
+  k_gather_i64<<<grid_for(E, 256), 256, 0, s>>>(t->ins_seq, stale.as<int64_t>(), E, seq.as<int64_t>());
+  SKB_LAUNCH_CHECK();
+  sort_pairs_i64(seq.as<int64_t>(), seq2.as<int64_t>(), stale.as<int64_t>(), slots2.as<int64_t>(), E, s);
+  k_evict_apply<<<grid_for(E * t->dim, 256), 256, 0, s>>>(slots2.as<int64_t>(), E, (int)t->dim, t->counters,
+                                                         t->free_list, t->live, t->last_step, t->arena);
+  SKB_LAUNCH_CHECK();
+  k_evict_counters<<<1, 1, 0, s>>>(t->counters, E);
+  SKB_LAUNCH_CHECK();
+  HEntry* nt = nullptr;
+  SKB_CUDA(cudaMallocAsync(&nt, sizeof(HEntry) * (t->idmap_cap + 1), s));
+  ht_fill(nt, t->idmap_cap + 1, -1, s);
+  k_rebuild_live<<<grid_for(t->idmap_cap + 1, 256), 256, 0, s>>>(t->idmap, t->idmap_cap, t->live, nt);
+  SKB_LAUNCH_CHECK();
+  SKB_CUDA(cudaFreeAsync(t->idmap, s));
+  t->idmap = nt;
+  table_refresh(t, s);
+  return E;
+}
+
+// ---------------------------------------------------------------------------
+// export / restore (embedding.py:276-308)
+// ---------------------------------------------------------------------------
+struct IdxSlotArena {
+  const int64_t* slots;
+  __device__ __forceinline__ int64_t operator()(int64_t i) const { return slots[i]; }
+};
+
+int64_t table_export(Table* t, int64_t* ids, float* w, float* m, float* v, int64_t* last, int64_t capacity,
+                     cudaStream_t s) {
+  const int64_t R = t->arena_rows;
+  if (R == 0) return 0;
+  Scratch slots(sizeof(int64_t) * R, s), cnt(sizeof(int64_t), s);
+  select_flagged_index(t->live, R, slots.as<int64_t>(), cnt.as<int64_t>(), s);
+  int64_t n = read_i64(cnt.as<int64_t>(), s);
+  if (n > capacity) raise(SKB_E_ARG, n, "export buffers hold %lld rows, table has %lld", (long long)capacity,
+                          (long long)n);
+  if (n == 0) return 0;
+  Scratch keys(sizeof(int64_t) * n, s), slots2(sizeof(int64_t) * n, s);
+  k_gather_i64<<<grid_for(n, 256), 256, 0, s>>>(t->slot_key, slots.as<int64_t>(), n, keys.as<int64_t>());
+  SKB_LAUNCH_CHECK();
+  sort_pairs_i64(keys.as<int64_t>(), ids, slots.as<int64_t>(), slots2.as<int64_t>(), n, s);
+  const int D = (int)t->dim;
+  IdxSlotArena ix{slots2.as<int64_t>()};
+  if (w) launch_rows_gather(ix, t->arena, 3 * D, w, D, n, D, s);
+  if (m) launch_rows_gather(ix, t->arena + D, 3 * D, m, D, n, D, s);
+  if (v) launch_rows_gather(ix, t->arena + 2 * D, 3 * D, v, D, n, D, s);
+  if (last) {
+    k_gather_i64<<<grid_for(n, 256), 256, 0, s>>>(t->last_step, slots2.as<int64_t>(), n, last);
+    SKB_LAUNCH_CHECK();
+  }
+  return n;
+}
+
+__global__ void k_present_flag(const int64_t* __restrict__ ids, int64_t n, const HEntry* __restrict__ map,
+                               uint64_t mask, int64_t cap, const HEntry* __restrict__ dt,
+                               const int64_t* __restrict__ hslot, unsigned long long* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (idmap_find(map, mask, cap, ids[i]) >= 0 || dt[hslot[i]].val != i) atomicMin(flag, (unsigned long long)i);
+}
+
+__global__ void k_restore(const int64_t* __restrict__ ids, int64_t n, const int64_t* __restrict__ counters,
+                          const int64_t* __restrict__ free_list, HEntry* map, uint64_t mask, int64_t cap,
+                          const int64_t* __restrict__ last_in, int64_t* __restrict__ last_step,
+                          uint8_t* __restrict__ live, int64_t* __restrict__ slot_key, int64_t* __restrict__ ins_seq,
+                          int64_t* __restrict__ slots_out) {
+  const int64_t A = counters[C_ALLOC], F = counters[C_FREE], seq = counters[C_SEQ];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t slot = assign_slot(i, F, A, free_list);
+    idmap_insert(map, mask, cap, ids[i], slot);
+    last_step[slot] = last_in[i];
+    live[slot] = 1;
+    slot_key[slot] = ids[i];
+    ins_seq[slot] = seq + i;
+    slots_out[i] = slot;
+  }
+}
+
+__global__ void k_set_i64(int64_t* p, int64_t v) { *p = v; }
+
+void table_restore(Table* t, const int64_t* ids, int64_t n, const float* w, const float* m, const float* v,
+                   const int64_t* last, cudaStream_t s) {
+  if (n == 0) return;
+  {
+    DedupResult r;
+    dedup_first_occurrence(ids, n, r, s);
+    DevFlag f(s);
+    k_present_flag<<<grid_for(n, 256), 256, 0, s>>>(ids, n, t->idmap, (uint64_t)(t->idmap_cap - 1), t->idmap_cap,
+                                                    r.table.as<HEntry>(), r.hslot.as<int64_t>(), f.ptr());
+    SKB_LAUNCH_CHECK();
+    int64_t bad = f.read();
+    if (bad >= 0) {
+      int64_t id = read_i64(ids + bad, s);
+      raise(SKB_E_VALUE, id, "restore_rows: id %lld already present", (long long)id);
+    }
+  }
+  table_reserve(t, n, s);
+  Scratch slots(sizeof(int64_t) * n, s), total(sizeof(int64_t), s);
+  k_restore<<<grid_for(n, 256), 256, 0, s>>>(ids, n, t->counters, t->free_list, t->idmap,
+                                            (uint64_t)(t->idmap_cap - 1), t->idmap_cap, last, t->last_step, t->live,
+                                            t->slot_key, t->ins_seq, slots.as<int64_t>());
+  SKB_LAUNCH_CHECK();
+  const int D = (int)t->dim;
+  IdxSlotArena ix{slots.as<int64_t>()};
+  launch_rows_scatter(ix, w, D, t->arena, 3 * D, n, D, s);
+  launch_rows_scatter(ix, m, D, t->arena + D, 3 * D, n, D, s);
+  launch_rows_scatter(ix, v, D, t->arena + 2 * D, 3 * D, n, D, s);
+  k_set_i64<<<1, 1, 0, s>>>(total.as<int64_t>(), n);
+  SKB_LAUNCH_CHECK();
+  k_finish_admit<<<1, 1, 0, s>>>(t->counters, total.as<int64_t>());
+  SKB_LAUNCH_CHECK();
+  table_note_inserts(t, n, s);
+}
+
+// ---------------------------------------------------------------------------
+// sparse Adam (optim.py:42-83)
+// ---------------------------------------------------------------------------
+template <int VEC>
+__global__ void k_adam_rows(const int64_t* __restrict__ offs, int64_t n, const float* __restrict__ grads, int D,
+                            AdamDev a, float* __restrict__ arena) {
+  const int per_row = D / VEC;
+  const int64_t total = n * per_row;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / per_row;
+    int c = (int)(t - i * per_row) * VEC;
+    float* row = arena + offs[i] * (int64_t)(3 * D);
+    if constexpr (VEC == 4) {
+      float4 p = *reinterpret_cast<float4*>(row + c), m = *reinterpret_cast<float4*>(row + D + c),
+             v = *reinterpret_cast<float4*>(row + 2 * D + c), g = ldg4(grads + i * D + c);
+      adam1(p.x, m.x, v.x, g.x, a);
+      adam1(p.y, m.y, v.y, g.y, a);
+      adam1(p.z, m.z, v.z, g.z, a);
+      adam1(p.w, m.w, v.w, g.w, a);
+      st4(row + c, p);
+      st4(row + D + c, m);
+      st4(row + 2 * D + c, v);
+    } else {
+      float p = row[c], m = row[D + c], v = row[2 * D + c];
+      adam1(p, m, v, grads[i * D + c], a);
+      row[c] = p;
+      row[D + c] = m;
+      row[2 * D + c] = v;
+    }
+  }
+}
+
+void table_adam(Table* t, const int64_t* offs, int64_t n, const float* grads, const skb_adam_t& sc, cudaStream_t s) {
+  AdamDev a = to_dev(sc);
+  const int D = (int)t->dim;
+  if (D % 4 == 0 && (uintptr_t)grads % 16 == 0)
+    k_adam_rows<4><<<grid_for(n * (D / 4), 256), 256, 0, s>>>(offs, n, grads, D, a, t->arena);
+  else
+    k_adam_rows<1><<<grid_for(n * D, 256), 256, 0, s>>>(offs, n, grads, D, a, t->arena);
+  SKB_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// misc accessors
+// ---------------------------------------------------------------------------
+__global__ void k_write_last(const int64_t* __restrict__ offs, int64_t n, const int64_t* __restrict__ vals,
+                             int64_t scalar, int64_t* __restrict__ last) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    last[offs[i]] = vals ? vals[i] : scalar;
+}
+
+__global__ void k_clear_aux(const int64_t* __restrict__ offs, int64_t n, int D, float* __restrict__ arena,
+                            int64_t* __restrict__ last) {
+  const int64_t total = n * D;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / D;
+    int c = (int)(t - i * D);
+    float* row = arena + offs[i] * (int64_t)(3 * D);
+    row[D + c] = 0.f;
+    row[2 * D + c] = 0.f;
+    if (c == 0) last[offs[i]] = 0;
+  }
+}
+
+__global__ void k_idmap_get(const int64_t* __restrict__ ids, int64_t n, const HEntry* __restrict__ map, uint64_t mask,
+                            int64_t cap, int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = idmap_find(map, mask, cap, ids[i]);
+}
+
+// put: update in place or insert (dict semantics: a new key is appended)
+__global__ void k_idmap_put(HEntry* map, uint64_t mask, int64_t cap, long long key, long long slot,
+                            int64_t* counters, int64_t* ins_seq) {
+  long long old = idmap_find(map, mask, cap, key);
+  if (old >= 0) {
+    if (key == kEmptyKey) {
+      map[cap].val = slot;
+    } else {
+      uint64_t i = bucket_hash((uint64_t)key) & mask;
+      while (map[i].key != key) i = (i + 1) & mask;
+      map[i].val = slot;
+    }
+    ins_seq[slot] = ins_seq[old];
+    return;
+  }
+  idmap_insert(map, mask, cap, key, slot);
+  ins_seq[slot] = counters[C_SEQ]++;
+  counters[C_ROWS] += 1;
+}
+
+// remove with backward-shift deletion (linear probing stays tombstone-free)
+__global__ void k_idmap_remove(HEntry* map, uint64_t mask, int64_t cap, long long key, int64_t* counters,
+                               int64_t* out_slot) {
+  if (key == kEmptyKey) {
+    *out_slot = map[cap].val;
+    if (map[cap].val >= 0) counters[C_ROWS] -= 1;
+    map[cap].val = -1;
+    return;
+  }
+  uint64_t i = bucket_hash((uint64_t)key) & mask;
+  while (true) {
+    if (map[i].key == key) break;
+    if (map[i].key == kEmptyKey) {
+      *out_slot = -1;
+      return;
+    }
+    i = (i + 1) & mask;
+  }
+  *out_slot = map[i].val;
+  counters[C_ROWS] -= 1;
+  map[i].key = kEmptyKey;
+  map[i].val = -1;
+  uint64_t j = i;
+  while (true) {
+    j = (j + 1) & mask;
+    if (map[j].key == kEmptyKey) break;
+    uint64_t h = bucket_hash((uint64_t)map[j].key) & mask;
+    bool stays = (i <= j) ? (i < h && h <= j) : (i < h || h <= j);
+    if (!stays) {
+      map[i] = map[j];
+      map[j].key = kEmptyKey;
+      map[j].val = -1;
+      i = j;
+    }
+  }
+}
+
+__global__ void k_entry_flags(const HEntry* __restrict__ map, int64_t cap, uint8_t* __restrict__ flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= cap; i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = (i == cap) ? (map[i].val >= 0) : (map[i].key != kEmptyKey);
+}
+
+__global__ void k_entry_pairs(const HEntry* __restrict__ map, int64_t cap, const int64_t* __restrict__ idx, int64_t n,
+                              const int64_t* __restrict__ ins_seq, int64_t* __restrict__ keys,
+                              int64_t* __restrict__ slots, int64_t* __restrict__ seq) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = idx[j];
+    HEntry e = map[i];
+    keys[j] = i == cap ? kEmptyKey : e.key;
+    slots[j] = e.val;
+    seq[j] = ins_seq[e.val];
+  }
+}
+
+__global__ void k_permute2(const int64_t* __restrict__ order, int64_t n, const int64_t* __restrict__ a,
+                           const int64_t* __restrict__ b, int64_t* __restrict__ ao, int64_t* __restrict__ bo) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    ao[j] = a[order[j]];
+    bo[j] = b[order[j]];
+  }
+}
+
+__global__ void k_iota64(int64_t* p, int64_t n) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) p[j] = j;
+}
+
+__global__ void k_initial_rows(const int64_t* __restrict__ ids, int64_t n, int D, uint64_t seed_mix, double scale,
+                               float* __restrict__ out) {
+  const int64_t total = n * D;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / D;
+    int c = (int)(t - i * D);
+    out[t] = init_value(mix64((uint64_t)ids[i] ^ seed_mix), c, scale);
+  }
+}
+
+}  // namespace skb
+
+using namespace skb;
+
+extern "C" {
+
+int skb_initial_rows(int64_t seed, const int64_t* ids, int64_t n, int64_t dim, float* out, void* stream) {
+  SKB_API_BEGIN
+  if (dim < 1) raise(SKB_E_VALUE, dim, "dim must be >= 1");
+  if (n <= 0) return SKB_OK;
+  k_initial_rows<<<grid_for(n * dim, 256), 256, 0, as_stream(stream)>>>(ids, n, (int)dim, mix64((uint64_t)seed),
+                                                                        1.0 / std::sqrt((double)dim), out);
+  SKB_LAUNCH_CHECK();
+  SKB_API_END
+}
+
+int skb_table_create(int64_t dim, int64_t seed, int64_t block_size, int64_t evict_threshold, int64_t capacity_hint,
+                     skb_table_t* out_host) {
+  SKB_API_BEGIN
+  if (dim < 1 || block_size < 1) raise(SKB_E_VALUE, dim, "dim and block_size must be >= 1");
+  Table* t = new Table();
+  t->dim = dim;
+  t->seed = seed;
+  t->block_size = block_size;
+  t->evict_threshold = evict_threshold;
+  SKB_CUDA(cudaGetDevice(&t->device));
+  t->init_scale = 1.0 / std::sqrt((double)dim);
+  t->seed_mix = mix64((uint64_t)seed);
+  cudaStream_t s = nullptr;
+  SKB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  SKB_CUDA(cudaMallocHost(&t->snap_host, sizeof(int64_t) * C_N));
+  SKB_CUDA(cudaEventCreateWithFlags(&t->snap_ev, cudaEventDisableTiming));
+  SKB_CUDA(cudaMalloc(&t->counters, sizeof(int64_t) * C_N));
+  SKB_CUDA(cudaMemsetAsync(t->counters, 0, sizeof(int64_t) * C_N, s));
+  int64_t rows = capacity_hint > 1024 ? capacity_hint : 1024;
+  grow_arena(t, rows, s);
+  rehash(t, next_pow2(rows * 2 > 2048 ? rows * 2 : 2048), s);
+  SKB_CUDA(cudaStreamSynchronize(s));
+  SKB_CUDA(cudaStreamDestroy(s));
+  *out_host = reinterpret_cast<skb_table_t>(t);
+  SKB_API_END
+}
+
+int skb_table_destroy(skb_table_t h) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  SKB_CUDA(cudaDeviceSynchronize());
+  cudaFree(t->arena);
+  cudaFree(t->last_step);
+  cudaFree(t->live);
+  cudaFree(t->slot_key);
+  cudaFree(t->ins_seq);
+  cudaFree(t->free_list);
+  cudaFree(t->idmap);
+  cudaFree(t->counters);
+  cudaFreeHost(t->snap_host);
+  cudaEventDestroy(t->snap_ev);
+  if (t->fused) fused_ctx_destroy(t->fused);
+  delete t;
+  SKB_API_END
+}
+
+int skb_table_stats(skb_table_t h, int64_t* stats_host, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  table_refresh(t, as_stream(stream));
+  stats_host[0] = t->known[C_ROWS];
+  stats_host[1] = t->known[C_ALLOC];
+  stats_host[2] = t->known[C_FREE];
+  stats_host[3] = reported_capacity(t);
+  stats_host[4] = t->arena_rows;
+  stats_host[5] = t->idmap_cap;
+  SKB_API_END
+}
+
+int skb_table_lookup_or_insert(skb_table_t h, const int64_t* ids, int64_t n, int64_t step, int64_t* offsets_out,
+                               void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  cudaStream_t s = as_stream(stream);
+  if (n <= 0) return SKB_OK;
+  if (first_duplicate(ids, n, s) >= 0) raise(SKB_E_VALUE, 0, "lookup_or_insert requires duplicate-free ids");
+  table_admit(t, ids, n, step, offsets_out, s);
+  SKB_API_END
+}
+
+int skb_table_admit_unique(skb_table_t h, const int64_t* ids, int64_t n, int64_t step, int64_t* offsets_out,
+                           void* stream) {
+  SKB_API_BEGIN
+  if (n <= 0) return SKB_OK;
+  table_admit(table_from(h), ids, n, step, offsets_out, as_stream(stream));
+  SKB_API_END
+}
+
+int skb_table_gather_unchecked(skb_table_t h, const int64_t* offsets, int64_t n, float* rows_out, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  if (n <= 0) return SKB_OK;
+  const int D = (int)t->dim;
+  launch_rows_gather(IdxArray{offsets}, t->arena, 3 * D, rows_out, D, n, D, as_stream(stream));
+  SKB_API_END
+}
+
+int skb_sparse_adam_step_unchecked(skb_table_t h, const int64_t* offsets, int64_t n, const float* grads,
+                                   const skb_adam_t* scalars_host, void* stream) {
+  SKB_API_BEGIN
+  if (n <= 0) return SKB_OK;
+  table_adam(table_from(h), offsets, n, grads, *scalars_host, as_stream(stream));
+  SKB_API_END
+}
+
+int skb_table_gather(skb_table_t h, const int64_t* offsets, int64_t n, float* rows_out, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  cudaStream_t s = as_stream(stream);
+  if (n <= 0) return SKB_OK;
+  check_live(t, offsets, n, "gather", s);
+  const int D = (int)t->dim;
+  launch_rows_gather(IdxArray{offsets}, t->arena, 3 * D, rows_out, D, n, D, s);
+  SKB_API_END
+}
+
+int skb_table_scatter_update(skb_table_t h, const int64_t* offsets, int64_t n, const float* rows, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  cudaStream_t s = as_stream(stream);
+  if (n <= 0) return SKB_OK;
+  if (first_duplicate(offsets, n, s) >= 0) raise(SKB_E_VALUE, 0, "scatter_update requires distinct offsets");
+  check_live(t, offsets, n, "scatter_update", s);
+  const int D = (int)t->dim;
+  launch_rows_scatter(IdxArray{offsets}, rows, D, t->arena, 3 * D, n, D, s);
+  SKB_API_END
+}
+
+int skb_table_evict(skb_table_t h, int64_t current_step, int64_t* n_evicted_host, void* stream) {
+  SKB_API_BEGIN
+  *n_evicted_host = table_evict(table_from(h), current_step, as_stream(stream));
+  SKB_API_END
+}
+
+int skb_table_export(skb_table_t h, int64_t* ids, float* w, float* m, float* v, int64_t* last_step, int64_t capacity,
+                     int64_t* n_out_host, void* stream) {
+  SKB_API_BEGIN
+  *n_out_host = table_export(table_from(h), ids, w, m, v, last_step, capacity, as_stream(stream));
+  SKB_API_END
+}
+
+int skb_table_restore(skb_table_t h, const int64_t* ids, int64_t n, const float* w, const float* m, const float* v,
+                      const int64_t* last_step, void* stream) {
+  SKB_API_BEGIN
+  table_restore(table_from(h), ids, n, w, m, v, last_step, as_stream(stream));
+  SKB_API_END
+}
+
+int skb_table_read_rows(skb_table_t h, const int64_t* offsets, int64_t n, int32_t which, float* out, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  cudaStream_t s = as_stream(stream);
+  if (which < 0 || which > 2) raise(SKB_E_ARG, which, "which must be 0 (w), 1 (m) or 2 (v)");
+  if (n <= 0) return SKB_OK;
+  check_range(t, offsets, n, s);
+  const int D = (int)t->dim;
+  launch_rows_gather(IdxArray{offsets}, t->arena + which * D, 3 * D, out, D, n, D, s);
+  SKB_API_END
+}
+
+int skb_table_write_rows(skb_table_t h, const int64_t* offsets, int64_t n, int32_t which, const float* rows,
+                         void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  cudaStream_t s = as_stream(stream);
+  if (which < 0 || which > 2) raise(SKB_E_ARG, which, "which must be 0 (w), 1 (m) or 2 (v)");
+  if (n <= 0) return SKB_OK;
+  check_range(t, offsets, n, s);
+  const int D = (int)t->dim;
+  launch_rows_scatter(IdxArray{offsets}, rows, D, t->arena + which * D, 3 * D, n, D, s);
+  SKB_API_END
+}
+
+int skb_table_read_last_step(skb_table_t h, const int64_t* offsets, int64_t n, int64_t* out, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  cudaStream_t s = as_stream(stream);
+  if (n <= 0) return SKB_OK;
+  check_range(t, offsets, n, s);
+  k_gather_i64<<<grid_for(n, 256), 256, 0, s>>>(t->last_step, offsets, n, out);
+  SKB_LAUNCH_CHECK();
+  SKB_API_END
+}
+
+int skb_table_write_last_step(skb_table_t h, const int64_t* offsets, int64_t n, const int64_t* vals, int64_t scalar,
+                              void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  cudaStream_t s = as_stream(stream);
+  if (n <= 0) return SKB_OK;
+  check_range(t, offsets, n, s);
+  k_write_last<<<grid_for(n, 256), 256, 0, s>>>(offsets, n, vals, scalar, t->last_step);
+  SKB_LAUNCH_CHECK();
+  SKB_API_END
+}
+
+int skb_table_clear_aux(skb_table_t h, const int64_t* offsets, int64_t n, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  cudaStream_t s = as_stream(stream);
+  if (n <= 0) return SKB_OK;
+  check_range(t, offsets, n, s);
+  k_clear_aux<<<grid_for(n * t->dim, 256), 256, 0, s>>>(offsets, n, (int)t->dim, t->arena, t->last_step);
+  SKB_LAUNCH_CHECK();
+  SKB_API_END
+}
+
+int skb_table_ensure_capacity(skb_table_t h, int64_t slots, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  cudaStream_t s = as_stream(stream);
+  if (slots > t->ensured_slots) t->ensured_slots = slots;
+  int64_t want = (slots + t->block_size - 1) / t->block_size * t->block_size;
+  if (want > t->arena_rows) grow_arena(t, want, s);
+  SKB_API_END
+}
+
+int skb_table_idmap_get(skb_table_t h, const int64_t* ids, int64_t n, int64_t* slots_out, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  cudaStream_t s = as_stream(stream);
+  if (n <= 0) return SKB_OK;
+  k_idmap_get<<<grid_for(n, 256), 256, 0, s>>>(ids, n, t->idmap, (uint64_t)(t->idmap_cap - 1), t->idmap_cap,
+                                              slots_out);
+  SKB_LAUNCH_CHECK();
+  SKB_API_END
+}
+
+int skb_table_idmap_put(skb_table_t h, int64_t id, int64_t slot, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  cudaStream_t s = as_stream(stream);
+  if (slot < 0) raise(SKB_E_VALUE, slot, "slot must be >= 0");
+  table_reserve(t, 1, s);
+  if (slot >= t->arena_rows) grow_arena(t, slot + 1, s);
+  k_idmap_put<<<1, 1, 0, s>>>(t->idmap, (uint64_t)(t->idmap_cap - 1), t->idmap_cap, id, slot, t->counters,
+                              t->ins_seq);
+  SKB_LAUNCH_CHECK();
+  table_refresh(t, s);
+  SKB_API_END
+}
+
+int skb_table_idmap_remove(skb_table_t h, int64_t id, int64_t* slot_out_host, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  cudaStream_t s = as_stream(stream);
+  Scratch out(sizeof(int64_t), s);
+  k_idmap_remove<<<1, 1, 0, s>>>(t->idmap, (uint64_t)(t->idmap_cap - 1), t->idmap_cap, id, t->counters,
+                                 out.as<int64_t>());
+  SKB_LAUNCH_CHECK();
+  int64_t slot = read_i64(out.as<int64_t>(), s);
+  table_refresh(t, s);
+  if (slot < 0) raise(SKB_E_KEY, id, "%lld", (long long)id);
+  *slot_out_host = slot;
+  SKB_API_END
+}
+
+int skb_table_free_list(skb_table_t h, int64_t* out, int64_t capacity, int64_t* n_out_host, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  cudaStream_t s = as_stream(stream);
+  table_refresh(t, s);
+  int64_t F = t->known[C_FREE];
+  if (F > capacity) raise(SKB_E_ARG, F, "free list has %lld entries, buffer holds %lld", (long long)F,
+                          (long long)capacity);
+  if (F) SKB_CUDA(cudaMemcpyAsync(out, t->free_list, sizeof(int64_t) * F, cudaMemcpyDeviceToDevice, s));
+  *n_out_host = F;
+  SKB_API_END
+}
+
+int skb_table_items(skb_table_t h, int64_t* ids, int64_t* slots, int64_t capacity, int64_t* n_out_host,
+                    void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  cudaStream_t s = as_stream(stream);
+  const int64_t cap = t->idmap_cap;
+  Scratch flags(cap + 1, s), idx(sizeof(int64_t) * (cap + 1), s), cnt(sizeof(int64_t), s);
+  k_entry_flags<<<grid_for(cap + 1, 256), 256, 0, s>>>(t->idmap, cap, flags.as<uint8_t>());
+  SKB_LAUNCH_CHECK();
+  select_flagged_index(flags.as<uint8_t>(), cap + 1, idx.as<int64_t>(), cnt.as<int64_t>(), s);
+  int64_t n = read_i64(cnt.as<int64_t>(), s);
+  if (n > capacity) raise(SKB_E_ARG, n, "items buffer too small");
+  *n_out_host = n;
+  if (n == 0) return SKB_OK;
+  Scratch k(8 * n, s), sl(8 * n, s), sq(8 * n, s), sq2(8 * n, s), ord(8 * n, s), ord2(8 * n, s);
+  k_entry_pairs<<<grid_for(n, 256), 256, 0, s>>>(t->idmap, cap, idx.as<int64_t>(), n, t->ins_seq, k.as<int64_t>(),
+                                                sl.as<int64_t>(), sq.as<int64_t>());
+  SKB_LAUNCH_CHECK();
+  k_iota64<<<grid_for(n, 256), 256, 0, s>>>(ord.as<int64_t>(), n);
+  SKB_LAUNCH_CHECK();
+  sort_pairs_i64(sq.as<int64_t>(), sq2.as<int64_t>(), ord.as<int64_t>(), ord2.as<int64_t>(), n, s);
+  k_permute2<<<grid_for(n, 256), 256, 0, s>>>(ord2.as<int64_t>(), n, k.as<int64_t>(), sl.as<int64_t>(), ids, slots);
+  SKB_LAUNCH_CHECK();
+  SKB_API_END
+}
+
+int skb_sparse_adam_step(skb_table_t h, const int64_t* offsets, int64_t n, const float* grads,
+                         const skb_adam_t* scalars_host, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  cudaStream_t s = as_stream(stream);
+  if (n <= 0) return SKB_OK;
+  if (first_duplicate(offsets, n, s) >= 0) raise(SKB_E_VALUE, 0, "sparse_adam_step requires distinct offsets");
+  check_range(t, offsets, n, s);
+  table_adam(t, offsets, n, grads, *scalars_host, s);
+  SKB_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+// table.cuh — the GPU dynamic embedding table (EmbeddingTable embedding.py:151-308).
+//
+// HBM layout (one table):
+//   idmap     HEntry[idmap_cap + 1]   open addressing, linear probing, load <= 0.5;
+//                                     {int64 key, int64 slot}; entry idmap_cap is
+//                                     the side slot for key == INT64_MIN (EMPTY).
+//   arena     float32[arena_rows][3*D]  AoS row = [w | m | v]: Adam reads and
+//                                     writes one contiguous 12*D-byte span; gather
+//                                     reads the leading 4*D bytes.
+//   last_step int64[arena_rows]        BlockStore last-touched step
+//   live      uint8[arena_rows]        EmbeddingTable._live
+//   slot_key  int64[arena_rows]        reverse map slot -> id (export / evict)
+//   ins_seq   int64[arena_rows]        dict insertion sequence of the live entry
+//                                     (evict appends stale slots in this order)
+//   free_list int64[arena_rows]        LIFO free list (top = free_list[F-1])
+//   counters  int64[4]                 {allocated, free_count, num_rows, seq}
+// Slot numbers are exactly the reference's offsets.
+#pragma once
+#include "common.cuh"
+
+namespace skb {
+
+enum { C_ALLOC = 0, C_FREE = 1, C_ROWS = 2, C_SEQ = 3, C_N = 4 };
+
+struct FusedCtx;  // fused.cu
+
+struct Table {
+  int64_t dim = 0, seed = 0, block_size = 0, evict_threshold = -1;
+  int device = 0;
+  double init_scale = 0.0;  // 1 / sqrt(dim), host double (embedding.py:34)
+  uint64_t seed_mix = 0;    // mix64(u64(seed))
+
+  float* arena = nullptr;
+  int64_t arena_rows = 0;
+  int64_t* last_step = nullptr;
+  uint8_t* live = nullptr;
+  int64_t* slot_key = nullptr;
+  int64_t* ins_seq = nullptr;
+  int64_t* free_list = nullptr;
+
+  HEntry* idmap = nullptr;
+  int64_t idmap_cap = 0;
+
+  int64_t* counters = nullptr;  // device int64[C_N]
+  int64_t ensured_slots = 0;    // BlockStore.ensure_capacity high-water mark (host)
+
+  // host-side upper bounds on device counters (async snapshot + pending adds)
+  int64_t* snap_host = nullptr;  // pinned int64[C_N]
+  cudaEvent_t snap_ev = nullptr;
+  bool snap_pending = false;
+  int64_t known[C_N] = {0, 0, 0, 0};
+  int64_t pending_adds = 0;
+
+  FusedCtx* fused = nullptr;
+
+  int64_t row_stride() const { return 3 * dim; }
+};
+
+Table* table_from(skb_table_t h);
+
+// Ensure room for n more insertions (arena + idmap), growing stream-ordered.
+void table_reserve(Table* t, int64_t n, cudaStream_t s);
+// After enqueueing an op that may insert up to n rows: update bounds, snapshot.
+void table_note_inserts(Table* t, int64_t n, cudaStream_t s);
+// Exact counters (synchronizes).
+void table_refresh(Table* t, cudaStream_t s);
+// admission of duplicate-free ids (no duplicate check), offsets out
+void table_admit(Table* t, const int64_t* ids, int64_t n, int64_t step, int64_t* offsets, cudaStream_t s);
+void fused_ctx_destroy(FusedCtx* c);
+
+// device helpers ------------------------------------------------------------
+__device__ __forceinline__ long long idmap_find(const HEntry* t, uint64_t mask, int64_t cap, long long key) {
+  if (key == kEmptyKey) return t[cap].val;
+  uint64_t i = bucket_hash((uint64_t)key) & mask;
+  while (true) {
+    HEntry e = ld_entry(t + i);
+    if (e.key == key) return e.val;
+    if (e.key == kEmptyKey) return -1;
+    i = (i + 1) & mask;
+  }
+}
+
+__device__ __forceinline__ void idmap_insert(HEntry* t, uint64_t mask, int64_t cap, long long key, long long slot) {
+  if (key == kEmptyKey) {
+    t[cap].val = slot;
+    return;
+  }
+  uint64_t i = bucket_hash((uint64_t)key) & mask;
+  while (true) {
+    long long prev = (long long)atomicCAS(reinterpret_cast<unsigned long long*>(&t[i].key),
+                                          (unsigned long long)kEmptyKey, (unsigned long long)key);
+    if (prev == kEmptyKey || prev == key) {
+      t[i].val = slot;
+      return;
+    }
+    i = (i + 1) & mask;
+  }
+}
+
+// initial_rows element (embedding.py:24-36), bit-exact: one double rounding
+// for the scale multiply and one float rounding.
+__device__ __forceinline__ float init_value(uint64_t base, int c, double scale) {
+  uint64_t u = mix64(base + (uint64_t)(c + 1) * kGolden);
+  double u01 = __dmul_rn((double)(u >> 11), 0x1p-53);
+  double x = __dsub_rn(__dmul_rn(2.0, u01), 1.0);
+  return __double2float_rn(__dmul_rn(x, scale));
+}
+
+// slot assignment of the k-th new id given free count F, allocated A
+// (free list LIFO first, then sequential growth; embedding.py:203-207)
+__device__ __forceinline__ int64_t assign_slot(int64_t k, int64_t F, int64_t A, const int64_t* free_list) {
+  return k < F ? free_list[F - 1 - k] : A + (k - F);
+}
+
+// Adam / AdamW on one float4 of a row, every op separately rounded
+// (optim.py:77-83).
+struct AdamDev {
+  float lr, b1, b2, eps, omb1, omb2, bc1, bc2, lrwd;
+  int decay;
+};
+__device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, const AdamDev& a) {
+  if (a.decay) p = __fsub_rn(p, __fmul_rn(a.lrwd, p));
+  m = __fadd_rn(__fmul_rn(a.b1, m), __fmul_rn(a.omb1, g));
+  v = __fadd_rn(__fmul_rn(a.b2, v), __fmul_rn(a.omb2, __fmul_rn(g, g)));
+  float mh = __fdiv_rn(m, a.bc1);
+  float vh = __fdiv_rn(v, a.bc2);
+  p = __fsub_rn(p, __fdiv_rn(__fmul_rn(a.lr, mh), __fadd_rn(__fsqrt_rn(vh), a.eps)));
+}
+inline AdamDev to_dev(const skb_adam_t& s) {
+  return AdamDev{s.lr, s.beta1, s.beta2, s.eps, s.one_minus_beta1, s.one_minus_beta2, s.bc1, s.bc2, s.lr_wd,
+                 (int)s.decoupled_decay};
+}
+
+}  // namespace skb

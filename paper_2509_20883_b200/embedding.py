@@ -1,0 +1,297 @@
+"""Conflict-free dynamic embedding storage on the GPU (reference embedding.py:1-308).
+
+An `EmbeddingTable` owns one native table handle (csrc/table.cu): an
+open-addressing IDMap in HBM in front of an AoS [w|m|v] row arena plus
+last_step / live / insertion-order side arrays.  Slot numbers (offsets) are
+bit-identical to the reference's dict + LIFO free list allocation; rows come
+from the same id-keyed initializer.  `IDMap` and `BlockStore` are views over
+the same handle exposing the reference's attributes.
+
+Arrays: numpy in -> numpy out (drop-in), CUDA tensor in -> CUDA tensor out.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as N
+from . import telemetry
+
+DEFAULT_BLOCK_SIZE = 65536
+
+
+def _check_dtype(dtype):
+    if np.dtype(dtype) != np.float32:
+        raise TypeError("the B200 table stores float32 rows (reference default dtype); got " + str(dtype))
+
+
+class _Handle:
+    """Owns a native skb_table_t."""
+
+    def __init__(self, dim, seed, block_size, evict_threshold, capacity_hint=0):
+        N.lib()
+        h = ctypes.c_void_p()
+        N.check(N.lib().skb_table_create(dim, seed, block_size,
+                                         -1 if evict_threshold is None else int(evict_threshold),
+                                         int(capacity_hint), ctypes.byref(h)))
+        self.h = h
+        self.device = N.torch().cuda.current_device()
+
+    def __del__(self):
+        try:
+            if self.h:
+                N.lib().skb_table_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def stats(self):
+        buf = (ctypes.c_int64 * 6)()
+        N.call("skb_table_stats", self.h, buf, N.stream_ptr())
+        return list(buf)
+
+
+def initial_rows(seed: int, ids, dim: int, dtype=np.float32):
+    """Deterministic initial rows keyed by (seed, id, column) (embedding.py:24-36),
+    computed by the same device function admission uses."""
+    _check_dtype(dtype)
+    as_np = not N.is_torch(ids)
+    ids_d = N.to_dev(np.atleast_1d(np.asarray(ids, np.int64)) if as_np else ids.reshape(-1), "int64")
+    n = ids_d.numel()
+    out = N.empty((n, dim), "float32")
+    if n:
+        seed64 = int(seed) & 0xFFFFFFFFFFFFFFFF
+        seed_i = seed64 - (1 << 64) if seed64 >= (1 << 63) else seed64
+        N.call("skb_initial_rows", seed_i, N.ptr(ids_d), n, int(dim), N.ptr(out), N.stream_ptr())
+    return N.out_like(out, as_np)
+
+
+class IDMap:
+    """First tier: feature id -> slot offset (embedding.py:39-61), device-resident.
+
+    `free_list` returns a snapshot list (bottom .. top); mutate the table
+    through EmbeddingTable methods.
+    """
+
+    def __init__(self, handle: _Handle):
+        self._h = handle
+
+    def __len__(self) -> int:
+        return self._h.stats()[0]
+
+    def get(self, fid: int):
+        d = N.to_dev(np.array([fid], np.int64), "int64")
+        out = N.empty((1,), "int64")
+        N.call("skb_table_idmap_get", self._h.h, N.ptr(d), 1, N.ptr(out), N.stream_ptr())
+        v = int(out.item())
+        return None if v < 0 else v
+
+    def get_many(self, fids):
+        as_np = not N.is_torch(fids)
+        d = N.to_dev(fids, "int64")
+        out = N.empty(d.shape, "int64")
+        if d.numel():
+            N.call("skb_table_idmap_get", self._h.h, N.ptr(d), d.numel(), N.ptr(out), N.stream_ptr())
+        return N.out_like(out, as_np)
+
+    def put(self, fid: int, slot: int) -> None:
+        N.call("skb_table_idmap_put", self._h.h, int(fid), int(slot), N.stream_ptr())
+
+    def remove(self, fid: int) -> int:
+        s = ctypes.c_int64()
+        N.call("skb_table_idmap_remove", self._h.h, int(fid), ctypes.byref(s), N.stream_ptr())
+        return int(s.value)
+
+    def items(self):
+        n = len(self) + 1
+        ids, slots = N.empty((n,), "int64"), N.empty((n,), "int64")
+        cnt = ctypes.c_int64()
+        N.call("skb_table_items", self._h.h, N.ptr(ids), N.ptr(slots), n, ctypes.byref(cnt), N.stream_ptr())
+        k = cnt.value
+        return list(zip(ids[:k].cpu().tolist(), slots[:k].cpu().tolist()))
+
+    @property
+    def free_list(self) -> list:
+        n = self._h.stats()[2]
+        out = N.empty((max(n, 1),), "int64")
+        cnt = ctypes.c_int64()
+        N.call("skb_table_free_list", self._h.h, N.ptr(out), n, ctypes.byref(cnt), N.stream_ptr())
+        return out[: cnt.value].cpu().tolist()
+
+
+class BlockStore:
+    """Second tier: rows + optimizer moments + last_step (embedding.py:64-148).
+
+    Physically one growable HBM arena (no blocks); `capacity` reports the
+    reference's block-granular value so growth stays transparent.
+    """
+
+    def __init__(self, dim: int, block_size: int = DEFAULT_BLOCK_SIZE, dtype=np.float32, *,
+                 _handle: _Handle | None = None):
+        if dim < 1 or block_size < 1:
+            raise ValueError("dim and block_size must be >= 1")
+        _check_dtype(dtype)
+        self.dim = dim
+        self.block_size = block_size
+        self.dtype = np.dtype(dtype)
+        self._h = _handle if _handle is not None else _Handle(dim, 0, block_size, None)
+
+    @property
+    def capacity(self) -> int:
+        return self._h.stats()[3]
+
+    def ensure_capacity(self, slots: int) -> None:
+        N.call("skb_table_ensure_capacity", self._h.h, int(slots), N.stream_ptr())
+
+    def _rows(self, which, offsets):
+        as_np = not N.is_torch(offsets)
+        o = N.to_dev(offsets, "int64").reshape(-1)
+        out = N.empty((o.numel(), self.dim), "float32")
+        if o.numel():
+            N.call("skb_table_read_rows", self._h.h, N.ptr(o), o.numel(), which, N.ptr(out), N.stream_ptr())
+        return N.out_like(out, as_np)
+
+    def _write(self, which, offsets, rows):
+        o = N.to_dev(offsets, "int64").reshape(-1)
+        r = N.to_dev(rows, "float32").reshape(o.numel(), self.dim) if o.numel() else None
+        if o.numel():
+            N.call("skb_table_write_rows", self._h.h, N.ptr(o), o.numel(), which, N.ptr(r), N.stream_ptr())
+
+    def read(self, offsets):
+        return self._rows(0, offsets)
+
+    def write(self, offsets, rows) -> None:
+        self._write(0, offsets, rows)
+
+    def read_state(self, offsets):
+        return self._rows(1, offsets), self._rows(2, offsets)
+
+    def write_state(self, offsets, m, v) -> None:
+        self._write(1, offsets, m)
+        self._write(2, offsets, v)
+
+    def read_last_step(self, offsets):
+        as_np = not N.is_torch(offsets)
+        o = N.to_dev(offsets, "int64").reshape(-1)
+        out = N.empty((o.numel(),), "int64")
+        if o.numel():
+            N.call("skb_table_read_last_step", self._h.h, N.ptr(o), o.numel(), N.ptr(out), N.stream_ptr())
+        return N.out_like(out, as_np)
+
+    def write_last_step(self, offsets, step) -> None:
+        o = N.to_dev(offsets, "int64").reshape(-1)
+        if not o.numel():
+            return
+        if np.ndim(step) == 0 and not N.is_torch(step):
+            N.call("skb_table_write_last_step", self._h.h, N.ptr(o), o.numel(), None, int(step), N.stream_ptr())
+        else:
+            v = N.to_dev(step, "int64").reshape(-1).expand(o.numel()).contiguous()
+            N.call("skb_table_write_last_step", self._h.h, N.ptr(o), o.numel(), N.ptr(v), 0, N.stream_ptr())
+
+    def clear_aux(self, offsets) -> None:
+        o = N.to_dev(offsets, "int64").reshape(-1)
+        if o.numel():
+            N.call("skb_table_clear_aux", self._h.h, N.ptr(o), o.numel(), N.stream_ptr())
+
+
+class EmbeddingTable:
+    """A named conflict-free embedding table with eviction (embedding.py:151-308)."""
+
+    def __init__(self, name: str, dim: int, seed: int = 0, block_size: int = DEFAULT_BLOCK_SIZE,
+                 evict_threshold: int | None = None, dtype=np.float32, *, capacity_hint: int = 0):
+        if dim < 1 or block_size < 1:
+            raise ValueError("dim and block_size must be >= 1")
+        _check_dtype(dtype)
+        self.name = name
+        self.dim = dim
+        self.seed = seed
+        self.evict_threshold = evict_threshold
+        self._h = _Handle(dim, seed, block_size, evict_threshold, capacity_hint)
+        self.idmap = IDMap(self._h)
+        self.store = BlockStore(dim, block_size, dtype, _handle=self._h)
+
+    @property
+    def handle(self):
+        return self._h.h
+
+    @property
+    def num_rows(self) -> int:
+        return self._h.stats()[0]
+
+    def lookup_or_insert(self, unique_ids, step: int):
+        """Slots for duplicate-free ids, admitting unknown ones (embedding.py:185-223)."""
+        telemetry.bump("embedding.lookup_or_insert")
+        as_np = not N.is_torch(unique_ids)
+        ids = N.to_dev(unique_ids, "int64").reshape(-1)
+        out = N.empty(ids.shape, "int64")
+        if ids.numel():
+            N.call("skb_table_lookup_or_insert", self._h.h, N.ptr(ids), ids.numel(), int(step), N.ptr(out),
+                   N.stream_ptr())
+        return N.out_like(out, as_np)
+
+    def _admit_unique(self, ids_dev, step: int):
+        """Admission for ids unique by construction (no duplicate check, no sync)."""
+        out = N.empty(ids_dev.shape, "int64")
+        if ids_dev.numel():
+            N.call("skb_table_admit_unique", self._h.h, N.ptr(ids_dev), ids_dev.numel(), int(step), N.ptr(out),
+                   N.stream_ptr())
+        return out
+
+    def gather(self, offsets):
+        """Rows at live slots, input order, duplicates allowed (embedding.py:233-238)."""
+        telemetry.bump("embedding.gather")
+        as_np = not N.is_torch(offsets)
+        o = N.to_dev(offsets, "int64").reshape(-1)
+        out = N.empty((o.numel(), self.dim), "float32")
+        if o.numel():
+            N.call("skb_table_gather", self._h.h, N.ptr(o), o.numel(), N.ptr(out), N.stream_ptr())
+        return N.out_like(out, as_np)
+
+    def scatter_update(self, offsets, rows) -> None:
+        """Replace rows at distinct live slots (embedding.py:240-250)."""
+        telemetry.bump("embedding.scatter_update")
+        o = N.to_dev(offsets, "int64").reshape(-1)
+        shape = tuple(rows.shape) if hasattr(rows, "shape") else np.asarray(rows).shape
+        if shape != (o.numel(), self.dim):
+            raise ValueError(f"rows shape {shape} != ({o.numel()}, {self.dim})")
+        if not o.numel():
+            return
+        r = N.to_dev(rows, "float32")
+        N.call("skb_table_scatter_update", self._h.h, N.ptr(o), o.numel(), N.ptr(r), N.stream_ptr())
+
+    def evict(self, current_step: int) -> int:
+        """Drop slots idle for more than evict_threshold steps (embedding.py:252-274)."""
+        telemetry.bump("embedding.evict")
+        if self.evict_threshold is None:
+            return 0
+        n = ctypes.c_int64()
+        N.call("skb_table_evict", self._h.h, int(current_step), ctypes.byref(n), N.stream_ptr())
+        return int(n.value)
+
+    def export_rows(self, as_numpy: bool = True):
+        """(ids, weight, m, v, last_step) of all live rows sorted by id (embedding.py:276-284)."""
+        n = self.num_rows
+        cap = max(n, 1)
+        ids, last = N.empty((cap,), "int64"), N.empty((cap,), "int64")
+        w, m, v = (N.empty((cap, self.dim), "float32") for _ in range(3))
+        cnt = ctypes.c_int64()
+        N.call("skb_table_export", self._h.h, N.ptr(ids), N.ptr(w), N.ptr(m), N.ptr(v), N.ptr(last), cap,
+               ctypes.byref(cnt), N.stream_ptr())
+        k = cnt.value
+        parts = (ids[:k], w[:k], m[:k], v[:k], last[:k])
+        return tuple(p.cpu().numpy() for p in parts) if as_numpy else parts
+
+    def restore_rows(self, ids, weight, m, v, last_step) -> None:
+        """Bulk-load checkpoint rows, bypassing the initializer (embedding.py:286-308)."""
+        d = N.to_dev(ids, "int64").reshape(-1)
+        n = d.numel()
+        if n == 0:
+            return
+        w_ = N.to_dev(weight, "float32").reshape(n, self.dim)
+        m_ = N.to_dev(m, "float32").reshape(n, self.dim)
+        v_ = N.to_dev(v, "float32").reshape(n, self.dim)
+        l_ = N.to_dev(last_step, "int64").reshape(-1).expand(n).contiguous()
+        N.call("skb_table_restore", self._h.h, N.ptr(d), n, N.ptr(w_), N.ptr(m_), N.ptr(v_), N.ptr(l_),
+               N.stream_ptr())

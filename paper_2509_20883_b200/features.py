@@ -1,0 +1,205 @@
+"""Feature engine on the GPU (reference features.py:1-189).
+
+Every transform is one multi-column descriptor kernel (csrc/features.cu,
+csrc/hashing.cu); a FusedPlan runs all its columns in one launch and counts
+that launch as its single dispatch (features.py:139-146).
+"""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+
+from . import _native as N
+from . import telemetry
+from .hashing import fnv1a64_packed, pack_strings
+from .ragged import RaggedTensor
+
+
+def _check_boundaries(boundaries) -> np.ndarray:
+    """features.py:21-27."""
+    b = np.asarray(boundaries.cpu().numpy() if N.is_torch(boundaries) else boundaries, dtype=np.float32)
+    if b.ndim != 1:
+        raise ValueError("boundaries must be a 1-D array")
+    if len(b) > 1 and np.any(np.diff(b) <= 0):
+        raise ValueError("boundaries must be strictly increasing")
+    return b
+
+
+def hash_feature(strings: RaggedTensor) -> RaggedTensor:
+    """Byte strings -> int64 ids via FNV-1a 64 (features.py:30-38).
+
+    Object arrays of bytes are packed on the host into the columnar
+    (offsets, blob) layout (columnio.py:96-102) and hashed on the GPU.
+    """
+    telemetry.bump("features.hash_feature")
+    vals = strings.values
+    blob, offs = pack_strings(list(vals))
+    hashed = fnv1a64_packed(blob, offs)
+    return strings.with_values(hashed)
+
+
+def hash_feature_packed(blob, str_offsets, row_offsets) -> RaggedTensor:
+    """Columnar variant: strings already packed as (blob uint8, str_offsets int64)."""
+    telemetry.bump("features.hash_feature")
+    return RaggedTensor(fnv1a64_packed(blob, str_offsets), row_offsets)
+
+
+def _bucketize_flat(vals_d, col_offs_d, C, edges_d, edge_offs_d):
+    n = vals_d.numel()
+    out = N.empty((n,), "int64")
+    if n:
+        N.call("skb_bucketize_multi", N.ptr(vals_d), N.ptr(col_offs_d), C, N.ptr(edges_d), N.ptr(edge_offs_d),
+               N.ptr(out), n, N.stream_ptr())
+    return out
+
+
+def bucketize(values: RaggedTensor, boundaries) -> RaggedTensor:
+    """bin(v) = #{edges e : v >= e} (features.py:41-53); NaN -> ValueError."""
+    telemetry.bump("features.bucketize")
+    b = _check_boundaries(boundaries)
+    as_np = not N.is_torch(values.values)
+    v = N.to_dev(values.values, "float32").reshape(-1)
+    edges = N.to_dev(b if len(b) else np.zeros(1, np.float32), "float32")
+    eo = N.to_dev(np.array([0, len(b)], np.int64), "int64")
+    co = N.to_dev(np.array([0, v.numel()], np.int64), "int64")
+    out = _bucketize_flat(v, co, 1, edges, eo)
+    return values.with_values(N.out_like(out, as_np))
+
+
+def mod_transform(ids: RaggedTensor, modulus: int) -> RaggedTensor:
+    """Non-negative remainder modulo `modulus` (features.py:56-62)."""
+    telemetry.bump("features.mod_transform")
+    if modulus <= 0:
+        raise ValueError("modulus must be > 0")
+    as_np = not N.is_torch(ids.values)
+    v = N.to_dev(ids.values, "int64").reshape(-1)
+    n = v.numel()
+    out = N.empty((n,), "int64")
+    if n:
+        co = N.to_dev(np.array([0, n], np.int64), "int64")
+        m = N.to_dev(np.array([modulus], np.int64), "int64")
+        N.call("skb_mod_multi", N.ptr(v), N.ptr(co), 1, N.ptr(m), N.ptr(out), n, N.stream_ptr())
+    return ids.with_values(N.out_like(out, as_np))
+
+
+def cross(a: RaggedTensor, b: RaggedTensor) -> RaggedTensor:
+    """Per-row x-major Cartesian product hashed pairwise (features.py:65-89)."""
+    telemetry.bump("features.cross")
+    if a.num_rows != b.num_rows:
+        raise ValueError(f"row-count mismatch: {a.num_rows} vs {b.num_rows}")
+    as_np = not N.is_torch(a.values)
+    av, bv = N.to_dev(a.values, "int64").reshape(-1), N.to_dev(b.values, "int64").reshape(-1)
+    ao, bo = N.to_dev(a.row_offsets, "int64"), N.to_dev(b.row_offsets, "int64")
+    rows = a.num_rows
+    oo = N.empty((rows + 1,), "int64")
+    N.call("skb_cross_offsets", N.ptr(ao), N.ptr(bo), rows, N.ptr(oo), N.stream_ptr())
+    total = int(oo[-1].item())
+    out = N.empty((total,), "int64")
+    if total:
+        N.call("skb_cross", N.ptr(av), N.ptr(ao), N.ptr(bv), N.ptr(bo), rows, N.ptr(oo), total, N.ptr(out),
+               N.stream_ptr())
+    if as_np:
+        return RaggedTensor(out.cpu().numpy(), oo.cpu().numpy())
+    return RaggedTensor(out, oo)
+
+
+class FusedPlan:
+    """Same-kind column transforms executed as one dispatch (features.py:92-162)."""
+
+    def __init__(self, kind: str, params: list):
+        if kind not in ("bucketize", "mod"):
+            raise ValueError(f"unknown fused kind {kind!r}")
+        self.kind = kind
+        self._lock = threading.Lock()
+        self._dispatches = 0
+        self._dev = None
+        if kind == "bucketize":
+            self.boundaries = [_check_boundaries(b) for b in params]
+        else:
+            self.moduli = np.asarray(params, dtype=np.int64)
+            if self.moduli.ndim != 1 or np.any(self.moduli <= 0):
+                raise ValueError("moduli must be positive")
+
+    @classmethod
+    def for_bucketize(cls, boundaries_per_column) -> "FusedPlan":
+        return cls("bucketize", list(boundaries_per_column))
+
+    @classmethod
+    def for_mod(cls, moduli) -> "FusedPlan":
+        return cls("mod", list(moduli))
+
+    @property
+    def num_columns(self) -> int:
+        return len(self.boundaries) if self.kind == "bucketize" else len(self.moduli)
+
+    @property
+    def dispatch_count(self) -> int:
+        with self._lock:
+            return self._dispatches
+
+    def _record_dispatch(self) -> None:
+        with self._lock:
+            self._dispatches += 1
+
+    def _params_dev(self):
+        """Per-column edges / moduli, uploaded once per plan."""
+        if self._dev is None:
+            if self.kind == "bucketize":
+                e = np.concatenate(self.boundaries) if self.boundaries else np.zeros(0, np.float32)
+                eo = np.zeros(len(self.boundaries) + 1, np.int64)
+                np.cumsum([len(b) for b in self.boundaries], out=eo[1:])
+                self._dev = (N.to_dev(e if len(e) else np.zeros(1, np.float32), "float32"), N.to_dev(eo, "int64"))
+            else:
+                self._dev = (N.to_dev(self.moduli, "int64"),)
+        return self._dev
+
+    def _concat(self, columns, dtype: str):
+        if len(columns) != self.num_columns:
+            raise ValueError(f"plan has {self.num_columns} columns, got {len(columns)}")
+        parts = [N.to_dev(c.values, dtype).reshape(-1) for c in columns]
+        lens = np.array([p.numel() for p in parts], np.int64)
+        co = np.zeros(len(parts) + 1, np.int64)
+        np.cumsum(lens, out=co[1:])
+        t = N.torch()
+        vals = t.cat(parts) if parts else N.empty((0,), dtype)
+        return vals.contiguous(), N.to_dev(co, "int64"), co
+
+
+def _split(out, co, columns, as_np):
+    res = []
+    for i, c in enumerate(columns):
+        piece = out[co[i]:co[i + 1]]
+        res.append(c.with_values(piece.cpu().numpy() if as_np else piece))
+    return res
+
+
+def fused_bucketize(plan: FusedPlan, columns: list) -> list:
+    """Bucketize many columns in one kernel launch (features.py:165-177)."""
+    telemetry.bump("features.fused_bucketize")
+    if plan.kind != "bucketize":
+        raise ValueError("plan is not a bucketize plan")
+    vals, co_d, co = plan._concat(columns, "float32")
+    edges, eo = plan._params_dev()
+    out = _bucketize_flat(vals, co_d, plan.num_columns, edges, eo)
+    plan._record_dispatch()
+    as_np = bool(columns) and not N.is_torch(columns[0].values)
+    return _split(out, co, columns, as_np)
+
+
+def fused_mod(plan: FusedPlan, columns: list) -> list:
+    """Modulus-reduce many columns in one kernel launch (features.py:180-189)."""
+    telemetry.bump("features.fused_mod")
+    if plan.kind != "mod":
+        raise ValueError("plan is not a mod plan")
+    vals, co_d, co = plan._concat(columns, "int64")
+    (mods,) = plan._params_dev()
+    n = vals.numel()
+    out = N.empty((n,), "int64")
+    if n:
+        N.call("skb_mod_multi", N.ptr(vals), N.ptr(co_d), plan.num_columns, N.ptr(mods), N.ptr(out), n,
+               N.stream_ptr())
+    plan._record_dispatch()
+    as_np = bool(columns) and not N.is_torch(columns[0].values)
+    return _split(out, co, columns, as_np)

@@ -1,0 +1,101 @@
+"""Fused sparse step for a request-merged logical table (SURVEY §8b additions).
+
+`lookup_pool` = keys_for + dedup/admission + gather + per-bag pooling in one
+native call; `pool_grad_adam` = the pooled-gradient backward: per unique row
+an in-order fold of dpooled[bag] (/len for mean) followed by Adam/AdamW on
+the row.  On a single shard the results are bit-identical to the reference
+pipeline train.py:130-195 (all_to_all_lookup -> segment_reduce ->
+per-row grad expansion -> all_to_all_grad_update), with per-position grads
+defined in float32 as dpooled[bag] / float32(len) for mean bags.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as N
+from . import telemetry
+from .optim import AdamConfig, adam_scalars
+from .segments import resolve_strategy
+from .sharding import LogicalTable
+
+_MODES = {"sum": 0, "mean": 1}
+
+
+class PackedBatch:
+    """One logical table's batch: member ids concatenated + bag offsets.
+
+    ids       int64 CUDA [N]      members' raw ids, members in `members` order
+    bag_offs  int64 CUDA [G+1]    bag offsets over positions (members' bags concatenated)
+    member_pos / member_bag       host int64 [F+1] ranges per member
+    """
+
+    def __init__(self, lt: LogicalTable, members, ids_list, offsets_list, strategy="auto"):
+        t = N.torch()
+        self.members = list(members)
+        ids_d = [N.to_dev(x, "int64").reshape(-1) for x in ids_list]
+        offs_d = [N.to_dev(o, "int64").reshape(-1) for o in offsets_list]
+        F = len(ids_d)
+        self.member_pos = np.zeros(F + 1, np.int64)
+        self.member_bag = np.zeros(F + 1, np.int64)
+        for f in range(F):
+            self.member_pos[f + 1] = self.member_pos[f] + ids_d[f].numel()
+            self.member_bag[f + 1] = self.member_bag[f] + offs_d[f].numel() - 1
+        self.ids = t.cat(ids_d).contiguous() if F > 1 else ids_d[0]
+        shifted = [offs_d[f][:-1] + int(self.member_pos[f]) for f in range(F)]
+        shifted.append(N.to_dev(np.array([self.member_pos[F]], np.int64), "int64"))
+        self.bag_offs = t.cat(shifted).contiguous()
+        self.salts = np.array([lt.salt(m) if lt.namespaced else 0 for m in self.members], np.uint64)
+        self.strategy = np.array(
+            [0 if resolve_strategy(strategy, int(self.member_pos[f + 1] - self.member_pos[f]),
+                                   int(self.member_bag[f + 1] - self.member_bag[f])) == "sequential" else 1
+             for f in range(F)], np.int32)
+        self.namespaced = lt.namespaced
+
+    @property
+    def num_ids(self) -> int:
+        return int(self.member_pos[-1])
+
+    @property
+    def num_bags(self) -> int:
+        return int(self.member_bag[-1])
+
+
+def lookup_pool(lt: LogicalTable, batch: PackedBatch, step: int, mode: str = "mean", out=None):
+    """Pooled embeddings [G, D] of every bag of the batch (single shard)."""
+    telemetry.bump("fused.lookup_pool")
+    if mode not in _MODES:
+        raise ValueError(f"unknown mode {mode!r}")
+    if lt.num_shards != 1 or lt.dist:
+        raise NotImplementedError("fused lookup_pool runs on one shard; use distributed.DistSparseStep for S > 1")
+    G = batch.num_bags
+    if out is None:
+        out = N.empty((G, lt.dim), "float32")
+    F = len(batch.members)
+    mp = (ctypes.c_int64 * (F + 1))(*batch.member_pos.tolist())
+    mb = (ctypes.c_int64 * (F + 1))(*batch.member_bag.tolist())
+    sl = (ctypes.c_uint64 * max(F, 1))(*[int(s) for s in batch.salts])
+    st = (ctypes.c_int32 * max(F, 1))(*batch.strategy.tolist())
+    N.call("skb_fused_forward", lt.local_table.handle, N.ptr(batch.ids), batch.num_ids, mp, sl, F,
+           1 if batch.namespaced else 0, N.ptr(batch.bag_offs), G, mb, st, _MODES[mode], int(step), N.ptr(out),
+           N.stream_ptr())
+    return out
+
+
+def pool_grad_adam(lt: LogicalTable, dpooled, cfg: AdamConfig, step: int) -> None:
+    """Backward of the last lookup_pool on `lt`: grad fold + Adam/AdamW on touched rows."""
+    telemetry.bump("fused.pool_grad_adam")
+    if step < 1:
+        raise ValueError("global step t must be >= 1")
+    g = N.to_dev(dpooled, "float32")
+    sc = adam_scalars(cfg, step)
+    N.call("skb_fused_backward", lt.local_table.handle, N.ptr(g), ctypes.byref(sc), N.stream_ptr())
+
+
+def last_step_stats(lt: LogicalTable):
+    """(unique rows touched, new rows admitted) of the last fused step (synchronizes)."""
+    u, k = ctypes.c_int64(), ctypes.c_int64()
+    N.call("skb_fused_last_unique", lt.local_table.handle, ctypes.byref(u), ctypes.byref(k), N.stream_ptr())
+    return int(u.value), int(k.value)
