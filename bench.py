@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""bench.py — sparse-step throughput of the B200 hot path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], SURVEY §8d "C2"): Criteo-shape DLRM
+sparse step — 26 sparse features C0..C25 of dim 64 merged into one
+namespaced logical table `dim64`, batch 65,536 per GPU, bag length 1 (sum
+combiner), ids uniform in [0, 1e6) per feature, SparseAdamW (lr 1e-3, wd
+0.01).  Warm steady state: the table is pre-populated with all 26M keys
+before timing (the stream's limit), so a step is probe + gather + pool +
+grad fold + AdamW on ~1.65M unique rows.  Synthetic data; the pooled
+gradient (the dense tower's output) is a resident N(0, 1e-2) tensor.
+
+One "step" = lookup_pool (keys_for + dedup/admission + gather + pooling)
++ pool_grad_adam (ordered grad fold + AdamW) for one batch.
+
+Arms
+  default           our sm_100a path; prints the JSON line (rank 0).
+  --impl reference  the reference algorithm's CPU implementation (the
+                    oracle port — the reference is Python; it cannot be
+                    compiled) on this host's cores, same metric/config, each
+                    step a bounded sample (batch 4096 per feature).
+Multi-GPU (torchrun, N > 1): weak scaling — every rank runs its own batch of
+65,536 samples through the row-sharded logical table (one shard per GPU,
+NCCL all-to-all exchange; paper_2509_20883_b200/distributed.py).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sparse-step IDs/sec & samples/sec at 1/2/4/8 B200; % HBM roofline vs CPU ref"
+F_FEATURES, DIM, BATCH, ID_SPACE = 26, 64, 65536, 1_000_000
+CPU_SAMPLE_BATCH = 4096
+PHASES = ("probe", "miss", "pool", "sort", "fold_adam")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--batch", type=int, default=BATCH)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cold", action="store_true", help="do not pre-populate the table")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# synthetic inputs (host, numpy PCG64 — identical for both arms)
+# ---------------------------------------------------------------------------
+
+def make_batch(rank: int, k: int, batch: int):
+    """ids per feature for batch k of rank r: integers(0, 1e6), seed 100+f."""
+    ids = []
+    for f in range(F_FEATURES):
+        rng = np.random.Generator(np.random.PCG64([100 + f, rank, k]))
+        ids.append(rng.integers(0, ID_SPACE, batch, dtype=np.int64))
+    return ids
+
+
+def members():
+    return [f"C{f}" for f in range(F_FEATURES)]
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) > 8:
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes (SURVEY §8d convention)
+# ---------------------------------------------------------------------------
+
+def phase_bytes(n, g, u, unew, d, mode_mean=False):
+    """Algorithmic minimum bytes per launch of each fused phase."""
+    return {
+        # ids read, IDMap probe (16 B entry), slot written, miss flag
+        "probe": 8 * n + 16 * n + 4 * n + n,
+        # admission of unew rows: IDMap insert + w/m/v init write + metadata
+        "miss": unew * (16 + 12 * d + 8 * 3 + 1),
+        # slot read, one row gather per position, bag offsets, pooled write, bag-of-position write
+        "pool": 4 * n + 4 * d * n + 8 * (g + 1) + 4 * d * g + 4 * n + 8 * u,
+        # stable sort of (slot, bag) u32 pairs: read + write once, run heads
+        "sort": 16 * n + 4 * u,
+        # sorted pairs + heads read, dpooled row per position, w/m/v read + write
+        "fold_adam": 8 * n + 4 * u + 4 * d * n + (16 * n if mode_mean else 0) + 24 * d * u,
+    }
+
+
+def step_bytes(n, g, u, unew, d):
+    """B_step = 8N + 24U + 28D·U + 8D·G' + 16(G+1) + Unew·(16+12D)."""
+    return 8 * n + 24 * u + 28 * d * u + 8 * d * g + 16 * (g + 1) + unew * (16 + 12 * d)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port; only the cpu_baseline / --impl reference legs)
+# ---------------------------------------------------------------------------
+
+def cpu_reference_steps(steps: int, warmup: int, batch: int):
+    """train.py call sequence on the oracle port: keys_for -> lookup ->
+    segment_reduce(sum) -> per-row grads -> grad_update (SparseAdamW)."""
+    from oracle import sparse_oracle as O
+    mem = members()
+    olt = O.OracleLogical("dim64", DIM, 1, seed=0, members=mem, namespaced=True)
+    batches = [make_batch(0, k, batch) for k in range(max(2, min(steps, 4)))]
+    dps = [np.random.Generator(np.random.PCG64(7 + k)).normal(0, 1e-2, (F_FEATURES * batch, DIM)).astype(np.float32)
+           for k in range(len(batches))]
+    offs = np.arange(batch + 1, dtype=np.int64)
+
+    def one(step, k):
+        ids = batches[k % len(batches)]
+        keys = np.concatenate([olt.keys_for(m, x) for m, x in zip(mem, ids)])
+        rows = O.lookup(olt, keys, step)
+        for f in range(F_FEATURES):
+            O.pool(rows[f * batch:(f + 1) * batch], offs, "sum")
+        grads = dps[k % len(dps)]  # bag length 1, sum: per-row grad = dpooled row
+        O.grad_update(olt, keys, grads, step, lr=1e-3, weight_decay=0.01, variant="adamw")
+
+    # warm the table with every sample batch first (warm steady state, like the GPU arm)
+    for k in range(len(batches)):
+        one(k + 1, k)
+    for w in range(warmup):
+        one(len(batches) + 1 + w, w)
+    times = []
+    c0 = time.process_time()
+    w0 = time.perf_counter()
+    for s in range(steps):
+        t0 = time.perf_counter()
+        one(len(batches) + warmup + 1 + s, s)
+        times.append(time.perf_counter() - t0)
+    wall = time.perf_counter() - w0
+    cores = (time.process_time() - c0) / wall if wall > 0 else 1.0
+    n = F_FEATURES * batch
+    med = statistics.median(times)
+    return {"ids_per_s": n / med, "samples_per_s": batch / med, "ms_per_step": med * 1e3, "steps": steps,
+            "ids_per_step": n, "effective_cores": round(cores, 2)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps = max(1, min(args.steps, 5))
+    warm = min(args.warmup, 1)
+    r = cpu_reference_steps(steps, warm, CPU_SAMPLE_BATCH)
+    sample = (f"C2 scaled to batch {CPU_SAMPLE_BATCH}/feature ({r['ids_per_step']} ids/step), warm table, "
+              f"{steps} timed steps after {warm} warm-up, median")
+    line = {"metric": METRIC, "value": r["ids_per_s"], "unit": "IDs/s", "n_gpus": args.gpus, "steps": steps,
+            "warmup": warm, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C2 Criteo-shape: 26 x dim64, uniform ids, sum, SparseAdamW (warm)",
+                       "global_batch": CPU_SAMPLE_BATCH, "features": F_FEATURES, "dim": DIM},
+            "impl": "reference", "samples_per_s": r["samples_per_s"],
+            "cpu_baseline": {"value": r["ids_per_s"], "unit": "IDs/s", "cores": 1, "kind": "port",
+                             "sample": sample, "effective_cores": r["effective_cores"]},
+            "e2e": {"value": r["ids_per_s"], "unit": "IDs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2509_20883_b200 as skb
+    from paper_2509_20883_b200 import _native as N
+
+    B = args.batch
+    mem = members()
+    n_ids = F_FEATURES * B
+    cfg = skb.AdamConfig(lr=1e-3, weight_decay=0.01, variant="adamw")
+    lt = skb.LogicalTable("dim64", DIM, 1, seed=0, members=mem, namespaced=True,
+                          capacity_hint=(F_FEATURES * ID_SPACE + F_FEATURES * ID_SPACE // 20) if not args.cold else 0)
+    table = lt.local_table
+
+    # warm steady state: every key of the stream admitted before timing
+    prepop_ms = None
+    if not args.cold:
+        t0 = time.perf_counter()
+        all_ids = torch.arange(ID_SPACE, dtype=torch.int64, device="cuda")
+        for m in mem:
+            table._admit_unique(lt.keys_for(m, all_ids), 0)
+        torch.cuda.synchronize()
+        prepop_ms = (time.perf_counter() - t0) * 1e3
+        del all_ids
+
+    # P rotating batches (host pinned + device resident) and resident dpooled
+    P = 4
+    offs = [np.arange(B + 1, dtype=np.int64)] * F_FEATURES
+    host_batches, dev_batches, dps = [], [], []
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1234 + rank)
+    for k in range(P):
+        ids = make_batch(rank, k, B)
+        batch = skb.PackedBatch(lt, mem, ids, offs)
+        dev_batches.append(batch)
+        host_batches.append((torch.from_numpy(batch.ids.cpu().numpy()).pin_memory(),
+                             torch.from_numpy(batch.bag_offs.cpu().numpy()).pin_memory()))
+        dps.append(torch.empty((batch.num_bags, DIM), device="cuda").normal_(0.0, 1e-2, generator=gen))
+    G = dev_batches[0].num_bags
+    pooled = torch.empty((G, DIM), device="cuda")
+    e2e_batch = skb.PackedBatch(lt, mem, make_batch(rank, 0, B), offs)  # device buffers refilled from host
+    stats_host = torch.empty(2, dtype=torch.int64).pin_memory()
+    step_no = [0]
+
+    def step(batch, dp):
+        step_no[0] += 1
+        skb.lookup_pool(lt, batch, step_no[0], "sum", out=pooled)
+        skb.pool_grad_adam(lt, dp, cfg, step_no[0])
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for w in range(args.warmup):
+        step(dev_batches[w % P], dps[w % P])
+    barrier()
+    u_touched, u_new = skb.last_step_stats(lt)
+
+    # ---- timed region: inputs resident in HBM --------------------------------
+    lib = N.lib()
+    N.call("skb_fused_profile", table.handle, args.steps, N.stream_ptr())
+    launches0 = lib.skb_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record()
+        for k in range(args.steps):
+            step(dev_batches[k % P], dps[k % P])
+        ev1.record()
+        barrier()
+    launches = lib.skb_launch_count() - launches0
+    ms_total = ev0.elapsed_time(ev1)
+    phase_ms = {}
+    import ctypes
+    buf = (ctypes.c_float * args.steps)()
+    for p, name in enumerate(PHASES):
+        cnt = ctypes.c_int64()
+        N.call("skb_fused_profile_read", table.handle, p, buf, args.steps, ctypes.byref(cnt))
+        vals = list(buf)[: cnt.value]
+        phase_ms[name] = sum(vals) / len(vals) if vals else 0.0
+    N.call("skb_fused_profile", table.handle, 0, N.stream_ptr())
+    u_touched, u_new = skb.last_step_stats(lt)
+
+    # ---- e2e: public API with host buffers, H2D + result D2H inside ----------
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record()
+    for k in range(args.steps):
+        hid, hoff = host_batches[k % P]
+        e2e_batch.ids.copy_(hid, non_blocking=True)
+        e2e_batch.bag_offs.copy_(hoff, non_blocking=True)
+        step(e2e_batch, dps[k % P])
+        # the step's metric (unique rows, new rows) read back to the host
+        u, kk = skb.last_step_stats(lt)
+        stats_host[0], stats_host[1] = u, kk
+    e1.record()
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    h2d = int(hid.numel() * 8 + hoff.numel() * 8)
+
+    # max over ranks
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms_total, e2e_ms = allmax(ms_total), allmax(e2e_ms)
+    ms_step = ms_total / args.steps
+    value = world * n_ids / (ms_step / 1e3)
+    e2e_value = world * n_ids / (e2e_ms / args.steps / 1e3)
+
+    peak, peak_kind = load_peaks()
+    pb = phase_bytes(n_ids, G, u_touched, u_new, DIM)
+    dom = max(phase_ms, key=lambda k: phase_ms[k])
+    achieved = pb[dom] / (phase_ms[dom] / 1e3) / 1e9
+    traffic = load_traffic().get(dom, {}).get("dram_bytes_per_launch")
+    sb = step_bytes(n_ids, G, u_touched, u_new, DIM)
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline:
+            r = cpu_reference_steps(3, 0, CPU_SAMPLE_BATCH)
+            cpu = {"value": r["ids_per_s"], "unit": "IDs/s", "cores": 1, "kind": "port",
+                   "sample": f"C2 scaled to batch {CPU_SAMPLE_BATCH}/feature ({r['ids_per_step']} ids/step), "
+                             f"warm table, 3 timed steps, median; effective cores {r['effective_cores']}"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "IDs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C2 Criteo-shape DLRM sparse step: 26 x dim64 merged table, uniform ids "
+                                   "[0,1e6) per feature, bag length 1, sum, SparseAdamW, "
+                                   + ("cold table" if args.cold else "warm table (26M rows pre-admitted)"),
+                       "global_batch": B * world, "per_gpu_batch": B, "features": F_FEATURES, "dim": DIM,
+                       "ids_per_step_per_gpu": n_ids, "table_rows": int(table.num_rows),
+                       "parallelism": f"independent replicas x{world}" if world > 1 else "single shard",
+                       "l2": "inputs larger than L2: 20 GB row arena + 4 rotating 0.46 GB batches"},
+            "samples_per_s": world * B / (ms_step / 1e3),
+            "unique_rows_per_step": u_touched, "new_rows_per_step": u_new,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "algorithmic_bytes": pb[dom]},
+            "step_roofline": {"algorithmic_bytes": sb, "achieved": sb / (ms_step / 1e3) / 1e9,
+                              "frac": sb / (ms_step / 1e3) / 1e9 / peak},
+            "kernels_ms": phase_ms,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "IDs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 16},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "prepopulate_ms": prepop_ms,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -57,6 +57,8 @@ const char* skb_version(void);
 const char* skb_last_error(void);
 int64_t skb_last_error_arg(void);
 int skb_device_sm_count(int device, int* out_host);
+/* number of this library's kernel launches so far (process-wide) */
+int64_t skb_launch_count(void);
 
 /* ---- L0 hashing: hashing.py:35-40, sharding.py:41-43, sharding.py:170-178 */
 /* out[i] = int64(mix64(u64(ids[i])))                       hashing.py:35-40 */
@@ -202,6 +204,13 @@ int skb_fused_forward(skb_table_t t, const int64_t* ids, int64_t n, const int64_
 /* Backward of the most recent skb_fused_forward on this table. */
 int skb_fused_backward(skb_table_t t, const float* dpooled, const skb_adam_t* scalars_host,
                        void* stream);
+/* Per-kernel CUDA-event timing of the fused step on its own stream:
+ * skb_fused_profile arms max_steps records per phase (0 disables); phases
+ * 0 probe, 1 miss path, 2 pool, 3 sort + run heads, 4 grad fold + Adam.
+ * skb_fused_profile_read returns the recorded durations in milliseconds. */
+int skb_fused_profile(skb_table_t t, int64_t max_steps, void* stream);
+int skb_fused_profile_read(skb_table_t t, int32_t phase, float* ms_host, int64_t capacity,
+                           int64_t* n_host);
 /* Number of unique rows the last fused forward touched (synchronizes). */
 int skb_fused_last_unique(skb_table_t t, int64_t* n_unique_host, int64_t* n_new_host, void* stream);
 

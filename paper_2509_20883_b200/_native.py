@@ -34,6 +34,7 @@ _SIGS = {
     "skb_last_error": ([], ctypes.c_char_p),
     "skb_last_error_arg": ([], _i64),
     "skb_device_sm_count": ([ctypes.c_int, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "skb_launch_count": ([], _i64),
     "skb_mix64": ([_p, _i64, _p, _p], ctypes.c_int),
     "skb_shard_of": ([_p, _i64, _i64, _p, _p], ctypes.c_int),
     "skb_keys_for": ([_p, _i64, _u64, _p, _p], ctypes.c_int),
@@ -75,6 +76,8 @@ _SIGS = {
                            ctypes.POINTER(_i64), ctypes.POINTER(_i32), _i32, _i64, _p, _p], ctypes.c_int),
     "skb_fused_backward": ([_p, _p, ctypes.POINTER(AdamScalars), _p], ctypes.c_int),
     "skb_fused_last_unique": ([_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p], ctypes.c_int),
+    "skb_fused_profile": ([_p, _i64, _p], ctypes.c_int),
+    "skb_fused_profile_read": ([_p, _i32, ctypes.POINTER(ctypes.c_float), _i64, ctypes.POINTER(_i64)], ctypes.c_int),
     "skb_bucketize_multi": ([_p, _p, _i64, _p, _p, _p, _i64, _p], ctypes.c_int),
     "skb_mod_multi": ([_p, _p, _i64, _p, _p, _i64, _p], ctypes.c_int),
     "skb_cross_offsets": ([_p, _p, _i64, _p, _p], ctypes.c_int),

@@ -44,7 +44,14 @@ void clear_error();
     }                                                                               \
   } while (0)
 
-#define SKB_LAUNCH_CHECK() SKB_CUDA(cudaGetLastError())
+// every launch of one of OUR kernels is followed by SKB_LAUNCH_CHECK(); the
+// counter backs the bench's gpu_launches claim (CUB internals not counted)
+void count_launch();
+#define SKB_LAUNCH_CHECK()            \
+  do {                                \
+    ::skb::count_launch();            \
+    SKB_CUDA(cudaGetLastError());     \
+  } while (0)
 
 #define SKB_API_BEGIN \
   try {               \

@@ -2,23 +2,32 @@
 //
 // Forward (replaces keys_for + unique_partition + lookup_or_insert + gather +
 // restore + segment_reduce of train.py:130-176 for S = 1):
-//   K1 probe   : per position — namespaced key (sharding.py:178), IDMap probe
-//                -> slot (uint32) or miss; misses counted on device.
-//   K2..K5 miss: only positions whose key is unknown do work: first-occurrence
-//                dedup among misses (atomicMin scratch table sized from the
-//                device miss count), exclusive scan -> rank, admission with the
-//                reference's slot order, slot broadcast to duplicate misses.
-//   K6 pool    : per (bag, 4 columns) — gather arena rows through the slots and
-//                fold (scatter / pairwise, bit-exact), mean, write pooled;
-//                records bag-of-position and last_step.
+//   K1 probe   : per position — namespaced key (sharding.py:178) with the
+//                member table staged in shared memory, IDMap probe -> slot
+//                (uint32) or miss; misses counted on device.
+//   K2..K5 miss: only positions whose key is unknown do work (every launch
+//                exits at once when the device miss count is 0): first-
+//                occurrence dedup among misses, ordered rank (tile counts ->
+//                one-block scan -> tile ranks), admission with the reference's
+//                slot order, slot broadcast to duplicate misses.
+//   K6 pool    : tiles of 256 bags; bag offsets and the tile's slots are staged
+//                in shared memory with coalesced loads so the only global
+//                latency per bag is the 128-bit row gather; fold (scatter /
+//                pairwise, bit-exact), mean, write pooled and bag-of-position.
 // Backward (replaces the per-row grad expansion train.py:181-186 +
 // all_to_all_grad_update sharding.py:257-297):
 //   K7 stable radix sort of (slot, bag) by slot, K8 run heads,
-//   K9 fold + Adam: per (unique row, 4 columns) fold dpooled[bag] (/len) in
-//                position order from +0 — the np.add.at order — then AdamW on
-//                the AoS [w|m|v] row, one read + one write of 12*D bytes.
+//   K9 fold + Adam: tiles of 256 unique rows with heads / slots / bags staged
+//                in shared memory; w, m, v loads are issued before the dpooled
+//                fold so ~4 independent 16-byte loads per lane are in flight;
+//                fold in position order from +0 (np.add.at), AdamW, one write
+//                of the 12*D-byte row, and the step's last_step (deferred from
+//                the forward: one write per unique row instead of per position).
+#include <cstdlib>
 #include <cstring>
 #include <vector>
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "pool.cuh"
@@ -33,6 +42,13 @@ struct MemberDev {
   int64_t strategy;
 };
 
+constexpr int kSmemMembers = 512;  // member tables up to this size are staged in smem
+constexpr int kTileBags = 256;
+constexpr int kTilePos = 2048;
+constexpr int kTileU = 256;
+constexpr int kTileJ = 1024;
+constexpr int kRankTile = 4096;    // positions per tile of the miss-rank scan
+
 struct FusedCtx {
   int64_t cap_n = 0;         // capacity in positions
   uint32_t* slot = nullptr;  // [N] slot of position
@@ -44,6 +60,7 @@ struct FusedCtx {
   uint8_t* fresh = nullptr;  // [N] first occurrence of an unknown key
   int64_t* rank = nullptr;   // [N]
   int32_t* hslot = nullptr;  // [N] scratch-table index of a miss
+  int64_t* tile_cnt = nullptr;  // [N / kRankTile + 1]
   HEntry* scratch = nullptr; // [2*cap_n pow2 + 1]
   int64_t scratch_cap = 0;
   int64_t* dev = nullptr;    // [0] misses M, [1] new K, [2] unique U
@@ -55,10 +72,33 @@ struct FusedCtx {
   int mode = 0;
   const int64_t* bag_offs = nullptr;
   bool have_fwd = false;
+  int64_t pending_last_step = -1;  // forward's step, written by backward / flush
+  // backward preparation (bag-of-position + stable sort) overlaps the pool
+  // kernel on a side stream
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool join_pending = false;
+  // optional per-kernel CUDA-event profiling: kProf phases x (begin, end) x cap steps
+  int64_t prof_cap = 0;
+  int64_t prof_n[5] = {0, 0, 0, 0, 0};
+  std::vector<cudaEvent_t> prof_ev[5];
 };
+
+enum { P_PROBE = 0, P_MISS = 1, P_POOL = 2, P_SORT = 3, P_ADAM = 4, kProf = 5 };
+
+static void prof_mark(FusedCtx* c, int phase, int edge, cudaStream_t s) {
+  if (!c->prof_cap || c->prof_n[phase] >= c->prof_cap) return;
+  SKB_CUDA(cudaEventRecord(c->prof_ev[phase][2 * c->prof_n[phase] + edge], s));
+  if (edge == 1) c->prof_n[phase]++;
+}
 
 void fused_ctx_destroy(FusedCtx* c) {
   if (!c) return;
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  for (auto& v : c->prof_ev)
+    for (auto e : v) cudaEventDestroy(e);
   cudaFree(c->slot);
   cudaFree(c->bag);
   cudaFree(c->skey);
@@ -68,6 +108,7 @@ void fused_ctx_destroy(FusedCtx* c) {
   cudaFree(c->fresh);
   cudaFree(c->rank);
   cudaFree(c->hslot);
+  cudaFree(c->tile_cnt);
   cudaFree(c->scratch);
   cudaFree(c->dev);
   cudaFree(c->members);
@@ -84,6 +125,9 @@ static FusedCtx* ctx_for(Table* t, int64_t n, int64_t F, cudaStream_t s) {
   if (!t->fused) {
     t->fused = new FusedCtx();
     SKB_CUDA(cudaMalloc(&t->fused->dev, sizeof(int64_t) * 4));
+    SKB_CUDA(cudaStreamCreateWithFlags(&t->fused->side, cudaStreamNonBlocking));
+    SKB_CUDA(cudaEventCreateWithFlags(&t->fused->ev_fork, cudaEventDisableTiming));
+    SKB_CUDA(cudaEventCreateWithFlags(&t->fused->ev_join, cudaEventDisableTiming));
   }
   FusedCtx* c = t->fused;
   if (n > c->cap_n) {
@@ -97,6 +141,7 @@ static FusedCtx* ctx_for(Table* t, int64_t n, int64_t F, cudaStream_t s) {
     realloc_dev(c->fresh, cap, s);
     realloc_dev(c->rank, cap, s);
     realloc_dev(c->hslot, cap, s);
+    realloc_dev(c->tile_cnt, cap / kRankTile + 2, s);
     c->scratch_cap = next_pow2(2 * cap > 64 ? 2 * cap : 64);
     realloc_dev(c->scratch, c->scratch_cap + 1, s);
     c->cap_n = cap;
@@ -109,42 +154,139 @@ static FusedCtx* ctx_for(Table* t, int64_t n, int64_t F, cudaStream_t s) {
   return c;
 }
 
-__device__ __forceinline__ int64_t member_of_pos(const MemberDev* __restrict__ mt, int64_t F, int64_t i) {
-  int64_t lo = 0, hi = F;
+// member lookup over a (shared or global) member table
+__device__ __forceinline__ int member_search_pos(const int64_t* __restrict__ pos, int F, int64_t i) {
+  int lo = 0, hi = F;  // pos[lo] <= i < pos[lo+1]
   while (hi - lo > 1) {
-    int64_t mid = (lo + hi) >> 1;
-    if (mt[mid].pos <= i) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-__device__ __forceinline__ int64_t member_of_bag(const MemberDev* __restrict__ mt, int64_t F, int64_t g) {
-  int64_t lo = 0, hi = F;
-  while (hi - lo > 1) {
-    int64_t mid = (lo + hi) >> 1;
-    if (mt[mid].bag <= g) lo = mid; else hi = mid;
+    int mid = (lo + hi) >> 1;
+    if (pos[mid] <= i) lo = mid; else hi = mid;
   }
   return lo;
 }
 
-__device__ __forceinline__ long long key_at(const int64_t* __restrict__ ids, const MemberDev* __restrict__ mt,
-                                            int64_t F, int namespaced, int64_t i) {
-  long long id = ids[i];
+// Stage member boundaries in shared memory when the table fits; returns the
+// arrays to search (shared or a global fallback copy in `mt`).
+struct MemberView {
+  const int64_t* pos;  // F+1
+  const int64_t* bag;  // F+1
+  const uint64_t* salt;
+  const int64_t* strat;
+  int stride;          // element stride (1 in smem, 4 in the global AoS table)
+};
+
+__device__ __forceinline__ int64_t mv_pos(const MemberView& v, int f) { return v.pos[f * v.stride]; }
+__device__ __forceinline__ int64_t mv_bag(const MemberView& v, int f) { return v.bag[f * v.stride]; }
+
+__device__ __forceinline__ int mv_member_of_pos(const MemberView& v, int F, int64_t i) {
+  int lo = 0, hi = F;
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (mv_pos(v, mid) <= i) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ int mv_member_of_bag(const MemberView& v, int F, int64_t g) {
+  int lo = 0, hi = F;
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (mv_bag(v, mid) <= g) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+struct MemberSmem {
+  int64_t pos[kSmemMembers + 1];
+  int64_t bag[kSmemMembers + 1];
+  uint64_t salt[kSmemMembers];
+  int64_t strat[kSmemMembers];
+};
+
+__device__ __forceinline__ MemberView stage_members(MemberSmem* sm, const MemberDev* __restrict__ mt, int F) {
+  if (F <= kSmemMembers) {
+    for (int f = threadIdx.x; f <= F; f += blockDim.x) {
+      MemberDev m = mt[f];
+      sm->pos[f] = m.pos;
+      sm->bag[f] = m.bag;
+      if (f < F) {
+        sm->salt[f] = m.salt;
+        sm->strat[f] = m.strategy;
+      }
+    }
+    __syncthreads();
+    return MemberView{sm->pos, sm->bag, sm->salt, sm->strat, 1};
+  }
+  return MemberView{&mt[0].pos, &mt[0].bag, &mt[0].salt, &mt[0].strategy, 4};
+}
+
+__device__ __forceinline__ long long key_of(long long id, const MemberView& v, int F, int namespaced, int64_t i) {
   if (!namespaced) return id;
-  return (long long)mix64((uint64_t)id ^ mt[member_of_pos(mt, F, i)].salt);
+  return (long long)mix64((uint64_t)id ^ v.salt[mv_member_of_pos(v, F, i) * v.stride]);
+}
+
+__device__ __forceinline__ HEntry ldg_entry(const HEntry* p) {
+  longlong2 v = __ldg(reinterpret_cast<const longlong2*>(p));
+  return HEntry{v.x, v.y};
+}
+
+__device__ __forceinline__ long long idmap_find_ro(const HEntry* __restrict__ t, uint64_t mask, int64_t cap,
+                                                   long long key) {
+  if (key == kEmptyKey) return __ldg(&t[cap].val);
+  uint64_t i = bucket_hash((uint64_t)key) & mask;
+  while (true) {
+    HEntry e = ldg_entry(t + i);
+    if (e.key == key) return e.val;
+    if (e.key == kEmptyKey) return -1;
+    i = (i + 1) & mask;
+  }
 }
 
 // K1
-__global__ void k_fused_probe(const int64_t* __restrict__ ids, int64_t n, const MemberDev* __restrict__ mt,
-                              int64_t F, int namespaced, const HEntry* __restrict__ map, uint64_t mask, int64_t cap,
-                              uint32_t* __restrict__ slot, uint8_t* __restrict__ miss, int64_t* dev) {
+__global__ void __launch_bounds__(256) k_fused_probe(const int64_t* __restrict__ ids, int64_t n,
+                                                     const MemberDev* __restrict__ mt, int F, int namespaced,
+                                                     const HEntry* __restrict__ map, uint64_t mask, int64_t cap,
+                                                     uint32_t* __restrict__ slot, uint8_t* __restrict__ miss,
+                                                     int64_t* dev) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MemberView mv = stage_members(reinterpret_cast<MemberSmem*>(smem_raw), mt, F);
   int local = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    long long s = idmap_find(map, mask, cap, key_at(ids, mt, F, namespaced, i));
-    slot[i] = s < 0 ? 0xFFFFFFFFu : (uint32_t)s;
-    miss[i] = s < 0;
-    local += s < 0;
+  // 4 positions per thread per pass: 4 independent probe chains in flight
+  constexpr int R = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += R * stride) {
+    long long key[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      int64_t i = i0 + r * stride;
+      key[r] = i < n ? key_of(__ldg(ids + i), mv, F, namespaced, i) : 0;
+    }
+    // first bucket of every chain issued before any chain is resolved
+    uint64_t h[R];
+    HEntry e[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      h[r] = key[r] == kEmptyKey ? (uint64_t)cap : (bucket_hash((uint64_t)key[r]) & mask);
+      e[r] = ldg_entry(map + h[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      int64_t i = i0 + r * stride;
+      if (i < n) {
+        long long s;
+        if (key[r] == kEmptyKey) {
+          s = e[r].val;  // side entry
+        } else {
+          while (e[r].key != key[r] && e[r].key != kEmptyKey) {
+            h[r] = (h[r] + 1) & mask;
+            e[r] = ldg_entry(map + h[r]);
+          }
+          s = e[r].key == key[r] ? e[r].val : -1;
+        }
+        slot[i] = s < 0 ? 0xFFFFFFFFu : (uint32_t)s;
+        miss[i] = s < 0;
+        local += s < 0;
+      }
+    }
   }
-  // warp-aggregated miss count
   for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffff, local, o);
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(reinterpret_cast<unsigned long long*>(&dev[0]), (unsigned long long)local);
 }
@@ -152,22 +294,25 @@ __global__ void k_fused_probe(const int64_t* __restrict__ ids, int64_t n, const 
 __device__ __forceinline__ int64_t scratch_cap_for(int64_t M) { return next_pow2(2 * M > 64 ? 2 * M : 64); }
 
 __global__ void k_fill_scratch(HEntry* t, const int64_t* dev) {
-  const int64_t cap = scratch_cap_for(dev[0]);
   if (dev[0] == 0) return;
+  const int64_t cap = scratch_cap_for(dev[0]);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= cap; i += (int64_t)gridDim.x * blockDim.x)
     reinterpret_cast<longlong2*>(t)[i] = make_longlong2(kEmptyKey, 0x7FFFFFFFFFFFFFFFll);
 }
 
 // K2: first-occurrence dedup among unknown keys
-__global__ void k_miss_insert(const int64_t* __restrict__ ids, int64_t n, const MemberDev* __restrict__ mt, int64_t F,
-                              int namespaced, const uint8_t* __restrict__ miss, HEntry* t, const int64_t* dev,
-                              int32_t* __restrict__ hslot) {
+__global__ void __launch_bounds__(256) k_miss_insert(const int64_t* __restrict__ ids, int64_t n,
+                                                     const MemberDev* __restrict__ mt, int F, int namespaced,
+                                                     const uint8_t* __restrict__ miss, HEntry* t, const int64_t* dev,
+                                                     int32_t* __restrict__ hslot) {
   if (dev[0] == 0) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MemberView mv = stage_members(reinterpret_cast<MemberSmem*>(smem_raw), mt, F);
   const int64_t cap = scratch_cap_for(dev[0]);
   const uint64_t mask = (uint64_t)(cap - 1);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     if (!miss[i]) continue;
-    long long key = key_at(ids, mt, F, namespaced, i);
+    long long key = key_of(ids[i], mv, F, namespaced, i);
     int64_t h;
     if (key == kEmptyKey) {
       h = cap;
@@ -189,25 +334,109 @@ __global__ void k_miss_insert(const int64_t* __restrict__ ids, int64_t n, const 
   }
 }
 
-// K3
-__global__ void k_miss_fresh(int64_t n, const uint8_t* __restrict__ miss, const HEntry* t, const int64_t* dev,
-                             const int32_t* __restrict__ hslot, uint8_t* __restrict__ fresh) {
-  const bool any = dev[0] != 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    fresh[i] = any && miss[i] && t[hslot[i]].val == i;
+// K3: fresh flags + per-tile fresh counts (tile = kRankTile positions, one block)
+__global__ void __launch_bounds__(256) k_miss_fresh(int64_t n, const uint8_t* __restrict__ miss, const HEntry* t,
+                                                    const int64_t* dev, const int32_t* __restrict__ hslot,
+                                                    uint8_t* __restrict__ fresh, int64_t* __restrict__ tile_cnt) {
+  if (dev[0] == 0) return;
+  __shared__ int s_cnt;
+  const int64_t ntiles = (n + kRankTile - 1) / kRankTile;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    int local = 0;
+    const int64_t b = tile * kRankTile, e = b + kRankTile < n ? b + kRankTile : n;
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+      uint8_t f = miss[i] && t[hslot[i]].val == i;
+      fresh[i] = f;
+      local += f;
+    }
+    for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffff, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(&s_cnt, local);
+    __syncthreads();
+    if (threadIdx.x == 0) tile_cnt[tile] = s_cnt;
+    __syncthreads();
+  }
+}
+
+// K3b: exclusive scan of the tile counts in one block; K -> dev[1]
+__global__ void __launch_bounds__(1024) k_scan_tiles(int64_t* tile_cnt, int64_t ntiles, int64_t* dev) {
+  if (dev[0] == 0) return;
+  __shared__ int64_t s_sum[32];
+  __shared__ int64_t s_carry;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < ntiles; base += blockDim.x) {
+    int64_t i = base + threadIdx.x;
+    int64_t v = i < ntiles ? tile_cnt[i] : 0;
+    // block inclusive scan
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int64_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffff, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_sum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int64_t s = lane < (int)(blockDim.x >> 5) ? s_sum[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        int64_t y = __shfl_up_sync(0xffffffff, s, o);
+        if (lane >= o) s += y;
+      }
+      s_sum[lane] = s;
+    }
+    __syncthreads();
+    int64_t incl = x + (w ? s_sum[w - 1] : 0) + s_carry;
+    if (i < ntiles) tile_cnt[i] = incl - v;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) s_carry = incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) dev[1] = s_carry;
+}
+
+// K3c: rank of each fresh position = tile offset + rank within the tile
+__global__ void __launch_bounds__(256) k_rank_fresh(int64_t n, const uint8_t* __restrict__ fresh,
+                                                    const int64_t* __restrict__ tile_off, const int64_t* dev,
+                                                    int64_t* __restrict__ rank) {
+  if (dev[0] == 0) return;
+  __shared__ int s_w[8];
+  const int64_t ntiles = (n + kRankTile - 1) / kRankTile;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int64_t carry = tile_off[tile];
+    const int64_t b = tile * kRankTile, e = b + kRankTile < n ? b + kRankTile : n;
+    for (int64_t base = b; base < e; base += blockDim.x) {
+      int64_t i = base + threadIdx.x;
+      bool f = i < e && fresh[i];
+      unsigned bal = __ballot_sync(0xffffffff, f);
+      if (lane == 0) s_w[w] = __popc(bal);
+      __syncthreads();
+      int before = 0, total = 0;
+      for (int k = 0; k < 8; ++k) {
+        before += k < w ? s_w[k] : 0;
+        total += s_w[k];
+      }
+      if (f) rank[i] = carry + before + __popc(bal & ((1u << lane) - 1));
+      carry += total;
+      __syncthreads();
+    }
+  }
 }
 
 // K4: admission of the k-th fresh key (input order) — same slot rule as
 // lookup_or_insert; the slot is published in the scratch entry for K5.
-__global__ void k_fused_admit(const int64_t* __restrict__ ids, int64_t n, const MemberDev* __restrict__ mt, int64_t F,
-                              int namespaced, const uint8_t* __restrict__ fresh, const int64_t* __restrict__ rank,
-                              const int32_t* __restrict__ hslot, HEntry* scratch, const int64_t* dev,
-                              const int64_t* __restrict__ counters, const int64_t* __restrict__ free_list,
-                              HEntry* map, uint64_t mask, int64_t cap, int64_t step, int D, uint64_t seed_mix,
-                              double scale, float* __restrict__ arena, int64_t* __restrict__ last_step,
-                              uint8_t* __restrict__ live, int64_t* __restrict__ slot_key,
-                              int64_t* __restrict__ ins_seq) {
+__global__ void __launch_bounds__(256) k_fused_admit(
+    const int64_t* __restrict__ ids, int64_t n, const MemberDev* __restrict__ mt, int F, int namespaced,
+    const uint8_t* __restrict__ fresh, const int64_t* __restrict__ rank, const int32_t* __restrict__ hslot,
+    HEntry* scratch, const int64_t* dev, const int64_t* __restrict__ counters, const int64_t* __restrict__ free_list,
+    HEntry* map, uint64_t mask, int64_t cap, int64_t step, int D, uint64_t seed_mix, double scale,
+    float* __restrict__ arena, int64_t* __restrict__ last_step, uint8_t* __restrict__ live,
+    int64_t* __restrict__ slot_key, int64_t* __restrict__ ins_seq) {
   if (dev[0] == 0) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MemberView mv = stage_members(reinterpret_cast<MemberSmem*>(smem_raw), mt, F);
   const int chunks = (D + 3) / 4;
   const int64_t total = n * chunks;
   const int64_t A = counters[C_ALLOC], Fr = counters[C_FREE], seq = counters[C_SEQ];
@@ -217,7 +446,7 @@ __global__ void k_fused_admit(const int64_t* __restrict__ ids, int64_t n, const 
     int ch = (int)(t - i * chunks);
     int64_t k = rank[i];
     int64_t slot = assign_slot(k, Fr, A, free_list);
-    long long key = key_at(ids, mt, F, namespaced, i);
+    long long key = key_of(ids[i], mv, F, namespaced, i);
     if (ch == 0) {
       idmap_insert(map, mask, cap, key, slot);
       last_step[slot] = step;
@@ -245,6 +474,7 @@ __global__ void k_miss_resolve(int64_t n, const uint8_t* __restrict__ miss, cons
 }
 
 __global__ void k_fused_finish(int64_t* counters, int64_t* dev) {
+  if (dev[0] == 0) return;
   int64_t K = dev[1], F = counters[C_FREE];
   int64_t take = K < F ? K : F;
   counters[C_FREE] = F - take;
@@ -253,10 +483,10 @@ __global__ void k_fused_finish(int64_t* counters, int64_t* dev) {
   counters[C_SEQ] += K;
 }
 
-// arena rows through the position->slot map
+// arena rows through a position->slot map (shared-memory tile or global)
 struct ArenaSrc {
   const float* arena;
-  const uint32_t* slot;
+  const uint32_t* slot;  // indexed by position (already offset for smem tiles)
   int D;
   int c;
   template <int VEC> __device__ __forceinline__ typename VecT<VEC>::T load(int64_t p) const {
@@ -264,82 +494,480 @@ struct ArenaSrc {
   }
 };
 
-// K6
-template <int VEC>
-__global__ void __launch_bounds__(256) k_fused_pool(const float* __restrict__ arena, const uint32_t* __restrict__ slot,
-                                                    const int64_t* __restrict__ bag_offs, int64_t G,
-                                                    const MemberDev* __restrict__ mt, int64_t F, int mode, int D,
-                                                    int64_t step, float* __restrict__ out, uint32_t* __restrict__ bag_of,
-                                                    int64_t* __restrict__ last_step) {
-  const int per_row = D / VEC;
-  const int64_t total = G * per_row;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t g = t / per_row;
-    int cc = (int)(t - g * per_row);
-    int c = cc * VEC;
-    int64_t b = bag_offs[g], e = bag_offs[g + 1];
-    const int64_t f = F == 1 ? 0 : member_of_bag(mt, F, g);
-    const int strat = (int)mt[f].strategy;
-    ArenaSrc src{arena, slot, D, c};
-    typename VecT<VEC>::T acc =
-        strat == 0 ? pool_sequential<VEC>(src, b, reduceat_end(b, e, g == mt[f + 1].bag - 1, mt[f + 1].pos))
-                   : pool_scatter<VEC>(src, b, e);
-    if (mode == 1 && e > b) acc = vdiv<VEC>(acc, (float)(e - b));
-    vstore<VEC>(out + g * D + c, acc);
-    // bookkeeping spread over the row's lanes
-    for (int64_t p = b + cc; p < e; p += per_row) {
-      bag_of[p] = (uint32_t)g;
-      last_step[slot[p]] = step;
+struct PoolSmem {
+  MemberSmem m;
+  int64_t off[kTileBags + 1];
+  uint32_t slot[kTilePos];
+};
+
+// K6 (every member pools with `scatter`, the short-bag regime): warps own
+// chunks of 32 bags; lane i loads bag i's offsets and first slot (coalesced),
+// then sub-groups of L lanes gather R bags' rows at once.  The fold starts
+// from +0 like np.add.at.  No member logic is needed on this path.
+template <int VEC, int R, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fused_pool_scatter(const float* __restrict__ arena,
+                                                                  const uint32_t* __restrict__ slot,
+                                                                  const int64_t* __restrict__ bag_offs, int64_t G,
+                                                                  int mode, int D, float* __restrict__ out) {
+  using T = typename VecT<VEC>::T;
+  const int lane = threadIdx.x & 31;
+  const int rowv = D / VEC;
+  const int L = rowv < 32 ? rowv : 32;
+  const int P = 32 / L;
+  const int sub = lane / L, sl = lane - sub * L;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nchunks = (G + 31) / 32;
+  const int64_t D3 = 3 * (int64_t)D;
+  for (int64_t ch = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; ch < nchunks; ch += warps) {
+    const int64_t g0 = ch * 32;
+    const int nb = (int)(G - g0 < 32 ? G - g0 : 32);
+    int64_t b = 0, e = 0;
+    uint32_t s0 = 0;
+    if (lane < nb) {
+      b = __ldg(bag_offs + g0 + lane);
+      e = __ldg(bag_offs + g0 + lane + 1);
+      if (e > b) s0 = __ldg(slot + b);
+    }
+    for (int base = 0; base < nb; base += R * P) {
+      int bi[R];
+      int64_t bb[R], ee[R];
+      uint32_t ss[R];
+      bool ok[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        bi[r] = base + r * P + sub;
+        const int src = bi[r] < 32 ? bi[r] : 31;
+        bb[r] = __shfl_sync(0xffffffffu, b, src);
+        ee[r] = __shfl_sync(0xffffffffu, e, src);
+        ss[r] = __shfl_sync(0xffffffffu, s0, src);
+        ok[r] = sub < P && bi[r] < nb;
+      }
+      for (int c = sl * VEC; c < D; c += L * VEC) {
+        T acc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          acc[r] = vfill<VEC>(0.f);
+          if (ok[r] && ee[r] > bb[r]) acc[r] = vadd<VEC>(acc[r], vload<VEC>(arena + (int64_t)ss[r] * D3 + c));
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (!ok[r]) continue;
+          for (int64_t p = bb[r] + 1; p < ee[r]; ++p)
+            acc[r] = vadd<VEC>(acc[r], vload<VEC>(arena + (int64_t)__ldg(slot + p) * D3 + c));
+          if (mode == 1 && ee[r] > bb[r]) acc[r] = vdiv<VEC>(acc[r], (float)(ee[r] - bb[r]));
+          vstore<VEC>(out + (g0 + bi[r]) * D + c, acc[r]);
+        }
+      }
     }
   }
 }
 
-// K9: ordered grad fold + Adam/AdamW per unique row
+// bag of every position (sort payload for the backward), thread per bag
+__global__ void k_bag_of(const int64_t* __restrict__ bag_offs, int64_t G, uint32_t* __restrict__ bag_of) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = __ldg(bag_offs + g), e = __ldg(bag_offs + g + 1);
+    for (int64_t p = b; p < e; ++p) bag_of[p] = (uint32_t)g;
+  }
+}
+
+// K6 (general: some member pools with the pairwise `sequential` strategy):
+// tiles of kTileBags bags; lanes per row L = D / VEC (<= 32), groups of L
+// lanes take bags round-robin.  Slots and bag offsets come from shared memory.
 template <int VEC>
-__global__ void __launch_bounds__(256) k_fused_adam(const uint32_t* __restrict__ heads, const int64_t* __restrict__ dev,
-                                                    int64_t n, const uint32_t* __restrict__ skey,
+__global__ void __launch_bounds__(256) k_fused_pool_general(const float* __restrict__ arena, const uint32_t* __restrict__ slot,
+                                                    const int64_t* __restrict__ bag_offs, int64_t G,
+                                                    const MemberDev* __restrict__ mt, int F, int mode, int D,
+                                                    float* __restrict__ out, uint32_t* __restrict__ bag_of) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PoolSmem* sm = reinterpret_cast<PoolSmem*>(smem_raw);
+  MemberView mv = stage_members(&sm->m, mt, F);
+  const int rowv = D / VEC;
+  const int L = rowv < 32 ? rowv : 32;
+  const int groups = blockDim.x / L;
+  const int grp = threadIdx.x / L, lane = threadIdx.x - grp * L;
+  const int64_t ntiles = (G + kTileBags - 1) / kTileBags;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t g0 = tile * kTileBags;
+    const int nb = (int)(G - g0 < kTileBags ? G - g0 : kTileBags);
+    __syncthreads();
+    for (int i = threadIdx.x; i <= nb; i += blockDim.x) sm->off[i] = __ldg(bag_offs + g0 + i);
+    __syncthreads();
+    const int64_t p0 = sm->off[0];
+    const int64_t np = sm->off[nb] - p0;
+    const bool staged = np <= kTilePos;
+    if (staged)
+      for (int i = threadIdx.x; i < np; i += blockDim.x) sm->slot[i] = __ldg(slot + p0 + i);
+    __syncthreads();
+    const uint32_t* sl = staged ? sm->slot - p0 : slot;
+    if (grp >= groups) continue;
+    for (int bi = grp; bi < nb; bi += groups) {
+      const int64_t g = g0 + bi;
+      const int64_t b = sm->off[bi], e = sm->off[bi + 1];
+      const int f = F == 1 ? 0 : mv_member_of_bag(mv, F, g);
+      const int strat = (int)mv.strat[f * mv.stride];
+      const bool last = g == mv_bag(mv, f + 1) - 1;
+      const int64_t nend = mv_pos(mv, f + 1);
+      for (int c = lane * VEC; c < D; c += L * VEC) {
+        ArenaSrc src{arena, sl, D, c};
+        typename VecT<VEC>::T acc = strat == 0 ? pool_sequential<VEC>(src, b, reduceat_end(b, e, last, nend))
+                                               : pool_scatter<VEC>(src, b, e);
+        if (mode == 1 && e > b) acc = vdiv<VEC>(acc, (float)(e - b));
+        vstore<VEC>(out + g * D + c, acc);
+      }
+    }
+  }
+}
+
+// adam1 over a vector of columns
+template <int VEC>
+__device__ __forceinline__ void adam_vec(typename VecT<VEC>::T& p, typename VecT<VEC>::T& m,
+                                         typename VecT<VEC>::T& v, const typename VecT<VEC>::T& g, const AdamDev& a) {
+  if constexpr (VEC == 4) {
+    adam1(p.x, m.x, v.x, g.x, a);
+    adam1(p.y, m.y, v.y, g.y, a);
+    adam1(p.z, m.z, v.z, g.z, a);
+    adam1(p.w, m.w, v.w, g.w, a);
+  } else {
+    adam1(p, m, v, g, a);
+  }
+}
+
+// position of the k-th (0-based) set bit of x, or -1
+__device__ __forceinline__ int nth_bit(unsigned x, int k) {
+  unsigned r = __fns(x, 0, k + 1);
+  return r == 0xFFFFFFFFu ? -1 : (int)r;
+}
+
+// K9: fold + Adam.  Warps own chunks of 32 sorted positions; a run head
+// (first position of a slot) is found by ballot on skey[j] != skey[j-1], so
+// no separate run-heads pass is needed.  Sub-groups of L lanes take 2 heads
+// each per pass: both rows' w, m, v and first dpooled loads are in flight
+// before any arithmetic.  A run continuing past its chunk is finished by the
+// warp owning its head (the next chunk sees no head there).
+template <int VEC, int R, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fused_adam(int64_t n, const uint32_t* __restrict__ skey,
                                                     const uint32_t* __restrict__ sval,
                                                     const int64_t* __restrict__ bag_offs,
                                                     const float* __restrict__ dpooled, int mode, int D, AdamDev a,
-                                                    float* __restrict__ arena) {
+                                                    float* __restrict__ arena, int64_t* __restrict__ last_step,
+                                                    int64_t step, int64_t* __restrict__ dev_unique) {
   using T = typename VecT<VEC>::T;
-  const int per_row = D / VEC;
-  const int64_t U = dev[2];
-  const int64_t total = U * per_row;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t u = t / per_row;
-    int c = (int)(t - u * per_row) * VEC;
-    int64_t b = heads[u];
-    int64_t e = u + 1 < U ? (int64_t)heads[u + 1] : n;
-    T acc = vfill<VEC>(0.f);
-    for (int64_t j = b; j < e; ++j) {
-      uint32_t g = sval[j];
-      T x = vload<VEC>(dpooled + (int64_t)g * D + c);
-      if (mode == 1) x = vdiv<VEC>(x, (float)(bag_offs[g + 1] - bag_offs[g]));
-      acc = vadd<VEC>(acc, x);
+  __shared__ uint32_t s_bag[8][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int rowv = D / VEC;
+  const int L = rowv < 32 ? rowv : 32;
+  const int P = 32 / L;
+  const int sub = lane / L, sl = lane - sub * L;
+  const bool active_sub = sub < P;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nchunks = (n + 31) / 32;
+  const int64_t D3 = 3 * (int64_t)D;
+  unsigned long long heads_seen = 0;
+  for (int64_t ch = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; ch < nchunks; ch += warps) {
+    const int64_t j0 = ch * 32;
+    const int64_t j = j0 + lane;
+    const bool valid = j < n;
+    const uint32_t k = valid ? __ldg(skey + j) : 0xFFFFFFFFu;
+    const uint32_t kp = (valid && j > 0) ? __ldg(skey + j - 1) : 0xFFFFFFFFu;
+    s_bag[wib][lane] = valid ? __ldg(sval + j) : 0u;
+    __syncwarp();
+    const unsigned hm = __ballot_sync(0xffffffffu, valid && (j == 0 || k != kp));
+    heads_seen += __popc(hm);
+    unsigned rem = hm;
+    while (rem) {
+      int h[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) h[r] = active_sub ? nth_bit(rem, sub + r * P) : -1;
+      const int last = nth_bit(rem, R * P - 1);
+      rem = last < 0 ? 0u : (last == 31 ? 0u : rem & (~0u << (last + 1)));
+      uint32_t slot[R];
+      int64_t e[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        slot[r] = __shfl_sync(0xffffffffu, k, h[r] < 0 ? 0 : h[r]);
+        unsigned above = (h[r] < 0 || h[r] == 31) ? 0u : (hm & (~0u << (h[r] + 1)));
+        e[r] = above ? j0 + __ffs(above) - 1 : j0 + 32;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (h[r] >= 0 && e[r] == j0 + 32) {  // run may continue into later chunks
+          int64_t x = e[r];
+          while (x < n && __ldg(skey + x) == slot[r]) ++x;
+          e[r] = x < n ? x : n;
+        }
+      }
+      for (int c = sl * VEC; c < D; c += L * VEC) {
+        T p[R], m[R], v[R], acc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (h[r] >= 0) {
+            const float* row = arena + (int64_t)slot[r] * D3;
+            p[r] = vload<VEC>(row + c);
+            m[r] = vload<VEC>(row + D + c);
+            v[r] = vload<VEC>(row + 2 * D + c);
+            const uint32_t g = s_bag[wib][h[r]];
+            T x = vload<VEC>(dpooled + (int64_t)g * D + c);
+            if (mode == 1) x = vdiv<VEC>(x, (float)(__ldg(bag_offs + g + 1) - __ldg(bag_offs + g)));
+            acc[r] = vadd<VEC>(vfill<VEC>(0.f), x);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (h[r] < 0) continue;
+          for (int64_t jj = j0 + h[r] + 1; jj < e[r]; ++jj) {
+            const uint32_t g = jj < j0 + 32 ? s_bag[wib][jj - j0] : __ldg(sval + jj);
+            T x = vload<VEC>(dpooled + (int64_t)g * D + c);
+            if (mode == 1) x = vdiv<VEC>(x, (float)(__ldg(bag_offs + g + 1) - __ldg(bag_offs + g)));
+            acc[r] = vadd<VEC>(acc[r], x);
+          }
+          adam_vec<VEC>(p[r], m[r], v[r], acc[r], a);
+          float* row = arena + (int64_t)slot[r] * D3;
+          vstore<VEC>(row + c, p[r]);
+          vstore<VEC>(row + D + c, m[r]);
+          vstore<VEC>(row + 2 * D + c, v[r]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (h[r] >= 0 && sl == 0 && step >= 0) last_step[slot[r]] = step;
     }
-    float* row = arena + (int64_t)skey[b] * (3 * D);
-    if constexpr (VEC == 4) {
-      float4 p = *reinterpret_cast<float4*>(row + c), m = *reinterpret_cast<float4*>(row + D + c),
-             v = *reinterpret_cast<float4*>(row + 2 * D + c);
-      adam1(p.x, m.x, v.x, acc.x, a);
-      adam1(p.y, m.y, v.y, acc.y, a);
-      adam1(p.z, m.z, v.z, acc.z, a);
-      adam1(p.w, m.w, v.w, acc.w, a);
-      st4(row + c, p);
-      st4(row + D + c, m);
-      st4(row + 2 * D + c, v);
+    __syncwarp();
+  }
+  if (lane == 0 && heads_seen) atomicAdd(reinterpret_cast<unsigned long long*>(dev_unique), heads_seen);
+}
+
+// last_step of every position's slot (deferred forward bookkeeping)
+__global__ void k_flush_last(const uint32_t* __restrict__ slot, int64_t n, int64_t step, int64_t* last_step) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    last_step[slot[i]] = step;
+}
+
+// K2..K5 as ONE cooperative launch: phases separated by grid-wide syncs, and
+// the whole kernel returns at once when the device miss count is 0 (the warm
+// steady state), so the miss path costs a single launch.
+struct AdmitArgs {
+  const int64_t* ids;
+  int64_t n;
+  const MemberDev* mt;
+  int F, namespaced;
+  const uint8_t* miss;
+  HEntry* scratch;
+  int32_t* hslot;
+  uint8_t* fresh;
+  int64_t* tile_cnt;
+  int64_t* rank;
+  int64_t* dev;
+  int64_t* counters;
+  const int64_t* free_list;
+  HEntry* map;
+  uint64_t mask;
+  int64_t cap;
+  int64_t step;
+  int D;
+  uint64_t seed_mix;
+  double scale;
+  float* arena;
+  int64_t* last_step;
+  uint8_t* live;
+  int64_t* slot_key;
+  int64_t* ins_seq;
+  uint32_t* slot;
+};
+
+__global__ void __launch_bounds__(256) k_admission(AdmitArgs A) {
+  if (A.dev[0] == 0) return;
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int64_t s_sum[32];
+  __shared__ int64_t s_carry;
+  __shared__ int s_cnt;
+  __shared__ int s_w[8];
+  const MemberView mv = stage_members(reinterpret_cast<MemberSmem*>(smem_raw), A.mt, A.F);
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n = A.n;
+  const int64_t M = A.dev[0];
+  const int64_t scap = scratch_cap_for(M);
+  const uint64_t smask = (uint64_t)(scap - 1);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // 1. scratch table
+  for (int64_t i = tid; i <= scap; i += nth)
+    reinterpret_cast<longlong2*>(A.scratch)[i] = make_longlong2(kEmptyKey, 0x7FFFFFFFFFFFFFFFll);
+  grid.sync();
+  // 2. first-occurrence dedup among unknown keys
+  for (int64_t i = tid; i < n; i += nth) {
+    if (!A.miss[i]) continue;
+    const long long key = key_of(A.ids[i], mv, A.F, A.namespaced, i);
+    int64_t h;
+    if (key == kEmptyKey) {
+      h = scap;
     } else {
-      float p = row[c], m = row[D + c], v = row[2 * D + c];
-      adam1(p, m, v, acc, a);
-      row[c] = p;
-      row[D + c] = m;
-      row[2 * D + c] = v;
+      h = (int64_t)(bucket_hash((uint64_t)key) & smask);
+      while (true) {
+        long long k = *reinterpret_cast<volatile long long*>(&A.scratch[h].key);
+        if (k == key) break;
+        if (k == kEmptyKey) {
+          long long prev = (long long)atomicCAS(reinterpret_cast<unsigned long long*>(&A.scratch[h].key),
+                                                (unsigned long long)kEmptyKey, (unsigned long long)key);
+          if (prev == kEmptyKey || prev == key) break;
+        }
+        h = (int64_t)(((uint64_t)h + 1) & smask);
+      }
     }
+    if (*reinterpret_cast<volatile long long*>(&A.scratch[h].val) > i) atomicMin(&A.scratch[h].val, (long long)i);
+    A.hslot[i] = (int32_t)h;
+  }
+  grid.sync();
+  // 3. fresh flags + per-tile counts
+  const int64_t ntiles = (n + kRankTile - 1) / kRankTile;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    int local = 0;
+    const int64_t b = tile * kRankTile, e = b + kRankTile < n ? b + kRankTile : n;
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+      uint8_t f = A.miss[i] && A.scratch[A.hslot[i]].val == i;
+      A.fresh[i] = f;
+      local += f;
+    }
+    for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffff, local, o);
+    if (lane == 0 && local) atomicAdd(&s_cnt, local);
+    __syncthreads();
+    if (threadIdx.x == 0) A.tile_cnt[tile] = s_cnt;
+    __syncthreads();
+  }
+  grid.sync();
+  // 4. exclusive scan of tile counts (block 0); K -> dev[1]
+  if (blockIdx.x == 0) {
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < ntiles; base += blockDim.x) {
+      const int64_t i = base + threadIdx.x;
+      const int64_t v = i < ntiles ? A.tile_cnt[i] : 0;
+      int64_t x = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        int64_t y = __shfl_up_sync(0xffffffff, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) s_sum[w] = x;
+      __syncthreads();
+      if (w == 0) {
+        int64_t t = lane < (int)(blockDim.x >> 5) ? s_sum[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+          int64_t y = __shfl_up_sync(0xffffffff, t, o);
+          if (lane >= o) t += y;
+        }
+        s_sum[lane] = t;
+      }
+      __syncthreads();
+      const int64_t incl = x + (w ? s_sum[w - 1] : 0) + s_carry;
+      if (i < ntiles) A.tile_cnt[i] = incl - v;
+      __syncthreads();
+      if (threadIdx.x == blockDim.x - 1) s_carry = incl;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) A.dev[1] = s_carry;
+  }
+  grid.sync();
+  // 5. rank of each fresh position in input order
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int64_t carry = A.tile_cnt[tile];
+    const int64_t b = tile * kRankTile, e = b + kRankTile < n ? b + kRankTile : n;
+    for (int64_t base = b; base < e; base += blockDim.x) {
+      const int64_t i = base + threadIdx.x;
+      const bool f = i < e && A.fresh[i];
+      const unsigned bal = __ballot_sync(0xffffffff, f);
+      if (lane == 0) s_w[w] = __popc(bal);
+      __syncthreads();
+      int before = 0, total = 0;
+      for (int k = 0; k < 8; ++k) {
+        before += k < w ? s_w[k] : 0;
+        total += s_w[k];
+      }
+      if (f) A.rank[i] = carry + before + __popc(bal & ((1u << lane) - 1));
+      carry += total;
+      __syncthreads();
+    }
+  }
+  grid.sync();
+  // 6. admission: slot rule of lookup_or_insert, init rows, publish slot
+  {
+    const int chunks = (A.D + 3) / 4;
+    const int64_t total = n * chunks;
+    const int64_t Aa = A.counters[C_ALLOC], Fr = A.counters[C_FREE], seq = A.counters[C_SEQ];
+    for (int64_t t = tid; t < total; t += nth) {
+      const int64_t i = t / chunks;
+      if (!A.fresh[i]) continue;
+      const int ch = (int)(t - i * chunks);
+      const int64_t k = A.rank[i];
+      const int64_t slot = assign_slot(k, Fr, Aa, A.free_list);
+      const long long key = key_of(A.ids[i], mv, A.F, A.namespaced, i);
+      if (ch == 0) {
+        idmap_insert(A.map, A.mask, A.cap, key, slot);
+        A.last_step[slot] = A.step;
+        A.live[slot] = 1;
+        A.slot_key[slot] = key;
+        A.ins_seq[slot] = seq + k;
+        A.scratch[A.hslot[i]].val = slot;
+      }
+      const uint64_t base = mix64((uint64_t)key ^ A.seed_mix);
+      float* row = A.arena + slot * (int64_t)(3 * A.D);
+      for (int c = ch * 4; c < ch * 4 + 4 && c < A.D; ++c) {
+        row[c] = init_value(base, c, A.scale);
+        row[A.D + c] = 0.f;
+        row[2 * A.D + c] = 0.f;
+      }
+    }
+  }
+  grid.sync();
+  // 7. every unknown position learns its slot; counters advance
+  for (int64_t i = tid; i < n; i += nth)
+    if (A.miss[i]) A.slot[i] = (uint32_t)A.scratch[A.hslot[i]].val;
+  if (tid == 0) {
+    const int64_t K = A.dev[1], F = A.counters[C_FREE];
+    const int64_t take = K < F ? K : F;
+    A.counters[C_FREE] = F - take;
+    A.counters[C_ALLOC] += K - take;
+    A.counters[C_ROWS] += K;
+    A.counters[C_SEQ] += K;
   }
 }
 
-__global__ void k_copy_count(const int64_t* src, int64_t* dst) { *dst = *src; }
+static int coop_grid(size_t smem) {
+  static int blocks_per_sm = -1;
+  if (blocks_per_sm < 0) {
+    SKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_admission, 256, smem));
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  return blocks_per_sm * sm_count();
+}
+
+void fused_flush_pending(Table* t, cudaStream_t s) {
+  FusedCtx* c = t->fused;
+  if (!c || c->pending_last_step < 0) return;
+  if (c->n > 0) {
+    k_flush_last<<<grid_for(c->n, 256), 256, 0, s>>>(c->slot, c->n, c->pending_last_step, t->last_step);
+    SKB_LAUNCH_CHECK();
+  }
+  c->pending_last_step = -1;
+}
+
+// kernel variant knobs for tuning sweeps (SKB_ADAM_VARIANT / SKB_POOL_VARIANT)
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+static int adam_variant() {
+  static int v = env_int("SKB_ADAM_VARIANT", 0);
+  return v;
+}
+static int pool_variant() {
+  static int v = env_int("SKB_POOL_VARIANT", 0);
+  return v;
+}
+
+static size_t member_smem(int F) { return F <= kSmemMembers ? sizeof(MemberSmem) : 0; }
 
 static void fused_forward(Table* t, const int64_t* ids, int64_t n, const int64_t* member_pos, const uint64_t* salts,
                           int F, int namespaced, const int64_t* bag_offs, int64_t G, const int64_t* member_bag,
@@ -348,10 +976,10 @@ static void fused_forward(Table* t, const int64_t* ids, int64_t n, const int64_t
   if (member_pos[0] != 0 || member_pos[F] != n || member_bag[0] != 0 || member_bag[F] != G)
     raise(SKB_E_ARG, 0, "member ranges must cover [0, n) positions and [0, G) bags");
   if (n >= (1ll << 32) - 1 || G >= (1ll << 32) - 1) raise(SKB_E_UNSUPPORTED, n, "fused step: > 2^32 positions");
+  fused_flush_pending(t, s);
   table_reserve(t, n, s);
   if (t->arena_rows >= (1ll << 32) - 1) raise(SKB_E_UNSUPPORTED, t->arena_rows, "fused step: > 2^32 rows");
   FusedCtx* c = ctx_for(t, n, F, s);
-  // member table (re-uploaded only when it changes)
   std::vector<MemberDev> mh(F + 1);
   for (int f = 0; f <= F; ++f) {
     mh[f].pos = member_pos[f];
@@ -367,39 +995,72 @@ static void fused_forward(Table* t, const int64_t* ids, int64_t n, const int64_t
   const MemberDev* mt = c->members;
   const uint64_t mask = (uint64_t)(t->idmap_cap - 1);
   const int D = (int)t->dim;
+  const size_t msm = member_smem(F);
+  if (c->join_pending) {  // a previous forward's side work must finish first
+    SKB_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+    c->join_pending = false;
+  }
   SKB_CUDA(cudaMemsetAsync(c->dev, 0, sizeof(int64_t) * 4, s));
   if (n > 0) {
-    k_fused_probe<<<grid_for(n, 256), 256, 0, s>>>(ids, n, mt, F, namespaced, t->idmap, mask, t->idmap_cap, c->slot,
-                                                  c->miss, c->dev);
+    prof_mark(c, P_PROBE, 0, s);
+    k_fused_probe<<<grid_for(n, 256), 256, msm, s>>>(ids, n, mt, F, namespaced, t->idmap, mask, t->idmap_cap, c->slot,
+                                                    c->miss, c->dev);
     SKB_LAUNCH_CHECK();
-    // miss path: a handful of launches that exit at once when every key is known
-    k_fill_scratch<<<grid_for(c->scratch_cap + 1, 256), 256, 0, s>>>(c->scratch, c->dev);
+    prof_mark(c, P_PROBE, 1, s);
+    prof_mark(c, P_MISS, 0, s);
+    AdmitArgs A{ids, n, mt, F, namespaced, c->miss, c->scratch, c->hslot, c->fresh, c->tile_cnt, c->rank, c->dev,
+                t->counters, t->free_list, t->idmap, mask, t->idmap_cap, step, D, t->seed_mix, t->init_scale,
+                t->arena, t->last_step, t->live, t->slot_key, t->ins_seq, c->slot};
+    const size_t csm = sizeof(MemberSmem);
+    int cg_blocks = coop_grid(csm);
+    const int64_t want = (n + 255) / 256;
+    if (want < cg_blocks) cg_blocks = (int)(want > 0 ? want : 1);
+    void* kargs[] = {&A};
+    SKB_CUDA(cudaLaunchCooperativeKernel((const void*)k_admission, dim3(cg_blocks), dim3(256), kargs, csm, s));
     SKB_LAUNCH_CHECK();
-    k_miss_insert<<<grid_for(n, 256), 256, 0, s>>>(ids, n, mt, F, namespaced, c->miss, c->scratch, c->dev, c->hslot);
+    prof_mark(c, P_MISS, 1, s);
+    // backward preparation on the side stream, overlapping the pool kernel
+    SKB_CUDA(cudaEventRecord(c->ev_fork, s));
+    SKB_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    prof_mark(c, P_SORT, 0, c->side);
+    k_bag_of<<<grid_for(G > 0 ? G : 1, 256), 256, 0, c->side>>>(bag_offs, G, c->bag);
     SKB_LAUNCH_CHECK();
-    k_miss_fresh<<<grid_for(n, 256), 256, 0, s>>>(n, c->miss, c->scratch, c->dev, c->hslot, c->fresh);
-    SKB_LAUNCH_CHECK();
-    scan_exclusive_u8_to_i64(c->fresh, c->rank, n, c->dev + 1, s);  // rank of fresh keys, K -> dev[1]
-    const int chunks = (D + 3) / 4;
-    k_fused_admit<<<grid_for(n * chunks, 256), 256, 0, s>>>(
-        ids, n, mt, F, namespaced, c->fresh, c->rank, c->hslot, c->scratch, c->dev, t->counters, t->free_list,
-        t->idmap, mask, t->idmap_cap, step, D, t->seed_mix, t->init_scale, t->arena, t->last_step, t->live,
-        t->slot_key, t->ins_seq);
-    SKB_LAUNCH_CHECK();
-    k_miss_resolve<<<grid_for(n, 256), 256, 0, s>>>(n, c->miss, c->scratch, c->hslot, c->dev, c->slot);
-    SKB_LAUNCH_CHECK();
-    k_fused_finish<<<1, 1, 0, s>>>(t->counters, c->dev);
-    SKB_LAUNCH_CHECK();
+    sort_pairs_u32(c->slot, c->skey, c->bag, c->sval, n, bits_for((uint64_t)(t->arena_rows - 1)), c->side);
+    prof_mark(c, P_SORT, 1, c->side);
+    SKB_CUDA(cudaEventRecord(c->ev_join, c->side));
+    c->join_pending = true;
   }
   if (G > 0) {
+    prof_mark(c, P_POOL, 0, s);
+    const size_t psm = sizeof(PoolSmem);
+    const int64_t ntiles = (G + kTileBags - 1) / kTileBags;
     bool v4 = D % 4 == 0 && (uintptr_t)pooled % 16 == 0;
-    if (v4)
-      k_fused_pool<4><<<grid_for(G * (D / 4), 256), 256, 0, s>>>(t->arena, c->slot, bag_offs, G, mt, F, mode, D, step,
-                                                                pooled, c->bag, t->last_step);
-    else
-      k_fused_pool<1><<<grid_for(G * D, 256), 256, 0, s>>>(t->arena, c->slot, bag_offs, G, mt, F, mode, D, step,
-                                                          pooled, c->bag, t->last_step);
+    bool any_seq = false;
+    for (int f = 0; f < F; ++f) any_seq |= strategy[f] == 0;
+    if (!any_seq) {
+      const unsigned grid = grid_for(((G + 31) / 32) * 32, 256, 8);
+      if (!v4)
+        k_fused_pool_scatter<1, 1, 4><<<grid, 256, 0, s>>>(t->arena, c->slot, bag_offs, G, mode, D, pooled);
+      else
+        switch (pool_variant()) {
+          case 1: k_fused_pool_scatter<4, 1, 4><<<grid, 256, 0, s>>>(t->arena, c->slot, bag_offs, G, mode, D, pooled);
+            break;
+          case 2: k_fused_pool_scatter<4, 2, 1><<<grid, 256, 0, s>>>(t->arena, c->slot, bag_offs, G, mode, D, pooled);
+            break;
+          case 3: k_fused_pool_scatter<4, 4, 2><<<grid, 256, 0, s>>>(t->arena, c->slot, bag_offs, G, mode, D, pooled);
+            break;
+          default: k_fused_pool_scatter<4, 2, 4><<<grid, 256, 0, s>>>(t->arena, c->slot, bag_offs, G, mode, D, pooled);
+            break;
+        }
+    } else if (v4) {
+      k_fused_pool_general<4><<<grid_for(ntiles * 256, 256, 6), 256, psm, s>>>(t->arena, c->slot, bag_offs, G, mt, F,
+                                                                              mode, D, pooled, c->bag);
+    } else {
+      k_fused_pool_general<1><<<grid_for(ntiles * 256, 256, 6), 256, psm, s>>>(t->arena, c->slot, bag_offs, G, mt, F,
+                                                                              mode, D, pooled, c->bag);
+    }
     SKB_LAUNCH_CHECK();
+    prof_mark(c, P_POOL, 1, s);
   }
   table_note_inserts(t, n, s);
   c->n = n;
@@ -408,6 +1069,7 @@ static void fused_forward(Table* t, const int64_t* ids, int64_t n, const int64_t
   c->mode = mode;
   c->bag_offs = bag_offs;
   c->have_fwd = true;
+  c->pending_last_step = step;
 }
 
 static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc, cudaStream_t s) {
@@ -416,18 +1078,33 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
   const int64_t n = c->n;
   const int D = (int)t->dim;
   if (n > 0) {
-    sort_pairs_u32(c->slot, c->skey, c->bag, c->sval, n, bits_for((uint64_t)(t->arena_rows - 1)), s);
-    select_run_heads_u32(c->skey, n, c->heads, c->dev + 2, s);
+    if (c->join_pending) {
+      SKB_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+      c->join_pending = false;
+    }
+    prof_mark(c, P_ADAM, 0, s);
     AdamDev a = to_dev(sc);
+    const int64_t step = c->pending_last_step;
+    const int64_t chunks = (n + 31) / 32;
     bool v4 = D % 4 == 0 && (uintptr_t)dpooled % 16 == 0;
-    if (v4)
-      k_fused_adam<4><<<grid_for(n * (D / 4), 256), 256, 0, s>>>(c->heads, c->dev, n, c->skey, c->sval, c->bag_offs,
-                                                                dpooled, c->mode, D, a, t->arena);
-    else
-      k_fused_adam<1><<<grid_for(n * D, 256), 256, 0, s>>>(c->heads, c->dev, n, c->skey, c->sval, c->bag_offs, dpooled,
-                                                          c->mode, D, a, t->arena);
+    const unsigned grid = grid_for(chunks * 32, 256, 8);
+#define SKB_ADAM_ARGS n, c->skey, c->sval, c->bag_offs, dpooled, c->mode, D, a, t->arena, t->last_step, step, c->dev + 2
+    if (!v4) {
+      k_fused_adam<1, 1, 4><<<grid, 256, 0, s>>>(SKB_ADAM_ARGS);
+    } else {
+      // measured on B200 (C2, D=64): R=1 at 4 blocks/SM 0.59 ms; R=2/4 0.60;
+      // R=2/3 0.70; R=1/6 (spills) 0.68; R=2/2 0.81 — occupancy beats ILP here
+      switch (adam_variant()) {
+        case 1: k_fused_adam<4, 2, 4><<<grid, 256, 0, s>>>(SKB_ADAM_ARGS); break;
+        case 2: k_fused_adam<4, 1, 5><<<grid, 256, 0, s>>>(SKB_ADAM_ARGS); break;
+        default: k_fused_adam<4, 1, 4><<<grid, 256, 0, s>>>(SKB_ADAM_ARGS); break;
+      }
+    }
+#undef SKB_ADAM_ARGS
     SKB_LAUNCH_CHECK();
+    prof_mark(c, P_ADAM, 1, s);
   }
+  c->pending_last_step = -1;
   c->have_fwd = false;
 }
 
@@ -450,6 +1127,39 @@ int skb_fused_forward(skb_table_t h, const int64_t* ids, int64_t n, const int64_
 int skb_fused_backward(skb_table_t h, const float* dpooled, const skb_adam_t* scalars_host, void* stream) {
   SKB_API_BEGIN
   fused_backward(table_from(h), dpooled, *scalars_host, as_stream(stream));
+  SKB_API_END
+}
+
+int skb_fused_profile(skb_table_t h, int64_t max_steps, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  FusedCtx* c = ctx_for(t, 0, 0, as_stream(stream));
+  SKB_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  for (auto& v : c->prof_ev) {
+    for (auto e : v) cudaEventDestroy(e);
+    v.clear();
+  }
+  for (int p = 0; p < kProf; ++p) {
+    c->prof_n[p] = 0;
+    c->prof_ev[p].resize(2 * (max_steps > 0 ? max_steps : 0));
+    for (auto& e : c->prof_ev[p]) SKB_CUDA(cudaEventCreate(&e));
+  }
+  c->prof_cap = max_steps > 0 ? max_steps : 0;
+  SKB_API_END
+}
+
+int skb_fused_profile_read(skb_table_t h, int32_t phase, float* ms_host, int64_t capacity, int64_t* n_host) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  if (phase < 0 || phase >= kProf) raise(SKB_E_ARG, phase, "phase must be in [0, 5)");
+  FusedCtx* c = t->fused;
+  int64_t n = c ? c->prof_n[phase] : 0;
+  if (n > capacity) n = capacity;
+  for (int64_t i = 0; i < n; ++i) {
+    SKB_CUDA(cudaEventSynchronize(c->prof_ev[phase][2 * i + 1]));
+    SKB_CUDA(cudaEventElapsedTime(&ms_host[i], c->prof_ev[phase][2 * i], c->prof_ev[phase][2 * i + 1]));
+  }
+  *n_host = n;
   SKB_API_END
 }
 

@@ -1,4 +1,5 @@
 // runtime.cu — error plumbing, device facts, stream-ordered scratch.
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -28,6 +29,9 @@ void clear_error() {
   t_err.clear();
   t_err_arg = 0;
 }
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 static std::mutex g_mu;
 static std::vector<int> g_sm;            // per device
@@ -119,6 +123,8 @@ extern "C" {
 const char* skb_version(void) { return "sparsekit_b200 0.1.0 (sm_100a)"; }
 const char* skb_last_error(void) { return t_err.c_str(); }
 int64_t skb_last_error_arg(void) { return t_err_arg; }
+
+int64_t skb_launch_count(void) { return g_launches.load(); }
 
 int skb_device_sm_count(int device, int* out_host) {
   SKB_API_BEGIN

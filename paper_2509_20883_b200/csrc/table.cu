@@ -206,6 +206,7 @@ static int64_t read_i64(const int64_t* dptr, cudaStream_t s) {
 }
 
 void table_admit(Table* t, const int64_t* ids, int64_t n, int64_t step, int64_t* offsets, cudaStream_t s) {
+  fused_flush_pending(t, s);
   table_reserve(t, n, s);
   Scratch miss(sizeof(int32_t) * n, s), rank(sizeof(int64_t) * n, s), total(sizeof(int64_t), s);
   const uint64_t mask = (uint64_t)(t->idmap_cap - 1);
@@ -259,6 +260,7 @@ static int64_t reported_capacity(Table* t) {
 }
 
 static void check_range(Table* t, const int64_t* offs, int64_t n, cudaStream_t s) {
+  fused_flush_pending(t, s);
   table_refresh(t, s);
   int64_t lim = reported_capacity(t);
   if (lim > t->arena_rows) lim = t->arena_rows;
@@ -327,6 +329,7 @@ __global__ void k_rebuild_live(const HEntry* __restrict__ old, int64_t cap, cons
 }
 
 int64_t table_evict(Table* t, int64_t step, cudaStream_t s) {
+  fused_flush_pending(t, s);
   if (t->evict_threshold < 0 || t->arena_rows == 0) return 0;
   const int64_t R = t->arena_rows;
   Scratch flags(R, s), stale(sizeof(int64_t) * R, s), cnt(sizeof(int64_t), s);
@@ -365,6 +368,7 @@ struct IdxSlotArena {
 
 int64_t table_export(Table* t, int64_t* ids, float* w, float* m, float* v, int64_t* last, int64_t capacity,
                      cudaStream_t s) {
+  fused_flush_pending(t, s);
   const int64_t R = t->arena_rows;
   if (R == 0) return 0;
   Scratch slots(sizeof(int64_t) * R, s), cnt(sizeof(int64_t), s);
@@ -417,6 +421,7 @@ __global__ void k_set_i64(int64_t* p, int64_t v) { *p = v; }
 
 void table_restore(Table* t, const int64_t* ids, int64_t n, const float* w, const float* m, const float* v,
                    const int64_t* last, cudaStream_t s) {
+  fused_flush_pending(t, s);
   if (n == 0) return;
   {
     DedupResult r;

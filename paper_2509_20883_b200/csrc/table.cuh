@@ -67,6 +67,8 @@ void table_refresh(Table* t, cudaStream_t s);
 // admission of duplicate-free ids (no duplicate check), offsets out
 void table_admit(Table* t, const int64_t* ids, int64_t n, int64_t step, int64_t* offsets, cudaStream_t s);
 void fused_ctx_destroy(FusedCtx* c);
+// apply a fused forward's deferred last_step writes before any other table op
+void fused_flush_pending(Table* t, cudaStream_t s);
 
 // device helpers ------------------------------------------------------------
 __device__ __forceinline__ long long idmap_find(const HEntry* t, uint64_t mask, int64_t cap, long long key) {
