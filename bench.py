@@ -27,6 +27,7 @@ NCCL all-to-all exchange; paper_2509_20883_b200/distributed.py).
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -288,23 +289,43 @@ def run_ours(args):
         dps.append(torch.empty((batch.num_bags, DIM), device="cuda").normal_(0.0, 1e-2, generator=gen))
     G = dev_batches[0].num_bags
     pooled = torch.empty((G, DIM), device="cuda")
-    e2e_batch = skb.PackedBatch(lt, mem, make_batch(rank, 0, B), offs)  # device buffers refilled from host
-    stats_host = torch.empty(2, dtype=torch.int64).pin_memory()
+    # two device batch buffers refilled from pinned host memory in the e2e arm
+    e2e_batches = [skb.PackedBatch(lt, mem, make_batch(rank, 0, B), offs) for _ in range(2)]
+    stats_host = torch.empty((args.steps, 4), dtype=torch.int64).pin_memory()
     step_no = [0]
 
-    def step(batch, dp):
-        step_no[0] += 1
-        skb.lookup_pool(lt, batch, step_no[0], "sum", out=pooled)
-        skb.pool_grad_adam(lt, dp, cfg, step_no[0])
+    def run_steps(get, count, after_backward=None):
+        """`count` pipelined steps: the index phase (probe, admission, sort) of
+        step k+1 is prefetched between the pool and the fold+Adam of step k,
+        so it runs on the table's index stream underneath the optimizer."""
+        first = step_no[0] + 1
+        skb.prefetch(lt, get(0)[0], first, "sum")
+        for k in range(count):
+            batch, dp = get(k)
+            skb.lookup_pool(lt, batch, first + k, "sum", out=pooled)
+            if k + 1 < count:
+                skb.prefetch(lt, get(k + 1)[0], first + k + 1, "sum")
+            skb.pool_grad_adam(lt, dp, cfg, first + k)
+            if after_backward:
+                after_backward(k)
+        step_no[0] += count
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for w in range(args.warmup):
-        step(dev_batches[w % P], dps[w % P])
+    clk = ClockSampler(local).__enter__()
+    t_wait = time.perf_counter()
+    while not clk.rows and time.perf_counter() - t_wait < 5.0:
+        time.sleep(0.02)
+    run_steps(lambda k: (dev_batches[k % P], dps[k % P]), args.warmup)
     barrier()
+    # untimed soak so clocks settle and the sampler sees the GPU under load
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < 0.4:
+        run_steps(lambda k: (dev_batches[k % P], dps[k % P]), 8)
+        barrier()
     u_touched, u_new = skb.last_step_stats(lt)
 
     # ---- timed region: inputs resident in HBM --------------------------------
@@ -312,17 +333,14 @@ def run_ours(args):
     N.call("skb_fused_profile", table.handle, args.steps, N.stream_ptr())
     launches0 = lib.skb_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        barrier()
-        ev0.record()
-        for k in range(args.steps):
-            step(dev_batches[k % P], dps[k % P])
-        ev1.record()
-        barrier()
+    barrier()
+    ev0.record()
+    run_steps(lambda k: (dev_batches[k % P], dps[k % P]), args.steps)
+    ev1.record()
+    barrier()
     launches = lib.skb_launch_count() - launches0
     ms_total = ev0.elapsed_time(ev1)
     phase_ms = {}
-    import ctypes
     buf = (ctypes.c_float * args.steps)()
     for p, name in enumerate(PHASES):
         cnt = ctypes.c_int64()
@@ -336,18 +354,29 @@ def run_ours(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     e0.record()
-    for k in range(args.steps):
-        hid, hoff = host_batches[k % P]
-        e2e_batch.ids.copy_(hid, non_blocking=True)
-        e2e_batch.bag_offs.copy_(hoff, non_blocking=True)
-        step(e2e_batch, dps[k % P])
-        # the step's metric (unique rows, new rows) read back to the host
-        u, kk = skb.last_step_stats(lt)
-        stats_host[0], stats_host[1] = u, kk
+    staged = {}
+
+    def get_e2e(k):
+        # H2D of step k's inputs from pinned host memory into one of two device
+        # batch buffers (the other may still be read by step k-1's backward)
+        if k not in staged:
+            hid, hoff = host_batches[k % P]
+            eb = e2e_batches[k % 2]
+            eb.ids.copy_(hid, non_blocking=True)
+            eb.bag_offs.copy_(hoff, non_blocking=True)
+            staged[k] = eb
+        return staged[k], dps[k % P]
+
+    def read_result(k):
+        # the step's metrics (misses, new rows, unique rows) back to the host
+        N.call("skb_fused_stats_async", table.handle, ctypes.c_void_p(stats_host[k].data_ptr()), N.stream_ptr())
+
+    run_steps(get_e2e, args.steps, read_result)
     e1.record()
     barrier()
     e2e_ms = e0.elapsed_time(e1)
-    h2d = int(hid.numel() * 8 + hoff.numel() * 8)
+    clk.__exit__(None, None, None)
+    h2d = int(host_batches[0][0].numel() * 8 + host_batches[0][1].numel() * 8)
 
     # max over ranks
     def allmax(x):
@@ -396,7 +425,7 @@ def run_ours(args):
                               "frac": sb / (ms_step / 1e3) / 1e9 / peak},
             "kernels_ms": phase_ms,
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "IDs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 16},
+            "e2e": {"value": e2e_value, "unit": "IDs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 32},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "prepopulate_ms": prepop_ms,

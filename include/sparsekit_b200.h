@@ -201,7 +201,17 @@ int skb_fused_forward(skb_table_t t, const int64_t* ids, int64_t n, const int64_
                       const int64_t* bag_offs, int64_t num_bags, const int64_t* member_bag_host,
                       const int32_t* strategy_host, int32_t mode, int64_t step, float* pooled_out,
                       void* stream);
-/* Backward of the most recent skb_fused_forward on this table. */
+/* Index phase only (probe, admission, sort) of a batch, enqueued on the
+ * table's internal index stream after `stream`'s pending work: prefetching
+ * batch k+1 before the backward of batch k overlaps its index work with the
+ * fold+Adam of step k (at most two batches in flight).  The following
+ * skb_fused_forward with the same arguments pools it.  Do not prefetch across
+ * an eviction / restore boundary (admission would precede it). */
+int skb_fused_prepare(skb_table_t t, const int64_t* ids, int64_t n, const int64_t* member_pos_host,
+                      const uint64_t* salts_host, int32_t num_members, int32_t namespaced,
+                      const int64_t* bag_offs, int64_t num_bags, const int64_t* member_bag_host,
+                      const int32_t* strategy_host, int32_t mode, int64_t step, void* stream);
+/* Backward of the oldest pooled, not yet backwarded fused batch. */
 int skb_fused_backward(skb_table_t t, const float* dpooled, const skb_adam_t* scalars_host,
                        void* stream);
 /* Per-kernel CUDA-event timing of the fused step on its own stream:
@@ -211,6 +221,9 @@ int skb_fused_backward(skb_table_t t, const float* dpooled, const skb_adam_t* sc
 int skb_fused_profile(skb_table_t t, int64_t max_steps, void* stream);
 int skb_fused_profile_read(skb_table_t t, int32_t phase, float* ms_host, int64_t capacity,
                            int64_t* n_host);
+/* Stream-ordered copy of the last completed fused step's counters
+ * {misses, new rows, unique rows, 0} into pinned host memory (no sync). */
+int skb_fused_stats_async(skb_table_t t, int64_t* dst_pinned_host, void* stream);
 /* Number of unique rows the last fused forward touched (synchronizes). */
 int skb_fused_last_unique(skb_table_t t, int64_t* n_unique_host, int64_t* n_new_host, void* stream);
 

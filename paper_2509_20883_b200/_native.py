@@ -74,8 +74,11 @@ _SIGS = {
     "skb_grad_fold": ([_p, _i64, _i64, _p, _i64, _p, _p], ctypes.c_int),
     "skb_fused_forward": ([_p, _p, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_u64), _i32, _i32, _p, _i64,
                            ctypes.POINTER(_i64), ctypes.POINTER(_i32), _i32, _i64, _p, _p], ctypes.c_int),
+    "skb_fused_prepare": ([_p, _p, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_u64), _i32, _i32, _p, _i64,
+                           ctypes.POINTER(_i64), ctypes.POINTER(_i32), _i32, _i64, _p], ctypes.c_int),
     "skb_fused_backward": ([_p, _p, ctypes.POINTER(AdamScalars), _p], ctypes.c_int),
     "skb_fused_last_unique": ([_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p], ctypes.c_int),
+    "skb_fused_stats_async": ([_p, _p, _p], ctypes.c_int),
     "skb_fused_profile": ([_p, _i64, _p], ctypes.c_int),
     "skb_fused_profile_read": ([_p, _i32, ctypes.POINTER(ctypes.c_float), _i64, ctypes.POINTER(_i64)], ctypes.c_int),
     "skb_bucketize_multi": ([_p, _p, _i64, _p, _p, _p, _i64, _p], ctypes.c_int),

@@ -49,35 +49,42 @@ constexpr int kTileU = 256;
 constexpr int kTileJ = 1024;
 constexpr int kRankTile = 4096;    // positions per tile of the miss-rank scan
 
-struct FusedCtx {
-  int64_t cap_n = 0;         // capacity in positions
-  uint32_t* slot = nullptr;  // [N] slot of position
-  uint32_t* bag = nullptr;   // [N] bag of position
-  uint32_t* skey = nullptr;  // [N] sorted slots
-  uint32_t* sval = nullptr;  // [N] bags in sorted order
-  uint32_t* heads = nullptr; // [N] run heads
-  uint8_t* miss = nullptr;   // [N]
-  uint8_t* fresh = nullptr;  // [N] first occurrence of an unknown key
-  int64_t* rank = nullptr;   // [N]
-  int32_t* hslot = nullptr;  // [N] scratch-table index of a miss
-  int64_t* tile_cnt = nullptr;  // [N / kRankTile + 1]
-  HEntry* scratch = nullptr; // [2*cap_n pow2 + 1]
+// One batch in flight through the pipeline: index results of its prepare
+// (slots, sort) and its metadata; two of these are double-buffered so the
+// index work of step k+1 overlaps the pool / fold+Adam of step k.
+struct BatchCtx {
+  int64_t cap_n = 0;          // capacity in positions
+  uint32_t* slot = nullptr;   // [N] slot of position
+  uint32_t* bag = nullptr;    // [N] bag of position
+  uint32_t* skey = nullptr;   // [N] sorted slots
+  uint32_t* sval = nullptr;   // [N] bags in sorted order
+  uint8_t* miss = nullptr;    // [N]
+  uint8_t* fresh = nullptr;   // [N] first occurrence of an unknown key
+  int64_t* rank = nullptr;    // [N]
+  int32_t* hslot = nullptr;   // [N] scratch-table index of a miss
+  int64_t* tile_cnt = nullptr;  // [N / kRankTile + 2]
+  HEntry* scratch = nullptr;  // [2*cap_n pow2 + 1]
   int64_t scratch_cap = 0;
-  int64_t* dev = nullptr;    // [0] misses M, [1] new K, [2] unique U
+  int64_t* dev = nullptr;     // [0] misses M, [1] new K, [2] unique U
   MemberDev* members = nullptr;
   int64_t members_cap = 0;
   std::vector<MemberDev> members_host;
-  // last forward
-  int64_t n = 0, G = 0, F = 0;
-  int mode = 0;
+  // identity + metadata of the prepared batch
+  const int64_t* ids = nullptr;
   const int64_t* bag_offs = nullptr;
-  bool have_fwd = false;
-  int64_t pending_last_step = -1;  // forward's step, written by backward / flush
-  // backward preparation (bag-of-position + stable sort) overlaps the pool
-  // kernel on a side stream
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  bool join_pending = false;
+  int64_t n = 0, G = 0, step = -1;
+  int F = 0, mode = 0;
+  bool any_seq = false;
+  bool last_written = false;  // deferred last_step already flushed
+  cudaEvent_t ev_ready = nullptr, ev_free = nullptr;
+  bool ever_used = false;
+};
+
+struct FusedCtx {
+  cudaStream_t side = nullptr;  // index stream: probe, admission, bag-of, sort
+  cudaEvent_t ev_in = nullptr, ev_side_last = nullptr;
+  BatchCtx b[2];
+  int64_t prep_count = 0, pool_count = 0, bwd_count = 0;
   // optional per-kernel CUDA-event profiling: kProf phases x (begin, end) x cap steps
   int64_t prof_cap = 0;
   int64_t prof_n[5] = {0, 0, 0, 0, 0};
@@ -92,26 +99,32 @@ static void prof_mark(FusedCtx* c, int phase, int edge, cudaStream_t s) {
   if (edge == 1) c->prof_n[phase]++;
 }
 
+static void batch_free(BatchCtx& B) {
+  cudaFree(B.slot);
+  cudaFree(B.bag);
+  cudaFree(B.skey);
+  cudaFree(B.sval);
+  cudaFree(B.miss);
+  cudaFree(B.fresh);
+  cudaFree(B.rank);
+  cudaFree(B.hslot);
+  cudaFree(B.tile_cnt);
+  cudaFree(B.scratch);
+  cudaFree(B.dev);
+  cudaFree(B.members);
+  if (B.ev_ready) cudaEventDestroy(B.ev_ready);
+  if (B.ev_free) cudaEventDestroy(B.ev_free);
+}
+
 void fused_ctx_destroy(FusedCtx* c) {
   if (!c) return;
-  if (c->side) cudaStreamDestroy(c->side);
-  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
-  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->side) cudaStreamSynchronize(c->side);
   for (auto& v : c->prof_ev)
     for (auto e : v) cudaEventDestroy(e);
-  cudaFree(c->slot);
-  cudaFree(c->bag);
-  cudaFree(c->skey);
-  cudaFree(c->sval);
-  cudaFree(c->heads);
-  cudaFree(c->miss);
-  cudaFree(c->fresh);
-  cudaFree(c->rank);
-  cudaFree(c->hslot);
-  cudaFree(c->tile_cnt);
-  cudaFree(c->scratch);
-  cudaFree(c->dev);
-  cudaFree(c->members);
+  for (auto& B : c->b) batch_free(B);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_in) cudaEventDestroy(c->ev_in);
+  if (c->ev_side_last) cudaEventDestroy(c->ev_side_last);
   delete c;
 }
 
@@ -121,37 +134,48 @@ static void realloc_dev(T*& p, int64_t count, cudaStream_t s) {
   SKB_CUDA(cudaMallocAsync(&p, sizeof(T) * (count > 0 ? count : 1), s));
 }
 
-static FusedCtx* ctx_for(Table* t, int64_t n, int64_t F, cudaStream_t s) {
+static FusedCtx* ctx_get(Table* t) {
   if (!t->fused) {
-    t->fused = new FusedCtx();
-    SKB_CUDA(cudaMalloc(&t->fused->dev, sizeof(int64_t) * 4));
-    SKB_CUDA(cudaStreamCreateWithFlags(&t->fused->side, cudaStreamNonBlocking));
-    SKB_CUDA(cudaEventCreateWithFlags(&t->fused->ev_fork, cudaEventDisableTiming));
-    SKB_CUDA(cudaEventCreateWithFlags(&t->fused->ev_join, cudaEventDisableTiming));
+    FusedCtx* c = new FusedCtx();
+    // highest priority: index blocks take SM slots as soon as fold+Adam
+    // blocks retire, so the prefetched index phase overlaps the optimizer
+    int lo = 0, hi = 0;
+    SKB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    SKB_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
+    SKB_CUDA(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+    SKB_CUDA(cudaEventCreateWithFlags(&c->ev_side_last, cudaEventDisableTiming));
+    for (auto& B : c->b) {
+      SKB_CUDA(cudaMalloc(&B.dev, sizeof(int64_t) * 4));
+      SKB_CUDA(cudaMemset(B.dev, 0, sizeof(int64_t) * 4));
+      SKB_CUDA(cudaEventCreateWithFlags(&B.ev_ready, cudaEventDisableTiming));
+      SKB_CUDA(cudaEventCreateWithFlags(&B.ev_free, cudaEventDisableTiming));
+    }
+    t->fused = c;
   }
-  FusedCtx* c = t->fused;
-  if (n > c->cap_n) {
+  return t->fused;
+}
+
+static void batch_reserve(BatchCtx& B, int64_t n, int64_t F, cudaStream_t s) {
+  if (n > B.cap_n) {
     int64_t cap = n + n / 4;
-    realloc_dev(c->slot, cap, s);
-    realloc_dev(c->bag, cap, s);
-    realloc_dev(c->skey, cap, s);
-    realloc_dev(c->sval, cap, s);
-    realloc_dev(c->heads, cap, s);
-    realloc_dev(c->miss, cap, s);
-    realloc_dev(c->fresh, cap, s);
-    realloc_dev(c->rank, cap, s);
-    realloc_dev(c->hslot, cap, s);
-    realloc_dev(c->tile_cnt, cap / kRankTile + 2, s);
-    c->scratch_cap = next_pow2(2 * cap > 64 ? 2 * cap : 64);
-    realloc_dev(c->scratch, c->scratch_cap + 1, s);
-    c->cap_n = cap;
+    realloc_dev(B.slot, cap, s);
+    realloc_dev(B.bag, cap, s);
+    realloc_dev(B.skey, cap, s);
+    realloc_dev(B.sval, cap, s);
+    realloc_dev(B.miss, cap, s);
+    realloc_dev(B.fresh, cap, s);
+    realloc_dev(B.rank, cap, s);
+    realloc_dev(B.hslot, cap, s);
+    realloc_dev(B.tile_cnt, cap / kRankTile + 2, s);
+    B.scratch_cap = next_pow2(2 * cap > 64 ? 2 * cap : 64);
+    realloc_dev(B.scratch, B.scratch_cap + 1, s);
+    B.cap_n = cap;
   }
-  if (F + 1 > c->members_cap) {
-    realloc_dev(c->members, F + 1, s);
-    c->members_cap = F + 1;
-    c->members_host.clear();
+  if (F + 1 > B.members_cap) {
+    realloc_dev(B.members, F + 1, s);
+    B.members_cap = F + 1;
+    B.members_host.clear();
   }
-  return c;
 }
 
 // member lookup over a (shared or global) member table
@@ -943,14 +967,20 @@ static int coop_grid(size_t smem) {
   return blocks_per_sm * sm_count();
 }
 
+// Pending-work barrier for every non-fused table op on stream s: index work
+// must be complete, and pooled batches still awaiting their backward get
+// their deferred last_step written (forward semantics of lookup_or_insert).
 void fused_flush_pending(Table* t, cudaStream_t s) {
   FusedCtx* c = t->fused;
-  if (!c || c->pending_last_step < 0) return;
-  if (c->n > 0) {
-    k_flush_last<<<grid_for(c->n, 256), 256, 0, s>>>(c->slot, c->n, c->pending_last_step, t->last_step);
+  if (!c) return;
+  if (c->prep_count > 0) SKB_CUDA(cudaStreamWaitEvent(s, c->ev_side_last, 0));
+  for (int64_t k = c->bwd_count; k < c->pool_count; ++k) {
+    BatchCtx& B = c->b[k % 2];
+    if (B.last_written || B.n == 0) continue;
+    k_flush_last<<<grid_for(B.n, 256), 256, 0, s>>>(B.slot, B.n, B.step, t->last_step);
     SKB_LAUNCH_CHECK();
+    B.last_written = true;
   }
-  c->pending_last_step = -1;
 }
 
 // kernel variant knobs for tuning sweeps (SKB_ADAM_VARIANT / SKB_POOL_VARIANT)
@@ -969,126 +999,171 @@ static int pool_variant() {
 
 static size_t member_smem(int F) { return F <= kSmemMembers ? sizeof(MemberSmem) : 0; }
 
-static void fused_forward(Table* t, const int64_t* ids, int64_t n, const int64_t* member_pos, const uint64_t* salts,
-                          int F, int namespaced, const int64_t* bag_offs, int64_t G, const int64_t* member_bag,
-                          const int32_t* strategy, int mode, int64_t step, float* pooled, cudaStream_t s) {
-  if (F < 1) raise(SKB_E_ARG, F, "need at least one member");
-  if (member_pos[0] != 0 || member_pos[F] != n || member_bag[0] != 0 || member_bag[F] != G)
+struct BatchArgs {
+  const int64_t* ids;
+  int64_t n;
+  const int64_t* member_pos;
+  const uint64_t* salts;
+  int F;
+  int namespaced;
+  const int64_t* bag_offs;
+  int64_t G;
+  const int64_t* member_bag;
+  const int32_t* strategy;
+  int mode;
+  int64_t step;
+};
+
+// Index phase of one batch on the table's index stream: probe, admission,
+// bag-of-position, stable sort.  Inputs are ordered after the caller's
+// stream `s`; the batch buffer is reused only after its previous backward.
+static void fused_prepare(Table* t, const BatchArgs& a, cudaStream_t s) {
+  if (a.F < 1) raise(SKB_E_ARG, a.F, "need at least one member");
+  if (a.member_pos[0] != 0 || a.member_pos[a.F] != a.n || a.member_bag[0] != 0 || a.member_bag[a.F] != a.G)
     raise(SKB_E_ARG, 0, "member ranges must cover [0, n) positions and [0, G) bags");
-  if (n >= (1ll << 32) - 1 || G >= (1ll << 32) - 1) raise(SKB_E_UNSUPPORTED, n, "fused step: > 2^32 positions");
-  fused_flush_pending(t, s);
-  table_reserve(t, n, s);
+  if (a.n >= (1ll << 32) - 1 || a.G >= (1ll << 32) - 1) raise(SKB_E_UNSUPPORTED, a.n, "fused step: > 2^32 positions");
+  FusedCtx* c = ctx_get(t);
+  if (c->prep_count - c->bwd_count >= 2)
+    raise(SKB_E_VALUE, 0, "fused pipeline full: two batches already in flight (run a backward first)");
+  cudaStream_t x = c->side;
+  BatchCtx& B = c->b[c->prep_count % 2];
+  SKB_CUDA(cudaEventRecord(c->ev_in, s));
+  SKB_CUDA(cudaStreamWaitEvent(x, c->ev_in, 0));
+  if (B.ever_used) SKB_CUDA(cudaStreamWaitEvent(x, B.ev_free, 0));
+  // growth moves the arena: quiesce the caller's stream first (rare)
+  if (table_needs_growth(t, a.n)) {
+    SKB_CUDA(cudaStreamSynchronize(s));
+    SKB_CUDA(cudaStreamSynchronize(x));
+  }
+  table_reserve(t, a.n, x);
   if (t->arena_rows >= (1ll << 32) - 1) raise(SKB_E_UNSUPPORTED, t->arena_rows, "fused step: > 2^32 rows");
-  FusedCtx* c = ctx_for(t, n, F, s);
-  std::vector<MemberDev> mh(F + 1);
-  for (int f = 0; f <= F; ++f) {
-    mh[f].pos = member_pos[f];
-    mh[f].bag = member_bag[f];
-    mh[f].salt = f < F ? salts[f] : 0;
-    mh[f].strategy = f < F ? strategy[f] : 0;
+  batch_reserve(B, a.n, a.F, x);
+  std::vector<MemberDev> mh(a.F + 1);
+  bool any_seq = false;
+  for (int f = 0; f <= a.F; ++f) {
+    mh[f].pos = a.member_pos[f];
+    mh[f].bag = a.member_bag[f];
+    mh[f].salt = f < a.F ? a.salts[f] : 0;
+    mh[f].strategy = f < a.F ? a.strategy[f] : 0;
+    if (f < a.F) any_seq |= a.strategy[f] == 0;
   }
-  if (c->members_host.size() != mh.size() || memcmp(c->members_host.data(), mh.data(), sizeof(MemberDev) * mh.size())) {
-    SKB_CUDA(cudaMemcpyAsync(c->members, mh.data(), sizeof(MemberDev) * mh.size(), cudaMemcpyHostToDevice, s));
-    SKB_CUDA(cudaStreamSynchronize(s));  // pageable source; rare (layout change)
-    c->members_host = mh;
+  if (B.members_host.size() != mh.size() || memcmp(B.members_host.data(), mh.data(), sizeof(MemberDev) * mh.size())) {
+    SKB_CUDA(cudaMemcpyAsync(B.members, mh.data(), sizeof(MemberDev) * mh.size(), cudaMemcpyHostToDevice, x));
+    SKB_CUDA(cudaStreamSynchronize(x));  // pageable source; rare (layout change)
+    B.members_host = mh;
   }
-  const MemberDev* mt = c->members;
+  const MemberDev* mt = B.members;
   const uint64_t mask = (uint64_t)(t->idmap_cap - 1);
   const int D = (int)t->dim;
-  const size_t msm = member_smem(F);
-  if (c->join_pending) {  // a previous forward's side work must finish first
-    SKB_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
-    c->join_pending = false;
-  }
-  SKB_CUDA(cudaMemsetAsync(c->dev, 0, sizeof(int64_t) * 4, s));
+  const int64_t n = a.n, G = a.G;
+  SKB_CUDA(cudaMemsetAsync(B.dev, 0, sizeof(int64_t) * 4, x));
   if (n > 0) {
-    prof_mark(c, P_PROBE, 0, s);
-    k_fused_probe<<<grid_for(n, 256), 256, msm, s>>>(ids, n, mt, F, namespaced, t->idmap, mask, t->idmap_cap, c->slot,
-                                                    c->miss, c->dev);
+    prof_mark(c, P_PROBE, 0, x);
+    k_fused_probe<<<grid_for(n, 256), 256, member_smem(a.F), x>>>(a.ids, n, mt, a.F, a.namespaced, t->idmap, mask,
+                                                                  t->idmap_cap, B.slot, B.miss, B.dev);
     SKB_LAUNCH_CHECK();
-    prof_mark(c, P_PROBE, 1, s);
-    prof_mark(c, P_MISS, 0, s);
-    AdmitArgs A{ids, n, mt, F, namespaced, c->miss, c->scratch, c->hslot, c->fresh, c->tile_cnt, c->rank, c->dev,
-                t->counters, t->free_list, t->idmap, mask, t->idmap_cap, step, D, t->seed_mix, t->init_scale,
-                t->arena, t->last_step, t->live, t->slot_key, t->ins_seq, c->slot};
+    prof_mark(c, P_PROBE, 1, x);
+    prof_mark(c, P_MISS, 0, x);
+    AdmitArgs A{a.ids, n, mt, a.F, a.namespaced, B.miss, B.scratch, B.hslot, B.fresh, B.tile_cnt, B.rank, B.dev,
+                t->counters, t->free_list, t->idmap, mask, t->idmap_cap, a.step, D, t->seed_mix, t->init_scale,
+                t->arena, t->last_step, t->live, t->slot_key, t->ins_seq, B.slot};
     const size_t csm = sizeof(MemberSmem);
     int cg_blocks = coop_grid(csm);
     const int64_t want = (n + 255) / 256;
     if (want < cg_blocks) cg_blocks = (int)(want > 0 ? want : 1);
     void* kargs[] = {&A};
-    SKB_CUDA(cudaLaunchCooperativeKernel((const void*)k_admission, dim3(cg_blocks), dim3(256), kargs, csm, s));
+    SKB_CUDA(cudaLaunchCooperativeKernel((const void*)k_admission, dim3(cg_blocks), dim3(256), kargs, csm, x));
     SKB_LAUNCH_CHECK();
-    prof_mark(c, P_MISS, 1, s);
-    // backward preparation on the side stream, overlapping the pool kernel
-    SKB_CUDA(cudaEventRecord(c->ev_fork, s));
-    SKB_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-    prof_mark(c, P_SORT, 0, c->side);
-    k_bag_of<<<grid_for(G > 0 ? G : 1, 256), 256, 0, c->side>>>(bag_offs, G, c->bag);
+    prof_mark(c, P_MISS, 1, x);
+    prof_mark(c, P_SORT, 0, x);
+    k_bag_of<<<grid_for(G > 0 ? G : 1, 256), 256, 0, x>>>(a.bag_offs, G, B.bag);
     SKB_LAUNCH_CHECK();
-    sort_pairs_u32(c->slot, c->skey, c->bag, c->sval, n, bits_for((uint64_t)(t->arena_rows - 1)), c->side);
-    prof_mark(c, P_SORT, 1, c->side);
-    SKB_CUDA(cudaEventRecord(c->ev_join, c->side));
-    c->join_pending = true;
+    sort_pairs_u32(B.slot, B.skey, B.bag, B.sval, n, bits_for((uint64_t)(t->arena_rows - 1)), x);
+    prof_mark(c, P_SORT, 1, x);
   }
+  table_note_inserts(t, n, x);
+  SKB_CUDA(cudaEventRecord(B.ev_ready, x));
+  SKB_CUDA(cudaEventRecord(c->ev_side_last, x));
+  B.ids = a.ids;
+  B.bag_offs = a.bag_offs;
+  B.n = n;
+  B.G = G;
+  B.F = a.F;
+  B.mode = a.mode;
+  B.step = a.step;
+  B.any_seq = any_seq;
+  B.last_written = false;
+  B.ever_used = true;
+  c->prep_count++;
+}
+
+// Pool phase on the caller's stream (uses the oldest prepared batch; prepares
+// it here when the caller did not prefetch).
+static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStream_t s) {
+  FusedCtx* c = ctx_get(t);
+  if (c->prep_count > c->pool_count) {
+    BatchCtx& H = c->b[c->pool_count % 2];
+    if (H.ids != a.ids || H.n != a.n || H.G != a.G || H.bag_offs != a.bag_offs || H.step != a.step ||
+        H.mode != a.mode)
+      raise(SKB_E_VALUE, 0, "fused forward does not match the prepared (prefetched) batch");
+  } else {
+    fused_prepare(t, a, s);
+  }
+  BatchCtx& B = c->b[c->pool_count % 2];
+  SKB_CUDA(cudaStreamWaitEvent(s, B.ev_ready, 0));
+  const int D = (int)t->dim;
+  const int64_t G = B.G;
   if (G > 0) {
     prof_mark(c, P_POOL, 0, s);
     const size_t psm = sizeof(PoolSmem);
     const int64_t ntiles = (G + kTileBags - 1) / kTileBags;
-    bool v4 = D % 4 == 0 && (uintptr_t)pooled % 16 == 0;
-    bool any_seq = false;
-    for (int f = 0; f < F; ++f) any_seq |= strategy[f] == 0;
-    if (!any_seq) {
+    const bool v4 = D % 4 == 0 && (uintptr_t)pooled % 16 == 0;
+    if (!B.any_seq) {
       const unsigned grid = grid_for(((G + 31) / 32) * 32, 256, 8);
+#define SKB_POOL_ARGS t->arena, B.slot, B.bag_offs, G, B.mode, D, pooled
       if (!v4)
-        k_fused_pool_scatter<1, 1, 4><<<grid, 256, 0, s>>>(t->arena, c->slot, bag_offs, G, mode, D, pooled);
+        k_fused_pool_scatter<1, 1, 4><<<grid, 256, 0, s>>>(SKB_POOL_ARGS);
       else
+        // measured on B200 (C2, D=64): R=2 at 4 blocks/SM 0.162 ms; R=2/1 0.204;
+        // R=1/4 0.236; R=4/2 0.235
         switch (pool_variant()) {
-          case 1: k_fused_pool_scatter<4, 1, 4><<<grid, 256, 0, s>>>(t->arena, c->slot, bag_offs, G, mode, D, pooled);
-            break;
-          case 2: k_fused_pool_scatter<4, 2, 1><<<grid, 256, 0, s>>>(t->arena, c->slot, bag_offs, G, mode, D, pooled);
-            break;
-          case 3: k_fused_pool_scatter<4, 4, 2><<<grid, 256, 0, s>>>(t->arena, c->slot, bag_offs, G, mode, D, pooled);
-            break;
-          default: k_fused_pool_scatter<4, 2, 4><<<grid, 256, 0, s>>>(t->arena, c->slot, bag_offs, G, mode, D, pooled);
-            break;
+          case 1: k_fused_pool_scatter<4, 1, 4><<<grid, 256, 0, s>>>(SKB_POOL_ARGS); break;
+          case 2: k_fused_pool_scatter<4, 2, 1><<<grid, 256, 0, s>>>(SKB_POOL_ARGS); break;
+          case 3: k_fused_pool_scatter<4, 4, 2><<<grid, 256, 0, s>>>(SKB_POOL_ARGS); break;
+          default: k_fused_pool_scatter<4, 2, 4><<<grid, 256, 0, s>>>(SKB_POOL_ARGS); break;
         }
+#undef SKB_POOL_ARGS
     } else if (v4) {
-      k_fused_pool_general<4><<<grid_for(ntiles * 256, 256, 6), 256, psm, s>>>(t->arena, c->slot, bag_offs, G, mt, F,
-                                                                              mode, D, pooled, c->bag);
+      k_fused_pool_general<4><<<grid_for(ntiles * 256, 256, 6), 256, psm, s>>>(t->arena, B.slot, B.bag_offs, G,
+                                                                              B.members, B.F, B.mode, D, pooled,
+                                                                              B.bag);
     } else {
-      k_fused_pool_general<1><<<grid_for(ntiles * 256, 256, 6), 256, psm, s>>>(t->arena, c->slot, bag_offs, G, mt, F,
-                                                                              mode, D, pooled, c->bag);
+      k_fused_pool_general<1><<<grid_for(ntiles * 256, 256, 6), 256, psm, s>>>(t->arena, B.slot, B.bag_offs, G,
+                                                                              B.members, B.F, B.mode, D, pooled,
+                                                                              B.bag);
     }
     SKB_LAUNCH_CHECK();
     prof_mark(c, P_POOL, 1, s);
   }
-  table_note_inserts(t, n, s);
-  c->n = n;
-  c->G = G;
-  c->F = F;
-  c->mode = mode;
-  c->bag_offs = bag_offs;
-  c->have_fwd = true;
-  c->pending_last_step = step;
+  c->pool_count++;
 }
 
 static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc, cudaStream_t s) {
   FusedCtx* c = t->fused;
-  if (!c || !c->have_fwd) raise(SKB_E_VALUE, 0, "fused backward without a preceding fused forward");
-  const int64_t n = c->n;
+  if (!c || c->bwd_count >= c->pool_count) raise(SKB_E_VALUE, 0, "fused backward without a preceding fused forward");
+  BatchCtx& B = c->b[c->bwd_count % 2];
+  const int64_t n = B.n;
   const int D = (int)t->dim;
   if (n > 0) {
-    if (c->join_pending) {
-      SKB_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
-      c->join_pending = false;
-    }
     prof_mark(c, P_ADAM, 0, s);
     AdamDev a = to_dev(sc);
-    const int64_t step = c->pending_last_step;
     const int64_t chunks = (n + 31) / 32;
-    bool v4 = D % 4 == 0 && (uintptr_t)dpooled % 16 == 0;
-    const unsigned grid = grid_for(chunks * 32, 256, 8);
-#define SKB_ADAM_ARGS n, c->skey, c->sval, c->bag_offs, dpooled, c->mode, D, a, t->arena, t->last_step, step, c->dev + 2
+    const bool v4 = D % 4 == 0 && (uintptr_t)dpooled % 16 == 0;
+    // non-persistent grid (one chunk per warp): retiring blocks free SM slots
+    // for the prefetched index phase of the next step
+    const unsigned grid = env_int("SKB_ADAM_PERSIST", 0) ? grid_for(chunks * 32, 256, 8)
+                                                         : (unsigned)((chunks + 7) / 8);
+#define SKB_ADAM_ARGS n, B.skey, B.sval, B.bag_offs, dpooled, B.mode, D, a, t->arena, t->last_step, B.step, B.dev + 2
     if (!v4) {
       k_fused_adam<1, 1, 4><<<grid, 256, 0, s>>>(SKB_ADAM_ARGS);
     } else {
@@ -1104,8 +1179,9 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     SKB_LAUNCH_CHECK();
     prof_mark(c, P_ADAM, 1, s);
   }
-  c->pending_last_step = -1;
-  c->have_fwd = false;
+  B.last_written = true;
+  SKB_CUDA(cudaEventRecord(B.ev_free, s));
+  c->bwd_count++;
 }
 
 }  // namespace skb
@@ -1114,13 +1190,25 @@ using namespace skb;
 
 extern "C" {
 
+int skb_fused_prepare(skb_table_t h, const int64_t* ids, int64_t n, const int64_t* member_pos_host,
+                      const uint64_t* salts_host, int32_t num_members, int32_t namespaced, const int64_t* bag_offs,
+                      int64_t num_bags, const int64_t* member_bag_host, const int32_t* strategy_host, int32_t mode,
+                      int64_t step, void* stream) {
+  SKB_API_BEGIN
+  BatchArgs a{ids, n, member_pos_host, salts_host, num_members, namespaced, bag_offs, num_bags, member_bag_host,
+              strategy_host, mode, step};
+  fused_prepare(table_from(h), a, as_stream(stream));
+  SKB_API_END
+}
+
 int skb_fused_forward(skb_table_t h, const int64_t* ids, int64_t n, const int64_t* member_pos_host,
                       const uint64_t* salts_host, int32_t num_members, int32_t namespaced, const int64_t* bag_offs,
                       int64_t num_bags, const int64_t* member_bag_host, const int32_t* strategy_host, int32_t mode,
                       int64_t step, float* pooled_out, void* stream) {
   SKB_API_BEGIN
-  fused_forward(table_from(h), ids, n, member_pos_host, salts_host, num_members, namespaced, bag_offs, num_bags,
-                member_bag_host, strategy_host, mode, step, pooled_out, as_stream(stream));
+  BatchArgs a{ids, n, member_pos_host, salts_host, num_members, namespaced, bag_offs, num_bags, member_bag_host,
+              strategy_host, mode, step};
+  fused_forward(table_from(h), a, pooled_out, as_stream(stream));
   SKB_API_END
 }
 
@@ -1133,8 +1221,9 @@ int skb_fused_backward(skb_table_t h, const float* dpooled, const skb_adam_t* sc
 int skb_fused_profile(skb_table_t h, int64_t max_steps, void* stream) {
   SKB_API_BEGIN
   Table* t = table_from(h);
-  FusedCtx* c = ctx_for(t, 0, 0, as_stream(stream));
+  FusedCtx* c = ctx_get(t);
   SKB_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  SKB_CUDA(cudaStreamSynchronize(c->side));
   for (auto& v : c->prof_ev) {
     for (auto e : v) cudaEventDestroy(e);
     v.clear();
@@ -1163,13 +1252,25 @@ int skb_fused_profile_read(skb_table_t h, int32_t phase, float* ms_host, int64_t
   SKB_API_END
 }
 
+int skb_fused_stats_async(skb_table_t h, int64_t* dst_pinned_host, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  FusedCtx* c = t->fused;
+  if (!c || c->bwd_count == 0) raise(SKB_E_VALUE, 0, "no fused step has completed on this table");
+  BatchCtx& B = c->b[(c->bwd_count - 1) % 2];
+  SKB_CUDA(cudaMemcpyAsync(dst_pinned_host, B.dev, sizeof(int64_t) * 4, cudaMemcpyDeviceToHost, as_stream(stream)));
+  SKB_API_END
+}
+
 int skb_fused_last_unique(skb_table_t h, int64_t* n_unique_host, int64_t* n_new_host, void* stream) {
   SKB_API_BEGIN
   Table* t = table_from(h);
-  if (!t->fused) raise(SKB_E_VALUE, 0, "no fused step has run on this table");
+  FusedCtx* c = t->fused;
+  if (!c || c->bwd_count == 0) raise(SKB_E_VALUE, 0, "no fused step has completed on this table");
+  BatchCtx& B = c->b[(c->bwd_count - 1) % 2];
   int64_t v[4];
   cudaStream_t s = as_stream(stream);
-  SKB_CUDA(cudaMemcpyAsync(v, t->fused->dev, sizeof(v), cudaMemcpyDeviceToHost, s));
+  SKB_CUDA(cudaMemcpyAsync(v, B.dev, sizeof(v), cudaMemcpyDeviceToHost, s));
   SKB_CUDA(cudaStreamSynchronize(s));
   *n_unique_host = v[2];
   *n_new_host = v[1];

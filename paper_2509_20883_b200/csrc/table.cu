@@ -90,6 +90,13 @@ static void harvest_snapshot(Table* t) {
   // pending_adds already excludes ops enqueued before the snapshot
 }
 
+bool table_needs_growth(Table* t, int64_t n) {
+  harvest_snapshot(t);
+  int64_t ub_alloc = t->known[C_ALLOC] + t->pending_adds + n;
+  int64_t ub_rows = t->known[C_ROWS] + t->pending_adds + n;
+  return !(ub_alloc <= t->arena_rows && ub_rows * 10 < t->idmap_cap * 9);
+}
+
 void table_reserve(Table* t, int64_t n, cudaStream_t s) {
   harvest_snapshot(t);
   int64_t ub_alloc = t->known[C_ALLOC] + t->pending_adds + n;

@@ -60,6 +60,8 @@ Table* table_from(skb_table_t h);
 
 // Ensure room for n more insertions (arena + idmap), growing stream-ordered.
 void table_reserve(Table* t, int64_t n, cudaStream_t s);
+// Whether table_reserve(n) might have to grow (host bound check, no sync).
+bool table_needs_growth(Table* t, int64_t n);
 // After enqueueing an op that may insert up to n rows: update bounds, snapshot.
 void table_note_inserts(Table* t, int64_t n, cudaStream_t s);
 // Exact counters (synchronizes).

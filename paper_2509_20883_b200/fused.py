@@ -53,6 +53,7 @@ class PackedBatch:
                                    int(self.member_bag[f + 1] - self.member_bag[f])) == "sequential" else 1
              for f in range(F)], np.int32)
         self.namespaced = lt.namespaced
+        self._c_args = None
 
     @property
     def num_ids(self) -> int:
@@ -63,24 +64,41 @@ class PackedBatch:
         return int(self.member_bag[-1])
 
 
-def lookup_pool(lt: LogicalTable, batch: PackedBatch, step: int, mode: str = "mean", out=None):
-    """Pooled embeddings [G, D] of every bag of the batch (single shard)."""
-    telemetry.bump("fused.lookup_pool")
+def _batch_args(lt: LogicalTable, batch: PackedBatch, step: int, mode: str):
     if mode not in _MODES:
         raise ValueError(f"unknown mode {mode!r}")
     if lt.num_shards != 1 or lt.dist:
-        raise NotImplementedError("fused lookup_pool runs on one shard; use distributed.DistSparseStep for S > 1")
-    G = batch.num_bags
-    if out is None:
-        out = N.empty((G, lt.dim), "float32")
+        raise NotImplementedError("the fused step runs on one shard; use all_to_all_lookup for S > 1")
     F = len(batch.members)
-    mp = (ctypes.c_int64 * (F + 1))(*batch.member_pos.tolist())
-    mb = (ctypes.c_int64 * (F + 1))(*batch.member_bag.tolist())
-    sl = (ctypes.c_uint64 * max(F, 1))(*[int(s) for s in batch.salts])
-    st = (ctypes.c_int32 * max(F, 1))(*batch.strategy.tolist())
-    N.call("skb_fused_forward", lt.local_table.handle, N.ptr(batch.ids), batch.num_ids, mp, sl, F,
-           1 if batch.namespaced else 0, N.ptr(batch.bag_offs), G, mb, st, _MODES[mode], int(step), N.ptr(out),
-           N.stream_ptr())
+    if batch._c_args is None:
+        batch._c_args = ((ctypes.c_int64 * (F + 1))(*batch.member_pos.tolist()),
+                         (ctypes.c_uint64 * max(F, 1))(*[int(s) for s in batch.salts]),
+                         (ctypes.c_int64 * (F + 1))(*batch.member_bag.tolist()),
+                         (ctypes.c_int32 * max(F, 1))(*batch.strategy.tolist()))
+    mp, sl, mb, st = batch._c_args
+    return (lt.local_table.handle, N.ptr(batch.ids), batch.num_ids, mp, sl, F, 1 if batch.namespaced else 0,
+            N.ptr(batch.bag_offs), batch.num_bags, mb, st, _MODES[mode], int(step))
+
+
+def prefetch(lt: LogicalTable, batch: PackedBatch, step: int, mode: str = "mean") -> None:
+    """Enqueue the index phase (probe, admission, sort) of a future step.
+
+    Issue it after `lookup_pool` of step k and before `pool_grad_adam` of
+    step k: the index work of step k+1 then runs on the table's index stream
+    underneath the fold+Adam of step k.  Admission happens at prefetch time,
+    so do not prefetch across an eviction / restore boundary.
+    """
+    telemetry.bump("fused.prefetch")
+    N.call("skb_fused_prepare", *_batch_args(lt, batch, step, mode), N.stream_ptr())
+
+
+def lookup_pool(lt: LogicalTable, batch: PackedBatch, step: int, mode: str = "mean", out=None):
+    """Pooled embeddings [G, D] of every bag of the batch (single shard)."""
+    telemetry.bump("fused.lookup_pool")
+    args = _batch_args(lt, batch, step, mode)
+    if out is None:
+        out = N.empty((batch.num_bags, lt.dim), "float32")
+    N.call("skb_fused_forward", *args, N.ptr(out), N.stream_ptr())
     return out
 
 

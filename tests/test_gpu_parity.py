@@ -390,3 +390,39 @@ def test_fused_with_eviction(skb):
 def test_fused_generic_dim(skb):
     specs = [("a", 64, lambda r, B: r.integers(0, 5, B))]
     _fused_vs_oracle(skb, 3, specs, steps=3, mode="mean", seed=2)
+
+
+def test_fused_pipelined_prefetch(skb):
+    """Prefetching step k+1's index phase under step k's fold+Adam gives the
+    same table state and pooled rows as the unpipelined oracle pipeline."""
+    import torch
+    rng = np.random.default_rng(21)
+    D, members, B, steps = 8, ["a", "b"], 96, 6
+    lt = skb.LogicalTable("dim8", D, 1, seed=2, members=members, namespaced=True)
+    olt = O.OracleLogical("dim8", D, 1, seed=2, members=members, namespaced=True)
+    cfg = skb.AdamConfig(lr=1e-2, weight_decay=0.01, variant="adamw")
+    batches, raw = [], []
+    for k in range(steps):
+        ids = [rng.integers(0, 300 + 100 * k, B * 2) for _ in members]  # new ids keep arriving
+        offs = [np.arange(0, 2 * B + 1, 2, dtype=np.int64) for _ in members]
+        batches.append(skb.PackedBatch(lt, members, ids, offs))
+        raw.append((ids, offs, rng.standard_normal((2 * B, D)).astype(np.float32)))
+    skb.prefetch(lt, batches[0], 1, "mean")
+    pooled_all = []
+    for k in range(steps):
+        pooled_all.append(skb.lookup_pool(lt, batches[k], k + 1, "mean").clone())
+        if k + 1 < steps:
+            skb.prefetch(lt, batches[k + 1], k + 2, "mean")
+        skb.pool_grad_adam(lt, torch.from_numpy(raw[k][2]).cuda(), cfg, k + 1)
+    with pytest.raises(ValueError):
+        skb.pool_grad_adam(lt, torch.from_numpy(raw[0][2]).cuda(), cfg, 9)
+    for k in range(steps):
+        ids, offs, dp = raw[k]
+        keys = np.concatenate([olt.keys_for(m, x) for m, x in zip(members, ids)])
+        rows = O.lookup(olt, keys, k + 1)
+        ref = np.concatenate([O.pool(rows[f * 2 * B:(f + 1) * 2 * B], offs[f], "mean") for f in range(2)])
+        eq(pooled_all[k], ref)
+        grads = np.repeat(dp / np.float32(2.0), 2, axis=0).astype(np.float32)
+        O.grad_update(olt, keys, grads, k + 1, lr=1e-2, weight_decay=0.01, variant="adamw")
+    for a, b in zip(lt.local_table.export_rows(), olt.shards[0].export_rows()):
+        eq(a, b)
