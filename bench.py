@@ -435,10 +435,96 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_dist(args):
+    """N > 1: weak scaling over the row-sharded table (one shard per GPU, NCCL
+    all-to-all exchange of ids, rows and grads; distributed.DistSparseStep)."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2509_20883_b200 as skb
+    from paper_2509_20883_b200 import _native as N
+    from paper_2509_20883_b200.distributed import DistSparseStep
+
+    B, mem = args.batch, members()
+    n_ids = F_FEATURES * B
+    cfg = skb.AdamConfig(lr=1e-3, weight_decay=0.01, variant="adamw")
+    per_rank = (F_FEATURES * ID_SPACE) // world
+    lt = skb.LogicalTable("dim64", DIM, world, seed=0, members=mem, namespaced=True, dist=True,
+                          capacity_hint=0 if args.cold else per_rank + per_rank // 10)
+    table = lt.local_table
+    if not args.cold:  # warm: each rank admits the keys it owns
+        all_ids = torch.arange(ID_SPACE, dtype=torch.int64, device="cuda")
+        plan = skb.ShardPlan(world)
+        for m in mem:
+            keys = lt.keys_for(m, all_ids)
+            table._admit_unique(keys[plan.shard_of(keys) == rank].contiguous(), 0)
+        torch.cuda.synchronize()
+    P = 4
+    offs = [np.arange(B + 1, dtype=np.int64)] * F_FEATURES
+    batches, dps = [], []
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1234 + rank)
+    for k in range(P):
+        b = skb.PackedBatch(lt, mem, make_batch(rank, k, B), offs)
+        batches.append(b)
+        dps.append(torch.empty((b.num_bags, DIM), device="cuda").normal_(0.0, 1e-2, generator=gen))
+    stepper = DistSparseStep(lt)
+    pooled = torch.empty((batches[0].num_bags, DIM), device="cuda")
+    step_no = [0]
+
+    def run(count):
+        for k in range(count):
+            step_no[0] += 1
+            stepper.forward(batches[k % P], step_no[0], "sum", out=pooled)
+            stepper.backward(dps[k % P], cfg, step_no[0])
+
+    clk = ClockSampler(local).__enter__()
+    run(args.warmup)
+    dist.barrier()
+    torch.cuda.synchronize()
+    lib = N.lib()
+    l0 = lib.skb_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    run(args.steps)
+    ev1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches = lib.skb_launch_count() - l0
+    clk.__exit__(None, None, None)
+    t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    if rank == 0:
+        peak, peak_kind = load_peaks()
+        line = {
+            "metric": METRIC, "value": world * n_ids / (ms_step / 1e3), "unit": "IDs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C2 Criteo-shape DLRM sparse step, row-sharded over GPUs: 26 x dim64, "
+                                   "uniform ids [0,1e6) per feature, bag length 1, sum, SparseAdamW, warm",
+                       "global_batch": B * world, "per_gpu_batch": B, "features": F_FEATURES, "dim": DIM,
+                       "parallelism": f"row-sharded x{world}, NCCL all-to-all (ids, rows, grads)",
+                       "l2": "inputs larger than L2"},
+            "samples_per_s": world * B / (ms_step / 1e3),
+            "roofline": None, "cpu_baseline": None,
+            "e2e": None, "gpu_launches": int(launches), "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        run_dist(args)
     else:
         run_ours(args)
 

@@ -227,6 +227,23 @@ int skb_fused_stats_async(skb_table_t t, int64_t* dst_pinned_host, void* stream)
 /* Number of unique rows the last fused forward touched (synchronizes). */
 int skb_fused_last_unique(skb_table_t t, int64_t* n_unique_host, int64_t* n_new_host, void* stream);
 
+/* ---- building blocks of the multi-GPU step (distributed.py) ------------
+ * members_dev: int64[F+1][4] = {first position, first bag, salt, strategy}
+ * per member (strategy 0 sequential / 1 scatter); last row = {N, G, 0, 0}. */
+/* out[i] = namespaced key of ids[i] for its member (keys_for, sharding.py:170-178) */
+int skb_keys_members(const int64_t* ids, int64_t n, const int64_t* members_dev, int32_t num_members,
+                     int64_t* out, void* stream);
+/* pooled[g] = fold over positions p of bag g of rows[idx[p] * row_stride ...]
+ * (segment_reduce semantics per member strategy, segments.py:61-91) */
+int skb_pool_indexed(const float* rows, int64_t row_stride, const uint32_t* idx, const int64_t* bag_offs,
+                     int64_t num_bags, const int64_t* members_dev, int32_t num_members,
+                     int32_t any_sequential, int32_t mode, int64_t dim, float* out, void* stream);
+/* out[u] = in-position-order fold from +0 of dpooled[bag(p)] (/len for mean)
+ * over positions p with idx[p] == u  (np.add.at, sharding.py:283-290) */
+int skb_fold_bags(const float* dpooled, int64_t dim, const uint32_t* idx, int64_t n, int64_t num_unique,
+                  const int64_t* bag_offs, int64_t num_bags, int32_t mode, int64_t max_index, float* out,
+                  void* stream);
+
 /* ---- feature engine: features.py ---------------------------------------- */
 /* bucketize / fused_bucketize features.py:41-53,165-177: columns concatenated,
  * col_offs[C+1], edges_cat with edge_offs[C+1]; NaN -> SKB_E_VALUE */

@@ -81,6 +81,9 @@ _SIGS = {
     "skb_fused_stats_async": ([_p, _p, _p], ctypes.c_int),
     "skb_fused_profile": ([_p, _i64, _p], ctypes.c_int),
     "skb_fused_profile_read": ([_p, _i32, ctypes.POINTER(ctypes.c_float), _i64, ctypes.POINTER(_i64)], ctypes.c_int),
+    "skb_keys_members": ([_p, _i64, _p, _i32, _p, _p], ctypes.c_int),
+    "skb_pool_indexed": ([_p, _i64, _p, _p, _i64, _p, _i32, _i32, _i32, _i64, _p, _p], ctypes.c_int),
+    "skb_fold_bags": ([_p, _i64, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p], ctypes.c_int),
     "skb_bucketize_multi": ([_p, _p, _i64, _p, _p, _p, _i64, _p], ctypes.c_int),
     "skb_mod_multi": ([_p, _p, _i64, _p, _p, _i64, _p], ctypes.c_int),
     "skb_cross_offsets": ([_p, _p, _i64, _p, _p], ctypes.c_int),

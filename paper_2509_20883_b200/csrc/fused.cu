@@ -511,10 +511,10 @@ __global__ void k_fused_finish(int64_t* counters, int64_t* dev) {
 struct ArenaSrc {
   const float* arena;
   const uint32_t* slot;  // indexed by position (already offset for smem tiles)
-  int D;
+  int64_t stride;        // floats per row: 3*D in the table arena, D for plain rows
   int c;
   template <int VEC> __device__ __forceinline__ typename VecT<VEC>::T load(int64_t p) const {
-    return vload<VEC>(arena + (int64_t)slot[p] * (3 * D) + c);
+    return vload<VEC>(arena + (int64_t)slot[p] * stride + c);
   }
 };
 
@@ -532,7 +532,8 @@ template <int VEC, int R, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_fused_pool_scatter(const float* __restrict__ arena,
                                                                   const uint32_t* __restrict__ slot,
                                                                   const int64_t* __restrict__ bag_offs, int64_t G,
-                                                                  int mode, int D, float* __restrict__ out) {
+                                                                  int mode, int D, int64_t stride,
+                                                                  float* __restrict__ out) {
   using T = typename VecT<VEC>::T;
   const int lane = threadIdx.x & 31;
   const int rowv = D / VEC;
@@ -541,7 +542,7 @@ __global__ void __launch_bounds__(256, MINB) k_fused_pool_scatter(const float* _
   const int sub = lane / L, sl = lane - sub * L;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nchunks = (G + 31) / 32;
-  const int64_t D3 = 3 * (int64_t)D;
+  const int64_t D3 = stride;
   for (int64_t ch = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; ch < nchunks; ch += warps) {
     const int64_t g0 = ch * 32;
     const int nb = (int)(G - g0 < 32 ? G - g0 : 32);
@@ -601,7 +602,7 @@ template <int VEC>
 __global__ void __launch_bounds__(256) k_fused_pool_general(const float* __restrict__ arena, const uint32_t* __restrict__ slot,
                                                     const int64_t* __restrict__ bag_offs, int64_t G,
                                                     const MemberDev* __restrict__ mt, int F, int mode, int D,
-                                                    float* __restrict__ out, uint32_t* __restrict__ bag_of) {
+                                                    int64_t stride, float* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PoolSmem* sm = reinterpret_cast<PoolSmem*>(smem_raw);
   MemberView mv = stage_members(&sm->m, mt, F);
@@ -632,7 +633,7 @@ __global__ void __launch_bounds__(256) k_fused_pool_general(const float* __restr
       const bool last = g == mv_bag(mv, f + 1) - 1;
       const int64_t nend = mv_pos(mv, f + 1);
       for (int c = lane * VEC; c < D; c += L * VEC) {
-        ArenaSrc src{arena, sl, D, c};
+        ArenaSrc src{arena, sl, stride, c};
         typename VecT<VEC>::T acc = strat == 0 ? pool_sequential<VEC>(src, b, reduceat_end(b, e, last, nend))
                                                : pool_scatter<VEC>(src, b, e);
         if (mode == 1 && e > b) acc = vdiv<VEC>(acc, (float)(e - b));
@@ -668,7 +669,7 @@ __device__ __forceinline__ int nth_bit(unsigned x, int k) {
 // each per pass: both rows' w, m, v and first dpooled loads are in flight
 // before any arithmetic.  A run continuing past its chunk is finished by the
 // warp owning its head (the next chunk sees no head there).
-template <int VEC, int R, int MINB>
+template <int VEC, int R, int MINB, bool ADAM = true>
 __global__ void __launch_bounds__(256, MINB) k_fused_adam(int64_t n, const uint32_t* __restrict__ skey,
                                                     const uint32_t* __restrict__ sval,
                                                     const int64_t* __restrict__ bag_offs,
@@ -725,10 +726,12 @@ __global__ void __launch_bounds__(256, MINB) k_fused_adam(int64_t n, const uint3
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (h[r] >= 0) {
-            const float* row = arena + (int64_t)slot[r] * D3;
-            p[r] = vload<VEC>(row + c);
-            m[r] = vload<VEC>(row + D + c);
-            v[r] = vload<VEC>(row + 2 * D + c);
+            if constexpr (ADAM) {
+              const float* row = arena + (int64_t)slot[r] * D3;
+              p[r] = vload<VEC>(row + c);
+              m[r] = vload<VEC>(row + D + c);
+              v[r] = vload<VEC>(row + 2 * D + c);
+            }
             const uint32_t g = s_bag[wib][h[r]];
             T x = vload<VEC>(dpooled + (int64_t)g * D + c);
             if (mode == 1) x = vdiv<VEC>(x, (float)(__ldg(bag_offs + g + 1) - __ldg(bag_offs + g)));
@@ -744,16 +747,20 @@ __global__ void __launch_bounds__(256, MINB) k_fused_adam(int64_t n, const uint3
             if (mode == 1) x = vdiv<VEC>(x, (float)(__ldg(bag_offs + g + 1) - __ldg(bag_offs + g)));
             acc[r] = vadd<VEC>(acc[r], x);
           }
-          adam_vec<VEC>(p[r], m[r], v[r], acc[r], a);
-          float* row = arena + (int64_t)slot[r] * D3;
-          vstore<VEC>(row + c, p[r]);
-          vstore<VEC>(row + D + c, m[r]);
-          vstore<VEC>(row + 2 * D + c, v[r]);
+          if constexpr (ADAM) {
+            adam_vec<VEC>(p[r], m[r], v[r], acc[r], a);
+            float* row = arena + (int64_t)slot[r] * D3;
+            vstore<VEC>(row + c, p[r]);
+            vstore<VEC>(row + D + c, m[r]);
+            vstore<VEC>(row + 2 * D + c, v[r]);
+          } else {  // fold only: acc -> out[key] (arena is the [U, D] output)
+            vstore<VEC>(arena + (int64_t)slot[r] * D + c, acc[r]);
+          }
         }
       }
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        if (h[r] >= 0 && sl == 0 && step >= 0) last_step[slot[r]] = step;
+        if (ADAM && h[r] >= 0 && sl == 0 && step >= 0) last_step[slot[r]] = step;
     }
     __syncwarp();
   }
@@ -1120,7 +1127,7 @@ static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStrea
     const bool v4 = D % 4 == 0 && (uintptr_t)pooled % 16 == 0;
     if (!B.any_seq) {
       const unsigned grid = grid_for(((G + 31) / 32) * 32, 256, 8);
-#define SKB_POOL_ARGS t->arena, B.slot, B.bag_offs, G, B.mode, D, pooled
+#define SKB_POOL_ARGS t->arena, B.slot, B.bag_offs, G, B.mode, D, 3 * (int64_t)D, pooled
       if (!v4)
         k_fused_pool_scatter<1, 1, 4><<<grid, 256, 0, s>>>(SKB_POOL_ARGS);
       else
@@ -1135,12 +1142,12 @@ static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStrea
 #undef SKB_POOL_ARGS
     } else if (v4) {
       k_fused_pool_general<4><<<grid_for(ntiles * 256, 256, 6), 256, psm, s>>>(t->arena, B.slot, B.bag_offs, G,
-                                                                              B.members, B.F, B.mode, D, pooled,
-                                                                              B.bag);
+                                                                              B.members, B.F, B.mode, D,
+                                                                              3 * (int64_t)D, pooled);
     } else {
       k_fused_pool_general<1><<<grid_for(ntiles * 256, 256, 6), 256, psm, s>>>(t->arena, B.slot, B.bag_offs, G,
-                                                                              B.members, B.F, B.mode, D, pooled,
-                                                                              B.bag);
+                                                                              B.members, B.F, B.mode, D,
+                                                                              3 * (int64_t)D, pooled);
     }
     SKB_LAUNCH_CHECK();
     prof_mark(c, P_POOL, 1, s);
@@ -1274,6 +1281,97 @@ int skb_fused_last_unique(skb_table_t h, int64_t* n_unique_host, int64_t* n_new_
   SKB_CUDA(cudaStreamSynchronize(s));
   *n_unique_host = v[2];
   *n_new_host = v[1];
+  SKB_API_END
+}
+
+}  // extern "C"
+
+namespace skb {
+// ---------------------------------------------------------------------------
+// generic building blocks for the multi-GPU step (distributed.py): keys of
+// every member in one launch, pooling from any row source through a
+// per-position row index, and the ordered fold of pooled grads per index.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_keys_members(const int64_t* __restrict__ ids, int64_t n,
+                                                      const MemberDev* __restrict__ mt, int F,
+                                                      int64_t* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const MemberView mv = stage_members(reinterpret_cast<MemberSmem*>(smem_raw), mt, F);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = key_of(__ldg(ids + i), mv, F, 1, i);
+}
+
+}  // namespace skb
+
+extern "C" {
+
+int skb_keys_members(const int64_t* ids, int64_t n, const int64_t* members_dev, int32_t num_members, int64_t* out,
+                     void* stream) {
+  SKB_API_BEGIN
+  if (n <= 0) return SKB_OK;
+  const skb::MemberDev* mt = reinterpret_cast<const skb::MemberDev*>(members_dev);
+  skb::k_keys_members<<<skb::grid_for(n, 256), 256, skb::member_smem(num_members), skb::as_stream(stream)>>>(
+      ids, n, mt, num_members, out);
+  SKB_LAUNCH_CHECK();
+  SKB_API_END
+}
+
+int skb_pool_indexed(const float* rows, int64_t row_stride, const uint32_t* idx, const int64_t* bag_offs,
+                     int64_t num_bags, const int64_t* members_dev, int32_t num_members, int32_t any_sequential,
+                     int32_t mode, int64_t dim, float* out, void* stream) {
+  SKB_API_BEGIN
+  using namespace skb;
+  cudaStream_t s = as_stream(stream);
+  const int64_t G = num_bags;
+  if (G <= 0) return SKB_OK;
+  const int D = (int)dim;
+  const bool v4 = D % 4 == 0 && row_stride % 4 == 0 && (uintptr_t)out % 16 == 0 && (uintptr_t)rows % 16 == 0;
+  const MemberDev* mt = reinterpret_cast<const MemberDev*>(members_dev);
+  if (!any_sequential) {
+    const unsigned grid = grid_for(((G + 31) / 32) * 32, 256, 8);
+    if (v4)
+      k_fused_pool_scatter<4, 2, 4><<<grid, 256, 0, s>>>(rows, idx, bag_offs, G, mode, D, row_stride, out);
+    else
+      k_fused_pool_scatter<1, 1, 4><<<grid, 256, 0, s>>>(rows, idx, bag_offs, G, mode, D, row_stride, out);
+  } else {
+    const int64_t ntiles = (G + kTileBags - 1) / kTileBags;
+    if (v4)
+      k_fused_pool_general<4><<<grid_for(ntiles * 256, 256, 6), 256, sizeof(PoolSmem), s>>>(
+          rows, idx, bag_offs, G, mt, num_members, mode, D, row_stride, out);
+    else
+      k_fused_pool_general<1><<<grid_for(ntiles * 256, 256, 6), 256, sizeof(PoolSmem), s>>>(
+          rows, idx, bag_offs, G, mt, num_members, mode, D, row_stride, out);
+  }
+  SKB_LAUNCH_CHECK();
+  SKB_API_END
+}
+
+int skb_fold_bags(const float* dpooled, int64_t dim, const uint32_t* idx, int64_t n, int64_t num_unique,
+                  const int64_t* bag_offs, int64_t num_bags, int32_t mode, int64_t max_index, float* out,
+                  void* stream) {
+  SKB_API_BEGIN
+  using namespace skb;
+  cudaStream_t s = as_stream(stream);
+  const int D = (int)dim;
+  if (num_unique > 0) SKB_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * num_unique * D, s));
+  if (n <= 0) return SKB_OK;
+  Scratch bag(4 * n, s), skey(4 * n, s), sval(4 * n, s), cnt(8, s);
+  k_bag_of<<<grid_for(num_bags > 0 ? num_bags : 1, 256), 256, 0, s>>>(bag_offs, num_bags, bag.as<uint32_t>());
+  SKB_LAUNCH_CHECK();
+  sort_pairs_u32(idx, skey.as<uint32_t>(), bag.as<uint32_t>(), sval.as<uint32_t>(), n,
+                 bits_for((uint64_t)(max_index > 0 ? max_index : 1)), s);
+  const int64_t chunks = (n + 31) / 32;
+  AdamDev none{};
+  const bool v4 = D % 4 == 0 && (uintptr_t)dpooled % 16 == 0 && (uintptr_t)out % 16 == 0;
+  if (v4)
+    k_fused_adam<4, 1, 4, false><<<(unsigned)((chunks + 7) / 8), 256, 0, s>>>(
+        n, skey.as<uint32_t>(), sval.as<uint32_t>(), bag_offs, dpooled, mode, D, none, out, nullptr, -1,
+        cnt.as<int64_t>());
+  else
+    k_fused_adam<1, 1, 4, false><<<(unsigned)((chunks + 7) / 8), 256, 0, s>>>(
+        n, skey.as<uint32_t>(), sval.as<uint32_t>(), bag_offs, dpooled, mode, D, none, out, nullptr, -1,
+        cnt.as<int64_t>());
+  SKB_LAUNCH_CHECK();
   SKB_API_END
 }
 

@@ -61,6 +61,8 @@ static void ensure_pool() {
   // keep freed scratch cached in the pool: per-step scratch is then free
   uint64_t thr = 8ull << 30;
   SKB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  // optional L2 fetch-granularity hint (random 16 B probes vs 128 B lines)
+  if (const char* g = getenv("SKB_L2_FETCH")) SKB_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, atoi(g)));
   g_pool_ready[dev] = true;
 }
 
