@@ -56,6 +56,7 @@ def parse():
     p.add_argument("--batch", type=int, default=BATCH)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cold", action="store_true", help="do not pre-populate the table")
+    p.add_argument("--no-pipeline", action="store_true", help="no cross-step prefetch of the index phase")
     return p.parse_args()
 
 
@@ -299,11 +300,12 @@ def run_ours(args):
         step k+1 is prefetched between the pool and the fold+Adam of step k,
         so it runs on the table's index stream underneath the optimizer."""
         first = step_no[0] + 1
-        skb.prefetch(lt, get(0)[0], first, "sum")
+        if not args.no_pipeline:
+            skb.prefetch(lt, get(0)[0], first, "sum")
         for k in range(count):
             batch, dp = get(k)
             skb.lookup_pool(lt, batch, first + k, "sum", out=pooled)
-            if k + 1 < count:
+            if k + 1 < count and not args.no_pipeline:
                 skb.prefetch(lt, get(k + 1)[0], first + k + 1, "sum")
             skb.pool_grad_adam(lt, dp, cfg, first + k)
             if after_backward:
@@ -444,8 +446,14 @@ def run_dist(args):
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_DIST_BACKEND=gloo lets several ranks share one GPU (functional check only)
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    local = local if backend == "nccl" else 0
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
     import paper_2509_20883_b200 as skb
     from paper_2509_20883_b200 import _native as N
     from paper_2509_20883_b200.distributed import DistSparseStep
