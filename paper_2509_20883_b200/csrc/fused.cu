@@ -1266,12 +1266,16 @@ static void fused_prepare(Table* t, const BatchArgs& a, cudaStream_t s) {
   SKB_CUDA(cudaEventRecord(c->ev_in, s));
   SKB_CUDA(cudaStreamWaitEvent(x, c->ev_in, 0));
   if (B.ever_used) SKB_CUDA(cudaStreamWaitEvent(x, B.ev_free, 0));
-  // growth moves the arena: quiesce the caller's stream first (rare)
-  if (table_needs_growth(t, a.n)) {
+  // growth moves the arena and side arrays: quiesce both streams before it and
+  // finish the copies before any later main-stream kernel (e.g. the pending
+  // fold+Adam of the previous step) can touch the new buffers (rare)
+  const bool grow = table_needs_growth(t, a.n);
+  if (grow) {
     SKB_CUDA(cudaStreamSynchronize(s));
     SKB_CUDA(cudaStreamSynchronize(x));
   }
   table_reserve(t, a.n, x);
+  if (grow) SKB_CUDA(cudaStreamSynchronize(x));
   if (t->arena_rows >= (1ll << 32) - 1) raise(SKB_E_UNSUPPORTED, t->arena_rows, "fused step: > 2^32 rows");
   batch_reserve(B, a.n, a.F, x);
   std::vector<MemberDev> mh(a.F + 1);
