@@ -30,6 +30,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "longfold.cuh"
 #include "pool.cuh"
 #include "table.cuh"
 
@@ -65,7 +66,9 @@ struct BatchCtx {
   int64_t* tile_cnt = nullptr;  // [N / kRankTile + 2]
   HEntry* scratch = nullptr;  // [2*cap_n pow2 + 1]
   int64_t scratch_cap = 0;
-  int64_t* dev = nullptr;     // [0] misses M, [1] new K, [2] unique U
+  int64_t* dev = nullptr;     // [0] misses M, [1] new K, [2] unique U, [3] long runs
+  LongRun* longs = nullptr;   // deferred long runs of the fold (hot ids)
+  int64_t longs_cap = 0;
   MemberDev* members = nullptr;
   int64_t members_cap = 0;
   std::vector<MemberDev> members_host;
@@ -112,6 +115,7 @@ static void batch_free(BatchCtx& B) {
   cudaFree(B.scratch);
   cudaFree(B.dev);
   cudaFree(B.members);
+  cudaFree(B.longs);
   if (B.ev_ready) cudaEventDestroy(B.ev_ready);
   if (B.ev_free) cudaEventDestroy(B.ev_free);
 }
@@ -169,6 +173,8 @@ static void batch_reserve(BatchCtx& B, int64_t n, int64_t F, cudaStream_t s) {
     realloc_dev(B.tile_cnt, cap / kRankTile + 2, s);
     B.scratch_cap = next_pow2(2 * cap > 64 ? 2 * cap : 64);
     realloc_dev(B.scratch, B.scratch_cap + 1, s);
+    B.longs_cap = cap / kLongRun + 1;
+    realloc_dev(B.longs, B.longs_cap, s);
     B.cap_n = cap;
   }
   if (F + 1 > B.members_cap) {
@@ -657,6 +663,26 @@ __device__ __forceinline__ void adam_vec(typename VecT<VEC>::T& p, typename VecT
   }
 }
 
+// First position >= x whose sorted key differs from `key` (keys are sorted,
+// so galloping + binary search: O(log run) dependent loads, not O(run)).
+__device__ __forceinline__ int64_t run_end(const uint32_t* __restrict__ skey, int64_t n, int64_t x, uint32_t key) {
+  if (x >= n || __ldg(skey + x) != key) return x;
+  int64_t lo = x, step = 1;  // skey[lo] == key
+  while (true) {
+    const int64_t hi = lo + step;
+    if (hi >= n || __ldg(skey + hi) != key) {
+      int64_t a = lo, b = hi < n ? hi : n;  // skey[a] == key, b is past the run
+      while (b - a > 1) {
+        const int64_t mid = (a + b) >> 1;
+        if (__ldg(skey + mid) == key) a = mid; else b = mid;
+      }
+      return b;
+    }
+    lo = hi;
+    step <<= 1;
+  }
+}
+
 // position of the k-th (0-based) set bit of x, or -1
 __device__ __forceinline__ int nth_bit(unsigned x, int k) {
   unsigned r = __fns(x, 0, k + 1);
@@ -675,7 +701,9 @@ __global__ void __launch_bounds__(256, MINB) k_fused_adam(int64_t n, const uint3
                                                     const int64_t* __restrict__ bag_offs,
                                                     const float* __restrict__ dpooled, int mode, int D, AdamDev a,
                                                     float* __restrict__ arena, int64_t* __restrict__ last_step,
-                                                    int64_t step, int64_t* __restrict__ dev_unique) {
+                                                    int64_t step, int64_t* __restrict__ dev_unique,
+                                                    LongRun* __restrict__ longs, int64_t* __restrict__ nlong,
+                                                    int64_t longs_cap) {
   using T = typename VecT<VEC>::T;
   __shared__ uint32_t s_bag[8][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -717,8 +745,13 @@ __global__ void __launch_bounds__(256, MINB) k_fused_adam(int64_t n, const uint3
       for (int r = 0; r < R; ++r) {
         if (h[r] >= 0 && e[r] == j0 + 32) {  // run may continue into later chunks
           int64_t x = e[r];
-          while (x < n && __ldg(skey + x) == slot[r]) ++x;
+          x = run_end(skey, n, x, slot[r]);
           e[r] = x < n ? x : n;
+        }
+        // hot ids: defer to the CTA-per-run long fold (VEC == 4 only)
+        if (VEC == 4 && longs && h[r] >= 0 && e[r] - (j0 + h[r]) > kLongRun) {
+          if (sl == 0) push_long_run(longs, nlong, longs_cap, slot[r], (uint32_t)(j0 + h[r]), (uint32_t)e[r]);
+          h[r] = -1;
         }
       }
       for (int c = sl * VEC; c < D; c += L * VEC) {
@@ -819,7 +852,9 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) k_fused_adam_tma(int64_t n,
                                                                     const float* __restrict__ dpooled, int mode, int D,
                                                                     AdamDev a, float* __restrict__ arena,
                                                                     int64_t* __restrict__ last_step, int64_t step,
-                                                                    int64_t* __restrict__ dev_unique) {
+                                                                    int64_t* __restrict__ dev_unique,
+                                                                    LongRun* __restrict__ longs,
+                                                                    int64_t* __restrict__ nlong, int64_t longs_cap) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int rowf = 3 * D;        // floats of [w|m|v]
   const int stage_f = kTmaRows * (rowf + D);
@@ -899,7 +934,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) k_fused_adam_tma(int64_t n,
             e = cbase + 32;
           } else {  // last head of the chunk: the run may cross the chunk / CTA slice
             int64_t x = cbase + h + 1;
-            while (x < n && __ldg(skey + x) == hk) ++x;
+            x = run_end(skey, n, x, hk);
             e = x;
           }
           const int slot_i = nrun + lane;
@@ -939,6 +974,10 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) k_fused_adam_tma(int64_t n,
     if (sub < P) {
       for (int i = grp; i < nr; i += groups) {
         const TmaDesc d = desc[s * kTmaRows + i];
+        if (d.je - d.jh > (uint32_t)kLongRun) {  // hot id: CTA-per-run long fold
+          if (sl == 0) push_long_run(longs, nlong, longs_cap, d.slot, d.jh, d.je);
+          continue;
+        }
         const float* srow = rows + ((int64_t)s * kTmaRows + i) * rowf;
         const float* sdp = dps + ((int64_t)s * kTmaRows + i) * D;
         float* grow = arena + (int64_t)d.slot * D3;
@@ -1389,6 +1428,20 @@ static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStrea
   c->pool_count++;
 }
 
+// dpooled[g] / float32(len(g)) per bag (len 0 bags untouched: no positions)
+__global__ void k_scale_bags(const float* __restrict__ dp, const int64_t* __restrict__ bag_offs, int64_t G, int D,
+                             float* __restrict__ out) {
+  const int per = D / 4;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < G * per; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = t / per;
+    const int c = (int)(t - g * per) * 4;
+    const float l = (float)(__ldg(bag_offs + g + 1) - __ldg(bag_offs + g));
+    float4 x = ldg4(dp + g * D + c);
+    if (l > 0.f) x = make_float4(__fdiv_rn(x.x, l), __fdiv_rn(x.y, l), __fdiv_rn(x.z, l), __fdiv_rn(x.w, l));
+    st4(out + g * D + c, x);
+  }
+}
+
 static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc, cudaStream_t s) {
   FusedCtx* c = t->fused;
   if (!c || c->bwd_count >= c->pool_count) raise(SKB_E_VALUE, 0, "fused backward without a preceding fused forward");
@@ -1400,11 +1453,23 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     AdamDev a = to_dev(sc);
     const int64_t chunks = (n + 31) / 32;
     const bool v4 = D % 4 == 0 && (uintptr_t)dpooled % 16 == 0;
+    // long mean bags: scale each bag's gradient once (the same fp32 division
+    // every position of the bag would do) and fold it as a sum
+    int mode = B.mode;
+    Scratch scaled;
+    if (mode == 1 && v4 && n >= 8 * B.G) {
+      scaled = Scratch(sizeof(float) * B.G * D, s);
+      k_scale_bags<<<grid_for(B.G * (D / 4), 256), 256, 0, s>>>(dpooled, B.bag_offs, B.G, D, scaled.as<float>());
+      SKB_LAUNCH_CHECK();
+      dpooled = scaled.as<float>();
+      mode = 0;
+    }
     // non-persistent grid (one chunk per warp): retiring blocks free SM slots
     // for the prefetched index phase of the next step
     const unsigned grid = env_int("SKB_ADAM_PERSIST", 0) ? grid_for(chunks * 32, 256, 8)
                                                          : (unsigned)((chunks + 7) / 8);
-#define SKB_ADAM_ARGS n, B.skey, B.sval, B.bag_offs, dpooled, B.mode, D, a, t->arena, t->last_step, B.step, B.dev + 2
+#define SKB_ADAM_ARGS n, B.skey, B.sval, B.bag_offs, dpooled, mode, D, a, t->arena, t->last_step, B.step, B.dev + 2, \
+                      (v4 ? B.longs : nullptr), B.dev + 3, B.longs_cap
     if (!v4) {
       k_fused_adam<1, 1, 4><<<grid, 256, 0, s>>>(SKB_ADAM_ARGS);
     } else {
@@ -1426,6 +1491,9 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     }
 #undef SKB_ADAM_ARGS
     SKB_LAUNCH_CHECK();
+    if (v4)
+      launch_long_fold<true>(B.longs, B.dev + 3, B.longs_cap, B.sval, dpooled, D, B.bag_offs, mode, a, t->arena,
+                             t->last_step, B.step, s);
     prof_mark(c, P_ADAM, 1, s);
   }
   B.last_written = true;
@@ -1597,7 +1665,10 @@ int skb_fold_bags(const float* dpooled, int64_t dim, const uint32_t* idx, int64_
   const int D = (int)dim;
   if (num_unique > 0) SKB_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * num_unique * D, s));
   if (n <= 0) return SKB_OK;
-  Scratch bag(4 * n, s), skey(4 * n, s), sval(4 * n, s), cnt(8, s);
+  Scratch bag(4 * n, s), skey(4 * n, s), sval(4 * n, s), cnt(16, s);
+  const int64_t lcap = n / kLongRun + 1;
+  Scratch longs(sizeof(LongRun) * lcap, s);
+  SKB_CUDA(cudaMemsetAsync(cnt.p, 0, 16, s));
   k_bag_of<<<grid_for(num_bags > 0 ? num_bags : 1, 256), 256, 0, s>>>(bag_offs, num_bags, bag.as<uint32_t>());
   SKB_LAUNCH_CHECK();
   sort_pairs_u32(idx, skey.as<uint32_t>(), bag.as<uint32_t>(), sval.as<uint32_t>(), n,
@@ -1608,12 +1679,15 @@ int skb_fold_bags(const float* dpooled, int64_t dim, const uint32_t* idx, int64_
   if (v4)
     k_fused_adam<4, 1, 4, false><<<(unsigned)((chunks + 7) / 8), 256, 0, s>>>(
         n, skey.as<uint32_t>(), sval.as<uint32_t>(), bag_offs, dpooled, mode, D, none, out, nullptr, -1,
-        cnt.as<int64_t>());
+        cnt.as<int64_t>(), longs.as<LongRun>(), cnt.as<int64_t>() + 1, lcap);
   else
     k_fused_adam<1, 1, 4, false><<<(unsigned)((chunks + 7) / 8), 256, 0, s>>>(
         n, skey.as<uint32_t>(), sval.as<uint32_t>(), bag_offs, dpooled, mode, D, none, out, nullptr, -1,
-        cnt.as<int64_t>());
+        cnt.as<int64_t>(), nullptr, nullptr, 0);
   SKB_LAUNCH_CHECK();
+  if (v4)
+    launch_long_fold<false>(longs.as<LongRun>(), cnt.as<int64_t>() + 1, lcap, sval.as<uint32_t>(), dpooled, D,
+                            bag_offs, mode, none, out, nullptr, -1, s);
   SKB_API_END
 }
 

@@ -12,6 +12,7 @@
 #include "common.cuh"
 #include "rows.cuh"
 #include "partition.cuh"
+#include "longfold.cuh"
 
 namespace skb {
 
@@ -173,7 +174,8 @@ void unique_partition(const int64_t* ids, int64_t n, int64_t S, int64_t* uniq, i
 template <int VEC>
 __global__ void k_fold_sorted(const uint32_t* __restrict__ heads, const int64_t* __restrict__ d_nseg, int64_t n,
                               const uint32_t* __restrict__ skey, const uint32_t* __restrict__ spos,
-                              const float* __restrict__ rows, int D, float* __restrict__ out) {
+                              const float* __restrict__ rows, int D, float* __restrict__ out,
+                              LongRun* __restrict__ longs, int64_t* __restrict__ nlong, int64_t longs_cap) {
   const int per_row = D / VEC;
   const int64_t nseg = *d_nseg;
   const int64_t total = nseg * per_row;
@@ -182,6 +184,10 @@ __global__ void k_fold_sorted(const uint32_t* __restrict__ heads, const int64_t*
     int c = (int)(t - sidx * per_row) * VEC;
     int64_t b = heads[sidx];
     int64_t e = sidx + 1 < nseg ? (int64_t)heads[sidx + 1] : n;
+    if (VEC == 4 && longs && e - b > kLongRun) {  // hot id: CTA-per-run long fold
+      if (c == 0) push_long_run(longs, nlong, longs_cap, skey[b], (uint32_t)b, (uint32_t)e);
+      continue;
+    }
     if constexpr (VEC == 4) {
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int64_t j = b; j < e; ++j) acc = add4(acc, ldg4(rows + (int64_t)spos[j] * D + c));
@@ -206,7 +212,10 @@ void grad_fold(const float* grads, int64_t n, int D, const int64_t* inverse, int
   SKB_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * U * D, s));
   if (n == 0 || U == 0) return;
   if (n >= (1ll << 32) || U >= (1ll << 32)) raise(SKB_E_UNSUPPORTED, n, "grad_fold: too many rows");
-  Scratch k(4 * n, s), v(4 * n, s), k2(4 * n, s), v2(4 * n, s), heads(4 * n, s), nseg(8, s);
+  Scratch k(4 * n, s), v(4 * n, s), k2(4 * n, s), v2(4 * n, s), heads(4 * n, s), nseg(16, s);
+  const int64_t lcap = n / kLongRun + 1;
+  Scratch longs(sizeof(LongRun) * lcap, s);
+  SKB_CUDA(cudaMemsetAsync(nseg.p, 0, 16, s));
   k_iota_keys<<<grid_for(n, 256), 256, 0, s>>>(inverse, n, k.as<uint32_t>(), v.as<uint32_t>());
   SKB_LAUNCH_CHECK();
   sort_pairs_u32(k.as<uint32_t>(), k2.as<uint32_t>(), v.as<uint32_t>(), v2.as<uint32_t>(), n,
@@ -215,11 +224,16 @@ void grad_fold(const float* grads, int64_t n, int D, const int64_t* inverse, int
   bool v4 = (D % 4 == 0) && ((uintptr_t)grads % 16 == 0) && ((uintptr_t)out % 16 == 0);
   if (v4)
     k_fold_sorted<4><<<grid_for(n * (D / 4), 256), 256, 0, s>>>(heads.as<uint32_t>(), nseg.as<int64_t>(), n,
-                                                               k2.as<uint32_t>(), v2.as<uint32_t>(), grads, D, out);
+                                                               k2.as<uint32_t>(), v2.as<uint32_t>(), grads, D, out,
+                                                               longs.as<LongRun>(), nseg.as<int64_t>() + 1, lcap);
   else
     k_fold_sorted<1><<<grid_for(n * D, 256), 256, 0, s>>>(heads.as<uint32_t>(), nseg.as<int64_t>(), n,
-                                                         k2.as<uint32_t>(), v2.as<uint32_t>(), grads, D, out);
+                                                         k2.as<uint32_t>(), v2.as<uint32_t>(), grads, D, out, nullptr,
+                                                         nullptr, 0);
   SKB_LAUNCH_CHECK();
+  if (v4)
+    launch_long_fold<false>(longs.as<LongRun>(), nseg.as<int64_t>() + 1, lcap, v2.as<uint32_t>(), grads, D, nullptr, 0,
+                            AdamDev{}, out, nullptr, -1, s);
 }
 
 struct IdxRestore {

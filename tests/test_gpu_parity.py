@@ -426,3 +426,53 @@ def test_fused_pipelined_prefetch(skb):
         O.grad_update(olt, keys, grads, k + 1, lr=1e-2, weight_decay=0.01, variant="adamw")
     for a, b in zip(lt.local_table.export_rows(), olt.shards[0].export_rows()):
         eq(a, b)
+
+
+def test_fused_hot_ids_long_runs(skb):
+    """Hot ids (runs of thousands of positions) take the CTA-per-run long
+    fold; still the exact np.add.at order (mean and sum, D = 8 and 64)."""
+    import torch
+    for D, mode in ((64, "mean"), (8, "sum"), (16, "mean")):
+        rng = np.random.default_rng(D)
+        members = ["h"]
+        lt = skb.LogicalTable(f"dim{D}", D, 1, seed=1, members=members, namespaced=True)
+        olt = O.OracleLogical(f"dim{D}", D, 1, seed=1, members=members, namespaced=True)
+        cfg = skb.AdamConfig(lr=1e-2, weight_decay=0.01, variant="adamw")
+        for step in range(1, 3):
+            lens = rng.integers(1, 9, 3000)
+            offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+            ids = rng.integers(0, 5000, int(offs[-1]))
+            hot = rng.random(len(ids)) < 0.6          # 60% of positions on 3 hot ids
+            ids[hot] = rng.integers(0, 3, int(hot.sum()))
+            batch = skb.PackedBatch(lt, members, [ids], [offs])
+            pooled = skb.lookup_pool(lt, batch, step, mode)
+            dp = rng.standard_normal((3000, D)).astype(np.float32)
+            skb.pool_grad_adam(lt, torch.from_numpy(dp).cuda(), cfg, step)
+            keys = olt.keys_for("h", ids)
+            rows = O.lookup(olt, keys, step)
+            eq(pooled, O.pool(rows, offs, mode))
+            g = dp / lens.astype(np.float32)[:, None] if mode == "mean" else dp
+            O.grad_update(olt, keys, np.repeat(g, lens, axis=0).astype(np.float32), step, lr=1e-2,
+                          weight_decay=0.01, variant="adamw")
+        for a, b in zip(lt.local_table.export_rows(), olt.shards[0].export_rows()):
+            eq(a, b)
+
+
+def test_grad_update_hot_ids_long_runs(skb):
+    """Drop-in all_to_all_grad_update with 40k-position runs == oracle."""
+    rng = np.random.default_rng(12)
+    D = 16
+    ids = rng.integers(0, 50, 60000)
+    ids[rng.random(60000) < 0.7] = 7
+    grads = (rng.standard_normal((60000, D)) * rng.choice([1.0, 1e3, 1e-3], (60000, D))).astype(np.float32)
+    cfg = skb.AdamConfig(lr=1e-2)
+    for S in (1, 3):
+        lt = skb.LogicalTable("t", D, S, seed=4)
+        olt = O.OracleLogical("t", D, S, seed=4)
+        plan = skb.ShardPlan(S)
+        eq(skb.all_to_all_lookup(lt, ids, plan, 1), O.lookup(olt, ids, 1))
+        skb.all_to_all_grad_update(lt, ids, grads, plan, cfg, 1)
+        O.grad_update(olt, ids, grads, 1, lr=1e-2)
+        for s in range(S):
+            for a, b in zip(lt.shards[s].export_rows(), olt.shards[s].export_rows()):
+                eq(a, b)
