@@ -23,19 +23,14 @@ __device__ __forceinline__ int64_t ht_insert_min(HEntry* t, uint64_t mask, int64
     i = cap;
   } else {
     i = (int64_t)(bucket_hash((uint64_t)key) & mask);
-    while (true) {
-      long long k = *reinterpret_cast<volatile long long*>(&t[i].key);
-      if (k == key) break;
-      if (k == kEmptyKey) {
-        long long prev = (long long)atomicCAS(reinterpret_cast<unsigned long long*>(&t[i].key),
-                                              (unsigned long long)kEmptyKey, (unsigned long long)key);
-        if (prev == kEmptyKey || prev == key) break;
-      }
+    while (true) {  // one atomic per probe: CAS returns the resident key
+      long long prev = (long long)atomicCAS(reinterpret_cast<unsigned long long*>(&t[i].key),
+                                            (unsigned long long)kEmptyKey, (unsigned long long)key);
+      if (prev == kEmptyKey || prev == key) break;
       i = (int64_t)(((uint64_t)i + 1) & mask);
     }
   }
-  // min is monotone: skip the atomic when a smaller position already won
-  if (*reinterpret_cast<volatile long long*>(&t[i].val) > pos) atomicMin(&t[i].val, pos);
+  atomicMin(&t[i].val, pos);
   return i;
 }
 
@@ -111,17 +106,142 @@ __global__ void k_inverse(const int64_t* __restrict__ ids, const int64_t* __rest
 }
 
 // ---------------------------------------------------------------------------
-void dedup_first_occurrence(const int64_t* ids, int64_t n, DedupResult& r, cudaStream_t s) {
+// Stable multi-split for S <= kSplitMaxS: per-tile per-shard counts of the
+// first occurrences, one-block shard-major scan, then an in-order emit in
+// which each warp ranks its first occurrences among same-shard lanes with
+// __match_any_sync and the block keeps running per-shard cursors.  Five
+// kernels, no sort; the output order is exactly sharding.py:87-100's.
+constexpr int kSplitTile = 1024;
+constexpr int kSplitMaxS = 256;
+
+__global__ void __launch_bounds__(256) k_split_count(const int64_t* __restrict__ ids, int64_t n, const HEntry* t,
+                                                     const int64_t* __restrict__ hslot, int S,
+                                                     int64_t* __restrict__ tile_cnt, int64_t ntiles) {
+  __shared__ int cnt[kSplitMaxS];
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int k = threadIdx.x; k < S; k += blockDim.x) cnt[k] = 0;
+    __syncthreads();
+    const int64_t b = tile * kSplitTile, e = b + kSplitTile < n ? b + kSplitTile : n;
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x)
+      if (t[hslot[i]].val == i) atomicAdd(&cnt[S == 1 ? 0 : (int)owner_of(ids[i], (uint64_t)S)], 1);
+    __syncthreads();
+    for (int k = threadIdx.x; k < S; k += blockDim.x) tile_cnt[(int64_t)k * ntiles + tile] = cnt[k];
+    __syncthreads();
+  }
+}
+
+// exclusive scan of m values in one block (each thread owns kScanItems
+// consecutive values per pass); totals of each shard row -> counts
+constexpr int kScanItems = 8;
+__global__ void __launch_bounds__(1024) k_split_scan(int64_t* __restrict__ v, int64_t m, int64_t ntiles, int S,
+                                                    int64_t* __restrict__ counts) {
+  __shared__ int64_t s_sum[32];
+  __shared__ int64_t s_carry;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  const int64_t per_pass = (int64_t)blockDim.x * kScanItems;
+  for (int64_t base = 0; base < m; base += per_pass) {
+    const int64_t i0 = base + (int64_t)threadIdx.x * kScanItems;
+    int64_t x[kScanItems];
+    int64_t local = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      x[k] = i0 + k < m ? v[i0 + k] : 0;
+      local += x[k];
+    }
+    int64_t incl = local;
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffff, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_sum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      int64_t q = lane < (int)(blockDim.x >> 5) ? s_sum[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        int64_t y = __shfl_up_sync(0xffffffff, q, o);
+        if (lane >= o) q += y;
+      }
+      s_sum[lane] = q;
+    }
+    __syncthreads();
+    int64_t run = incl - local + (w ? s_sum[w - 1] : 0) + s_carry;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      if (i0 + k < m) v[i0 + k] = run;
+      run += x[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) s_carry = run;
+    __syncthreads();
+  }
+  for (int k = threadIdx.x; k < S; k += blockDim.x) {
+    const int64_t start = v[(int64_t)k * ntiles];
+    const int64_t end = k + 1 < S ? v[(int64_t)(k + 1) * ntiles] : s_carry;
+    counts[k] = end - start;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_split_emit(const int64_t* __restrict__ ids, int64_t n, HEntry* t,
+                                                    const int64_t* __restrict__ hslot, int S,
+                                                    const int64_t* __restrict__ tile_off, int64_t ntiles,
+                                                    int64_t* __restrict__ uniq) {
+  __shared__ int64_t run[kSplitMaxS];    // running output cursor per shard
+  __shared__ int64_t base0[kSplitMaxS];  // shard start in the concatenated output
+  __shared__ int wcnt[8][kSplitMaxS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int k = threadIdx.x; k < S; k += blockDim.x) {
+      run[k] = tile_off[(int64_t)k * ntiles + tile];
+      base0[k] = tile_off[(int64_t)k * ntiles];
+    }
+    const int64_t b = tile * kSplitTile, e = b + kSplitTile < n ? b + kSplitTile : n;
+    for (int64_t r0 = b; r0 < e; r0 += blockDim.x) {
+      for (int k = threadIdx.x; k < 8 * S; k += blockDim.x) (&wcnt[0][0])[(k / S) * kSplitMaxS + k % S] = 0;
+      __syncthreads();
+      const int64_t i = r0 + threadIdx.x;
+      const bool first = i < e && t[hslot[i]].val == i;
+      const int sh = first ? (S == 1 ? 0 : (int)owner_of(ids[i], (uint64_t)S)) : -1;
+      const unsigned grp = __match_any_sync(0xffffffffu, sh);
+      const int rank = __popc(grp & ((1u << lane) - 1));
+      if (first && rank == 0) wcnt[w][sh] = __popc(grp);
+      __syncthreads();
+      if (first) {
+        int64_t off = run[sh] + rank;
+        for (int q = 0; q < w; ++q) off += wcnt[q][sh];
+        uniq[off] = ids[i];
+        t[hslot[i]].val = off - base0[sh];
+      }
+      __syncthreads();
+      for (int k = threadIdx.x; k < S; k += blockDim.x) {
+        int64_t tot = 0;
+        for (int q = 0; q < 8; ++q) tot += wcnt[q][k];
+        run[k] += tot;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+void dedup_insert(const int64_t* ids, int64_t n, DedupResult& r, cudaStream_t s) {
   r.cap = next_pow2(n * 2 > 64 ? n * 2 : 64);
   r.table = Scratch(sizeof(HEntry) * (r.cap + 1), s);
   r.hslot = Scratch(sizeof(int64_t) * (n ? n : 1), s);
-  r.fpos = Scratch(sizeof(int64_t) * (n ? n : 1), s);
-  r.d_u = Scratch(sizeof(int64_t) * 2, s);
   HEntry* t = r.table.as<HEntry>();
   ht_fill(t, r.cap + 1, (long long)0x7FFFFFFFFFFFFFFFll, s);
   if (n > 0) {
     k_dedup_insert<<<grid_for(n, 256), 256, 0, s>>>(ids, n, t, (uint64_t)(r.cap - 1), r.cap, r.hslot.as<int64_t>());
     SKB_LAUNCH_CHECK();
+  }
+}
+
+void dedup_first_occurrence(const int64_t* ids, int64_t n, DedupResult& r, cudaStream_t s) {
+  dedup_insert(ids, n, r, s);
+  r.fpos = Scratch(sizeof(int64_t) * (n ? n : 1), s);
+  r.d_u = Scratch(sizeof(int64_t) * 2, s);
+  HEntry* t = r.table.as<HEntry>();
+  if (n > 0) {
     Scratch flags(n, s);
     k_first_flags<<<grid_for(n, 256), 256, 0, s>>>(t, r.hslot.as<int64_t>(), n, flags.as<uint8_t>());
     SKB_LAUNCH_CHECK();
@@ -135,6 +255,24 @@ void unique_partition(const int64_t* ids, int64_t n, int64_t S, int64_t* uniq, i
                       int64_t* inv_pos, cudaStream_t s) {
   if (n == 0) {
     SKB_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * S, s));
+    return;
+  }
+  if (S <= kSplitMaxS) {  // stable multi-split, no sort
+    DedupResult r;
+    dedup_insert(ids, n, r, s);
+    HEntry* t = r.table.as<HEntry>();
+    const int64_t ntiles = (n + kSplitTile - 1) / kSplitTile;
+    Scratch tc(sizeof(int64_t) * S * ntiles, s);
+    k_split_count<<<grid_for(ntiles * 256, 256), 256, 0, s>>>(ids, n, t, r.hslot.as<int64_t>(), (int)S,
+                                                              tc.as<int64_t>(), ntiles);
+    SKB_LAUNCH_CHECK();
+    k_split_scan<<<1, 1024, 0, s>>>(tc.as<int64_t>(), S * ntiles, ntiles, (int)S, counts);
+    SKB_LAUNCH_CHECK();
+    k_split_emit<<<grid_for(ntiles * 256, 256), 256, 0, s>>>(ids, n, t, r.hslot.as<int64_t>(), (int)S,
+                                                             tc.as<int64_t>(), ntiles, uniq);
+    SKB_LAUNCH_CHECK();
+    k_inverse<<<grid_for(n, 256), 256, 0, s>>>(ids, r.hslot.as<int64_t>(), t, n, (uint64_t)S, inv_shard, inv_pos);
+    SKB_LAUNCH_CHECK();
     return;
   }
   DedupResult r;

@@ -13,6 +13,8 @@ struct DedupResult {
   Scratch d_u;       // int64: U (device)
 };
 void dedup_first_occurrence(const int64_t* ids, int64_t n, DedupResult& r, cudaStream_t s);
+// table + hslot only (no compaction of first occurrences)
+void dedup_insert(const int64_t* ids, int64_t n, DedupResult& r, cudaStream_t s);
 
 void unique_partition(const int64_t* ids, int64_t n, int64_t S, int64_t* uniq, int64_t* counts,
                       int64_t* inv_shard, int64_t* inv_pos, cudaStream_t s);

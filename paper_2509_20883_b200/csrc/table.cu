@@ -198,7 +198,7 @@ __global__ void k_dup_flag(const HEntry* t, const int64_t* __restrict__ hslot, i
 static int64_t first_duplicate(const int64_t* ids, int64_t n, cudaStream_t s) {
   if (n < 2) return -1;
   DedupResult r;
-  dedup_first_occurrence(ids, n, r, s);
+  dedup_insert(ids, n, r, s);
   DevFlag f(s);
   k_dup_flag<<<grid_for(n, 256), 256, 0, s>>>(r.table.as<HEntry>(), r.hslot.as<int64_t>(), n, f.ptr());
   SKB_LAUNCH_CHECK();
@@ -432,7 +432,7 @@ void table_restore(Table* t, const int64_t* ids, int64_t n, const float* w, cons
   if (n == 0) return;
   {
     DedupResult r;
-    dedup_first_occurrence(ids, n, r, s);
+    dedup_insert(ids, n, r, s);
     DevFlag f(s);
     k_present_flag<<<grid_for(n, 256), 256, 0, s>>>(ids, n, t->idmap, (uint64_t)(t->idmap_cap - 1), t->idmap_cap,
                                                     r.table.as<HEntry>(), r.hslot.as<int64_t>(), f.ptr());
