@@ -291,22 +291,36 @@ def run_ours(args):
     G = dev_batches[0].num_bags
     pooled = torch.empty((G, DIM), device="cuda")
     # two device batch buffers refilled from pinned host memory in the e2e arm
-    e2e_batches = [skb.PackedBatch(lt, mem, make_batch(rank, 0, B), offs) for _ in range(2)]
+    e2e_batches = [skb.PackedBatch(lt, mem, make_batch(rank, 0, B), offs) for _ in range(3)]
+    copy_stream = torch.cuda.Stream()
+    buf_free = [torch.cuda.Event() for _ in range(3)]
     stats_host = torch.empty((args.steps, 4), dtype=torch.int64).pin_memory()
     step_no = [0]
 
-    def run_steps(get, count, after_backward=None):
+    def run_steps(get, count, after_backward=None, before_step=None, input_stream=None):
         """`count` pipelined steps: the index phase (probe, admission, sort) of
         step k+1 is prefetched between the pool and the fold+Adam of step k,
-        so it runs on the table's index stream underneath the optimizer."""
+        so it runs on the table's index stream underneath the optimizer.
+        `input_stream`: the stream the step's inputs arrive on (the prefetch
+        orders itself after that stream instead of the compute stream)."""
         first = step_no[0] + 1
+
+        def pre(k):
+            if input_stream is None:
+                skb.prefetch(lt, get(k)[0], first + k, "sum")
+            else:
+                with torch.cuda.stream(input_stream):
+                    skb.prefetch(lt, get(k)[0], first + k, "sum")
+
         if not args.no_pipeline:
-            skb.prefetch(lt, get(0)[0], first, "sum")
+            pre(0)
         for k in range(count):
+            if before_step:
+                before_step(k)
             batch, dp = get(k)
             skb.lookup_pool(lt, batch, first + k, "sum", out=pooled)
             if k + 1 < count and not args.no_pipeline:
-                skb.prefetch(lt, get(k + 1)[0], first + k + 1, "sum")
+                pre(k + 1)
             skb.pool_grad_adam(lt, dp, cfg, first + k)
             if after_backward:
                 after_backward(k)
@@ -358,22 +372,37 @@ def run_ours(args):
     e0.record()
     staged = {}
 
-    def get_e2e(k):
-        # H2D of step k's inputs from pinned host memory into one of two device
-        # batch buffers (the other may still be read by step k-1's backward)
-        if k not in staged:
+    # H2D of step k's inputs from pinned host memory on a copy stream, two
+    # steps ahead, into one of three device batch buffers; a buffer is
+    # refilled only after the backward of the step that last read it.
+    main_stream = torch.cuda.current_stream()
+
+    def stage(k):
+        if k >= args.steps or k in staged:
+            return
+        eb = e2e_batches[k % 3]
+        copy_stream.wait_event(buf_free[k % 3])
+        with torch.cuda.stream(copy_stream):
             hid, hoff = host_batches[k % P]
-            eb = e2e_batches[k % 2]
             eb.ids.copy_(hid, non_blocking=True)
             eb.bag_offs.copy_(hoff, non_blocking=True)
-            staged[k] = eb
+        staged[k] = eb
+
+    def get_e2e(k):
+        stage(k)
         return staged[k], dps[k % P]
 
-    def read_result(k):
+    def before_step(k):
+        stage(k + 2)
+
+    def after_e2e(k):
+        buf_free[k % 3].record(main_stream)
         # the step's metrics (misses, new rows, unique rows) back to the host
         N.call("skb_fused_stats_async", table.handle, ctypes.c_void_p(stats_host[k].data_ptr()), N.stream_ptr())
 
-    run_steps(get_e2e, args.steps, read_result)
+    # the compute stream sees the copied inputs through the prefetch's
+    # ready event (index stream waited on the copy stream)
+    run_steps(get_e2e, args.steps, after_e2e, before_step, input_stream=copy_stream)
     e1.record()
     barrier()
     e2e_ms = e0.elapsed_time(e1)
