@@ -76,6 +76,7 @@ void table_refresh(Table* t, cudaStream_t s) {
   SKB_CUDA(cudaStreamSynchronize(s));
   for (int i = 0; i < C_N; ++i) t->known[i] = t->snap_host[i];
   t->pending_adds = 0;
+  t->adds_after_snap = 0;
   t->snap_pending = false;
 }
 
@@ -87,7 +88,9 @@ static void harvest_snapshot(Table* t) {
   }
   for (int i = 0; i < C_N; ++i) t->known[i] = t->snap_host[i];
   t->snap_pending = false;
-  // pending_adds already excludes ops enqueued before the snapshot
+  // the snapshot covers every op enqueued before it; later ones stay pending
+  t->pending_adds = t->adds_after_snap;
+  t->adds_after_snap = 0;
 }
 
 bool table_needs_growth(Table* t, int64_t n) {
@@ -117,12 +120,16 @@ void table_reserve(Table* t, int64_t n, cudaStream_t s) {
 }
 
 void table_note_inserts(Table* t, int64_t n, cudaStream_t s) {
+  // `known` stays the last HARVESTED snapshot until the in-flight one lands,
+  // so every admission since then must stay in pending_adds (upper bound)
   t->pending_adds += n;
-  if (!t->snap_pending) {
+  if (t->snap_pending) {
+    t->adds_after_snap += n;
+  } else {
     SKB_CUDA(cudaMemcpyAsync(t->snap_host, t->counters, sizeof(int64_t) * C_N, cudaMemcpyDeviceToHost, s));
     SKB_CUDA(cudaEventRecord(t->snap_ev, s));
     t->snap_pending = true;
-    t->pending_adds = 0;  // ops before this point are covered by the snapshot
+    t->adds_after_snap = 0;  // this op is covered by the new snapshot
   }
 }
 

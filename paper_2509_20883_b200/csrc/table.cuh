@@ -49,7 +49,8 @@ struct Table {
   cudaEvent_t snap_ev = nullptr;
   bool snap_pending = false;
   int64_t known[C_N] = {0, 0, 0, 0};
-  int64_t pending_adds = 0;
+  int64_t pending_adds = 0;      // row admissions enqueued but not covered by `known`
+  int64_t adds_after_snap = 0;   // ... of which enqueued after the in-flight snapshot
 
   FusedCtx* fused = nullptr;
 

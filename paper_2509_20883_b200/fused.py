@@ -83,10 +83,11 @@ def _batch_args(lt: LogicalTable, batch: PackedBatch, step: int, mode: str):
 def prefetch(lt: LogicalTable, batch: PackedBatch, step: int, mode: str = "mean") -> None:
     """Enqueue the index phase (probe, admission, sort) of a future step.
 
-    Issue it after `lookup_pool` of step k and before `pool_grad_adam` of
-    step k: the index work of step k+1 then runs on the table's index stream
-    underneath the fold+Adam of step k.  Admission happens at prefetch time,
-    so do not prefetch across an eviction / restore boundary.
+    Issue it for step k+1 before `lookup_pool` of step k (or between that
+    and `pool_grad_adam` of step k): the index work of step k+1 then runs on
+    the table's index stream underneath step k's pool and fold+Adam.  At
+    most two batches are in flight.  Admission happens at prefetch time, so
+    do not prefetch across an eviction / restore boundary.
     """
     telemetry.bump("fused.prefetch")
     N.call("skb_fused_prepare", *_batch_args(lt, batch, step, mode), N.stream_ptr())

@@ -392,9 +392,11 @@ def test_fused_generic_dim(skb):
     _fused_vs_oracle(skb, 3, specs, steps=3, mode="mean", seed=2)
 
 
-def test_fused_pipelined_prefetch(skb):
-    """Prefetching step k+1's index phase under step k's fold+Adam gives the
-    same table state and pooled rows as the unpipelined oracle pipeline."""
+@pytest.mark.parametrize("early", [False, True])
+def test_fused_pipelined_prefetch(skb, early):
+    """Prefetching step k+1's index phase under step k's fold+Adam (issued
+    before or after step k's pool) gives the same table state and pooled
+    rows as the unpipelined oracle pipeline."""
     import torch
     rng = np.random.default_rng(21)
     D, members, B, steps = 8, ["a", "b"], 96, 6
@@ -410,8 +412,10 @@ def test_fused_pipelined_prefetch(skb):
     skb.prefetch(lt, batches[0], 1, "mean")
     pooled_all = []
     for k in range(steps):
+        if early and k + 1 < steps:
+            skb.prefetch(lt, batches[k + 1], k + 2, "mean")
         pooled_all.append(skb.lookup_pool(lt, batches[k], k + 1, "mean").clone())
-        if k + 1 < steps:
+        if not early and k + 1 < steps:
             skb.prefetch(lt, batches[k + 1], k + 2, "mean")
         skb.pool_grad_adam(lt, torch.from_numpy(raw[k][2]).cuda(), cfg, k + 1)
     with pytest.raises(ValueError):
@@ -476,3 +480,31 @@ def test_grad_update_hot_ids_long_runs(skb):
         for s in range(S):
             for a, b in zip(lt.shards[s].export_rows(), olt.shards[s].export_rows()):
                 eq(a, b)
+
+
+def test_fused_growth_under_async_snapshots(skb):
+    """Every step admits only new ids into a table that starts empty and is
+    enqueued without host syncs, so the host's row bound must stay an upper
+    bound while its counter snapshots are still in flight (regression: a
+    stale snapshot under-reserved the arena and admission wrote past it)."""
+    import torch
+    D, members, B, steps = 16, ["a"], 60_000, 8
+    lt = skb.LogicalTable("dim16", D, 1, seed=3, members=members, namespaced=True)
+    olt = O.OracleLogical("dim16", D, 1, seed=3, members=members, namespaced=True)
+    cfg = skb.AdamConfig(lr=1e-2)
+    offs = [np.arange(B + 1, dtype=np.int64)]
+    batches = [skb.PackedBatch(lt, members, [np.arange(k * B, (k + 1) * B, dtype=np.int64)], offs)
+               for k in range(steps)]
+    dp = torch.zeros((B, D), device="cuda")
+    pooled = []
+    skb.prefetch(lt, batches[0], 1, "sum")
+    for k in range(steps):
+        pooled.append(skb.lookup_pool(lt, batches[k], k + 1, "sum").clone())
+        if k + 1 < steps:
+            skb.prefetch(lt, batches[k + 1], k + 2, "sum")
+        skb.pool_grad_adam(lt, dp, cfg, k + 1)
+    torch.cuda.synchronize()
+    assert lt.num_rows == steps * B
+    for k in (0, steps - 1):
+        keys = olt.keys_for("a", np.arange(k * B, (k + 1) * B, dtype=np.int64))
+        eq(pooled[k], O.pool(O.lookup(olt, keys, k + 1), offs[0], "sum"))
