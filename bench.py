@@ -316,15 +316,18 @@ def run_ours(args):
 
         if not args.no_pipeline:
             pre(0)
+        pipelined = not args.no_pipeline
         for k in range(count):
-            if before_step:
-                before_step(k)
             batch, dp = get(k)
-            if not args.prefetch_late and k + 1 < count and not args.no_pipeline:
+            if pipelined and not args.prefetch_late and k + 1 < count:
                 pre(k + 1)
+                if before_step:  # after the prefetch: it must not queue behind later copies
+                    before_step(k)
             skb.lookup_pool(lt, batch, first + k, "sum", out=pooled)
-            if args.prefetch_late and k + 1 < count and not args.no_pipeline:
+            if pipelined and args.prefetch_late and k + 1 < count:
                 pre(k + 1)
+            if before_step and (args.prefetch_late or not pipelined or k + 1 >= count):
+                before_step(k)
             skb.pool_grad_adam(lt, dp, cfg, first + k)
             if after_backward:
                 after_backward(k)
@@ -376,6 +379,7 @@ def run_ours(args):
     e0.record()
     staged = {}
 
+    copy_ev = []
     # H2D of step k's inputs from pinned host memory on a copy stream, two
     # steps ahead, into one of three device batch buffers; a buffer is
     # refilled only after the backward of the step that last read it.
@@ -388,8 +392,12 @@ def run_ours(args):
         copy_stream.wait_event(buf_free[k % 3])
         with torch.cuda.stream(copy_stream):
             hid, hoff = host_batches[k % P]
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(copy_stream)
             eb.ids.copy_(hid, non_blocking=True)
             eb.bag_offs.copy_(hoff, non_blocking=True)
+            c1.record(copy_stream)
+            copy_ev.append((c0, c1))
         staged[k] = eb
 
     def get_e2e(k):
@@ -397,6 +405,8 @@ def run_ours(args):
         return staged[k], dps[k % P]
 
     def before_step(k):
+        # stage step k+2's inputs once step k+1's prefetch has been issued on
+        # the copy stream (so that prefetch does not wait for this copy)
         stage(k + 2)
 
     def after_e2e(k):
@@ -410,6 +420,7 @@ def run_ours(args):
     e1.record()
     barrier()
     e2e_ms = e0.elapsed_time(e1)
+    h2d_ms = statistics.median(a.elapsed_time(b) for a, b in copy_ev) if copy_ev else None
     clk.__exit__(None, None, None)
     h2d = int(host_batches[0][0].numel() * 8 + host_batches[0][1].numel() * 8)
 
@@ -462,7 +473,8 @@ def run_ours(args):
                               "frac": sb / (ms_step / 1e3) / 1e9 / peak},
             "kernels_ms": phase_ms,
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "IDs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 32},
+            "e2e": {"value": e2e_value, "unit": "IDs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 32,
+                    "h2d_ms_per_step": h2d_ms},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "prepopulate_ms": prepop_ms,
