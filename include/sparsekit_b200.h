@@ -275,6 +275,21 @@ int skb_ragged_pad_dense(const void* values, int64_t elem_bytes, int64_t width, 
                          int64_t rows, int64_t max_len, const void* pad_host, void* out,
                          uint8_t* mask, void* stream);
 
+/* ---- checkpoint boundary (checkpoint.py:192-313) ------------------------ */
+/* Stable ascending (signed) argsort of int64 keys: sorted_keys[i] =
+ * keys[perm[i]] — the global key order of save_sharded (checkpoint.py:212-214,
+ * np.argsort(ids, kind="stable")). */
+int skb_argsort_i64(const int64_t* keys, int64_t n, int64_t* sorted_keys, int64_t* perm, void* stream);
+/* Row moves of row_bytes (multiple of 4) bytes: gather out[i] = src[idx[i]]
+ * (save: rows into key order), scatter out[idx[i]] = src[i] (load_sharded
+ * re-routing rows to target shards, checkpoint.py:300-311). */
+int skb_gather_rows(const void* src, int64_t row_bytes, const int64_t* idx, int64_t n, void* out, void* stream);
+int skb_scatter_rows(const void* src, int64_t row_bytes, const int64_t* idx, int64_t n, void* out, void* stream);
+/* dest[i] = shard_base[inv_shard[i]] + inv_pos[i]: position of input i in the
+ * shard-grouped (stable) order of a unique_partition result */
+int skb_partition_dest(const int64_t* shard_base, const int64_t* inv_shard, const int64_t* inv_pos, int64_t n,
+                       int64_t* dest, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -589,3 +589,62 @@ def cross_rows(a_vals, a_offs, b_vals, b_offs):
                 ys.append(b_vals[b_offs[r] + j])
     vals = fnv1a_pair(np.asarray(xs, np.int64), np.asarray(ys, np.int64)).view(np.int64)
     return vals, offs
+
+
+# ---------------------------------------------------------------------------
+# Checkpoint container (checkpoint.py:1-17, 47-72, 123-252)
+# ---------------------------------------------------------------------------
+
+def safetensors_bytes(tensors: dict) -> bytes:
+    """One SafeTensors container, assembled by hand: u64-LE header length,
+    compact JSON header with entries in name order, packed LE payloads
+    (checkpoint.py:47-72, no __metadata__)."""
+    import json
+    import struct
+    entries, raws, off = [], [], 0
+    for name in sorted(tensors):
+        a = np.asarray(tensors[name])
+        if a.dtype == np.float32:
+            tag, raw = "F32", a.astype("<f4").tobytes()
+        elif a.dtype == np.int64:
+            tag, raw = "I64", a.astype("<i8").tobytes()
+        else:
+            raise TypeError(a.dtype)
+        shape = ",".join(str(d) for d in a.shape)
+        entries.append(f'{json.dumps(name)}:{{"dtype":"{tag}","shape":[{shape}],'
+                       f'"data_offsets":[{off},{off + len(raw)}]}}')
+        raws.append(raw)
+        off += len(raw)
+    head = ("{" + ",".join(entries) + "}").encode("utf-8")
+    return struct.pack("<Q", len(head)) + head + b"".join(raws)
+
+
+def checkpoint_files(groups, num_files: int, global_step: int) -> dict:
+    """save_sharded (checkpoint.py:192-252) as {file name: bytes}.
+
+    groups: [(name, [OracleTable shards], members, namespaced)], members = []
+    for a plain table.  Rows of all shards are merged in key order and split
+    contiguously, the first n % num_files files taking one extra row."""
+    import json
+    names = [f"ckpt-{i:05d}-of-{num_files:05d}.safetensors" for i in range(num_files)]
+    files = [dict() for _ in range(num_files)]
+    metas = []
+    for name, shards, members, namespaced in groups:
+        ex = [t.export_rows() for t in shards]
+        cols = [np.concatenate([e[i] for e in ex]) for i in range(5)]
+        order = np.argsort(cols[0], kind="stable")
+        cols = [c[order] for c in cols]
+        n = len(order)
+        counts = [n // num_files + (1 if i < n % num_files else 0) for i in range(num_files)]
+        t0 = shards[0]
+        metas.append({"name": name, "dim": t0.dim, "rows_per_file": counts, "global_step": global_step,
+                      "seed": t0.seed, "block_size": t0.block_size, "evict_threshold": t0.evict_threshold,
+                      "members": list(members), "namespaced": bool(namespaced)})
+        lo = 0
+        for i, c in enumerate(counts):
+            for part, col in zip(("ids", "weight", "m", "v", "last_step"), cols):
+                files[i][f"{name}.{part}"] = col[lo:lo + c]
+            lo += c
+    out = {fn: safetensors_bytes(t) for fn, t in zip(names, files)}
+    out["manifest.json"] = json.dumps({"version": 1, "files": names, "tables": metas}, indent=2).encode("utf-8")
+    return out

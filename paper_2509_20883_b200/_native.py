@@ -91,6 +91,11 @@ _SIGS = {
     "skb_ragged_truncate": ([_p, _i64, _i64, _i32, _p, _p, _p], ctypes.c_int),
     "skb_gather_elems": ([_p, _i64, _p, _i64, _p, _p], ctypes.c_int),
     "skb_ragged_pad_dense": ([_p, _i64, _i64, _p, _i64, _i64, _p, _p, _p, _p], ctypes.c_int),
+    # checkpoint boundary (checkpoint.py:192-313)
+    "skb_argsort_i64": ([_p, _i64, _p, _p, _p], ctypes.c_int),
+    "skb_gather_rows": ([_p, _i64, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_scatter_rows": ([_p, _i64, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_partition_dest": ([_p, _p, _p, _i64, _p, _p], ctypes.c_int),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -27,3 +27,10 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device in this container")
     return torch.device("cuda", 0)
+
+
+@pytest.fixture(scope="session")
+def skb(cuda):
+    """The package on a CUDA box (GPU tests only)."""
+    import paper_2509_20883_b200 as m
+    return m
