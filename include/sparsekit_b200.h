@@ -39,6 +39,7 @@ extern "C" {
 #define SKB_E_NOMEM 5       /* device allocation failure     */
 #define SKB_E_ARG 6         /* bad argument at the C boundary */
 #define SKB_E_UNSUPPORTED 7
+#define SKB_E_IO 8          /* reference raises ColumnIOError */
 
 typedef struct skb_table* skb_table_t;
 
@@ -289,6 +290,30 @@ int skb_scatter_rows(const void* src, int64_t row_bytes, const int64_t* idx, int
  * shard-grouped (stable) order of a unique_partition result */
 int skb_partition_dest(const int64_t* shard_base, const int64_t* inv_shard, const int64_t* inv_pos, int64_t n,
                        int64_t* dest, void* stream);
+
+/* ---- input side: columnar batch reader (columnio.py:328-409) ----------- */
+typedef struct skb_reader_s* skb_reader_t;
+/* chunks: [nchunks][5] int64 {path index, absolute byte offset, byte length,
+ * rows, chunk index within its file} — this shard's chunks in global order
+ * (the plan of columnio.py:306-325).  Columns in schema order: dtype 0 f32,
+ * 1 i64, 2 bytes; ragged; selected (unselected columns are never decoded).
+ * Batches of batch_rows rows (the last may be short) concatenate rows across
+ * chunk boundaries; `threads` decoder threads, up to prefetch_depth batches
+ * assembled ahead; pinned != 0: batch buffers are page-locked for `device`.
+ * Decode / truncation errors -> SKB_E_IO with the reference's message. */
+int skb_reader_open(const char* const* paths, int64_t npaths, const int64_t* chunks, int64_t nchunks,
+                    const char* const* col_names, const int32_t* col_dtype, const int32_t* col_ragged,
+                    const int32_t* col_selected, int64_t ncols, int64_t batch_rows, int64_t prefetch_depth,
+                    int32_t threads, int32_t pinned, int32_t device, skb_reader_t* out);
+/* advance to the next batch (blocks); *rows = 0 at the end.  The previous
+ * batch's buffers are recycled. */
+int skb_reader_next(skb_reader_t r, int64_t* rows);
+/* selected column j of the current batch: row_offsets [rows+1] (int64),
+ * values (n_values elements; for bytes columns the blob of blob_bytes bytes
+ * with str_offsets [n_values+1]) — host pointers valid until the next call */
+int skb_reader_column(skb_reader_t r, int64_t j, const int64_t** row_offsets, const void** values,
+                      int64_t* n_values, const int64_t** str_offsets, int64_t* blob_bytes);
+int skb_reader_close(skb_reader_t r);
 
 #ifdef __cplusplus
 }

@@ -16,6 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsparsekit_b200.so")
 
 SKB_OK, SKB_E_VALUE, SKB_E_INDEX, SKB_E_KEY, SKB_E_CUDA, SKB_E_NOMEM, SKB_E_ARG, SKB_E_UNSUPPORTED = range(8)
+SKB_E_IO = 8
 
 _i64, _u64, _i32, _p = ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, ctypes.c_void_p
 
@@ -96,6 +97,12 @@ _SIGS = {
     "skb_gather_rows": ([_p, _i64, _p, _i64, _p, _p], ctypes.c_int),
     "skb_scatter_rows": ([_p, _i64, _p, _i64, _p, _p], ctypes.c_int),
     "skb_partition_dest": ([_p, _p, _p, _i64, _p, _p], ctypes.c_int),
+    # input side (columnio.py:328-409): host-side native reader
+    "skb_reader_open": ([_p, _i64, _p, _i64, _p, _p, _p, _p, _i64, _i64, _i64, ctypes.c_int32, ctypes.c_int32,
+                         ctypes.c_int32, _p], ctypes.c_int),
+    "skb_reader_next": ([_p, _p], ctypes.c_int),
+    "skb_reader_column": ([_p, _i64, _p, _p, _p, _p, _p], ctypes.c_int),
+    "skb_reader_close": ([_p], ctypes.c_int),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -116,6 +123,23 @@ def load_library(path: str = LIB_PATH):
         fn.argtypes = args
         fn.restype = res
     return lib
+
+
+_host_lib = None
+
+
+def host_lib():
+    """The bound library for HOST-ONLY entry points (the columnar reader's
+    file decode); needs no CUDA device because that work is host IO by
+    nature — no device computation is ever routed through here."""
+    global _host_lib
+    if _lib is not None:
+        return _lib
+    if _host_lib is None:
+        with _lock:
+            if _host_lib is None:
+                _host_lib = load_library()
+    return _host_lib
 
 
 def lib():

@@ -35,6 +35,8 @@ def hash_feature(strings: RaggedTensor) -> RaggedTensor:
     """
     telemetry.bump("features.hash_feature")
     vals = strings.values
+    if hasattr(vals, "blob") and hasattr(vals, "offsets"):  # columnio.PackedStrings (reader output)
+        return RaggedTensor._trusted(fnv1a64_packed(vals.blob, vals.offsets), strings.row_offsets)
     blob, offs = pack_strings(list(vals))
     hashed = fnv1a64_packed(blob, offs)
     return strings.with_values(hashed)
