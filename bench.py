@@ -551,12 +551,46 @@ def run_dist(args):
     torch.cuda.synchronize()
     dist.barrier()
     launches = lib.skb_launch_count() - l0
+    # per-rank traffic of the last step: local unique rows U, owner rows U2,
+    # bytes sent to peers per direction (ids + rows back + grads)
+    ctx_counts = stepper.last_counts
+    U = int(sum(ctx_counts["send"]))
+    U2 = int(ctx_counts["owner_unique"])
+    sent_remote = sum(c for j, c in enumerate(ctx_counts["send"]) if j != rank)
+    recv_remote = sum(c for j, c in enumerate(ctx_counts["recv"]) if j != rank)
+    xbytes = sent_remote * (8 + 4 * DIM) + recv_remote * 4 * DIM
+
+    # e2e: each step's ids + offsets copied H2D from pinned host memory, the
+    # step's pooled checksum row read back
+    host = [(torch.from_numpy(b.ids.cpu().numpy()).pin_memory(),
+             torch.from_numpy(b.bag_offs.cpu().numpy()).pin_memory()) for b in batches]
+    e2e_b = [skb.PackedBatch(lt, mem, make_batch(rank, 0, B), offs) for _ in range(2)]
+    res = torch.empty((args.steps, DIM), dtype=torch.float32).pin_memory()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(args.steps):
+        step_no[0] += 1
+        eb = e2e_b[k % 2]
+        eb.ids.copy_(host[k % P][0], non_blocking=True)
+        eb.bag_offs.copy_(host[k % P][1], non_blocking=True)
+        stepper.forward(eb, step_no[0], "sum", out=pooled)
+        stepper.backward(dps[k % P], cfg, step_no[0])
+        res[k].copy_(pooled[0], non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
     clk.__exit__(None, None, None)
-    t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ev0.elapsed_time(ev1), e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_step = float(t.item()) / args.steps
+    ms_step = float(t[0].item()) / args.steps
+    e2e_ms = float(t[1].item()) / args.steps
     if rank == 0:
         peak, peak_kind = load_peaks()
+        G = batches[0].num_bags
+        sb = step_bytes(n_ids, G, U2, 0, DIM)
+        h2d = int(host[0][0].numel() * 8 + host[0][1].numel() * 8)
         line = {
             "metric": METRIC, "value": world * n_ids / (ms_step / 1e3), "unit": "IDs/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -567,8 +601,15 @@ def run_dist(args):
                        "parallelism": f"row-sharded x{world}, NCCL all-to-all (ids, rows, grads)",
                        "l2": "inputs larger than L2"},
             "samples_per_s": world * B / (ms_step / 1e3),
-            "roofline": None, "cpu_baseline": None,
-            "e2e": None, "gpu_launches": int(launches), "clocks": clk.summary(),
+            "roofline": {"bound": "hbm", "kernel": "step (rank-0 local HBM bytes)", "achieved": sb / ms_step / 1e6,
+                         "peak": peak, "unit": "GB/s", "frac": sb / ms_step / 1e6 / peak, "traffic": None,
+                         "peak_kind": peak_kind, "algorithmic_bytes": sb},
+            "exchange": {"bytes_per_step_per_direction": xbytes, "GB_per_s": xbytes / ms_step / 1e6,
+                         "nvlink_peak_GB_per_s": 900.0, "local_unique": U, "owner_unique": U2},
+            "cpu_baseline": None,
+            "e2e": {"value": world * n_ids / (e2e_ms / 1e3), "unit": "IDs/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": 4 * DIM},
+            "gpu_launches": int(launches), "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

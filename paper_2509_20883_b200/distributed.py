@@ -208,6 +208,7 @@ class DistSparseStep:
         self.comm = comm or Comm(lt.group)
         self.ops = GpuOps()
         self._ctx = None
+        self.last_counts = None
 
     @staticmethod
     def members_dev(batch):
@@ -252,6 +253,7 @@ class DistSparseStep:
                    any_seq, mcode, D, N.ptr(pooled), N.stream_ptr())
         self._ctx = dict(batch=batch, counts=counts, recv_counts=recv_counts, gidx=gidx, U=int(sum(counts)),
                          inv2=inv2, u2=u2, offs=offs, mode=mcode)
+        self.last_counts = {"send": list(counts), "recv": list(recv_counts), "owner_unique": int(u2.numel())}
         return pooled
 
     def backward(self, dpooled, cfg, step: int):
