@@ -268,6 +268,47 @@ static void check_live(Table* t, const int64_t* offs, int64_t n, const char* op,
   }
 }
 
+// scatter_update's checks (embedding.py:240-250) in one pass: distinctness
+// through a bitmap over the arena rows (offsets are slot numbers, so a
+// bitmap beats a hash set), liveness, range.  Reference order: duplicates
+// (ValueError) before liveness (IndexError); an out-of-range offset can only
+// be a duplicate of another out-of-range one, so that rare case re-checks
+// distinctness with the hash path before choosing the error.
+__global__ void k_scatter_check(const int64_t* __restrict__ offs, int64_t n, const uint8_t* __restrict__ live,
+                                int64_t rows, uint32_t* __restrict__ bitmap, unsigned long long* flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = offs[i];
+    if (o < 0 || o >= rows) {
+      atomicMin(&flags[1], (unsigned long long)i);
+      atomicMin(&flags[2], (unsigned long long)i);
+      continue;
+    }
+    const uint32_t bit = 1u << (o & 31);
+    if (atomicOr(&bitmap[o >> 5], bit) & bit) atomicMin(&flags[0], (unsigned long long)i);
+    if (!live[o]) atomicMin(&flags[1], (unsigned long long)i);
+  }
+}
+
+static void scatter_checks(Table* t, const int64_t* offs, int64_t n, cudaStream_t s) {
+  const int64_t words = (t->arena_rows + 31) / 32 + 1;
+  Scratch bm(sizeof(uint32_t) * words, s), fl(sizeof(unsigned long long) * 3, s);
+  SKB_CUDA(cudaMemsetAsync(bm.p, 0, sizeof(uint32_t) * words, s));
+  SKB_CUDA(cudaMemsetAsync(fl.p, 0xFF, sizeof(unsigned long long) * 3, s));
+  k_scatter_check<<<grid_for(n, 256), 256, 0, s>>>(offs, n, t->live, t->arena_rows, bm.as<uint32_t>(),
+                                                   fl.as<unsigned long long>());
+  SKB_LAUNCH_CHECK();
+  unsigned long long f[3];
+  SKB_CUDA(cudaMemcpyAsync(f, fl.p, sizeof f, cudaMemcpyDeviceToHost, s));
+  SKB_CUDA(cudaStreamSynchronize(s));
+  const unsigned long long none = ~0ull;
+  const bool dup = f[2] != none ? first_duplicate(offs, n, s) >= 0 : f[0] != none;
+  if (dup) raise(SKB_E_VALUE, 0, "scatter_update requires distinct offsets");
+  if (f[1] != none) {
+    const int64_t o = read_i64(offs + (int64_t)f[1], s);
+    raise(SKB_E_INDEX, o, "scatter_update: offset %lld is not a live slot", (long long)o);
+  }
+}
+
 static int64_t reported_capacity(Table* t) {
   int64_t hw = t->known[C_ALLOC] > t->ensured_slots ? t->known[C_ALLOC] : t->ensured_slots;
   return (hw + t->block_size - 1) / t->block_size * t->block_size;
@@ -750,9 +791,15 @@ int skb_table_gather(skb_table_t h, const int64_t* offsets, int64_t n, float* ro
   Table* t = table_from(h);
   cudaStream_t s = as_stream(stream);
   if (n <= 0) return SKB_OK;
-  check_live(t, offsets, n, "gather", s);
   const int D = (int)t->dim;
-  launch_rows_gather(IdxArray{offsets}, t->arena, 3 * D, rows_out, D, n, D, s);
+  DevFlag f(s);
+  launch_rows_gather_checked(IdxArray{offsets}, t->arena, 3 * D, rows_out, D, n, D, t->live, t->arena_rows, f.ptr(),
+                             s);
+  const int64_t bad = f.read();
+  if (bad >= 0) {
+    const int64_t o = read_i64(offsets + bad, s);
+    raise(SKB_E_INDEX, o, "gather: offset %lld is not a live slot", (long long)o);
+  }
   SKB_API_END
 }
 
@@ -761,8 +808,7 @@ int skb_table_scatter_update(skb_table_t h, const int64_t* offsets, int64_t n, c
   Table* t = table_from(h);
   cudaStream_t s = as_stream(stream);
   if (n <= 0) return SKB_OK;
-  if (first_duplicate(offsets, n, s) >= 0) raise(SKB_E_VALUE, 0, "scatter_update requires distinct offsets");
-  check_live(t, offsets, n, "scatter_update", s);
+  scatter_checks(t, offsets, n, s);
   const int D = (int)t->dim;
   launch_rows_scatter(IdxArray{offsets}, rows, D, t->arena, 3 * D, n, D, s);
   SKB_API_END
