@@ -276,6 +276,13 @@ int skb_ragged_pad_dense(const void* values, int64_t elem_bytes, int64_t width, 
                          int64_t rows, int64_t max_len, const void* pad_host, void* out,
                          uint8_t* mask, void* stream);
 
+/* Graph mode for the fused step: each phase's device work
+ * (index phase / pool / fold+Adam) is captured as a CUDA graph on its second
+ * call with an unchanged signature (buffers, sizes, table arrays) and replayed
+ * with the step and Adam scalars patched in; growth re-primes.  Results are
+ * identical to eager mode.  Default off (SKB_FUSED_GRAPHS=1 turns it on). */
+int skb_fused_set_graphs(skb_table_t t, int32_t enable);
+
 /* ---- checkpoint boundary (checkpoint.py:192-313) ------------------------ */
 /* Stable ascending (signed) argsort of int64 keys: sorted_keys[i] =
  * keys[perm[i]] — the global key order of save_sharded (checkpoint.py:212-214,

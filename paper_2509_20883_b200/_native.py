@@ -92,6 +92,7 @@ _SIGS = {
     "skb_ragged_truncate": ([_p, _i64, _i64, _i32, _p, _p, _p], ctypes.c_int),
     "skb_gather_elems": ([_p, _i64, _p, _i64, _p, _p], ctypes.c_int),
     "skb_ragged_pad_dense": ([_p, _i64, _i64, _p, _i64, _i64, _p, _p, _p, _p], ctypes.c_int),
+    "skb_fused_set_graphs": ([_p, ctypes.c_int32], ctypes.c_int),
     # checkpoint boundary (checkpoint.py:192-313)
     "skb_argsort_i64": ([_p, _i64, _p, _p, _p], ctypes.c_int),
     "skb_gather_rows": ([_p, _i64, _p, _i64, _p, _p], ctypes.c_int),

@@ -30,6 +30,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "graph.cuh"
 #include "longfold.cuh"
 #include "pool.cuh"
 #include "table.cuh"
@@ -81,6 +82,8 @@ struct BatchCtx {
   bool last_written = false;  // deferred last_step already flushed
   cudaEvent_t ev_ready = nullptr, ev_free = nullptr;
   bool ever_used = false;
+  int64_t gen = 0;  // bumped when a buffer above is reallocated / the member table changes
+  StepGraph g_prep, g_fwd, g_bwd;  // graph mode: captured device work of each phase
 };
 
 struct FusedCtx {
@@ -88,6 +91,8 @@ struct FusedCtx {
   cudaEvent_t ev_in = nullptr, ev_side_last = nullptr;
   BatchCtx b[2];
   int64_t prep_count = 0, pool_count = 0, bwd_count = 0;
+  bool graphs = false;  // replay each phase's device work as a CUDA graph
+  cudaStream_t cap = nullptr;  // capture stream of graph mode
   // optional per-kernel CUDA-event profiling: kProf phases x (begin, end) x cap steps
   int64_t prof_cap = 0;
   int64_t prof_n[5] = {0, 0, 0, 0, 0};
@@ -126,7 +131,13 @@ void fused_ctx_destroy(FusedCtx* c) {
   for (auto& v : c->prof_ev)
     for (auto e : v) cudaEventDestroy(e);
   for (auto& B : c->b) batch_free(B);
+  for (auto& B : c->b) {
+    B.g_prep.reset();
+    B.g_fwd.reset();
+    B.g_bwd.reset();
+  }
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->cap) cudaStreamDestroy(c->cap);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
   if (c->ev_side_last) cudaEventDestroy(c->ev_side_last);
   delete c;
@@ -154,6 +165,8 @@ static FusedCtx* ctx_get(Table* t) {
       SKB_CUDA(cudaEventCreateWithFlags(&B.ev_ready, cudaEventDisableTiming));
       SKB_CUDA(cudaEventCreateWithFlags(&B.ev_free, cudaEventDisableTiming));
     }
+    if (const char* g = getenv("SKB_FUSED_GRAPHS")) c->graphs = atoi(g) != 0;
+    SKB_CUDA(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
     t->fused = c;
   }
   return t->fused;
@@ -176,11 +189,13 @@ static void batch_reserve(BatchCtx& B, int64_t n, int64_t F, cudaStream_t s) {
     B.longs_cap = cap / kLongRun + 1;
     realloc_dev(B.longs, B.longs_cap, s);
     B.cap_n = cap;
+    B.gen++;
   }
   if (F + 1 > B.members_cap) {
     realloc_dev(B.members, F + 1, s);
     B.members_cap = F + 1;
     B.members_host.clear();
+    B.gen++;
   }
 }
 
@@ -1017,6 +1032,7 @@ static int env_int(const char* name, int dflt);
 template <int ROWS, int THREADS, int MINB, class... Args>
 static void launch_adam_tma(int64_t n, int D, cudaStream_t s, Args... args) {
   auto* kern = k_fused_adam_tma<ROWS, THREADS, MINB>;
+  note_param_kernel((const void*)kern, 15, 7, 10);
   const size_t sm = tma_smem_bytes(D, ROWS);
   static size_t sm_set = 0;
   if (sm_set < sm) {
@@ -1025,7 +1041,15 @@ static void launch_adam_tma(int64_t n, int D, cudaStream_t s, Args... args) {
   }
   // non-persistent: each CTA owns a fixed slice of sorted positions and
   // retires, so the high-priority index stream can take SM slots (pipeline)
-  const int64_t per_cta = env_int("SKB_TMA_SLICE", 1024);
+  // slice: 1024 positions (measured best on C2), shrunk for small batches so
+  // at least ~4 CTAs per SM share the work (a C1-size batch of 4096
+  // positions on 4 CTAs took 130 us of serial ring latency)
+  static const int64_t slice_env = env_int("SKB_TMA_SLICE", 0);
+  int64_t per_cta = slice_env;
+  if (per_cta == 0) {
+    const int64_t want = (n + 4 * sm_count() - 1) / (4 * sm_count());
+    per_cta = want < 64 ? 64 : (want > 1024 ? 1024 : want);
+  }
   int64_t ctas = per_cta > 0 ? (n + per_cta - 1) / per_cta : 0;
   if (per_cta <= 0) {
     int per_sm = 0;
@@ -1277,6 +1301,39 @@ static int pool_variant() {
 
 static size_t member_smem(int F) { return F <= kSmemMembers ? sizeof(MemberSmem) : 0; }
 
+
+std::vector<ParamKernel>& param_kernels() {
+  static std::vector<ParamKernel> v;
+  return v;
+}
+void note_param_kernel(const void* func, int nargs, int ia, int is) {
+  for (const ParamKernel& k : param_kernels())
+    if (k.func == func) return;
+  param_kernels().push_back(ParamKernel{func, nargs, ia, is});
+}
+
+// kernels of the step whose arguments carry the step / Adam scalars
+// (argument positions are verified against the live values at capture)
+static void register_param_kernels() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  note_param_kernel((const void*)k_fused_admit, 25, -1, 15);
+  note_param_kernel((const void*)k_fused_adam<1, 1, 4>, 15, 7, 10);
+  note_param_kernel((const void*)k_fused_adam<4, 2, 4>, 15, 7, 10);
+  note_param_kernel((const void*)k_fused_adam<4, 1, 5>, 15, 7, 10);
+  note_param_kernel((const void*)k_fused_adam<4, 1, 4>, 15, 7, 10);
+  note_param_kernel((const void*)k_long_fold<true>, 12, 8, 11);
+}
+
+// graph mode is off while per-phase event profiling is on (events cannot be
+// recorded from inside a replayed graph)
+static bool graph_mode(const FusedCtx* c) {
+  if (!c->graphs || c->prof_cap != 0) return false;
+  register_param_kernels();
+  return true;
+}
+
 // Admission as a chain of ordinary launches that each return at once when
 // the probe found no misses (SKB_ADMIT_COOP=0).  The default is the single
 // cooperative launch: measured on C2 warm it is 0.853 vs 0.876 ms/step
@@ -1375,6 +1432,8 @@ static void fused_prepare(Table* t, const BatchArgs& a, cudaStream_t s) {
   const uint64_t mask = (uint64_t)(t->idmap_cap - 1);
   const int D = (int)t->dim;
   const int64_t n = a.n, G = a.G;
+  const bool graph = graph_mode(c);
+  auto work = [&](cudaStream_t x) {
   SKB_CUDA(cudaMemsetAsync(B.dev, 0, sizeof(int64_t) * 4, x));
   if (n > 0) {
     prof_mark(c, P_PROBE, 0, x);
@@ -1387,7 +1446,8 @@ static void fused_prepare(Table* t, const BatchArgs& a, cudaStream_t s) {
                 t->counters, t->free_list, t->idmap, mask, t->idmap_cap, a.step, D, t->seed_mix, t->init_scale,
                 t->arena, t->last_step, t->live, t->slot_key, t->ins_seq, B.slot, t->arena_rows};
     const size_t csm = sizeof(MemberSmem);
-    if (admit_coop()) {
+    static const int graph_coop = env_int("SKB_GRAPH_COOP", 0);
+    if (admit_coop() && (!graph || graph_coop)) {
       int cg_blocks = coop_grid(csm);
       if (cg_blocks > sm_count()) cg_blocks = sm_count();  // 1 per SM: co-resides with fold+Adam
       const int64_t want = (n + 255) / 256;
@@ -1404,6 +1464,16 @@ static void fused_prepare(Table* t, const BatchArgs& a, cudaStream_t s) {
     SKB_LAUNCH_CHECK();
     sort_pairs_u32(B.slot, B.skey, B.bag, B.sval, n, bits_for((uint64_t)(t->arena_rows - 1)), x);
     prof_mark(c, P_SORT, 1, x);
+  }
+  };
+  if (graph) {
+    GraphKey k;
+    int64_t* v = k.v;
+    v[0] = t->gen; v[1] = B.gen; v[2] = (int64_t)a.ids; v[3] = n; v[4] = (int64_t)a.bag_offs; v[5] = G;
+    v[6] = a.F; v[7] = a.namespaced; v[8] = (int64_t)B.members; v[9] = t->arena_rows; v[10] = t->idmap_cap;
+    B.g_prep.run(k, x, c->cap, a.step, nullptr, work);
+  } else {
+    work(x);
   }
   table_note_inserts(t, n, x);
   SKB_CUDA(cudaEventRecord(B.ev_ready, x));
@@ -1437,6 +1507,7 @@ static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStrea
   SKB_CUDA(cudaStreamWaitEvent(s, B.ev_ready, 0));
   const int D = (int)t->dim;
   const int64_t G = B.G;
+  auto work = [&](cudaStream_t s) {
   if (G > 0) {
     prof_mark(c, P_POOL, 0, s);
     const size_t psm = sizeof(PoolSmem);
@@ -1469,6 +1540,16 @@ static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStrea
     SKB_LAUNCH_CHECK();
     prof_mark(c, P_POOL, 1, s);
   }
+  };
+  if (graph_mode(c) && G > 0) {
+    GraphKey k;
+    int64_t* v = k.v;
+    v[0] = t->gen; v[1] = B.gen; v[2] = (int64_t)pooled; v[3] = B.n; v[4] = (int64_t)B.bag_offs; v[5] = G;
+    v[6] = B.mode; v[7] = B.any_seq; v[8] = B.F; v[9] = (int64_t)B.members;
+    B.g_fwd.run(k, s, c->cap, B.step, nullptr, work);
+  } else {
+    work(s);
+  }
   c->pool_count++;
 }
 
@@ -1492,9 +1573,12 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
   BatchCtx& B = c->b[c->bwd_count % 2];
   const int64_t n = B.n;
   const int D = (int)t->dim;
+  const AdamDev a = to_dev(sc);
+  const float* dpooled_in = dpooled;
+  auto work = [&](cudaStream_t s) {
+  const float* dpooled = dpooled_in;
   if (n > 0) {
     prof_mark(c, P_ADAM, 0, s);
-    AdamDev a = to_dev(sc);
     const int64_t chunks = (n + 31) / 32;
     const bool v4 = D % 4 == 0 && (uintptr_t)dpooled % 16 == 0;
     // long mean bags: scale each bag's gradient once (the same fp32 division
@@ -1510,7 +1594,8 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     }
     // non-persistent grid (one chunk per warp): retiring blocks free SM slots
     // for the prefetched index phase of the next step
-    const unsigned grid = env_int("SKB_ADAM_PERSIST", 0) ? grid_for(chunks * 32, 256, 8)
+    static const int persist = env_int("SKB_ADAM_PERSIST", 0);
+    const unsigned grid = persist ? grid_for(chunks * 32, 256, 8)
                                                          : (unsigned)((chunks + 7) / 8);
 #define SKB_ADAM_ARGS n, B.skey, B.sval, B.bag_offs, dpooled, mode, D, a, t->arena, t->last_step, B.step, B.dev + 2, \
                       (v4 ? B.longs : nullptr), B.dev + 3, B.longs_cap
@@ -1539,6 +1624,16 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
       launch_long_fold<true>(B.longs, B.dev + 3, B.longs_cap, B.sval, dpooled, D, B.bag_offs, mode, a, t->arena,
                              t->last_step, B.step, s);
     prof_mark(c, P_ADAM, 1, s);
+  }
+  };
+  if (graph_mode(c) && n > 0) {
+    GraphKey k;
+    int64_t* v = k.v;
+    v[0] = t->gen; v[1] = B.gen; v[2] = (int64_t)dpooled; v[3] = n; v[4] = (int64_t)B.bag_offs; v[5] = B.G;
+    v[6] = B.mode;
+    B.g_bwd.run(k, s, c->cap, B.step, &a, work);
+  } else {
+    work(s);
   }
   B.last_written = true;
   SKB_CUDA(cudaEventRecord(B.ev_free, s));
@@ -1576,6 +1671,21 @@ int skb_fused_forward(skb_table_t h, const int64_t* ids, int64_t n, const int64_
 int skb_fused_backward(skb_table_t h, const float* dpooled, const skb_adam_t* scalars_host, void* stream) {
   SKB_API_BEGIN
   fused_backward(table_from(h), dpooled, *scalars_host, as_stream(stream));
+  SKB_API_END
+}
+
+int skb_fused_set_graphs(skb_table_t h, int32_t enable) {
+  SKB_API_BEGIN
+  FusedCtx* c = ctx_get(table_from(h));
+  if (enable) register_param_kernels();
+  c->graphs = enable != 0;
+  if (!c->graphs)
+    for (auto& B : c->b) {
+      B.g_prep.reset();
+      B.g_fwd.reset();
+      B.g_bwd.reset();
+      B.g_prep.primed = B.g_fwd.primed = B.g_bwd.primed = false;
+    }
   SKB_API_END
 }
 

@@ -44,6 +44,7 @@ static void grow_arena(Table* t, int64_t new_rows, cudaStream_t s) {
   grow_array(t->ins_seq, old, new_rows, s);
   grow_array(t->free_list, old, new_rows, s);
   t->arena_rows = new_rows;
+  t->gen++;
 }
 
 __global__ void k_rehash(const HEntry* __restrict__ old, int64_t old_cap, HEntry* nt, uint64_t mask, int64_t cap) {
@@ -69,6 +70,7 @@ static void rehash(Table* t, int64_t new_cap, cudaStream_t s) {
   }
   t->idmap = nt;
   t->idmap_cap = new_cap;
+  t->gen++;
 }
 
 void table_refresh(Table* t, cudaStream_t s) {
@@ -409,6 +411,7 @@ int64_t table_evict(Table* t, int64_t step, cudaStream_t s) {
   SKB_LAUNCH_CHECK();
   SKB_CUDA(cudaFreeAsync(t->idmap, s));
   t->idmap = nt;
+  t->gen++;
   table_refresh(t, s);
   return E;
 }

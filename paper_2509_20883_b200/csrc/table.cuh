@@ -26,6 +26,7 @@ struct FusedCtx;  // fused.cu
 
 struct Table {
   int64_t dim = 0, seed = 0, block_size = 0, evict_threshold = -1;
+  int64_t gen = 0;  // bumped whenever a device array is reallocated (captured graphs bake pointers)
   int device = 0;
   double init_scale = 0.0;  // 1 / sqrt(dim), host double (embedding.py:34)
   uint64_t seed_mix = 0;    // mix64(u64(seed))

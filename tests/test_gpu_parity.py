@@ -508,3 +508,59 @@ def test_fused_growth_under_async_snapshots(skb):
     for k in (0, steps - 1):
         keys = olt.keys_for("a", np.arange(k * B, (k + 1) * B, dtype=np.int64))
         eq(pooled[k], O.pool(O.lookup(olt, keys, k + 1), offs[0], "sum"))
+
+
+@pytest.mark.parametrize("mode", ["sum", "mean"])
+def test_fused_graph_mode_equals_eager(skb, mode):
+    """Graph-mode steps (capture on the 2nd call, replay with patched step /
+    Adam scalars) leave bit-identical pooled rows and table state; table
+    growth and eviction between steps re-prime the graphs."""
+    import torch
+    D, members, B = 16, ["a", "b"], 64
+    cfg = skb.AdamConfig(lr=1e-2, weight_decay=0.01, variant="adamw")
+    rng = np.random.default_rng(8)
+    specs = []
+    for k in range(9):
+        hi = 200 if k < 4 else 2000   # new ids keep arriving after step 4: growth
+        ids = [rng.integers(0, hi, 3 * B) for _ in members]
+        ids[0][: B] = 7                 # a hot id: long runs through the long fold
+        offs = [np.arange(0, 3 * B + 1, 3, dtype=np.int64) for _ in members]
+        specs.append((ids, offs, rng.standard_normal((2 * B, D)).astype(np.float32)))
+    outs = []
+    for graphs in (False, True):
+        lt = skb.LogicalTable("dim16", D, 1, seed=4, members=members, namespaced=True, evict_threshold=3)
+        skb.use_graphs(lt, graphs)
+        # fixed device buffers refilled every step: the graph-replay contract
+        bufs = [skb.PackedBatch(lt, members, specs[0][0], specs[0][1]) for _ in range(2)]
+        pooled = torch.empty((2 * B, D), device="cuda")
+        dp = torch.empty((2 * B, D), device="cuda")
+        got = []
+
+        def load(k):
+            b = bufs[k % 2]
+            b.ids.copy_(torch.from_numpy(np.concatenate(specs[k][0])).cuda())
+            return b
+
+        skb.prefetch(lt, load(0), 1, mode)
+        for k in range(9):
+            if k == 6:  # eviction: drains, rebuilds the IDMap (graphs re-prime)
+                skb.lookup_pool(lt, bufs[k % 2], k + 1, mode, out=pooled)
+                dp.copy_(torch.from_numpy(specs[k][2]).cuda())
+                skb.pool_grad_adam(lt, dp, cfg, k + 1)
+                got.append(pooled.cpu().numpy().copy())
+                lt.evict(k + 1)
+                if k + 1 < 9:
+                    skb.prefetch(lt, load(k + 1), k + 2, mode)
+                continue
+            skb.lookup_pool(lt, bufs[k % 2], k + 1, mode, out=pooled)
+            if k + 1 < 9 and k != 5:
+                skb.prefetch(lt, load(k + 1), k + 2, mode)
+            dp.copy_(torch.from_numpy(specs[k][2]).cuda())
+            skb.pool_grad_adam(lt, dp, cfg, k + 1)
+            got.append(pooled.cpu().numpy().copy())
+        ex = lt.local_table.export_rows()
+        outs.append((got, ex))
+    for a, b in zip(outs[0][0], outs[1][0]):
+        assert np.array_equal(a.view(np.int32), b.view(np.int32))
+    for x, y in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
