@@ -115,6 +115,9 @@ struct HostMailbox {
   ~HostMailbox();
 };
 
+// pinned int64[4] owned by the calling host thread (small synchronous readbacks)
+int64_t* pinned_mailbox();
+
 // Device error flag: {code, arg}; kernels record the first (lowest-index)
 // offending element with atomicMin on a packed key.
 struct DevFlag {

@@ -9,6 +9,8 @@
 // stable radix sort on the owner shard gives the stable per-shard split.  The
 // per-shard rank is written back into the scratch entry so every position's
 // inverse is one probe-free lookup (hslot cached from the insert pass).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "rows.cuh"
 #include "partition.cuh"
@@ -106,120 +108,261 @@ __global__ void k_inverse(const int64_t* __restrict__ ids, const int64_t* __rest
 }
 
 // ---------------------------------------------------------------------------
-// Stable multi-split for S <= kSplitMaxS: per-tile per-shard counts of the
-// first occurrences, one-block shard-major scan, then an in-order emit in
-// which each warp ranks its first occurrences among same-shard lanes with
-// __match_any_sync and the block keeps running per-shard cursors.  Five
-// kernels, no sort; the output order is exactly sharding.py:87-100's.
-constexpr int kSplitTile = 1024;
+// Stable multi-split for S <= kSplitMaxS in four launches, no sort, no
+// look-back spinning and no host round trip:
+//   k_part_init    table {EMPTY, INT64_MAX} + zeroed tile-done counter
+//   k_part_insert  every position claims its key's bucket and lowers the
+//                  bucket's position to its own index (one 128-bit CAS in the
+//                  common case) -> the bucket holds the key's first occurrence
+//   k_part_count   tile of kPartTile positions per block: first occurrences
+//                  ranked per owner shard inside the tile (__match_any_sync +
+//                  per-warp running counts) -> lrank[i]; per-(shard, tile)
+//                  counts; the LAST block to finish scans them shard-major
+//                  into global offsets (shard base included) and the counts
+//   k_part_emit    per position i with first occurrence f (the bucket value):
+//                  global rank = off[shard][tile(f)] + lrank[f];
+//                  inv_pos = rank - base[shard]; f == i stores the id
+// Output order is exactly sharding.py:87-100's (global first-occurrence
+// order within each shard, shards concatenated in shard order).
 constexpr int kSplitMaxS = 256;
+constexpr int kPartThreads = 256;
+constexpr int kPartRounds = 4;                             // 32-position rounds per warp
+constexpr int kPartTile = kPartThreads * kPartRounds;      // 1024 positions per tile
+constexpr int kPartU = 1;                                  // insert chains per thread
+constexpr int kScanSmem = 8192;                            // int32 staging of the tile-count scan
 
-__global__ void __launch_bounds__(256) k_split_count(const int64_t* __restrict__ ids, int64_t n, const HEntry* t,
-                                                     const int64_t* __restrict__ hslot, int S,
-                                                     int64_t* __restrict__ tile_cnt, int64_t ntiles) {
-  __shared__ int cnt[kSplitMaxS];
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    for (int k = threadIdx.x; k < S; k += blockDim.x) cnt[k] = 0;
-    __syncthreads();
-    const int64_t b = tile * kSplitTile, e = b + kSplitTile < n ? b + kSplitTile : n;
-    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x)
-      if (t[hslot[i]].val == i) atomicAdd(&cnt[S == 1 ? 0 : (int)owner_of(ids[i], (uint64_t)S)], 1);
-    __syncthreads();
-    for (int k = threadIdx.x; k < S; k += blockDim.x) tile_cnt[(int64_t)k * ntiles + tile] = cnt[k];
-    __syncthreads();
+// table fill + zeroed counters, one launch
+__global__ void k_part_init(HEntry* t, int64_t count, unsigned long long* status, int64_t nstatus) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += stride)
+    reinterpret_cast<longlong2*>(t)[i] = make_longlong2(kEmptyKey, 0x7FFFFFFFFFFFFFFFll);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nstatus; i += stride) status[i] = 0ull;
+}
+
+// 128-bit CAS on a whole {key, first position} entry (sm_90+ atom.cas.b128)
+__device__ __forceinline__ void cas_entry(HEntry* p, long long ck, long long cv, long long nk, long long nv,
+                                          long long& ok, long long& ov) {
+  asm volatile("{\n\t.reg .b128 c, n, o;\n\t"
+               "mov.b128 c, {%2, %3};\n\t"
+               "mov.b128 n, {%4, %5};\n\t"
+               "atom.global.cas.b128 o, [%6], c, n;\n\t"
+               "mov.b128 {%0, %1}, o;\n\t}"
+               : "=l"(ok), "=l"(ov)
+               : "l"(ck), "l"(cv), "l"(nk), "l"(nv), "l"(p)
+               : "memory");
+}
+
+// insert-or-lower: the bucket ends as {key, min position}.  One 128-bit CAS
+// per position in the common case (empty bucket, or the key already held by
+// an earlier position); a later-held key is lowered by re-trying with the
+// observed entry; a foreign key moves on to the next bucket.
+template <int kPartU>
+__global__ void __launch_bounds__(kPartThreads) k_part_insert(const int64_t* __restrict__ ids, int64_t n, HEntry* t,
+                                                              uint64_t mask, int64_t cap,
+                                                              uint32_t* __restrict__ hslot) {
+  constexpr long long kMaxPos = 0x7FFFFFFFFFFFFFFFll;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < n; base += stride * kPartU) {
+    long long key[kPartU], ck[kPartU], cv[kPartU];
+    uint64_t slot[kPartU];
+    bool done[kPartU];
+#pragma unroll
+    for (int u = 0; u < kPartU; ++u) {
+      const int64_t i = base + u * stride;
+      done[u] = i >= n;
+      key[u] = done[u] ? 0 : ids[i];
+      slot[u] = key[u] == kEmptyKey ? (uint64_t)cap : (bucket_hash((uint64_t)key[u]) & mask);
+      ck[u] = kEmptyKey;
+      cv[u] = kMaxPos;
+    }
+    bool more = true;
+    while (more) {  // all live chains advance one CAS per round
+      more = false;
+#pragma unroll
+      for (int u = 0; u < kPartU; ++u) {
+        if (done[u]) continue;
+        const long long i = (long long)(base + u * stride);
+        long long ok, ov;
+        if (key[u] == kEmptyKey) {  // side entry: only the position is contended
+          atomicMin(&t[cap].val, i);
+          done[u] = true;
+          continue;
+        }
+        cas_entry(&t[slot[u]], ck[u], cv[u], key[u], i, ok, ov);
+        if ((ok == ck[u] && ov == cv[u]) || (ok == key[u] && ov <= i)) {
+          done[u] = true;
+        } else if (ok == key[u]) {  // held by a later position: lower it
+          ck[u] = ok;
+          cv[u] = ov;
+          more = true;
+        } else {  // foreign key: next bucket
+          slot[u] = (slot[u] + 1) & mask;
+          ck[u] = kEmptyKey;
+          cv[u] = kMaxPos;
+          more = true;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kPartU; ++u) {
+      const int64_t i = base + u * stride;
+      if (i < n) hslot[i] = (uint32_t)slot[u];
+    }
   }
 }
 
-// exclusive scan of m values in one block (each thread owns kScanItems
-// consecutive values per pass); totals of each shard row -> counts
-constexpr int kScanItems = 8;
-__global__ void __launch_bounds__(1024) k_split_scan(int64_t* __restrict__ v, int64_t m, int64_t ntiles, int S,
-                                                    int64_t* __restrict__ counts) {
-  __shared__ int64_t s_sum[32];
-  __shared__ int64_t s_carry;
+__global__ void __launch_bounds__(kPartThreads) k_part_count(const int64_t* __restrict__ ids, int64_t n,
+                                                             const HEntry* __restrict__ t,
+                                                             const uint32_t* __restrict__ hslot, int S,
+                                                             int64_t ntiles, int* __restrict__ off,
+                                                             uint32_t* __restrict__ lrank_out,
+                                                             unsigned long long* done, int64_t* __restrict__ counts) {
+  constexpr int W = kPartThreads / 32;
+  __shared__ int sbuf[kScanSmem + kScanSmem / 32];  // wc during the tile, scan staging (padded) in the last block
+  int (*wc)[kSplitMaxS] = reinterpret_cast<int (*)[kSplitMaxS]>(sbuf);  // per-warp per-shard counts -> warp bases
+  __shared__ bool s_last;
+  for (int k = threadIdx.x; k < W * kSplitMaxS; k += blockDim.x) sbuf[k] = 0;
+  const int64_t tile = blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_carry = 0;
+  const unsigned lt_mask = (1u << lane) - 1;
+  const int64_t i0 = tile * kPartTile + (int64_t)w * (32 * kPartRounds) + lane;
+  uint32_t hs[kPartRounds];
+  long long fv[kPartRounds], key[kPartRounds];
+  int sh[kPartRounds], lr[kPartRounds];
+  // every load of the tile's rounds in flight before any warp intrinsic
+#pragma unroll
+  for (int r = 0; r < kPartRounds; ++r)
+    if (i0 + r * 32 < n) hs[r] = hslot[i0 + r * 32];
+#pragma unroll
+  for (int r = 0; r < kPartRounds; ++r) {
+    fv[r] = -1;
+    if (i0 + r * 32 < n) {
+      fv[r] = t[hs[r]].val;
+      key[r] = ids[i0 + r * 32];
+    }
+  }
   __syncthreads();
-  const int64_t per_pass = (int64_t)blockDim.x * kScanItems;
-  for (int64_t base = 0; base < m; base += per_pass) {
-    const int64_t i0 = base + (int64_t)threadIdx.x * kScanItems;
-    int64_t x[kScanItems];
-    int64_t local = 0;
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-      x[k] = i0 + k < m ? v[i0 + k] : 0;
-      local += x[k];
+  for (int r = 0; r < kPartRounds; ++r) {
+    const bool first = fv[r] == i0 + r * 32;
+    sh[r] = first ? (S == 1 ? 0 : (int)owner_of(key[r], (uint64_t)S)) : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, sh[r]);
+    const int lower = __popc(grp & lt_mask);
+    lr[r] = first ? wc[w][sh[r]] + lower : 0;
+    __syncwarp();
+    if (first && lower == 0) wc[w][sh[r]] += __popc(grp);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < S; k += blockDim.x) {  // warp bases inside the tile, tile count
+    int run = 0;
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      const int c = wc[q][k];
+      wc[q][k] = run;
+      run += c;
     }
-    int64_t incl = local;
+    off[(int64_t)k * ntiles + tile] = run;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kPartRounds; ++r)
+    if (sh[r] >= 0) lrank_out[i0 + r * 32] = (uint32_t)(wc[w][sh[r]] + lr[r]);
+  __syncthreads();  // sbuf is reused by the scan
+  // last block to finish: exclusive scan of the shard-major counts, staged
+  // through shared memory kScanSmem values at a time (all loads in flight)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(done, 1ull) == (unsigned long long)(gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int64_t m = (int64_t)S * ntiles;
+  constexpr int kPer = kScanSmem / kPartThreads;
+  __shared__ int s_sum[W];
+  int carry = 0;
+  for (int64_t b0 = 0; b0 < m; b0 += kScanSmem) {
+    const int64_t cnt = m - b0 < kScanSmem ? m - b0 : kScanSmem;
+    for (int k = threadIdx.x; k < cnt; k += kPartThreads) sbuf[k + (k >> 5)] = __ldcg(&off[b0 + k]);
+    __syncthreads();
+    int loc = 0;
+#pragma unroll 8
+    for (int k = 0; k < kPer; ++k) {
+      const int j = threadIdx.x * kPer + k;
+      loc += j < cnt ? sbuf[j + (j >> 5)] : 0;
+    }
+    int inc = loc;
     for (int o = 1; o < 32; o <<= 1) {
-      int64_t y = __shfl_up_sync(0xffffffff, incl, o);
-      if (lane >= o) incl += y;
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
     }
-    if (lane == 31) s_sum[w] = incl;
+    if (lane == 31) s_sum[w] = inc;
     __syncthreads();
-    if (w == 0) {
-      int64_t q = lane < (int)(blockDim.x >> 5) ? s_sum[lane] : 0;
-      for (int o = 1; o < 32; o <<= 1) {
-        int64_t y = __shfl_up_sync(0xffffffff, q, o);
-        if (lane >= o) q += y;
-      }
-      s_sum[lane] = q;
-    }
-    __syncthreads();
-    int64_t run = incl - local + (w ? s_sum[w - 1] : 0) + s_carry;
+    int run = carry + inc - loc;
+    int tot = 0;
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-      if (i0 + k < m) v[i0 + k] = run;
-      run += x[k];
+    for (int q = 0; q < W; ++q) {
+      const int v = s_sum[q];
+      if (q < w) run += v;
+      tot += v;
     }
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) s_carry = run;
+#pragma unroll 8
+    for (int k = 0; k < kPer; ++k) {
+      const int j = threadIdx.x * kPer + k;
+      if (j < cnt) {
+        const int x = sbuf[j + (j >> 5)];
+        off[b0 + j] = run;
+        run += x;
+      }
+    }
+    carry += tot;
     __syncthreads();
   }
   for (int k = threadIdx.x; k < S; k += blockDim.x) {
-    const int64_t start = v[(int64_t)k * ntiles];
-    const int64_t end = k + 1 < S ? v[(int64_t)(k + 1) * ntiles] : s_carry;
-    counts[k] = end - start;
+    const int b = off[(int64_t)k * ntiles];
+    const int e = k + 1 < S ? off[(int64_t)(k + 1) * ntiles] : carry;
+    counts[k] = e - b;
   }
 }
 
-__global__ void __launch_bounds__(256) k_split_emit(const int64_t* __restrict__ ids, int64_t n, HEntry* t,
-                                                    const int64_t* __restrict__ hslot, int S,
-                                                    const int64_t* __restrict__ tile_off, int64_t ntiles,
-                                                    int64_t* __restrict__ uniq) {
-  __shared__ int64_t run[kSplitMaxS];    // running output cursor per shard
-  __shared__ int64_t base0[kSplitMaxS];  // shard start in the concatenated output
-  __shared__ int wcnt[8][kSplitMaxS];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    for (int k = threadIdx.x; k < S; k += blockDim.x) {
-      run[k] = tile_off[(int64_t)k * ntiles + tile];
-      base0[k] = tile_off[(int64_t)k * ntiles];
+__global__ void __launch_bounds__(kPartThreads) k_part_emit(const int64_t* __restrict__ ids, int64_t n,
+                                                            const HEntry* __restrict__ t,
+                                                            const uint32_t* __restrict__ hslot, int S,
+                                                            int64_t ntiles, const int* __restrict__ off,
+                                                            const uint32_t* __restrict__ lrank,
+                                                            int64_t* __restrict__ uniq,
+                                                            int64_t* __restrict__ inv_shard,
+                                                            int64_t* __restrict__ inv_pos) {
+  constexpr int U = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b0 < n; b0 += stride * U) {
+    long long f[U], key[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = b0 + u * stride;
+      if (i < n) {
+        key[u] = ids[i];
+        f[u] = t[hslot[i]].val;
+      }
     }
-    const int64_t b = tile * kSplitTile, e = b + kSplitTile < n ? b + kSplitTile : n;
-    for (int64_t r0 = b; r0 < e; r0 += blockDim.x) {
-      for (int k = threadIdx.x; k < 8 * S; k += blockDim.x) (&wcnt[0][0])[(k / S) * kSplitMaxS + k % S] = 0;
-      __syncthreads();
-      const int64_t i = r0 + threadIdx.x;
-      const bool first = i < e && t[hslot[i]].val == i;
-      const int sh = first ? (S == 1 ? 0 : (int)owner_of(ids[i], (uint64_t)S)) : -1;
-      const unsigned grp = __match_any_sync(0xffffffffu, sh);
-      const int rank = __popc(grp & ((1u << lane) - 1));
-      if (first && rank == 0) wcnt[w][sh] = __popc(grp);
-      __syncthreads();
-      if (first) {
-        int64_t off = run[sh] + rank;
-        for (int q = 0; q < w; ++q) off += wcnt[q][sh];
-        uniq[off] = ids[i];
-        t[hslot[i]].val = off - base0[sh];
+    uint32_t lr[U];
+    int sh[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = b0 + u * stride;
+      if (i < n) {
+        lr[u] = lrank[f[u]];
+        sh[u] = S == 1 ? 0 : (int)owner_of(key[u], (uint64_t)S);
       }
-      __syncthreads();
-      for (int k = threadIdx.x; k < S; k += blockDim.x) {
-        int64_t tot = 0;
-        for (int q = 0; q < 8; ++q) tot += wcnt[q][k];
-        run[k] += tot;
-      }
-      __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = b0 + u * stride;
+      if (i >= n) continue;
+      const int64_t g = __ldg(&off[(int64_t)sh[u] * ntiles + f[u] / kPartTile]) + lr[u];
+      inv_pos[i] = g - __ldg(&off[(int64_t)sh[u] * ntiles]);
+      if (inv_shard) inv_shard[i] = sh[u];
+      if (f[u] == i) uniq[g] = key[u];
     }
   }
 }
@@ -257,21 +400,27 @@ void unique_partition(const int64_t* ids, int64_t n, int64_t S, int64_t* uniq, i
     SKB_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * S, s));
     return;
   }
-  if (S <= kSplitMaxS) {  // stable multi-split, no sort
-    DedupResult r;
-    dedup_insert(ids, n, r, s);
-    HEntry* t = r.table.as<HEntry>();
-    const int64_t ntiles = (n + kSplitTile - 1) / kSplitTile;
-    Scratch tc(sizeof(int64_t) * S * ntiles, s);
-    k_split_count<<<grid_for(ntiles * 256, 256), 256, 0, s>>>(ids, n, t, r.hslot.as<int64_t>(), (int)S,
-                                                              tc.as<int64_t>(), ntiles);
+  if (S <= kSplitMaxS && n < (1ll << 30)) {  // stable multi-split, no sort
+    const int64_t cap = next_pow2(n * 2 > 64 ? n * 2 : 64);
+    const int64_t ntiles = (n + kPartTile - 1) / kPartTile;
+    // one stream-ordered allocation carved into the five work arrays
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t b_t = al(sizeof(HEntry) * (cap + 1)), b_h = al(4 * n), b_o = al(sizeof(int) * ntiles * S);
+    Scratch work(b_t + 2 * b_h + b_o + 256, s);
+    HEntry* t = work.as<HEntry>();
+    uint32_t* hs = reinterpret_cast<uint32_t*>(work.as<char>() + b_t);
+    uint32_t* lr = reinterpret_cast<uint32_t*>(work.as<char>() + b_t + b_h);
+    int* off = reinterpret_cast<int*>(work.as<char>() + b_t + 2 * b_h);
+    unsigned long long* done = reinterpret_cast<unsigned long long*>(work.as<char>() + b_t + 2 * b_h + b_o);
+    k_part_init<<<grid_for(cap + 1, 256), 256, 0, s>>>(t, cap + 1, done, 1);
     SKB_LAUNCH_CHECK();
-    k_split_scan<<<1, 1024, 0, s>>>(tc.as<int64_t>(), S * ntiles, ntiles, (int)S, counts);
+    k_part_insert<kPartU><<<grid_for((n + kPartU - 1) / kPartU, kPartThreads), kPartThreads, 0, s>>>(
+        ids, n, t, (uint64_t)(cap - 1), cap, hs);
     SKB_LAUNCH_CHECK();
-    k_split_emit<<<grid_for(ntiles * 256, 256), 256, 0, s>>>(ids, n, t, r.hslot.as<int64_t>(), (int)S,
-                                                             tc.as<int64_t>(), ntiles, uniq);
+    k_part_count<<<(unsigned)ntiles, kPartThreads, 0, s>>>(ids, n, t, hs, (int)S, ntiles, off, lr, done, counts);
     SKB_LAUNCH_CHECK();
-    k_inverse<<<grid_for(n, 256), 256, 0, s>>>(ids, r.hslot.as<int64_t>(), t, n, (uint64_t)S, inv_shard, inv_pos);
+    k_part_emit<<<grid_for((n + 3) / 4, kPartThreads), kPartThreads, 0, s>>>(
+        ids, n, t, hs, (int)S, ntiles, off, lr, uniq, inv_shard, inv_pos);
     SKB_LAUNCH_CHECK();
     return;
   }

@@ -96,8 +96,13 @@ DevFlag::DevFlag(cudaStream_t st) : buf(16, st), s(st) {
   SKB_LAUNCH_CHECK();
 }
 
+int64_t* pinned_mailbox() {  // per host thread; a D2H into pageable memory is staged and slower
+  thread_local HostMailbox box(4);
+  return box.h;
+}
+
 int64_t DevFlag::read() {
-  int64_t h[2];
+  int64_t* h = pinned_mailbox();
   SKB_CUDA(cudaMemcpyAsync(h, buf.p, 16, cudaMemcpyDeviceToHost, s));
   SKB_CUDA(cudaStreamSynchronize(s));
   return (uint64_t)h[0] == ~0ull ? -1 : h[0];

@@ -270,65 +270,186 @@ static void check_live(Table* t, const int64_t* offs, int64_t n, const char* op,
   }
 }
 
-// scatter_update's checks (embedding.py:240-250) in one pass: distinctness
-// through a bitmap over the arena rows (offsets are slot numbers, so a
-// bitmap beats a hash set), liveness, range.  Reference order: duplicates
-// (ValueError) before liveness (IndexError); an out-of-range offset can only
-// be a duplicate of another out-of-range one, so that rare case re-checks
-// distinctness with the hash path before choosing the error.
-__global__ void k_scatter_check(const int64_t* __restrict__ offs, int64_t n, const uint8_t* __restrict__ live,
-                                int64_t rows, uint32_t* __restrict__ bitmap, unsigned long long* flags) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o = offs[i];
-    if (o < 0 || o >= rows) {
-      atomicMin(&flags[1], (unsigned long long)i);
-      atomicMin(&flags[2], (unsigned long long)i);
-      continue;
-    }
-    const uint32_t bit = 1u << (o & 31);
-    if (atomicOr(&bitmap[o >> 5], bit) & bit) atomicMin(&flags[0], (unsigned long long)i);
-    if (!live[o]) atomicMin(&flags[1], (unsigned long long)i);
-  }
-}
-
-static void scatter_checks(Table* t, const int64_t* offs, int64_t n, cudaStream_t s) {
-  const int64_t words = (t->arena_rows + 31) / 32 + 1;
-  Scratch bm(sizeof(uint32_t) * words, s), fl(sizeof(unsigned long long) * 3, s);
-  SKB_CUDA(cudaMemsetAsync(bm.p, 0, sizeof(uint32_t) * words, s));
-  SKB_CUDA(cudaMemsetAsync(fl.p, 0xFF, sizeof(unsigned long long) * 3, s));
-  k_scatter_check<<<grid_for(n, 256), 256, 0, s>>>(offs, n, t->live, t->arena_rows, bm.as<uint32_t>(),
-                                                   fl.as<unsigned long long>());
-  SKB_LAUNCH_CHECK();
-  unsigned long long f[3];
-  SKB_CUDA(cudaMemcpyAsync(f, fl.p, sizeof f, cudaMemcpyDeviceToHost, s));
-  SKB_CUDA(cudaStreamSynchronize(s));
-  const unsigned long long none = ~0ull;
-  const bool dup = f[2] != none ? first_duplicate(offs, n, s) >= 0 : f[0] != none;
-  if (dup) raise(SKB_E_VALUE, 0, "scatter_update requires distinct offsets");
-  if (f[1] != none) {
-    const int64_t o = read_i64(offs + (int64_t)f[1], s);
-    raise(SKB_E_INDEX, o, "scatter_update: offset %lld is not a live slot", (long long)o);
-  }
-}
-
 static int64_t reported_capacity(Table* t) {
   int64_t hw = t->known[C_ALLOC] > t->ensured_slots ? t->known[C_ALLOC] : t->ensured_slots;
   return (hw + t->block_size - 1) / t->block_size * t->block_size;
 }
 
-static void check_range(Table* t, const int64_t* offs, int64_t n, cudaStream_t s) {
-  fused_flush_pending(t, s);
+// ---------------------------------------------------------------------------
+// checked row ops without extra round trips.  Every check runs on the device
+// against the table's persistent flags and is read back once (pinned, one
+// synchronize); the store limit (BlockStore.capacity, embedding.py:83-85)
+// is computed on the device from the allocation counter, so no counter
+// refresh.  Check-then-write ops (scatter_update embedding.py:240-250,
+// BlockStore.write embedding.py:113-115) are two back-to-back launches with
+// no host round trip between them: the check kernel sets the flags, the
+// write kernel reads them on the device and writes only if nothing was
+// flagged — the table is untouched on error, as in the reference.
+//   flags[0] duplicate (min index)   flags[1] not live / out of range
+//   flags[2] out of range (scatter_update: duplicates then need the hash test)
+// ---------------------------------------------------------------------------
+constexpr unsigned long long kNoFlag = ~0ull;
+
+__device__ __forceinline__ int64_t store_limit(const int64_t* counters, int64_t ensured, int64_t bs, int64_t rows) {
+  const int64_t hw = counters[C_ALLOC] > ensured ? counters[C_ALLOC] : ensured;
+  const int64_t cap = (hw + bs - 1) / bs * bs;
+  return cap < rows ? cap : rows;
+}
+
+__global__ void k_check_range(const int64_t* __restrict__ offs, int64_t n, const int64_t* __restrict__ counters,
+                              int64_t ensured, int64_t bs, int64_t rows, unsigned long long* flags) {
+  const int64_t limit = store_limit(counters, ensured, bs, rows);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t o = offs[i];
+    if (o < 0 || o >= limit) atomicMin(&flags[1], (unsigned long long)i);
+  }
+}
+
+// MODE 0: scatter_update (distinct + live), MODE 1: BlockStore.write (range)
+template <int MODE>
+__global__ void __launch_bounds__(256) k_check_rows(const int64_t* __restrict__ offs, int64_t n,
+                                                    const uint8_t* __restrict__ live,
+                                                    const int64_t* __restrict__ counters, int64_t ensured,
+                                                    int64_t bs, int64_t rows, uint32_t* bitmap,
+                                                    unsigned long long* flags) {
+  const int64_t limit = MODE == 1 ? store_limit(counters, ensured, bs, rows) : rows;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t o = offs[i];
+    if (o < 0 || o >= limit) {
+      atomicMin(&flags[1], (unsigned long long)i);
+      if (MODE == 0) atomicMin(&flags[2], (unsigned long long)i);
+      continue;
+    }
+    if (MODE == 0) {
+      const uint32_t bit = 1u << (o & 31);
+      if (atomicOr(&bitmap[o >> 5], bit) & bit) atomicMin(&flags[0], (unsigned long long)i);
+      if (!live[o]) atomicMin(&flags[1], (unsigned long long)i);
+    }
+  }
+}
+
+// second launch of a check-then-write op: writes only if the check kernel
+// flagged nothing (read on the device — no host round trip in between), and
+// returns the distinctness bitmap to all-clear
+template <int VEC, int MODE>
+__global__ void __launch_bounds__(256) k_write_rows_if_clear(const int64_t* __restrict__ offs, int64_t n,
+                                                             const float* __restrict__ src, int D, float* dst,
+                                                             int64_t dstride, int64_t rows, uint32_t* bitmap,
+                                                             const unsigned long long* flags) {
+  const bool ok = __ldcg(&flags[0]) == kNoFlag && __ldcg(&flags[1]) == kNoFlag;
+  using V = typename VecT<VEC>::T;
+  constexpr int U = kRowsUnroll;
+  const int per_row = D / VEC;
+  const int64_t total = n * per_row;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < total; base += stride * U) {
+    int64_t r[U], row[U];
+    int col[U];
+    V v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t t = base + u * stride;
+      r[u] = -1;
+      if (t < total) {
+        row[u] = t / per_row;
+        col[u] = (int)(t - row[u] * per_row) * VEC;
+        r[u] = offs[row[u]];
+        if (MODE == 0 && col[u] == 0 && r[u] >= 0 && r[u] < rows) bitmap[r[u] >> 5] = 0u;
+        if (ok) v[u] = vload<VEC>(src + row[u] * (int64_t)D + col[u]);
+      }
+    }
+    if (ok) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (r[u] >= 0) vstore<VEC>(dst + r[u] * dstride + col[u], v[u]);
+    }
+  }
+}
+
+template <int VEC, int MODE>
+static void launch_checked_scatter(Table* t, const int64_t* offs, int64_t n, const float* src, float* dst,
+                                   cudaStream_t s) {
+  k_check_rows<MODE><<<grid_for(n, 256), 256, 0, s>>>(offs, n, t->live, t->counters, t->ensured_slots,
+                                                      t->block_size, t->arena_rows, t->bitmap, t->dflags);
+  SKB_LAUNCH_CHECK();
+  const int D = (int)t->dim;
+  k_write_rows_if_clear<VEC, MODE><<<grid_for((n * (D / VEC) + kRowsUnroll - 1) / kRowsUnroll, 256), 256, 0, s>>>(
+      offs, n, src, D, dst, 3 * t->dim, t->arena_rows, t->bitmap, t->dflags);
+  SKB_LAUNCH_CHECK();
+}
+
+// pinned readback of the persistent flags (synchronizes)
+static const int64_t* flags_fetch(Table* t, cudaStream_t s) {
+  SKB_CUDA(cudaMemcpyAsync(t->hflags, t->dflags, sizeof(int64_t) * 4, cudaMemcpyDeviceToHost, s));
+  SKB_CUDA(cudaStreamSynchronize(s));
+  return t->hflags;
+}
+static void flags_rearm(Table* t, cudaStream_t s) {
+  SKB_CUDA(cudaMemsetAsync(t->dflags, 0xFF, sizeof(unsigned long long) * 4, s));
+  SKB_CUDA(cudaStreamSynchronize(s));
+}
+
+static void ensure_bitmap(Table* t, cudaStream_t s) {
+  const int64_t words = (t->arena_rows + 31) / 32 + 1;
+  if (words <= t->bitmap_words) return;
+  if (t->bitmap) SKB_CUDA(cudaFreeAsync(t->bitmap, s));
+  SKB_CUDA(cudaMallocAsync(&t->bitmap, sizeof(uint32_t) * words, s));
+  SKB_CUDA(cudaMemsetAsync(t->bitmap, 0, sizeof(uint32_t) * words, s));
+  t->bitmap_words = words;
+}
+
+static void raise_range(Table* t, const int64_t* offs, int64_t bad, cudaStream_t s) {
+  const int64_t o = read_i64(offs + bad, s);
   table_refresh(t, s);
   int64_t lim = reported_capacity(t);
   if (lim > t->arena_rows) lim = t->arena_rows;
-  DevFlag f(s);
-  k_check_range<<<grid_for(n, 256), 256, 0, s>>>(offs, n, lim, f.ptr());
+  raise(SKB_E_INDEX, o, "offset %lld is outside the store capacity %lld", (long long)o, (long long)lim);
+}
+
+static void check_range(Table* t, const int64_t* offs, int64_t n, cudaStream_t s) {
+  fused_flush_pending(t, s);
+  k_check_range<<<grid_for(n, 256), 256, 0, s>>>(offs, n, t->counters, t->ensured_slots, t->block_size,
+                                                 t->arena_rows, t->dflags);
   SKB_LAUNCH_CHECK();
-  int64_t bad = f.read();
-  if (bad >= 0) {
-    int64_t o = read_i64(offs + bad, s);
-    raise(SKB_E_INDEX, o, "offset %lld is outside the store capacity %lld", (long long)o, (long long)lim);
+  const int64_t bad = flags_fetch(t, s)[1];
+  if ((uint64_t)bad != kNoFlag) {
+    flags_rearm(t, s);
+    raise_range(t, offs, bad, s);
   }
+}
+
+// BlockStore.write of column `which` (range-checked, one launch)
+static void checked_write(Table* t, const int64_t* offs, int64_t n, int which, const float* rows, cudaStream_t s) {
+  fused_flush_pending(t, s);
+  float* dst = t->arena + which * t->dim;
+  const bool v4 = t->dim % 4 == 0 && (uintptr_t)rows % 16 == 0;
+  if (v4) launch_checked_scatter<4, 1>(t, offs, n, rows, dst, s);
+  else launch_checked_scatter<1, 1>(t, offs, n, rows, dst, s);
+  const int64_t bad = flags_fetch(t, s)[1];
+  if ((uint64_t)bad != kNoFlag) {
+    flags_rearm(t, s);
+    raise_range(t, offs, bad, s);
+  }
+}
+
+// EmbeddingTable.scatter_update: distinct + live, then write (one launch)
+static void checked_scatter_update(Table* t, const int64_t* offs, int64_t n, const float* rows, cudaStream_t s) {
+  ensure_bitmap(t, s);
+  const bool v4 = t->dim % 4 == 0 && (uintptr_t)rows % 16 == 0;
+  if (v4) launch_checked_scatter<4, 0>(t, offs, n, rows, t->arena, s);
+  else launch_checked_scatter<1, 0>(t, offs, n, rows, t->arena, s);
+  const int64_t* f = flags_fetch(t, s);
+  const unsigned long long f0 = (uint64_t)f[0], f1 = (uint64_t)f[1], f2 = (uint64_t)f[2];
+  if (f0 == kNoFlag && f1 == kNoFlag) return;
+  flags_rearm(t, s);
+  // reference order: duplicates (ValueError) before liveness (IndexError); an
+  // out-of-range offset can only duplicate another out-of-range one, so that
+  // rare case re-checks distinctness with the hash path
+  const bool dup = f2 != kNoFlag ? first_duplicate(offs, n, s) >= 0 : f0 != kNoFlag;
+  if (dup) raise(SKB_E_VALUE, 0, "scatter_update requires distinct offsets");
+  const int64_t o = read_i64(offs + (int64_t)f1, s);
+  raise(SKB_E_INDEX, o, "scatter_update: offset %lld is not a live slot", (long long)o);
 }
 
 // ---------------------------------------------------------------------------
@@ -712,6 +833,9 @@ int skb_table_create(int64_t dim, int64_t seed, int64_t block_size, int64_t evic
   SKB_CUDA(cudaEventCreateWithFlags(&t->snap_ev, cudaEventDisableTiming));
   SKB_CUDA(cudaMalloc(&t->counters, sizeof(int64_t) * C_N));
   SKB_CUDA(cudaMemsetAsync(t->counters, 0, sizeof(int64_t) * C_N, s));
+  SKB_CUDA(cudaMalloc(&t->dflags, sizeof(unsigned long long) * 4));
+  SKB_CUDA(cudaMemsetAsync(t->dflags, 0xFF, sizeof(unsigned long long) * 4, s));
+  SKB_CUDA(cudaMallocHost(&t->hflags, sizeof(int64_t) * 4));
   int64_t rows = capacity_hint > 1024 ? capacity_hint : 1024;
   grow_arena(t, rows, s);
   rehash(t, next_pow2(rows * 2 > 2048 ? rows * 2 : 2048), s);
@@ -733,6 +857,9 @@ int skb_table_destroy(skb_table_t h) {
   cudaFree(t->free_list);
   cudaFree(t->idmap);
   cudaFree(t->counters);
+  cudaFree(t->dflags);
+  cudaFree(t->bitmap);
+  cudaFreeHost(t->hflags);
   cudaFreeHost(t->snap_host);
   cudaEventDestroy(t->snap_ev);
   if (t->fused) fused_ctx_destroy(t->fused);
@@ -795,11 +922,11 @@ int skb_table_gather(skb_table_t h, const int64_t* offsets, int64_t n, float* ro
   cudaStream_t s = as_stream(stream);
   if (n <= 0) return SKB_OK;
   const int D = (int)t->dim;
-  DevFlag f(s);
-  launch_rows_gather_checked(IdxArray{offsets}, t->arena, 3 * D, rows_out, D, n, D, t->live, t->arena_rows, f.ptr(),
-                             s);
-  const int64_t bad = f.read();
-  if (bad >= 0) {
+  launch_rows_gather_checked(IdxArray{offsets}, t->arena, 3 * D, rows_out, D, n, D, t->live, t->arena_rows,
+                             t->dflags, s);
+  const int64_t bad = flags_fetch(t, s)[0];
+  if ((uint64_t)bad != kNoFlag) {
+    flags_rearm(t, s);
     const int64_t o = read_i64(offsets + bad, s);
     raise(SKB_E_INDEX, o, "gather: offset %lld is not a live slot", (long long)o);
   }
@@ -811,9 +938,7 @@ int skb_table_scatter_update(skb_table_t h, const int64_t* offsets, int64_t n, c
   Table* t = table_from(h);
   cudaStream_t s = as_stream(stream);
   if (n <= 0) return SKB_OK;
-  scatter_checks(t, offsets, n, s);
-  const int D = (int)t->dim;
-  launch_rows_scatter(IdxArray{offsets}, rows, D, t->arena, 3 * D, n, D, s);
+  checked_scatter_update(t, offsets, n, rows, s);
   SKB_API_END
 }
 
@@ -856,9 +981,7 @@ int skb_table_write_rows(skb_table_t h, const int64_t* offsets, int64_t n, int32
   cudaStream_t s = as_stream(stream);
   if (which < 0 || which > 2) raise(SKB_E_ARG, which, "which must be 0 (w), 1 (m) or 2 (v)");
   if (n <= 0) return SKB_OK;
-  check_range(t, offsets, n, s);
-  const int D = (int)t->dim;
-  launch_rows_scatter(IdxArray{offsets}, rows, D, t->arena + which * D, 3 * D, n, D, s);
+  checked_write(t, offsets, n, which, rows, s);
   SKB_API_END
 }
 

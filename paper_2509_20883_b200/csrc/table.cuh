@@ -55,6 +55,14 @@ struct Table {
 
   FusedCtx* fused = nullptr;
 
+  // checked ops: persistent error flags (device, ~0 = clear; re-armed only
+  // after an error), their pinned readback, and a zeroed slot bitmap for
+  // scatter_update's distinctness test (cleared again by the op that set it)
+  unsigned long long* dflags = nullptr;  // [4]
+  int64_t* hflags = nullptr;             // pinned [4]
+  uint32_t* bitmap = nullptr;
+  int64_t bitmap_words = 0;
+
   int64_t row_stride() const { return 3 * dim; }
 };
 

@@ -189,6 +189,43 @@ def test_table_errors(skb):
     assert len(t.idmap) == 1
 
 
+@pytest.mark.parametrize("D", [3, 16])
+def test_checked_row_ops_leave_table_untouched_and_rearm(skb, D):
+    """scatter_update / BlockStore.write check before writing (one cooperative
+    launch): on error nothing is written, the persistent device flags and the
+    distinctness bitmap are re-armed, and repeated calls with the same
+    offsets do not see stale duplicate bits."""
+    rng = np.random.default_rng(D)
+    n = 200_000
+    t = skb.EmbeddingTable("c", D, seed=1, block_size=4096)
+    o = t.lookup_or_insert(np.arange(n, dtype=np.int64) * 7 + 3, 1)
+    before = t.gather(o)
+    perm = rng.permutation(n)
+    rows = rng.standard_normal((n, D)).astype(np.float32)
+    bad = o[perm].copy()
+    bad[n - 1] = bad[17]  # one duplicate at the end
+    with pytest.raises(ValueError, match="distinct"):
+        t.scatter_update(bad, rows)
+    eq(t.gather(o), before)
+    bad = o[perm].copy()
+    bad[5] = n + 10  # in the arena, not live
+    with pytest.raises(IndexError, match=f"scatter_update: offset {n + 10} is not a live slot"):
+        t.scatter_update(bad, rows)
+    eq(t.gather(o), before)
+    for _ in range(2):  # same offsets twice: the bitmap was cleared by the first call
+        t.scatter_update(o[perm], rows)
+        eq(t.gather(o[perm]), rows)
+    cap = t.store.capacity
+    with pytest.raises(IndexError, match="outside the store capacity"):
+        t.store.write(np.array([0, cap + 5], np.int64), np.zeros((2, D), np.float32))
+    eq(t.gather(o[perm]), rows)
+    t.store.write(o[:3], np.ones((3, D), np.float32))
+    eq(t.gather(o[:3]), np.ones((3, D), np.float32))
+    with pytest.raises(IndexError, match="gather: offset -4"):
+        t.gather(np.array([o[0], -4], np.int64))
+    eq(t.gather(o[:3]), np.ones((3, D), np.float32))
+
+
 @pytest.mark.parametrize("name", ["short", "long", "len1", "empty_all"])
 @pytest.mark.parametrize("D", [1, 3, 16])
 def test_segments(skb, golden, name, D):
