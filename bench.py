@@ -59,6 +59,11 @@ def parse():
     p.add_argument("--no-pipeline", action="store_true", help="no cross-step prefetch of the index phase")
     p.add_argument("--prefetch-late", action="store_true",
                    help="issue step k+1's index phase after step k's pool (default: before it)")
+    p.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
+                   help="c2 (default) is the headline line; c1/c3/c4/c5 measure SURVEY §8d's other configs "
+                        "on one GPU (their own JSON line each, not the headline)")
+    p.add_argument("--c3-rows", type=float, default=1.25e8,
+                   help="c3: grow the shard to this many rows (1e9 rows / 8 GPUs per GPU)")
     return p.parse_args()
 
 
@@ -617,7 +622,10 @@ def run_dist(args):
 
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.workload != "c2":
+        from bench_configs import run_config
+        run_config(args)
+    elif args.impl == "reference":
         run_reference(args)
     elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
         run_dist(args)

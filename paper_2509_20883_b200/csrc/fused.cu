@@ -32,6 +32,7 @@
 #include "common.cuh"
 #include "graph.cuh"
 #include "longfold.cuh"
+#include "tma.cuh"
 #include "pool.cuh"
 #include "table.cuh"
 
@@ -833,34 +834,6 @@ struct TmaDesc {
   uint32_t slot, bag, jh, je;
 };
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst_smem)),
-      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
 template <int kTmaRows, int kTmaThreads, int MINB>
 __global__ void __launch_bounds__(kTmaThreads, MINB) k_fused_adam_tma(int64_t n, const uint32_t* __restrict__ skey,
                                                                     const uint32_t* __restrict__ sval,
@@ -1335,13 +1308,19 @@ static bool graph_mode(const FusedCtx* c) {
 }
 
 // Admission as a chain of ordinary launches that each return at once when
-// the probe found no misses (SKB_ADMIT_COOP=0).  The default is the single
-// cooperative launch: measured on C2 warm it is 0.853 vs 0.876 ms/step
-// (early prefetch) and 0.898 vs 0.901 (late prefetch), since eight launches
-// on the index stream each queue behind the fold+Adam grid.
-static bool admit_coop() {
+// the probe found no misses, or as ONE cooperative launch.  The cooperative
+// kernel is capped at one CTA per SM so it co-resides with the previous
+// step's fold+Adam: best when there is little or nothing to admit (C2 warm:
+// 0.853 vs 0.876 ms/step, since eight launches on the index stream each
+// queue behind the fold+Adam grid), but a growth regime (C3's zipf tail:
+// ~400K new rows per step) runs 1.6x faster on the full-width phased grids.
+// SKB_ADMIT_COOP: 1 (default) adaptive on the table's recent growth, 0
+// always phased, 2 always cooperative.
+constexpr int64_t kGrowthPhased = 65536;
+static bool admit_coop(Table* t) {
   static int v = env_int("SKB_ADMIT_COOP", 1);
-  return v != 0;
+  if (v != 1) return v == 2;
+  return table_recent_growth(t) < kGrowthPhased;
 }
 
 static void launch_admission_phased(const AdmitArgs& A, size_t msm, cudaStream_t x) {
@@ -1447,7 +1426,7 @@ static void fused_prepare(Table* t, const BatchArgs& a, cudaStream_t s) {
                 t->arena, t->last_step, t->live, t->slot_key, t->ins_seq, B.slot, t->arena_rows};
     const size_t csm = sizeof(MemberSmem);
     static const int graph_coop = env_int("SKB_GRAPH_COOP", 0);
-    if (admit_coop() && (!graph || graph_coop)) {
+    if ((!graph || graph_coop) && admit_coop(t)) {
       int cg_blocks = coop_grid(csm);
       if (cg_blocks > sm_count()) cg_blocks = sm_count();  // 1 per SM: co-resides with fold+Adam
       const int64_t want = (n + 255) / 256;

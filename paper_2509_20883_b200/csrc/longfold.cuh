@@ -4,15 +4,14 @@
 // left fold in input order (sharding.py:289).  For a hot id with ~10^6
 // positions that chain is inherently serial in fp32; what must not be serial
 // is the memory traffic.  Runs longer than kLongRun are deferred by the main
-// fold kernels into a device list; here one CTA owns one long run: warps
-// 1..7 stage the run's gradient rows tile by tile into shared memory with
-// cp.async (double buffered), while warp 0 folds the previous tile from
-// shared memory in position order and finally applies Adam (or writes the
-// folded row).  Cost ~ one FADD latency per position instead of one DRAM
-// round trip.
+// fold kernels into a device list; here one CTA owns one long run at a time:
+// a producer warp streams the run's gradient rows through a TMA ring while
+// consumer warps fold them in position order (details at k_long_fold).
+// Cost ~ one FADD latency per position instead of one DRAM round trip.
 #pragma once
 #include "common.cuh"
 #include "table.cuh"
+#include "tma.cuh"
 
 namespace skb {
 
@@ -28,80 +27,141 @@ __device__ __forceinline__ void push_long_run(LongRun* list, int64_t* count, int
   if ((int64_t)i < cap) list[i] = LongRun{key, jh, je, 0};
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
-               "l"(gmem)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
+// One CTA folds one long run at a time (runs strided over CTAs).  Consumer
+// warps 0..NC-1 each own 128 columns (float4 per lane) and fold a stage's
+// rows in position order from +0; the remaining NPW warps are producers
+// filling a kLfStages-deep shared-memory ring of kLfStageBytes stages with
+// 16-byte cp.async copies of the run's gradient rows.  Producer warp pw owns
+// the stages it = pw (mod NPW), so NPW stages are being addressed (row index
+// loads) and copied at once; each lane signals the stage's `full` mbarrier
+// when ITS copies land (cp.async.mbarrier.arrive.noinc).  ~kLfStages x 16 KB
+// stay in flight per CTA and the single serial FADD chain is fed at ~one
+// row per add latency.  (Small per-row TMA bulk
+// copies were measured slower: per-copy issue cost; the earlier
+// double-buffered version was bound by one DRAM round trip per tile.)
 // rows: gradient source rows (dpooled [G, D] or per-position grads [N, D]);
-// ridx[j]: row of sorted position j; mean: divide by len(bag ridx[j]).
+// ridx[j]: row of sorted position j; mode 1 (mean): divide by len(bag ridx[j]).
 // ADAM: update arena row `key` (and last_step); else write out[key * D].
+constexpr int kLfStages = 12;
+constexpr int kLfStageBytes = 16384;
+constexpr int kLfMaxTP = 256;   // rows per stage cap (small dims)
+constexpr int kLfMaxPW = 8;     // producer warps (index buffers)
+
+// rows per stage: kLfStageBytes of rows, at most kLfMaxTP (small dims)
+__host__ __device__ inline int long_fold_tp(int D) {
+  const int tp = kLfStageBytes / (4 * D);
+  return tp < 1 ? 1 : (tp > kLfMaxTP ? kLfMaxTP : tp);
+}
+__host__ __device__ inline int long_fold_consumers(int D) { return (D + 127) / 128; }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 template <bool ADAM>
-__global__ void __launch_bounds__(256) k_long_fold(const LongRun* __restrict__ runs, const int64_t* __restrict__ nruns,
-                                                   int64_t cap, const uint32_t* __restrict__ ridx,
-                                                   const float* __restrict__ rows, int D,
-                                                   const int64_t* __restrict__ bag_offs, int mode, AdamDev a,
-                                                   float* __restrict__ out, int64_t* __restrict__ last_step,
-                                                   int64_t step) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int TP = 16384 / D;  // positions per tile: 64 KB of rows per buffer
-  float* buf = reinterpret_cast<float*>(smem_raw);                    // [2][TP][D]
-  float* lenb = buf + 2 * (int64_t)TP * D;                             // [2][TP] 1/len helpers (lengths)
+__global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __restrict__ nruns, int64_t cap,
+                            const uint32_t* __restrict__ ridx, const float* __restrict__ rows, int D,
+                            const int64_t* __restrict__ bag_offs, int mode, AdamDev a, float* __restrict__ out,
+                            int64_t* __restrict__ last_step, int64_t step) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int TP = long_fold_tp(D);
+  const int64_t stage_f = (int64_t)TP * D;  // floats per stage
+  float* buf = reinterpret_cast<float*>(smem_raw);
+  float* lens = buf + kLfStages * stage_f;
+  uint32_t* idx = reinterpret_cast<uint32_t*>(lens + kLfStages * TP);  // [kLfMaxPW][kLfMaxTP]
+  uint64_t* full = reinterpret_cast<uint64_t*>(idx + kLfMaxPW * kLfMaxTP + ((kLfStages * TP) & 1));
+  uint64_t* empty = full + kLfStages;
+  const int NC = long_fold_consumers(D);
   const int64_t R = *nruns < cap ? *nruns : cap;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int chunks = D / 4;  // 16-byte chunks per row
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kLfStages; ++s) {
+      mbar_init(&full[s], mode == 1 ? 64u : 32u);  // the owning producer warp's lanes
+      mbar_init(&empty[s], NC);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t it = 0;  // stage sequence number, identical in producers and consumers
+  if (warp >= NC) {  // ---------------- producers: warp pw fills stages it = pw (mod NPW) ----------------
+    const int pw = warp - NC, NPW = (int)(blockDim.x >> 5) - NC;
+    const int cpr = D / 4;  // 16-byte chunks per row
+    for (int64_t r = blockIdx.x; r < R; r += gridDim.x) {
+      const LongRun run = runs[r];
+      for (int64_t p0 = run.jh; p0 < run.je; p0 += TP, ++it) {
+        if ((int)(it % (uint32_t)NPW) != pw) continue;
+        const int s = (int)(it % kLfStages);
+        const uint32_t ph = (it / kLfStages) & 1u;
+        const int np = (int)((int64_t)run.je - p0 < TP ? (int64_t)run.je - p0 : TP);
+        const int items = np * cpr;
+        float* dst = buf + s * stage_f;
+        // the stage's row indices: one coalesced batch of loads per lane, staged in
+        // the warp's index buffer (a single memory latency per stage)
+        uint32_t gi[kLfMaxTP / 32];
+#pragma unroll
+        for (int k = 0; k < kLfMaxTP / 32; ++k) {
+          const int row = k * 32 + lane;
+          gi[k] = row < np ? __ldg(ridx + p0 + row) : 0u;
+        }
+        uint32_t* ix = idx + pw * kLfMaxTP;
+#pragma unroll
+        for (int k = 0; k < kLfMaxTP / 32; ++k) {
+          const int row = k * 32 + lane;
+          if (row < np) ix[row] = gi[k];
+        }
+        mbar_wait(&empty[s], ph ^ 1u);  // the stage (rows and lens) is free again
+        if (mode == 1) {
+#pragma unroll
+          for (int k = 0; k < kLfMaxTP / 32; ++k) {
+            const int row = k * 32 + lane;
+            if (row < np) lens[s * TP + row] = (float)(__ldg(bag_offs + gi[k] + 1) - __ldg(bag_offs + gi[k]));
+          }
+        }
+        __syncwarp();
+        for (int i = lane; i < items; i += 32) {
+          const int row = i / cpr, ch = i - row * cpr;
+          cp_async16(dst + (int64_t)row * D + ch * 4, rows + (int64_t)ix[row] * D + ch * 4);
+        }
+        if (mode == 1) mbar_arrive(&full[s]);  // release of the lens stores
+        cp_async_arrive_noinc(&full[s]);       // fires when this lane's copies have landed
+        __syncwarp();                          // ix is rewritten by this warp's next stage
+      }
+    }
+    return;
+  }
+  // ---------------- consumers: warp w owns columns [128 w, 128 (w+1)) ----------------
+  const int c = warp * 128 + lane * 4;
+  const bool active = c < D;
   for (int64_t r = blockIdx.x; r < R; r += gridDim.x) {
     const LongRun run = runs[r];
-    const int64_t jb = run.jh, je = run.je;
-    const int64_t ntile = (je - jb + TP - 1) / TP;
-    // stage tile t into buffer t & 1 (warps 1..7, or all warps for tile 0)
-    auto stage = [&](int64_t t, int tid0, int nthr) {
-      const int64_t p0 = jb + t * TP;
-      const int np = (int)(je - p0 < TP ? je - p0 : TP);
-      float* dst = buf + (int64_t)(t & 1) * TP * D;
-      float* ld = lenb + (int64_t)(t & 1) * TP;
-      (void)ld;
-      if (mode == 1) {  // mean: the staging warps divide, the folding warp only adds
-        for (int i = threadIdx.x - tid0; i < np * chunks; i += nthr) {
-          const int p = i / chunks, ch = i - p * chunks;
-          const uint32_t g = __ldg(ridx + p0 + p);
-          const float l = (float)(__ldg(bag_offs + g + 1) - __ldg(bag_offs + g));
-          float4 x = ldg4(rows + (int64_t)g * D + ch * 4);
-          x = make_float4(__fdiv_rn(x.x, l), __fdiv_rn(x.y, l), __fdiv_rn(x.z, l), __fdiv_rn(x.w, l));
-          st4(dst + (int64_t)p * D + ch * 4, x);
-        }
-      } else {
-        for (int i = threadIdx.x - tid0; i < np * chunks; i += nthr) {
-          const int p = i / chunks, ch = i - p * chunks;
-          const uint32_t g = __ldg(ridx + p0 + p);
-          cp_async16(dst + (int64_t)p * D + ch * 4, rows + (int64_t)g * D + ch * 4);
-        }
-      }
-      cp_async_commit();
-    };
-    stage(0, 0, blockDim.x);
-    cp_async_wait_all();
-    __syncthreads();
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int64_t t = 0; t < ntile; ++t) {
-      if (warp > 0 && t + 1 < ntile) stage(t + 1, 32, blockDim.x - 32);
-      if (warp == 0 && lane < chunks) {
-        const int64_t p0 = jb + t * TP;
-        const int np = (int)(je - p0 < TP ? je - p0 : TP);
-        const float* src = buf + (int64_t)(t & 1) * TP * D + lane * 4;
-        const float* ld = lenb + (int64_t)(t & 1) * TP;
-        (void)ld;
+    for (int64_t p0 = run.jh; p0 < run.je; p0 += TP, ++it) {
+      const int s = (int)(it % kLfStages);
+      const uint32_t ph = (it / kLfStages) & 1u;
+      const int np = (int)((int64_t)run.je - p0 < TP ? (int64_t)run.je - p0 : TP);
+      mbar_wait(&full[s], ph);
+      if (active) {
+        const float* src = buf + s * stage_f + c;
+        if (mode == 1) {
+          const float* ls = lens + s * TP;
+#pragma unroll 4
+          for (int p = 0; p < np; ++p) {
+            const float4 x = *reinterpret_cast<const float4*>(src + (int64_t)p * D);
+            const float l = ls[p];
+            acc = add4(acc, make_float4(__fdiv_rn(x.x, l), __fdiv_rn(x.y, l), __fdiv_rn(x.z, l), __fdiv_rn(x.w, l)));
+          }
+        } else {
 #pragma unroll 8
-        for (int p = 0; p < np; ++p) acc = add4(acc, *reinterpret_cast<const float4*>(src + (int64_t)p * D));
+          for (int p = 0; p < np; ++p) acc = add4(acc, *reinterpret_cast<const float4*>(src + (int64_t)p * D));
+        }
       }
-      if (warp > 0) cp_async_wait_all();
-      __syncthreads();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
     }
-    if (warp == 0 && lane < chunks) {
-      const int c = lane * 4;
+    if (active) {
       if constexpr (ADAM) {
         float* row = out + (int64_t)run.key * (3 * D);
         float4 p = *reinterpret_cast<float4*>(row + c), m = *reinterpret_cast<float4*>(row + D + c),
@@ -113,55 +173,22 @@ __global__ void __launch_bounds__(256) k_long_fold(const LongRun* __restrict__ r
         st4(row + c, p);
         st4(row + D + c, m);
         st4(row + 2 * D + c, v);
-        if (lane == 0 && step >= 0) last_step[run.key] = step;
+        if (c == 0 && step >= 0) last_step[run.key] = step;
       } else {
         st4(out + (int64_t)run.key * D + c, acc);
       }
     }
-    // D > 128 needs more lanes than warp 0 has: handled by a second pass of
-    // column groups (lanes cover 128 columns per pass)
-    for (int cbase = 128; cbase < D; cbase += 128) {
-      __syncthreads();
-      // recompute for columns [cbase, cbase + 128) by re-streaming the run
-      // (rare: only dims > 128), same order, same arithmetic
-      float4 acc2 = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (warp == 0 && cbase + lane * 4 < D) {
-        for (int64_t j = jb; j < je; ++j) {
-          const uint32_t g = __ldg(ridx + j);
-          float4 x = ldg4(rows + (int64_t)g * D + cbase + lane * 4);
-          if (mode == 1) {
-            const float l = (float)(__ldg(bag_offs + g + 1) - __ldg(bag_offs + g));
-            x = make_float4(__fdiv_rn(x.x, l), __fdiv_rn(x.y, l), __fdiv_rn(x.z, l), __fdiv_rn(x.w, l));
-          }
-          acc2 = add4(acc2, x);
-        }
-        const int c = cbase + lane * 4;
-        if constexpr (ADAM) {
-          float* row = out + (int64_t)run.key * (3 * D);
-          float4 p = *reinterpret_cast<float4*>(row + c), m = *reinterpret_cast<float4*>(row + D + c),
-                 v = *reinterpret_cast<float4*>(row + 2 * D + c);
-          adam1(p.x, m.x, v.x, acc2.x, a);
-          adam1(p.y, m.y, v.y, acc2.y, a);
-          adam1(p.z, m.z, v.z, acc2.z, a);
-          adam1(p.w, m.w, v.w, acc2.w, a);
-          st4(row + c, p);
-          st4(row + D + c, m);
-          st4(row + 2 * D + c, v);
-        } else {
-          st4(out + (int64_t)run.key * D + c, acc2);
-        }
-      }
-    }
-    __syncthreads();
   }
 }
 
 inline size_t long_fold_smem(int D) {
-  const int TP = 16384 / D;
-  return (size_t)2 * TP * D * sizeof(float) + (size_t)2 * TP * sizeof(float);
+  const int TP = long_fold_tp(D);
+  return (size_t)kLfStages * TP * D * sizeof(float) + (size_t)kLfStages * TP * sizeof(float) +
+         (size_t)(kLfMaxPW * kLfMaxTP + ((kLfStages * TP) & 1)) * sizeof(uint32_t) + 2 * kLfStages * sizeof(uint64_t);
 }
 
 // Launch the long-run pass (CTAs exit at once when the list is empty).
+// Requires D % 4 == 0 and 16-byte aligned rows (the callers' vector path).
 template <bool ADAM>
 inline void launch_long_fold(const LongRun* runs, const int64_t* nruns, int64_t cap, const uint32_t* ridx,
                              const float* rows, int D, const int64_t* bag_offs, int mode, AdamDev a, float* out,
@@ -172,10 +199,12 @@ inline void launch_long_fold(const LongRun* runs, const int64_t* nruns, int64_t 
     SKB_CUDA(cudaFuncSetAttribute(k_long_fold<ADAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     set = sm;
   }
-  int64_t grid = cap < 2 * (int64_t)sm_count() ? cap : 2 * (int64_t)sm_count();
+  const int nc = long_fold_consumers(D);
+  const int threads = 32 * (nc + (nc > 4 ? 4 : 8 - nc));  // >= 4 producer warps, <= kLfMaxPW
+  int64_t grid = cap < (int64_t)sm_count() ? cap : (int64_t)sm_count();
   if (grid < 1) grid = 1;
-  k_long_fold<ADAM><<<(unsigned)grid, 256, sm, s>>>(runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out,
-                                                    last_step, step);
+  k_long_fold<ADAM><<<(unsigned)grid, threads, sm, s>>>(runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out,
+                                                        last_step, step);
   SKB_LAUNCH_CHECK();
 }
 

@@ -23,16 +23,18 @@ __device__ __forceinline__ int64_t ht_insert_min(HEntry* t, uint64_t mask, int64
   int64_t i;
   if (key == kEmptyKey) {
     i = cap;
-  } else {
+  } else {  // read before any atomic: repeated (hot) keys find their bucket without one
     i = (int64_t)(bucket_hash((uint64_t)key) & mask);
-    while (true) {  // one atomic per probe: CAS returns the resident key
-      long long prev = (long long)atomicCAS(reinterpret_cast<unsigned long long*>(&t[i].key),
-                                            (unsigned long long)kEmptyKey, (unsigned long long)key);
-      if (prev == kEmptyKey || prev == key) break;
+    while (true) {
+      long long k = __ldcg(&t[i].key);
+      if (k == kEmptyKey)
+        k = (long long)atomicCAS(reinterpret_cast<unsigned long long*>(&t[i].key), (unsigned long long)kEmptyKey,
+                                 (unsigned long long)key);
+      if (k == kEmptyKey || k == key) break;
       i = (int64_t)(((uint64_t)i + 1) & mask);
     }
   }
-  atomicMin(&t[i].val, pos);
+  if (__ldcg(&t[i].val) > pos) atomicMin(&t[i].val, pos);
   return i;
 }
 
@@ -152,61 +154,58 @@ __device__ __forceinline__ void cas_entry(HEntry* p, long long ck, long long cv,
                : "memory");
 }
 
-// insert-or-lower: the bucket ends as {key, min position}.  One 128-bit CAS
-// per position in the common case (empty bucket, or the key already held by
-// an earlier position); a later-held key is lowered by re-trying with the
-// observed entry; a foreign key moves on to the next bucket.
+// insert-or-lower: the bucket ends as {key, min position}.  The bucket is
+// read first (L2, no atomic): a bucket already holding the key at an earlier
+// position needs no atomic at all — hot keys (zipf) would otherwise serialise
+// every occurrence on one address — and a foreign key moves on to the next
+// bucket (keys are never removed).  Otherwise one 128-bit CAS claims an empty
+// bucket or lowers a later position; a failed CAS re-examines the bucket
+// with the value it returned.
+__device__ __forceinline__ uint64_t insert_or_lower(HEntry* t, uint64_t slot, uint64_t mask, long long key,
+                                                    long long i) {
+  constexpr long long kMaxPos = 0x7FFFFFFFFFFFFFFFll;
+  longlong2 e = __ldcg(reinterpret_cast<const longlong2*>(&t[slot]));
+  while (true) {
+    if (e.x == key) {
+      if (e.y <= i) return slot;
+    } else if (e.x != kEmptyKey) {
+      slot = (slot + 1) & mask;
+      e = __ldcg(reinterpret_cast<const longlong2*>(&t[slot]));
+      continue;
+    } else {
+      e.y = kMaxPos;  // an empty bucket always holds {EMPTY, max}
+    }
+    long long ok, ov;
+    cas_entry(&t[slot], e.x, e.y, key, i, ok, ov);
+    if (ok == e.x && ov == e.y) return slot;
+    e = make_longlong2(ok, ov);
+  }
+}
+
 template <int kPartU>
 __global__ void __launch_bounds__(kPartThreads) k_part_insert(const int64_t* __restrict__ ids, int64_t n, HEntry* t,
                                                               uint64_t mask, int64_t cap,
                                                               uint32_t* __restrict__ hslot) {
-  constexpr long long kMaxPos = 0x7FFFFFFFFFFFFFFFll;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < n; base += stride * kPartU) {
-    long long key[kPartU], ck[kPartU], cv[kPartU];
-    uint64_t slot[kPartU];
-    bool done[kPartU];
+    long long key[kPartU];
 #pragma unroll
     for (int u = 0; u < kPartU; ++u) {
       const int64_t i = base + u * stride;
-      done[u] = i >= n;
-      key[u] = done[u] ? 0 : ids[i];
-      slot[u] = key[u] == kEmptyKey ? (uint64_t)cap : (bucket_hash((uint64_t)key[u]) & mask);
-      ck[u] = kEmptyKey;
-      cv[u] = kMaxPos;
+      key[u] = i < n ? ids[i] : 0;
     }
-    bool more = true;
-    while (more) {  // all live chains advance one CAS per round
-      more = false;
 #pragma unroll
-      for (int u = 0; u < kPartU; ++u) {
-        if (done[u]) continue;
-        const long long i = (long long)(base + u * stride);
-        long long ok, ov;
-        if (key[u] == kEmptyKey) {  // side entry: only the position is contended
-          atomicMin(&t[cap].val, i);
-          done[u] = true;
-          continue;
-        }
-        cas_entry(&t[slot[u]], ck[u], cv[u], key[u], i, ok, ov);
-        if ((ok == ck[u] && ov == cv[u]) || (ok == key[u] && ov <= i)) {
-          done[u] = true;
-        } else if (ok == key[u]) {  // held by a later position: lower it
-          ck[u] = ok;
-          cv[u] = ov;
-          more = true;
-        } else {  // foreign key: next bucket
-          slot[u] = (slot[u] + 1) & mask;
-          ck[u] = kEmptyKey;
-          cv[u] = kMaxPos;
-          more = true;
-        }
+    for (int u = 0; u < kPartU; ++u) {
+      const int64_t i = base + u * stride;
+      if (i >= n) continue;
+      uint64_t slot;
+      if (key[u] == kEmptyKey) {  // side entry: only the position is contended
+        slot = (uint64_t)cap;
+        if (__ldcg(&t[cap].val) > i) atomicMin(&t[cap].val, (long long)i);
+      } else {
+        slot = insert_or_lower(t, bucket_hash((uint64_t)key[u]) & mask, mask, key[u], (long long)i);
       }
-    }
-#pragma unroll
-    for (int u = 0; u < kPartU; ++u) {
-      const int64_t i = base + u * stride;
-      if (i < n) hslot[i] = (uint32_t)slot[u];
+      hslot[i] = (uint32_t)slot;
     }
   }
 }

@@ -88,11 +88,17 @@ static void harvest_snapshot(Table* t) {
     cudaGetLastError();  // clear cudaErrorNotReady
     return;
   }
+  t->recent_growth = t->snap_host[C_ROWS] - t->known[C_ROWS];
   for (int i = 0; i < C_N; ++i) t->known[i] = t->snap_host[i];
   t->snap_pending = false;
   // the snapshot covers every op enqueued before it; later ones stay pending
   t->pending_adds = t->adds_after_snap;
   t->adds_after_snap = 0;
+}
+
+int64_t table_recent_growth(Table* t) {
+  harvest_snapshot(t);
+  return t->recent_growth;
 }
 
 bool table_needs_growth(Table* t, int64_t n) {

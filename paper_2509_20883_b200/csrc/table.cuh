@@ -52,6 +52,7 @@ struct Table {
   int64_t known[C_N] = {0, 0, 0, 0};
   int64_t pending_adds = 0;      // row admissions enqueued but not covered by `known`
   int64_t adds_after_snap = 0;   // ... of which enqueued after the in-flight snapshot
+  int64_t recent_growth = 0;     // rows admitted between the last two harvested snapshots
 
   FusedCtx* fused = nullptr;
 
@@ -76,6 +77,9 @@ bool table_needs_growth(Table* t, int64_t n);
 void table_note_inserts(Table* t, int64_t n, cudaStream_t s);
 // Exact counters (synchronizes).
 void table_refresh(Table* t, cudaStream_t s);
+// Rows admitted between the two latest counter snapshots (no sync): tells a
+// growth regime (cold tables, zipf tails) from the warm steady state.
+int64_t table_recent_growth(Table* t);
 // admission of duplicate-free ids (no duplicate check), offsets out
 void table_admit(Table* t, const int64_t* ids, int64_t n, int64_t step, int64_t* offsets, cudaStream_t s);
 void fused_ctx_destroy(FusedCtx* c);
