@@ -217,9 +217,59 @@ def to_dev(x, dtype: str, device=None):
             x = x.to(dev)
         return x.contiguous()
     a = np.ascontiguousarray(np.asarray(x, dtype=np.dtype(dtype)))
+    if a.nbytes <= _H2DStaging.SLOT and dev.type == "cuda":
+        return _staging().put(a, tdt, dev)
     if not a.flags.writeable:
         a = a.copy()
     return t.from_numpy(a).to(dev)
+
+
+class _H2DStaging:
+    """Pinned ring for small host->device copies (offsets, counts, member
+    tables): a pageable copy synchronizes the stream, so every such upload
+    inside a step would stall the host behind the GPU.  Each slot is refilled
+    only after the event of its previous copy has completed."""
+
+    SLOT = 64 << 10
+    NSLOT = 64
+
+    def __init__(self):
+        t = torch()
+        self.buf = t.empty(self.SLOT * self.NSLOT, dtype=t.uint8, pin_memory=True)
+        self.host = self.buf.numpy()
+        self.events = [None] * self.NSLOT
+        self.next = 0
+        self.lock = threading.Lock()
+
+    def put(self, a: np.ndarray, tdt, dev):
+        t = torch()
+        with self.lock:
+            k = self.next
+            self.next = (k + 1) % self.NSLOT
+            if self.events[k] is not None:
+                self.events[k].synchronize()
+            lo = k * self.SLOT
+            self.host[lo:lo + a.nbytes] = a.reshape(-1).view(np.uint8)
+            src = self.buf[lo:lo + a.nbytes].view(tdt).reshape(a.shape)
+            out = t.empty(a.shape, dtype=tdt, device=dev)
+            out.copy_(src, non_blocking=True)
+            ev = t.cuda.Event()
+            ev.record()
+            self.events[k] = ev
+        return out
+
+
+_STAGING = None
+_STAGING_LOCK = threading.Lock()
+
+
+def _staging() -> _H2DStaging:
+    global _STAGING
+    if _STAGING is None:
+        with _STAGING_LOCK:
+            if _STAGING is None:
+                _STAGING = _H2DStaging()
+    return _STAGING
 
 
 def empty(shape, dtype: str, device=None):

@@ -74,6 +74,8 @@ struct BatchCtx {
   MemberDev* members = nullptr;
   int64_t members_cap = 0;
   std::vector<MemberDev> members_host;
+  MemberDev* members_pinned = nullptr;  // upload staging (ragged batches change it every step)
+  cudaEvent_t members_ev = nullptr;     // the staging buffer's last upload
   // identity + metadata of the prepared batch
   const int64_t* ids = nullptr;
   const int64_t* bag_offs = nullptr;
@@ -121,6 +123,8 @@ static void batch_free(BatchCtx& B) {
   cudaFree(B.scratch);
   cudaFree(B.dev);
   cudaFree(B.members);
+  if (B.members_pinned) cudaFreeHost(B.members_pinned);
+  if (B.members_ev) cudaEventDestroy(B.members_ev);
   cudaFree(B.longs);
   if (B.ev_ready) cudaEventDestroy(B.ev_ready);
   if (B.ev_free) cudaEventDestroy(B.ev_free);
@@ -194,6 +198,10 @@ static void batch_reserve(BatchCtx& B, int64_t n, int64_t F, cudaStream_t s) {
   }
   if (F + 1 > B.members_cap) {
     realloc_dev(B.members, F + 1, s);
+    if (B.members_ev) SKB_CUDA(cudaEventSynchronize(B.members_ev));
+    if (B.members_pinned) SKB_CUDA(cudaFreeHost(B.members_pinned));
+    SKB_CUDA(cudaMallocHost(&B.members_pinned, sizeof(MemberDev) * (F + 1)));
+    if (!B.members_ev) SKB_CUDA(cudaEventCreateWithFlags(&B.members_ev, cudaEventDisableTiming));
     B.members_cap = F + 1;
     B.members_host.clear();
     B.gen++;
@@ -1403,8 +1411,12 @@ static void fused_prepare(Table* t, const BatchArgs& a, cudaStream_t s) {
     if (f < a.F) any_seq |= a.strategy[f] == 0;
   }
   if (B.members_host.size() != mh.size() || memcmp(B.members_host.data(), mh.data(), sizeof(MemberDev) * mh.size())) {
-    SKB_CUDA(cudaMemcpyAsync(B.members, mh.data(), sizeof(MemberDev) * mh.size(), cudaMemcpyHostToDevice, x));
-    SKB_CUDA(cudaStreamSynchronize(x));  // pageable source; rare (layout change)
+    // stream-ordered upload through pinned staging (no host sync): the side
+    // stream already waited for this batch buffer's previous backward
+    SKB_CUDA(cudaEventSynchronize(B.members_ev));  // the staging copy of the previous upload has run
+    memcpy(B.members_pinned, mh.data(), sizeof(MemberDev) * mh.size());
+    SKB_CUDA(cudaMemcpyAsync(B.members, B.members_pinned, sizeof(MemberDev) * mh.size(), cudaMemcpyHostToDevice, x));
+    SKB_CUDA(cudaEventRecord(B.members_ev, x));
     B.members_host = mh;
   }
   const MemberDev* mt = B.members;

@@ -9,6 +9,8 @@
 // consumer warps fold them in position order (details at k_long_fold).
 // Cost ~ one FADD latency per position instead of one DRAM round trip.
 #pragma once
+#include <cstdlib>
+
 #include "common.cuh"
 #include "table.cuh"
 #include "tma.cuh"
@@ -65,21 +67,20 @@ template <bool ADAM>
 __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __restrict__ nruns, int64_t cap,
                             const uint32_t* __restrict__ ridx, const float* __restrict__ rows, int D,
                             const int64_t* __restrict__ bag_offs, int mode, AdamDev a, float* __restrict__ out,
-                            int64_t* __restrict__ last_step, int64_t step) {
+                            int64_t* __restrict__ last_step, int64_t step, int nst) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int TP = long_fold_tp(D);
   const int64_t stage_f = (int64_t)TP * D;  // floats per stage
   float* buf = reinterpret_cast<float*>(smem_raw);
-  float* lens = buf + kLfStages * stage_f;
-  uint32_t* idx = reinterpret_cast<uint32_t*>(lens + kLfStages * TP);  // [kLfMaxPW][kLfMaxTP]
-  uint64_t* full = reinterpret_cast<uint64_t*>(idx + kLfMaxPW * kLfMaxTP + ((kLfStages * TP) & 1));
+  uint32_t* idx = reinterpret_cast<uint32_t*>(buf + kLfStages * stage_f);  // [kLfMaxPW][kLfMaxTP]
+  uint64_t* full = reinterpret_cast<uint64_t*>(idx + kLfMaxPW * kLfMaxTP);
   uint64_t* empty = full + kLfStages;
   const int NC = long_fold_consumers(D);
   const int64_t R = *nruns < cap ? *nruns : cap;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kLfStages; ++s) {
-      mbar_init(&full[s], mode == 1 ? 64u : 32u);  // the owning producer warp's lanes
+      mbar_init(&full[s], 32);  // the owning producer warp's lanes
       mbar_init(&empty[s], NC);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -93,8 +94,8 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
       const LongRun run = runs[r];
       for (int64_t p0 = run.jh; p0 < run.je; p0 += TP, ++it) {
         if ((int)(it % (uint32_t)NPW) != pw) continue;
-        const int s = (int)(it % kLfStages);
-        const uint32_t ph = (it / kLfStages) & 1u;
+        const int s = (int)(it % (uint32_t)nst);
+        const uint32_t ph = (it / (uint32_t)nst) & 1u;
         const int np = (int)((int64_t)run.je - p0 < TP ? (int64_t)run.je - p0 : TP);
         const int items = np * cpr;
         float* dst = buf + s * stage_f;
@@ -112,21 +113,42 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
           const int row = k * 32 + lane;
           if (row < np) ix[row] = gi[k];
         }
-        mbar_wait(&empty[s], ph ^ 1u);  // the stage (rows and lens) is free again
+        __syncwarp();                   // ix visible to the whole warp
+        mbar_wait(&empty[s], ph ^ 1u);  // the stage is free again
         if (mode == 1) {
+          // mean bags: the producer divides by the bag length (x / len, exactly
+          // the reference's per-position grad) so the fold chain stays one FADD
+          for (int b = lane; b < items; b += 4 * 32) {
+            float4 x[4];
+            float l[4];
 #pragma unroll
-          for (int k = 0; k < kLfMaxTP / 32; ++k) {
-            const int row = k * 32 + lane;
-            if (row < np) lens[s * TP + row] = (float)(__ldg(bag_offs + gi[k] + 1) - __ldg(bag_offs + gi[k]));
+            for (int k = 0; k < 4; ++k) {
+              const int i = b + k * 32;
+              if (i < items) {
+                const int row = i / cpr, ch = i - row * cpr;
+                const uint32_t gg = ix[row];
+                x[k] = ldg4(rows + (int64_t)gg * D + ch * 4);
+                l[k] = (float)(__ldg(bag_offs + gg + 1) - __ldg(bag_offs + gg));
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int i = b + k * 32;
+              if (i < items) {
+                const int row = i / cpr, ch = i - row * cpr;
+                st4(dst + (int64_t)row * D + ch * 4, make_float4(__fdiv_rn(x[k].x, l[k]), __fdiv_rn(x[k].y, l[k]),
+                                                                 __fdiv_rn(x[k].z, l[k]), __fdiv_rn(x[k].w, l[k])));
+              }
+            }
           }
+          mbar_arrive(&full[s]);  // release of this lane's stores
+        } else {
+          for (int i = lane; i < items; i += 32) {
+            const int row = i / cpr, ch = i - row * cpr;
+            cp_async16(dst + (int64_t)row * D + ch * 4, rows + (int64_t)ix[row] * D + ch * 4);
+          }
+          cp_async_arrive_noinc(&full[s]);  // fires when this lane's copies have landed
         }
-        __syncwarp();
-        for (int i = lane; i < items; i += 32) {
-          const int row = i / cpr, ch = i - row * cpr;
-          cp_async16(dst + (int64_t)row * D + ch * 4, rows + (int64_t)ix[row] * D + ch * 4);
-        }
-        if (mode == 1) mbar_arrive(&full[s]);  // release of the lens stores
-        cp_async_arrive_noinc(&full[s]);       // fires when this lane's copies have landed
         __syncwarp();                          // ix is rewritten by this warp's next stage
       }
     }
@@ -139,24 +161,14 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
     const LongRun run = runs[r];
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int64_t p0 = run.jh; p0 < run.je; p0 += TP, ++it) {
-      const int s = (int)(it % kLfStages);
-      const uint32_t ph = (it / kLfStages) & 1u;
+      const int s = (int)(it % (uint32_t)nst);
+      const uint32_t ph = (it / (uint32_t)nst) & 1u;
       const int np = (int)((int64_t)run.je - p0 < TP ? (int64_t)run.je - p0 : TP);
       mbar_wait(&full[s], ph);
       if (active) {
         const float* src = buf + s * stage_f + c;
-        if (mode == 1) {
-          const float* ls = lens + s * TP;
-#pragma unroll 4
-          for (int p = 0; p < np; ++p) {
-            const float4 x = *reinterpret_cast<const float4*>(src + (int64_t)p * D);
-            const float l = ls[p];
-            acc = add4(acc, make_float4(__fdiv_rn(x.x, l), __fdiv_rn(x.y, l), __fdiv_rn(x.z, l), __fdiv_rn(x.w, l)));
-          }
-        } else {
 #pragma unroll 8
-          for (int p = 0; p < np; ++p) acc = add4(acc, *reinterpret_cast<const float4*>(src + (int64_t)p * D));
-        }
+        for (int p = 0; p < np; ++p) acc = add4(acc, *reinterpret_cast<const float4*>(src + (int64_t)p * D));
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -183,8 +195,8 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
 
 inline size_t long_fold_smem(int D) {
   const int TP = long_fold_tp(D);
-  return (size_t)kLfStages * TP * D * sizeof(float) + (size_t)kLfStages * TP * sizeof(float) +
-         (size_t)(kLfMaxPW * kLfMaxTP + ((kLfStages * TP) & 1)) * sizeof(uint32_t) + 2 * kLfStages * sizeof(uint64_t);
+  return (size_t)kLfStages * TP * D * sizeof(float) + (size_t)kLfMaxPW * kLfMaxTP * sizeof(uint32_t) +
+         2 * kLfStages * sizeof(uint64_t);
 }
 
 // Launch the long-run pass (CTAs exit at once when the list is empty).
@@ -200,11 +212,16 @@ inline void launch_long_fold(const LongRun* runs, const int64_t* nruns, int64_t 
     set = sm;
   }
   const int nc = long_fold_consumers(D);
-  const int threads = 32 * (nc + (nc > 4 ? 4 : 8 - nc));  // >= 4 producer warps, <= kLfMaxPW
+  static const int env_pw = getenv("SKB_LF_PW") ? atoi(getenv("SKB_LF_PW")) : 0;
+  static const int env_st = getenv("SKB_LF_STAGES") ? atoi(getenv("SKB_LF_STAGES")) : kLfStages;
+  const int npw = env_pw > 0 && env_pw <= kLfMaxPW ? env_pw : (nc > 4 ? 4 : 8 - nc);  // >= 4 producer warps
+  const int threads = 32 * (nc + npw);
+  int nst = env_st >= 2 && env_st <= kLfStages ? env_st : kLfStages;
+  if (nst < npw) nst = npw;  // a producer warp must never get a full ring lap ahead (parity waits)
   int64_t grid = cap < (int64_t)sm_count() ? cap : (int64_t)sm_count();
   if (grid < 1) grid = 1;
   k_long_fold<ADAM><<<(unsigned)grid, threads, sm, s>>>(runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out,
-                                                        last_step, step);
+                                                        last_step, step, nst);
   SKB_LAUNCH_CHECK();
 }
 

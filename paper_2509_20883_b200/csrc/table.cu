@@ -101,20 +101,29 @@ int64_t table_recent_growth(Table* t) {
   return t->recent_growth;
 }
 
-bool table_needs_growth(Table* t, int64_t n) {
-  harvest_snapshot(t);
-  int64_t ub_alloc = t->known[C_ALLOC] + t->pending_adds + n;
-  int64_t ub_rows = t->known[C_ROWS] + t->pending_adds + n;
-  return !(ub_alloc <= t->arena_rows && ub_rows * 10 < t->idmap_cap * 9);
+static bool bound_ok(const Table* t, int64_t n) {
+  const int64_t ub_alloc = t->known[C_ALLOC] + t->pending_adds + n;
+  const int64_t ub_rows = t->known[C_ROWS] + t->pending_adds + n;
+  return ub_alloc <= t->arena_rows && ub_rows * 10 < t->idmap_cap * 9;  // never fill the probe table
 }
 
-void table_reserve(Table* t, int64_t n, cudaStream_t s) {
+// The no-sync bound counts every position of the steps enqueued since the
+// last harvested snapshot as a possible new row.  When it fails, first wait
+// for the in-flight snapshot only (a step or so behind the host, not a full
+// drain of the queue) and re-check; only then does the caller refresh.
+static bool bound_ok_after_snapshot(Table* t, int64_t n) {
   harvest_snapshot(t);
-  int64_t ub_alloc = t->known[C_ALLOC] + t->pending_adds + n;
-  int64_t ub_rows = t->known[C_ROWS] + t->pending_adds + n;
-  bool arena_ok = ub_alloc <= t->arena_rows;
-  bool map_ok = ub_rows * 10 < t->idmap_cap * 9;  // hard bound: never fill the probe table
-  if (arena_ok && map_ok) return;
+  if (bound_ok(t, n)) return true;
+  if (!t->snap_pending) return false;
+  SKB_CUDA(cudaEventSynchronize(t->snap_ev));
+  harvest_snapshot(t);
+  return bound_ok(t, n);
+}
+
+bool table_needs_growth(Table* t, int64_t n) { return !bound_ok_after_snapshot(t, n); }
+
+void table_reserve(Table* t, int64_t n, cudaStream_t s) {
+  if (bound_ok_after_snapshot(t, n)) return;
   table_refresh(t, s);
   int64_t need_alloc = t->known[C_ALLOC] + n;
   int64_t need_rows = t->known[C_ROWS] + n;

@@ -89,22 +89,48 @@ def mod_transform(ids: RaggedTensor, modulus: int) -> RaggedTensor:
 def cross(a: RaggedTensor, b: RaggedTensor) -> RaggedTensor:
     """Per-row x-major Cartesian product hashed pairwise (features.py:65-89)."""
     telemetry.bump("features.cross")
-    if a.num_rows != b.num_rows:
-        raise ValueError(f"row-count mismatch: {a.num_rows} vs {b.num_rows}")
-    as_np = not N.is_torch(a.values)
-    av, bv = N.to_dev(a.values, "int64").reshape(-1), N.to_dev(b.values, "int64").reshape(-1)
-    ao, bo = N.to_dev(a.row_offsets, "int64"), N.to_dev(b.row_offsets, "int64")
-    rows = a.num_rows
-    oo = N.empty((rows + 1,), "int64")
-    N.call("skb_cross_offsets", N.ptr(ao), N.ptr(bo), rows, N.ptr(oo), N.stream_ptr())
-    total = int(oo[-1].item())
-    out = N.empty((total,), "int64")
-    if total:
-        N.call("skb_cross", N.ptr(av), N.ptr(ao), N.ptr(bv), N.ptr(bo), rows, N.ptr(oo), total, N.ptr(out),
-               N.stream_ptr())
-    if as_np:
-        return RaggedTensor(out.cpu().numpy(), oo.cpu().numpy())
-    return RaggedTensor(out, oo)
+    return _cross_pairs([(a, b)])[0]
+
+
+def cross_many(pairs, sizes=None) -> list:
+    """`cross` over many column pairs with ONE host read of the output sizes
+    (a step's crossed features: offsets for every pair, one readback of all
+    totals, then one hashing launch per pair).  `sizes`: the output lengths
+    (sum over rows of len_a * len_b) when the caller already knows them from
+    host-side offsets (e.g. the input pipeline) — then nothing synchronizes."""
+    telemetry.bump("features.cross", len(pairs))
+    return _cross_pairs(list(pairs), sizes)
+
+
+def _cross_pairs(pairs, sizes=None):
+    t = N.torch()
+    prep = []
+    for a, b in pairs:
+        if a.num_rows != b.num_rows:
+            raise ValueError(f"row-count mismatch: {a.num_rows} vs {b.num_rows}")
+        as_np = not N.is_torch(a.values)
+        av, bv = N.to_dev(a.values, "int64").reshape(-1), N.to_dev(b.values, "int64").reshape(-1)
+        ao, bo = N.to_dev(a.row_offsets, "int64"), N.to_dev(b.row_offsets, "int64")
+        rows = a.num_rows
+        oo = N.empty((rows + 1,), "int64")
+        N.call("skb_cross_offsets", N.ptr(ao), N.ptr(bo), rows, N.ptr(oo), N.stream_ptr())
+        prep.append((as_np, av, ao, bv, bo, rows, oo))
+    if not prep:
+        return []
+    if sizes is not None:
+        if len(sizes) != len(prep):
+            raise ValueError(f"{len(sizes)} sizes for {len(prep)} column pairs")
+        totals = [int(x) for x in sizes]
+    else:
+        totals = t.stack([p[6][-1] for p in prep]).cpu().tolist()  # the single synchronisation
+    res = []
+    for (as_np, av, ao, bv, bo, rows, oo), total in zip(prep, totals):
+        out = N.empty((int(total),), "int64")
+        if total:
+            N.call("skb_cross", N.ptr(av), N.ptr(ao), N.ptr(bv), N.ptr(bo), rows, N.ptr(oo), int(total), N.ptr(out),
+                   N.stream_ptr())
+        res.append(RaggedTensor(out.cpu().numpy(), oo.cpu().numpy()) if as_np else RaggedTensor(out, oo))
+    return res
 
 
 class FusedPlan:

@@ -44,9 +44,15 @@ class PackedBatch:
             self.member_pos[f + 1] = self.member_pos[f] + ids_d[f].numel()
             self.member_bag[f + 1] = self.member_bag[f] + offs_d[f].numel() - 1
         self.ids = t.cat(ids_d).contiguous() if F > 1 else ids_d[0]
-        shifted = [offs_d[f][:-1] + int(self.member_pos[f]) for f in range(F)]
-        shifted.append(N.to_dev(np.array([self.member_pos[F]], np.int64), "int64"))
-        self.bag_offs = t.cat(shifted).contiguous()
+        # members' bag offsets shifted by their first position, in three launches
+        # and no host round trip: cat(offs_f[:-1], 0) + repeat(member_pos, bags_f (+1))
+        G = int(self.member_bag[F])
+        dev = self.ids.device
+        heads = t.cat([o[:-1] for o in offs_d] + [t.zeros(1, dtype=t.int64, device=dev)])
+        reps = np.append(np.diff(self.member_bag), 1).astype(np.int64)
+        shift = t.repeat_interleave(N.to_dev(self.member_pos, "int64", dev), N.to_dev(reps, "int64", dev),
+                                    output_size=G + 1)
+        self.bag_offs = (heads + shift).contiguous()
         self.salts = np.array([lt.salt(m) if lt.namespaced else 0 for m in self.members], np.uint64)
         self.strategy = np.array(
             [0 if resolve_strategy(strategy, int(self.member_pos[f + 1] - self.member_pos[f]),

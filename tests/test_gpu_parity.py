@@ -345,6 +345,29 @@ def test_features(skb, golden):
     eq(h.values, golden["fnv.hash"])
 
 
+def test_cross_many(skb, golden, cuda):
+    """cross_many == cross per pair, with the sizes read back or given."""
+    import torch
+    rng = np.random.default_rng(11)
+    pairs, sizes = [], []
+    for _ in range(5):
+        la, lb = rng.integers(0, 6, 300), rng.integers(0, 6, 300)
+        oa = np.concatenate([[0], np.cumsum(la)]).astype(np.int64)
+        ob = np.concatenate([[0], np.cumsum(lb)]).astype(np.int64)
+        a = skb.RaggedTensor(torch.from_numpy(rng.integers(-50, 50, oa[-1])).to(cuda), torch.from_numpy(oa).to(cuda))
+        b = skb.RaggedTensor(torch.from_numpy(rng.integers(0, 10**12, ob[-1])).to(cuda), torch.from_numpy(ob).to(cuda))
+        pairs.append((a, b))
+        sizes.append(int((la * lb).sum()))
+    for res in (skb.cross_many(pairs), skb.cross_many(pairs, sizes=sizes)):
+        for (a, b), c in zip(pairs, res):
+            ov, oo = O.cross_rows(a.values.cpu().numpy(), a.row_offsets.cpu().numpy(), b.values.cpu().numpy(),
+                                  b.row_offsets.cpu().numpy())
+            eq(c.values, ov)
+            eq(c.row_offsets, oo)
+    with pytest.raises(ValueError, match="sizes"):
+        skb.cross_many(pairs, sizes=sizes[:2])
+
+
 def test_ragged(skb, golden):
     rr = skb.RaggedTensor(np.arange(20, dtype=np.int64), np.array([0, 5, 5, 12, 20]))
     t3 = rr.truncate(3, "tail")
