@@ -1304,7 +1304,7 @@ static void register_param_kernels() {
   note_param_kernel((const void*)k_fused_adam<4, 2, 4>, 15, 7, 10);
   note_param_kernel((const void*)k_fused_adam<4, 1, 5>, 15, 7, 10);
   note_param_kernel((const void*)k_fused_adam<4, 1, 4>, 15, 7, 10);
-  note_param_kernel((const void*)k_long_fold<true>, 12, 8, 11);
+  note_param_kernel((const void*)k_long_fold<true>, 13, 8, 11);  // (runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out, last_step, step, nst)
 }
 
 // graph mode is off while per-phase event profiling is on (events cannot be
