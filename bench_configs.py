@@ -253,7 +253,6 @@ def c4(args):
     G, L, D = 8192, 1000, 64
     n = G * L
     lt = skb.LogicalTable("seq", D, 1, seed=4, members=["seq"], namespaced=False, capacity_hint=3_000_000)
-    plan = skb.ShardPlan(1)
     offs_d = torch.arange(0, n + 1, L, dtype=torch.int64, device="cuda")
     P = 2
     ids = [torch.from_numpy(np.random.Generator(np.random.PCG64(4 + k)).zipf(1.1, n).astype(np.int64)).cuda()
@@ -261,10 +260,24 @@ def c4(args):
     dtile = torch.randn((G, L * D), device="cuda") * 1e-2
     cfg = skb.AdamConfig(lr=1e-3, weight_decay=0.01, variant="adamw")
     step = [0]
+    fused = not args.no_pipeline  # --no-pipeline: the drop-in API path instead of the fused step
+    if fused:
+        # truncate(1000, "tail") keeps every length-1000 sequence whole: the
+        # fused tile combiner then reads each bag's first k = 1000 rows
+        batches = []
+        for k in range(P):
+            x = skb.RaggedTensor(ids[k], offs_d).truncate(L, "tail")
+            batches.append(skb.PackedBatch(lt, ["seq"], [x.values], [x.row_offsets]))
+        tiles = torch.empty((G, L * D), device="cuda")
+    plan = skb.ShardPlan(1)
 
     def run(count):
-        for k in range(count):
+        for _ in range(count):
             step[0] += 1
+            if fused:
+                skb.lookup_pool(lt, batches[step[0] % P], step[0], "tile", out=tiles, k=L, pad=0.0)
+                skb.pool_grad_adam(lt, dtile, cfg, step[0])
+                continue
             x = skb.RaggedTensor(ids[step[0] % P], offs_d).truncate(L, "tail")
             rows = skb.all_to_all_lookup(lt, x.values, plan, step[0])
             skb.segment_tile(rows, x.row_offsets, L, pad=0.0)
@@ -301,8 +314,9 @@ def c4(args):
                "sample": f"C4 scaled to batch {cg} ({cg * L} ids/step), 2 steps median; effective cores {cores}"}
     _line(args, "c4", n / (ms / 1e3), ms, n, G, sb, cpu,
           {"workload": "C4: 8192 sequences x length 1000, zipf(1.1) ids, dim64, truncate(1000,'tail') + "
-                       "segment_tile(k=1000) -> [8192, 64000], tile-gradient backward + SparseAdamW (drop-in "
-                       "API path: all_to_all_lookup -> segment_tile -> all_to_all_grad_update)",
+                       "segment_tile(k=1000) -> [8192, 64000], tile-gradient backward + SparseAdamW; "
+                       + ("fused step, tile combiner" if fused else
+                          "drop-in API path: all_to_all_lookup -> segment_tile -> all_to_all_grad_update"),
            "global_batch": G, "seq_len": L, "dim": D, "parallelism": "single shard",
            "l2": "inputs larger than L2 (2.1 GB tile per step)"},
           {"unique_rows_per_step": u})

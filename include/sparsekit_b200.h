@@ -212,6 +212,20 @@ int skb_fused_prepare(skb_table_t t, const int64_t* ids, int64_t n, const int64_
                       const uint64_t* salts_host, int32_t num_members, int32_t namespaced,
                       const int64_t* bag_offs, int64_t num_bags, const int64_t* member_bag_host,
                       const int32_t* strategy_host, int32_t mode, int64_t step, void* stream);
+/* Tile combiner (segment_tile, segments.py:94-116) on the fused path: the
+ * forward writes tiles_out[G, k*dim] (the first min(len, k) rows of each bag,
+ * `pad` after them); skb_fused_backward then takes dtiles [G, k*dim] and
+ * folds each position's tile row (zero past k) in position order before
+ * SparseAdam/AdamW — identical to segment_tile + the per-position gradient
+ * expansion + all_to_all_grad_update.  Same prefetch rules as above. */
+int skb_fused_prepare_tile(skb_table_t t, const int64_t* ids, int64_t n, const int64_t* member_pos_host,
+                           const uint64_t* salts_host, int32_t num_members, int32_t namespaced,
+                           const int64_t* bag_offs, int64_t num_bags, const int64_t* member_bag_host, int64_t k,
+                           float pad, int64_t step, void* stream);
+int skb_fused_forward_tile(skb_table_t t, const int64_t* ids, int64_t n, const int64_t* member_pos_host,
+                           const uint64_t* salts_host, int32_t num_members, int32_t namespaced,
+                           const int64_t* bag_offs, int64_t num_bags, const int64_t* member_bag_host, int64_t k,
+                           float pad, int64_t step, float* tiles_out, void* stream);
 /* Backward of the oldest pooled, not yet backwarded fused batch. */
 int skb_fused_backward(skb_table_t t, const float* dpooled, const skb_adam_t* scalars_host,
                        void* stream);

@@ -77,6 +77,10 @@ _SIGS = {
                            ctypes.POINTER(_i64), ctypes.POINTER(_i32), _i32, _i64, _p, _p], ctypes.c_int),
     "skb_fused_prepare": ([_p, _p, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_u64), _i32, _i32, _p, _i64,
                            ctypes.POINTER(_i64), ctypes.POINTER(_i32), _i32, _i64, _p], ctypes.c_int),
+    "skb_fused_prepare_tile": ([_p, _p, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_u64), _i32, _i32, _p, _i64,
+                                ctypes.POINTER(_i64), _i64, ctypes.c_float, _i64, _p], ctypes.c_int),
+    "skb_fused_forward_tile": ([_p, _p, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_u64), _i32, _i32, _p, _i64,
+                                ctypes.POINTER(_i64), _i64, ctypes.c_float, _i64, _p, _p], ctypes.c_int),
     "skb_fused_backward": ([_p, _p, ctypes.POINTER(AdamScalars), _p], ctypes.c_int),
     "skb_fused_last_unique": ([_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p], ctypes.c_int),
     "skb_fused_stats_async": ([_p, _p, _p], ctypes.c_int),

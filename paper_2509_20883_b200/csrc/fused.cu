@@ -80,6 +80,8 @@ struct BatchCtx {
   const int64_t* ids = nullptr;
   const int64_t* bag_offs = nullptr;
   int64_t n = 0, G = 0, step = -1;
+  int64_t tile_k = 0;  // mode 2: tile width (rows per bag)
+  float pad = 0.f;
   int F = 0, mode = 0;
   bool any_seq = false;
   bool last_written = false;  // deferred last_step already flushed
@@ -91,6 +93,7 @@ struct BatchCtx {
 
 struct FusedCtx {
   cudaStream_t side = nullptr;  // index stream: probe, admission, bag-of, sort
+  float* zrow = nullptr;        // D zeros: the gradient row of tile positions past k
   cudaEvent_t ev_in = nullptr, ev_side_last = nullptr;
   BatchCtx b[2];
   int64_t prep_count = 0, pool_count = 0, bwd_count = 0;
@@ -143,6 +146,7 @@ void fused_ctx_destroy(FusedCtx* c) {
   }
   if (c->side) cudaStreamDestroy(c->side);
   if (c->cap) cudaStreamDestroy(c->cap);
+  cudaFree(c->zrow);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
   if (c->ev_side_last) cudaEventDestroy(c->ev_side_last);
   delete c;
@@ -172,6 +176,8 @@ static FusedCtx* ctx_get(Table* t) {
     }
     if (const char* g = getenv("SKB_FUSED_GRAPHS")) c->graphs = atoi(g) != 0;
     SKB_CUDA(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+    SKB_CUDA(cudaMalloc(&c->zrow, sizeof(float) * (t->dim + 4)));
+    SKB_CUDA(cudaMemset(c->zrow, 0, sizeof(float) * (t->dim + 4)));
     t->fused = c;
   }
   return t->fused;
@@ -714,6 +720,68 @@ __device__ __forceinline__ int nth_bit(unsigned x, int k) {
   return r == 0xFFFFFFFFu ? -1 : (int)r;
 }
 
+// gradient row of a sorted position: dpooled[g], or the all-zero row for
+// positions outside their bag's tile (tile combiner, j >= k): folding +0 into
+// a left fold from +0 never changes it, but the row is still touched
+constexpr uint32_t kZeroRow = 0xFFFFFFFFu;
+__device__ __forceinline__ const float* grad_row(const float* dp, const float* zrow, uint32_t g, int D) {
+  return g == kZeroRow ? zrow : dp + (int64_t)g * D;
+}
+
+// tile combiner, index phase: gradient row of every position = its row of the
+// bag's tile (g*k + j) for j < k, the zero row past k (segment_tile keeps only
+// the first k rows, segments.py:94-116); one warp per bag
+__global__ void k_tile_row_of(const int64_t* __restrict__ bag_offs, int64_t G, int64_t k, uint32_t* __restrict__ row_of) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < G; g += nw) {
+    const int64_t b = __ldg(bag_offs + g), e = __ldg(bag_offs + g + 1);
+    for (int64_t p = b + lane; p < e; p += 32) {
+      const int64_t j = p - b;
+      row_of[p] = j < k ? (uint32_t)(g * k + j) : kZeroRow;
+    }
+  }
+}
+
+// tile combiner, forward: out[g, j*D:(j+1)*D] = w[slot of position off[g]+j]
+// for j < min(len, k), `pad` for len <= j < k (segment_tile, bit-exact copy).
+// U independent row fetches per thread, as in the row gather.
+template <int VEC>
+__global__ void __launch_bounds__(256) k_fused_tile(const float* __restrict__ arena, const uint32_t* __restrict__ slot,
+                                                    const int64_t* __restrict__ bag_offs, int64_t G, int64_t k, int D,
+                                                    int64_t D3, float pad, float* __restrict__ out) {
+  using V = typename VecT<VEC>::T;
+  constexpr int U = 4;
+  const int per_row = D / VEC;
+  const int64_t total = G * k * per_row;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < total; base += stride * U) {
+    V v[U];
+    int64_t orow[U];
+    int col[U];
+    bool have[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t t = base + u * stride;
+      have[u] = false;
+      orow[u] = -1;
+      if (t < total) {
+        orow[u] = t / per_row;
+        col[u] = (int)(t - orow[u] * per_row) * VEC;
+        const int64_t g = orow[u] / k, j = orow[u] - g * k;
+        const int64_t b = __ldg(bag_offs + g), e = __ldg(bag_offs + g + 1);
+        if (j < e - b) {
+          have[u] = true;
+          v[u] = vload<VEC>(arena + (int64_t)__ldg(slot + b + j) * D3 + col[u]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (orow[u] >= 0) vstore<VEC>(out + orow[u] * D + col[u], have[u] ? v[u] : vfill<VEC>(pad));
+  }
+}
+
 // K9: fold + Adam.  Warps own chunks of 32 sorted positions; a run head
 // (first position of a slot) is found by ballot on skey[j] != skey[j-1], so
 // no separate run-heads pass is needed.  Sub-groups of L lanes take 2 heads
@@ -728,7 +796,7 @@ __global__ void __launch_bounds__(256, MINB) k_fused_adam(int64_t n, const uint3
                                                     float* __restrict__ arena, int64_t* __restrict__ last_step,
                                                     int64_t step, int64_t* __restrict__ dev_unique,
                                                     LongRun* __restrict__ longs, int64_t* __restrict__ nlong,
-                                                    int64_t longs_cap) {
+                                                    int64_t longs_cap, const float* __restrict__ zrow = nullptr) {
   using T = typename VecT<VEC>::T;
   __shared__ uint32_t s_bag[8][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -791,7 +859,7 @@ __global__ void __launch_bounds__(256, MINB) k_fused_adam(int64_t n, const uint3
               v[r] = vload<VEC>(row + 2 * D + c);
             }
             const uint32_t g = s_bag[wib][h[r]];
-            T x = vload<VEC>(dpooled + (int64_t)g * D + c);
+            T x = vload<VEC>(grad_row(dpooled, zrow, g, D) + c);
             if (mode == 1) x = vdiv<VEC>(x, (float)(__ldg(bag_offs + g + 1) - __ldg(bag_offs + g)));
             acc[r] = vadd<VEC>(vfill<VEC>(0.f), x);
           }
@@ -801,7 +869,7 @@ __global__ void __launch_bounds__(256, MINB) k_fused_adam(int64_t n, const uint3
           if (h[r] < 0) continue;
           for (int64_t jj = j0 + h[r] + 1; jj < e[r]; ++jj) {
             const uint32_t g = jj < j0 + 32 ? s_bag[wib][jj - j0] : __ldg(sval + jj);
-            T x = vload<VEC>(dpooled + (int64_t)g * D + c);
+            T x = vload<VEC>(grad_row(dpooled, zrow, g, D) + c);
             if (mode == 1) x = vdiv<VEC>(x, (float)(__ldg(bag_offs + g + 1) - __ldg(bag_offs + g)));
             acc[r] = vadd<VEC>(acc[r], x);
           }
@@ -851,7 +919,8 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) k_fused_adam_tma(int64_t n,
                                                                     int64_t* __restrict__ last_step, int64_t step,
                                                                     int64_t* __restrict__ dev_unique,
                                                                     LongRun* __restrict__ longs,
-                                                                    int64_t* __restrict__ nlong, int64_t longs_cap) {
+                                                                    int64_t* __restrict__ nlong, int64_t longs_cap,
+                                                                    const float* __restrict__ zrow) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int rowf = 3 * D;        // floats of [w|m|v]
   const int stage_f = kTmaRows * (rowf + D);
@@ -937,7 +1006,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) k_fused_adam_tma(int64_t n,
           const int slot_i = nrun + lane;
           desc[s * kTmaRows + slot_i] = TmaDesc{hk, hb, (uint32_t)(cbase + h), (uint32_t)e};
           bulk_g2s(rows + ((int64_t)s * kTmaRows + slot_i) * rowf, arena + (int64_t)hk * D3, row_bytes, &full[s]);
-          bulk_g2s(dps + ((int64_t)s * kTmaRows + slot_i) * D, dpooled + (int64_t)hb * D, dp_bytes, &full[s]);
+          bulk_g2s(dps + ((int64_t)s * kTmaRows + slot_i) * D, grad_row(dpooled, zrow, hb, D), dp_bytes, &full[s]);
         }
         const int last = nth_bit(pend, take - 1);
         pend = (last == 31) ? 0u : pend & (~0u << (last + 1));
@@ -987,7 +1056,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) k_fused_adam_tma(int64_t n,
           float4 acc = add4(make_float4(0.f, 0.f, 0.f, 0.f), x);
           for (uint32_t jj = d.jh + 1; jj < d.je; ++jj) {
             const uint32_t g = __ldg(sval + jj);
-            float4 y = ldg4(dpooled + (int64_t)g * D + c);
+            float4 y = ldg4(grad_row(dpooled, zrow, g, D) + c);
             if (mode == 1) y = vdiv<4>(y, (float)(__ldg(bag_offs + g + 1) - __ldg(bag_offs + g)));
             acc = add4(acc, y);
           }
@@ -1013,7 +1082,7 @@ static int env_int(const char* name, int dflt);
 template <int ROWS, int THREADS, int MINB, class... Args>
 static void launch_adam_tma(int64_t n, int D, cudaStream_t s, Args... args) {
   auto* kern = k_fused_adam_tma<ROWS, THREADS, MINB>;
-  note_param_kernel((const void*)kern, 15, 7, 10);
+  note_param_kernel((const void*)kern, 16, 7, 10);
   const size_t sm = tma_smem_bytes(D, ROWS);
   static size_t sm_set = 0;
   if (sm_set < sm) {
@@ -1300,11 +1369,11 @@ static void register_param_kernels() {
   if (done) return;
   done = true;
   note_param_kernel((const void*)k_fused_admit, 25, -1, 15);
-  note_param_kernel((const void*)k_fused_adam<1, 1, 4>, 15, 7, 10);
-  note_param_kernel((const void*)k_fused_adam<4, 2, 4>, 15, 7, 10);
-  note_param_kernel((const void*)k_fused_adam<4, 1, 5>, 15, 7, 10);
-  note_param_kernel((const void*)k_fused_adam<4, 1, 4>, 15, 7, 10);
-  note_param_kernel((const void*)k_long_fold<true>, 13, 8, 11);  // (runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out, last_step, step, nst)
+  note_param_kernel((const void*)k_fused_adam<1, 1, 4>, 16, 7, 10);
+  note_param_kernel((const void*)k_fused_adam<4, 2, 4>, 16, 7, 10);
+  note_param_kernel((const void*)k_fused_adam<4, 1, 5>, 16, 7, 10);
+  note_param_kernel((const void*)k_fused_adam<4, 1, 4>, 16, 7, 10);
+  note_param_kernel((const void*)k_long_fold<true>, 14, 8, 11);  // (runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out, last_step, step, nst, zrow)
 }
 
 // graph mode is off while per-phase event profiling is on (events cannot be
@@ -1371,6 +1440,8 @@ struct BatchArgs {
   const int32_t* strategy;
   int mode;
   int64_t step;
+  int64_t tile_k = 0;  // mode 2 (tile combiner): rows kept per bag
+  float pad = 0.f;     // mode 2: fill of a bag's rows past its length
 };
 
 // Index phase of one batch on the table's index stream: probe, admission,
@@ -1451,7 +1522,10 @@ static void fused_prepare(Table* t, const BatchArgs& a, cudaStream_t s) {
     }
     prof_mark(c, P_MISS, 1, x);
     prof_mark(c, P_SORT, 0, x);
-    k_bag_of<<<grid_for(G > 0 ? G : 1, 256), 256, 0, x>>>(a.bag_offs, G, B.bag);
+    if (a.mode == 2)  // tile: the gradient row of a position is its tile row (or the zero row past k)
+      k_tile_row_of<<<grid_for((G > 0 ? G : 1) * 32, 256), 256, 0, x>>>(a.bag_offs, G, a.tile_k, B.bag);
+    else
+      k_bag_of<<<grid_for(G > 0 ? G : 1, 256), 256, 0, x>>>(a.bag_offs, G, B.bag);
     SKB_LAUNCH_CHECK();
     sort_pairs_u32(B.slot, B.skey, B.bag, B.sval, n, bits_for((uint64_t)(t->arena_rows - 1)), x);
     prof_mark(c, P_SORT, 1, x);
@@ -1475,6 +1549,8 @@ static void fused_prepare(Table* t, const BatchArgs& a, cudaStream_t s) {
   B.G = G;
   B.F = a.F;
   B.mode = a.mode;
+  B.tile_k = a.tile_k;
+  B.pad = a.pad;
   B.step = a.step;
   B.any_seq = any_seq;
   B.last_written = false;
@@ -1489,7 +1565,7 @@ static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStrea
   if (c->prep_count > c->pool_count) {
     BatchCtx& H = c->b[c->pool_count % 2];
     if (H.ids != a.ids || H.n != a.n || H.G != a.G || H.bag_offs != a.bag_offs || H.step != a.step ||
-        H.mode != a.mode)
+        H.mode != a.mode || H.tile_k != a.tile_k)
       raise(SKB_E_VALUE, 0, "fused forward does not match the prepared (prefetched) batch");
   } else {
     fused_prepare(t, a, s);
@@ -1504,7 +1580,15 @@ static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStrea
     const size_t psm = sizeof(PoolSmem);
     const int64_t ntiles = (G + kTileBags - 1) / kTileBags;
     const bool v4 = D % 4 == 0 && (uintptr_t)pooled % 16 == 0;
-    if (!B.any_seq) {
+    if (B.mode == 2) {  // tile combiner: [G, k*D] rows, pad past each bag's length
+      const int64_t items = G * B.tile_k * (v4 ? D / 4 : D);
+      if (v4)
+        k_fused_tile<4><<<grid_for((items + 3) / 4, 256), 256, 0, s>>>(t->arena, B.slot, B.bag_offs, G, B.tile_k, D,
+                                                                        3 * (int64_t)D, B.pad, pooled);
+      else
+        k_fused_tile<1><<<grid_for((items + 3) / 4, 256), 256, 0, s>>>(t->arena, B.slot, B.bag_offs, G, B.tile_k, D,
+                                                                        3 * (int64_t)D, B.pad, pooled);
+    } else if (!B.any_seq) {
       const unsigned grid = grid_for(((G + 31) / 32) * 32, 256, 8);
 #define SKB_POOL_ARGS t->arena, B.slot, B.bag_offs, G, B.mode, D, 3 * (int64_t)D, pooled
       if (!v4)
@@ -1536,7 +1620,8 @@ static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStrea
     GraphKey k;
     int64_t* v = k.v;
     v[0] = t->gen; v[1] = B.gen; v[2] = (int64_t)pooled; v[3] = B.n; v[4] = (int64_t)B.bag_offs; v[5] = G;
-    v[6] = B.mode; v[7] = B.any_seq; v[8] = B.F; v[9] = (int64_t)B.members;
+    v[6] = B.mode; v[7] = B.any_seq; v[8] = B.F; v[9] = (int64_t)B.members; v[10] = B.tile_k;
+    memcpy(&v[11], &B.pad, sizeof(float));
     B.g_fwd.run(k, s, c->cap, B.step, nullptr, work);
   } else {
     work(s);
@@ -1574,7 +1659,7 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     const bool v4 = D % 4 == 0 && (uintptr_t)dpooled % 16 == 0;
     // long mean bags: scale each bag's gradient once (the same fp32 division
     // every position of the bag would do) and fold it as a sum
-    int mode = B.mode;
+    int mode = B.mode == 2 ? 0 : B.mode;  // tile: per-position tile rows, folded as a sum
     Scratch scaled;
     if (mode == 1 && v4 && n >= 8 * B.G) {
       scaled = Scratch(sizeof(float) * B.G * D, s);
@@ -1589,7 +1674,7 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     const unsigned grid = persist ? grid_for(chunks * 32, 256, 8)
                                                          : (unsigned)((chunks + 7) / 8);
 #define SKB_ADAM_ARGS n, B.skey, B.sval, B.bag_offs, dpooled, mode, D, a, t->arena, t->last_step, B.step, B.dev + 2, \
-                      (v4 ? B.longs : nullptr), B.dev + 3, B.longs_cap
+                      (v4 ? B.longs : nullptr), B.dev + 3, B.longs_cap, (const float*)c->zrow
     if (!v4) {
       k_fused_adam<1, 1, 4><<<grid, 256, 0, s>>>(SKB_ADAM_ARGS);
     } else {
@@ -1613,7 +1698,7 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     SKB_LAUNCH_CHECK();
     if (v4)
       launch_long_fold<true>(B.longs, B.dev + 3, B.longs_cap, B.sval, dpooled, D, B.bag_offs, mode, a, t->arena,
-                             t->last_step, B.step, s);
+                             t->last_step, B.step, s, c->zrow);
     prof_mark(c, P_ADAM, 1, s);
   }
   };
@@ -1621,7 +1706,7 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     GraphKey k;
     int64_t* v = k.v;
     v[0] = t->gen; v[1] = B.gen; v[2] = (int64_t)dpooled; v[3] = n; v[4] = (int64_t)B.bag_offs; v[5] = B.G;
-    v[6] = B.mode;
+    v[6] = B.mode; v[7] = B.tile_k;
     B.g_bwd.run(k, s, c->cap, B.step, &a, work);
   } else {
     work(s);
@@ -1645,6 +1730,40 @@ int skb_fused_prepare(skb_table_t h, const int64_t* ids, int64_t n, const int64_
   BatchArgs a{ids, n, member_pos_host, salts_host, num_members, namespaced, bag_offs, num_bags, member_bag_host,
               strategy_host, mode, step};
   fused_prepare(table_from(h), a, as_stream(stream));
+  SKB_API_END
+}
+
+// mode 2 checks shared by the tile entry points
+static BatchArgs tile_args(BatchArgs a, int64_t k, float pad) {
+  if (k < 0) raise(SKB_E_VALUE, k, "k must be >= 0");
+  if (a.G * (k > 0 ? k : 1) >= (int64_t)kZeroRow) raise(SKB_E_UNSUPPORTED, a.G, "fused tile: G * k >= 2^32 - 1");
+  a.mode = 2;
+  a.tile_k = k;
+  a.pad = pad;
+  return a;
+}
+
+int skb_fused_prepare_tile(skb_table_t h, const int64_t* ids, int64_t n, const int64_t* member_pos_host,
+                           const uint64_t* salts_host, int32_t num_members, int32_t namespaced,
+                           const int64_t* bag_offs, int64_t num_bags, const int64_t* member_bag_host, int64_t k,
+                           float pad, int64_t step, void* stream) {
+  SKB_API_BEGIN
+  std::vector<int32_t> strat(num_members > 0 ? num_members : 1, 1);
+  BatchArgs a{ids, n, member_pos_host, salts_host, num_members, namespaced, bag_offs, num_bags, member_bag_host,
+              strat.data(), 2, step};
+  fused_prepare(table_from(h), tile_args(a, k, pad), as_stream(stream));
+  SKB_API_END
+}
+
+int skb_fused_forward_tile(skb_table_t h, const int64_t* ids, int64_t n, const int64_t* member_pos_host,
+                           const uint64_t* salts_host, int32_t num_members, int32_t namespaced,
+                           const int64_t* bag_offs, int64_t num_bags, const int64_t* member_bag_host, int64_t k,
+                           float pad, int64_t step, float* tiles_out, void* stream) {
+  SKB_API_BEGIN
+  std::vector<int32_t> strat(num_members > 0 ? num_members : 1, 1);
+  BatchArgs a{ids, n, member_pos_host, salts_host, num_members, namespaced, bag_offs, num_bags, member_bag_host,
+              strat.data(), 2, step};
+  fused_forward(table_from(h), tile_args(a, k, pad), tiles_out, as_stream(stream));
   SKB_API_END
 }
 

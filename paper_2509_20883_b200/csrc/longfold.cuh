@@ -30,7 +30,7 @@ __device__ __forceinline__ void push_long_run(LongRun* list, int64_t* count, int
 }
 
 // One CTA folds one long run at a time (runs strided over CTAs).  Consumer
-// warps 0..NC-1 each own 128 columns (float4 per lane) and fold a stage's
+// warps 0..NC-1 each own 32 columns (one per lane) and fold a stage's
 // rows in position order from +0; the remaining NPW warps are producers
 // filling a kLfStages-deep shared-memory ring of kLfStageBytes stages with
 // 16-byte cp.async copies of the run's gradient rows.  Producer warp pw owns
@@ -54,7 +54,12 @@ __host__ __device__ inline int long_fold_tp(int D) {
   const int tp = kLfStageBytes / (4 * D);
   return tp < 1 ? 1 : (tp > kLfMaxTP ? kLfMaxTP : tp);
 }
-__host__ __device__ inline int long_fold_consumers(int D) { return (D + 127) / 128; }
+constexpr int kLfMaxNC = 16;  // consumer warps
+constexpr int kLfCols = 4;    // columns per consumer lane: dims up to 32 * kLfMaxNC * kLfCols = 2048
+__host__ __device__ inline int long_fold_consumers(int D) {
+  const int nc = (D + 31) / 32;
+  return nc < kLfMaxNC ? nc : kLfMaxNC;
+}
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
@@ -67,7 +72,8 @@ template <bool ADAM>
 __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __restrict__ nruns, int64_t cap,
                             const uint32_t* __restrict__ ridx, const float* __restrict__ rows, int D,
                             const int64_t* __restrict__ bag_offs, int mode, AdamDev a, float* __restrict__ out,
-                            int64_t* __restrict__ last_step, int64_t step, int nst) {
+                            int64_t* __restrict__ last_step, int64_t step, int nst,
+                            const float* __restrict__ zrow) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int TP = long_fold_tp(D);
   const int64_t stage_f = (int64_t)TP * D;  // floats per stage
@@ -127,7 +133,7 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
               if (i < items) {
                 const int row = i / cpr, ch = i - row * cpr;
                 const uint32_t gg = ix[row];
-                x[k] = ldg4(rows + (int64_t)gg * D + ch * 4);
+                x[k] = ldg4((gg == 0xFFFFFFFFu ? zrow : rows + (int64_t)gg * D) + ch * 4);
                 l[k] = (float)(__ldg(bag_offs + gg + 1) - __ldg(bag_offs + gg));
               }
             }
@@ -145,7 +151,8 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
         } else {
           for (int i = lane; i < items; i += 32) {
             const int row = i / cpr, ch = i - row * cpr;
-            cp_async16(dst + (int64_t)row * D + ch * 4, rows + (int64_t)ix[row] * D + ch * 4);
+            const uint32_t gg = ix[row];  // 0xFFFFFFFF: the zero row (tile positions past k)
+            cp_async16(dst + (int64_t)row * D + ch * 4, (gg == 0xFFFFFFFFu ? zrow : rows + (int64_t)gg * D) + ch * 4);
           }
           cp_async_arrive_noinc(&full[s]);  // fires when this lane's copies have landed
         }
@@ -154,40 +161,48 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
     }
     return;
   }
-  // ---------------- consumers: warp w owns columns [128 w, 128 (w+1)) ----------------
-  const int c = warp * 128 + lane * 4;
-  const bool active = c < D;
+  // ---------------- consumers: warp w owns columns 32 w + lane (+ 32 NC, ...) ----------------
+  // one column per lane: a row costs each warp one LDS + one FADD (the fp32
+  // chain's 4-cycle latency), not four FADDs on one fma pipe; dims above
+  // 32 * kLfMaxNC give a lane up to kLfCols columns
+  const int c0 = warp * 32 + lane;
+  const int cstep = 32 * NC;
   for (int64_t r = blockIdx.x; r < R; r += gridDim.x) {
     const LongRun run = runs[r];
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float acc[kLfCols];
+#pragma unroll
+    for (int q = 0; q < kLfCols; ++q) acc[q] = 0.f;
     for (int64_t p0 = run.jh; p0 < run.je; p0 += TP, ++it) {
       const int s = (int)(it % (uint32_t)nst);
       const uint32_t ph = (it / (uint32_t)nst) & 1u;
       const int np = (int)((int64_t)run.je - p0 < TP ? (int64_t)run.je - p0 : TP);
       mbar_wait(&full[s], ph);
-      if (active) {
-        const float* src = buf + s * stage_f + c;
-#pragma unroll 8
-        for (int p = 0; p < np; ++p) acc = add4(acc, *reinterpret_cast<const float4*>(src + (int64_t)p * D));
+#pragma unroll
+      for (int q = 0; q < kLfCols; ++q) {
+        const int c = c0 + q * cstep;
+        if (c < D) {
+          const float* src = buf + s * stage_f + c;
+#pragma unroll 16
+          for (int p = 0; p < np; ++p) acc[q] = __fadd_rn(acc[q], src[(int64_t)p * D]);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    if (active) {
+#pragma unroll
+    for (int q = 0; q < kLfCols; ++q) {
+      const int c = c0 + q * cstep;
+      if (c >= D) continue;
       if constexpr (ADAM) {
         float* row = out + (int64_t)run.key * (3 * D);
-        float4 p = *reinterpret_cast<float4*>(row + c), m = *reinterpret_cast<float4*>(row + D + c),
-               v = *reinterpret_cast<float4*>(row + 2 * D + c);
-        adam1(p.x, m.x, v.x, acc.x, a);
-        adam1(p.y, m.y, v.y, acc.y, a);
-        adam1(p.z, m.z, v.z, acc.z, a);
-        adam1(p.w, m.w, v.w, acc.w, a);
-        st4(row + c, p);
-        st4(row + D + c, m);
-        st4(row + 2 * D + c, v);
+        float p = row[c], m = row[D + c], v = row[2 * D + c];
+        adam1(p, m, v, acc[q], a);
+        row[c] = p;
+        row[D + c] = m;
+        row[2 * D + c] = v;
         if (c == 0 && step >= 0) last_step[run.key] = step;
       } else {
-        st4(out + (int64_t)run.key * D + c, acc);
+        out[(int64_t)run.key * D + c] = acc[q];
       }
     }
   }
@@ -204,7 +219,8 @@ inline size_t long_fold_smem(int D) {
 template <bool ADAM>
 inline void launch_long_fold(const LongRun* runs, const int64_t* nruns, int64_t cap, const uint32_t* ridx,
                              const float* rows, int D, const int64_t* bag_offs, int mode, AdamDev a, float* out,
-                             int64_t* last_step, int64_t step, cudaStream_t s) {
+                             int64_t* last_step, int64_t step, cudaStream_t s, const float* zrow = nullptr) {
+  if (D > 32 * kLfMaxNC * kLfCols) raise(SKB_E_UNSUPPORTED, D, "long-run fold: dim > %d", 32 * kLfMaxNC * kLfCols);
   const size_t sm = long_fold_smem(D);
   static size_t set = 0;
   if (set < sm) {
@@ -221,7 +237,7 @@ inline void launch_long_fold(const LongRun* runs, const int64_t* nruns, int64_t 
   int64_t grid = cap < (int64_t)sm_count() ? cap : (int64_t)sm_count();
   if (grid < 1) grid = 1;
   k_long_fold<ADAM><<<(unsigned)grid, threads, sm, s>>>(runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out,
-                                                        last_step, step, nst);
+                                                        last_step, step, nst, zrow);
   SKB_LAUNCH_CHECK();
 }
 

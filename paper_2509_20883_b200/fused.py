@@ -21,7 +21,7 @@ from .optim import AdamConfig, adam_scalars
 from .segments import resolve_strategy
 from .sharding import LogicalTable
 
-_MODES = {"sum": 0, "mean": 1}
+_MODES = {"sum": 0, "mean": 1, "tile": 2}
 
 
 class PackedBatch:
@@ -86,7 +86,17 @@ def _batch_args(lt: LogicalTable, batch: PackedBatch, step: int, mode: str):
             N.ptr(batch.bag_offs), batch.num_bags, mb, st, _MODES[mode], int(step))
 
 
-def prefetch(lt: LogicalTable, batch: PackedBatch, step: int, mode: str = "mean") -> None:
+def _tile_args(args, k, pad):
+    """Entry-point arguments of the tile combiner (segment_tile: k rows per bag, `pad` after)."""
+    if k is None:
+        raise ValueError("mode 'tile' needs k (rows kept per bag)")
+    if k < 0:
+        raise ValueError("k must be >= 0")
+    h, ids, n, mp, sl, F, ns, bo, G, mb, _st, _mode, step = args
+    return (h, ids, n, mp, sl, F, ns, bo, G, mb, int(k), float(pad), step)
+
+
+def prefetch(lt: LogicalTable, batch: PackedBatch, step: int, mode: str = "mean", k=None, pad: float = 0.0) -> None:
     """Enqueue the index phase (probe, admission, sort) of a future step.
 
     Issue it for step k+1 before `lookup_pool` of step k (or between that
@@ -96,13 +106,26 @@ def prefetch(lt: LogicalTable, batch: PackedBatch, step: int, mode: str = "mean"
     do not prefetch across an eviction / restore boundary.
     """
     telemetry.bump("fused.prefetch")
-    N.call("skb_fused_prepare", *_batch_args(lt, batch, step, mode), N.stream_ptr())
+    args = _batch_args(lt, batch, step, mode)
+    if mode == "tile":
+        N.call("skb_fused_prepare_tile", *_tile_args(args, k, pad), N.stream_ptr())
+    else:
+        N.call("skb_fused_prepare", *args, N.stream_ptr())
 
 
-def lookup_pool(lt: LogicalTable, batch: PackedBatch, step: int, mode: str = "mean", out=None):
-    """Pooled embeddings [G, D] of every bag of the batch (single shard)."""
+def lookup_pool(lt: LogicalTable, batch: PackedBatch, step: int, mode: str = "mean", out=None, k=None,
+                pad: float = 0.0):
+    """Pooled embeddings [G, D] of every bag of the batch (single shard);
+    mode "tile": the bags' first k rows concatenated, [G, k*D], rows past a
+    bag's length filled with `pad` (segment_tile, segments.py:94-116)."""
     telemetry.bump("fused.lookup_pool")
     args = _batch_args(lt, batch, step, mode)
+    if mode == "tile":
+        targs = _tile_args(args, k, pad)
+        if out is None:
+            out = N.empty((batch.num_bags, int(k) * lt.dim), "float32")
+        N.call("skb_fused_forward_tile", *targs, N.ptr(out), N.stream_ptr())
+        return out
     if out is None:
         out = N.empty((batch.num_bags, lt.dim), "float32")
     N.call("skb_fused_forward", *args, N.ptr(out), N.stream_ptr())
@@ -110,7 +133,8 @@ def lookup_pool(lt: LogicalTable, batch: PackedBatch, step: int, mode: str = "me
 
 
 def pool_grad_adam(lt: LogicalTable, dpooled, cfg: AdamConfig, step: int) -> None:
-    """Backward of the last lookup_pool on `lt`: grad fold + Adam/AdamW on touched rows."""
+    """Backward of the last lookup_pool on `lt`: grad fold + Adam/AdamW on touched rows.
+    `dpooled` has the forward output's shape ([G, D], or [G, k*D] for tile)."""
     telemetry.bump("fused.pool_grad_adam")
     if step < 1:
         raise ValueError("global step t must be >= 1")

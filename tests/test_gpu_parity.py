@@ -383,8 +383,9 @@ def test_ragged(skb, golden):
     eq(rows.truncate(1, "tail").values, np.array([2, 3, 10, 11], np.float32))
 
 
-def _fused_vs_oracle(skb, D, member_specs, steps, mode, seed=0, evict_every=0, thr=None, cfg=None):
-    """Drive the fused step and the oracle pipeline side by side."""
+def _fused_vs_oracle(skb, D, member_specs, steps, mode, seed=0, evict_every=0, thr=None, cfg=None, k=None, pad=0.0):
+    """Drive the fused step and the oracle pipeline side by side (mode "tile":
+    oracle = segment_tile + per-position tile gradients, zero past k)."""
     import torch
     rng = np.random.default_rng(seed)
     members = [m for m, _, _ in member_specs]
@@ -399,9 +400,10 @@ def _fused_vs_oracle(skb, D, member_specs, steps, mode, seed=0, evict_every=0, t
             ids.append(rng.zipf(1.2, int(lens.sum())).astype(np.int64) if m.startswith("z")
                        else rng.integers(0, 500, int(lens.sum())))
         batch = skb.PackedBatch(lt, members, ids, offs)
-        pooled = skb.lookup_pool(lt, batch, step, mode)
+        pooled = skb.lookup_pool(lt, batch, step, mode, k=k, pad=pad)
         G = batch.num_bags
-        dp = rng.standard_normal((G, D)).astype(np.float32)
+        W = D * k if mode == "tile" else D
+        dp = rng.standard_normal((G, W)).astype(np.float32)
         skb.pool_grad_adam(lt, torch.from_numpy(dp).cuda(), cfg, step)
         # oracle: train.py-style pipeline on the concatenated keys
         keys = np.concatenate([olt.keys_for(m, x) for m, x in zip(members, ids)])
@@ -409,12 +411,20 @@ def _fused_vs_oracle(skb, D, member_specs, steps, mode, seed=0, evict_every=0, t
         ref, grads, pos, bag = [], [], 0, 0
         for f, (m, B, _) in enumerate(member_specs):
             n_f = len(ids[f])
-            ref.append(O.pool(rows[pos:pos + n_f], offs[f], mode))
             lens = np.diff(offs[f])
             g = dp[bag:bag + B]
-            if mode == "mean":
-                g = g / np.maximum(lens, 1).astype(np.float32)[:, None]
-            grads.append(np.repeat(g, lens, axis=0).astype(np.float32))
+            if mode == "tile":
+                ref.append(O.tile(rows[pos:pos + n_f], offs[f], k, pad))
+                gt = np.zeros((n_f, D), np.float32)
+                for b in range(B):
+                    take = min(k, int(lens[b]))
+                    gt[offs[f][b]:offs[f][b] + take] = g[b].reshape(k, D)[:take]
+                grads.append(gt)
+            else:
+                ref.append(O.pool(rows[pos:pos + n_f], offs[f], mode))
+                if mode == "mean":
+                    g = g / np.maximum(lens, 1).astype(np.float32)[:, None]
+                grads.append(np.repeat(g, lens, axis=0).astype(np.float32))
             pos += n_f
             bag += B
         eq(pooled, np.concatenate(ref))
@@ -445,6 +455,23 @@ def test_fused_with_eviction(skb):
     specs = [("a", 128, lambda r, B: r.integers(1, 4, B))]
     _fused_vs_oracle(skb, 4, specs, steps=12, mode="sum", seed=9, evict_every=3, thr=2,
                      cfg=skb.AdamConfig(lr=0.05))
+
+
+@pytest.mark.parametrize("D", [16, 3])
+def test_fused_tile_combiner(skb, D):
+    """Fused tile combiner == segment_tile + tile-gradient expansion + grad
+    update: bags shorter than k (pad rows), longer than k (positions past k
+    fold a zero gradient but their rows are still updated), empty bags, and a
+    zipf member whose hot ids take the long-run fold."""
+    specs = [("a", 150, lambda r, B: r.integers(0, 12, B)),
+             ("zb", 60, lambda r, B: r.integers(20, 90, B))]
+    _fused_vs_oracle(skb, D, specs, steps=3, mode="tile", seed=5, k=7, pad=-1.5)
+
+
+def test_fused_tile_c4_like(skb):
+    """C4 shape in miniature: truncated length-k sequences of zipf ids, k = len."""
+    specs = [("zseq", 64, lambda r, B: np.full(B, 200, np.int64))]
+    _fused_vs_oracle(skb, 16, specs, steps=2, mode="tile", seed=6, k=200, pad=0.0)
 
 
 def test_fused_generic_dim(skb):
