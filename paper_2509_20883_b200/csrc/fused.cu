@@ -94,6 +94,11 @@ struct BatchCtx {
 struct FusedCtx {
   cudaStream_t side = nullptr;  // index stream: probe, admission, bag-of, sort
   float* zrow = nullptr;        // D zeros: the gradient row of tile positions past k
+  LongFoldPack pack;            // mega-run packing buffers of the long-run fold (backward only)
+  int64_t pack_gen = 0;
+  int64_t* lf_host = nullptr;   // pinned: long runs of a recent backward (async readback)
+  cudaEvent_t lf_ev = nullptr;
+  int64_t lf_last = 1;          // > 0: long runs seen recently (pack mega runs)
   cudaEvent_t ev_in = nullptr, ev_side_last = nullptr;
   BatchCtx b[2];
   int64_t prep_count = 0, pool_count = 0, bwd_count = 0;
@@ -147,6 +152,12 @@ void fused_ctx_destroy(FusedCtx* c) {
   if (c->side) cudaStreamDestroy(c->side);
   if (c->cap) cudaStreamDestroy(c->cap);
   cudaFree(c->zrow);
+  cudaFree(c->pack.images);
+  if (c->lf_host) cudaFreeHost(c->lf_host);
+  if (c->lf_ev) cudaEventDestroy(c->lf_ev);
+  cudaFree(c->pack.mlist);
+  cudaFree(c->pack.moff);
+  cudaFree(c->pack.mcount);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
   if (c->ev_side_last) cudaEventDestroy(c->ev_side_last);
   delete c;
@@ -176,6 +187,9 @@ static FusedCtx* ctx_get(Table* t) {
     }
     if (const char* g = getenv("SKB_FUSED_GRAPHS")) c->graphs = atoi(g) != 0;
     SKB_CUDA(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+    SKB_CUDA(cudaMallocHost(&c->lf_host, sizeof(int64_t)));
+    *c->lf_host = 1;
+    SKB_CUDA(cudaEventCreateWithFlags(&c->lf_ev, cudaEventDisableTiming));
     SKB_CUDA(cudaMalloc(&c->zrow, sizeof(float) * (t->dim + 4)));
     SKB_CUDA(cudaMemset(c->zrow, 0, sizeof(float) * (t->dim + 4)));
     t->fused = c;
@@ -1373,7 +1387,7 @@ static void register_param_kernels() {
   note_param_kernel((const void*)k_fused_adam<4, 2, 4>, 16, 7, 10);
   note_param_kernel((const void*)k_fused_adam<4, 1, 5>, 16, 7, 10);
   note_param_kernel((const void*)k_fused_adam<4, 1, 4>, 16, 7, 10);
-  note_param_kernel((const void*)k_long_fold<true>, 14, 8, 11);  // (runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out, last_step, step, nst, zrow)
+  note_param_kernel((const void*)k_long_fold<true>, 15, 8, 11);  // (runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out, last_step, step, nst, zrow, packed)
 }
 
 // graph mode is off while per-phase event profiling is on (events cannot be
@@ -1643,12 +1657,42 @@ __global__ void k_scale_bags(const float* __restrict__ dp, const int64_t* __rest
   }
 }
 
+// packing buffers for the batch's possible mega runs: plain cudaMalloc (grown
+// rarely, synchronously) — taking them from the stream-ordered pool that the
+// per-step scratch cycles through made step times bimodal (measured on C2)
+static void pack_reserve(FusedCtx* c, int64_t rows, int64_t runs, int D, cudaStream_t s) {
+  LongFoldPack& P = c->pack;
+  const int64_t imgs = long_fold_pack_images(rows, D);
+  const bool grow_img = imgs > P.cap_images, grow_runs = runs > P.cap_runs || !P.mcount;
+  if (!grow_img && !grow_runs) return;
+  SKB_CUDA(cudaStreamSynchronize(s));
+  if (grow_img) {
+    if (P.images) SKB_CUDA(cudaFree(P.images));
+    SKB_CUDA(cudaMalloc(&P.images, sizeof(float) * imgs * long_fold_stage_f(D)));
+    P.cap_images = imgs;
+  }
+  if (grow_runs) {
+    if (P.mlist) SKB_CUDA(cudaFree(P.mlist));
+    if (P.moff) SKB_CUDA(cudaFree(P.moff));
+    if (!P.mcount) SKB_CUDA(cudaMalloc(&P.mcount, sizeof(int64_t) * 2));
+    SKB_CUDA(cudaMalloc(&P.mlist, sizeof(uint32_t) * runs));
+    SKB_CUDA(cudaMalloc(&P.moff, sizeof(uint32_t) * runs));
+    P.cap_runs = runs;
+  }
+  c->pack_gen++;
+}
+
 static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc, cudaStream_t s) {
   FusedCtx* c = t->fused;
   if (!c || c->bwd_count >= c->pool_count) raise(SKB_E_VALUE, 0, "fused backward without a preceding fused forward");
   BatchCtx& B = c->b[c->bwd_count % 2];
   const int64_t n = B.n;
   const int D = (int)t->dim;
+  if (n > 0 && D % 4 == 0) pack_reserve(c, n, B.longs_cap, D, s);
+  // long runs seen by a recent backward (no sync: the last completed readback)
+  if (cudaEventQuery(c->lf_ev) == cudaSuccess) c->lf_last = *c->lf_host;
+  else cudaGetLastError();
+  const bool deep = c->lf_last > 0;  // long runs recently: pack mega runs for TMA streaming
   const AdamDev a = to_dev(sc);
   const float* dpooled_in = dpooled;
   auto work = [&](cudaStream_t s) {
@@ -1698,7 +1742,7 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     SKB_LAUNCH_CHECK();
     if (v4)
       launch_long_fold<true>(B.longs, B.dev + 3, B.longs_cap, B.sval, dpooled, D, B.bag_offs, mode, a, t->arena,
-                             t->last_step, B.step, s, c->zrow);
+                             t->last_step, B.step, s, c->zrow, &c->pack, deep);
     prof_mark(c, P_ADAM, 1, s);
   }
   };
@@ -1706,11 +1750,16 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     GraphKey k;
     int64_t* v = k.v;
     v[0] = t->gen; v[1] = B.gen; v[2] = (int64_t)dpooled; v[3] = n; v[4] = (int64_t)B.bag_offs; v[5] = B.G;
-    v[6] = B.mode; v[7] = B.tile_k;
+    v[6] = B.mode; v[7] = B.tile_k; v[8] = c->pack_gen; v[9] = deep;
     B.g_bwd.run(k, s, c->cap, B.step, &a, work);
   } else {
     work(s);
   }
+  if (n > 0 && D % 4 == 0 && cudaEventQuery(c->lf_ev) != cudaErrorNotReady) {  // one readback in flight
+    SKB_CUDA(cudaMemcpyAsync(c->lf_host, B.dev + 3, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    SKB_CUDA(cudaEventRecord(c->lf_ev, s));
+  }
+  cudaGetLastError();
   B.last_written = true;
   SKB_CUDA(cudaEventRecord(B.ev_free, s));
   c->bwd_count++;
@@ -1949,9 +1998,14 @@ int skb_fold_bags(const float* dpooled, int64_t dim, const uint32_t* idx, int64_
         n, skey.as<uint32_t>(), sval.as<uint32_t>(), bag_offs, dpooled, mode, D, none, out, nullptr, -1,
         cnt.as<int64_t>(), nullptr, nullptr, 0);
   SKB_LAUNCH_CHECK();
-  if (v4)
+  if (v4) {
+    const int64_t imgs = long_fold_pack_images(n, D);
+    Scratch prow(sizeof(float) * imgs * long_fold_stage_f(D), s), pl(sizeof(uint32_t) * lcap, s),
+        po(sizeof(uint32_t) * lcap, s), pc(sizeof(int64_t) * 2, s);
+    LongFoldPack pk{prow.as<float>(), imgs, pl.as<uint32_t>(), po.as<uint32_t>(), pc.as<int64_t>(), lcap};
     launch_long_fold<false>(longs.as<LongRun>(), cnt.as<int64_t>() + 1, lcap, sval.as<uint32_t>(), dpooled, D,
-                            bag_offs, mode, none, out, nullptr, -1, s);
+                            bag_offs, mode, none, out, nullptr, -1, s, nullptr, &pk);
+  }
   SKB_API_END
 }
 

@@ -5,8 +5,8 @@
 // positions that chain is inherently serial in fp32; what must not be serial
 // is the memory traffic.  Runs longer than kLongRun are deferred by the main
 // fold kernels into a device list; here one CTA owns one long run at a time:
-// a producer warp streams the run's gradient rows through a TMA ring while
-// consumer warps fold them in position order (details at k_long_fold).
+// producer warps stream the run's gradient rows through a shared-memory ring
+// while consumer warps fold them in position order (details at k_long_fold).
 // Cost ~ one FADD latency per position instead of one DRAM round trip.
 #pragma once
 #include <cstdlib>
@@ -18,6 +18,8 @@
 namespace skb {
 
 constexpr int kLongRun = 32;  // runs longer than this are deferred
+constexpr uint32_t kNoPack = 0xFFFFFFFFu;  // LongRun.pad: not packed
+constexpr int64_t kMegaRun = 8192;         // runs at least this long are packed for TMA streaming
 
 struct LongRun {
   uint32_t key, jh, je, pad;
@@ -29,36 +31,51 @@ __device__ __forceinline__ void push_long_run(LongRun* list, int64_t* count, int
   if ((int64_t)i < cap) list[i] = LongRun{key, jh, je, 0};
 }
 
-// One CTA folds one long run at a time (runs strided over CTAs).  Consumer
-// warps 0..NC-1 each own 32 columns (one per lane) and fold a stage's
-// rows in position order from +0; the remaining NPW warps are producers
-// filling a kLfStages-deep shared-memory ring of kLfStageBytes stages with
-// 16-byte cp.async copies of the run's gradient rows.  Producer warp pw owns
-// the stages it = pw (mod NPW), so NPW stages are being addressed (row index
-// loads) and copied at once; each lane signals the stage's `full` mbarrier
-// when ITS copies land (cp.async.mbarrier.arrive.noinc).  ~kLfStages x 16 KB
-// stay in flight per CTA and the single serial FADD chain is fed at ~one
-// row per add latency.  (Small per-row TMA bulk
-// copies were measured slower: per-copy issue cost; the earlier
-// double-buffered version was bound by one DRAM round trip per tile.)
+// One CTA folds one long run at a time (runs strided over CTAs).  A stage
+// holds TP consecutive positions of the run.  Consumer warps 0..NC-1 own
+// the columns (one per lane, kLfCols per lane above 32*kLfMaxNC) and fold a
+// stage's rows in position order from +0; the remaining NPW warps produce:
+//  - ordinary runs: producer warp pw owns the stages it = pw (mod NPW),
+//    loads the stage's row indices once, then 16-byte cp.async copies of the
+//    gradient rows (row-major stage), each lane signalling `full` when ITS
+//    copies land (cp.async.mbarrier.arrive.noinc).  One SM's outstanding-
+//    request budget caps this at ~25 GB/s.
+//  - mega runs (>= kMegaRun positions, the few hottest ids): k_pack_rows has
+//    already laid the run out as stage IMAGES — each stage transposed to
+//    column-major with a padded column stride PS = TP + 4 — so a stage is
+//    ONE TMA bulk copy, and a consumer lane reads four positions of its
+//    column with one conflict-free LDS.128: the serial chain, not the load
+//    path, sets the pace (~4 cycles per position).
 // rows: gradient source rows (dpooled [G, D] or per-position grads [N, D]);
-// ridx[j]: row of sorted position j; mode 1 (mean): divide by len(bag ridx[j]).
+// ridx[j]: row of sorted position j (0xFFFFFFFF: the zero row `zrow`);
+// mode 1 (mean): divide by len(bag ridx[j]).
 // ADAM: update arena row `key` (and last_step); else write out[key * D].
 constexpr int kLfStages = 12;
-constexpr int kLfStageBytes = 16384;
-constexpr int kLfMaxTP = 256;   // rows per stage cap (small dims)
+constexpr int kLfStageBytes = 32768;
+constexpr int kLfMaxTP = 512;   // rows per stage cap (small dims)
 constexpr int kLfMaxPW = 8;     // producer warps (index buffers)
+constexpr int kLfPad = 4;       // column padding of a packed stage image
+constexpr int kLfSmemBudget = 192 * 1024;  // ring + index buffers; leaves room for co-resident index-stream CTAs
 
-// rows per stage: kLfStageBytes of rows, at most kLfMaxTP (small dims)
+// rows per stage: kLfStageBytes of rows, a multiple of 4 (16-byte columns in
+// a packed image), at most kLfMaxTP (small dims)
 __host__ __device__ inline int long_fold_tp(int D) {
-  const int tp = kLfStageBytes / (4 * D);
-  return tp < 1 ? 1 : (tp > kLfMaxTP ? kLfMaxTP : tp);
+  const int tp = (kLfStageBytes / (4 * D)) & ~3;
+  return tp < 4 ? 4 : (tp > kLfMaxTP ? kLfMaxTP : tp);
 }
+// floats of one stage slot: a row-major stage (TP*D) or a packed image (D*(TP+4))
+__host__ __device__ inline int64_t long_fold_stage_f(int D) { return (int64_t)D * (long_fold_tp(D) + kLfPad); }
 constexpr int kLfMaxNC = 16;  // consumer warps
 constexpr int kLfCols = 4;    // columns per consumer lane: dims up to 32 * kLfMaxNC * kLfCols = 2048
 __host__ __device__ inline int long_fold_consumers(int D) {
   const int nc = (D + 31) / 32;
   return nc < kLfMaxNC ? nc : kLfMaxNC;
+}
+// ring depth that fits the shared-memory budget
+inline int long_fold_stages(int D, int budget = kLfSmemBudget) {
+  const int64_t fixed = (int64_t)kLfMaxPW * kLfMaxTP * 4 + 2 * kLfStages * 8;
+  int64_t st = (budget - fixed) / (long_fold_stage_f(D) * 4);
+  return (int)(st > kLfStages ? kLfStages : (st < 2 ? 2 : st));
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -73,19 +90,20 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
                             const uint32_t* __restrict__ ridx, const float* __restrict__ rows, int D,
                             const int64_t* __restrict__ bag_offs, int mode, AdamDev a, float* __restrict__ out,
                             int64_t* __restrict__ last_step, int64_t step, int nst,
-                            const float* __restrict__ zrow) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+                            const float* __restrict__ zrow, const float* __restrict__ packed) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int TP = long_fold_tp(D);
-  const int64_t stage_f = (int64_t)TP * D;  // floats per stage
+  const int PS = TP + kLfPad;                   // column stride of a packed image
+  const int64_t stage_f = long_fold_stage_f(D);  // floats per stage slot
   float* buf = reinterpret_cast<float*>(smem_raw);
-  uint32_t* idx = reinterpret_cast<uint32_t*>(buf + kLfStages * stage_f);  // [kLfMaxPW][kLfMaxTP]
+  uint32_t* idx = reinterpret_cast<uint32_t*>(buf + (int64_t)nst * stage_f);  // [kLfMaxPW][kLfMaxTP]
   uint64_t* full = reinterpret_cast<uint64_t*>(idx + kLfMaxPW * kLfMaxTP);
   uint64_t* empty = full + kLfStages;
   const int NC = long_fold_consumers(D);
   const int64_t R = *nruns < cap ? *nruns : cap;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kLfStages; ++s) {
+    for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 32);  // the owning producer warp's lanes
       mbar_init(&empty[s], NC);
     }
@@ -98,13 +116,26 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
     const int cpr = D / 4;  // 16-byte chunks per row
     for (int64_t r = blockIdx.x; r < R; r += gridDim.x) {
       const LongRun run = runs[r];
+      const bool img = packed && run.pad != kNoPack;
       for (int64_t p0 = run.jh; p0 < run.je; p0 += TP, ++it) {
         if ((int)(it % (uint32_t)NPW) != pw) continue;
         const int s = (int)(it % (uint32_t)nst);
         const uint32_t ph = (it / (uint32_t)nst) & 1u;
         const int np = (int)((int64_t)run.je - p0 < TP ? (int64_t)run.je - p0 : TP);
-        const int items = np * cpr;
         float* dst = buf + s * stage_f;
+        if (img) {  // one bulk copy of the stage image
+          const uint32_t bytes = (uint32_t)D * (uint32_t)PS * 4u;
+          mbar_wait(&empty[s], ph ^ 1u);
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&full[s], bytes);
+            bulk_g2s(dst, packed + ((int64_t)run.pad + (p0 - run.jh) / TP) * stage_f, bytes, &full[s]);
+          } else {
+            mbar_arrive(&full[s]);
+          }
+          __syncwarp();
+          continue;
+        }
+        const int items = np * cpr;
         // the stage's row indices: one coalesced batch of loads per lane, staged in
         // the warp's index buffer (a single memory latency per stage)
         uint32_t gi[kLfMaxTP / 32];
@@ -156,19 +187,18 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
           }
           cp_async_arrive_noinc(&full[s]);  // fires when this lane's copies have landed
         }
-        __syncwarp();                          // ix is rewritten by this warp's next stage
+        __syncwarp();  // ix is rewritten by this warp's next stage
       }
     }
     return;
   }
   // ---------------- consumers: warp w owns columns 32 w + lane (+ 32 NC, ...) ----------------
-  // one column per lane: a row costs each warp one LDS + one FADD (the fp32
-  // chain's 4-cycle latency), not four FADDs on one fma pipe; dims above
-  // 32 * kLfMaxNC give a lane up to kLfCols columns
+  // one column per lane: a position costs each warp one FADD on the chain
   const int c0 = warp * 32 + lane;
   const int cstep = 32 * NC;
   for (int64_t r = blockIdx.x; r < R; r += gridDim.x) {
     const LongRun run = runs[r];
+    const bool img = packed && run.pad != kNoPack;
     float acc[kLfCols];
 #pragma unroll
     for (int q = 0; q < kLfCols; ++q) acc[q] = 0.f;
@@ -180,7 +210,39 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
 #pragma unroll
       for (int q = 0; q < kLfCols; ++q) {
         const int c = c0 + q * cstep;
-        if (c < D) {
+        if (c >= D) continue;
+        if (img) {  // column-major image: four positions per 16-byte load,
+                    // the next 16 positions' loads issued before this 16's adds
+          const float* col = buf + s * stage_f + (int64_t)c * PS;
+          const float4* c4 = reinterpret_cast<const float4*>(col);
+          const int n16 = np & ~15;
+          if (n16) {
+            float4 x[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) x[k] = c4[k];
+            for (int p = 16; p < n16; p += 16) {
+              float4 y[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) y[k] = c4[(p >> 2) + k];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                acc[q] = __fadd_rn(acc[q], x[k].x);
+                acc[q] = __fadd_rn(acc[q], x[k].y);
+                acc[q] = __fadd_rn(acc[q], x[k].z);
+                acc[q] = __fadd_rn(acc[q], x[k].w);
+                x[k] = y[k];
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              acc[q] = __fadd_rn(acc[q], x[k].x);
+              acc[q] = __fadd_rn(acc[q], x[k].y);
+              acc[q] = __fadd_rn(acc[q], x[k].z);
+              acc[q] = __fadd_rn(acc[q], x[k].w);
+            }
+          }
+          for (int p = n16; p < np; ++p) acc[q] = __fadd_rn(acc[q], col[p]);
+        } else {
           const float* src = buf + s * stage_f + c;
 #pragma unroll 16
           for (int p = 0; p < np; ++p) acc[q] = __fadd_rn(acc[q], src[(int64_t)p * D]);
@@ -208,37 +270,186 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
   }
 }
 
-inline size_t long_fold_smem(int D) {
-  const int TP = long_fold_tp(D);
-  return (size_t)kLfStages * TP * D * sizeof(float) + (size_t)kLfMaxPW * kLfMaxTP * sizeof(uint32_t) +
+// ---------------------------------------------------------------------------
+// Mega-run packing: the whole grid gathers the gradient rows of the runs of
+// at least kMegaRun positions into stage images (see k_long_fold), so the
+// CTA folding such a run streams it with one bulk copy per stage.
+struct LongFoldPack {
+  float* images = nullptr;    // [cap_images][D * (TP + kLfPad)]
+  int64_t cap_images = 0;
+  uint32_t* mlist = nullptr;  // [cap_runs] run index of each mega run
+  uint32_t* moff = nullptr;   // [cap_runs] first image of each mega run (ascending; kNoPack if it did not fit)
+  int64_t* mcount = nullptr;  // [2] mega runs, images in use
+  int64_t cap_runs = 0;
+};
+
+// one block: exclusive scans of (is mega, stage images) over the run list;
+// run.pad = first image (kNoPack for ordinary runs or past capacity)
+static __global__ void __launch_bounds__(1024) k_pack_plan(LongRun* runs, const int64_t* __restrict__ nruns,
+                                                           int64_t cap, int TP, int64_t cap_images,
+                                                           uint32_t* __restrict__ mlist, uint32_t* __restrict__ moff,
+                                                           int64_t* __restrict__ mcount) {
+  __shared__ int64_t s_c[32], s_l[32];
+  __shared__ int64_t s_cc, s_cl;
+  __shared__ unsigned long long s_fit;  // images of the fitted runs (a prefix of the mega list)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
+  const int64_t R = *nruns < cap ? *nruns : cap;
+  if (threadIdx.x == 0) {
+    s_cc = s_cl = 0;
+    s_fit = 0;
+  }
+  __syncthreads();
+  for (int64_t b0 = 0; b0 < R; b0 += blockDim.x) {
+    const int64_t r = b0 + threadIdx.x;
+    int64_t len = 0;
+    if (r < R) len = (int64_t)runs[r].je - runs[r].jh;
+    const int64_t f = (r < R && len >= kMegaRun) ? 1 : 0, l = f ? (len + TP - 1) / TP : 0;
+    int64_t ic = f, il = l;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t yc = __shfl_up_sync(0xffffffffu, ic, o), yl = __shfl_up_sync(0xffffffffu, il, o);
+      if (lane >= o) {
+        ic += yc;
+        il += yl;
+      }
+    }
+    if (lane == 31) {
+      s_c[w] = ic;
+      s_l[w] = il;
+    }
+    __syncthreads();
+    int64_t bc = s_cc, bl = s_cl, tc = 0, tl = 0;
+    for (int q = 0; q < W; ++q) {
+      if (q < w) {
+        bc += s_c[q];
+        bl += s_l[q];
+      }
+      tc += s_c[q];
+      tl += s_l[q];
+    }
+    const int64_t xc = bc + ic - f, xl = bl + il - l;
+    if (r < R) {
+      const bool fits = f && xl + l <= cap_images;
+      runs[r].pad = fits ? (uint32_t)xl : kNoPack;
+      if (fits) atomicMax(&s_fit, (unsigned long long)(xl + l));
+      if (f) {
+        mlist[xc] = (uint32_t)r;
+        moff[xc] = fits ? (uint32_t)xl : kNoPack;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_cc += tc;
+      s_cl += tl;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    mcount[0] = s_cc;
+    mcount[1] = (int64_t)s_fit;
+  }
+}
+
+// one block per stage image: TP gradient rows gathered row-major into shared
+// memory (coalesced reads of whole rows; / len for mean bags; zero row past a
+// tile's k), written out column-major with the padded stride (coalesced)
+static __global__ void __launch_bounds__(256) k_pack_rows(const LongRun* __restrict__ runs,
+                                                          const uint32_t* __restrict__ mlist,
+                                                          const uint32_t* __restrict__ moff,
+                                                          const int64_t* __restrict__ mcount,
+                                                          const uint32_t* __restrict__ ridx,
+                                                          const float* __restrict__ rows,
+                                                          const float* __restrict__ zrow, int D,
+                                                          const int64_t* __restrict__ bag_offs, int mode,
+                                                          float* __restrict__ images) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* tile = reinterpret_cast<float*>(smem_raw);  // [TP][D + 1]
+  const int TP = long_fold_tp(D), PS = TP + kLfPad;
+  const int64_t stage_f = long_fold_stage_f(D);
+  const int64_t nm = mcount[0], nimg = mcount[1];
+  for (int64_t im = blockIdx.x; im < nimg; im += gridDim.x) {
+    int64_t lo = 0, hi = nm;  // the mega run owning image im (moff ascending; unfitted runs are a kNoPack suffix)
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)__ldg(moff + mid) <= im) lo = mid; else hi = mid;
+    }
+    const LongRun run = runs[__ldg(mlist + lo)];
+    const int64_t j0 = (int64_t)run.jh + (im - (int64_t)__ldg(moff + lo)) * TP;
+    const int np = (int)((int64_t)run.je - j0 < TP ? (int64_t)run.je - j0 : TP);
+    __syncthreads();  // the previous image's tile has been written out
+    for (int64_t t = threadIdx.x; t < (int64_t)np * D; t += blockDim.x) {
+      const int p = (int)(t / D), c = (int)(t - (int64_t)p * D);
+      const uint32_t g = __ldg(ridx + j0 + p);
+      float x = g == 0xFFFFFFFFu ? zrow[c] : __ldg(rows + (int64_t)g * D + c);
+      if (mode == 1) x = __fdiv_rn(x, (float)(__ldg(bag_offs + g + 1) - __ldg(bag_offs + g)));
+      tile[p * (D + 1) + c] = x;
+    }
+    __syncthreads();
+    float* img = images + im * stage_f;
+    for (int64_t t = threadIdx.x; t < (int64_t)D * TP; t += blockDim.x) {
+      const int c = (int)(t / TP), p = (int)(t - (int64_t)c * TP);
+      img[(int64_t)c * PS + p] = p < np ? tile[p * (D + 1) + c] : 0.f;
+    }
+  }
+}
+
+inline size_t long_fold_smem(int D, int nst) {
+  return (size_t)nst * long_fold_stage_f(D) * sizeof(float) + (size_t)kLfMaxPW * kLfMaxTP * sizeof(uint32_t) +
          2 * kLfStages * sizeof(uint64_t);
 }
 
-// Launch the long-run pass (CTAs exit at once when the list is empty).
+// Launch the long-run pass (CTAs exit at once when the list is empty); with
+// `pack`, mega runs are first gathered into stage images (plan + pack).
 // Requires D % 4 == 0 and 16-byte aligned rows (the callers' vector path).
 template <bool ADAM>
-inline void launch_long_fold(const LongRun* runs, const int64_t* nruns, int64_t cap, const uint32_t* ridx,
+inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, const uint32_t* ridx,
                              const float* rows, int D, const int64_t* bag_offs, int mode, AdamDev a, float* out,
-                             int64_t* last_step, int64_t step, cudaStream_t s, const float* zrow = nullptr) {
+                             int64_t* last_step, int64_t step, cudaStream_t s, const float* zrow = nullptr,
+                             const LongFoldPack* pack = nullptr, bool expect_mega = true) {
   if (D > 32 * kLfMaxNC * kLfCols) raise(SKB_E_UNSUPPORTED, D, "long-run fold: dim > %d", 32 * kLfMaxNC * kLfCols);
-  const size_t sm = long_fold_smem(D);
-  static size_t set = 0;
+  const int nc = long_fold_consumers(D);
+  static const int env_pw = getenv("SKB_LF_PW") ? atoi(getenv("SKB_LF_PW")) : 0;
+  static const int env_st = getenv("SKB_LF_STAGES") ? atoi(getenv("SKB_LF_STAGES")) : kLfStages;
+  int npw = env_pw > 0 && env_pw <= kLfMaxPW ? env_pw : (nc > 4 ? 4 : 8 - nc);  // >= 4 producer warps
+  int nst = env_st >= 2 && env_st <= kLfStages ? env_st : kLfStages;
+  if (nst > long_fold_stages(D)) nst = long_fold_stages(D);
+  if (npw > nst) npw = nst;  // a producer warp must never get a full ring lap ahead (parity waits)
+  const int threads = 32 * (nc + npw);
+  const size_t sm = long_fold_smem(D, nst);
+  static size_t set = 0;  // attribute raised to the largest size launched so far
   if (set < sm) {
     SKB_CUDA(cudaFuncSetAttribute(k_long_fold<ADAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     set = sm;
   }
-  const int nc = long_fold_consumers(D);
-  static const int env_pw = getenv("SKB_LF_PW") ? atoi(getenv("SKB_LF_PW")) : 0;
-  static const int env_st = getenv("SKB_LF_STAGES") ? atoi(getenv("SKB_LF_STAGES")) : kLfStages;
-  const int npw = env_pw > 0 && env_pw <= kLfMaxPW ? env_pw : (nc > 4 ? 4 : 8 - nc);  // >= 4 producer warps
-  const int threads = 32 * (nc + npw);
-  int nst = env_st >= 2 && env_st <= kLfStages ? env_st : kLfStages;
-  if (nst < npw) nst = npw;  // a producer warp must never get a full ring lap ahead (parity waits)
+  const float* packed = nullptr;
+  static const bool env_pack = getenv("SKB_LF_PACK") ? atoi(getenv("SKB_LF_PACK")) != 0 : true;
+  // expect_mega: the caller saw long runs recently (else the two packing
+  // launches are skipped; mega runs then take the cp.async path, same result)
+  if (env_pack && expect_mega && pack && pack->images && pack->cap_runs >= cap) {
+    const int TP = long_fold_tp(D);
+    k_pack_plan<<<1, 1024, 0, s>>>(runs, nruns, cap, TP, pack->cap_images, pack->mlist, pack->moff, pack->mcount);
+    SKB_LAUNCH_CHECK();
+    const size_t psm = (size_t)TP * (D + 1) * sizeof(float);
+    static size_t pset = 0;
+    if (pset < psm) {
+      SKB_CUDA(cudaFuncSetAttribute(k_pack_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+      pset = psm;
+    }
+    k_pack_rows<<<grid_for(pack->cap_images * 256, 256, 4), 256, psm, s>>>(
+        runs, pack->mlist, pack->moff, pack->mcount, ridx, rows, zrow, D, bag_offs, mode, pack->images);
+    SKB_LAUNCH_CHECK();
+    packed = pack->images;
+  }
   int64_t grid = cap < (int64_t)sm_count() ? cap : (int64_t)sm_count();
   if (grid < 1) grid = 1;
   k_long_fold<ADAM><<<(unsigned)grid, threads, sm, s>>>(runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out,
-                                                        last_step, step, nst, zrow);
+                                                        last_step, step, nst, zrow, packed);
   SKB_LAUNCH_CHECK();
+}
+
+// stage images needed to pack up to `rows` positions of mega runs
+inline int64_t long_fold_pack_images(int64_t rows, int D) {
+  const int64_t tp = long_fold_tp(D);
+  return rows / tp + rows / kMegaRun + 1;
 }
 
 }  // namespace skb

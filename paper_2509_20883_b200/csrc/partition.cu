@@ -517,9 +517,14 @@ void grad_fold(const float* grads, int64_t n, int D, const int64_t* inverse, int
                                                          k2.as<uint32_t>(), v2.as<uint32_t>(), grads, D, out, nullptr,
                                                          nullptr, 0);
   SKB_LAUNCH_CHECK();
-  if (v4)
+  if (v4) {
+    const int64_t imgs = long_fold_pack_images(n, D);
+    Scratch prow(sizeof(float) * imgs * long_fold_stage_f(D), s), pl(sizeof(uint32_t) * lcap, s),
+        po(sizeof(uint32_t) * lcap, s), pc(sizeof(int64_t) * 2, s);
+    LongFoldPack pk{prow.as<float>(), imgs, pl.as<uint32_t>(), po.as<uint32_t>(), pc.as<int64_t>(), lcap};
     launch_long_fold<false>(longs.as<LongRun>(), nseg.as<int64_t>() + 1, lcap, v2.as<uint32_t>(), grads, D, nullptr, 0,
-                            AdamDev{}, out, nullptr, -1, s);
+                            AdamDev{}, out, nullptr, -1, s, nullptr, &pk);
+  }
 }
 
 struct IdxRestore {
