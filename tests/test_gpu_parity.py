@@ -469,9 +469,17 @@ def test_fused_tile_combiner(skb, D):
 
 
 def test_fused_tile_c4_like(skb):
-    """C4 shape in miniature: truncated length-k sequences of zipf ids, k = len."""
-    specs = [("zseq", 64, lambda r, B: np.full(B, 200, np.int64))]
-    _fused_vs_oracle(skb, 16, specs, steps=2, mode="tile", seed=6, k=200, pad=0.0)
+    """C4 shape in miniature: truncated length-k sequences of zipf ids, k = len
+    (the head id's run exceeds 8192 positions: packed stage images)."""
+    specs = [("zseq", 320, lambda r, B: np.full(B, 200, np.int64))]
+    _fused_vs_oracle(skb, 16, specs, steps=3, mode="tile", seed=6, k=200, pad=0.0)
+
+
+def test_fused_tile_mega_runs_past_k(skb):
+    """Tile combiner with bags far longer than k: most positions of the hot
+    ids' mega runs fold the zero row (packed images included)."""
+    specs = [("zlong", 160, lambda r, B: r.integers(100, 300, B))]
+    _fused_vs_oracle(skb, 32, specs, steps=2, mode="tile", seed=7, k=40, pad=0.5)
 
 
 def test_fused_generic_dim(skb):
@@ -523,21 +531,24 @@ def test_fused_hot_ids_long_runs(skb):
     """Hot ids (runs of thousands of positions) take the CTA-per-run long
     fold; still the exact np.add.at order (mean and sum, D = 8 and 64)."""
     import torch
-    for D, mode in ((64, "mean"), (8, "sum"), (16, "mean")):
-        rng = np.random.default_rng(D)
+    # 3000 bags: long runs (cp.async path); 24000 bags: mega runs >= 8192
+    # positions (grid-packed stage images + TMA streaming)
+    for D, mode, nb in ((64, "mean", 3000), (8, "sum", 3000), (16, "mean", 3000), (64, "mean", 24000),
+                        (16, "sum", 24000), (128, "sum", 24000)):
+        rng = np.random.default_rng(D + nb)
         members = ["h"]
         lt = skb.LogicalTable(f"dim{D}", D, 1, seed=1, members=members, namespaced=True)
         olt = O.OracleLogical(f"dim{D}", D, 1, seed=1, members=members, namespaced=True)
         cfg = skb.AdamConfig(lr=1e-2, weight_decay=0.01, variant="adamw")
-        for step in range(1, 3):
-            lens = rng.integers(1, 9, 3000)
+        for step in range(1, 4):
+            lens = rng.integers(1, 9, nb)
             offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
             ids = rng.integers(0, 5000, int(offs[-1]))
             hot = rng.random(len(ids)) < 0.6          # 60% of positions on 3 hot ids
             ids[hot] = rng.integers(0, 3, int(hot.sum()))
             batch = skb.PackedBatch(lt, members, [ids], [offs])
             pooled = skb.lookup_pool(lt, batch, step, mode)
-            dp = rng.standard_normal((3000, D)).astype(np.float32)
+            dp = rng.standard_normal((nb, D)).astype(np.float32)
             skb.pool_grad_adam(lt, torch.from_numpy(dp).cuda(), cfg, step)
             keys = olt.keys_for("h", ids)
             rows = O.lookup(olt, keys, step)
