@@ -265,6 +265,12 @@ int skb_fold_bags(const float* dpooled, int64_t dim, const uint32_t* idx, int64_
 int skb_bucketize_multi(const float* values, const int64_t* col_offs, int64_t num_cols,
                         const float* edges_cat, const int64_t* edge_offs, int64_t* out,
                         int64_t n_total, void* stream);
+/* Same, without the synchronous NaN check: the lowest index of a NaN input is
+ * atomicMin-ed into *nan_flag (device, caller-initialised to ~0) for the
+ * caller to read at its next synchronisation point (deferred ValueError). */
+int skb_bucketize_multi_async(const float* values, const int64_t* col_offs, int64_t num_cols, const float* edges_cat,
+                              const int64_t* edge_offs, int64_t* out, int64_t n_total, unsigned long long* nan_flag,
+                              void* stream);
 /* mod_transform / fused_mod features.py:56-62,180-189 (moduli > 0 checked on host) */
 int skb_mod_multi(const int64_t* values, const int64_t* col_offs, int64_t num_cols,
                   const int64_t* moduli, int64_t* out, int64_t n_total, void* stream);

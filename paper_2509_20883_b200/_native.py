@@ -90,6 +90,7 @@ _SIGS = {
     "skb_pool_indexed": ([_p, _i64, _p, _p, _i64, _p, _i32, _i32, _i32, _i64, _p, _p], ctypes.c_int),
     "skb_fold_bags": ([_p, _i64, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p], ctypes.c_int),
     "skb_bucketize_multi": ([_p, _p, _i64, _p, _p, _p, _i64, _p], ctypes.c_int),
+    "skb_bucketize_multi_async": ([_p, _p, _i64, _p, _p, _p, _i64, _p, _p], ctypes.c_int),
     "skb_mod_multi": ([_p, _p, _i64, _p, _p, _i64, _p], ctypes.c_int),
     "skb_cross_offsets": ([_p, _p, _i64, _p, _p], ctypes.c_int),
     "skb_cross": ([_p, _p, _p, _p, _i64, _p, _i64, _p, _p], ctypes.c_int),
@@ -175,6 +176,30 @@ def check(status: int) -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(lib(), name)(*args))
+
+
+if os.environ.get("SKB_PROFILE_CALLS"):
+    # host time spent inside each C-ABI entry point (diagnostics only)
+    import atexit
+    import collections
+    import time as _time
+
+    _CALL_T = collections.defaultdict(lambda: [0, 0.0])
+    _plain_call = call
+
+    def call(name: str, *args) -> None:  # noqa: F811
+        t0 = _time.perf_counter()
+        try:
+            _plain_call(name, *args)
+        finally:
+            rec = _CALL_T[name]
+            rec[0] += 1
+            rec[1] += _time.perf_counter() - t0
+
+    @atexit.register
+    def _report_calls():
+        for k, (n, t) in sorted(_CALL_T.items(), key=lambda kv: -kv[1][1])[:20]:
+            print(f"[skb calls] {k:36s} {n:7d} calls {t * 1e3:10.2f} ms  {t / n * 1e6:8.1f} us/call")
 
 
 # ---------------------------------------------------------------------------

@@ -68,6 +68,17 @@ int skb_bucketize_multi(const float* values, const int64_t* col_offs, int64_t nu
   SKB_API_END
 }
 
+int skb_bucketize_multi_async(const float* values, const int64_t* col_offs, int64_t num_cols, const float* edges_cat,
+                              const int64_t* edge_offs, int64_t* out, int64_t n_total, unsigned long long* nan_flag,
+                              void* stream) {
+  SKB_API_BEGIN
+  if (n_total <= 0) return SKB_OK;
+  k_bucketize<<<grid_for(n_total, 256), 256, 0, as_stream(stream)>>>(values, col_offs, num_cols, edges_cat, edge_offs,
+                                                                     n_total, out, nan_flag);
+  SKB_LAUNCH_CHECK();
+  SKB_API_END
+}
+
 int skb_mod_multi(const int64_t* values, const int64_t* col_offs, int64_t num_cols, const int64_t* moduli,
                   int64_t* out, int64_t n_total, void* stream) {
   SKB_API_BEGIN

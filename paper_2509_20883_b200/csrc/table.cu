@@ -6,7 +6,9 @@
 // miss flags -> insert: the k-th unknown id (input order) gets
 // free_list[F-1-k] if k < F else allocated + k - F, so offsets are identical
 // to the reference's dict loop while every id is handled by its own thread.
+#include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -15,6 +17,8 @@
 #include "table.cuh"
 
 namespace skb {
+
+static std::atomic<int64_t> g_snap_waits{0}, g_refreshes{0};  // SKB_DEBUG_SYNC diagnostics
 
 Table* table_from(skb_table_t h) {
   if (!h) raise(SKB_E_ARG, 0, "null table handle");
@@ -74,6 +78,7 @@ static void rehash(Table* t, int64_t new_cap, cudaStream_t s) {
 }
 
 void table_refresh(Table* t, cudaStream_t s) {
+  g_refreshes++;
   SKB_CUDA(cudaMemcpyAsync(t->snap_host, t->counters, sizeof(int64_t) * C_N, cudaMemcpyDeviceToHost, s));
   SKB_CUDA(cudaStreamSynchronize(s));
   for (int i = 0; i < C_N; ++i) t->known[i] = t->snap_host[i];
@@ -115,6 +120,7 @@ static bool bound_ok_after_snapshot(Table* t, int64_t n) {
   harvest_snapshot(t);
   if (bound_ok(t, n)) return true;
   if (!t->snap_pending) return false;
+  g_snap_waits++;
   SKB_CUDA(cudaEventSynchronize(t->snap_ev));
   harvest_snapshot(t);
   return bound_ok(t, n);
@@ -863,6 +869,9 @@ int skb_table_create(int64_t dim, int64_t seed, int64_t block_size, int64_t evic
 int skb_table_destroy(skb_table_t h) {
   SKB_API_BEGIN
   Table* t = table_from(h);
+  if (getenv("SKB_DEBUG_SYNC"))
+    fprintf(stderr, "[skb] snapshot waits %lld, counter refreshes %lld (all tables so far)\n",
+            (long long)g_snap_waits.load(), (long long)g_refreshes.load());
   SKB_CUDA(cudaDeviceSynchronize());
   cudaFree(t->arena);
   cudaFree(t->last_step);

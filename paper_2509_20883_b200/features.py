@@ -48,12 +48,63 @@ def hash_feature_packed(blob, str_offsets, row_offsets) -> RaggedTensor:
     return RaggedTensor(fnv1a64_packed(blob, str_offsets), row_offsets)
 
 
+_DEFERRED = threading.local()
+
+
+class deferred_checks:
+    """Context for input pipelines: data-dependent checks of the feature
+    engine (bucketize's NaN -> ValueError, features.py:50-51) are recorded on
+    the device instead of being read back per call — no host synchronisation
+    inside the step — and raised (same exception and message) when the
+    context exits or at `check_deferred()`.  Outside the context every call
+    raises synchronously, exactly like the reference."""
+
+    def __enter__(self):
+        stack = getattr(_DEFERRED, "stack", None)
+        if stack is None:
+            stack = _DEFERRED.stack = []
+        stack.append([])
+        return self
+
+    def __exit__(self, exc_type, exc, tb):
+        flags = _DEFERRED.stack.pop()
+        if exc_type is None:
+            _raise_pending(flags)
+        return False
+
+
+def check_deferred() -> None:
+    """Read the checks recorded so far in the innermost deferred_checks()
+    context (one synchronisation) and raise the first failure."""
+    stack = getattr(_DEFERRED, "stack", None)
+    if stack:
+        flags, stack[-1] = stack[-1], []
+        _raise_pending(flags)
+
+
+def _raise_pending(flags):
+    if not flags:
+        return
+    t = N.torch()
+    vals = t.cat([f for f, _ in flags]).cpu().tolist()
+    for v, (_, msg) in zip(vals, flags):
+        if v != -1:  # ~0 as int64: nothing flagged
+            raise ValueError(msg)
+
+
 def _bucketize_flat(vals_d, col_offs_d, C, edges_d, edge_offs_d):
     n = vals_d.numel()
     out = N.empty((n,), "int64")
     if n:
-        N.call("skb_bucketize_multi", N.ptr(vals_d), N.ptr(col_offs_d), C, N.ptr(edges_d), N.ptr(edge_offs_d),
-               N.ptr(out), n, N.stream_ptr())
+        stack = getattr(_DEFERRED, "stack", None)
+        if stack:
+            flag = N.torch().full((1,), -1, dtype=N.torch().int64, device=vals_d.device)
+            N.call("skb_bucketize_multi_async", N.ptr(vals_d), N.ptr(col_offs_d), C, N.ptr(edges_d),
+                   N.ptr(edge_offs_d), N.ptr(out), n, N.ptr(flag), N.stream_ptr())
+            stack[-1].append((flag, "bucketize input contains NaN"))
+        else:
+            N.call("skb_bucketize_multi", N.ptr(vals_d), N.ptr(col_offs_d), C, N.ptr(edges_d), N.ptr(edge_offs_d),
+                   N.ptr(out), n, N.stream_ptr())
     return out
 
 
@@ -129,7 +180,8 @@ def _cross_pairs(pairs, sizes=None):
         if total:
             N.call("skb_cross", N.ptr(av), N.ptr(ao), N.ptr(bv), N.ptr(bo), rows, N.ptr(oo), int(total), N.ptr(out),
                    N.stream_ptr())
-        res.append(RaggedTensor(out.cpu().numpy(), oo.cpu().numpy()) if as_np else RaggedTensor(out, oo))
+        # offsets come from the validated inputs by construction: carried as trusted
+        res.append(RaggedTensor(out.cpu().numpy(), oo.cpu().numpy()) if as_np else RaggedTensor._trusted(out, oo))
     return res
 
 

@@ -345,6 +345,31 @@ def test_features(skb, golden):
     eq(h.values, golden["fnv.hash"])
 
 
+def test_deferred_feature_checks(skb, cuda):
+    """deferred_checks(): bucketize's NaN ValueError is raised at the context
+    exit / check_deferred() instead of per call; results are unchanged."""
+    import torch
+    edges = np.linspace(0.05, 0.95, 10, dtype=np.float32)
+    vals = np.random.default_rng(3).random(1000, dtype=np.float32)
+    rt = skb.RaggedTensor(torch.from_numpy(vals).to(cuda), torch.tensor([0, 1000]).to(cuda))
+    with skb.deferred_checks():
+        got = skb.bucketize(rt, edges)
+    eq(got.values, O.bucketize_values(vals, edges))
+    bad = vals.copy()
+    bad[517] = np.nan
+    rb = skb.RaggedTensor(torch.from_numpy(bad).to(cuda), torch.tensor([0, 1000]).to(cuda))
+    with pytest.raises(ValueError, match="NaN"):
+        with skb.deferred_checks():
+            skb.bucketize(rb, edges)  # no exception here
+            skb.bucketize(rt, edges)
+    with skb.deferred_checks():
+        skb.bucketize(rb, edges)
+        with pytest.raises(ValueError, match="NaN"):
+            skb.check_deferred()
+    with pytest.raises(ValueError, match="NaN"):
+        skb.bucketize(rb, edges)  # outside: synchronous, as the reference
+
+
 def test_cross_many(skb, golden, cuda):
     """cross_many == cross per pair, with the sizes read back or given."""
     import torch
