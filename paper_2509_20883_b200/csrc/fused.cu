@@ -1358,6 +1358,9 @@ static int adam_variant() {
   static int v = env_int("SKB_ADAM_VARIANT", 0);
   return v;
 }
+static bool adam_tma_fits(int mode, int D, int64_t recent_long_runs) {
+  return mode == 0 && D >= 48 && recent_long_runs == 0;
+}
 static int pool_variant() {
   static int v = env_int("SKB_POOL_VARIANT", 0);
   return v;
@@ -1724,7 +1727,13 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     } else {
       // measured on B200 (C2, D=64): R=1 at 4 blocks/SM 0.59 ms; R=2/4 0.60;
       // R=2/3 0.70; R=1/6 (spills) 0.68; R=2/2 0.81 — occupancy beats ILP here
-      switch (adam_variant()) {
+      // default: the TMA ring for singleton-heavy sum batches of wide rows
+      // (C2: 0.855 vs 0.904 ms/step), the register kernel otherwise — mean
+      // bags (per-position division), narrow rows (per-copy TMA cost) and
+      // hot-id batches (extra gradient rows per run): C5's five tables 6.1 ->
+      // 3.4 ms, C3 1.13 -> 0.91 ms, C4 7.99 -> 7.76 ms (B200)
+      const int var = adam_variant() ? adam_variant() : (adam_tma_fits(mode, D, c->lf_last) ? 0 : 2);
+      switch (var) {
         case 1: k_fused_adam<4, 2, 4><<<grid, 256, 0, s>>>(SKB_ADAM_ARGS); break;
         case 2: k_fused_adam<4, 1, 5><<<grid, 256, 0, s>>>(SKB_ADAM_ARGS); break;
         case 3: k_fused_adam<4, 1, 4><<<grid, 256, 0, s>>>(SKB_ADAM_ARGS); break;
@@ -1750,12 +1759,13 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     GraphKey k;
     int64_t* v = k.v;
     v[0] = t->gen; v[1] = B.gen; v[2] = (int64_t)dpooled; v[3] = n; v[4] = (int64_t)B.bag_offs; v[5] = B.G;
-    v[6] = B.mode; v[7] = B.tile_k; v[8] = c->pack_gen; v[9] = deep;
+    v[6] = B.mode; v[7] = B.tile_k; v[8] = c->pack_gen; v[9] = deep;  // deep also picks the fold kernel
     B.g_bwd.run(k, s, c->cap, B.step, &a, work);
   } else {
     work(s);
   }
-  if (n > 0 && D % 4 == 0 && cudaEventQuery(c->lf_ev) != cudaErrorNotReady) {  // one readback in flight
+  // sampled every 4th backward: a heuristic input, and small steps are launch-bound
+  if (n > 0 && D % 4 == 0 && (c->bwd_count & 3) == 0 && cudaEventQuery(c->lf_ev) != cudaErrorNotReady) {
     SKB_CUDA(cudaMemcpyAsync(c->lf_host, B.dev + 3, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     SKB_CUDA(cudaEventRecord(c->lf_ev, s));
   }
