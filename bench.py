@@ -533,7 +533,10 @@ def run_dist(args):
         b = skb.PackedBatch(lt, mem, make_batch(rank, k, B), offs)
         batches.append(b)
         dps.append(torch.empty((b.num_bags, DIM), device="cuda").normal_(0.0, 1e-2, generator=gen))
-    stepper = DistSparseStep(lt)
+    # rows / grads over peer memory (CUDA IPC windows, NVLink P2P stores from
+    # the producing kernel); BENCH_TRANSPORT=nccl: all_to_all_v instead
+    transport = os.environ.get("BENCH_TRANSPORT", "p2p")
+    stepper = DistSparseStep(lt, transport=transport)
     pooled = torch.empty((batches[0].num_bags, DIM), device="cuda")
     step_no = [0]
 
@@ -587,6 +590,8 @@ def run_dist(args):
     torch.cuda.synchronize()
     dist.barrier()
     clk.__exit__(None, None, None)
+    if stepper.win is not None:
+        stepper.win.close_all()
     t = torch.tensor([ev0.elapsed_time(ev1), e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t[0].item()) / args.steps
@@ -603,7 +608,9 @@ def run_dist(args):
             "config": {"workload": "C2 Criteo-shape DLRM sparse step, row-sharded over GPUs: 26 x dim64, "
                                    "uniform ids [0,1e6) per feature, bag length 1, sum, SparseAdamW, warm",
                        "global_batch": B * world, "per_gpu_batch": B, "features": F_FEATURES, "dim": DIM,
-                       "parallelism": f"row-sharded x{world}, NCCL all-to-all (ids, rows, grads)",
+                       "parallelism": f"row-sharded x{world}: ids all_to_all_v; rows and grads "
+                                      + ("stored into peers' IPC windows by the producing kernels"
+                                         if transport == "p2p" else "all_to_all_v"),
                        "l2": "inputs larger than L2"},
             "samples_per_s": world * B / (ms_step / 1e3),
             "roofline": {"bound": "hbm", "kernel": "step (rank-0 local HBM bytes)", "achieved": sb / ms_step / 1e6,

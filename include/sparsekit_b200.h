@@ -342,6 +342,27 @@ int skb_reader_column(skb_reader_t r, int64_t j, const int64_t** row_offsets, co
                       int64_t* n_values, const int64_t** str_offsets, int64_t* blob_bytes);
 int skb_reader_close(skb_reader_t r);
 
+/* ---- peer-memory transport of the row-sharded exchange ----
+ * Replaces distributed.py's rows / grads all_to_all_v: the producing kernel
+ * stores every row straight into the consuming rank's window (CUDA IPC
+ * memory; NVLink P2P stores between GPUs).  Handles are 64-byte
+ * cudaIpcMemHandle_t blobs, exchanged by the caller (all_gather). */
+int skb_ipc_alloc(int64_t bytes, void** ptr_out, void* handle_out);
+int skb_ipc_open(const void* handle, void** ptr_out);
+int skb_ipc_close(void* ptr);
+int skb_ipc_free(void* ptr);
+/* owner side of the lookup: for the q-th id received (requester j = segment
+ * of q in recv_prefix[0..R]), w row of slot slots_u[inv[q]] -> window_j at row
+ * dst_base[j] + q - recv_prefix[j].  Device arrays: slots_u, inv,
+ * recv_prefix, peer_windows (float*[R]), dst_base. */
+int skb_p2p_send_rows(skb_table_t t, const int64_t* slots_u, const int64_t* inv, int64_t nrecv,
+                      const int64_t* recv_prefix, int32_t num_ranks, float* const* peer_windows,
+                      const int64_t* dst_base, void* stream);
+/* requester side of the update: row i of rows[n, dim] (owner s = segment of i
+ * in seg_prefix) -> window_s at row dst_base[s] + i - seg_prefix[s]. */
+int skb_p2p_send_grads(const float* rows, int64_t dim, int64_t n, const int64_t* seg_prefix, int32_t num_ranks,
+                       float* const* peer_windows, const int64_t* dst_base, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,6 +82,12 @@ _SIGS = {
     "skb_fused_forward_tile": ([_p, _p, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_u64), _i32, _i32, _p, _i64,
                                 ctypes.POINTER(_i64), _i64, ctypes.c_float, _i64, _p, _p], ctypes.c_int),
     "skb_fused_backward": ([_p, _p, ctypes.POINTER(AdamScalars), _p], ctypes.c_int),
+    "skb_ipc_alloc": ([_i64, ctypes.POINTER(_p), _p], ctypes.c_int),
+    "skb_ipc_open": ([_p, ctypes.POINTER(_p)], ctypes.c_int),
+    "skb_ipc_close": ([_p], ctypes.c_int),
+    "skb_ipc_free": ([_p], ctypes.c_int),
+    "skb_p2p_send_rows": ([_p, _p, _p, _i64, _p, _i32, _p, _p, _p], ctypes.c_int),
+    "skb_p2p_send_grads": ([_p, _i64, _i64, _p, _i32, _p, _p, _p], ctypes.c_int),
     "skb_fused_last_unique": ([_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p], ctypes.c_int),
     "skb_fused_stats_async": ([_p, _p, _p], ctypes.c_int),
     "skb_fused_profile": ([_p, _i64, _p], ctypes.c_int),

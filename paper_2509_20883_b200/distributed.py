@@ -58,6 +58,28 @@ class Comm:
         self.dist.all_to_all_single(r, s, group=self.group)
         return [int(x) for x in r.cpu().tolist()]
 
+    def count_matrix(self, send_counts):
+        """All ranks' per-owner counts, C[r][s] (one all_gather + one readback)."""
+        import torch
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        s = torch.as_tensor(list(send_counts), dtype=torch.int64, device=dev)
+        out = [torch.empty_like(s) for _ in range(self.size)]
+        self.dist.all_gather(out, s, group=self.group)
+        return [[int(x) for x in t.cpu().tolist()] for t in out]
+
+    def barrier_after_device_writes(self):
+        """Order every rank's peer-memory stores before any rank reads them:
+        a one-element all-reduce on the stream (NCCL: no host sync), or a
+        device sync + host barrier (gloo)."""
+        import torch
+        if self.backend == "nccl":
+            if getattr(self, "_one", None) is None:
+                self._one = torch.zeros(1, device="cuda")
+            self.dist.all_reduce(self._one, group=self.group)
+        else:
+            torch.cuda.synchronize()
+            self.dist.barrier(group=self.group)
+
     def a2av(self, send, send_counts, recv_counts):
         """all_to_all_v along dim 0 with per-peer splits."""
         import torch
@@ -190,6 +212,68 @@ def dist_grad_update(lt, ids_d, grads, cfg, step: int):
     exchange_grad_update(comm, GpuOps(), lt.local_table, ids_d, g, cfg, step, lt.dim)
 
 
+class P2PWindows:
+    """Receive windows in CUDA IPC memory that every peer maps: the producing
+    kernel stores rows straight into the consuming rank's window (NVLink P2P
+    stores between GPUs; ranks sharing one GPU in the tests).  Grown
+    collectively: every rank takes the same decision from the all-gathered
+    count matrix, then handles are re-exchanged."""
+
+    def __init__(self, comm: "Comm", dim: int):
+        self.comm, self.dim = comm, dim
+        self.cap, self.local, self.opened, self.peers_dev = {}, {}, {}, {}
+
+    def ensure(self, name: str, rows_per_rank) -> None:
+        need = max(rows_per_rank) if rows_per_rank else 0
+        if need <= self.cap.get(name, 0) and name in self.local:
+            return
+        import ctypes as C
+        import torch
+        cap = max(need, int(self.cap.get(name, 0) * 1.5), 1024)
+        self.close(name)
+        ptr, handle = C.c_void_p(), (C.c_char * 64)()
+        N.call("skb_ipc_alloc", cap * self.dim * 4, C.byref(ptr), handle)
+        handles = [None] * self.comm.size
+        self.comm.dist.all_gather_object(handles, bytes(handle), group=self.comm.group)
+        peers = []
+        for j, h in enumerate(handles):
+            if j == self.comm.rank:
+                peers.append(ptr.value)
+            else:
+                q = C.c_void_p()
+                N.call("skb_ipc_open", (C.c_char * 64).from_buffer_copy(h), C.byref(q))
+                peers.append(q.value)
+                self.opened.setdefault(name, []).append(q.value)
+        self.local[name], self.cap[name] = ptr.value, cap
+        self.peers_dev[name] = torch.tensor(peers, dtype=torch.int64, device="cuda")
+
+    def ptr(self, name: str):
+        import ctypes as C
+        return C.c_void_p(self.local[name])
+
+    def close(self, name: str) -> None:
+        if name not in self.local:
+            return
+        import ctypes as C
+        import torch
+        torch.cuda.synchronize()
+        self.comm.dist.barrier(group=self.comm.group)  # nobody touches the old windows any more
+        for q in self.opened.pop(name, []):
+            N.call("skb_ipc_close", C.c_void_p(q))
+        N.call("skb_ipc_free", C.c_void_p(self.local.pop(name)))
+
+    def close_all(self) -> None:
+        for name in list(self.local):
+            self.close(name)
+
+
+def _prefix(xs):
+    out = [0]
+    for x in xs:
+        out.append(out[-1] + int(x))
+    return out
+
+
 class DistSparseStep:
     """Fused multi-GPU sparse step for one row-sharded logical table.
 
@@ -201,12 +285,16 @@ class DistSparseStep:
               all-to-all -> owner cross-rank fold in rank order -> AdamW.
     """
 
-    def __init__(self, lt, comm: Comm | None = None):
+    def __init__(self, lt, comm: Comm | None = None, transport: str = "nccl"):
         if not lt.dist:
             raise ValueError("DistSparseStep needs a LogicalTable built with dist=True")
+        if transport not in ("nccl", "p2p"):
+            raise ValueError(f"unknown transport {transport!r}")
         self.lt = lt
         self.comm = comm or Comm(lt.group)
         self.ops = GpuOps()
+        self.transport = transport
+        self.win = P2PWindows(self.comm, lt.dim) if transport == "p2p" else None
         self._ctx = None
         self.last_counts = None
 
@@ -238,21 +326,40 @@ class DistSparseStep:
             keys = batch.ids
         uniq, counts, inv_s, inv_p = ops.partition(keys, S)
         gidx = ops.global_index(counts, inv_s, inv_p).to(t.int32)
-        recv_counts = comm.counts(counts)
+        cmat = None
+        if self.win is None:
+            recv_counts = comm.counts(counts)
+        else:
+            cmat = comm.count_matrix(counts)
+            recv_counts = [cmat[r][comm.rank] for r in range(S)]
         recv_ids = comm.a2av(uniq, counts, recv_counts)
         u2, inv2 = ops.dedup(recv_ids)
         offs = ops.admit(lt.local_table, u2, step)
-        rows2 = ops.gather(lt.local_table, offs)
-        send_rows = ops.take_rows(rows2, inv2)
-        recv_rows = comm.a2av(send_rows, recv_counts, counts)
+        if self.win is None:
+            rows2 = ops.gather(lt.local_table, offs)
+            send_rows = ops.take_rows(rows2, inv2)
+            recv_rows = comm.a2av(send_rows, recv_counts, counts)
+            rows_ptr = N.ptr(recv_rows)
+        else:
+            # owner gathers each requested row straight into the requester's window
+            me = comm.rank
+            self.win.ensure("rows", [sum(cmat[j]) for j in range(S)])
+            nrecv = int(sum(recv_counts))
+            pre = N.to_dev(np.array(_prefix(recv_counts), np.int64), "int64")
+            base = N.to_dev(np.array([sum(cmat[j][:me]) for j in range(S)], np.int64), "int64")
+            if nrecv:
+                N.call("skb_p2p_send_rows", lt.local_table.handle, N.ptr(offs), N.ptr(inv2), nrecv, N.ptr(pre), S,
+                       N.ptr(self.win.peers_dev["rows"]), N.ptr(base), N.stream_ptr())
+            comm.barrier_after_device_writes()
+            rows_ptr = self.win.ptr("rows")
         pooled = out if out is not None else N.empty((G, D), "float32")
         mcode = {"sum": 0, "mean": 1}[mode]
         any_seq = int(bool((batch.strategy == 0).any()))
         if G:
-            N.call("skb_pool_indexed", N.ptr(recv_rows), D, N.ptr(gidx), N.ptr(batch.bag_offs), G, N.ptr(mdev), F,
+            N.call("skb_pool_indexed", rows_ptr, D, N.ptr(gidx), N.ptr(batch.bag_offs), G, N.ptr(mdev), F,
                    any_seq, mcode, D, N.ptr(pooled), N.stream_ptr())
         self._ctx = dict(batch=batch, counts=counts, recv_counts=recv_counts, gidx=gidx, U=int(sum(counts)),
-                         inv2=inv2, u2=u2, offs=offs, mode=mcode)
+                         inv2=inv2, u2=u2, offs=offs, mode=mcode, cmat=cmat)
         self.last_counts = {"send": list(counts), "recv": list(recv_counts), "owner_unique": int(u2.numel())}
         return pooled
 
@@ -268,7 +375,26 @@ class DistSparseStep:
         if n:
             N.call("skb_fold_bags", N.ptr(g), D, N.ptr(c["gidx"]), n, c["U"], N.ptr(b.bag_offs), b.num_bags,
                    c["mode"], max(c["U"] - 1, 0), N.ptr(agg), N.stream_ptr())
-        recv_g = comm.a2av(agg[: c["U"]], c["counts"], c["recv_counts"])
-        g2 = ops.fold(recv_g, c["inv2"], c["u2"].numel())
+        if self.win is None:
+            recv_g = comm.a2av(agg[: c["U"]], c["counts"], c["recv_counts"])
+            g2 = ops.fold(recv_g, c["inv2"], c["u2"].numel())
+        else:
+            # requester stores its folded gradients straight into each owner's
+            # window, at the owner's rank-ordered receive offset
+            cmat, S, me = c["cmat"], comm.size, comm.rank
+            self.win.ensure("grads", [sum(cmat[r][s] for r in range(S)) for s in range(S)])
+            seg = N.to_dev(np.array(_prefix(c["counts"]), np.int64), "int64")
+            base = N.to_dev(np.array([sum(cmat[r][s] for r in range(me)) for s in range(S)], np.int64), "int64")
+            if c["U"]:
+                N.call("skb_p2p_send_grads", N.ptr(agg), D, c["U"], N.ptr(seg), S, N.ptr(self.win.peers_dev["grads"]),
+                       N.ptr(base), N.stream_ptr())
+            comm.barrier_after_device_writes()
+            nrecv = int(sum(c["recv_counts"]))
+            U2 = c["u2"].numel()
+            g2 = N.empty((max(U2, 1), D), "float32")
+            if nrecv or U2:
+                N.call("skb_grad_fold", self.win.ptr("grads"), nrecv, D, N.ptr(c["inv2"]), U2, N.ptr(g2),
+                       N.stream_ptr())
+            g2 = g2[:U2]
         ops.adam(lt.local_table, c["offs"], g2, cfg, step)
         self._ctx = None

@@ -173,7 +173,7 @@ def fused_inputs(rank, k):
     return ids, offs, dp
 
 
-def _fused_worker(rank, port, out_dir):
+def _fused_worker(rank, port, out_dir, transport="nccl"):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -182,7 +182,7 @@ def _fused_worker(rank, port, out_dir):
     from paper_2509_20883_b200.distributed import DistSparseStep
     torch.cuda.set_device(0)
     lt = skb.LogicalTable("dim4", DIM, S, seed=3, members=MEMBERS, namespaced=True, dist=True)
-    stepper = DistSparseStep(lt)
+    stepper = DistSparseStep(lt, transport=transport)
     cfg = skb.AdamConfig(lr=LR, weight_decay=0.01, variant="adamw")
     pooled = []
     for k in range(STEPS):
@@ -192,6 +192,8 @@ def _fused_worker(rank, port, out_dir):
         stepper.backward(torch.from_numpy(dp).cuda(), cfg, k + 1)
     ex = lt.local_table.export_rows()
     np.savez(os.path.join(out_dir, f"fused{rank}.npz"), *pooled, ids=ex[0], w=ex[1], m=ex[2], v=ex[3])
+    if stepper.win is not None:
+        stepper.win.close_all()
     dist.barrier()
     dist.destroy_process_group()
 
@@ -230,6 +232,23 @@ def test_dist_sparse_step_gpu(tmp_path, cuda):
         assert np.array_equal(z["ids"], ex[0])
         for key, j in (("w", 1), ("m", 2), ("v", 3)):
             np.testing.assert_allclose(z[key], ex[j], rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.gpu
+def test_dist_sparse_step_p2p_transport(tmp_path, cuda):
+    """Peer-memory transport (rows gathered straight into the requester's IPC
+    window, folded grads stored straight into the owner's window) is
+    bit-identical to the all_to_all transport (2 ranks sharing one GPU)."""
+    a, b = tmp_path / "a2a", tmp_path / "p2p"
+    a.mkdir()
+    b.mkdir()
+    mp.spawn(_fused_worker, args=(_free_port(), str(a), "nccl"), nprocs=S, join=True)
+    mp.spawn(_fused_worker, args=(_free_port(), str(b), "p2p"), nprocs=S, join=True)
+    for r in range(S):
+        za, zb = np.load(a / f"fused{r}.npz"), np.load(b / f"fused{r}.npz")
+        assert sorted(za.files) == sorted(zb.files)
+        for k in za.files:
+            assert np.array_equal(za[k].view(np.uint8), zb[k].view(np.uint8)), k
 
 
 @pytest.mark.gpu
