@@ -53,6 +53,7 @@ def traffic(kind, **k):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--repeats", type=int, default=20)
+    ap.add_argument("--rows", action="store_true", help="also measure the other SURVEY §8(a) rows")
     args = ap.parse_args()
     import torch
     import paper_2509_20883_b200 as skb
@@ -165,6 +166,83 @@ def main():
     report("gather", traffic("gather", n=R, d=D), sec, "1M x 16 (trusted offsets)")
     sec = timed(lambda: N.call("skb_table_write_rows", table.handle, N.ptr(sidx), R, 0, N.ptr(newr), N.stream_ptr()))
     report("scatter", traffic("scatter", n=R, d=D), sec, "1M x 16 (BlockStore.write, range-checked)")
+
+    # ---- the remaining SURVEY §8(a) rows through the public API (device tensors;
+    # bytes = each input read once + each output written once)
+    if args.rows:
+        rows_out = []
+
+        def row(tag, name, nbytes, fn, shape):
+            sec = timed(fn)
+            rows_out.append({"row": tag, "op": name, "shape": shape, "bytes": int(nbytes), "time_us": sec * 1e6,
+                             "achieved_gbs": nbytes / sec / 1e9, "mbu_pct": 100 * nbytes / sec / peak})
+            print(json.dumps(rows_out[-1]), flush=True)
+
+        n = 1_000_000
+        ids1 = torch.from_numpy(rng.integers(-(1 << 62), 1 << 62, n, dtype=np.int64)).cuda()
+        plan8 = skb.ShardPlan(8)
+        row("a1", "shard_of (mix64 % S)", 16 * n, lambda: plan8.shard_of(ids1), "1M ids, 8 shards")
+        lt = skb.LogicalTable("dim16", 16, 1, seed=0, members=["m0"], namespaced=True)
+        row("a2", "keys_for (namespaced key)", 16 * n, lambda: lt.keys_for("m0", ids1), "1M ids")
+        row("a4", "initial_rows", 8 * n + 64 * n, lambda: skb.initial_rows(3, ids1, 16), "1M ids x 16")
+        t2 = skb.EmbeddingTable("a5", 16, seed=0, capacity_hint=2 * n)
+        uniq = torch.arange(n, dtype=torch.int64, device="cuda") * 7919
+        t2.lookup_or_insert(uniq, 1)
+        # warm: every id present -> probe + offsets + last_step (duplicate check included)
+        row("a5", "lookup_or_insert (warm, dup-checked)", 8 * n + 16 * n + 8 * n + 8 * n,
+            lambda: t2.lookup_or_insert(uniq, 2), "1M unique ids, all present")
+        offs_u = t2.lookup_or_insert(uniq, 2)
+        gsrc = torch.randn((n, 16), device="cuda")
+        cfg = skb.AdamConfig(lr=1e-3, weight_decay=0.01, variant="adamw")
+        row("a13", "sparse_adam_step (distinct-checked)", 8 * n + 64 * n + 2 * 192 * n,
+            lambda: skb.sparse_adam_step(t2.store, offs_u, gsrc, cfg, 3), "1M rows x 16, AdamW")
+        pos = torch.from_numpy(rng.integers(0, n // 4, n, dtype=np.int64)).cuda()
+        pr = skb.unique_partition(pos, skb.ShardPlan(4))
+        per = [torch.randn((len(x), 16), device="cuda") for x in pr.shard_ids]
+        row("a8", "PartitionResult.restore", 16 * n + 64 * n + 64 * pr.num_unique, lambda: pr.restore(per),
+            "1M positions x 16, 4 shards")
+        grads = torch.randn((n, 16), device="cuda")
+        inv = pr.inverse_pos + torch.tensor(pr._bases(), device="cuda")[pr.inverse_shard]
+        fout = torch.empty((pr.num_unique, 16), device="cuda")
+        row("a12", "grad pre-aggregation (ordered fold)", 8 * n + 64 * n + 64 * pr.num_unique,
+            lambda: N.call("skb_grad_fold", N.ptr(grads), n, 16, N.ptr(inv.contiguous()), pr.num_unique, N.ptr(fout),
+                           N.stream_ptr()), "1M positions x 16 -> ~250K rows")
+        row("a19", "load_stats", 8 * n + 64, lambda: skb.load_stats(ids1, plan8), "1M ids, 8 shards")
+        tok = rng.integers(0, 1_000_000, n).astype("S7")
+        ln = np.char.str_len(tok).astype(np.int64)
+        so = np.zeros(n + 1, np.int64)
+        np.cumsum(ln, out=so[1:])
+        blob = tok.view(np.uint8).reshape(n, 7)[np.arange(7)[None, :] < ln[:, None]]
+        bd, sd = torch.from_numpy(blob).cuda(), torch.from_numpy(so).cuda()
+        row_offs = torch.arange(0, n + 1, 4, dtype=torch.int64, device="cuda")
+        row("a15", "hash_feature (FNV-1a, packed strings)", len(blob) + 8 * (n + 1) + 8 * n,
+            lambda: skb.hash_feature_packed(bd, sd, row_offs), "1M strings (~6 B)")
+        R = 65536
+        la, lb = rng.integers(0, 6, R), rng.integers(0, 6, R)
+        oa = np.concatenate([[0], np.cumsum(la)]).astype(np.int64)
+        ob = np.concatenate([[0], np.cumsum(lb)]).astype(np.int64)
+        A = skb.RaggedTensor(torch.from_numpy(rng.integers(0, 1 << 40, oa[-1])).cuda(), torch.from_numpy(oa).cuda())
+        Bt = skb.RaggedTensor(torch.from_numpy(rng.integers(0, 1 << 40, ob[-1])).cuda(), torch.from_numpy(ob).cuda())
+        tot = int((la * lb).sum())
+        row("a18", "cross (pairwise FNV)", 8 * (oa[-1] + ob[-1]) + 24 * R + 8 * tot,
+            lambda: skb.cross_many([(A, Bt)], sizes=[tot]), f"64K rows, {tot} outputs")
+        seq_o = torch.arange(0, n + 1, 250, dtype=torch.int64, device="cuda")
+        RT = skb.RaggedTensor(ids1, seq_o)
+        row("a20", "RaggedTensor.truncate(100, tail)", 8 * n + 8 * (n // 250 + 1) * 2 + 8 * 100 * (n // 250),
+            lambda: RT.truncate(100, "tail"), "4000 rows x 250 -> 100")
+        t3 = skb.EmbeddingTable("a14", 16, seed=0, evict_threshold=1, capacity_hint=2 * n)
+
+        def evict_cycle():
+            t3.lookup_or_insert(uniq, 10)
+            t3.evict(20)  # every row stale
+
+        row("a14", "admit 1M + evict 1M (cycle)", 2 * (8 * n + 16 * n + 192 * n), evict_cycle,
+            "1M ids admitted then evicted")
+        print("\n| §8 row | op | shape | time (us) | GB/s | % of peak |")
+        print("|---|---|---|---|---|---|")
+        for r in rows_out:
+            print(f"| {r['row']} | {r['op']} | {r['shape']} | {r['time_us']:.1f} | {r['achieved_gbs']:.0f} | "
+                  f"{r['mbu_pct']:.1f} |")
 
     print(f"\n| op | shape | time (us) | GB/s | MBU on B200 (% of {peak_kind} peak) | RecIS MBU on H20 (paper) |")
     print("|---|---|---|---|---|---|")
