@@ -252,7 +252,10 @@ def c4(args):
     import paper_2509_20883_b200 as skb
     G, L, D = 8192, 1000, 64
     n = G * L
-    lt = skb.LogicalTable("seq", D, 1, seed=4, members=["seq"], namespaced=False, capacity_hint=3_000_000)
+    # capacity: the table's ~2.35M rows plus three steps of positions, the
+    # host's no-sync admission bound (every in-flight position a possible new
+    # row); a tighter arena makes every step synchronise to refresh counters
+    lt = skb.LogicalTable("seq", D, 1, seed=4, members=["seq"], namespaced=False, capacity_hint=2_400_000 + 3 * n)
     offs_d = torch.arange(0, n + 1, L, dtype=torch.int64, device="cuda")
     P = 2
     ids = [torch.from_numpy(np.random.Generator(np.random.PCG64(4 + k)).zipf(1.1, n).astype(np.int64)).cuda()
@@ -286,12 +289,25 @@ def c4(args):
 
     run(max(args.warmup, 3))
     torch.cuda.synchronize()
+    import ctypes
+    from paper_2509_20883_b200 import _native as N
+    if fused:
+        N.call("skb_fused_profile", lt.local_table.handle, args.steps, N.stream_ptr())
     e0, e1 = _events()
     e0.record()
     run(args.steps)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
+    phase_ms = {}
+    if fused:
+        buf = (ctypes.c_float * args.steps)()
+        for p_, name in enumerate(B.PHASES):
+            cnt = ctypes.c_int64()
+            N.call("skb_fused_profile_read", lt.local_table.handle, p_, buf, args.steps, ctypes.byref(cnt))
+            vals = list(buf)[: cnt.value]
+            phase_ms[name] = [round(v, 3) for v in vals]
+        N.call("skb_fused_profile", lt.local_table.handle, 0, N.stream_ptr())
     u = int(torch.unique(ids[step[0] % P]).numel())
     sb = B.step_bytes(n, n, u, 0, D)  # G' = G*k = n tile rows
 
@@ -319,7 +335,7 @@ def c4(args):
                           "drop-in API path: all_to_all_lookup -> segment_tile -> all_to_all_grad_update"),
            "global_batch": G, "seq_len": L, "dim": D, "parallelism": "single shard",
            "l2": "inputs larger than L2 (2.1 GB tile per step)"},
-          {"unique_rows_per_step": u})
+          {"unique_rows_per_step": u, "kernels_ms_per_step": phase_ms})
 
 
 # ---------------------------------------------------------------------------

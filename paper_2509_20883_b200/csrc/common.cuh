@@ -218,6 +218,10 @@ void select_flagged_index32(const uint8_t* flags, int64_t n, uint32_t* out, int6
 // stable radix sort of (uint32 key, uint32 val) pairs on bits [0, end_bit)
 void sort_pairs_u32(const uint32_t* k_in, uint32_t* k_out, const uint32_t* v_in, uint32_t* v_out,
                     int64_t n, int end_bit, cudaStream_t s);
+// the same sort with caller-owned temp storage (no allocation per call)
+size_t sort_pairs_u32_bytes(int64_t n, int end_bit);
+void sort_pairs_u32_ws(const uint32_t* k_in, uint32_t* k_out, const uint32_t* v_in, uint32_t* v_out, int64_t n,
+                       int end_bit, void* ws, size_t ws_bytes, cudaStream_t s);
 // stable radix sort of (int64 key, int64 val) pairs (signed order)
 void sort_pairs_i64(const int64_t* k_in, int64_t* k_out, const int64_t* v_in, int64_t* v_out,
                     int64_t n, cudaStream_t s);

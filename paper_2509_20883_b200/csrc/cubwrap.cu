@@ -105,6 +105,19 @@ void sort_pairs_u32(const uint32_t* k_in, uint32_t* k_out, const uint32_t* v_in,
       s);
 }
 
+size_t sort_pairs_u32_bytes(int64_t n, int end_bit) {
+  size_t bytes = 0;
+  SKB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                           (const uint32_t*)nullptr, (uint32_t*)nullptr, n, 0, end_bit, nullptr));
+  return bytes;
+}
+
+void sort_pairs_u32_ws(const uint32_t* k_in, uint32_t* k_out, const uint32_t* v_in, uint32_t* v_out, int64_t n,
+                       int end_bit, void* ws, size_t ws_bytes, cudaStream_t s) {
+  if (n == 0) return;
+  SKB_CUDA(cub::DeviceRadixSort::SortPairs(ws, ws_bytes, k_in, k_out, v_in, v_out, n, 0, end_bit, s));
+}
+
 void sort_pairs_i64(const int64_t* k_in, int64_t* k_out, const int64_t* v_in, int64_t* v_out,
                     int64_t n, cudaStream_t s) {
   if (n == 0) return;

@@ -74,6 +74,8 @@ struct BatchCtx {
   MemberDev* members = nullptr;
   int64_t members_cap = 0;
   std::vector<MemberDev> members_host;
+  void* sort_ws = nullptr;              // CUB temp storage of the index sort (persistent: no per-step
+  size_t sort_ws_bytes = 0;             //  allocation on the index stream)
   MemberDev* members_pinned = nullptr;  // upload staging (ragged batches change it every step)
   cudaEvent_t members_ev = nullptr;     // the staging buffer's last upload
   // identity + metadata of the prepared batch
@@ -131,6 +133,7 @@ static void batch_free(BatchCtx& B) {
   cudaFree(B.scratch);
   cudaFree(B.dev);
   cudaFree(B.members);
+  cudaFree(B.sort_ws);
   if (B.members_pinned) cudaFreeHost(B.members_pinned);
   if (B.members_ev) cudaEventDestroy(B.members_ev);
   cudaFree(B.longs);
@@ -1489,6 +1492,16 @@ static void fused_prepare(Table* t, const BatchArgs& a, cudaStream_t s) {
   if (grow) SKB_CUDA(cudaStreamSynchronize(x));
   if (t->arena_rows >= (1ll << 32) - 1) raise(SKB_E_UNSUPPORTED, t->arena_rows, "fused step: > 2^32 rows");
   batch_reserve(B, a.n, a.F, x);
+  {  // persistent CUB workspace of the index sort (32 key bits: enough for any arena)
+    const size_t need = sort_pairs_u32_bytes(B.cap_n > a.n ? B.cap_n : a.n, 32);
+    if (need > B.sort_ws_bytes) {
+      uint8_t* w = static_cast<uint8_t*>(B.sort_ws);
+      realloc_dev(w, (int64_t)need, x);
+      B.sort_ws = w;
+      B.sort_ws_bytes = need;
+      B.gen++;
+    }
+  }
   std::vector<MemberDev> mh(a.F + 1);
   bool any_seq = false;
   for (int f = 0; f <= a.F; ++f) {
@@ -1544,7 +1557,8 @@ static void fused_prepare(Table* t, const BatchArgs& a, cudaStream_t s) {
     else
       k_bag_of<<<grid_for(G > 0 ? G : 1, 256), 256, 0, x>>>(a.bag_offs, G, B.bag);
     SKB_LAUNCH_CHECK();
-    sort_pairs_u32(B.slot, B.skey, B.bag, B.sval, n, bits_for((uint64_t)(t->arena_rows - 1)), x);
+    const int sbits = bits_for((uint64_t)(t->arena_rows - 1));
+    sort_pairs_u32_ws(B.slot, B.skey, B.bag, B.sval, n, sbits, B.sort_ws, B.sort_ws_bytes, x);
     prof_mark(c, P_SORT, 1, x);
   }
   };

@@ -19,7 +19,12 @@ namespace skb {
 
 constexpr int kLongRun = 32;  // runs longer than this are deferred
 constexpr uint32_t kNoPack = 0xFFFFFFFFu;  // LongRun.pad: not packed
-constexpr int64_t kMegaRun = 8192;         // runs at least this long are packed for TMA streaming
+constexpr int64_t kMegaRunMin = 2048;      // smallest run ever packed for TMA streaming
+// runs at least this long are packed (SKB_LF_MEGA overrides, >= kMegaRunMin)
+inline int64_t mega_run_threshold() {
+  static const int64_t v = getenv("SKB_LF_MEGA") ? atoll(getenv("SKB_LF_MEGA")) : 8192;
+  return v < kMegaRunMin ? kMegaRunMin : v;
+}
 
 struct LongRun {
   uint32_t key, jh, je, pad;
@@ -40,7 +45,7 @@ __device__ __forceinline__ void push_long_run(LongRun* list, int64_t* count, int
 //    gradient rows (row-major stage), each lane signalling `full` when ITS
 //    copies land (cp.async.mbarrier.arrive.noinc).  One SM's outstanding-
 //    request budget caps this at ~25 GB/s.
-//  - mega runs (>= kMegaRun positions, the few hottest ids): k_pack_rows has
+//  - mega runs (>= mega_run_threshold() positions, the hottest ids): k_pack_rows has
 //    already laid the run out as stage IMAGES — each stage transposed to
 //    column-major with a padded column stride PS = TP + 4 — so a stage is
 //    ONE TMA bulk copy, and a consumer lane reads four positions of its
@@ -272,7 +277,7 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
 
 // ---------------------------------------------------------------------------
 // Mega-run packing: the whole grid gathers the gradient rows of the runs of
-// at least kMegaRun positions into stage images (see k_long_fold), so the
+// at least mega_run_threshold() positions into stage images (see k_long_fold), so the
 // CTA folding such a run streams it with one bulk copy per stage.
 struct LongFoldPack {
   float* images = nullptr;    // [cap_images][D * (TP + kLfPad)]
@@ -286,7 +291,7 @@ struct LongFoldPack {
 // one block: exclusive scans of (is mega, stage images) over the run list;
 // run.pad = first image (kNoPack for ordinary runs or past capacity)
 static __global__ void __launch_bounds__(1024) k_pack_plan(LongRun* runs, const int64_t* __restrict__ nruns,
-                                                           int64_t cap, int TP, int64_t cap_images,
+                                                           int64_t cap, int TP, int64_t mega, int64_t cap_images,
                                                            uint32_t* __restrict__ mlist, uint32_t* __restrict__ moff,
                                                            int64_t* __restrict__ mcount) {
   __shared__ int64_t s_c[32], s_l[32];
@@ -303,7 +308,7 @@ static __global__ void __launch_bounds__(1024) k_pack_plan(LongRun* runs, const 
     const int64_t r = b0 + threadIdx.x;
     int64_t len = 0;
     if (r < R) len = (int64_t)runs[r].je - runs[r].jh;
-    const int64_t f = (r < R && len >= kMegaRun) ? 1 : 0, l = f ? (len + TP - 1) / TP : 0;
+    const int64_t f = (r < R && len >= mega) ? 1 : 0, l = f ? (len + TP - 1) / TP : 0;
     int64_t ic = f, il = l;
     for (int o = 1; o < 32; o <<= 1) {
       const int64_t yc = __shfl_up_sync(0xffffffffu, ic, o), yl = __shfl_up_sync(0xffffffffu, il, o);
@@ -426,7 +431,8 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
   // launches are skipped; mega runs then take the cp.async path, same result)
   if (env_pack && expect_mega && pack && pack->images && pack->cap_runs >= cap) {
     const int TP = long_fold_tp(D);
-    k_pack_plan<<<1, 1024, 0, s>>>(runs, nruns, cap, TP, pack->cap_images, pack->mlist, pack->moff, pack->mcount);
+    k_pack_plan<<<1, 1024, 0, s>>>(runs, nruns, cap, TP, mega_run_threshold(), pack->cap_images, pack->mlist,
+                                   pack->moff, pack->mcount);
     SKB_LAUNCH_CHECK();
     const size_t psm = (size_t)TP * (D + 1) * sizeof(float);
     static size_t pset = 0;
@@ -449,7 +455,7 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
 // stage images needed to pack up to `rows` positions of mega runs
 inline int64_t long_fold_pack_images(int64_t rows, int D) {
   const int64_t tp = long_fold_tp(D);
-  return rows / tp + rows / kMegaRun + 1;
+  return rows / tp + rows / kMegaRunMin + 1;
 }
 
 }  // namespace skb

@@ -61,6 +61,13 @@ static void ensure_pool() {
   // keep freed scratch cached in the pool: per-step scratch is then free
   uint64_t thr = 8ull << 30;
   SKB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  // never let an allocation on one stream wait for another stream's pending
+  // free: the index stream's scratch (CUB sort temp storage) reusing a block
+  // the main stream freed made it wait behind fold+Adam (C4/C5 step times
+  // 8 -> 100 ms at random); without internal dependencies the pool takes
+  // fresh (cached) memory instead
+  int no = 0;
+  SKB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no));
   // optional L2 fetch-granularity hint (random 16 B probes vs 128 B lines)
   if (const char* g = getenv("SKB_L2_FETCH")) SKB_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, atoi(g)));
   g_pool_ready[dev] = true;
