@@ -20,10 +20,13 @@ namespace skb {
 constexpr int kLongRun = 32;  // runs longer than this are deferred
 constexpr uint32_t kNoPack = 0xFFFFFFFFu;  // LongRun.pad: not packed
 constexpr int64_t kMegaRunMin = 2048;      // smallest run ever packed for TMA streaming
-// runs at least this long are packed (SKB_LF_MEGA overrides, >= kMegaRunMin)
-inline int64_t mega_run_threshold() {
-  static const int64_t v = getenv("SKB_LF_MEGA") ? atoll(getenv("SKB_LF_MEGA")) : 8192;
-  return v < kMegaRunMin ? kMegaRunMin : v;
+// runs at least this long are packed: 8192 positions, or 2048 for mean bags
+// (their unpacked producers divide row by row, ~4x slower than the 16-byte
+// copies of sum bags); SKB_LF_MEGA overrides (>= kMegaRunMin)
+inline int64_t mega_run_threshold(int mode) {
+  static const int64_t v = getenv("SKB_LF_MEGA") ? atoll(getenv("SKB_LF_MEGA")) : 0;
+  if (v > 0) return v < kMegaRunMin ? kMegaRunMin : v;
+  return mode == 1 ? 2048 : 8192;
 }
 
 struct LongRun {
@@ -45,7 +48,7 @@ __device__ __forceinline__ void push_long_run(LongRun* list, int64_t* count, int
 //    gradient rows (row-major stage), each lane signalling `full` when ITS
 //    copies land (cp.async.mbarrier.arrive.noinc).  One SM's outstanding-
 //    request budget caps this at ~25 GB/s.
-//  - mega runs (>= mega_run_threshold() positions, the hottest ids): k_pack_rows has
+//  - mega runs (>= mega_run_threshold(mode) positions, the hottest ids): k_pack_rows has
 //    already laid the run out as stage IMAGES — each stage transposed to
 //    column-major with a padded column stride PS = TP + 4 — so a stage is
 //    ONE TMA bulk copy, and a consumer lane reads four positions of its
@@ -277,7 +280,7 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
 
 // ---------------------------------------------------------------------------
 // Mega-run packing: the whole grid gathers the gradient rows of the runs of
-// at least mega_run_threshold() positions into stage images (see k_long_fold), so the
+// at least mega_run_threshold(mode) positions into stage images (see k_long_fold), so the
 // CTA folding such a run streams it with one bulk copy per stage.
 struct LongFoldPack {
   float* images = nullptr;    // [cap_images][D * (TP + kLfPad)]
@@ -431,7 +434,7 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
   // launches are skipped; mega runs then take the cp.async path, same result)
   if (env_pack && expect_mega && pack && pack->images && pack->cap_runs >= cap) {
     const int TP = long_fold_tp(D);
-    k_pack_plan<<<1, 1024, 0, s>>>(runs, nruns, cap, TP, mega_run_threshold(), pack->cap_images, pack->mlist,
+    k_pack_plan<<<1, 1024, 0, s>>>(runs, nruns, cap, TP, mega_run_threshold(mode), pack->cap_images, pack->mlist,
                                    pack->moff, pack->mcount);
     SKB_LAUNCH_CHECK();
     const size_t psm = (size_t)TP * (D + 1) * sizeof(float);
