@@ -71,8 +71,14 @@ __host__ __device__ inline int long_fold_tp(int D) {
   const int tp = (kLfStageBytes / (4 * D)) & ~3;
   return tp < 4 ? 4 : (tp > kLfMaxTP ? kLfMaxTP : tp);
 }
-// floats of one stage slot: a row-major stage (TP*D) or a packed image (D*(TP+4))
+// floats of one stage slot: a row-major stage (TP*D) or a packed image
 __host__ __device__ inline int64_t long_fold_stage_f(int D) { return (int64_t)D * (long_fold_tp(D) + kLfPad); }
+// packed image of one 32-column group (min(32, D) columns): the whole slot,
+// column-major with stride PSI = TPI + kLfPad, TPI positions (multiple of 4)
+__host__ __device__ inline int long_fold_img_w(int D) { return D < 32 ? D : 32; }
+__host__ __device__ inline int long_fold_tpi(int D) {
+  return (int)((long_fold_stage_f(D) / long_fold_img_w(D) - kLfPad) & ~3ll);
+}
 constexpr int kLfMaxNC = 16;  // consumer warps
 constexpr int kLfCols = 4;    // columns per consumer lane: dims up to 32 * kLfMaxNC * kLfCols = 2048
 __host__ __device__ inline int long_fold_consumers(int D) {
@@ -100,14 +106,16 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
                             int64_t* __restrict__ last_step, int64_t step, int nst,
                             const float* __restrict__ zrow, const float* __restrict__ packed) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int TP = long_fold_tp(D);
-  const int PS = TP + kLfPad;                   // column stride of a packed image
+  const int TP = long_fold_tp(D);                // positions per row-major stage
+  const int TPI = long_fold_tpi(D);              // positions per packed column-group image
+  const int PS = TPI + kLfPad;                   // column stride of a packed image
   const int64_t stage_f = long_fold_stage_f(D);  // floats per stage slot
   float* buf = reinterpret_cast<float*>(smem_raw);
   uint32_t* idx = reinterpret_cast<uint32_t*>(buf + (int64_t)nst * stage_f);  // [kLfMaxPW][kLfMaxTP]
   uint64_t* full = reinterpret_cast<uint64_t*>(idx + kLfMaxPW * kLfMaxTP);
   uint64_t* empty = full + kLfStages;
   const int NC = long_fold_consumers(D);
+  const int NCG = (D + 31) / 32;  // 32-column groups: work units of a packed run
   const int64_t R = *nruns < cap ? *nruns : cap;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -122,21 +130,28 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
   if (warp >= NC) {  // ---------------- producers: warp pw fills stages it = pw (mod NPW) ----------------
     const int pw = warp - NC, NPW = (int)(blockDim.x >> 5) - NC;
     const int cpr = D / 4;  // 16-byte chunks per row
-    for (int64_t r = blockIdx.x; r < R; r += gridDim.x) {
+    for (int64_t wu = blockIdx.x; wu < R * NCG; wu += gridDim.x) {
+      const int64_t r = wu / NCG;
+      const int cg = (int)(wu - r * NCG);
       const LongRun run = runs[r];
       const bool img = packed && run.pad != kNoPack;
-      for (int64_t p0 = run.jh; p0 < run.je; p0 += TP, ++it) {
+      if (!img && cg > 0) continue;  // unpacked runs: one unit covers every column
+      const int ncol = D - 32 * cg < 32 ? D - 32 * cg : 32;
+      const int step_p = img ? TPI : TP;
+      const int64_t nimg = img ? ((int64_t)run.je - run.jh + TPI - 1) / TPI : 0;  // images per column group
+      for (int64_t p0 = run.jh; p0 < run.je; p0 += step_p, ++it) {
         if ((int)(it % (uint32_t)NPW) != pw) continue;
         const int s = (int)(it % (uint32_t)nst);
         const uint32_t ph = (it / (uint32_t)nst) & 1u;
         const int np = (int)((int64_t)run.je - p0 < TP ? (int64_t)run.je - p0 : TP);
         float* dst = buf + s * stage_f;
-        if (img) {  // one bulk copy of the stage image
-          const uint32_t bytes = (uint32_t)D * (uint32_t)PS * 4u;
+        if (img) {  // one bulk copy: this column group's image of TPI positions
+          const uint32_t bytes = (uint32_t)ncol * (uint32_t)PS * 4u;
           mbar_wait(&empty[s], ph ^ 1u);
           if (lane == 0) {
             mbar_arrive_expect_tx(&full[s], bytes);
-            bulk_g2s(dst, packed + ((int64_t)run.pad + (p0 - run.jh) / TP) * stage_f, bytes, &full[s]);
+            const int64_t im = (int64_t)run.pad + (int64_t)cg * nimg + (p0 - run.jh) / TPI;
+            bulk_g2s(dst, packed + im * stage_f, bytes, &full[s]);
           } else {
             mbar_arrive(&full[s]);
           }
@@ -201,27 +216,32 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
     return;
   }
   // ---------------- consumers: warp w owns columns 32 w + lane (+ 32 NC, ...) ----------------
-  // one column per lane: a position costs each warp one FADD on the chain
+  // one column per lane: a position costs each warp one FADD on the chain.
+  // A packed (mega) run is split into column groups of 32: each unit (run,
+  // group) streams only its columns, so the hottest id's rows are read by
+  // ceil(D/32) CTAs in parallel — each with its own serial chain per column
   const int c0 = warp * 32 + lane;
   const int cstep = 32 * NC;
-  for (int64_t r = blockIdx.x; r < R; r += gridDim.x) {
+  for (int64_t wu = blockIdx.x; wu < R * NCG; wu += gridDim.x) {
+    const int64_t r = wu / NCG;
+    const int cg = (int)(wu - r * NCG);
     const LongRun run = runs[r];
     const bool img = packed && run.pad != kNoPack;
+    if (!img && cg > 0) continue;
+    const int ncol = D - 32 * cg < 32 ? D - 32 * cg : 32;
+    const int step_p = img ? TPI : TP;
     float acc[kLfCols];
 #pragma unroll
     for (int q = 0; q < kLfCols; ++q) acc[q] = 0.f;
-    for (int64_t p0 = run.jh; p0 < run.je; p0 += TP, ++it) {
+    for (int64_t p0 = run.jh; p0 < run.je; p0 += step_p, ++it) {
       const int s = (int)(it % (uint32_t)nst);
       const uint32_t ph = (it / (uint32_t)nst) & 1u;
-      const int np = (int)((int64_t)run.je - p0 < TP ? (int64_t)run.je - p0 : TP);
+      const int np = (int)((int64_t)run.je - p0 < step_p ? (int64_t)run.je - p0 : step_p);
       mbar_wait(&full[s], ph);
-#pragma unroll
-      for (int q = 0; q < kLfCols; ++q) {
-        const int c = c0 + q * cstep;
-        if (c >= D) continue;
-        if (img) {  // column-major image: four positions per 16-byte load,
-                    // the next 16 positions' loads issued before this 16's adds
-          const float* col = buf + s * stage_f + (int64_t)c * PS;
+      if (img) {  // column-major image slice: four positions per 16-byte load,
+                  // the next 16 positions' loads issued before this 16's adds
+        if (warp == 0 && lane < ncol) {
+          const float* col = buf + s * stage_f + (int64_t)lane * PS;
           const float4* c4 = reinterpret_cast<const float4*>(col);
           const int n16 = np & ~15;
           if (n16) {
@@ -234,23 +254,28 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
               for (int k = 0; k < 4; ++k) y[k] = c4[(p >> 2) + k];
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
-                acc[q] = __fadd_rn(acc[q], x[k].x);
-                acc[q] = __fadd_rn(acc[q], x[k].y);
-                acc[q] = __fadd_rn(acc[q], x[k].z);
-                acc[q] = __fadd_rn(acc[q], x[k].w);
+                acc[0] = __fadd_rn(acc[0], x[k].x);
+                acc[0] = __fadd_rn(acc[0], x[k].y);
+                acc[0] = __fadd_rn(acc[0], x[k].z);
+                acc[0] = __fadd_rn(acc[0], x[k].w);
                 x[k] = y[k];
               }
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              acc[q] = __fadd_rn(acc[q], x[k].x);
-              acc[q] = __fadd_rn(acc[q], x[k].y);
-              acc[q] = __fadd_rn(acc[q], x[k].z);
-              acc[q] = __fadd_rn(acc[q], x[k].w);
+              acc[0] = __fadd_rn(acc[0], x[k].x);
+              acc[0] = __fadd_rn(acc[0], x[k].y);
+              acc[0] = __fadd_rn(acc[0], x[k].z);
+              acc[0] = __fadd_rn(acc[0], x[k].w);
             }
           }
-          for (int p = n16; p < np; ++p) acc[q] = __fadd_rn(acc[q], col[p]);
-        } else {
+          for (int p = n16; p < np; ++p) acc[0] = __fadd_rn(acc[0], col[p]);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < kLfCols; ++q) {
+          const int c = c0 + q * cstep;
+          if (c >= D) continue;
           const float* src = buf + s * stage_f + c;
 #pragma unroll 16
           for (int p = 0; p < np; ++p) acc[q] = __fadd_rn(acc[q], src[(int64_t)p * D]);
@@ -259,10 +284,17 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
+    // results: packed unit -> its column group (warp 0); unpacked -> all columns
 #pragma unroll
     for (int q = 0; q < kLfCols; ++q) {
-      const int c = c0 + q * cstep;
-      if (c >= D) continue;
+      int c;
+      if (img) {
+        if (q > 0 || warp != 0 || lane >= ncol) continue;
+        c = 32 * cg + lane;
+      } else {
+        c = c0 + q * cstep;
+        if (c >= D) continue;
+      }
       if constexpr (ADAM) {
         float* row = out + (int64_t)run.key * (3 * D);
         float p = row[c], m = row[D + c], v = row[2 * D + c];
@@ -283,7 +315,7 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
 // at least mega_run_threshold(mode) positions into stage images (see k_long_fold), so the
 // CTA folding such a run streams it with one bulk copy per stage.
 struct LongFoldPack {
-  float* images = nullptr;    // [cap_images][D * (TP + kLfPad)]
+  float* images = nullptr;    // [cap_images][stage slot]: per (mega run, 32-column group, TPI positions)
   int64_t cap_images = 0;
   uint32_t* mlist = nullptr;  // [cap_runs] run index of each mega run
   uint32_t* moff = nullptr;   // [cap_runs] first image of each mega run (ascending; kNoPack if it did not fit)
@@ -294,7 +326,8 @@ struct LongFoldPack {
 // one block: exclusive scans of (is mega, stage images) over the run list;
 // run.pad = first image (kNoPack for ordinary runs or past capacity)
 static __global__ void __launch_bounds__(1024) k_pack_plan(LongRun* runs, const int64_t* __restrict__ nruns,
-                                                           int64_t cap, int TP, int64_t mega, int64_t cap_images,
+                                                           int64_t cap, int TPI, int NCG, int64_t mega,
+                                                           int64_t cap_images,
                                                            uint32_t* __restrict__ mlist, uint32_t* __restrict__ moff,
                                                            int64_t* __restrict__ mcount) {
   __shared__ int64_t s_c[32], s_l[32];
@@ -311,7 +344,7 @@ static __global__ void __launch_bounds__(1024) k_pack_plan(LongRun* runs, const 
     const int64_t r = b0 + threadIdx.x;
     int64_t len = 0;
     if (r < R) len = (int64_t)runs[r].je - runs[r].jh;
-    const int64_t f = (r < R && len >= mega) ? 1 : 0, l = f ? (len + TP - 1) / TP : 0;
+    const int64_t f = (r < R && len >= mega) ? 1 : 0, l = f ? NCG * ((len + TPI - 1) / TPI) : 0;
     int64_t ic = f, il = l;
     for (int o = 1; o < 32; o <<= 1) {
       const int64_t yc = __shfl_up_sync(0xffffffffu, ic, o), yl = __shfl_up_sync(0xffffffffu, il, o);
@@ -357,9 +390,10 @@ static __global__ void __launch_bounds__(1024) k_pack_plan(LongRun* runs, const 
   }
 }
 
-// one block per stage image: TP gradient rows gathered row-major into shared
-// memory (coalesced reads of whole rows; / len for mean bags; zero row past a
-// tile's k), written out column-major with the padded stride (coalesced)
+// one block per image (run, column group g, stage k): TPI gradient rows'
+// columns [32g, 32g + W) gathered row-major into shared memory (coalesced
+// row segments; / len for mean bags; zero row past a tile's k), written out
+// column-major with the padded stride (coalesced)
 static __global__ void __launch_bounds__(256) k_pack_rows(const LongRun* __restrict__ runs,
                                                           const uint32_t* __restrict__ mlist,
                                                           const uint32_t* __restrict__ moff,
@@ -370,32 +404,36 @@ static __global__ void __launch_bounds__(256) k_pack_rows(const LongRun* __restr
                                                           const int64_t* __restrict__ bag_offs, int mode,
                                                           float* __restrict__ images) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float* tile = reinterpret_cast<float*>(smem_raw);  // [TP][D + 1]
-  const int TP = long_fold_tp(D), PS = TP + kLfPad;
+  float* tile = reinterpret_cast<float*>(smem_raw);  // [TPI][W + 1]
+  const int W = long_fold_img_w(D), TPI = long_fold_tpi(D), PS = TPI + kLfPad;
   const int64_t stage_f = long_fold_stage_f(D);
-  const int64_t nm = mcount[0], nimg = mcount[1];
-  for (int64_t im = blockIdx.x; im < nimg; im += gridDim.x) {
+  const int64_t nm = mcount[0], nimg_all = mcount[1];
+  for (int64_t im = blockIdx.x; im < nimg_all; im += gridDim.x) {
     int64_t lo = 0, hi = nm;  // the mega run owning image im (moff ascending; unfitted runs are a kNoPack suffix)
     while (hi - lo > 1) {
       const int64_t mid = (lo + hi) >> 1;
       if ((int64_t)__ldg(moff + mid) <= im) lo = mid; else hi = mid;
     }
     const LongRun run = runs[__ldg(mlist + lo)];
-    const int64_t j0 = (int64_t)run.jh + (im - (int64_t)__ldg(moff + lo)) * TP;
-    const int np = (int)((int64_t)run.je - j0 < TP ? (int64_t)run.je - j0 : TP);
+    const int64_t per_group = ((int64_t)run.je - run.jh + TPI - 1) / TPI;
+    const int64_t local = im - (int64_t)__ldg(moff + lo);
+    const int g = (int)(local / per_group);
+    const int64_t j0 = (int64_t)run.jh + (local - (int64_t)g * per_group) * TPI;
+    const int np = (int)((int64_t)run.je - j0 < TPI ? (int64_t)run.je - j0 : TPI);
+    const int c0 = 32 * g, w = D - c0 < W ? D - c0 : W;
     __syncthreads();  // the previous image's tile has been written out
-    for (int64_t t = threadIdx.x; t < (int64_t)np * D; t += blockDim.x) {
-      const int p = (int)(t / D), c = (int)(t - (int64_t)p * D);
-      const uint32_t g = __ldg(ridx + j0 + p);
-      float x = g == 0xFFFFFFFFu ? zrow[c] : __ldg(rows + (int64_t)g * D + c);
-      if (mode == 1) x = __fdiv_rn(x, (float)(__ldg(bag_offs + g + 1) - __ldg(bag_offs + g)));
-      tile[p * (D + 1) + c] = x;
+    for (int64_t t = threadIdx.x; t < (int64_t)np * w; t += blockDim.x) {
+      const int p = (int)(t / w), c = (int)(t - (int64_t)p * w);
+      const uint32_t gi = __ldg(ridx + j0 + p);
+      float x = gi == 0xFFFFFFFFu ? zrow[c0 + c] : __ldg(rows + (int64_t)gi * D + c0 + c);
+      if (mode == 1) x = __fdiv_rn(x, (float)(__ldg(bag_offs + gi + 1) - __ldg(bag_offs + gi)));
+      tile[p * (W + 1) + c] = x;
     }
     __syncthreads();
     float* img = images + im * stage_f;
-    for (int64_t t = threadIdx.x; t < (int64_t)D * TP; t += blockDim.x) {
-      const int c = (int)(t / TP), p = (int)(t - (int64_t)c * TP);
-      img[(int64_t)c * PS + p] = p < np ? tile[p * (D + 1) + c] : 0.f;
+    for (int64_t t = threadIdx.x; t < (int64_t)w * TPI; t += blockDim.x) {
+      const int c = (int)(t / TPI), p = (int)(t - (int64_t)c * TPI);
+      img[(int64_t)c * PS + p] = p < np ? tile[p * (W + 1) + c] : 0.f;
     }
   }
 }
@@ -433,11 +471,11 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
   // expect_mega: the caller saw long runs recently (else the two packing
   // launches are skipped; mega runs then take the cp.async path, same result)
   if (env_pack && expect_mega && pack && pack->images && pack->cap_runs >= cap) {
-    const int TP = long_fold_tp(D);
-    k_pack_plan<<<1, 1024, 0, s>>>(runs, nruns, cap, TP, mega_run_threshold(mode), pack->cap_images, pack->mlist,
-                                   pack->moff, pack->mcount);
+    const int TPI = long_fold_tpi(D);
+    k_pack_plan<<<1, 1024, 0, s>>>(runs, nruns, cap, TPI, (D + 31) / 32, mega_run_threshold(mode),
+                                   pack->cap_images, pack->mlist, pack->moff, pack->mcount);
     SKB_LAUNCH_CHECK();
-    const size_t psm = (size_t)TP * (D + 1) * sizeof(float);
+    const size_t psm = (size_t)TPI * (long_fold_img_w(D) + 1) * sizeof(float);
     static size_t pset = 0;
     if (pset < psm) {
       SKB_CUDA(cudaFuncSetAttribute(k_pack_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
@@ -457,8 +495,8 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
 
 // stage images needed to pack up to `rows` positions of mega runs
 inline int64_t long_fold_pack_images(int64_t rows, int D) {
-  const int64_t tp = long_fold_tp(D);
-  return rows / tp + rows / kMegaRunMin + 1;
+  const int64_t ng = (D + 31) / 32, tpi = long_fold_tpi(D);
+  return ng * (rows / tpi + rows / kMegaRunMin + 1);
 }
 
 }  // namespace skb
