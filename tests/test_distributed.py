@@ -166,9 +166,10 @@ def fused_inputs(rank, k):
     rng = np.random.default_rng(500 + 10 * rank + k)
     ids, offs = [], []
     for _ in MEMBERS:
-        lens = rng.integers(0, 4, FB)
+        # step 2 carries ~30x the positions: the P2P windows must grow collectively
+        lens = rng.integers(0, 4, FB) if k != 2 else rng.integers(20, 100, FB)
         offs.append(np.concatenate([[0], np.cumsum(lens)]).astype(np.int64))
-        ids.append(rng.integers(0, 80, int(lens.sum())).astype(np.int64))
+        ids.append(rng.integers(0, 80 if k != 2 else 4000, int(lens.sum())).astype(np.int64))
     dp = rng.standard_normal((len(MEMBERS) * FB, DIM)).astype(np.float32)
     return ids, offs, dp
 
