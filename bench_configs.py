@@ -469,21 +469,43 @@ def c5(args):
             cols[60 + j] = (v, o)
         return cols
 
+    def build(k):
+        """feature engine + one packed batch per table for step k"""
+        cols = features(devs[k % P])
+        out = {}
+        for di, dd in enumerate(DIMS5):
+            idx = [i for i in range(200) if i % 5 == di]
+            out[dd] = skb.PackedBatch(lts[dd], members[dd], [cols[i][0] for i in idx], [cols[i][1] for i in idx])
+        return out
+
+    pending = {}
+
     def run(count):
+        # cross-step pipeline: step k+1's feature engine and index phase (probe,
+        # admission, sort; per table on its index stream) are issued before
+        # step k's backward, so they run underneath the fold+Adam of step k
+        first = step[0] + 1
+        if first not in pending:
+            pending[first] = build(first)
+            for dd in DIMS5:
+                skb.prefetch(lts[dd], pending[first][dd], first, "mean")
         for _ in range(count):
             step[0] += 1
-            d = devs[step[0] % P]
-            cols = features(d)
+            k = step[0]
+            cur = pending.pop(k)
             per = {}
-            for di, dd in enumerate(DIMS5):
-                idx = [i for i in range(200) if i % 5 == di]
-                batch = skb.PackedBatch(lts[dd], members[dd], [cols[i][0] for i in idx], [cols[i][1] for i in idx])
-                pooled = skb.lookup_pool(lts[dd], batch, step[0], "mean")
+            for dd in DIMS5:
+                batch = cur[dd]
+                skb.lookup_pool(lts[dd], batch, k, "mean")
                 key = (dd, batch.num_bags)
                 if key not in grads:
                     grads[key] = torch.randn((batch.num_bags, dd), device="cuda") * 1e-2
-                skb.pool_grad_adam(lts[dd], grads[key], cfg, step[0])
                 per[dd] = (batch.num_ids, batch.num_bags)
+            pending[k + 1] = build(k + 1)
+            for dd in DIMS5:
+                skb.prefetch(lts[dd], pending[k + 1][dd], k + 1, "mean")
+            for dd in DIMS5:
+                skb.pool_grad_adam(lts[dd], grads[(dd, cur[dd].num_bags)], cfg, k)
             stats["per"] = per
 
     # the feature engine's data checks (bucketize NaN) are read once per run
