@@ -64,6 +64,7 @@ struct BatchCtx {
   uint8_t* miss = nullptr;    // [N]
   uint8_t* fresh = nullptr;   // [N] first occurrence of an unknown key
   int64_t* rank = nullptr;    // [N]
+  uint32_t* fpos = nullptr;   // [N] position of the k-th fresh (new) key: admission walks K rows, not N
   int32_t* hslot = nullptr;   // [N] scratch-table index of a miss
   int64_t* tile_cnt = nullptr;  // [N / kRankTile + 2]
   HEntry* scratch = nullptr;  // [2*cap_n pow2 + 1]
@@ -128,6 +129,7 @@ static void batch_free(BatchCtx& B) {
   cudaFree(B.miss);
   cudaFree(B.fresh);
   cudaFree(B.rank);
+  cudaFree(B.fpos);
   cudaFree(B.hslot);
   cudaFree(B.tile_cnt);
   cudaFree(B.scratch);
@@ -210,6 +212,7 @@ static void batch_reserve(BatchCtx& B, int64_t n, int64_t F, cudaStream_t s) {
     realloc_dev(B.miss, cap, s);
     realloc_dev(B.fresh, cap, s);
     realloc_dev(B.rank, cap, s);
+    realloc_dev(B.fpos, cap, s);
     realloc_dev(B.hslot, cap, s);
     realloc_dev(B.tile_cnt, cap / kRankTile + 2, s);
     B.scratch_cap = next_pow2(2 * cap > 64 ? 2 * cap : 64);
@@ -476,7 +479,7 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(int64_t* tile_cnt, int64_t 
 // K3c: rank of each fresh position = tile offset + rank within the tile
 __global__ void __launch_bounds__(256) k_rank_fresh(int64_t n, const uint8_t* __restrict__ fresh,
                                                     const int64_t* __restrict__ tile_off, const int64_t* dev,
-                                                    int64_t* __restrict__ rank) {
+                                                    int64_t* __restrict__ rank, uint32_t* __restrict__ fpos) {
   if (dev[0] == 0) return;
   __shared__ int s_w[8];
   const int64_t ntiles = (n + kRankTile - 1) / kRankTile;
@@ -495,7 +498,11 @@ __global__ void __launch_bounds__(256) k_rank_fresh(int64_t n, const uint8_t* __
         before += k < w ? s_w[k] : 0;
         total += s_w[k];
       }
-      if (f) rank[i] = carry + before + __popc(bal & ((1u << lane) - 1));
+      if (f) {
+        const int64_t r = carry + before + __popc(bal & ((1u << lane) - 1));
+        rank[i] = r;
+        fpos[r] = (uint32_t)i;
+      }
       carry += total;
       __syncthreads();
     }
@@ -506,7 +513,7 @@ __global__ void __launch_bounds__(256) k_rank_fresh(int64_t n, const uint8_t* __
 // lookup_or_insert; the slot is published in the scratch entry for K5.
 __global__ void __launch_bounds__(256) k_fused_admit(
     const int64_t* __restrict__ ids, int64_t n, const MemberDev* __restrict__ mt, int F, int namespaced,
-    const uint8_t* __restrict__ fresh, const int64_t* __restrict__ rank, const int32_t* __restrict__ hslot,
+    const uint32_t* __restrict__ fpos, const int32_t* __restrict__ hslot,
     HEntry* scratch, const int64_t* dev, const int64_t* __restrict__ counters, const int64_t* __restrict__ free_list,
     HEntry* map, uint64_t mask, int64_t cap, int64_t step, int D, uint64_t seed_mix, double scale,
     float* __restrict__ arena, int64_t* __restrict__ last_step, uint8_t* __restrict__ live,
@@ -515,13 +522,12 @@ __global__ void __launch_bounds__(256) k_fused_admit(
   extern __shared__ __align__(16) unsigned char smem_raw[];
   MemberView mv = stage_members(reinterpret_cast<MemberSmem*>(smem_raw), mt, F);
   const int chunks = (D + 3) / 4;
-  const int64_t total = n * chunks;
+  const int64_t total = dev[1] * chunks;  // K new keys (their positions compacted by k_rank_fresh)
   const int64_t A = counters[C_ALLOC], Fr = counters[C_FREE], seq = counters[C_SEQ];
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = t / chunks;
-    if (!fresh[i]) continue;
-    int ch = (int)(t - i * chunks);
-    int64_t k = rank[i];
+    const int64_t k = t / chunks;
+    const int64_t i = fpos[k];
+    const int ch = (int)(t - k * chunks);
     int64_t slot = assign_slot(k, Fr, A, free_list);
     if (slot >= arena_rows) __trap();  // host reservation bound violated: fail loudly
     long long key = key_of(ids[i], mv, F, namespaced, i);
@@ -1147,6 +1153,7 @@ struct AdmitArgs {
   uint8_t* fresh;
   int64_t* tile_cnt;
   int64_t* rank;
+  uint32_t* fpos;
   int64_t* dev;
   int64_t* counters;
   const int64_t* free_list;
@@ -1277,7 +1284,11 @@ __global__ void __launch_bounds__(256) k_admission(AdmitArgs A) {
         before += k < w ? s_w[k] : 0;
         total += s_w[k];
       }
-      if (f) A.rank[i] = carry + before + __popc(bal & ((1u << lane) - 1));
+      if (f) {
+        const int64_t r = carry + before + __popc(bal & ((1u << lane) - 1));
+        A.rank[i] = r;
+        A.fpos[r] = (uint32_t)i;
+      }
       carry += total;
       __syncthreads();
     }
@@ -1286,13 +1297,12 @@ __global__ void __launch_bounds__(256) k_admission(AdmitArgs A) {
   // 6. admission: slot rule of lookup_or_insert, init rows, publish slot
   {
     const int chunks = (A.D + 3) / 4;
-    const int64_t total = n * chunks;
+    const int64_t total = A.dev[1] * chunks;  // K new keys, compacted in phase 5
     const int64_t Aa = A.counters[C_ALLOC], Fr = A.counters[C_FREE], seq = A.counters[C_SEQ];
     for (int64_t t = tid; t < total; t += nth) {
-      const int64_t i = t / chunks;
-      if (!A.fresh[i]) continue;
-      const int ch = (int)(t - i * chunks);
-      const int64_t k = A.rank[i];
+      const int64_t k = t / chunks;
+      const int64_t i = A.fpos[k];
+      const int ch = (int)(t - k * chunks);
       const int64_t slot = assign_slot(k, Fr, Aa, A.free_list);
       if (slot >= A.arena_rows) __trap();  // host reservation bound violated: fail loudly
       const long long key = key_of(A.ids[i], mv, A.F, A.namespaced, i);
@@ -1388,7 +1398,7 @@ static void register_param_kernels() {
   static bool done = false;
   if (done) return;
   done = true;
-  note_param_kernel((const void*)k_fused_admit, 25, -1, 15);
+  note_param_kernel((const void*)k_fused_admit, 24, -1, 14);  // step is argument 14 (ids, n, mt, F, ns, fpos, hslot, ...)
   note_param_kernel((const void*)k_fused_adam<1, 1, 4>, 16, 7, 10);
   note_param_kernel((const void*)k_fused_adam<4, 2, 4>, 16, 7, 10);
   note_param_kernel((const void*)k_fused_adam<4, 1, 5>, 16, 7, 10);
@@ -1433,11 +1443,11 @@ static void launch_admission_phased(const AdmitArgs& A, size_t msm, cudaStream_t
   SKB_LAUNCH_CHECK();
   k_scan_tiles<<<1, 1024, 0, x>>>(A.tile_cnt, ntiles, A.dev);
   SKB_LAUNCH_CHECK();
-  k_rank_fresh<<<tiles, 256, 0, x>>>(n, A.fresh, A.tile_cnt, A.dev, A.rank);
+  k_rank_fresh<<<tiles, 256, 0, x>>>(n, A.fresh, A.tile_cnt, A.dev, A.rank, A.fpos);
   SKB_LAUNCH_CHECK();
   const int chunks = (A.D + 3) / 4;
   k_fused_admit<<<grid_for(n * chunks, 256, 4), 256, msm, x>>>(
-      A.ids, n, A.mt, A.F, A.namespaced, A.fresh, A.rank, A.hslot, A.scratch, A.dev, A.counters, A.free_list, A.map,
+      A.ids, n, A.mt, A.F, A.namespaced, A.fpos, A.hslot, A.scratch, A.dev, A.counters, A.free_list, A.map,
       A.mask, A.cap, A.step, A.D, A.seed_mix, A.scale, A.arena, A.last_step, A.live, A.slot_key, A.ins_seq,
       A.arena_rows);
   SKB_LAUNCH_CHECK();
@@ -1534,7 +1544,7 @@ static void fused_prepare(Table* t, const BatchArgs& a, cudaStream_t s) {
     SKB_LAUNCH_CHECK();
     prof_mark(c, P_PROBE, 1, x);
     prof_mark(c, P_MISS, 0, x);
-    AdmitArgs A{a.ids, n, mt, a.F, a.namespaced, B.miss, B.scratch, B.hslot, B.fresh, B.tile_cnt, B.rank, B.dev,
+    AdmitArgs A{a.ids, n, mt, a.F, a.namespaced, B.miss, B.scratch, B.hslot, B.fresh, B.tile_cnt, B.rank, B.fpos, B.dev,
                 t->counters, t->free_list, t->idmap, mask, t->idmap_cap, a.step, D, t->seed_mix, t->init_scale,
                 t->arena, t->last_step, t->live, t->slot_key, t->ins_seq, B.slot, t->arena_rows};
     const size_t csm = sizeof(MemberSmem);
