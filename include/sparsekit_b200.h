@@ -84,6 +84,10 @@ int skb_fnv1a64_pairs(const int64_t* x, const int64_t* y, int64_t n, int64_t* ou
 int skb_unique_partition(const int64_t* ids, int64_t n, int64_t num_shards, int64_t* uniq_out,
                          int64_t* shard_counts_out, int64_t* inv_shard, int64_t* inv_pos,
                          void* stream);
+/* counts_out[S] (device): unique ids owned by each shard — load_stats
+ * sharding.py:103-119 without materialising the partition */
+int skb_shard_unique_counts(const int64_t* ids, int64_t n, int64_t num_shards, int64_t* counts_out,
+                            void* stream);
 /* out[i,:] = rows_cat[shard_base[inv_shard[i]] + inv_pos[i], :]
  *                                          PartitionResult.restore sharding.py:58-66 */
 int skb_partition_restore(const float* rows_cat, int64_t dim, const int64_t* shard_base,

@@ -43,6 +43,7 @@ _SIGS = {
     "skb_fnv1a64_strings": ([_p, _p, _i64, _p, _p], ctypes.c_int),
     "skb_fnv1a64_pairs": ([_p, _p, _i64, _p, _p], ctypes.c_int),
     "skb_unique_partition": ([_p, _i64, _i64, _p, _p, _p, _p, _p], ctypes.c_int),
+    "skb_shard_unique_counts": ([_p, _i64, _i64, _p, _p], ctypes.c_int),
     "skb_partition_restore": ([_p, _i64, _p, _p, _p, _i64, _p, _p], ctypes.c_int),
     "skb_table_create": ([_i64, _i64, _i64, _i64, _i64, ctypes.POINTER(_p)], ctypes.c_int),
     "skb_table_destroy": ([_p], ctypes.c_int),

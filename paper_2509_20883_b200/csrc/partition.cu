@@ -378,6 +378,115 @@ void dedup_insert(const int64_t* ids, int64_t n, DedupResult& r, cudaStream_t s)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Duplicate test (the distinctness precondition of lookup_or_insert,
+// embedding.py:196-198, and of the offset checks): a key-only claim table,
+// half the bytes of the {key, position} dedup table and no per-position
+// output.  A position whose key is already claimed (read first, then one
+// 64-bit CAS) flags itself; kEmptyKey counts on a side word.  Any flagged
+// position proves a duplicate — which one is not needed by any caller.
+// ---------------------------------------------------------------------------
+__global__ void k_claim_init(longlong2* t, int64_t count2, unsigned long long* flag) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count2; i += stride)
+    t[i] = make_longlong2(kEmptyKey, kEmptyKey);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    flag[0] = ~0ull;  // DevFlag word
+    flag[1] = 0ull;   // occurrences of kEmptyKey
+  }
+}
+
+// COUNT: the position that claims a key also counts it for its owner shard
+// (shard histogram in shared memory, S <= kClaimMaxS) — load_stats' per-shard
+// unique counts without building the partition
+constexpr int kClaimMaxS = 4096;
+
+template <bool COUNT>
+__global__ void __launch_bounds__(256) k_claim_keys(const int64_t* __restrict__ ids, int64_t n, long long* t,
+                                                    uint64_t mask, unsigned long long* flag, int S,
+                                                    unsigned long long* counts) {
+  constexpr int U = 4;
+  __shared__ unsigned int hist[COUNT ? kClaimMaxS : 1];
+  if (COUNT) {
+    for (int k = threadIdx.x; k < S; k += blockDim.x) hist[k] = 0u;
+    __syncthreads();
+  }
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < n; base += stride * U) {
+    long long key[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) key[u] = base + u * stride < n ? __ldg(ids + base + u * stride) : 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * stride;
+      if (i >= n) continue;
+      bool dup = false;
+      if (key[u] == kEmptyKey) {
+        dup = atomicAdd(&flag[1], 1ull) != 0ull;
+      } else {
+        uint64_t slot = bucket_hash((uint64_t)key[u]) & mask;
+        while (true) {
+          long long k = __ldcg(t + slot);
+          if (k == kEmptyKey)
+            k = (long long)atomicCAS(reinterpret_cast<unsigned long long*>(t + slot), (unsigned long long)kEmptyKey,
+                                     (unsigned long long)key[u]);
+          if (k == kEmptyKey) break;
+          if (k == key[u]) { dup = true; break; }
+          slot = (slot + 1) & mask;
+        }
+      }
+      if (COUNT) {
+        if (!dup) atomicAdd(&hist[owner_of(key[u], (uint64_t)S)], 1u);
+      } else if (dup) {
+        atomicMin(&flag[0], (unsigned long long)i);
+      }
+    }
+  }
+  if (COUNT) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < S; k += blockDim.x)
+      if (hist[k]) atomicAdd(&counts[k], (unsigned long long)hist[k]);
+  }
+}
+
+__global__ void k_zero_u64(unsigned long long* p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 0ull;
+}
+
+bool has_duplicate(const int64_t* ids, int64_t n, cudaStream_t s) {
+  if (n < 2) return false;
+  const int64_t cap = next_pow2(n * 2 > 64 ? n * 2 : 64);
+  Scratch t(sizeof(long long) * cap, s);
+  DevFlag f(s);
+  k_claim_init<<<grid_for(cap / 2, 256), 256, 0, s>>>(t.as<longlong2>(), cap / 2, f.ptr());
+  SKB_LAUNCH_CHECK();
+  k_claim_keys<false><<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(ids, n, t.as<long long>(), (uint64_t)(cap - 1),
+                                                                 f.ptr(), 1, nullptr);
+  SKB_LAUNCH_CHECK();
+  return f.read() >= 0;
+}
+
+// per-shard unique-id counts (device int64[S]), no host round trip
+static void shard_unique_counts(const int64_t* ids, int64_t n, int64_t S, int64_t* counts, cudaStream_t s) {
+  k_zero_u64<<<grid_for(S, 256), 256, 0, s>>>(reinterpret_cast<unsigned long long*>(counts), S);
+  SKB_LAUNCH_CHECK();
+  if (n <= 0) return;
+  if (S > kClaimMaxS) {  // rare: many shards — the partition already produces the counts
+    Scratch a(sizeof(int64_t) * n, s), b(sizeof(int64_t) * n, s), c(sizeof(int64_t) * n, s);
+    unique_partition(ids, n, S, a.as<int64_t>(), counts, b.as<int64_t>(), c.as<int64_t>(), s);
+    return;
+  }
+  const int64_t cap = next_pow2(n * 2 > 64 ? n * 2 : 64);
+  Scratch t(sizeof(long long) * cap, s), f(16, s);
+  k_claim_init<<<grid_for(cap / 2, 256), 256, 0, s>>>(t.as<longlong2>(), cap / 2, f.as<unsigned long long>());
+  SKB_LAUNCH_CHECK();
+  k_claim_keys<true><<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(ids, n, t.as<long long>(), (uint64_t)(cap - 1),
+                                                                f.as<unsigned long long>(), (int)S,
+                                                                reinterpret_cast<unsigned long long*>(counts));
+  SKB_LAUNCH_CHECK();
+}
+
 void dedup_first_occurrence(const int64_t* ids, int64_t n, DedupResult& r, cudaStream_t s) {
   dedup_insert(ids, n, r, s);
   r.fpos = Scratch(sizeof(int64_t) * (n ? n : 1), s);
@@ -546,6 +655,14 @@ int skb_unique_partition(const int64_t* ids, int64_t n, int64_t num_shards, int6
   if (num_shards < 1) raise(SKB_E_VALUE, num_shards, "num_shards must be >= 1");
   if (n < 0) raise(SKB_E_ARG, n, "negative length");
   unique_partition(ids, n, num_shards, uniq_out, shard_counts_out, inv_shard, inv_pos, as_stream(stream));
+  SKB_API_END
+}
+
+int skb_shard_unique_counts(const int64_t* ids, int64_t n, int64_t num_shards, int64_t* counts_out, void* stream) {
+  SKB_API_BEGIN
+  if (num_shards < 1) raise(SKB_E_ARG, num_shards, "num_shards must be >= 1");
+  if (n < 0) raise(SKB_E_ARG, n, "n must be >= 0");
+  shard_unique_counts(ids, n, num_shards, counts_out, as_stream(stream));
   SKB_API_END
 }
 

@@ -16,6 +16,9 @@ void dedup_first_occurrence(const int64_t* ids, int64_t n, DedupResult& r, cudaS
 // table + hslot only (no compaction of first occurrences)
 void dedup_insert(const int64_t* ids, int64_t n, DedupResult& r, cudaStream_t s);
 
+// true when some id of ids[0:n) occurs twice (synchronizes)
+bool has_duplicate(const int64_t* ids, int64_t n, cudaStream_t s);
+
 void unique_partition(const int64_t* ids, int64_t n, int64_t S, int64_t* uniq, int64_t* counts,
                       int64_t* inv_shard, int64_t* inv_pos, cudaStream_t s);
 

@@ -217,24 +217,6 @@ __global__ void k_finish_admit(int64_t* counters, const int64_t* __restrict__ to
   counters[C_SEQ] += K;
 }
 
-// duplicate detector: first position whose id occurred earlier
-__global__ void k_dup_flag(const HEntry* t, const int64_t* __restrict__ hslot, int64_t n,
-                           unsigned long long* flag) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    if (t[hslot[i]].val != i) atomicMin(flag, (unsigned long long)i);
-}
-
-// returns the first position i such that ids[i] repeats an earlier id, or -1
-static int64_t first_duplicate(const int64_t* ids, int64_t n, cudaStream_t s) {
-  if (n < 2) return -1;
-  DedupResult r;
-  dedup_insert(ids, n, r, s);
-  DevFlag f(s);
-  k_dup_flag<<<grid_for(n, 256), 256, 0, s>>>(r.table.as<HEntry>(), r.hslot.as<int64_t>(), n, f.ptr());
-  SKB_LAUNCH_CHECK();
-  return f.read();
-}
-
 static int64_t read_i64(const int64_t* dptr, cudaStream_t s) {
   int64_t v = 0;
   SKB_CUDA(cudaMemcpyAsync(&v, dptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -326,27 +308,28 @@ __global__ void k_check_range(const int64_t* __restrict__ offs, int64_t n, const
   }
 }
 
-// MODE 0: scatter_update (distinct + live), MODE 1: BlockStore.write (range)
+// MODE 0: scatter_update (distinct + live), MODE 1: BlockStore.write (range),
+// MODE 2: sparse_adam_step (distinct + range)
 template <int MODE>
 __global__ void __launch_bounds__(256) k_check_rows(const int64_t* __restrict__ offs, int64_t n,
                                                     const uint8_t* __restrict__ live,
                                                     const int64_t* __restrict__ counters, int64_t ensured,
                                                     int64_t bs, int64_t rows, uint32_t* bitmap,
                                                     unsigned long long* flags) {
-  const int64_t limit = MODE == 1 ? store_limit(counters, ensured, bs, rows) : rows;
+  const int64_t limit = MODE != 0 ? store_limit(counters, ensured, bs, rows) : rows;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     const int64_t o = offs[i];
     if (o < 0 || o >= limit) {
       atomicMin(&flags[1], (unsigned long long)i);
-      if (MODE == 0) atomicMin(&flags[2], (unsigned long long)i);
+      if (MODE != 1) atomicMin(&flags[2], (unsigned long long)i);
       continue;
     }
-    if (MODE == 0) {
+    if (MODE != 1) {
       const uint32_t bit = 1u << (o & 31);
       if (atomicOr(&bitmap[o >> 5], bit) & bit) atomicMin(&flags[0], (unsigned long long)i);
-      if (!live[o]) atomicMin(&flags[1], (unsigned long long)i);
     }
+    if (MODE == 0 && !live[o]) atomicMin(&flags[1], (unsigned long long)i);
   }
 }
 
@@ -428,6 +411,33 @@ static void raise_range(Table* t, const int64_t* offs, int64_t bad, cudaStream_t
   raise(SKB_E_INDEX, o, "offset %lld is outside the store capacity %lld", (long long)o, (long long)lim);
 }
 
+__global__ void k_clear_bits(const int64_t* __restrict__ offs, int64_t n, int64_t rows, uint32_t* bitmap) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = offs[i];
+    if (o >= 0 && o < rows) bitmap[o >> 5] = 0u;
+  }
+}
+
+// sparse_adam_step preconditions (embedding.py sparse_adam_step): distinct
+// offsets (ValueError) before the store range (IndexError) — two launches and
+// one readback, distinctness on the slot bitmap instead of a hash table
+static void check_adam_offsets(Table* t, const int64_t* offs, int64_t n, cudaStream_t s) {
+  fused_flush_pending(t, s);
+  ensure_bitmap(t, s);
+  k_check_rows<2><<<grid_for(n, 256), 256, 0, s>>>(offs, n, t->live, t->counters, t->ensured_slots, t->block_size,
+                                                  t->arena_rows, t->bitmap, t->dflags);
+  SKB_LAUNCH_CHECK();
+  k_clear_bits<<<grid_for(n, 256), 256, 0, s>>>(offs, n, t->arena_rows, t->bitmap);
+  SKB_LAUNCH_CHECK();
+  const int64_t* f = flags_fetch(t, s);
+  const unsigned long long f0 = (uint64_t)f[0], f1 = (uint64_t)f[1], f2 = (uint64_t)f[2];
+  if (f0 == kNoFlag && f1 == kNoFlag) return;
+  flags_rearm(t, s);
+  const bool dup = f2 != kNoFlag ? has_duplicate(offs, n, s) : f0 != kNoFlag;
+  if (dup) raise(SKB_E_VALUE, 0, "sparse_adam_step requires distinct offsets");
+  raise_range(t, offs, (int64_t)f1, s);
+}
+
 static void check_range(Table* t, const int64_t* offs, int64_t n, cudaStream_t s) {
   fused_flush_pending(t, s);
   k_check_range<<<grid_for(n, 256), 256, 0, s>>>(offs, n, t->counters, t->ensured_slots, t->block_size,
@@ -467,7 +477,7 @@ static void checked_scatter_update(Table* t, const int64_t* offs, int64_t n, con
   // reference order: duplicates (ValueError) before liveness (IndexError); an
   // out-of-range offset can only duplicate another out-of-range one, so that
   // rare case re-checks distinctness with the hash path
-  const bool dup = f2 != kNoFlag ? first_duplicate(offs, n, s) >= 0 : f0 != kNoFlag;
+  const bool dup = f2 != kNoFlag ? has_duplicate(offs, n, s) : f0 != kNoFlag;
   if (dup) raise(SKB_E_VALUE, 0, "scatter_update requires distinct offsets");
   const int64_t o = read_i64(offs + (int64_t)f1, s);
   raise(SKB_E_INDEX, o, "scatter_update: offset %lld is not a live slot", (long long)o);
@@ -910,7 +920,7 @@ int skb_table_lookup_or_insert(skb_table_t h, const int64_t* ids, int64_t n, int
   Table* t = table_from(h);
   cudaStream_t s = as_stream(stream);
   if (n <= 0) return SKB_OK;
-  if (first_duplicate(ids, n, s) >= 0) raise(SKB_E_VALUE, 0, "lookup_or_insert requires duplicate-free ids");
+  if (has_duplicate(ids, n, s)) raise(SKB_E_VALUE, 0, "lookup_or_insert requires duplicate-free ids");
   table_admit(t, ids, n, step, offsets_out, s);
   SKB_API_END
 }
@@ -1138,8 +1148,7 @@ int skb_sparse_adam_step(skb_table_t h, const int64_t* offsets, int64_t n, const
   Table* t = table_from(h);
   cudaStream_t s = as_stream(stream);
   if (n <= 0) return SKB_OK;
-  if (first_duplicate(offsets, n, s) >= 0) raise(SKB_E_VALUE, 0, "sparse_adam_step requires distinct offsets");
-  check_range(t, offsets, n, s);
+  check_adam_offsets(t, offsets, n, s);
   table_adam(t, offsets, n, grads, *scalars_host, s);
   SKB_API_END
 }

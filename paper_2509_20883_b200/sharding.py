@@ -136,8 +136,9 @@ def load_stats(ids, plan: ShardPlan) -> LoadStats:
     """Per-shard unique-id counts and max/mean imbalance (sharding.py:103-119)."""
     telemetry.bump("sharding.load_stats")
     d = N.to_dev(ids, "int64").reshape(-1)
-    _, counts, _, _ = _partition_dev(d, plan.num_shards)
-    c = np.asarray(counts, np.int64)
+    counts = N.empty((plan.num_shards,), "int64")
+    N.call("skb_shard_unique_counts", N.ptr(d), d.numel(), plan.num_shards, N.ptr(counts), N.stream_ptr())
+    c = counts.cpu().numpy()
     total = int(c.sum())
     if total == 0:
         return LoadStats(c, 1.0)

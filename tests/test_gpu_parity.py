@@ -290,6 +290,59 @@ def test_adam_spec_and_errors(skb, golden):
         skb.sparse_adam_step(t.store, [0], np.ones((1, 1), np.float32), skb.AdamConfig(), 0)
 
 
+def test_distinctness_checks_large(skb):
+    """lookup_or_insert's duplicate test (key-claim table) and
+    sparse_adam_step's offset checks (slot bitmap): a single repeated pair in
+    1M positions is caught, INT64_MIN is a key like any other, duplicates are
+    reported before out-of-range offsets, and a rejected call leaves the
+    table untouched and the bitmap clear for the next call."""
+    rng = np.random.default_rng(11)
+    n = 1_000_000
+    ids = rng.permutation(np.arange(-n, n, 2, dtype=np.int64))
+    bad = ids.copy()
+    bad[n - 1] = bad[12345]
+    t = skb.EmbeddingTable("dup", 4, seed=2, capacity_hint=n)
+    with pytest.raises(ValueError, match="duplicate-free"):
+        t.lookup_or_insert(bad, 1)
+    assert t.num_rows == 0
+    mn = np.iinfo(np.int64).min
+    with pytest.raises(ValueError, match="duplicate-free"):
+        t.lookup_or_insert([mn, 5, mn], 1)
+    t.lookup_or_insert([mn, 5], 1)
+    offs = t.lookup_or_insert(ids, 1)
+    assert t.num_rows == n + 2
+    g = np.ones((n, 4), np.float32)
+    cfg = skb.AdamConfig(lr=0.1)
+    before = t.store.read(offs[:8])
+    dup = offs.copy()
+    dup[-1] = dup[0]
+    with pytest.raises(ValueError, match="distinct"):
+        skb.sparse_adam_step(t.store, dup, g, cfg, 1)
+    far = offs.copy()
+    far[7] = 1 << 40
+    far[9] = 1 << 40  # duplicated out-of-range offset: still a ValueError first
+    with pytest.raises(ValueError, match="distinct"):
+        skb.sparse_adam_step(t.store, far, g, cfg, 1)
+    far[9] = -3
+    with pytest.raises(IndexError, match="offset 1099511627776"):
+        skb.sparse_adam_step(t.store, far, g, cfg, 1)
+    eq(t.store.read(offs[:8]), before)
+    skb.sparse_adam_step(t.store, offs, g, cfg, 1)  # bitmap left clear by the rejected calls
+    assert not np.array_equal(t.store.read(offs[:8]), before)
+
+
+@pytest.mark.parametrize("S", [3, 8, 5000])
+def test_load_stats_large(skb, cuda, S):
+    import torch
+    rng = np.random.default_rng(S)
+    ids = rng.integers(-(1 << 62), 1 << 62, 300_000)
+    ids = np.concatenate([ids, ids[:50_000], [np.iinfo(np.int64).min] * 3])
+    st = skb.load_stats(torch.from_numpy(ids).to(cuda), skb.ShardPlan(S))
+    c, imb = O.shard_load(ids, S)
+    eq(st.counts, c)
+    assert st.imbalance == imb
+
+
 @pytest.mark.parametrize("S", [1, 4])
 def test_sharded_lookup_update(skb, golden, S):
     lts = skb.merge_tables_by_dim([("A", 8), ("B", 8), ("C", 4)], num_shards=S, seed=17)
