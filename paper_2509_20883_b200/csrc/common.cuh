@@ -222,9 +222,10 @@ void sort_pairs_u32(const uint32_t* k_in, uint32_t* k_out, const uint32_t* v_in,
 size_t sort_pairs_u32_bytes(int64_t n, int end_bit);
 void sort_pairs_u32_ws(const uint32_t* k_in, uint32_t* k_out, const uint32_t* v_in, uint32_t* v_out, int64_t n,
                        int end_bit, void* ws, size_t ws_bytes, cudaStream_t s);
-// stable radix sort of (int64 key, int64 val) pairs (signed order)
+// stable radix sort of (int64 key, int64 val) pairs (signed order); keys
+// known to lie in [0, 2^end_bit) may pass end_bit < 64 (fewer passes)
 void sort_pairs_i64(const int64_t* k_in, int64_t* k_out, const int64_t* v_in, int64_t* v_out,
-                    int64_t n, cudaStream_t s);
+                    int64_t n, cudaStream_t s, int end_bit = 64);
 // segment heads of a sorted u32 key array: out = indices i where i==0 or k[i]!=k[i-1]
 void select_run_heads_u32(const uint32_t* keys, int64_t n, uint32_t* out, int64_t* d_count,
                           cudaStream_t s);

@@ -119,11 +119,11 @@ void sort_pairs_u32_ws(const uint32_t* k_in, uint32_t* k_out, const uint32_t* v_
 }
 
 void sort_pairs_i64(const int64_t* k_in, int64_t* k_out, const int64_t* v_in, int64_t* v_out,
-                    int64_t n, cudaStream_t s) {
+                    int64_t n, cudaStream_t s, int end_bit) {
   if (n == 0) return;
   run_cub(
       [&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, k_in, k_out, v_in, v_out, n, 0, 64, s);
+        return cub::DeviceRadixSort::SortPairs(t, b, k_in, k_out, v_in, v_out, n, 0, end_bit, s);
       },
       s);
 }

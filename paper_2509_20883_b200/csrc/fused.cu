@@ -541,11 +541,7 @@ __global__ void __launch_bounds__(256) k_fused_admit(
     }
     uint64_t base = mix64((uint64_t)key ^ seed_mix);
     float* row = arena + slot * (int64_t)(3 * D);
-    for (int c = ch * 4; c < ch * 4 + 4 && c < D; ++c) {
-      row[c] = init_value(base, c, scale);
-      row[D + c] = 0.f;
-      row[2 * D + c] = 0.f;
-    }
+    init_row_chunk(row, D, ch, base, scale);
   }
 }
 
@@ -1316,11 +1312,7 @@ __global__ void __launch_bounds__(256) k_admission(AdmitArgs A) {
       }
       const uint64_t base = mix64((uint64_t)key ^ A.seed_mix);
       float* row = A.arena + slot * (int64_t)(3 * A.D);
-      for (int c = ch * 4; c < ch * 4 + 4 && c < A.D; ++c) {
-        row[c] = init_value(base, c, A.scale);
-        row[A.D + c] = 0.f;
-        row[2 * A.D + c] = 0.f;
-      }
+      init_row_chunk(row, A.D, ch, base, A.scale);
     }
   }
   grid.sync();

@@ -200,11 +200,7 @@ __global__ void k_admit(const int64_t* __restrict__ ids, int64_t n, const int32_
     }
     uint64_t base = mix64((uint64_t)key ^ seed_mix);
     float* row = arena + slot * (int64_t)(3 * D);
-    for (int c = ch * 4; c < ch * 4 + 4 && c < D; ++c) {
-      row[c] = init_value(base, c, scale);
-      row[D + c] = 0.f;
-      row[2 * D + c] = 0.f;
-    }
+    init_row_chunk(row, D, ch, base, scale);
   }
 }
 
@@ -498,19 +494,29 @@ __global__ void k_gather_i64(const int64_t* __restrict__ src, const int64_t* __r
     out[i] = src[idx[i]];
 }
 
+// one thread per (evicted slot, 4-column chunk): zero the Adam moments
+// (16-byte stores when D % 4 == 0); chunk 0 returns the slot to the free list
 __global__ void k_evict_apply(const int64_t* __restrict__ slots, int64_t E, int D, int64_t* counters,
                               int64_t* __restrict__ free_list, uint8_t* __restrict__ live,
                               int64_t* __restrict__ last, float* __restrict__ arena) {
   const int64_t F = counters[C_FREE];
-  const int64_t total = E * D;
+  const int chunks = (D + 3) >> 2;
+  const int64_t total = E * chunks;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t j = t / D;
-    int c = (int)(t - j * D);
-    int64_t s = slots[j];
+    const int64_t j = t / chunks;
+    const int c0 = (int)(t - j * chunks) * 4;
+    const int64_t s = slots[j];
     float* row = arena + s * (int64_t)(3 * D);
-    row[D + c] = 0.f;
-    row[2 * D + c] = 0.f;
-    if (c == 0) {
+    if ((D & 3) == 0) {
+      *reinterpret_cast<float4*>(row + D + c0) = make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(row + 2 * D + c0) = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      for (int c = c0; c < c0 + 4 && c < D; ++c) {
+        row[D + c] = 0.f;
+        row[2 * D + c] = 0.f;
+      }
+    }
+    if (c0 == 0) {
       free_list[F + j] = s;
       live[s] = 0;
       last[s] = 0;
@@ -541,17 +547,25 @@ int64_t table_evict(Table* t, int64_t step, cudaStream_t s) {
   fused_flush_pending(t, s);
   if (t->evict_threshold < 0 || t->arena_rows == 0) return 0;
   const int64_t R = t->arena_rows;
-  Scratch flags(R, s), stale(sizeof(int64_t) * R, s), cnt(sizeof(int64_t), s);
+  Scratch flags(R, s), stale(sizeof(int64_t) * R, s), cnt(sizeof(int64_t) * 2, s);
   k_stale<<<grid_for(R, 256), 256, 0, s>>>(t->live, t->last_step, R, step, t->evict_threshold, flags.as<uint8_t>());
   SKB_LAUNCH_CHECK();
   select_flagged_index(flags.as<uint8_t>(), R, stale.as<int64_t>(), cnt.as<int64_t>(), s);
-  int64_t E = read_i64(cnt.as<int64_t>(), s);
+  // E and the insertion-sequence counter in one readback: every ins_seq is
+  // below C_SEQ, so the order sort needs only bit_width(C_SEQ) key bits
+  SKB_CUDA(cudaMemcpyAsync(cnt.as<int64_t>() + 1, t->counters + C_SEQ, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  int64_t* h = pinned_mailbox();
+  SKB_CUDA(cudaMemcpyAsync(h, cnt.p, sizeof(int64_t) * 2, cudaMemcpyDeviceToHost, s));
+  SKB_CUDA(cudaStreamSynchronize(s));
+  const int64_t E = h[0], seq_hi = h[1];
   if (E == 0) return 0;
+  int bits = 1;
+  while (bits < 64 && (seq_hi >> bits) != 0) ++bits;
   Scratch seq(sizeof(int64_t) * E, s), seq2(sizeof(int64_t) * E, s), slots2(sizeof(int64_t) * E, s);
   k_gather_i64<<<grid_for(E, 256), 256, 0, s>>>(t->ins_seq, stale.as<int64_t>(), E, seq.as<int64_t>());
   SKB_LAUNCH_CHECK();
-  sort_pairs_i64(seq.as<int64_t>(), seq2.as<int64_t>(), stale.as<int64_t>(), slots2.as<int64_t>(), E, s);
-  k_evict_apply<<<grid_for(E * t->dim, 256), 256, 0, s>>>(slots2.as<int64_t>(), E, (int)t->dim, t->counters,
+  sort_pairs_i64(seq.as<int64_t>(), seq2.as<int64_t>(), stale.as<int64_t>(), slots2.as<int64_t>(), E, s, bits);
+  k_evict_apply<<<grid_for(E * ((t->dim + 3) / 4), 256), 256, 0, s>>>(slots2.as<int64_t>(), E, (int)t->dim, t->counters,
                                                          t->free_list, t->live, t->last_step, t->arena);
   SKB_LAUNCH_CHECK();
   k_evict_counters<<<1, 1, 0, s>>>(t->counters, E);

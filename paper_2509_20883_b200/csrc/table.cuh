@@ -124,6 +124,26 @@ __device__ __forceinline__ float init_value(uint64_t base, int c, double scale) 
   return __double2float_rn(__dmul_rn(x, scale));
 }
 
+// chunk ch (columns 4ch..4ch+3) of a freshly admitted row: initial weights,
+// zero Adam moments.  16-byte stores when D % 4 == 0 (arena rows are then
+// 16-byte aligned: 3*D floats per row).
+__device__ __forceinline__ void init_row_chunk(float* row, int D, int ch, uint64_t base, double scale) {
+  const int c0 = ch * 4;
+  if ((D & 3) == 0) {
+    const float4 w = make_float4(init_value(base, c0, scale), init_value(base, c0 + 1, scale),
+                                 init_value(base, c0 + 2, scale), init_value(base, c0 + 3, scale));
+    *reinterpret_cast<float4*>(row + c0) = w;
+    *reinterpret_cast<float4*>(row + D + c0) = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(row + 2 * D + c0) = make_float4(0.f, 0.f, 0.f, 0.f);
+  } else {
+    for (int c = c0; c < c0 + 4 && c < D; ++c) {
+      row[c] = init_value(base, c, scale);
+      row[D + c] = 0.f;
+      row[2 * D + c] = 0.f;
+    }
+  }
+}
+
 // slot assignment of the k-th new id given free count F, allocated A
 // (free list LIFO first, then sequential growth; embedding.py:203-207)
 __device__ __forceinline__ int64_t assign_slot(int64_t k, int64_t F, int64_t A, const int64_t* free_list) {

@@ -29,10 +29,25 @@ def main():
     seq_o = torch.arange(0, n + 1, 250, dtype=torch.int64, device="cuda")
     RT = skb.RaggedTensor(ids1, seq_o)
     marker = torch.zeros(1, device="cuda")
+    from paper_2509_20883_b200 import _native as N
+    pos = torch.from_numpy(rng.integers(0, n // 4, n, dtype=np.int64)).cuda()
+    pr = skb.unique_partition(pos, skb.ShardPlan(4))
+    grads = torch.randn((n, 16), device="cuda")
+    inv = (pr.inverse_pos + torch.tensor(pr._bases(), device="cuda")[pr.inverse_shard]).contiguous()
+    fout = torch.empty((pr.num_unique, 16), device="cuda")
+    t3 = skb.EmbeddingTable("a14", 16, seed=0, evict_threshold=1, capacity_hint=2 * n)
+
+    def evict_cycle():
+        t3.lookup_or_insert(uniq, 10)
+        t3.evict(20)
+
     ops = [("a4", lambda: skb.initial_rows(3, ids1, 16)),
            ("a5", lambda: t2.lookup_or_insert(uniq, 2)),
            ("a19", lambda: skb.load_stats(ids1, plan8)),
-           ("a20", lambda: RT.truncate(100, "tail"))]
+           ("a20", lambda: RT.truncate(100, "tail")),
+           ("a12", lambda: N.call("skb_grad_fold", N.ptr(grads), n, 16, N.ptr(inv), pr.num_unique, N.ptr(fout),
+                                  N.stream_ptr())),
+           ("a14", evict_cycle)]
     for _, fn in ops:
         fn()
     torch.cuda.synchronize()
