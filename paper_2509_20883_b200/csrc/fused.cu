@@ -584,21 +584,58 @@ struct PoolSmem {
 // chunks of 32 bags; lane i loads bag i's offsets and first slot (coalesced),
 // then sub-groups of L lanes gather R bags' rows at once.  The fold starts
 // from +0 like np.add.at.  No member logic is needed on this path.
+// one chunk of 32 bags (warp-cooperative), see k_fused_pool_scatter
+template <int VEC, int R>
+__device__ __forceinline__ void pool_chunk(const float* __restrict__ arena, const uint32_t* __restrict__ slot,
+                                           int64_t g0, int nb, int64_t b, int64_t e, uint32_t s0, int lane, int mode,
+                                           int D, int64_t D3, float* __restrict__ out) {
+  using T = typename VecT<VEC>::T;
+  const int rowv = D / VEC;
+  const int L = rowv < 32 ? rowv : 32;
+  const int P = 32 / L;
+  const int sub = lane / L, sl = lane - sub * L;
+  for (int base = 0; base < nb; base += R * P) {
+    int bi[R];
+    int64_t bb[R], ee[R];
+    uint32_t ss[R];
+    bool ok[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      bi[r] = base + r * P + sub;
+      const int src = bi[r] < 32 ? bi[r] : 31;
+      bb[r] = __shfl_sync(0xffffffffu, b, src);
+      ee[r] = __shfl_sync(0xffffffffu, e, src);
+      ss[r] = __shfl_sync(0xffffffffu, s0, src);
+      ok[r] = sub < P && bi[r] < nb;
+    }
+    for (int c = sl * VEC; c < D; c += L * VEC) {
+      T acc[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        acc[r] = vfill<VEC>(0.f);
+        if (ok[r] && ee[r] > bb[r]) acc[r] = vadd<VEC>(acc[r], vload<VEC>(arena + (int64_t)ss[r] * D3 + c));
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!ok[r]) continue;
+        for (int64_t p = bb[r] + 1; p < ee[r]; ++p)
+          acc[r] = vadd<VEC>(acc[r], vload<VEC>(arena + (int64_t)__ldg(slot + p) * D3 + c));
+        if (mode == 1 && ee[r] > bb[r]) acc[r] = vdiv<VEC>(acc[r], (float)(ee[r] - bb[r]));
+        vstore<VEC>(out + (g0 + bi[r]) * D + c, acc[r]);
+      }
+    }
+  }
+}
+
 template <int VEC, int R, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_fused_pool_scatter(const float* __restrict__ arena,
                                                                   const uint32_t* __restrict__ slot,
                                                                   const int64_t* __restrict__ bag_offs, int64_t G,
                                                                   int mode, int D, int64_t stride,
                                                                   float* __restrict__ out) {
-  using T = typename VecT<VEC>::T;
   const int lane = threadIdx.x & 31;
-  const int rowv = D / VEC;
-  const int L = rowv < 32 ? rowv : 32;
-  const int P = 32 / L;
-  const int sub = lane / L, sl = lane - sub * L;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nchunks = (G + 31) / 32;
-  const int64_t D3 = stride;
   for (int64_t ch = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; ch < nchunks; ch += warps) {
     const int64_t g0 = ch * 32;
     const int nb = (int)(G - g0 < 32 ? G - g0 : 32);
@@ -609,36 +646,62 @@ __global__ void __launch_bounds__(256, MINB) k_fused_pool_scatter(const float* _
       e = __ldg(bag_offs + g0 + lane + 1);
       if (e > b) s0 = __ldg(slot + b);
     }
-    for (int base = 0; base < nb; base += R * P) {
-      int bi[R];
-      int64_t bb[R], ee[R];
-      uint32_t ss[R];
-      bool ok[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        bi[r] = base + r * P + sub;
-        const int src = bi[r] < 32 ? bi[r] : 31;
-        bb[r] = __shfl_sync(0xffffffffu, b, src);
-        ee[r] = __shfl_sync(0xffffffffu, e, src);
-        ss[r] = __shfl_sync(0xffffffffu, s0, src);
-        ok[r] = sub < P && bi[r] < nb;
-      }
-      for (int c = sl * VEC; c < D; c += L * VEC) {
-        T acc[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          acc[r] = vfill<VEC>(0.f);
-          if (ok[r] && ee[r] > bb[r]) acc[r] = vadd<VEC>(acc[r], vload<VEC>(arena + (int64_t)ss[r] * D3 + c));
+    pool_chunk<VEC, R>(arena, slot, g0, nb, b, e, s0, lane, mode, D, stride, out);
+  }
+}
+
+// K6 staged variant (D % 4 == 0, D <= 128): a chunk whose 32 bags all hold
+// exactly one id (the one-hot regime of C2) is a pure row gather — the
+// warp's lanes issue 16-byte cp.async copies of all its rows into shared
+// memory at once (no registers held while they fly: far more bytes in flight
+// per SM than register-staged loads), then stream the chunk's contiguous
+// output rows out.  +0.0f is added on the way out: np.add.at's fold from +0
+// maps -0 to +0 (and x/1 == x for mean).  Other chunks take pool_chunk.
+__global__ void __launch_bounds__(256) k_fused_pool_staged(const float* __restrict__ arena,
+                                                           const uint32_t* __restrict__ slot,
+                                                           const int64_t* __restrict__ bag_offs, int64_t G, int mode,
+                                                           int D, int64_t stride, float* __restrict__ out) {
+  extern __shared__ __align__(16) float pool_buf[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float* buf = pool_buf + (int64_t)w * 32 * D;
+  const int rowv = D >> 2;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nchunks = (G + 31) / 32;
+  for (int64_t ch = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; ch < nchunks; ch += warps) {
+    const int64_t g0 = ch * 32;
+    const int nb = (int)(G - g0 < 32 ? G - g0 : 32);
+    int64_t b = 0, e = 0;
+    uint32_t s0 = 0;
+    if (lane < nb) {
+      b = __ldg(bag_offs + g0 + lane);
+      e = __ldg(bag_offs + g0 + lane + 1);
+      if (e > b) s0 = __ldg(slot + b);
+    }
+    if (__all_sync(0xffffffffu, lane >= nb || e - b == 1)) {
+      for (int it = 0; it < rowv; ++it) {  // piece q = it*32 + lane of nb*rowv 16-byte pieces
+        const int q = it * 32 + lane;
+        const int r = q / rowv;
+        const uint32_t sr = __shfl_sync(0xffffffffu, s0, r & 31);
+        if (r < nb) {
+          const int c = (q - r * rowv) * 4;
+          cp_async16(buf + r * D + c, arena + (int64_t)sr * stride + c);
         }
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if (!ok[r]) continue;
-          for (int64_t p = bb[r] + 1; p < ee[r]; ++p)
-            acc[r] = vadd<VEC>(acc[r], vload<VEC>(arena + (int64_t)__ldg(slot + p) * D3 + c));
-          if (mode == 1 && ee[r] > bb[r]) acc[r] = vdiv<VEC>(acc[r], (float)(ee[r] - bb[r]));
-          vstore<VEC>(out + (g0 + bi[r]) * D + c, acc[r]);
-        }
       }
+      asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
+      float4* dst = reinterpret_cast<float4*>(out + g0 * D);
+      const float4* src = reinterpret_cast<const float4*>(buf);
+      for (int q = lane; q < nb * rowv; q += 32) {
+        float4 v = src[q];
+        v.x = __fadd_rn(v.x, 0.f);
+        v.y = __fadd_rn(v.y, 0.f);
+        v.z = __fadd_rn(v.z, 0.f);
+        v.w = __fadd_rn(v.w, 0.f);
+        __stcs(dst + q, v);
+      }
+      __syncwarp();
+    } else {
+      pool_chunk<4, 2>(arena, slot, g0, nb, b, e, s0, lane, mode, D, stride, out);
     }
   }
 }
@@ -1629,7 +1692,21 @@ static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStrea
       else
         // measured on B200 (C2, D=64): R=2 at 4 blocks/SM 0.162 ms; R=2/1 0.204;
         // R=1/4 0.236; R=4/2 0.235
-        switch (pool_variant()) {
+        switch (pool_variant() == 0 && D <= 128 ? 4 : pool_variant()) {
+          case 4: {
+            const size_t sm = (size_t)8 * 32 * D * sizeof(float);
+            static int attr_set = 0;
+            if (sm > 48 * 1024 && attr_set < (int)sm) {
+              SKB_CUDA(cudaFuncSetAttribute(k_fused_pool_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+              attr_set = (int)sm;
+            }
+            static const int bps_env = env_int("SKB_POOL_BPS", 0);
+            // 128 KB of staging per SM: D=64 -> 2 blocks/SM (measured best on C2 — the
+            // rest of the SM stays free for the index stream's overlapping sort)
+            const int bps = bps_env > 0 ? bps_env : (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)(128 * 1024) / sm));
+            k_fused_pool_staged<<<grid_for(((G + 31) / 32) * 32, 256, bps), 256, sm, s>>>(SKB_POOL_ARGS);
+            break;
+          }
           case 1: k_fused_pool_scatter<4, 1, 4><<<grid, 256, 0, s>>>(SKB_POOL_ARGS); break;
           case 2: k_fused_pool_scatter<4, 2, 1><<<grid, 256, 0, s>>>(SKB_POOL_ARGS); break;
           case 3: k_fused_pool_scatter<4, 4, 2><<<grid, 256, 0, s>>>(SKB_POOL_ARGS); break;

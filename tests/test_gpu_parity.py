@@ -515,6 +515,30 @@ def _fused_vs_oracle(skb, D, member_specs, steps, mode, seed=0, evict_every=0, t
     eq(lt.local_table.idmap.free_list, olt.shards[0].free)
 
 
+@pytest.mark.parametrize("D,mode", [(64, "sum"), (64, "mean"), (128, "sum"), (8, "sum")])
+def test_fused_onehot_negative_zero(skb, D, mode):
+    """One-hot chunks take the staged row-gather pool: it must still fold from
+    +0 like np.add.at (-0.0 -> +0.0), and chunks mixing bag lengths 0/1/2
+    take the general path in the same launch."""
+    import torch
+    lt = skb.LogicalTable(f"nz{D}", D, 1, seed=4, members=["f"], namespaced=False)
+    keys = np.arange(200, dtype=np.int64)
+    t = lt.local_table
+    offs = t.lookup_or_insert(keys, 1)
+    rows = np.random.default_rng(D).standard_normal((200, D)).astype(np.float32)
+    rows[::3, ::2] = -0.0
+    t.scatter_update(offs, rows)
+    lens = np.ones(160, np.int64)
+    lens[100:] = np.random.default_rng(1).integers(0, 3, 60)
+    ids = np.concatenate([np.arange(100), np.random.default_rng(2).integers(0, 200, int(lens[100:].sum()))])
+    bo = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    batch = skb.PackedBatch(lt, ["f"], [ids], [bo])
+    pooled = skb.lookup_pool(lt, batch, 2, mode)
+    eq(pooled, O.pool(rows[ids], bo, mode))
+    assert rows[0, 0] == 0 and np.signbit(rows[0, 0]) and not np.signbit(pooled.cpu().numpy()[0, 0])
+    skb.pool_grad_adam(lt, torch.zeros((160, D), device="cuda"), skb.AdamConfig(), 2)
+
+
 def test_fused_c1_shape(skb):
     # C1: dim16, B4096, 1 feature, bag length 1, sum, AdamW
     _fused_vs_oracle(skb, 16, [("f0", 4096, lambda r, B: np.ones(B, np.int64))], steps=4, mode="sum")
