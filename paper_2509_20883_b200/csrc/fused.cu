@@ -1692,7 +1692,10 @@ static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStrea
       else
         // measured on B200 (C2, D=64): R=2 at 4 blocks/SM 0.162 ms; R=2/1 0.204;
         // R=1/4 0.236; R=4/2 0.235
-        switch (pool_variant() == 0 && D <= 128 ? 4 : pool_variant()) {
+        // staged one-hot gather only for one-hot batches (n == G): its shared
+        // staging halves the resident warps of the general chunks (C5: mixed
+        // bag lengths ran 0.75 ms/step slower through it)
+        switch (pool_variant() == 0 && D <= 128 && B.n == G ? 4 : pool_variant()) {
           case 4: {
             const size_t sm = (size_t)8 * 32 * D * sizeof(float);
             static int attr_set = 0;
