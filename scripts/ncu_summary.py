@@ -46,7 +46,7 @@ def main(rep, launches, tag):
     json.dump({"tag": tag, "kernels": summary, "launch_shares_last_steps": shares}, open(f"profiles/ncu_{tag}.json", "w"), indent=1)
     # bench.py reads the dominant kernel's dram bytes per launch from here
     simple = {}
-    for key, pat in (("fold_adam", "k_fused_adam_tma"), ("pool", "k_fused_pool_scatter"), ("probe", "k_fused_probe")):
+    for key, pat in (("fold_adam", "k_fused_adam_tma"), ("pool", "k_fused_pool_s"), ("probe", "k_fused_probe")):
         for name, v in summary.items():
             if pat in name:
                 simple[key] = {"kernel": name, "dram_bytes_per_launch": v["dram_bytes_per_launch"], "tag": tag}
