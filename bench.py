@@ -230,7 +230,7 @@ def run_reference(args):
     if rank != 0:
         return
     steps = max(1, min(args.steps, 5))
-    warm = min(args.warmup, 1)
+    warm = min(args.warmup, 5)  # each step ~0.35 s: the whole arm stays within seconds
     r = cpu_reference_steps(steps, warm, CPU_SAMPLE_BATCH)
     sample = (f"C2 scaled to batch {CPU_SAMPLE_BATCH}/feature ({r['ids_per_step']} ids/step), warm table, "
               f"{steps} timed steps after {warm} warm-up, median")
