@@ -162,6 +162,7 @@ void fused_ctx_destroy(FusedCtx* c) {
   if (c->lf_ev) cudaEventDestroy(c->lf_ev);
   cudaFree(c->pack.mlist);
   cudaFree(c->pack.moff);
+  cudaFree(c->pack.morder);
   cudaFree(c->pack.mcount);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
   if (c->ev_side_last) cudaEventDestroy(c->ev_side_last);
@@ -1458,7 +1459,7 @@ static void register_param_kernels() {
   note_param_kernel((const void*)k_fused_adam<4, 2, 4>, 16, 7, 10);
   note_param_kernel((const void*)k_fused_adam<4, 1, 5>, 16, 7, 10);
   note_param_kernel((const void*)k_fused_adam<4, 1, 4>, 16, 7, 10);
-  note_param_kernel((const void*)k_long_fold<true>, 15, 8, 11);  // (runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out, last_step, step, nst, zrow, packed)
+  note_param_kernel((const void*)k_long_fold<true>, 18, 8, 11);  // (runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out, last_step, step, nst, zrow, packed, mlist, morder, mcount)
 }
 
 // graph mode is off while per-phase event profiling is on (events cannot be
@@ -1773,9 +1774,11 @@ static void pack_reserve(FusedCtx* c, int64_t rows, int64_t runs, int D, cudaStr
   if (grow_runs) {
     if (P.mlist) SKB_CUDA(cudaFree(P.mlist));
     if (P.moff) SKB_CUDA(cudaFree(P.moff));
+    if (P.morder) SKB_CUDA(cudaFree(P.morder));
     if (!P.mcount) SKB_CUDA(cudaMalloc(&P.mcount, sizeof(int64_t) * 2));
     SKB_CUDA(cudaMalloc(&P.mlist, sizeof(uint32_t) * runs));
     SKB_CUDA(cudaMalloc(&P.moff, sizeof(uint32_t) * runs));
+    SKB_CUDA(cudaMalloc(&P.morder, sizeof(uint32_t) * runs));
     P.cap_runs = runs;
   }
   c->pack_gen++;

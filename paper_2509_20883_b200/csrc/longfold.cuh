@@ -73,11 +73,19 @@ __host__ __device__ inline int long_fold_tp(int D) {
 }
 // floats of one stage slot: a row-major stage (TP*D) or a packed image
 __host__ __device__ inline int64_t long_fold_stage_f(int D) { return (int64_t)D * (long_fold_tp(D) + kLfPad); }
-// packed image of one 32-column group (min(32, D) columns): the whole slot,
-// column-major with stride PSI = TPI + kLfPad, TPI positions (multiple of 4)
-__host__ __device__ inline int long_fold_img_w(int D) { return D < 32 ? D : 32; }
+// Column groups of a packed (mega) run: kLfGW columns each, one work unit
+// (one CTA, one serial chain per column) per group — the hottest id's rows
+// are folded by ceil(D / kLfGW) CTAs in parallel, each streaming only its
+// columns (a 32-column group left the C4 hot run bound by one SM's stream).
+constexpr int kLfGW = 8;
+__host__ __device__ inline int long_fold_groups(int D) { return (D + kLfGW - 1) / kLfGW; }
+// packed image of one column group (min(kLfGW, D) columns): the whole slot,
+// column-major with stride PS = TPI + kLfPad; TPI a multiple of 32 so PS is
+// 4 (mod 32) and eight lanes' LDS.128 of their columns hit distinct banks
+__host__ __device__ inline int long_fold_img_w(int D) { return D < kLfGW ? D : kLfGW; }
 __host__ __device__ inline int long_fold_tpi(int D) {
-  return (int)((long_fold_stage_f(D) / long_fold_img_w(D) - kLfPad) & ~3ll);
+  const int64_t t = ((long_fold_stage_f(D) / long_fold_img_w(D) - kLfPad) / 32) * 32;
+  return (int)(t < 32 ? 32 : t);
 }
 constexpr int kLfMaxNC = 16;  // consumer warps
 constexpr int kLfCols = 4;    // columns per consumer lane: dims up to 32 * kLfMaxNC * kLfCols = 2048
@@ -99,12 +107,32 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// work unit wu -> (run, column group, packed?); false: nothing to do
+__device__ __forceinline__ bool long_fold_unit(int64_t wu, int64_t MU, int NCG, const LongRun* __restrict__ runs,
+                                               const uint32_t* __restrict__ mlist,
+                                               const uint32_t* __restrict__ morder, const float* packed,
+                                               LongRun& run, int& cg, bool& img) {
+  if (wu < MU) {  // column group of a mega run; unfitted mega runs come back as ordinary units
+    const int64_t m = wu / NCG;
+    cg = (int)(wu - m * NCG);
+    run = runs[__ldg(mlist + __ldg(morder + m))];
+    img = run.pad != kNoPack;
+    return img;
+  }
+  run = runs[wu - MU];
+  cg = 0;
+  img = false;
+  return !(packed && run.pad != kNoPack);  // packed runs were covered by their groups
+}
+
 template <bool ADAM>
 __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __restrict__ nruns, int64_t cap,
                             const uint32_t* __restrict__ ridx, const float* __restrict__ rows, int D,
                             const int64_t* __restrict__ bag_offs, int mode, AdamDev a, float* __restrict__ out,
                             int64_t* __restrict__ last_step, int64_t step, int nst,
-                            const float* __restrict__ zrow, const float* __restrict__ packed) {
+                            const float* __restrict__ zrow, const float* __restrict__ packed,
+                            const uint32_t* __restrict__ mlist, const uint32_t* __restrict__ morder,
+                            const int64_t* __restrict__ mcount) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int TP = long_fold_tp(D);                // positions per row-major stage
   const int TPI = long_fold_tpi(D);              // positions per packed column-group image
@@ -115,8 +143,14 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
   uint64_t* full = reinterpret_cast<uint64_t*>(idx + kLfMaxPW * kLfMaxTP);
   uint64_t* empty = full + kLfStages;
   const int NC = long_fold_consumers(D);
-  const int NCG = (D + 31) / 32;  // 32-column groups: work units of a packed run
+  const int NCG = long_fold_groups(D);  // column groups: work units of a packed run
   const int64_t R = *nruns < cap ? *nruns : cap;
+  // work units: first every packed (mega) run's column groups, longest run
+  // first (morder), so the hottest ids' chains start in the first wave on
+  // distinct SMs; then one unit per ordinary run.  Producers and consumers
+  // walk the same sequence.
+  const int64_t MU = packed ? (mcount[0] < R ? mcount[0] : R) * NCG : 0;
+  const int64_t units = MU + R;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
@@ -130,13 +164,12 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
   if (warp >= NC) {  // ---------------- producers: warp pw fills stages it = pw (mod NPW) ----------------
     const int pw = warp - NC, NPW = (int)(blockDim.x >> 5) - NC;
     const int cpr = D / 4;  // 16-byte chunks per row
-    for (int64_t wu = blockIdx.x; wu < R * NCG; wu += gridDim.x) {
-      const int64_t r = wu / NCG;
-      const int cg = (int)(wu - r * NCG);
-      const LongRun run = runs[r];
-      const bool img = packed && run.pad != kNoPack;
-      if (!img && cg > 0) continue;  // unpacked runs: one unit covers every column
-      const int ncol = D - 32 * cg < 32 ? D - 32 * cg : 32;
+    for (int64_t wu = blockIdx.x; wu < units; wu += gridDim.x) {
+      int cg;
+      LongRun run;
+      bool img;
+      if (!long_fold_unit(wu, MU, NCG, runs, mlist, morder, packed, run, cg, img)) continue;
+      const int ncol = D - kLfGW * cg < kLfGW ? D - kLfGW * cg : kLfGW;
       const int step_p = img ? TPI : TP;
       const int64_t nimg = img ? ((int64_t)run.je - run.jh + TPI - 1) / TPI : 0;  // images per column group
       for (int64_t p0 = run.jh; p0 < run.je; p0 += step_p, ++it) {
@@ -217,18 +250,17 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
   }
   // ---------------- consumers: warp w owns columns 32 w + lane (+ 32 NC, ...) ----------------
   // one column per lane: a position costs each warp one FADD on the chain.
-  // A packed (mega) run is split into column groups of 32: each unit (run,
+  // A packed (mega) run is split into column groups of kLfGW: each unit (run,
   // group) streams only its columns, so the hottest id's rows are read by
   // ceil(D/32) CTAs in parallel — each with its own serial chain per column
   const int c0 = warp * 32 + lane;
   const int cstep = 32 * NC;
-  for (int64_t wu = blockIdx.x; wu < R * NCG; wu += gridDim.x) {
-    const int64_t r = wu / NCG;
-    const int cg = (int)(wu - r * NCG);
-    const LongRun run = runs[r];
-    const bool img = packed && run.pad != kNoPack;
-    if (!img && cg > 0) continue;
-    const int ncol = D - 32 * cg < 32 ? D - 32 * cg : 32;
+  for (int64_t wu = blockIdx.x; wu < units; wu += gridDim.x) {
+    int cg;
+    LongRun run;
+    bool img;
+    if (!long_fold_unit(wu, MU, NCG, runs, mlist, morder, packed, run, cg, img)) continue;
+    const int ncol = D - kLfGW * cg < kLfGW ? D - kLfGW * cg : kLfGW;
     const int step_p = img ? TPI : TP;
     float acc[kLfCols];
 #pragma unroll
@@ -290,7 +322,7 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
       int c;
       if (img) {
         if (q > 0 || warp != 0 || lane >= ncol) continue;
-        c = 32 * cg + lane;
+        c = kLfGW * cg + lane;
       } else {
         c = c0 + q * cstep;
         if (c >= D) continue;
@@ -315,12 +347,13 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
 // at least mega_run_threshold(mode) positions into stage images (see k_long_fold), so the
 // CTA folding such a run streams it with one bulk copy per stage.
 struct LongFoldPack {
-  float* images = nullptr;    // [cap_images][stage slot]: per (mega run, 32-column group, TPI positions)
+  float* images = nullptr;    // [cap_images][stage slot]: per (mega run, column group, TPI positions)
   int64_t cap_images = 0;
   uint32_t* mlist = nullptr;  // [cap_runs] run index of each mega run
   uint32_t* moff = nullptr;   // [cap_runs] first image of each mega run (ascending; kNoPack if it did not fit)
   int64_t* mcount = nullptr;  // [2] mega runs, images in use
   int64_t cap_runs = 0;
+  uint32_t* morder = nullptr; // [cap_runs] mega-list indices, longest run first
 };
 
 // one block: exclusive scans of (is mega, stage images) over the run list;
@@ -329,7 +362,9 @@ static __global__ void __launch_bounds__(1024) k_pack_plan(LongRun* runs, const 
                                                            int64_t cap, int TPI, int NCG, int64_t mega,
                                                            int64_t cap_images,
                                                            uint32_t* __restrict__ mlist, uint32_t* __restrict__ moff,
-                                                           int64_t* __restrict__ mcount) {
+                                                           int64_t* __restrict__ mcount, uint32_t* __restrict__ morder) {
+  constexpr int kSortMax = 2048;
+  __shared__ uint32_t s_len[kSortMax];
   __shared__ int64_t s_c[32], s_l[32];
   __shared__ int64_t s_cc, s_cl;
   __shared__ unsigned long long s_fit;  // images of the fitted runs (a prefix of the mega list)
@@ -388,6 +423,28 @@ static __global__ void __launch_bounds__(1024) k_pack_plan(LongRun* runs, const 
     mcount[0] = s_cc;
     mcount[1] = (int64_t)s_fit;
   }
+  // longest-first order of the mega runs (rank by length, ties by list
+  // position); beyond kSortMax mega runs: list order
+  __syncthreads();
+  const int64_t M = s_cc;
+  if (M <= kSortMax) {
+    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+      const LongRun ri = runs[mlist[i]];
+      s_len[i] = ri.je - ri.jh;
+    }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+      const uint32_t li = s_len[i];
+      int64_t rank = 0;
+      for (int64_t j = 0; j < M; ++j) {
+        const uint32_t lj = s_len[j];
+        rank += (lj > li || (lj == li && j < i)) ? 1 : 0;
+      }
+      morder[rank] = (uint32_t)i;
+    }
+  } else {
+    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) morder[i] = (uint32_t)i;
+  }
 }
 
 // one block per image (run, column group g, stage k): TPI gradient rows'
@@ -420,7 +477,7 @@ static __global__ void __launch_bounds__(256) k_pack_rows(const LongRun* __restr
     const int g = (int)(local / per_group);
     const int64_t j0 = (int64_t)run.jh + (local - (int64_t)g * per_group) * TPI;
     const int np = (int)((int64_t)run.je - j0 < TPI ? (int64_t)run.je - j0 : TPI);
-    const int c0 = 32 * g, w = D - c0 < W ? D - c0 : W;
+    const int c0 = kLfGW * g, w = D - c0 < W ? D - c0 : W;
     __syncthreads();  // the previous image's tile has been written out
     for (int64_t t = threadIdx.x; t < (int64_t)np * w; t += blockDim.x) {
       const int p = (int)(t / w), c = (int)(t - (int64_t)p * w);
@@ -472,8 +529,8 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
   // launches are skipped; mega runs then take the cp.async path, same result)
   if (env_pack && expect_mega && pack && pack->images && pack->cap_runs >= cap) {
     const int TPI = long_fold_tpi(D);
-    k_pack_plan<<<1, 1024, 0, s>>>(runs, nruns, cap, TPI, (D + 31) / 32, mega_run_threshold(mode),
-                                   pack->cap_images, pack->mlist, pack->moff, pack->mcount);
+    k_pack_plan<<<1, 1024, 0, s>>>(runs, nruns, cap, TPI, long_fold_groups(D), mega_run_threshold(mode),
+                                   pack->cap_images, pack->mlist, pack->moff, pack->mcount, pack->morder);
     SKB_LAUNCH_CHECK();
     const size_t psm = (size_t)TPI * (long_fold_img_w(D) + 1) * sizeof(float);
     static size_t pset = 0;
@@ -489,13 +546,16 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
   int64_t grid = cap < (int64_t)sm_count() ? cap : (int64_t)sm_count();
   if (grid < 1) grid = 1;
   k_long_fold<ADAM><<<(unsigned)grid, threads, sm, s>>>(runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out,
-                                                        last_step, step, nst, zrow, packed);
+                                                        last_step, step, nst, zrow, packed,
+                                                        packed ? pack->mlist : nullptr,
+                                                        packed ? pack->morder : nullptr,
+                                                        packed ? pack->mcount : nullptr);
   SKB_LAUNCH_CHECK();
 }
 
 // stage images needed to pack up to `rows` positions of mega runs
 inline int64_t long_fold_pack_images(int64_t rows, int D) {
-  const int64_t ng = (D + 31) / 32, tpi = long_fold_tpi(D);
+  const int64_t ng = long_fold_groups(D), tpi = long_fold_tpi(D);
   return ng * (rows / tpi + rows / kMegaRunMin + 1);
 }
 

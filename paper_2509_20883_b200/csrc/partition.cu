@@ -629,8 +629,9 @@ void grad_fold(const float* grads, int64_t n, int D, const int64_t* inverse, int
   if (v4) {
     const int64_t imgs = long_fold_pack_images(n, D);
     Scratch prow(sizeof(float) * imgs * long_fold_stage_f(D), s), pl(sizeof(uint32_t) * lcap, s),
-        po(sizeof(uint32_t) * lcap, s), pc(sizeof(int64_t) * 2, s);
-    LongFoldPack pk{prow.as<float>(), imgs, pl.as<uint32_t>(), po.as<uint32_t>(), pc.as<int64_t>(), lcap};
+        po(sizeof(uint32_t) * lcap, s), pc(sizeof(int64_t) * 2, s), pr(sizeof(uint32_t) * lcap, s);
+    LongFoldPack pk{prow.as<float>(), imgs, pl.as<uint32_t>(), po.as<uint32_t>(), pc.as<int64_t>(), lcap,
+                    pr.as<uint32_t>()};
     launch_long_fold<false>(longs.as<LongRun>(), nseg.as<int64_t>() + 1, lcap, v2.as<uint32_t>(), grads, D, nullptr, 0,
                             AdamDev{}, out, nullptr, -1, s, nullptr, &pk);
   }
