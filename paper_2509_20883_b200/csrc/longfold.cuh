@@ -447,10 +447,16 @@ static __global__ void __launch_bounds__(1024) k_pack_plan(LongRun* runs, const 
   }
 }
 
-// one block per image (run, column group g, stage k): TPI gradient rows'
-// columns [32g, 32g + W) gathered row-major into shared memory (coalesced
-// row segments; / len for mean bags; zero row past a tile's k), written out
-// column-major with the padded stride (coalesced)
+// one block per (mega run, stage k): the stage's TPI gradient rows are read
+// whole (coalesced 16-byte loads; / len for mean bags; zero row past a
+// tile's k) kPackSub positions at a time into shared memory, then written
+// out as contiguous column segments of all the run's column-group images at
+// once — every gradient byte is read once (a block per image re-read each row
+// per column group), every image byte written once.
+inline int pack_sub(int D) {
+  const int sp = 16384 / D;
+  return sp > 64 ? 64 : (sp < 4 ? 4 : sp & ~3);
+}
 static __global__ void __launch_bounds__(256) k_pack_rows(const LongRun* __restrict__ runs,
                                                           const uint32_t* __restrict__ mlist,
                                                           const uint32_t* __restrict__ moff,
@@ -458,39 +464,49 @@ static __global__ void __launch_bounds__(256) k_pack_rows(const LongRun* __restr
                                                           const uint32_t* __restrict__ ridx,
                                                           const float* __restrict__ rows,
                                                           const float* __restrict__ zrow, int D,
-                                                          const int64_t* __restrict__ bag_offs, int mode,
+                                                          const int64_t* __restrict__ bag_offs, int mode, int SP,
                                                           float* __restrict__ images) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float* tile = reinterpret_cast<float*>(smem_raw);  // [TPI][W + 1]
-  const int W = long_fold_img_w(D), TPI = long_fold_tpi(D), PS = TPI + kLfPad;
+  float* tile = reinterpret_cast<float*>(smem_raw);  // [SP][D + 1]
+  const int TPI = long_fold_tpi(D), PS = TPI + kLfPad, NCG = long_fold_groups(D);
   const int64_t stage_f = long_fold_stage_f(D);
-  const int64_t nm = mcount[0], nimg_all = mcount[1];
-  for (int64_t im = blockIdx.x; im < nimg_all; im += gridDim.x) {
-    int64_t lo = 0, hi = nm;  // the mega run owning image im (moff ascending; unfitted runs are a kNoPack suffix)
+  const int64_t nm = mcount[0], npair = mcount[1] / NCG;  // (run, stage) pairs of the fitted runs
+  const int cpr = D >> 2;
+  for (int64_t q = blockIdx.x; q < npair; q += gridDim.x) {
+    int64_t lo = 0, hi = nm;  // the mega run owning pair q (moff / NCG ascending; unfitted: kNoPack suffix)
     while (hi - lo > 1) {
       const int64_t mid = (lo + hi) >> 1;
-      if ((int64_t)__ldg(moff + mid) <= im) lo = mid; else hi = mid;
+      if ((int64_t)__ldg(moff + mid) / NCG <= q) lo = mid; else hi = mid;
     }
     const LongRun run = runs[__ldg(mlist + lo)];
     const int64_t per_group = ((int64_t)run.je - run.jh + TPI - 1) / TPI;
-    const int64_t local = im - (int64_t)__ldg(moff + lo);
-    const int g = (int)(local / per_group);
-    const int64_t j0 = (int64_t)run.jh + (local - (int64_t)g * per_group) * TPI;
+    const int64_t k = q - (int64_t)__ldg(moff + lo) / NCG;
+    const int64_t img0 = (int64_t)__ldg(moff + lo) + k;  // image of group g: img0 + g * per_group
+    const int64_t j0 = (int64_t)run.jh + k * TPI;
     const int np = (int)((int64_t)run.je - j0 < TPI ? (int64_t)run.je - j0 : TPI);
-    const int c0 = kLfGW * g, w = D - c0 < W ? D - c0 : W;
-    __syncthreads();  // the previous image's tile has been written out
-    for (int64_t t = threadIdx.x; t < (int64_t)np * w; t += blockDim.x) {
-      const int p = (int)(t / w), c = (int)(t - (int64_t)p * w);
-      const uint32_t gi = __ldg(ridx + j0 + p);
-      float x = gi == 0xFFFFFFFFu ? zrow[c0 + c] : __ldg(rows + (int64_t)gi * D + c0 + c);
-      if (mode == 1) x = __fdiv_rn(x, (float)(__ldg(bag_offs + gi + 1) - __ldg(bag_offs + gi)));
-      tile[p * (W + 1) + c] = x;
-    }
-    __syncthreads();
-    float* img = images + im * stage_f;
-    for (int64_t t = threadIdx.x; t < (int64_t)w * TPI; t += blockDim.x) {
-      const int c = (int)(t / TPI), p = (int)(t - (int64_t)c * TPI);
-      img[(int64_t)c * PS + p] = p < np ? tile[p * (W + 1) + c] : 0.f;
+    for (int p0 = 0; p0 < np; p0 += SP) {
+      const int sp = np - p0 < SP ? np - p0 : SP;
+      __syncthreads();  // the previous sub-chunk has been written out
+      for (int t = threadIdx.x; t < sp * cpr; t += blockDim.x) {
+        const int p = t / cpr, c4 = t - p * cpr;
+        const uint32_t gi = __ldg(ridx + j0 + p0 + p);
+        float4 x = ldg4((gi == 0xFFFFFFFFu ? zrow : rows + (int64_t)gi * D) + c4 * 4);
+        if (mode == 1) {
+          const float l = (float)(__ldg(bag_offs + gi + 1) - __ldg(bag_offs + gi));
+          x = make_float4(__fdiv_rn(x.x, l), __fdiv_rn(x.y, l), __fdiv_rn(x.z, l), __fdiv_rn(x.w, l));
+        }
+        float* dst = tile + p * (D + 1) + c4 * 4;
+        dst[0] = x.x;
+        dst[1] = x.y;
+        dst[2] = x.z;
+        dst[3] = x.w;
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < D * sp; t += blockDim.x) {
+        const int c = t / sp, p = t - c * sp;
+        const int g = c / kLfGW, cl = c - g * kLfGW;
+        images[(img0 + (int64_t)g * per_group) * stage_f + (int64_t)cl * PS + p0 + p] = tile[p * (D + 1) + c];
+      }
     }
   }
 }
@@ -532,14 +548,15 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
     k_pack_plan<<<1, 1024, 0, s>>>(runs, nruns, cap, TPI, long_fold_groups(D), mega_run_threshold(mode),
                                    pack->cap_images, pack->mlist, pack->moff, pack->mcount, pack->morder);
     SKB_LAUNCH_CHECK();
-    const size_t psm = (size_t)TPI * (long_fold_img_w(D) + 1) * sizeof(float);
+    const int sp = pack_sub(D);
+    const size_t psm = (size_t)sp * (D + 1) * sizeof(float);
     static size_t pset = 0;
-    if (pset < psm) {
+    if (pset < psm && psm > 48 * 1024) {
       SKB_CUDA(cudaFuncSetAttribute(k_pack_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
       pset = psm;
     }
-    k_pack_rows<<<grid_for(pack->cap_images * 256, 256, 4), 256, psm, s>>>(
-        runs, pack->mlist, pack->moff, pack->mcount, ridx, rows, zrow, D, bag_offs, mode, pack->images);
+    k_pack_rows<<<grid_for(pack->cap_images / long_fold_groups(D) * 256 + 256, 256, 4), 256, psm, s>>>(
+        runs, pack->mlist, pack->moff, pack->mcount, ridx, rows, zrow, D, bag_offs, mode, sp, pack->images);
     SKB_LAUNCH_CHECK();
     packed = pack->images;
   }
