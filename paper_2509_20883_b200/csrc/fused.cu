@@ -103,6 +103,11 @@ struct FusedCtx {
   cudaEvent_t lf_ev = nullptr;
   int64_t lf_last = 1;          // > 0: long runs seen recently (pack mega runs)
   cudaEvent_t ev_in = nullptr, ev_side_last = nullptr;
+  // hot-id batches: the long-run fold runs on its own stream concurrently
+  // with the main fold kernel (forked after the runs are listed, joined
+  // before the step ends)
+  cudaStream_t lf_stream = nullptr;
+  cudaEvent_t lf_fork = nullptr, lf_join = nullptr;
   BatchCtx b[2];
   int64_t prep_count = 0, pool_count = 0, bwd_count = 0;
   bool graphs = false;  // replay each phase's device work as a CUDA graph
@@ -166,6 +171,9 @@ void fused_ctx_destroy(FusedCtx* c) {
   cudaFree(c->pack.mcount);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
   if (c->ev_side_last) cudaEventDestroy(c->ev_side_last);
+  if (c->lf_stream) cudaStreamDestroy(c->lf_stream);
+  if (c->lf_fork) cudaEventDestroy(c->lf_fork);
+  if (c->lf_join) cudaEventDestroy(c->lf_join);
   delete c;
 }
 
@@ -185,6 +193,9 @@ static FusedCtx* ctx_get(Table* t) {
     SKB_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
     SKB_CUDA(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
     SKB_CUDA(cudaEventCreateWithFlags(&c->ev_side_last, cudaEventDisableTiming));
+    SKB_CUDA(cudaStreamCreateWithPriority(&c->lf_stream, cudaStreamNonBlocking, hi));
+    SKB_CUDA(cudaEventCreateWithFlags(&c->lf_fork, cudaEventDisableTiming));
+    SKB_CUDA(cudaEventCreateWithFlags(&c->lf_join, cudaEventDisableTiming));
     for (auto& B : c->b) {
       SKB_CUDA(cudaMalloc(&B.dev, sizeof(int64_t) * 4));
       SKB_CUDA(cudaMemset(B.dev, 0, sizeof(int64_t) * 4));
@@ -1819,8 +1830,26 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     static const int persist = env_int("SKB_ADAM_PERSIST", 0);
     const unsigned grid = persist ? grid_for(chunks * 32, 256, 8)
                                                          : (unsigned)((chunks + 7) / 8);
+    // hot-id batches (eager mode): list the long runs now and fold them on
+    // lf_stream while the main fold kernel handles the rest (it skips the
+    // listed runs: longs_cap 0) — the hot chains no longer follow the main
+    // fold, they run beside it
+    static const int overlap_env = env_int("SKB_LF_OVERLAP", 1);
+    const bool overlap = overlap_env && deep && v4 && !graph_mode(c);
+    if (overlap) {
+      k_list_long_runs<<<grid_for(n, 256), 256, 0, s>>>(B.skey, n, B.longs, B.dev + 3, B.longs_cap);
+      SKB_LAUNCH_CHECK();
+      SKB_CUDA(cudaEventRecord(c->lf_fork, s));
+      SKB_CUDA(cudaStreamWaitEvent(c->lf_stream, c->lf_fork, 0));
+      static const int budget_env = env_int("SKB_LF_BUDGET", 0);
+      launch_long_fold<true>(B.longs, B.dev + 3, B.longs_cap, B.sval, dpooled, D, B.bag_offs, mode, a, t->arena,
+                             t->last_step, B.step, c->lf_stream, c->zrow, &c->pack, deep,
+                             budget_env > 0 ? budget_env * 1024 : kLfSmemBudget);
+      SKB_CUDA(cudaEventRecord(c->lf_join, c->lf_stream));
+    }
+    const int64_t lcap = overlap ? 0 : B.longs_cap;
 #define SKB_ADAM_ARGS n, B.skey, B.sval, B.bag_offs, dpooled, mode, D, a, t->arena, t->last_step, B.step, B.dev + 2, \
-                      (v4 ? B.longs : nullptr), B.dev + 3, B.longs_cap, (const float*)c->zrow
+                      (v4 ? B.longs : nullptr), B.dev + 3, lcap, (const float*)c->zrow
     if (!v4) {
       k_fused_adam<1, 1, 4><<<grid, 256, 0, s>>>(SKB_ADAM_ARGS);
     } else {
@@ -1848,7 +1877,9 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     }
 #undef SKB_ADAM_ARGS
     SKB_LAUNCH_CHECK();
-    if (v4)
+    if (overlap)
+      SKB_CUDA(cudaStreamWaitEvent(s, c->lf_join, 0));
+    else if (v4)
       launch_long_fold<true>(B.longs, B.dev + 3, B.longs_cap, B.sval, dpooled, D, B.bag_offs, mode, a, t->arena,
                              t->last_step, B.step, s, c->zrow, &c->pack, deep);
     prof_mark(c, P_ADAM, 1, s);

@@ -33,10 +33,32 @@ struct LongRun {
   uint32_t key, jh, je, pad;
 };
 
+// cap == 0: the runs were listed up front (k_list_long_runs) — skip, do not push
 __device__ __forceinline__ void push_long_run(LongRun* list, int64_t* count, int64_t cap, uint32_t key, uint32_t jh,
                                               uint32_t je) {
+  if (cap <= 0) return;
   unsigned long long i = atomicAdd(reinterpret_cast<unsigned long long*>(count), 1ull);
   if ((int64_t)i < cap) list[i] = LongRun{key, jh, je, 0};
+}
+
+// Up-front listing of the long runs of a sorted key array (so the long fold
+// can start concurrently with the main fold kernel, which then skips them):
+// a head j (j == 0 or key change) starts a run longer than kLongRun iff
+// skey[j + kLongRun] still holds its key; its end is a binary search.
+static __global__ void k_list_long_runs(const uint32_t* __restrict__ skey, int64_t n, LongRun* list, int64_t* count,
+                                        int64_t cap) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = __ldg(skey + j);
+    if (j > 0 && __ldg(skey + j - 1) == k) continue;
+    if (j + kLongRun >= n || __ldg(skey + j + kLongRun) != k) continue;
+    int64_t lo = j + kLongRun, hi = n;  // skey[lo] == k; first index > lo with a different key
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(skey + mid) == k) lo = mid; else hi = mid;
+    }
+    unsigned long long i = atomicAdd(reinterpret_cast<unsigned long long*>(count), 1ull);
+    if ((int64_t)i < cap) list[i] = LongRun{k, (uint32_t)j, (uint32_t)hi, 0};
+  }
 }
 
 // One CTA folds one long run at a time (runs strided over CTAs).  A stage
@@ -523,14 +545,15 @@ template <bool ADAM>
 inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, const uint32_t* ridx,
                              const float* rows, int D, const int64_t* bag_offs, int mode, AdamDev a, float* out,
                              int64_t* last_step, int64_t step, cudaStream_t s, const float* zrow = nullptr,
-                             const LongFoldPack* pack = nullptr, bool expect_mega = true) {
+                             const LongFoldPack* pack = nullptr, bool expect_mega = true,
+                             int smem_budget = kLfSmemBudget) {
   if (D > 32 * kLfMaxNC * kLfCols) raise(SKB_E_UNSUPPORTED, D, "long-run fold: dim > %d", 32 * kLfMaxNC * kLfCols);
   const int nc = long_fold_consumers(D);
   static const int env_pw = getenv("SKB_LF_PW") ? atoi(getenv("SKB_LF_PW")) : 0;
   static const int env_st = getenv("SKB_LF_STAGES") ? atoi(getenv("SKB_LF_STAGES")) : kLfStages;
   int npw = env_pw > 0 && env_pw <= kLfMaxPW ? env_pw : (nc > 4 ? 4 : 8 - nc);  // >= 4 producer warps
   int nst = env_st >= 2 && env_st <= kLfStages ? env_st : kLfStages;
-  if (nst > long_fold_stages(D)) nst = long_fold_stages(D);
+  if (nst > long_fold_stages(D, smem_budget)) nst = long_fold_stages(D, smem_budget);
   if (npw > nst) npw = nst;  // a producer warp must never get a full ring lap ahead (parity waits)
   const int threads = 32 * (nc + npw);
   const size_t sm = long_fold_smem(D, nst);
