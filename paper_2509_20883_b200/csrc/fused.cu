@@ -839,40 +839,47 @@ __global__ void k_tile_row_of(const int64_t* __restrict__ bag_offs, int64_t G, i
 
 // tile combiner, forward: out[g, j*D:(j+1)*D] = w[slot of position off[g]+j]
 // for j < min(len, k), `pad` for len <= j < k (segment_tile, bit-exact copy).
-// U independent row fetches per thread, as in the row gather.
 template <int VEC>
 __global__ void __launch_bounds__(256) k_fused_tile(const float* __restrict__ arena, const uint32_t* __restrict__ slot,
                                                     const int64_t* __restrict__ bag_offs, int64_t G, int64_t k, int D,
-                                                    int64_t D3, float pad, float* __restrict__ out) {
+                                                    int64_t D3, float pad, float* __restrict__ out, int wpb) {
+  // wpb warps own one bag's [k, D] output tile at a time: the bag's offsets are
+  // read once, the tile is a contiguous run of k * D / VEC vectors walked
+  // 32 lanes x U at a time (U loads in flight per lane), and the row / column
+  // of an element come from 32-bit shifts (no 64-bit division per element)
   using V = typename VecT<VEC>::T;
   constexpr int U = 4;
   const int per_row = D / VEC;
-  const int64_t total = G * k * per_row;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < total; base += stride * U) {
-    V v[U];
-    int64_t orow[U];
-    int col[U];
-    bool have[U];
+  const bool pow2 = (per_row & (per_row - 1)) == 0;
+  const int sh = __ffs(per_row) - 1;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t tile_v = k * per_row;  // vectors per bag tile
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < G * wpb; w += warps) {
+    const int64_t g = w / wpb;
+    const int part = (int)(w - g * wpb);
+    const int64_t b = __ldg(bag_offs + g), len = __ldg(bag_offs + g + 1) - b;
+    float* dst = out + g * k * D;
+    for (int64_t q0 = lane + (int64_t)part * 32 * U; q0 < tile_v; q0 += (int64_t)32 * U * wpb) {
+      V v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t t = base + u * stride;
-      have[u] = false;
-      orow[u] = -1;
-      if (t < total) {
-        orow[u] = t / per_row;
-        col[u] = (int)(t - orow[u] * per_row) * VEC;
-        const int64_t g = orow[u] / k, j = orow[u] - g * k;
-        const int64_t b = __ldg(bag_offs + g), e = __ldg(bag_offs + g + 1);
-        if (j < e - b) {
-          have[u] = true;
-          v[u] = vload<VEC>(arena + (int64_t)__ldg(slot + b + j) * D3 + col[u]);
+      for (int u = 0; u < U; ++u) {
+        const int64_t q = q0 + 32 * u;
+        v[u] = vfill<VEC>(pad);
+        if (q < tile_v) {
+          const int64_t j = pow2 ? (q >> sh) : q / per_row;
+          if (j < len) {
+            const int c = (int)(q - j * per_row) * VEC;
+            v[u] = vload<VEC>(arena + (int64_t)__ldg(slot + b + j) * D3 + c);
+          }
         }
       }
-    }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (orow[u] >= 0) vstore<VEC>(out + orow[u] * D + col[u], have[u] ? v[u] : vfill<VEC>(pad));
+      for (int u = 0; u < U; ++u) {
+        const int64_t q = q0 + 32 * u;
+        if (q < tile_v) vstore<VEC>(dst + q * VEC, v[u]);
+      }
+    }
   }
 }
 
@@ -1689,13 +1696,15 @@ static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStrea
     const int64_t ntiles = (G + kTileBags - 1) / kTileBags;
     const bool v4 = D % 4 == 0 && (uintptr_t)pooled % 16 == 0;
     if (B.mode == 2) {  // tile combiner: [G, k*D] rows, pad past each bag's length
-      const int64_t items = G * B.tile_k * (v4 ? D / 4 : D);
+      // warps per bag tile: enough warps to fill the GPU when bags are few
+      const int64_t want = (int64_t)sm_count() * 64;
+      const int wpb = (int)std::min<int64_t>(64, std::max<int64_t>(1, (want + G - 1) / G));
       if (v4)
-        k_fused_tile<4><<<grid_for((items + 3) / 4, 256), 256, 0, s>>>(t->arena, B.slot, B.bag_offs, G, B.tile_k, D,
-                                                                        3 * (int64_t)D, B.pad, pooled);
+        k_fused_tile<4><<<grid_for(G * wpb * 32, 256), 256, 0, s>>>(t->arena, B.slot, B.bag_offs, G, B.tile_k, D,
+                                                                    3 * (int64_t)D, B.pad, pooled, wpb);
       else
-        k_fused_tile<1><<<grid_for((items + 3) / 4, 256), 256, 0, s>>>(t->arena, B.slot, B.bag_offs, G, B.tile_k, D,
-                                                                        3 * (int64_t)D, B.pad, pooled);
+        k_fused_tile<1><<<grid_for(G * wpb * 32, 256), 256, 0, s>>>(t->arena, B.slot, B.bag_offs, G, B.tile_k, D,
+                                                                    3 * (int64_t)D, B.pad, pooled, wpb);
     } else if (!B.any_seq) {
       const unsigned grid = grid_for(((G + 31) / 32) * 32, 256, 8);
 #define SKB_POOL_ARGS t->arena, B.slot, B.bag_offs, G, B.mode, D, 3 * (int64_t)D, pooled
