@@ -23,6 +23,8 @@ __global__ void __launch_bounds__(256) k_rows_gather(Idx idx, const float* __res
   using V = typename VecT<VEC>::T;
   constexpr int U = kRowsUnroll;
   const int per_row = D / VEC;
+  const bool pow2 = (per_row & (per_row - 1)) == 0;
+  const int sh = __ffs(per_row) - 1;
   const int64_t total = n * per_row;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < total; base += stride * U) {
@@ -33,7 +35,7 @@ __global__ void __launch_bounds__(256) k_rows_gather(Idx idx, const float* __res
       const int64_t t = base + u * stride;
       r[u] = -2;  // -2: no item
       if (t < total) {
-        row[u] = t / per_row;
+        row[u] = pow2 ? (t >> sh) : t / per_row;  // no 64-bit division for power-of-two row widths
         col[u] = (int)(t - row[u] * per_row) * VEC;
         r[u] = idx(row[u]);
         if constexpr (CHECK) {
@@ -81,6 +83,8 @@ __global__ void __launch_bounds__(256) k_rows_scatter(Idx idx, const float* __re
   using V = typename VecT<VEC>::T;
   constexpr int U = kRowsUnroll;
   const int per_row = D / VEC;
+  const bool pow2 = (per_row & (per_row - 1)) == 0;
+  const int sh = __ffs(per_row) - 1;
   const int64_t total = n * per_row;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < total; base += stride * U) {
@@ -93,7 +97,7 @@ __global__ void __launch_bounds__(256) k_rows_scatter(Idx idx, const float* __re
       const int64_t t = base + u * stride;
       r[u] = -1;
       if (t < total) {
-        row[u] = t / per_row;
+        row[u] = pow2 ? (t >> sh) : t / per_row;  // no 64-bit division for power-of-two row widths
         col[u] = (int)(t - row[u] * per_row) * VEC;
         r[u] = idx(row[u]);
         v[u] = vload<VEC>(src + row[u] * sstride + col[u]);

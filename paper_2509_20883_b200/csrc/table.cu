@@ -341,6 +341,8 @@ __global__ void __launch_bounds__(256) k_write_rows_if_clear(const int64_t* __re
   using V = typename VecT<VEC>::T;
   constexpr int U = kRowsUnroll;
   const int per_row = D / VEC;
+  const bool pow2 = (per_row & (per_row - 1)) == 0;
+  const int sh = __ffs(per_row) - 1;
   const int64_t total = n * per_row;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < total; base += stride * U) {
@@ -352,7 +354,7 @@ __global__ void __launch_bounds__(256) k_write_rows_if_clear(const int64_t* __re
       const int64_t t = base + u * stride;
       r[u] = -1;
       if (t < total) {
-        row[u] = t / per_row;
+        row[u] = pow2 ? (t >> sh) : t / per_row;  // no 64-bit division for power-of-two row widths
         col[u] = (int)(t - row[u] * per_row) * VEC;
         r[u] = offs[row[u]];
         if (MODE == 0 && col[u] == 0 && r[u] >= 0 && r[u] < rows) bitmap[r[u] >> 5] = 0u;
