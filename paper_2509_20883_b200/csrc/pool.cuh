@@ -18,6 +18,13 @@ template <int VEC> __device__ __forceinline__ typename VecT<VEC>::T vadd(typenam
 template <> __device__ __forceinline__ float4 vadd<4>(float4 a, float4 b) { return add4(a, b); }
 template <> __device__ __forceinline__ float vadd<1>(float a, float b) { return __fadd_rn(a, b); }
 
+template <int VEC> __device__ __forceinline__ typename VecT<VEC>::T vshfl(typename VecT<VEC>::T v, int src);
+template <> __device__ __forceinline__ float4 vshfl<4>(float4 v, int src) {
+  return make_float4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
+                     __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
+}
+template <> __device__ __forceinline__ float vshfl<1>(float v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+
 template <int VEC> __device__ __forceinline__ typename VecT<VEC>::T vload(const float* p);
 template <> __device__ __forceinline__ float4 vload<4>(const float* p) { return ldg4(p); }
 template <> __device__ __forceinline__ float vload<1>(const float* p) { return __ldg(p); }

@@ -30,6 +30,143 @@ __global__ void k_segment_reduce(const float* __restrict__ rows, int D, const in
   }
 }
 
+// Long `sequential` segments: numpy's pairwise tree over rows[b+1:e] has
+// leaves of <= 128 rows that are independent; one warp per (segment, column
+// vector) folds leaf i on lane i (the 8-accumulator leaf loop, unchanged),
+// then every lane evaluates the tree in numpy's order with the leaf values
+// fetched by shuffle — the same additions in the same order as pw_sum, with
+// up to 32 leaves' loads in flight instead of one thread's.
+__device__ __forceinline__ int pw_leaves(int64_t n, int64_t* lb, int64_t* ln, int cap) {
+  int64_t sb[24], sn[24];  // DFS stack (depth <= log2(n / 64) + 1)
+  int sp = 0, k = 0;
+  sb[sp] = 0;
+  sn[sp++] = n;
+  while (sp > 0) {
+    const int64_t b = sb[--sp], m = sn[sp];
+    if (m <= 128) {
+      if (k < cap) {
+        lb[k] = b;
+        ln[k] = m;
+      }
+      ++k;
+      continue;
+    }
+    int64_t n2 = m / 2;
+    n2 -= n2 % 8;
+    sb[sp] = b + n2;  // right pushed first: the left half is visited first
+    sn[sp++] = m - n2;
+    sb[sp] = b;
+    sn[sp++] = n2;
+  }
+  return k;
+}
+
+// numpy's tree over the leaves of a length-n pairwise sum; leaf i's value
+// lives on lane i * cpw + col (uniform control flow: every lane walks the tree)
+template <int VEC>
+__device__ typename VecT<VEC>::T pw_combine(int64_t n, typename VecT<VEC>::T v, int cpw, int col) {
+  using T = typename VecT<VEC>::T;
+  struct Frame {
+    int64_t n;
+    T left;
+    int stage;
+  };
+  Frame st[24];
+  int sp = 0, leaf = 0;
+  st[sp++] = Frame{n, vfill<VEC>(0.f), 0};
+  T result = vfill<VEC>(0.f);
+  bool have = false;
+  while (sp > 0) {
+    Frame& f = st[sp - 1];
+    if (!have) {
+      if (f.n <= 128) {
+        result = vshfl<VEC>(v, leaf++ * cpw + col);
+        have = true;
+        --sp;
+        continue;
+      }
+      int64_t n2 = f.n / 2;
+      n2 -= n2 % 8;
+      st[sp++] = Frame{n2, vfill<VEC>(0.f), 0};
+    } else {
+      int64_t n2 = f.n / 2;
+      n2 -= n2 % 8;
+      if (f.stage == 0) {
+        f.left = result;
+        f.stage = 1;
+        have = false;
+        st[sp++] = Frame{f.n - n2, vfill<VEC>(0.f), 0};
+      } else {
+        result = vadd<VEC>(f.left, result);
+        --sp;
+      }
+    }
+  }
+  return result;
+}
+
+// pw_leaf with two 8-row blocks' loads in flight (the same additions in the
+// same order: r[j] = (r[j] + a[j]) + b[j])
+template <int VEC, class Src>
+__device__ __forceinline__ typename VecT<VEC>::T pw_leaf_x2(const Src& s, int64_t b, int64_t n) {
+  using T = typename VecT<VEC>::T;
+  if (n < 8) return pw_leaf<VEC>(s, b, n);
+  T r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = s.template load<VEC>(b + j);
+  int64_t i = 8;
+  const int64_t lim = n - (n % 8);
+  for (; i + 16 <= lim; i += 16) {
+    T x[8], y[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = s.template load<VEC>(b + i + j);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) y[j] = s.template load<VEC>(b + i + 8 + j);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = vadd<VEC>(vadd<VEC>(r[j], x[j]), y[j]);
+  }
+  for (; i < lim; i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = vadd<VEC>(r[j], s.template load<VEC>(b + i + j));
+  }
+  T res = vadd<VEC>(vadd<VEC>(vadd<VEC>(r[0], r[1]), vadd<VEC>(r[2], r[3])),
+                    vadd<VEC>(vadd<VEC>(r[4], r[5]), vadd<VEC>(r[6], r[7])));
+  for (; i < n; ++i) res = vadd<VEC>(res, s.template load<VEC>(b + i));
+  return res;
+}
+
+// one warp per (segment, column vector): lane i folds leaf i
+template <int VEC>
+__global__ void __launch_bounds__(256) k_segment_reduce_warp(const float* __restrict__ rows, int D,
+                                                             const int64_t* __restrict__ offs, int64_t G, int mode,
+                                                             float* __restrict__ out) {
+  using T = typename VecT<VEC>::T;
+  const int per_row = D / VEC;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < G * per_row; w += warps) {
+    const int64_t g = w / per_row;
+    const int c = (int)(w - g * per_row) * VEC;
+    const int64_t b = offs[g], e0 = offs[g + 1];
+    const int64_t e = reduceat_end(b, e0, g == G - 1, offs[G]);
+    RowSrc src{rows, D, c};
+    T acc;
+    int64_t lb[32], ln[32];
+    const int nl = e - b > 129 ? pw_leaves(e - b - 1, lb, ln, 32) : 1;
+    if (nl == 1 || nl > 32) {  // one leaf (or a very long tree): lane 0, serial pairwise
+      acc = lane == 0 ? pool_sequential<VEC>(src, b, e) : vfill<VEC>(0.f);
+    } else {
+      T v = vfill<VEC>(0.f);
+      if (lane < nl) v = pw_leaf_x2<VEC>(src, b + 1 + lb[lane], ln[lane]);  // all leaves at once
+      acc = vadd<VEC>(src.template load<VEC>(b), pw_combine<VEC>(e - b - 1, v, 1, 0));
+    }
+    if (lane == 0) {
+      if (mode == 1 && e0 > b) acc = vdiv<VEC>(acc, (float)(e0 - b));
+      vstore<VEC>(out + g * D + c, acc);
+    }
+  }
+}
+
 template <int VEC>
 __global__ void k_segment_tile(const float* __restrict__ rows, int D, const int64_t* __restrict__ offs, int64_t G,
                                int64_t k, float pad, float* __restrict__ out) {
@@ -118,10 +255,20 @@ int skb_segment_reduce(const float* rows, int64_t n, int64_t dim, const int64_t*
                        int32_t mode, int32_t strategy, float* out, void* stream) {
   SKB_API_BEGIN
   cudaStream_t s = as_stream(stream);
-  (void)n;
   if (num_segments <= 0 || dim <= 0) return SKB_OK;
   const int D = (int)dim;
-  if (D % 4 == 0 && (uintptr_t)rows % 16 == 0 && (uintptr_t)out % 16 == 0)
+  const bool v4 = D % 4 == 0 && (uintptr_t)rows % 16 == 0 && (uintptr_t)out % 16 == 0;
+  if (strategy == 0 && n >= 256 * num_segments) {  // long sequential segments: warp-parallel pairwise leaves
+    if (v4)
+      k_segment_reduce_warp<4><<<grid_for(num_segments * (D / 4) * 32, 256), 256, 0, s>>>(rows, D, offsets,
+                                                                                          num_segments, mode, out);
+    else
+      k_segment_reduce_warp<1><<<grid_for(num_segments * D * 32, 256), 256, 0, s>>>(rows, D, offsets, num_segments,
+                                                                                    mode, out);
+    SKB_LAUNCH_CHECK();
+    return SKB_OK;
+  }
+  if (v4)
     k_segment_reduce<4><<<grid_for(num_segments * (D / 4), 128), 128, 0, s>>>(rows, D, offsets, num_segments, mode,
                                                                              strategy, out);
   else

@@ -264,6 +264,20 @@ def test_segments_large_random(skb):
             eq(skb.segment_reduce(rows, offs, "mean", strat), O.pool(rows, offs, "mean", strat))
 
 
+@pytest.mark.parametrize("D", [16, 3])
+def test_segments_long_sequential_tree(skb, D):
+    """Long sequential segments take the warp-parallel pairwise kernel (leaves
+    on lanes, tree combined in numpy order): lengths 129-6000 (1 to > 32
+    leaves), empty segments, and trailing empties (the reduceat clip)."""
+    rng = np.random.default_rng(D)
+    lens = np.concatenate([[129, 130, 137, 256, 1000, 1001, 4095, 4097, 6000, 0, 1, 2],
+                           rng.integers(100, 3000, 20), [0, 0]])
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    rows = (rng.standard_normal((int(offs[-1]), D)) * 100).astype(np.float32)
+    for mode in ("sum", "mean"):
+        eq(skb.segment_reduce(rows, offs, mode, "sequential"), O.pool(rows, offs, mode, "sequential"))
+
+
 @pytest.mark.parametrize("variant,wd", [("adam", 0.0), ("adamw", 0.01), ("adamw", 0.0), ("adam", 0.3)])
 def test_adam(skb, golden, variant, wd):
     cfg = skb.AdamConfig(lr=0.01, weight_decay=wd, variant=variant)
