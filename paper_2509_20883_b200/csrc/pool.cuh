@@ -79,6 +79,15 @@ __device__ __forceinline__ typename VecT<VEC>::T pw_leaf(const Src& s, int64_t b
   for (int j = 0; j < 8; ++j) r[j] = s.template load<VEC>(b + j);
   int64_t i = 8;
   const int64_t lim = n - (n % 8);
+  for (; i + 16 <= lim; i += 16) {  // two 8-row blocks' loads in flight; same add order per accumulator
+    T x[8], y[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = s.template load<VEC>(b + i + j);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) y[j] = s.template load<VEC>(b + i + 8 + j);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = vadd<VEC>(vadd<VEC>(r[j], x[j]), y[j]);
+  }
   for (; i < lim; i += 8) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) r[j] = vadd<VEC>(r[j], s.template load<VEC>(b + i + j));

@@ -105,36 +105,6 @@ __device__ typename VecT<VEC>::T pw_combine(int64_t n, typename VecT<VEC>::T v, 
   return result;
 }
 
-// pw_leaf with two 8-row blocks' loads in flight (the same additions in the
-// same order: r[j] = (r[j] + a[j]) + b[j])
-template <int VEC, class Src>
-__device__ __forceinline__ typename VecT<VEC>::T pw_leaf_x2(const Src& s, int64_t b, int64_t n) {
-  using T = typename VecT<VEC>::T;
-  if (n < 8) return pw_leaf<VEC>(s, b, n);
-  T r[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) r[j] = s.template load<VEC>(b + j);
-  int64_t i = 8;
-  const int64_t lim = n - (n % 8);
-  for (; i + 16 <= lim; i += 16) {
-    T x[8], y[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) x[j] = s.template load<VEC>(b + i + j);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) y[j] = s.template load<VEC>(b + i + 8 + j);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = vadd<VEC>(vadd<VEC>(r[j], x[j]), y[j]);
-  }
-  for (; i < lim; i += 8) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = vadd<VEC>(r[j], s.template load<VEC>(b + i + j));
-  }
-  T res = vadd<VEC>(vadd<VEC>(vadd<VEC>(r[0], r[1]), vadd<VEC>(r[2], r[3])),
-                    vadd<VEC>(vadd<VEC>(r[4], r[5]), vadd<VEC>(r[6], r[7])));
-  for (; i < n; ++i) res = vadd<VEC>(res, s.template load<VEC>(b + i));
-  return res;
-}
-
 // one warp per (segment, column vector): lane i folds leaf i
 template <int VEC>
 __global__ void __launch_bounds__(256) k_segment_reduce_warp(const float* __restrict__ rows, int D,
@@ -157,7 +127,7 @@ __global__ void __launch_bounds__(256) k_segment_reduce_warp(const float* __rest
       acc = lane == 0 ? pool_sequential<VEC>(src, b, e) : vfill<VEC>(0.f);
     } else {
       T v = vfill<VEC>(0.f);
-      if (lane < nl) v = pw_leaf_x2<VEC>(src, b + 1 + lb[lane], ln[lane]);  // all leaves at once
+      if (lane < nl) v = pw_leaf<VEC>(src, b + 1 + lb[lane], ln[lane]);  // all leaves at once
       acc = vadd<VEC>(src.template load<VEC>(b), pw_combine<VEC>(e - b - 1, v, 1, 0));
     }
     if (lane == 0) {
