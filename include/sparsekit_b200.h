@@ -162,6 +162,10 @@ int skb_table_idmap_remove(skb_table_t t, int64_t id, int64_t* slot_out_host, vo
 /* free_list copy (bottom .. top), n_out_host <= capacity */
 int skb_table_free_list(skb_table_t t, int64_t* out, int64_t capacity, int64_t* n_out_host,
                         void* stream);
+/* IDMap.free_list mutation (embedding.py:46: a plain mutable list): replace the
+ * free list with slots[0..n) (bottom .. top, device int64); every slot must be
+ * in [0, arena rows) -> SKB_E_VALUE otherwise */
+int skb_table_set_free_list(skb_table_t t, const int64_t* slots, int64_t n, void* stream);
 /* items(): (id, slot) pairs in dict insertion order */
 int skb_table_items(skb_table_t t, int64_t* ids, int64_t* slots, int64_t capacity,
                     int64_t* n_out_host, void* stream);
@@ -181,6 +185,17 @@ int skb_segment_reduce(const float* rows, int64_t n, int64_t dim, const int64_t*
 /* segment_tile segments.py:94-116 -> out [num_segments, k*dim] */
 int skb_segment_tile(const float* rows, int64_t n, int64_t dim, const int64_t* offsets,
                      int64_t num_segments, int64_t k, float pad, float* out, void* stream);
+/* Other row dtypes (the reference's output dtype follows its input,
+ * segments.py:51-58, 103-116).  float64: the same fold orders in double.
+ * int64 (any integer input widened): wrapping sum, order-free.  tile_x64: a
+ * bit copy of 8-byte elements (float64 or int64) with the pad as raw bits. */
+int skb_segment_reduce_f64(const double* rows, int64_t n, int64_t dim, const int64_t* offsets,
+                           int64_t num_segments, int32_t mode, int32_t strategy, double* out,
+                           void* stream);
+int skb_segment_sum_i64(const int64_t* rows, int64_t n, int64_t dim, const int64_t* offsets,
+                        int64_t num_segments, int64_t* out, void* stream);
+int skb_segment_tile_x64(const void* rows, int64_t n, int64_t dim, const int64_t* offsets,
+                         int64_t num_segments, int64_t k, uint64_t pad_bits, void* out, void* stream);
 /* _check_segments segments.py:25-33 / _check_offsets ragged.py:32-42 on device:
  * SKB_E_VALUE if offsets[0] != 0, decreasing, or offsets[len-1] != n_expected */
 int skb_validate_offsets(const int64_t* offsets, int64_t len, int64_t n_expected, void* stream);
@@ -283,8 +298,12 @@ int skb_mod_multi(const int64_t* values, const int64_t* col_offs, int64_t num_co
 int skb_cross_offsets(const int64_t* a_offs, const int64_t* b_offs, int64_t rows,
                       int64_t* out_offs, void* stream);
 int skb_cross(const int64_t* a_vals, const int64_t* a_offs, const int64_t* b_vals,
-              const int64_t* b_offs, int64_t rows, const int64_t* out_offs, int64_t total,
-              int64_t* out, void* stream);
+              const int64_t* b_offs, int64_t rows, const int64_t* out_offs, int64_t total, int64_t* out,
+              int64_t* size_flag, void* stream);
+/* size_flag (optional device int64, caller sets -1): set to the true product
+ * count when `total` (a caller-supplied size, features.cross_many(sizes=))
+ * differs from out_offs[rows]; positions past the true count are zeroed and
+ * never read past the inputs */
 /* RaggedTensor.truncate ragged.py:139-163: new offsets + element gather index */
 int skb_ragged_truncate(const int64_t* offs, int64_t rows, int64_t max_len, int32_t tail,
                         int64_t* new_offs, int64_t* src_index, void* stream);
@@ -305,6 +324,15 @@ int skb_ragged_pad_dense(const void* values, int64_t elem_bytes, int64_t width, 
  * call with an unchanged signature (buffers, sizes, table arrays) and replayed
  * with the step and Adam scalars patched in; growth re-primes.  Results are
  * identical to eager mode.  Default off (SKB_FUSED_GRAPHS=1 turns it on). */
+/* Kernel variant of the fused step, per table (tuning sweeps and tests):
+ * adam 0 = auto (TMA ring <16,192,4> for sum batches of D >= 48 without
+ * recent long runs, else the register kernel), 1-3 register shapes, 4-8 TMA
+ * ring shapes; pool 0 = auto (staged one-hot gather when n == G), 1-4 forced;
+ * -1 = the SKB_ADAM_VARIANT / SKB_POOL_VARIANT environment default.
+ * last_variants: what the last backward / pool ran (adam 0 = TMA default,
+ * -1 = generic-D kernel; pool -1 generic-D, 10 pairwise general). */
+int skb_fused_set_variants(skb_table_t t, int32_t adam_variant, int32_t pool_variant);
+int skb_fused_last_variants(skb_table_t t, int32_t* adam_host, int32_t* pool_host);
 int skb_fused_set_graphs(skb_table_t t, int32_t enable);
 
 /* ---- checkpoint boundary (checkpoint.py:192-313) ------------------------ */

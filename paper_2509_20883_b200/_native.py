@@ -68,10 +68,14 @@ _SIGS = {
     "skb_table_idmap_put": ([_p, _i64, _i64, _p], ctypes.c_int),
     "skb_table_idmap_remove": ([_p, _i64, ctypes.POINTER(_i64), _p], ctypes.c_int),
     "skb_table_free_list": ([_p, _p, _i64, ctypes.POINTER(_i64), _p], ctypes.c_int),
+    "skb_table_set_free_list": ([_p, _p, _i64, _p], ctypes.c_int),
     "skb_table_items": ([_p, _p, _p, _i64, ctypes.POINTER(_i64), _p], ctypes.c_int),
     "skb_sparse_adam_step": ([_p, _p, _i64, _p, ctypes.POINTER(AdamScalars), _p], ctypes.c_int),
     "skb_segment_reduce": ([_p, _i64, _i64, _p, _i64, _i32, _i32, _p, _p], ctypes.c_int),
     "skb_segment_tile": ([_p, _i64, _i64, _p, _i64, _i64, ctypes.c_float, _p, _p], ctypes.c_int),
+    "skb_segment_reduce_f64": ([_p, _i64, _i64, _p, _i64, _i32, _i32, _p, _p], ctypes.c_int),
+    "skb_segment_sum_i64": ([_p, _i64, _i64, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_segment_tile_x64": ([_p, _i64, _i64, _p, _i64, _i64, _u64, _p, _p], ctypes.c_int),
     "skb_validate_offsets": ([_p, _i64, _i64, _p], ctypes.c_int),
     "skb_grad_fold": ([_p, _i64, _i64, _p, _i64, _p, _p], ctypes.c_int),
     "skb_fused_forward": ([_p, _p, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_u64), _i32, _i32, _p, _i64,
@@ -100,10 +104,12 @@ _SIGS = {
     "skb_bucketize_multi_async": ([_p, _p, _i64, _p, _p, _p, _i64, _p, _p], ctypes.c_int),
     "skb_mod_multi": ([_p, _p, _i64, _p, _p, _i64, _p], ctypes.c_int),
     "skb_cross_offsets": ([_p, _p, _i64, _p, _p], ctypes.c_int),
-    "skb_cross": ([_p, _p, _p, _p, _i64, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_cross": ([_p, _p, _p, _p, _i64, _p, _i64, _p, _p, _p], ctypes.c_int),
     "skb_ragged_truncate": ([_p, _i64, _i64, _i32, _p, _p, _p], ctypes.c_int),
     "skb_gather_elems": ([_p, _i64, _p, _i64, _p, _p], ctypes.c_int),
     "skb_ragged_pad_dense": ([_p, _i64, _i64, _p, _i64, _i64, _p, _p, _p, _p], ctypes.c_int),
+    "skb_fused_set_variants": ([_p, _i32, _i32], ctypes.c_int),
+    "skb_fused_last_variants": ([_p, ctypes.POINTER(_i32), ctypes.POINTER(_i32)], ctypes.c_int),
     "skb_fused_set_graphs": ([_p, ctypes.c_int32], ctypes.c_int),
     # checkpoint boundary (checkpoint.py:192-313)
     "skb_argsort_i64": ([_p, _i64, _p, _p, _p], ctypes.c_int),

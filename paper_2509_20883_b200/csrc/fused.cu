@@ -110,6 +110,10 @@ struct FusedCtx {
   cudaEvent_t lf_fork = nullptr, lf_join = nullptr;
   BatchCtx b[2];
   int64_t prep_count = 0, pool_count = 0, bwd_count = 0;
+  // per-table kernel variant overrides (-1: SKB_ADAM_VARIANT / SKB_POOL_VARIANT)
+  // and the variants the last backward / pool actually ran (tests pin them)
+  int adam_var = -1, pool_var = -1;
+  int last_adam = -1, last_pool = -1;
   bool graphs = false;  // replay each phase's device work as a CUDA graph
   cudaStream_t cap = nullptr;  // capture stream of graph mode
   // optional per-kernel CUDA-event profiling: kProf phases x (begin, end) x cap steps
@@ -1436,6 +1440,21 @@ void fused_flush_pending(Table* t, cudaStream_t s) {
   }
 }
 
+void fused_wait_index(Table* t, cudaStream_t s) {
+  FusedCtx* c = t->fused;
+  if (c && c->prep_count > 0) SKB_CUDA(cudaStreamWaitEvent(s, c->ev_side_last, 0));
+}
+
+void fused_require_quiet(Table* t, bool allow_pooled, const char* op) {
+  FusedCtx* c = t->fused;
+  if (!c) return;
+  if (c->prep_count > c->pool_count)
+    raise(SKB_E_VALUE, 0, "%s while a prefetched fused batch is not pooled yet (prefetch admitted its ids): "
+          "run its lookup_pool and pool_grad_adam first", op);
+  if (!allow_pooled && c->pool_count > c->bwd_count)
+    raise(SKB_E_VALUE, 0, "%s between a fused lookup_pool and its pool_grad_adam", op);
+}
+
 // kernel variant knobs for tuning sweeps (SKB_ADAM_VARIANT / SKB_POOL_VARIANT)
 static int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
@@ -1708,6 +1727,9 @@ static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStrea
     } else if (!B.any_seq) {
       const unsigned grid = grid_for(((G + 31) / 32) * 32, 256, 8);
 #define SKB_POOL_ARGS t->arena, B.slot, B.bag_offs, G, B.mode, D, 3 * (int64_t)D, pooled
+      const int pv = c->pool_var >= 0 ? c->pool_var : pool_variant();
+      const int pvar = !v4 ? -1 : (pv == 0 && D <= 128 && B.n == G ? 4 : pv);
+      c->last_pool = pvar;
       if (!v4)
         k_fused_pool_scatter<1, 1, 4><<<grid, 256, 0, s>>>(SKB_POOL_ARGS);
       else
@@ -1716,7 +1738,7 @@ static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStrea
         // staged one-hot gather only for one-hot batches (n == G): its shared
         // staging halves the resident warps of the general chunks (C5: mixed
         // bag lengths ran 0.75 ms/step slower through it)
-        switch (pool_variant() == 0 && D <= 128 && B.n == G ? 4 : pool_variant()) {
+        switch (pvar) {
           case 4: {
             const size_t sm = (size_t)8 * 32 * D * sizeof(float);
             static int attr_set = 0;
@@ -1738,6 +1760,7 @@ static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStrea
         }
 #undef SKB_POOL_ARGS
     } else if (v4) {
+      c->last_pool = 10;  // general (pairwise) pool
       k_fused_pool_general<4><<<grid_for(ntiles * 256, 256, 6), 256, psm, s>>>(t->arena, B.slot, B.bag_offs, G,
                                                                               B.members, B.F, B.mode, D,
                                                                               3 * (int64_t)D, pooled);
@@ -1860,6 +1883,7 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
 #define SKB_ADAM_ARGS n, B.skey, B.sval, B.bag_offs, dpooled, mode, D, a, t->arena, t->last_step, B.step, B.dev + 2, \
                       (v4 ? B.longs : nullptr), B.dev + 3, lcap, (const float*)c->zrow
     if (!v4) {
+      c->last_adam = -1;  // generic-D register kernel
       k_fused_adam<1, 1, 4><<<grid, 256, 0, s>>>(SKB_ADAM_ARGS);
     } else {
       // measured on B200 (C2, D=64): R=1 at 4 blocks/SM 0.59 ms; R=2/4 0.60;
@@ -1869,7 +1893,9 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
       // bags (per-position division), narrow rows (per-copy TMA cost) and
       // hot-id batches (extra gradient rows per run): C5's five tables 6.1 ->
       // 3.4 ms, C3 1.13 -> 0.91 ms, C4 7.99 -> 7.76 ms (B200)
-      const int var = adam_variant() ? adam_variant() : (adam_tma_fits(mode, D, c->lf_last) ? 0 : 2);
+      const int forced = c->adam_var >= 0 ? c->adam_var : adam_variant();
+      const int var = forced ? forced : (adam_tma_fits(mode, D, c->lf_last) ? 0 : 2);
+      c->last_adam = var;
       switch (var) {
         case 1: k_fused_adam<4, 2, 4><<<grid, 256, 0, s>>>(SKB_ADAM_ARGS); break;
         case 2: k_fused_adam<4, 1, 5><<<grid, 256, 0, s>>>(SKB_ADAM_ARGS); break;
@@ -1979,6 +2005,23 @@ int skb_fused_forward(skb_table_t h, const int64_t* ids, int64_t n, const int64_
 int skb_fused_backward(skb_table_t h, const float* dpooled, const skb_adam_t* scalars_host, void* stream) {
   SKB_API_BEGIN
   fused_backward(table_from(h), dpooled, *scalars_host, as_stream(stream));
+  SKB_API_END
+}
+
+int skb_fused_set_variants(skb_table_t h, int32_t adam_variant, int32_t pool_variant) {
+  SKB_API_BEGIN
+  if (adam_variant > 8 || pool_variant > 4) raise(SKB_E_VALUE, 0, "adam variant must be <= 8, pool variant <= 4");
+  FusedCtx* c = ctx_get(table_from(h));
+  c->adam_var = adam_variant;
+  c->pool_var = pool_variant;
+  SKB_API_END
+}
+
+int skb_fused_last_variants(skb_table_t h, int32_t* adam_host, int32_t* pool_host) {
+  SKB_API_BEGIN
+  FusedCtx* c = ctx_get(table_from(h));
+  *adam_host = c->last_adam;
+  *pool_host = c->last_pool;
   SKB_API_END
 }
 

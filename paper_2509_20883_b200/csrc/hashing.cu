@@ -51,8 +51,15 @@ __global__ void k_fnv_pairs(const int64_t* __restrict__ x, const int64_t* __rest
 // output offsets (x-major product, features.py:65-89).
 __global__ void k_cross(const int64_t* __restrict__ a, const int64_t* __restrict__ aoff,
                         const int64_t* __restrict__ b, const int64_t* __restrict__ boff, int64_t rows,
-                        const int64_t* __restrict__ ooff, int64_t total, int64_t* __restrict__ out) {
+                        const int64_t* __restrict__ ooff, int64_t total, int64_t* __restrict__ out,
+                        int64_t* size_flag) {
+  const int64_t true_total = ooff[rows];
+  if (size_flag && blockIdx.x == 0 && threadIdx.x == 0 && true_total != total) *size_flag = true_total;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    if (t >= true_total) {  // a caller-supplied size larger than the products: never read past the inputs
+      out[t] = 0;
+      continue;
+    }
     int64_t lo = 0, hi = rows;  // find r with ooff[r] <= t < ooff[r+1]
     while (hi - lo > 1) {
       int64_t mid = (lo + hi) >> 1;
@@ -141,11 +148,14 @@ int skb_cross_offsets(const int64_t* a_offs, const int64_t* b_offs, int64_t rows
 }
 
 int skb_cross(const int64_t* a_vals, const int64_t* a_offs, const int64_t* b_vals, const int64_t* b_offs,
-              int64_t rows, const int64_t* out_offs, int64_t total, int64_t* out, void* stream) {
+              int64_t rows, const int64_t* out_offs, int64_t total, int64_t* out, int64_t* size_flag,
+              void* stream) {
   SKB_API_BEGIN
-  if (total <= 0) return SKB_OK;
-  k_cross<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(a_vals, a_offs, b_vals, b_offs, rows, out_offs,
-                                                               total, out);
+  if (total < 0) raise(SKB_E_VALUE, total, "cross: negative output size");
+  // total == 0 still launches one thread when a size flag wants the check
+  if (total == 0 && !size_flag) return SKB_OK;
+  k_cross<<<total > 0 ? grid_for(total, 256) : 1, 256, 0, as_stream(stream)>>>(a_vals, a_offs, b_vals, b_offs, rows,
+                                                                               out_offs, total, out, size_flag);
   SKB_LAUNCH_CHECK();
   SKB_API_END
 }

@@ -9,14 +9,17 @@ namespace skb {
 template <int VEC> struct VecT;
 template <> struct VecT<4> { using T = float4; };
 template <> struct VecT<1> { using T = float; };
+template <> struct VecT<0> { using T = double; };  // float64 rows (segments.py keeps the input dtype)
 
 template <int VEC> __device__ __forceinline__ typename VecT<VEC>::T vfill(float x);
 template <> __device__ __forceinline__ float4 vfill<4>(float x) { return make_float4(x, x, x, x); }
 template <> __device__ __forceinline__ float vfill<1>(float x) { return x; }
+template <> __device__ __forceinline__ double vfill<0>(float x) { return (double)x; }
 
 template <int VEC> __device__ __forceinline__ typename VecT<VEC>::T vadd(typename VecT<VEC>::T a, typename VecT<VEC>::T b);
 template <> __device__ __forceinline__ float4 vadd<4>(float4 a, float4 b) { return add4(a, b); }
 template <> __device__ __forceinline__ float vadd<1>(float a, float b) { return __fadd_rn(a, b); }
+template <> __device__ __forceinline__ double vadd<0>(double a, double b) { return __dadd_rn(a, b); }
 
 template <int VEC> __device__ __forceinline__ typename VecT<VEC>::T vshfl(typename VecT<VEC>::T v, int src);
 template <> __device__ __forceinline__ float4 vshfl<4>(float4 v, int src) {
@@ -47,6 +50,14 @@ struct RowSrc {
   template <int VEC> __device__ __forceinline__ typename VecT<VEC>::T load(int64_t p) const {
     return vload<VEC>(rows + p * D + c);
   }
+};
+
+// rows[p * D + c] of a float64 matrix (one column per thread)
+struct RowSrcD {
+  const double* rows;
+  int D;
+  int c;
+  template <int VEC> __device__ __forceinline__ double load(int64_t p) const { return __ldg(rows + p * D + c); }
 };
 
 // np.add.at semantics: ((+0 + r_b) + r_{b+1}) + ...

@@ -137,6 +137,50 @@ __global__ void __launch_bounds__(256) k_segment_reduce_warp(const float* __rest
   }
 }
 
+// float64 rows: one thread per (segment, column), the same fold orders in
+// double (numpy's pairwise_sum is one template for float and double)
+__global__ void k_segment_reduce_f64(const double* __restrict__ rows, int D, const int64_t* __restrict__ offs,
+                                     int64_t G, int mode, int strategy, double* __restrict__ out) {
+  const int64_t total = G * D;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = t / D;
+    const int c = (int)(t - g * D);
+    const int64_t b = offs[g], e = offs[g + 1];
+    RowSrcD src{rows, D, c};
+    double acc = strategy == 0 ? pool_sequential<0>(src, b, reduceat_end(b, e, g == G - 1, offs[G]))
+                               : pool_scatter<0>(src, b, e);
+    if (mode == 1 && e > b) acc = __ddiv_rn(acc, (double)(e - b));
+    out[g * D + c] = acc;
+  }
+}
+
+// integer rows: wrapping int64 sums (order-independent, so one kernel serves
+// both strategies)
+__global__ void k_segment_sum_i64(const int64_t* __restrict__ rows, int D, const int64_t* __restrict__ offs,
+                                  int64_t G, int64_t* __restrict__ out) {
+  const int64_t total = G * D;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = t / D;
+    const int c = (int)(t - g * D);
+    uint64_t acc = 0;
+    for (int64_t p = offs[g]; p < offs[g + 1]; ++p) acc += (uint64_t)__ldg(rows + p * D + c);
+    out[t] = (int64_t)acc;
+  }
+}
+
+// 8-byte elements (float64 or int64 rows): a bit copy, pad given as bits
+__global__ void k_segment_tile_x64(const uint64_t* __restrict__ rows, int D, const int64_t* __restrict__ offs,
+                                   int64_t G, int64_t k, uint64_t pad, uint64_t* __restrict__ out) {
+  const int64_t total = G * k * D;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t gj = t / D;
+    const int c = (int)(t - gj * D);
+    const int64_t g = gj / k, j = gj - g * k;
+    const int64_t b = offs[g], len = offs[g + 1] - b;
+    out[t] = j < len ? __ldg(rows + (b + j) * D + c) : pad;
+  }
+}
+
 template <int VEC>
 __global__ void k_segment_tile(const float* __restrict__ rows, int D, const int64_t* __restrict__ offs, int64_t G,
                                int64_t k, float pad, float* __restrict__ out) {
@@ -261,6 +305,40 @@ int skb_segment_tile(const float* rows, int64_t n, int64_t dim, const int64_t* o
                                                                                out);
   else
     k_segment_tile<1><<<grid_for(num_segments * k * D, 256), 256, 0, s>>>(rows, D, offsets, num_segments, k, pad, out);
+  SKB_LAUNCH_CHECK();
+  SKB_API_END
+}
+
+int skb_segment_reduce_f64(const double* rows, int64_t n, int64_t dim, const int64_t* offsets, int64_t num_segments,
+                           int32_t mode, int32_t strategy, double* out, void* stream) {
+  SKB_API_BEGIN
+  (void)n;
+  if (num_segments <= 0 || dim <= 0) return SKB_OK;
+  k_segment_reduce_f64<<<grid_for(num_segments * dim, 128), 128, 0, as_stream(stream)>>>(
+      rows, (int)dim, offsets, num_segments, mode, strategy, out);
+  SKB_LAUNCH_CHECK();
+  SKB_API_END
+}
+
+int skb_segment_sum_i64(const int64_t* rows, int64_t n, int64_t dim, const int64_t* offsets, int64_t num_segments,
+                        int64_t* out, void* stream) {
+  SKB_API_BEGIN
+  (void)n;
+  if (num_segments <= 0 || dim <= 0) return SKB_OK;
+  k_segment_sum_i64<<<grid_for(num_segments * dim, 128), 128, 0, as_stream(stream)>>>(rows, (int)dim, offsets,
+                                                                                      num_segments, out);
+  SKB_LAUNCH_CHECK();
+  SKB_API_END
+}
+
+int skb_segment_tile_x64(const void* rows, int64_t n, int64_t dim, const int64_t* offsets, int64_t num_segments,
+                         int64_t k, uint64_t pad_bits, void* out, void* stream) {
+  SKB_API_BEGIN
+  (void)n;
+  if (k < 0) raise(SKB_E_VALUE, k, "k must be >= 0");
+  if (num_segments <= 0 || k == 0 || dim <= 0) return SKB_OK;
+  k_segment_tile_x64<<<grid_for(num_segments * k * dim, 256), 256, 0, as_stream(stream)>>>(
+      static_cast<const uint64_t*>(rows), (int)dim, offsets, num_segments, k, pad_bits, static_cast<uint64_t*>(out));
   SKB_LAUNCH_CHECK();
   SKB_API_END
 }

@@ -79,6 +79,10 @@ static void rehash(Table* t, int64_t new_cap, cudaStream_t s) {
 
 void table_refresh(Table* t, cudaStream_t s) {
   g_refreshes++;
+  // a prefetched batch's admission may still run on the fused index stream:
+  // the counters are read after it (else num_rows / export would size from
+  // stale counters and the next reserve would miss that batch's rows)
+  fused_wait_index(t, s);
   SKB_CUDA(cudaMemcpyAsync(t->snap_host, t->counters, sizeof(int64_t) * C_N, cudaMemcpyDeviceToHost, s));
   SKB_CUDA(cudaStreamSynchronize(s));
   for (int i = 0; i < C_N; ++i) t->known[i] = t->snap_host[i];
@@ -464,6 +468,7 @@ static void checked_write(Table* t, const int64_t* offs, int64_t n, int which, c
 
 // EmbeddingTable.scatter_update: distinct + live, then write (one launch)
 static void checked_scatter_update(Table* t, const int64_t* offs, int64_t n, const float* rows, cudaStream_t s) {
+  fused_require_quiet(t, true, "scatter_update");
   ensure_bitmap(t, s);
   const bool v4 = t->dim % 4 == 0 && (uintptr_t)rows % 16 == 0;
   if (v4) launch_checked_scatter<4, 0>(t, offs, n, rows, t->arena, s);
@@ -484,10 +489,15 @@ static void checked_scatter_update(Table* t, const int64_t* offs, int64_t n, con
 // ---------------------------------------------------------------------------
 // eviction (embedding.py:252-274)
 // ---------------------------------------------------------------------------
-__global__ void k_stale(const uint8_t* __restrict__ live, const int64_t* __restrict__ last, int64_t rows, int64_t step,
-                        int64_t thr, uint8_t* __restrict__ flags) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
-    flags[i] = (live[i] && (step - last[i]) > thr) ? 1 : 0;
+// stale IDMap entries (embedding.py:262-264 iterates the dict, not the live
+// flags: an id removed from the IDMap is never evicted, a put entry is)
+__global__ void k_stale_entries(const HEntry* __restrict__ map, int64_t cap, const int64_t* __restrict__ last,
+                                int64_t step, int64_t thr, uint8_t* __restrict__ flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= cap; i += (int64_t)gridDim.x * blockDim.x) {
+    const HEntry e = map[i];
+    const bool valid = i == cap ? e.val >= 0 : e.key != kEmptyKey;
+    flags[i] = (valid && (step - last[e.val]) > thr) ? 1 : 0;
+  }
 }
 
 __global__ void k_gather_i64(const int64_t* __restrict__ src, const int64_t* __restrict__ idx, int64_t n,
@@ -531,28 +541,35 @@ __global__ void k_evict_counters(int64_t* counters, int64_t E) {
   counters[C_ROWS] -= E;
 }
 
-// keep only entries whose slot is still live (rebuild instead of tombstones)
-__global__ void k_rebuild_live(const HEntry* __restrict__ old, int64_t cap, const uint8_t* __restrict__ live,
+// keep every entry except the evicted ones (rebuild instead of tombstones)
+__global__ void k_rebuild_drop(const HEntry* __restrict__ old, int64_t cap, const uint8_t* __restrict__ drop,
                                HEntry* nt) {
   const uint64_t mask = (uint64_t)(cap - 1);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= cap; i += (int64_t)gridDim.x * blockDim.x) {
     HEntry e = old[i];
     if (i == cap) {
-      nt[cap].val = (e.val >= 0 && live[e.val]) ? e.val : -1;
-    } else if (e.key != kEmptyKey && live[e.val]) {
+      nt[cap].val = drop[i] ? -1 : e.val;
+    } else if (e.key != kEmptyKey && !drop[i]) {
       idmap_insert(nt, mask, cap, e.key, e.val);
     }
   }
 }
 
+__global__ void k_entry_pairs(const HEntry* __restrict__ map, int64_t cap, const int64_t* __restrict__ idx, int64_t n,
+                              const int64_t* __restrict__ ins_seq, int64_t* __restrict__ keys,
+                              int64_t* __restrict__ slots, int64_t* __restrict__ seq);
+
 int64_t table_evict(Table* t, int64_t step, cudaStream_t s) {
+  fused_require_quiet(t, false, "evict");
   fused_flush_pending(t, s);
-  if (t->evict_threshold < 0 || t->arena_rows == 0) return 0;
-  const int64_t R = t->arena_rows;
-  Scratch flags(R, s), stale(sizeof(int64_t) * R, s), cnt(sizeof(int64_t) * 2, s);
-  k_stale<<<grid_for(R, 256), 256, 0, s>>>(t->live, t->last_step, R, step, t->evict_threshold, flags.as<uint8_t>());
+  if (t->evict_threshold == kNoEvict || t->arena_rows == 0) return 0;
+  // stale IDMap entries, in dict insertion order (embedding.py:262-272)
+  const int64_t cap = t->idmap_cap;
+  Scratch flags(cap + 1, s), idx(sizeof(int64_t) * (cap + 1), s), cnt(sizeof(int64_t) * 2, s);
+  k_stale_entries<<<grid_for(cap + 1, 256), 256, 0, s>>>(t->idmap, cap, t->last_step, step, t->evict_threshold,
+                                                         flags.as<uint8_t>());
   SKB_LAUNCH_CHECK();
-  select_flagged_index(flags.as<uint8_t>(), R, stale.as<int64_t>(), cnt.as<int64_t>(), s);
+  select_flagged_index(flags.as<uint8_t>(), cap + 1, idx.as<int64_t>(), cnt.as<int64_t>(), s);
   // E and the insertion-sequence counter in one readback: every ins_seq is
   // below C_SEQ, so the order sort needs only bit_width(C_SEQ) key bits
   SKB_CUDA(cudaMemcpyAsync(cnt.as<int64_t>() + 1, t->counters + C_SEQ, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
@@ -563,19 +580,21 @@ int64_t table_evict(Table* t, int64_t step, cudaStream_t s) {
   if (E == 0) return 0;
   int bits = 1;
   while (bits < 64 && (seq_hi >> bits) != 0) ++bits;
-  Scratch seq(sizeof(int64_t) * E, s), seq2(sizeof(int64_t) * E, s), slots2(sizeof(int64_t) * E, s);
-  k_gather_i64<<<grid_for(E, 256), 256, 0, s>>>(t->ins_seq, stale.as<int64_t>(), E, seq.as<int64_t>());
+  Scratch keys(sizeof(int64_t) * E, s), slots(sizeof(int64_t) * E, s), seq(sizeof(int64_t) * E, s),
+      seq2(sizeof(int64_t) * E, s), slots2(sizeof(int64_t) * E, s);
+  k_entry_pairs<<<grid_for(E, 256), 256, 0, s>>>(t->idmap, cap, idx.as<int64_t>(), E, t->ins_seq, keys.as<int64_t>(),
+                                                slots.as<int64_t>(), seq.as<int64_t>());
   SKB_LAUNCH_CHECK();
-  sort_pairs_i64(seq.as<int64_t>(), seq2.as<int64_t>(), stale.as<int64_t>(), slots2.as<int64_t>(), E, s, bits);
+  sort_pairs_i64(seq.as<int64_t>(), seq2.as<int64_t>(), slots.as<int64_t>(), slots2.as<int64_t>(), E, s, bits);
   k_evict_apply<<<grid_for(E * ((t->dim + 3) / 4), 256), 256, 0, s>>>(slots2.as<int64_t>(), E, (int)t->dim, t->counters,
                                                          t->free_list, t->live, t->last_step, t->arena);
   SKB_LAUNCH_CHECK();
   k_evict_counters<<<1, 1, 0, s>>>(t->counters, E);
   SKB_LAUNCH_CHECK();
   HEntry* nt = nullptr;
-  SKB_CUDA(cudaMallocAsync(&nt, sizeof(HEntry) * (t->idmap_cap + 1), s));
-  ht_fill(nt, t->idmap_cap + 1, -1, s);
-  k_rebuild_live<<<grid_for(t->idmap_cap + 1, 256), 256, 0, s>>>(t->idmap, t->idmap_cap, t->live, nt);
+  SKB_CUDA(cudaMallocAsync(&nt, sizeof(HEntry) * (cap + 1), s));
+  ht_fill(nt, cap + 1, -1, s);
+  k_rebuild_drop<<<grid_for(cap + 1, 256), 256, 0, s>>>(t->idmap, cap, flags.as<uint8_t>(), nt);
   SKB_LAUNCH_CHECK();
   SKB_CUDA(cudaFreeAsync(t->idmap, s));
   t->idmap = nt;
@@ -592,19 +611,26 @@ struct IdxSlotArena {
   __device__ __forceinline__ int64_t operator()(int64_t i) const { return slots[i]; }
 };
 
+__global__ void k_entry_flags(const HEntry* __restrict__ map, int64_t cap, uint8_t* __restrict__ flags);
+
+// the IDMap's entries sorted by id (embedding.py:276-284 iterates the dict:
+// a slot whose id was removed from the IDMap is not exported, even if live)
 int64_t table_export(Table* t, int64_t* ids, float* w, float* m, float* v, int64_t* last, int64_t capacity,
                      cudaStream_t s) {
   fused_flush_pending(t, s);
-  const int64_t R = t->arena_rows;
-  if (R == 0) return 0;
-  Scratch slots(sizeof(int64_t) * R, s), cnt(sizeof(int64_t), s);
-  select_flagged_index(t->live, R, slots.as<int64_t>(), cnt.as<int64_t>(), s);
+  const int64_t cap = t->idmap_cap;
+  Scratch flags(cap + 1, s), idx(sizeof(int64_t) * (cap + 1), s), cnt(sizeof(int64_t), s);
+  k_entry_flags<<<grid_for(cap + 1, 256), 256, 0, s>>>(t->idmap, cap, flags.as<uint8_t>());
+  SKB_LAUNCH_CHECK();
+  select_flagged_index(flags.as<uint8_t>(), cap + 1, idx.as<int64_t>(), cnt.as<int64_t>(), s);
   int64_t n = read_i64(cnt.as<int64_t>(), s);
   if (n > capacity) raise(SKB_E_ARG, n, "export buffers hold %lld rows, table has %lld", (long long)capacity,
                           (long long)n);
   if (n == 0) return 0;
-  Scratch keys(sizeof(int64_t) * n, s), slots2(sizeof(int64_t) * n, s);
-  k_gather_i64<<<grid_for(n, 256), 256, 0, s>>>(t->slot_key, slots.as<int64_t>(), n, keys.as<int64_t>());
+  Scratch keys(sizeof(int64_t) * n, s), slots(sizeof(int64_t) * n, s), seq(sizeof(int64_t) * n, s),
+      slots2(sizeof(int64_t) * n, s);
+  k_entry_pairs<<<grid_for(n, 256), 256, 0, s>>>(t->idmap, cap, idx.as<int64_t>(), n, t->ins_seq, keys.as<int64_t>(),
+                                                slots.as<int64_t>(), seq.as<int64_t>());
   SKB_LAUNCH_CHECK();
   sort_pairs_i64(keys.as<int64_t>(), ids, slots.as<int64_t>(), slots2.as<int64_t>(), n, s);
   const int D = (int)t->dim;
@@ -645,8 +671,14 @@ __global__ void k_restore(const int64_t* __restrict__ ids, int64_t n, const int6
 
 __global__ void k_set_i64(int64_t* p, int64_t v) { *p = v; }
 
+__global__ void k_range_flag(const int64_t* __restrict__ v, int64_t n, int64_t hi, unsigned long long* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (v[i] < 0 || v[i] >= hi) atomicMin(flag, (unsigned long long)i);
+}
+
 void table_restore(Table* t, const int64_t* ids, int64_t n, const float* w, const float* m, const float* v,
                    const int64_t* last, cudaStream_t s) {
+  fused_require_quiet(t, false, "restore_rows");
   fused_flush_pending(t, s);
   if (n == 0) return;
   {
@@ -1113,6 +1145,7 @@ int skb_table_idmap_put(skb_table_t h, int64_t id, int64_t slot, void* stream) {
   Table* t = table_from(h);
   cudaStream_t s = as_stream(stream);
   if (slot < 0) raise(SKB_E_VALUE, slot, "slot must be >= 0");
+  fused_require_quiet(t, false, "IDMap.put");
   table_reserve(t, 1, s);
   if (slot >= t->arena_rows) grow_arena(t, slot + 1, s);
   k_idmap_put<<<1, 1, 0, s>>>(t->idmap, (uint64_t)(t->idmap_cap - 1), t->idmap_cap, id, slot, t->counters,
@@ -1126,6 +1159,8 @@ int skb_table_idmap_remove(skb_table_t h, int64_t id, int64_t* slot_out_host, vo
   SKB_API_BEGIN
   Table* t = table_from(h);
   cudaStream_t s = as_stream(stream);
+  fused_require_quiet(t, false, "IDMap.remove");
+  fused_flush_pending(t, s);
   Scratch out(sizeof(int64_t), s);
   k_idmap_remove<<<1, 1, 0, s>>>(t->idmap, (uint64_t)(t->idmap_cap - 1), t->idmap_cap, id, t->counters,
                                  out.as<int64_t>());
@@ -1147,6 +1182,31 @@ int skb_table_free_list(skb_table_t h, int64_t* out, int64_t capacity, int64_t* 
                           (long long)capacity);
   if (F) SKB_CUDA(cudaMemcpyAsync(out, t->free_list, sizeof(int64_t) * F, cudaMemcpyDeviceToDevice, s));
   *n_out_host = F;
+  SKB_API_END
+}
+
+int skb_table_set_free_list(skb_table_t h, const int64_t* slots, int64_t n, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  cudaStream_t s = as_stream(stream);
+  if (n < 0) raise(SKB_E_VALUE, n, "free list length must be >= 0");
+  fused_require_quiet(t, false, "free_list mutation");
+  fused_flush_pending(t, s);
+  if (n > 0) {
+    DevFlag f(s);
+    k_range_flag<<<grid_for(n, 256), 256, 0, s>>>(slots, n, t->arena_rows, f.ptr());
+    SKB_LAUNCH_CHECK();
+    const int64_t bad = f.read();
+    if (bad >= 0) {
+      const int64_t o = read_i64(slots + bad, s);
+      raise(SKB_E_VALUE, o, "free_list: slot %lld is outside the store (%lld rows)", (long long)o,
+            (long long)t->arena_rows);
+    }
+    SKB_CUDA(cudaMemcpyAsync(t->free_list, slots, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, s));
+  }
+  k_set_i64<<<1, 1, 0, s>>>(t->counters + C_FREE, n);
+  SKB_LAUNCH_CHECK();
+  table_refresh(t, s);
   SKB_API_END
 }
 

@@ -22,10 +22,14 @@ namespace skb {
 
 enum { C_ALLOC = 0, C_FREE = 1, C_ROWS = 2, C_SEQ = 3, C_N = 4 };
 
+// evict_threshold=None (eviction disabled); any other value, negative ones
+// included, evicts with the reference's `step - last_step > threshold`
+constexpr int64_t kNoEvict = (int64_t)0x8000000000000000ull;  // INT64_MIN
+
 struct FusedCtx;  // fused.cu
 
 struct Table {
-  int64_t dim = 0, seed = 0, block_size = 0, evict_threshold = -1;
+  int64_t dim = 0, seed = 0, block_size = 0, evict_threshold = kNoEvict;
   int64_t gen = 0;  // bumped whenever a device array is reallocated (captured graphs bake pointers)
   int device = 0;
   double init_scale = 0.0;  // 1 / sqrt(dim), host double (embedding.py:34)
@@ -85,6 +89,12 @@ void table_admit(Table* t, const int64_t* ids, int64_t n, int64_t step, int64_t*
 void fused_ctx_destroy(FusedCtx* c);
 // apply a fused forward's deferred last_step writes before any other table op
 void fused_flush_pending(Table* t, cudaStream_t s);
+// order stream s after the fused index stream's last work (counter reads)
+void fused_wait_index(Table* t, cudaStream_t s);
+// ValueError while a prefetched fused batch is not pooled yet (its ids are
+// admitted already), or — allow_pooled false — while a fused step awaits its
+// backward: `op` would change slots that batch still uses
+void fused_require_quiet(Table* t, bool allow_pooled, const char* op);
 
 // device helpers ------------------------------------------------------------
 __device__ __forceinline__ long long idmap_find(const HEntry* t, uint64_t mask, int64_t cap, long long key) {

@@ -34,7 +34,7 @@ class _Handle:
         N.lib()
         h = ctypes.c_void_p()
         N.check(N.lib().skb_table_create(dim, seed, block_size,
-                                         -1 if evict_threshold is None else int(evict_threshold),
+                                         -(1 << 63) if evict_threshold is None else int(evict_threshold),
                                          int(capacity_hint), ctypes.byref(h)))
         self.h = h
         self.device = N.torch().cuda.current_device()
@@ -68,11 +68,45 @@ def initial_rows(seed: int, ids, dim: int, dtype=np.float32):
     return N.out_like(out, as_np)
 
 
+class FreeList(list):
+    """`IDMap.free_list` (embedding.py:46): a plain list of reusable slots
+    (bottom .. top, the top is popped first).  It holds a copy of the device
+    free list; every mutating list operation writes the whole list back to the
+    table (skb_table_set_free_list), so code that edits the reference's list
+    in place keeps working.  Reads are list reads of the copy."""
+
+    def __init__(self, handle, items):
+        super().__init__(items)
+        self._h = handle
+
+    def _push(self):
+        vals = [int(x) for x in list.__iter__(self)]
+        d = N.to_dev(np.asarray(vals, np.int64), "int64") if vals else None
+        N.call("skb_table_set_free_list", self._h.h, N.ptr(d) if d is not None else None, len(vals),
+               N.stream_ptr())
+
+
+def _writeback(name):
+    base = getattr(list, name)
+
+    def op(self, *a, **k):
+        r = base(self, *a, **k)
+        self._push()
+        return self if name in ("__iadd__", "__imul__") else r
+    op.__name__ = name
+    return op
+
+
+for _m in ("append", "extend", "insert", "pop", "remove", "clear", "sort", "reverse", "__setitem__",
+           "__delitem__", "__iadd__", "__imul__"):
+    setattr(FreeList, _m, _writeback(_m))
+
+
 class IDMap:
     """First tier: feature id -> slot offset (embedding.py:39-61), device-resident.
 
-    `free_list` returns a snapshot list (bottom .. top); mutate the table
-    through EmbeddingTable methods.
+    `free_list` is a `FreeList`: a list copy whose in-place mutations are
+    written back to the device table.
     """
 
     def __init__(self, handle: _Handle):
@@ -113,12 +147,16 @@ class IDMap:
         return list(zip(ids[:k].cpu().tolist(), slots[:k].cpu().tolist()))
 
     @property
-    def free_list(self) -> list:
+    def free_list(self) -> FreeList:
         n = self._h.stats()[2]
         out = N.empty((max(n, 1),), "int64")
         cnt = ctypes.c_int64()
         N.call("skb_table_free_list", self._h.h, N.ptr(out), n, ctypes.byref(cnt), N.stream_ptr())
-        return out[: cnt.value].cpu().tolist()
+        return FreeList(self._h, out[: cnt.value].cpu().tolist())
+
+    @free_list.setter
+    def free_list(self, slots) -> None:
+        FreeList(self._h, list(slots))._push()
 
 
 class BlockStore:

@@ -168,21 +168,36 @@ def _cross_pairs(pairs, sizes=None):
         prep.append((as_np, av, ao, bv, bo, rows, oo))
     if not prep:
         return []
+    flags = None
     if sizes is not None:
         if len(sizes) != len(prep):
             raise ValueError(f"{len(sizes)} sizes for {len(prep)} column pairs")
         totals = [int(x) for x in sizes]
+        if any(x < 0 for x in totals):
+            raise ValueError("cross sizes must be >= 0")
+        # caller-supplied sizes are checked against the device totals: inside
+        # deferred_checks() at its exit, otherwise right here (one sync)
+        flags = t.full((len(prep),), -1, dtype=t.int64, device=prep[0][1].device)
     else:
         totals = t.stack([p[6][-1] for p in prep]).cpu().tolist()  # the single synchronisation
     res = []
-    for (as_np, av, ao, bv, bo, rows, oo), total in zip(prep, totals):
+    for i, ((as_np, av, ao, bv, bo, rows, oo), total) in enumerate(zip(prep, totals)):
         out = N.empty((int(total),), "int64")
-        if total:
+        if total or flags is not None:
             N.call("skb_cross", N.ptr(av), N.ptr(ao), N.ptr(bv), N.ptr(bo), rows, N.ptr(oo), int(total), N.ptr(out),
-                   N.stream_ptr())
+                   N.ptr(flags[i:i + 1]) if flags is not None else None, N.stream_ptr())
         # offsets come from the validated inputs by construction: carried as trusted
-        res.append(RaggedTensor(out.cpu().numpy(), oo.cpu().numpy()) if as_np else RaggedTensor._trusted(out, oo))
-    return res
+        res.append((as_np, out, oo))
+    if flags is not None:
+        stack = getattr(_DEFERRED, "stack", None)
+        pending = [(flags[i:i + 1], f"cross_many: sizes[{i}] = {totals[i]} does not match the rows' product count")
+                   for i in range(len(prep))]
+        if stack:
+            stack[-1].extend(pending)
+        else:
+            _raise_pending(pending)
+    return [RaggedTensor(out.cpu().numpy(), oo.cpu().numpy()) if as_np else RaggedTensor._trusted(out, oo)
+            for as_np, out, oo in res]
 
 
 class FusedPlan:

@@ -103,7 +103,9 @@ def prefetch(lt: LogicalTable, batch: PackedBatch, step: int, mode: str = "mean"
     and `pool_grad_adam` of step k): the index work of step k+1 then runs on
     the table's index stream underneath step k's pool and fold+Adam.  At
     most two batches are in flight.  Admission happens at prefetch time, so
-    do not prefetch across an eviction / restore boundary.
+    table edits that would move slots the prefetched batch already holds
+    (evict, restore_rows, IDMap put / remove / free_list, scatter_update)
+    raise ValueError until that batch has been pooled and backwarded.
     """
     telemetry.bump("fused.prefetch")
     args = _batch_args(lt, batch, step, mode)
@@ -159,3 +161,18 @@ def use_graphs(lt: LogicalTable, enable: bool = True) -> None:
     mode; it removes the per-kernel launch cost that dominates small batches."""
     for t in lt.shards:
         N.call("skb_fused_set_graphs", t.handle, int(bool(enable)))
+
+
+def set_variants(lt: LogicalTable, adam: int = -1, pool: int = -1) -> None:
+    """Force the fused step's fold+Adam / pool kernel variant on `lt`
+    (-1 = environment default, 0 = auto).  Every variant is
+    bit-exact; this exists for sweeps and for the parity tests."""
+    for t in lt.shards:
+        N.call("skb_fused_set_variants", t.handle, int(adam), int(pool))
+
+
+def last_variants(lt: LogicalTable):
+    """(fold+Adam variant, pool variant) the last fused step ran on shard 0."""
+    a, p = ctypes.c_int32(), ctypes.c_int32()
+    N.call("skb_fused_last_variants", lt.shards[0].handle, ctypes.byref(a), ctypes.byref(p))
+    return int(a.value), int(p.value)

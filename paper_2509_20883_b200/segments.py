@@ -62,6 +62,34 @@ def _rows2d(rows):
     return (r if r.ndim == 2 else r[:, None]), True
 
 
+def _row_kind(rows):
+    """(kind, device dtype, output dtype name).  The output dtype follows the
+    rows (segments.py:51-58, 103-116): float32 and float64 have bit-exact
+    kernels, integer rows are widened to int64 (wrapping sums, cast back)."""
+    name = str(rows.dtype).replace("torch.", "")
+    if name in ("float32", "float64"):
+        return name, name, name
+    if name in ("int8", "int16", "int32", "int64", "uint8", "uint16", "uint32", "uint64"):
+        return "int", "int64", name
+    raise TypeError(f"segment ops take float or integer rows, got {name}")
+
+
+def _cast_out(out, name):
+    t = N.torch()
+    if str(out.dtype).replace("torch.", "") == name:
+        return out
+    if name.startswith("uint") and not hasattr(t, name):
+        return out  # reinterpreted below on the numpy side
+    return out.to(getattr(t, name))
+
+
+def _finish(out, name, as_np):
+    if as_np:
+        a = out.cpu().numpy()
+        return a if a.dtype == np.dtype(name) else a.astype(np.dtype(name))
+    return _cast_out(out, name)
+
+
 def segment_reduce(rows, segments, mode: str = "sum", strategy: str = "auto"):
     """Pool contiguous row segments (segments.py:61-91)."""
     telemetry.bump("segments.segment_reduce")
@@ -72,16 +100,24 @@ def segment_reduce(rows, segments, mode: str = "sum", strategy: str = "auto"):
         raise ValueError(f"unknown mode {mode!r}")
     G = (offs.numel() if N.is_torch(offs) else len(offs)) - 1
     strategy = resolve_strategy(strategy, n, G)
-    r = N.to_dev(rows, "float32")
+    kind, dt, oname = _row_kind(rows)
+    if kind == "int" and mode == "mean":
+        # segments.py:88-90 divides in place into the integer output
+        raise TypeError(f"Cannot cast ufunc 'divide' output from dtype('float64') to dtype('{oname}') "
+                        "with casting rule 'same_kind'")
+    r = N.to_dev(rows.astype(np.int64) if (kind == "int" and not N.is_torch(rows)) else rows, dt)
     o = N.to_dev(offs, "int64")
-    out = N.empty((G, dim), "float32")
+    out = N.empty((G, dim), dt)
     if G and dim:
         if n == 0:
             out.zero_()
+        elif kind == "int":
+            N.call("skb_segment_sum_i64", N.ptr(r), n, dim, N.ptr(o), G, N.ptr(out), N.stream_ptr())
         else:
-            N.call("skb_segment_reduce", N.ptr(r), n, dim, N.ptr(o), G, _MODES[mode], _STRATEGIES[strategy],
-                   N.ptr(out), N.stream_ptr())
-    return N.out_like(out, as_np)
+            fn = "skb_segment_reduce" if dt == "float32" else "skb_segment_reduce_f64"
+            N.call(fn, N.ptr(r), n, dim, N.ptr(o), G, _MODES[mode], _STRATEGIES[strategy], N.ptr(out),
+                   N.stream_ptr())
+    return _finish(out, oname, as_np)
 
 
 def segment_tile(rows, segments, k: int, pad: float = 0.0):
@@ -93,9 +129,16 @@ def segment_tile(rows, segments, k: int, pad: float = 0.0):
     n, dim = int(rows.shape[0]), int(rows.shape[1])
     offs = _check_segments(segments, n)
     G = (offs.numel() if N.is_torch(offs) else len(offs)) - 1
-    out = N.empty((G, k * dim), "float32")
+    kind, dt, oname = _row_kind(rows)
+    out = N.empty((G, k * dim), dt)
     if G and k and dim:
-        r = N.to_dev(rows, "float32")
+        r = N.to_dev(rows.astype(np.int64) if (kind == "int" and not N.is_torch(rows)) else rows, dt)
         o = N.to_dev(offs, "int64")
-        N.call("skb_segment_tile", N.ptr(r), n, dim, N.ptr(o), G, int(k), float(pad), N.ptr(out), N.stream_ptr())
-    return N.out_like(out, as_np)
+        if dt == "float32":
+            N.call("skb_segment_tile", N.ptr(r), n, dim, N.ptr(o), G, int(k), float(pad), N.ptr(out), N.stream_ptr())
+        else:
+            # np.full(..., pad, dtype=rows.dtype): the pad cast to the row dtype, as raw 8-byte bits
+            bits = np.array([pad], dtype=np.dtype(oname)).astype(np.dtype(dt)).view(np.uint64)[0]
+            N.call("skb_segment_tile_x64", N.ptr(r), n, dim, N.ptr(o), G, int(k), int(bits), N.ptr(out),
+                   N.stream_ptr())
+    return _finish(out, oname, as_np)

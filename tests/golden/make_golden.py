@@ -18,6 +18,7 @@ import numpy as np
 sys.dont_write_bytecode = True
 REF = "/root/reference/pkg/src/sparsekit"
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
+OUT2 = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden_edges.npz")
 
 
 def load_ref():
@@ -254,5 +255,76 @@ def main():
     print(f"wrote {len(g)} arrays to {OUT}")
 
 
+def table_edge_trace(tb, log):
+    """IDMap edits (remove / put / free_list mutation) interleaved with
+    admission, eviction and export (embedding.py:39-61, 185-308).  The same
+    driver runs the reference, the oracle and the GPU table; `log` records
+    every observable result.  `tb` exposes the reference's table API."""
+    log("o1", tb.lookup_or_insert(np.arange(10, dtype=np.int64), 1))
+    log("rm3", np.array([tb.idmap.remove(3)], np.int64))       # slot stays live, leaves the dict
+    log("len1", np.array([len(tb.idmap)], np.int64))
+    log("ex1", *tb.export_rows())
+    log("o2", tb.lookup_or_insert(np.arange(5, 15, dtype=np.int64), 4))
+    log("ev1", np.array([tb.evict(4)], np.int64))             # ids 0..4 minus 3 are stale
+    log("fl1", np.array(tb.idmap.free_list, np.int64))
+    fl = tb.idmap.free_list
+    fl.reverse()                                              # in-place mutation of the reference's list
+    fl.append(3)                                              # the removed id's slot, reused next
+    log("fl2", np.array(tb.idmap.free_list, np.int64))
+    log("o3", tb.lookup_or_insert(np.array([100, 101, 102], np.int64), 5))
+    tb.idmap.put(200, 7)                                      # an entry sharing slot 7 with id 7
+    log("len2", np.array([len(tb.idmap)], np.int64))
+    log("ex2", *tb.export_rows())
+    log("ev2", np.array([tb.evict(9)], np.int64))
+    log("fl3", np.array(tb.idmap.free_list, np.int64))
+    log("ex3", *tb.export_rows())
+
+
+def negative_threshold_trace(tb, log):
+    """evict_threshold < 0: `step - last > thr` holds for every row."""
+    log("o1", tb.lookup_or_insert(np.arange(6, dtype=np.int64), 3))
+    log("ev", np.array([tb.evict(3)], np.int64))
+    log("fl", np.array(tb.idmap.free_list, np.int64))
+    log("o2", tb.lookup_or_insert(np.array([50, 51], np.int64), 4))
+
+
+def edges():
+    """golden_edges.npz: drop-in edge cases added in round 2."""
+    load_ref()
+    from sparsekit_ref import segments as SG, embedding as EM
+    rng = np.random.Generator(np.random.PCG64(77))
+    g = {}
+
+    def logger(prefix):
+        def log(name, *arrs):
+            for i, a in enumerate(arrs):
+                g[f"{prefix}.{name}.{i}"] = np.asarray(a)
+        return log
+
+    table_edge_trace(EM.EmbeddingTable("e", 4, seed=2, block_size=4, evict_threshold=2), logger("idmap"))
+    negative_threshold_trace(EM.EmbeddingTable("n", 4, seed=2, block_size=4, evict_threshold=-1), logger("negthr"))
+    # float64 / integer rows keep their dtype (segments.py:51-58, 103-116)
+    lens = np.array([0, 1, 2, 7, 8, 9, 17, 130, 300, 0, 3])
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    n = int(offs[-1])
+    r64 = rng.standard_normal((n, 3)) * rng.choice([1.0, 1e8, 1e-8], size=(n, 3))
+    ri = rng.integers(-(2**40), 2**40, (n, 3))
+    g["seg64.offs"], g["seg64.rows"], g["segi.rows"] = offs, r64, ri
+    for mode in ("sum", "mean"):
+        for strat in ("sequential", "scatter", "auto"):
+            g[f"seg64.{mode}.{strat}"] = SG.segment_reduce(r64, offs, mode, strat)
+    for strat in ("sequential", "scatter"):
+        g[f"segi.sum.{strat}"] = SG.segment_reduce(ri, offs, "sum", strat)
+        g[f"segi32.sum.{strat}"] = SG.segment_reduce(ri.astype(np.int32), offs, "sum", strat)
+    g["seg64.tile4"] = SG.segment_tile(r64, offs, 4, pad=-2.5)
+    g["segi.tile4"] = SG.segment_tile(ri, offs, 4, pad=-7)
+    np.savez_compressed(OUT2, **g)
+    print(f"wrote {len(g)} arrays to {OUT2}")
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "edges":
+        edges()
+    else:
+        main()
+        edges()

@@ -475,13 +475,18 @@ def test_ragged(skb, golden):
     eq(rows.truncate(1, "tail").values, np.array([2, 3, 10, 11], np.float32))
 
 
-def _fused_vs_oracle(skb, D, member_specs, steps, mode, seed=0, evict_every=0, thr=None, cfg=None, k=None, pad=0.0):
+def _fused_vs_oracle(skb, D, member_specs, steps, mode, seed=0, evict_every=0, thr=None, cfg=None, k=None, pad=0.0,
+                     variants=None, check=None, id_hi=500):
     """Drive the fused step and the oracle pipeline side by side (mode "tile":
-    oracle = segment_tile + per-position tile gradients, zero past k)."""
+    oracle = segment_tile + per-position tile gradients, zero past k).
+    variants=(adam, pool) forces the fused kernels; check(step, lt) runs
+    after every backward (e.g. to assert which kernel ran)."""
     import torch
     rng = np.random.default_rng(seed)
     members = [m for m, _, _ in member_specs]
     lt = skb.LogicalTable(f"dim{D}", D, 1, seed=seed, members=members, namespaced=True, evict_threshold=thr)
+    if variants is not None:
+        skb.set_variants(lt, *variants)
     olt = O.OracleLogical(f"dim{D}", D, 1, seed=seed, members=members, namespaced=True, evict_threshold=thr)
     cfg = cfg or skb.AdamConfig(lr=1e-2, weight_decay=0.01, variant="adamw")
     for step in range(1, steps + 1):
@@ -490,13 +495,15 @@ def _fused_vs_oracle(skb, D, member_specs, steps, mode, seed=0, evict_every=0, t
             lens = gen(rng, B)
             offs.append(np.concatenate([[0], np.cumsum(lens)]).astype(np.int64))
             ids.append(rng.zipf(1.2, int(lens.sum())).astype(np.int64) if m.startswith("z")
-                       else rng.integers(0, 500, int(lens.sum())))
+                       else rng.integers(0, id_hi, int(lens.sum())))
         batch = skb.PackedBatch(lt, members, ids, offs)
         pooled = skb.lookup_pool(lt, batch, step, mode, k=k, pad=pad)
         G = batch.num_bags
         W = D * k if mode == "tile" else D
         dp = rng.standard_normal((G, W)).astype(np.float32)
         skb.pool_grad_adam(lt, torch.from_numpy(dp).cuda(), cfg, step)
+        if check is not None:
+            check(step, lt)
         # oracle: train.py-style pipeline on the concatenated keys
         keys = np.concatenate([olt.keys_for(m, x) for m, x in zip(members, ids)])
         rows = O.lookup(olt, keys, step)
@@ -529,6 +536,51 @@ def _fused_vs_oracle(skb, D, member_specs, steps, mode, seed=0, evict_every=0, t
     eq(lt.local_table.idmap.free_list, olt.shards[0].free)
 
 
+def _expect_adam(want):
+    def check(step, lt):
+        got = skb_last(lt)[0]
+        # auto mode starts every table on the register kernel until a backward
+        # has shown no long runs (one sampled readback), then takes the TMA ring
+        if want != 0 or step >= 3:
+            assert got == want, (step, got, want)
+    return check
+
+
+def skb_last(lt):
+    import paper_2509_20883_b200 as m
+    return m.last_variants(lt)
+
+
+@pytest.mark.parametrize("variant", list(range(9)))
+@pytest.mark.parametrize("D", [64, 128])
+def test_fused_adam_variants_onehot_sum(skb, variant, D):
+    """The headline fold+Adam kernels against the oracle on the C2 regime:
+    sum, bag length 1, uniform ids with repeats (multi-position runs), 5
+    steps.  variant 0 = auto, which must settle on the TMA ring
+    k_fused_adam_tma<16,192,4>; 1-3 register shapes; 4-8 TMA ring shapes."""
+    specs = [("a", 3000, lambda r, B: np.ones(B, np.int64)), ("b", 2000, lambda r, B: np.ones(B, np.int64))]
+    _fused_vs_oracle(skb, D, specs, steps=5, mode="sum", seed=30 + variant, variants=(variant, -1),
+                     check=_expect_adam(variant), id_hi=2500)
+
+
+@pytest.mark.parametrize("variant", [0, 2, 4, 5, 6, 7, 8])
+def test_fused_adam_variants_mean_hot(skb, variant):
+    """Forced fold+Adam variants with mean bags, empty bags and zipf hot ids
+    (runs > 32 positions leave the ring for the long fold)."""
+    specs = [("a", 700, lambda r, B: r.integers(0, 5, B)), ("zb", 400, lambda r, B: r.integers(1, 9, B))]
+    _fused_vs_oracle(skb, 64, specs, steps=4, mode="mean", seed=50 + variant, variants=(variant, -1),
+                     check=_expect_adam(variant if variant else 2))
+
+
+@pytest.mark.parametrize("pool", [1, 2, 3, 4])
+def test_fused_pool_variants(skb, pool):
+    """Forced pool kernels (1-3 register shapes, 4 staged one-hot gather with
+    its register fallback for mixed chunks) against the oracle."""
+    specs = [("a", 900, lambda r, B: np.where(r.random(B) < 0.8, 1, r.integers(0, 4, B)))]
+    _fused_vs_oracle(skb, 64, specs, steps=3, mode="sum", seed=70 + pool, variants=(-1, pool),
+                     check=lambda step, lt: skb_last(lt)[1] == pool or pytest.fail("pool variant"))
+
+
 @pytest.mark.parametrize("D,mode", [(64, "sum"), (64, "mean"), (128, "sum"), (8, "sum")])
 def test_fused_onehot_negative_zero(skb, D, mode):
     """One-hot chunks take the staged row-gather pool: it must still fold from
@@ -550,7 +602,18 @@ def test_fused_onehot_negative_zero(skb, D, mode):
     pooled = skb.lookup_pool(lt, batch, 2, mode)
     eq(pooled, O.pool(rows[ids], bo, mode))
     assert rows[0, 0] == 0 and np.signbit(rows[0, 0]) and not np.signbit(pooled.cpu().numpy()[0, 0])
-    skb.pool_grad_adam(lt, torch.zeros((160, D), device="cuda"), skb.AdamConfig(), 2)
+    dp = np.random.default_rng(D + 1).standard_normal((160, D)).astype(np.float32)
+    dp[::5] = -0.0
+    skb.pool_grad_adam(lt, torch.from_numpy(dp).cuda(), skb.AdamConfig(), 2)
+    # the backward against the oracle (same rows, the same per-position grads)
+    olt = O.OracleLogical(f"nz{D}", D, 1, seed=4, members=["f"], namespaced=False)
+    o = olt.shards[0]
+    o.scatter_update(o.lookup_or_insert(keys, 1), rows)
+    O.lookup(olt, ids, 2)
+    g = dp / np.maximum(np.diff(bo), 1).astype(np.float32)[:, None] if mode == "mean" else dp
+    O.grad_update(olt, ids, np.repeat(g, np.diff(bo), axis=0).astype(np.float32), 2)
+    for a, b in zip(t.export_rows(), o.export_rows()):
+        eq(a, b)
 
 
 def test_fused_c1_shape(skb):
