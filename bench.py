@@ -185,13 +185,13 @@ def load_traffic():
 # CPU reference (oracle port; only the cpu_baseline / --impl reference legs)
 # ---------------------------------------------------------------------------
 
-def cpu_reference_steps(steps: int, warmup: int, batch: int):
+def cpu_reference_steps(steps: int, warmup: int, batch: int, rank: int = 0):
     """train.py call sequence on the oracle port: keys_for -> lookup ->
     segment_reduce(sum) -> per-row grads -> grad_update (SparseAdamW)."""
     from oracle import sparse_oracle as O
     mem = members()
     olt = O.OracleLogical("dim64", DIM, 1, seed=0, members=mem, namespaced=True)
-    batches = [make_batch(0, k, batch) for k in range(max(2, min(steps, 4)))]
+    batches = [make_batch(rank, k, batch) for k in range(max(2, min(steps, 4)))]
     dps = [np.random.Generator(np.random.PCG64(7 + k)).normal(0, 1e-2, (F_FEATURES * batch, DIM)).astype(np.float32)
            for k in range(len(batches))]
     offs = np.arange(batch + 1, dtype=np.int64)
@@ -225,23 +225,96 @@ def cpu_reference_steps(steps: int, warmup: int, batch: int):
             "ids_per_step": n, "effective_cores": round(cores, 2)}
 
 
+def host_info():
+    """What the CPU numbers ran on."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        affinity = len(os.sched_getaffinity(0))
+    except AttributeError:
+        affinity = os.cpu_count() or 1
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "affinity_cores": affinity, "numpy": np.__version__}
+
+
+def _cpu_worker(a):
+    wid, steps, warmup, batch, barrier, out = a
+    import time as _t
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[wid % len(os.sched_getaffinity(0))]})
+    except (AttributeError, OSError):
+        pass
+    barrier.wait()
+    t0 = _t.perf_counter()
+    r = cpu_reference_steps(steps, warmup, batch, rank=wid)
+    out.put((wid, r, t0, _t.perf_counter()))
+
+
+def cpu_reference_parallel(steps: int, warmup: int, batch: int, procs: int):
+    """`procs` independent replicas of the oracle's train.py step, one
+    process per host core (the reference is numpy + the GIL: its only
+    parallelism is a per-shard thread pool, sharding.py:222-227, so one
+    process per core is the most it can use).  Each replica owns its own
+    table and its own sample batches (rank-seeded); aggregate = total ids of
+    the timed steps / the slowest replica's timed time."""
+    import multiprocessing as mp
+    if procs <= 1:
+        r = cpu_reference_steps(steps, warmup, batch)
+        return r, 1
+    ctx = mp.get_context("fork")
+    barrier, out = ctx.Barrier(procs), ctx.Queue()
+    ps = [ctx.Process(target=_cpu_worker, args=((w, steps, warmup, batch, barrier, out),)) for w in range(procs)]
+    for p in ps:
+        p.start()
+    res = [out.get() for _ in ps]
+    for p in ps:
+        p.join()
+    per = [r for _, r, _, _ in res]
+    slowest = max(r["ms_per_step"] for r in per)
+    agg = sum(r["ids_per_step"] for r in per) / (slowest / 1e3)
+    return {"ids_per_s": agg, "samples_per_s": agg / F_FEATURES, "ms_per_step": slowest, "steps": steps,
+            "ids_per_step": sum(r["ids_per_step"] for r in per),
+            "effective_cores": round(sum(r["effective_cores"] for r in per), 2),
+            "per_process_ids_per_s": [round(r["ids_per_s"]) for r in per]}, procs
+
+
+def cpu_procs() -> int:
+    env = os.environ.get("BENCH_CPU_PROCS")
+    if env:
+        return max(1, int(env))
+    return max(1, min(host_info()["affinity_cores"], 64))
+
+
+def cpu_baseline_line(steps, warmup):
+    procs = cpu_procs()
+    r, procs = cpu_reference_parallel(steps, warmup, CPU_SAMPLE_BATCH, procs)
+    sample = (f"C2 at batch {CPU_SAMPLE_BATCH}/feature ({F_FEATURES * CPU_SAMPLE_BATCH} ids per replica-step), "
+              f"warm tables; {procs} independent oracle-port replicas, one process per core, each {steps} timed "
+              f"steps after {warmup} warm-up; value = all replicas' ids / the slowest replica's median step")
+    return r, {"value": r["ids_per_s"], "unit": "IDs/s", "cores": procs, "kind": "port", "sample": sample,
+               "effective_cores": r["effective_cores"], **host_info()}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     steps = max(1, min(args.steps, 5))
     warm = min(args.warmup, 5)  # each step ~0.35 s: the whole arm stays within seconds
-    r = cpu_reference_steps(steps, warm, CPU_SAMPLE_BATCH)
-    sample = (f"C2 scaled to batch {CPU_SAMPLE_BATCH}/feature ({r['ids_per_step']} ids/step), warm table, "
-              f"{steps} timed steps after {warm} warm-up, median")
+    r, cpu = cpu_baseline_line(steps, warm)
     line = {"metric": METRIC, "value": r["ids_per_s"], "unit": "IDs/s", "n_gpus": args.gpus, "steps": steps,
             "warmup": warm, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "C2 Criteo-shape: 26 x dim64, uniform ids, sum, SparseAdamW (warm)",
-                       "global_batch": CPU_SAMPLE_BATCH, "features": F_FEATURES, "dim": DIM},
-            "impl": "reference", "samples_per_s": r["samples_per_s"],
-            "cpu_baseline": {"value": r["ids_per_s"], "unit": "IDs/s", "cores": 1, "kind": "port",
-                             "sample": sample, "effective_cores": r["effective_cores"]},
+                       "global_batch": CPU_SAMPLE_BATCH * cpu["cores"], "per_process_batch": CPU_SAMPLE_BATCH,
+                       "features": F_FEATURES, "dim": DIM},
+            "impl": "reference", "samples_per_s": r["samples_per_s"], "cpu_baseline": cpu,
             "e2e": {"value": r["ids_per_s"], "unit": "IDs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -448,16 +521,16 @@ def run_ours(args):
     # phase wall times overlap across the two streams, so not max(phase_ms)
     dom = max((k for k in phase_ms if k in pb), key=lambda k: pb[k])
     achieved = pb[dom] / (phase_ms[dom] / 1e3) / 1e9
-    traffic = load_traffic().get(dom, {}).get("dram_bytes_per_launch")
+    tr = load_traffic().get(dom, {})
+    traffic = tr.get("dram_bytes_per_launch")
+    traffic_src = (f"ncu --set full capture of {tr.get('kernel')} (profiles/ncu_summary.json, tag {tr.get('tag')}); "
+                   "not measured in this run") if tr else None
     sb = step_bytes(n_ids, G, u_touched, u_new, DIM)
 
     if rank == 0:
         cpu = None
-        if not args.no_cpu_baseline:
-            r = cpu_reference_steps(3, 0, CPU_SAMPLE_BATCH)
-            cpu = {"value": r["ids_per_s"], "unit": "IDs/s", "cores": 1, "kind": "port",
-                   "sample": f"C2 scaled to batch {CPU_SAMPLE_BATCH}/feature ({r['ids_per_step']} ids/step), "
-                             f"warm table, 3 timed steps, median; effective cores {r['effective_cores']}"}
+        if not args.no_cpu_baseline and world == 1:
+            cpu = cpu_baseline_line(3, 0)[1]
         line = {
             "metric": METRIC, "value": value, "unit": "IDs/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -472,8 +545,8 @@ def run_ours(args):
             "samples_per_s": world * B / (ms_step / 1e3),
             "unique_rows_per_step": u_touched, "new_rows_per_step": u_new,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "algorithmic_bytes": pb[dom]},
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_kind": peak_kind, "algorithmic_bytes": pb[dom]},
             "step_roofline": {"algorithmic_bytes": sb, "achieved": sb / (ms_step / 1e3) / 1e9,
                               "frac": sb / (ms_step / 1e3) / 1e9 / peak},
             "kernels_ms": phase_ms,
@@ -533,10 +606,9 @@ def run_dist(args):
         b = skb.PackedBatch(lt, mem, make_batch(rank, k, B), offs)
         batches.append(b)
         dps.append(torch.empty((b.num_bags, DIM), device="cuda").normal_(0.0, 1e-2, generator=gen))
-    # rows / grads over peer memory (CUDA IPC windows, NVLink P2P stores from
-    # the producing kernel); BENCH_TRANSPORT=nccl: all_to_all_v instead
-    transport = os.environ.get("BENCH_TRANSPORT", "p2p")
-    stepper = DistSparseStep(lt, transport=transport)
+    # ids, rows and grads over peer memory (CUDA IPC windows, NVLink P2P
+    # stores from the producing kernels); the owner side is the fused step
+    stepper = DistSparseStep(lt)
     pooled = torch.empty((batches[0].num_bags, DIM), device="cuda")
     step_no = [0]
 
@@ -563,7 +635,7 @@ def run_dist(args):
     # bytes sent to peers per direction (ids + rows back + grads)
     ctx_counts = stepper.last_counts
     U = int(sum(ctx_counts["send"]))
-    U2 = int(ctx_counts["owner_unique"])
+    U2 = stepper.owner_unique()
     sent_remote = sum(c for j, c in enumerate(ctx_counts["send"]) if j != rank)
     recv_remote = sum(c for j, c in enumerate(ctx_counts["recv"]) if j != rank)
     xbytes = sent_remote * (8 + 4 * DIM) + recv_remote * 4 * DIM
@@ -590,8 +662,7 @@ def run_dist(args):
     torch.cuda.synchronize()
     dist.barrier()
     clk.__exit__(None, None, None)
-    if stepper.win is not None:
-        stepper.win.close_all()
+    stepper.win.close_all()
     t = torch.tensor([ev0.elapsed_time(ev1), e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t[0].item()) / args.steps
@@ -608,9 +679,8 @@ def run_dist(args):
             "config": {"workload": "C2 Criteo-shape DLRM sparse step, row-sharded over GPUs: 26 x dim64, "
                                    "uniform ids [0,1e6) per feature, bag length 1, sum, SparseAdamW, warm",
                        "global_batch": B * world, "per_gpu_batch": B, "features": F_FEATURES, "dim": DIM,
-                       "parallelism": f"row-sharded x{world}: ids all_to_all_v; rows and grads "
-                                      + ("stored into peers' IPC windows by the producing kernels"
-                                         if transport == "p2p" else "all_to_all_v"),
+                       "parallelism": f"row-sharded x{world}: ids, rows and grads stored into peers' IPC "
+                                      "windows by the producing kernels (NVLink P2P); owner side = fused step",
                        "l2": "inputs larger than L2"},
             "samples_per_s": world * B / (ms_step / 1e3),
             "roofline": {"bound": "hbm", "kernel": "step (rank-0 local HBM bytes)", "achieved": sb / ms_step / 1e6,
@@ -627,8 +697,43 @@ def run_dist(args):
     dist.destroy_process_group()
 
 
+def launch_cmd(args_argv, n: int, port: int):
+    """The torchrun command `bench.py --gpus N` re-executes itself under when
+    it was started as a plain process (one rank per GPU, 127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(args_argv)
+
+
+def self_launch(args) -> int:
+    """--gpus N > 1 without a torchrun environment: spawn N ranks.  Needs N
+    visible GPUs; BENCH_SHARED_GPU=1 runs the N ranks on one GPU with gloo
+    control (a functional check of the multi-rank path, not a measurement)."""
+    import socket
+    import torch
+    shared = os.environ.get("BENCH_SHARED_GPU") == "1"
+    have = torch.cuda.device_count()
+    if have < args.gpus and not shared:
+        print(json.dumps({"metric": METRIC, "n_gpus": args.gpus, "error":
+                          f"--gpus {args.gpus} needs {args.gpus} visible GPUs, found {have} "
+                          "(BENCH_SHARED_GPU=1 runs the ranks on one GPU for a functional check)"}), flush=True)
+        return 2
+    env = dict(os.environ)
+    if shared:
+        env["BENCH_DIST_BACKEND"] = "gloo"
+    # communicator setup lines (one per rank) go to stderr: the JSON line stays alone on stdout
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    return subprocess.call(launch_cmd(sys.argv[1:], args.gpus, port), env=env)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        sys.exit(self_launch(args))
     if args.workload != "c2":
         from bench_configs import run_config
         run_config(args)

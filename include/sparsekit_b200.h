@@ -42,6 +42,7 @@ extern "C" {
 #define SKB_E_IO 8          /* reference raises ColumnIOError */
 
 typedef struct skb_table* skb_table_t;
+typedef struct skb_dist* skb_dist_t;  /* requester context of the multi-GPU step (dist.cu) */
 
 /* Host-computed float32 Adam scalars, exactly as optim.py:69-75 forms them
  * (bias corrections use Python double pow, then round to float32). */
@@ -60,6 +61,8 @@ int64_t skb_last_error_arg(void);
 int skb_device_sm_count(int device, int* out_host);
 /* number of this library's kernel launches so far (process-wide) */
 int64_t skb_launch_count(void);
+/* stream-ordered copy between any two addresses (device, pinned host, IPC) */
+int skb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
 
 /* ---- L0 hashing: hashing.py:35-40, sharding.py:41-43, sharding.py:170-178 */
 /* out[i] = int64(mix64(u64(ids[i])))                       hashing.py:35-40 */
@@ -225,8 +228,9 @@ int skb_fused_forward(skb_table_t t, const int64_t* ids, int64_t n, const int64_
  * table's internal index stream after `stream`'s pending work: prefetching
  * batch k+1 before the backward of batch k overlaps its index work with the
  * fold+Adam of step k (at most two batches in flight).  The following
- * skb_fused_forward with the same arguments pools it.  Do not prefetch across
- * an eviction / restore boundary (admission would precede it). */
+ * skb_fused_forward with the same arguments pools it.  Table edits that would
+ * move the prefetched batch's slots (evict, restore, IDMap put / remove /
+ * free list, scatter_update) fail with SKB_E_VALUE until it is pooled. */
 int skb_fused_prepare(skb_table_t t, const int64_t* ids, int64_t n, const int64_t* member_pos_host,
                       const uint64_t* salts_host, int32_t num_members, int32_t namespaced,
                       const int64_t* bag_offs, int64_t num_bags, const int64_t* member_bag_host,
@@ -248,6 +252,18 @@ int skb_fused_forward_tile(skb_table_t t, const int64_t* ids, int64_t n, const i
 /* Backward of the oldest pooled, not yet backwarded fused batch. */
 int skb_fused_backward(skb_table_t t, const float* dpooled, const skb_adam_t* scalars_host,
                        void* stream);
+/* flags bit 0 (SKB_BWD_PRESCALED): dpooled already holds the per-position
+ * gradient of each bag (e.g. train.py:181-186's float32(dpooled64 / len)),
+ * folded as given even for mean bags — bit-exact with the reference's float64
+ * per-row expansion. */
+#define SKB_BWD_PRESCALED 1
+int skb_fused_backward_ex(skb_table_t t, const float* dpooled, const skb_adam_t* scalars_host,
+                          int32_t flags, void* stream);
+/* load_stats (sharding.py:103-119) of the last prepared fused batch for a
+ * plan of num_shards shards: per-shard counts of its unique keys (device
+ * int64[num_shards], zeroed here; stream-ordered, no sync) — what train.py
+ * computes every step (train.py:223-228), from the step's own sorted keys. */
+int skb_fused_shard_counts(skb_table_t t, int64_t num_shards, int64_t* counts_out, void* stream);
 /* Per-kernel CUDA-event timing of the fused step on its own stream:
  * skb_fused_profile arms max_steps records per phase (0 disables); phases
  * 0 probe, 1 miss path, 2 pool, 3 sort + run heads, 4 grad fold + Adam.
@@ -394,6 +410,58 @@ int skb_p2p_send_rows(skb_table_t t, const int64_t* slots_u, const int64_t* inv,
  * in seg_prefix) -> window_s at row dst_base[s] + i - seg_prefix[s]. */
 int skb_p2p_send_grads(const float* rows, int64_t dim, int64_t n, const int64_t* seg_prefix, int32_t num_ranks,
                        float* const* peer_windows, const int64_t* dst_base, void* stream);
+/* Stream-ordered barrier over peer memory (no kernel, no host round trip, no
+ * NCCL): epoch written into slot `rank` of every peer's int64[num_ranks] flag
+ * window (cuStreamWriteValue64, behind a memory barrier), then the stream
+ * waits until every slot of this rank's window reached `epoch`
+ * (cuStreamWaitValue64).  flag_ptrs_host[j] = rank j's flag window as mapped
+ * here.  memops_supported reports whether the driver exposes the ops. */
+int skb_p2p_memops_supported(int32_t* supported_host);
+int skb_p2p_barrier(const int64_t* flag_ptrs_host, int32_t num_ranks, int32_t rank, int64_t epoch,
+                    void* stream);
+/* counts[num_ranks] -> row `rank` of every peer's num_ranks x num_ranks count
+ * matrix window (the all-gather of the multi-GPU step's per-owner counts). */
+int skb_p2p_put_counts(const int64_t* counts, int32_t num_ranks, int32_t rank, int64_t* const* peer_windows,
+                       void* stream);
+
+/* ---- fused row-sharded multi-GPU step (replaces the exchange of
+ * sharding.py:222-297 as driven by train.py:120-195).  One process per GPU.
+ * Requester context: persistent buffers, no per-step allocation; every
+ * transfer is a P2P store by the producing kernel into the consumer's IPC
+ * window.  Per step (S ranks, this rank r):
+ *   skb_dist_prepare      keys + unique_partition (reference order) + sort; counts[S] on device
+ *   (caller)              all-gather counts -> C[q][j] on the host (the step's one sync)
+ *   skb_dist_send_ids     uniq segment j -> owner j's id window at sum_{q<r} C[q][j]
+ *   skb_fused_forward_send (owner) fused index phase of the received ids + row
+ *                         gather stored into each requester q's row window
+ *   skb_dist_pool         pooled[G, D] from this rank's row window
+ *   skb_dist_fold_send    per-unique ordered fold of dpooled -> owner grad windows
+ *   skb_fused_backward    (owner) rank-ordered fold of the grad window + Adam
+ * Window layouts: id / grad window of owner j = every rank's segment for j,
+ * rank-ordered; row window of requester q = q's unique list (owner order). */
+int skb_dist_create(int64_t dim, int32_t num_ranks, skb_dist_t* out_host);
+int skb_dist_destroy(skb_dist_t d);
+int skb_dist_prepare(skb_dist_t d, const int64_t* ids, int64_t n, const int64_t* member_pos_host,
+                     const uint64_t* salts_host, int32_t num_members, int32_t namespaced,
+                     const int64_t* bag_offs, int64_t num_bags, const int64_t* member_bag_host,
+                     const int32_t* strategy_host, int64_t* counts_out, void* stream);
+int skb_dist_send_ids(skb_dist_t d, int64_t num_unique, const int64_t* seg_prefix,
+                      int64_t* const* peer_windows, const int64_t* dst_base, void* stream);
+int skb_dist_pool(skb_dist_t d, const float* rows, int32_t mode, float* out, void* stream);
+int skb_dist_fold_send(skb_dist_t d, const float* dpooled, int32_t mode, int64_t num_unique,
+                       const int64_t* seg_prefix, float* const* peer_windows, const int64_t* dst_base,
+                       void* stream);
+/* device pointers of the prepared batch (tests / diagnostics) */
+int skb_dist_buffers(skb_dist_t d, const int64_t** uniq_out, const int64_t** counts_out,
+                     const uint32_t** gidx_out);
+/* owner side: the received ids (n, rank-ordered segments recv_prefix[0..S])
+ * as a batch of one-id bags through the fused index phase (admission in the
+ * rank-ordered first-occurrence order), then row q -> requester j's window
+ * at dst_base[j] + q - recv_prefix[j].  skb_fused_backward with the grad
+ * window as dpooled completes the step. */
+int skb_fused_forward_send(skb_table_t t, const int64_t* recv_ids, int64_t n, int64_t step,
+                           const int64_t* recv_prefix, int32_t num_ranks, float* const* peer_windows,
+                           const int64_t* dst_base, void* stream);
 
 #ifdef __cplusplus
 }

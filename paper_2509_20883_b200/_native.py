@@ -36,6 +36,7 @@ _SIGS = {
     "skb_last_error_arg": ([], _i64),
     "skb_device_sm_count": ([ctypes.c_int, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "skb_launch_count": ([], _i64),
+    "skb_memcpy_async": ([_p, _p, _i64, _p], ctypes.c_int),
     "skb_mix64": ([_p, _i64, _p, _p], ctypes.c_int),
     "skb_shard_of": ([_p, _i64, _i64, _p, _p], ctypes.c_int),
     "skb_keys_for": ([_p, _i64, _u64, _p, _p], ctypes.c_int),
@@ -87,16 +88,29 @@ _SIGS = {
     "skb_fused_forward_tile": ([_p, _p, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_u64), _i32, _i32, _p, _i64,
                                 ctypes.POINTER(_i64), _i64, ctypes.c_float, _i64, _p, _p], ctypes.c_int),
     "skb_fused_backward": ([_p, _p, ctypes.POINTER(AdamScalars), _p], ctypes.c_int),
+    "skb_fused_backward_ex": ([_p, _p, ctypes.POINTER(AdamScalars), _i32, _p], ctypes.c_int),
+    "skb_fused_shard_counts": ([_p, _i64, _p, _p], ctypes.c_int),
     "skb_ipc_alloc": ([_i64, ctypes.POINTER(_p), _p], ctypes.c_int),
     "skb_ipc_open": ([_p, ctypes.POINTER(_p)], ctypes.c_int),
     "skb_ipc_close": ([_p], ctypes.c_int),
     "skb_ipc_free": ([_p], ctypes.c_int),
     "skb_p2p_send_rows": ([_p, _p, _p, _i64, _p, _i32, _p, _p, _p], ctypes.c_int),
     "skb_p2p_send_grads": ([_p, _i64, _i64, _p, _i32, _p, _p, _p], ctypes.c_int),
+    "skb_p2p_memops_supported": ([ctypes.POINTER(_i32)], ctypes.c_int),
+    "skb_p2p_barrier": ([_p, _i32, _i32, _i64, _p], ctypes.c_int),
+    "skb_p2p_put_counts": ([_p, _i32, _i32, _p, _p], ctypes.c_int),
     "skb_fused_last_unique": ([_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p], ctypes.c_int),
     "skb_fused_stats_async": ([_p, _p, _p], ctypes.c_int),
     "skb_fused_profile": ([_p, _i64, _p], ctypes.c_int),
     "skb_fused_profile_read": ([_p, _i32, ctypes.POINTER(ctypes.c_float), _i64, ctypes.POINTER(_i64)], ctypes.c_int),
+    "skb_dist_create": ([_i64, _i32, ctypes.POINTER(_p)], ctypes.c_int),
+    "skb_dist_destroy": ([_p], ctypes.c_int),
+    "skb_dist_prepare": ([_p, _p, _i64, _p, _p, _i32, _i32, _p, _i64, _p, _p, _p, _p], ctypes.c_int),
+    "skb_dist_send_ids": ([_p, _i64, _p, _p, _p, _p], ctypes.c_int),
+    "skb_dist_pool": ([_p, _p, _i32, _p, _p], ctypes.c_int),
+    "skb_dist_fold_send": ([_p, _p, _i32, _i64, _p, _p, _p, _p], ctypes.c_int),
+    "skb_dist_buffers": ([_p, ctypes.POINTER(_p), ctypes.POINTER(_p), ctypes.POINTER(_p)], ctypes.c_int),
+    "skb_fused_forward_send": ([_p, _p, _i64, _i64, _p, _i32, _p, _p, _p], ctypes.c_int),
     "skb_keys_members": ([_p, _i64, _p, _i32, _p, _p], ctypes.c_int),
     "skb_pool_indexed": ([_p, _i64, _p, _p, _i64, _p, _i32, _i32, _i32, _i64, _p, _p], ctypes.c_int),
     "skb_fold_bags": ([_p, _i64, _p, _i64, _i64, _p, _i64, _i32, _i64, _p, _p], ctypes.c_int),

@@ -30,20 +30,15 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "fused.cuh"
 #include "graph.cuh"
+#include "p2p.cuh"
 #include "longfold.cuh"
 #include "tma.cuh"
 #include "pool.cuh"
 #include "table.cuh"
 
 namespace skb {
-
-struct MemberDev {
-  int64_t pos;   // first position of member f (pos[F] = N)
-  int64_t bag;   // first bag of member f (bag[F] = G)
-  uint64_t salt;
-  int64_t strategy;
-};
 
 constexpr int kSmemMembers = 512;  // member tables up to this size are staged in smem
 constexpr int kTileBags = 256;
@@ -114,6 +109,8 @@ struct FusedCtx {
   // and the variants the last backward / pool actually ran (tests pin them)
   int adam_var = -1, pool_var = -1;
   int last_adam = -1, last_pool = -1;
+  int64_t* iota = nullptr;  // 0, 1, 2, ...: bag offsets of one-id bags (owner side of the multi-GPU step)
+  int64_t iota_cap = 0;
   bool graphs = false;  // replay each phase's device work as a CUDA graph
   cudaStream_t cap = nullptr;  // capture stream of graph mode
   // optional per-kernel CUDA-event profiling: kProf phases x (begin, end) x cap steps
@@ -166,6 +163,7 @@ void fused_ctx_destroy(FusedCtx* c) {
   if (c->side) cudaStreamDestroy(c->side);
   if (c->cap) cudaStreamDestroy(c->cap);
   cudaFree(c->zrow);
+  cudaFree(c->iota);
   cudaFree(c->pack.images);
   if (c->lf_host) cudaFreeHost(c->lf_host);
   if (c->lf_ev) cudaEventDestroy(c->lf_ev);
@@ -722,6 +720,10 @@ __global__ void __launch_bounds__(256) k_fused_pool_staged(const float* __restri
   }
 }
 
+__global__ void k_iota_offs(int64_t* p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = i;
+}
+
 // bag of every position (sort payload for the backward), thread per bag
 __global__ void k_bag_of(const int64_t* __restrict__ bag_offs, int64_t G, uint32_t* __restrict__ bag_of) {
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
@@ -1213,6 +1215,24 @@ static void launch_adam_tma(int64_t n, int D, cudaStream_t s, Args... args) {
   }
   if (ctas < 1) ctas = 1;
   kern<<<(unsigned)ctas, THREADS, sm, s>>>(args...);
+}
+
+// load_stats of a prepared batch: one count per run head of the sorted slots
+// (= per unique key), histogrammed by owner shard in shared memory
+__global__ void __launch_bounds__(256) k_head_shard_counts(const uint32_t* __restrict__ skey, int64_t n,
+                                                           const int64_t* __restrict__ slot_key, int S,
+                                                           unsigned long long* counts) {
+  __shared__ unsigned int hist[4096];
+  for (int k = threadIdx.x; k < S; k += blockDim.x) hist[k] = 0u;
+  __syncthreads();
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = __ldg(skey + j);
+    if (j == 0 || __ldg(skey + j - 1) != k)
+      atomicAdd(&hist[S == 1 ? 0 : (int)(mix64((uint64_t)__ldg(slot_key + k)) % (uint64_t)S)], 1u);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < S; k += blockDim.x)
+    if (hist[k]) atomicAdd(&counts[k], (unsigned long long)hist[k]);
 }
 
 // last_step of every position's slot (deferred forward bookkeeping)
@@ -1827,7 +1847,8 @@ static void pack_reserve(FusedCtx* c, int64_t rows, int64_t runs, int D, cudaStr
   c->pack_gen++;
 }
 
-static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc, cudaStream_t s) {
+static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc, cudaStream_t s,
+                           bool prescaled = false) {
   FusedCtx* c = t->fused;
   if (!c || c->bwd_count >= c->pool_count) raise(SKB_E_VALUE, 0, "fused backward without a preceding fused forward");
   BatchCtx& B = c->b[c->bwd_count % 2];
@@ -1848,7 +1869,9 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     const bool v4 = D % 4 == 0 && (uintptr_t)dpooled % 16 == 0;
     // long mean bags: scale each bag's gradient once (the same fp32 division
     // every position of the bag would do) and fold it as a sum
-    int mode = B.mode == 2 ? 0 : B.mode;  // tile: per-position tile rows, folded as a sum
+    // tile: per-position tile rows, folded as a sum; prescaled: the caller's
+    // rows already are the per-position gradients
+    int mode = (B.mode == 2 || prescaled) ? 0 : B.mode;
     Scratch scaled;
     if (mode == 1 && v4 && n >= 8 * B.G) {
       scaled = Scratch(sizeof(float) * B.G * D, s);
@@ -1924,7 +1947,7 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     GraphKey k;
     int64_t* v = k.v;
     v[0] = t->gen; v[1] = B.gen; v[2] = (int64_t)dpooled; v[3] = n; v[4] = (int64_t)B.bag_offs; v[5] = B.G;
-    v[6] = B.mode; v[7] = B.tile_k; v[8] = c->pack_gen; v[9] = deep;  // deep also picks the fold kernel
+    v[6] = B.mode + (prescaled ? 8 : 0); v[7] = B.tile_k; v[8] = c->pack_gen; v[9] = deep;  // deep also picks the fold kernel
     B.g_bwd.run(k, s, c->cap, B.step, &a, work);
   } else {
     work(s);
@@ -2005,6 +2028,30 @@ int skb_fused_forward(skb_table_t h, const int64_t* ids, int64_t n, const int64_
 int skb_fused_backward(skb_table_t h, const float* dpooled, const skb_adam_t* scalars_host, void* stream) {
   SKB_API_BEGIN
   fused_backward(table_from(h), dpooled, *scalars_host, as_stream(stream));
+  SKB_API_END
+}
+
+int skb_fused_backward_ex(skb_table_t h, const float* dpooled, const skb_adam_t* scalars_host, int32_t flags,
+                          void* stream) {
+  SKB_API_BEGIN
+  fused_backward(table_from(h), dpooled, *scalars_host, as_stream(stream), (flags & SKB_BWD_PRESCALED) != 0);
+  SKB_API_END
+}
+
+int skb_fused_shard_counts(skb_table_t h, int64_t num_shards, int64_t* counts_out, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  FusedCtx* c = t->fused;
+  if (num_shards < 1 || num_shards > 4096) raise(SKB_E_VALUE, num_shards, "num_shards must be in [1, 4096]");
+  if (!c || c->prep_count == 0) raise(SKB_E_VALUE, 0, "no fused batch has been prepared on this table");
+  cudaStream_t s = as_stream(stream);
+  BatchCtx& B = c->b[(c->prep_count - 1) % 2];
+  SKB_CUDA(cudaMemsetAsync(counts_out, 0, sizeof(int64_t) * num_shards, s));
+  SKB_CUDA(cudaStreamWaitEvent(s, B.ev_ready, 0));
+  if (B.n > 0)
+    k_head_shard_counts<<<grid_for(B.n, 256), 256, 0, s>>>(B.skey, B.n, t->slot_key, (int)num_shards,
+                                                          reinterpret_cast<unsigned long long*>(counts_out));
+  SKB_LAUNCH_CHECK();
   SKB_API_END
 }
 
@@ -2103,8 +2150,8 @@ int skb_fused_last_unique(skb_table_t h, int64_t* n_unique_host, int64_t* n_new_
 
 namespace skb {
 // ---------------------------------------------------------------------------
-// generic building blocks for the multi-GPU step (distributed.py): keys of
-// every member in one launch, pooling from any row source through a
+// generic building blocks for the multi-GPU step (dist.cu, distributed.py):
+// keys of every member in one launch, pooling from any row source through a
 // per-position row index, and the ordered fold of pooled grads per index.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_keys_members(const int64_t* __restrict__ ids, int64_t n,
@@ -2116,6 +2163,98 @@ __global__ void __launch_bounds__(256) k_keys_members(const int64_t* __restrict_
     out[i] = key_of(__ldg(ids + i), mv, F, 1, i);
 }
 
+void keys_of_members(const int64_t* ids, int64_t n, const MemberDev* mt, int F, int64_t* out, cudaStream_t s) {
+  if (n <= 0) return;
+  k_keys_members<<<grid_for(n, 256), 256, member_smem(F), s>>>(ids, n, mt, F, out);
+  SKB_LAUNCH_CHECK();
+}
+
+void bag_of_positions(const int64_t* bag_offs, int64_t G, uint32_t* bag_of, cudaStream_t s) {
+  k_bag_of<<<grid_for(G > 0 ? G : 1, 256), 256, 0, s>>>(bag_offs, G, bag_of);
+  SKB_LAUNCH_CHECK();
+}
+
+void pool_by_index(const float* rows, int64_t stride, const uint32_t* idx, const int64_t* bag_offs, int64_t G,
+                   const MemberDev* mt, int F, bool any_sequential, int mode, int D, float* out, cudaStream_t s) {
+  if (G <= 0) return;
+  const bool v4 = D % 4 == 0 && stride % 4 == 0 && (uintptr_t)out % 16 == 0 && (uintptr_t)rows % 16 == 0;
+  if (!any_sequential) {
+    const unsigned grid = grid_for(((G + 31) / 32) * 32, 256, 8);
+    if (v4)
+      k_fused_pool_scatter<4, 2, 4><<<grid, 256, 0, s>>>(rows, idx, bag_offs, G, mode, D, stride, out);
+    else
+      k_fused_pool_scatter<1, 1, 4><<<grid, 256, 0, s>>>(rows, idx, bag_offs, G, mode, D, stride, out);
+  } else {
+    const int64_t ntiles = (G + kTileBags - 1) / kTileBags;
+    if (v4)
+      k_fused_pool_general<4><<<grid_for(ntiles * 256, 256, 6), 256, sizeof(PoolSmem), s>>>(
+          rows, idx, bag_offs, G, mt, F, mode, D, stride, out);
+    else
+      k_fused_pool_general<1><<<grid_for(ntiles * 256, 256, 6), 256, sizeof(PoolSmem), s>>>(
+          rows, idx, bag_offs, G, mt, F, mode, D, stride, out);
+  }
+  SKB_LAUNCH_CHECK();
+}
+
+void fold_sorted(int64_t n, const uint32_t* skey, const uint32_t* sval, const int64_t* bag_offs,
+                 const float* dpooled, int mode, int D, float* out, const FoldWork& w, cudaStream_t s) {
+  SKB_CUDA(cudaMemsetAsync(w.cnt, 0, sizeof(int64_t) * 2, s));
+  if (n <= 0) return;
+  const int64_t chunks = (n + 31) / 32;
+  AdamDev none{};
+  const bool v4 = D % 4 == 0 && (uintptr_t)dpooled % 16 == 0 && (uintptr_t)out % 16 == 0;
+  if (v4) {
+    k_fused_adam<4, 1, 4, false><<<(unsigned)((chunks + 7) / 8), 256, 0, s>>>(
+        n, skey, sval, bag_offs, dpooled, mode, D, none, out, nullptr, -1, w.cnt, w.longs, w.cnt + 1, w.lcap);
+    SKB_LAUNCH_CHECK();
+    launch_long_fold<false>(w.longs, w.cnt + 1, w.lcap, sval, dpooled, D, bag_offs, mode, none, out, nullptr, -1, s,
+                            nullptr, w.pack);
+  } else {
+    k_fused_adam<1, 1, 4, false><<<(unsigned)((chunks + 7) / 8), 256, 0, s>>>(
+        n, skey, sval, bag_offs, dpooled, mode, D, none, out, nullptr, -1, w.cnt, nullptr, nullptr, 0);
+    SKB_LAUNCH_CHECK();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Owner side of the row-sharded step (distributed.py): the ids
+// every rank sent this owner (rank-ordered, each rank's list in its own
+// first-occurrence order) go through the fused index phase as a batch of
+// one-id bags — probe, admission in global first-occurrence order, sort —
+// and the "pool" of that batch is a gather of each position's row stored
+// straight into the requesting rank's receive window (NVLink P2P stores).
+// The matching backward is skb_fused_backward with the gradient window as
+// dpooled: every slot folds its ranks' partial sums in rank order, then
+// Adam, on the same TMA / register kernels as the single-GPU step.
+// ---------------------------------------------------------------------------
+static const int64_t* iota_offsets(FusedCtx* c, int64_t n, cudaStream_t s) {
+  if (n + 1 > c->iota_cap) {
+    if (c->iota) SKB_CUDA(cudaFreeAsync(c->iota, s));
+    const int64_t cap = (n + 1) + (n + 1) / 4;
+    SKB_CUDA(cudaMallocAsync(&c->iota, sizeof(int64_t) * cap, s));
+    k_iota_offs<<<grid_for(cap, 256), 256, 0, s>>>(c->iota, cap);
+    SKB_LAUNCH_CHECK();
+    c->iota_cap = cap;
+  }
+  return c->iota;
+}
+
+static void fused_forward_send(Table* t, const int64_t* recv_ids, int64_t n, int64_t step, const int64_t* recv_pre,
+                               int S, float* const* peers, const int64_t* dst_base, cudaStream_t s) {
+  FusedCtx* c = ctx_get(t);
+  if (c->prep_count > c->pool_count) raise(SKB_E_VALUE, 0, "forward_send: a prefetched batch is pending");
+  const int64_t* bag_offs = iota_offsets(c, n, s);
+  const int64_t mpos[2] = {0, n}, mbag[2] = {0, n};
+  const uint64_t salt[1] = {0};
+  const int32_t strat[1] = {1};
+  BatchArgs a{recv_ids, n, mpos, salt, 1, 0, bag_offs, n, mbag, strat, 0, step};
+  fused_prepare(t, a, s);
+  BatchCtx& B = c->b[c->pool_count % 2];
+  SKB_CUDA(cudaStreamWaitEvent(s, B.ev_ready, 0));
+  p2p_send_slot_rows(t->arena, 3 * t->dim, B.slot, n, (int)t->dim, recv_pre, S, peers, dst_base, s);
+  c->pool_count++;
+}
+
 }  // namespace skb
 
 extern "C" {
@@ -2123,11 +2262,8 @@ extern "C" {
 int skb_keys_members(const int64_t* ids, int64_t n, const int64_t* members_dev, int32_t num_members, int64_t* out,
                      void* stream) {
   SKB_API_BEGIN
-  if (n <= 0) return SKB_OK;
-  const skb::MemberDev* mt = reinterpret_cast<const skb::MemberDev*>(members_dev);
-  skb::k_keys_members<<<skb::grid_for(n, 256), 256, skb::member_smem(num_members), skb::as_stream(stream)>>>(
-      ids, n, mt, num_members, out);
-  SKB_LAUNCH_CHECK();
+  skb::keys_of_members(ids, n, reinterpret_cast<const skb::MemberDev*>(members_dev), num_members, out,
+                       skb::as_stream(stream));
   SKB_API_END
 }
 
@@ -2135,29 +2271,8 @@ int skb_pool_indexed(const float* rows, int64_t row_stride, const uint32_t* idx,
                      int64_t num_bags, const int64_t* members_dev, int32_t num_members, int32_t any_sequential,
                      int32_t mode, int64_t dim, float* out, void* stream) {
   SKB_API_BEGIN
-  using namespace skb;
-  cudaStream_t s = as_stream(stream);
-  const int64_t G = num_bags;
-  if (G <= 0) return SKB_OK;
-  const int D = (int)dim;
-  const bool v4 = D % 4 == 0 && row_stride % 4 == 0 && (uintptr_t)out % 16 == 0 && (uintptr_t)rows % 16 == 0;
-  const MemberDev* mt = reinterpret_cast<const MemberDev*>(members_dev);
-  if (!any_sequential) {
-    const unsigned grid = grid_for(((G + 31) / 32) * 32, 256, 8);
-    if (v4)
-      k_fused_pool_scatter<4, 2, 4><<<grid, 256, 0, s>>>(rows, idx, bag_offs, G, mode, D, row_stride, out);
-    else
-      k_fused_pool_scatter<1, 1, 4><<<grid, 256, 0, s>>>(rows, idx, bag_offs, G, mode, D, row_stride, out);
-  } else {
-    const int64_t ntiles = (G + kTileBags - 1) / kTileBags;
-    if (v4)
-      k_fused_pool_general<4><<<grid_for(ntiles * 256, 256, 6), 256, sizeof(PoolSmem), s>>>(
-          rows, idx, bag_offs, G, mt, num_members, mode, D, row_stride, out);
-    else
-      k_fused_pool_general<1><<<grid_for(ntiles * 256, 256, 6), 256, sizeof(PoolSmem), s>>>(
-          rows, idx, bag_offs, G, mt, num_members, mode, D, row_stride, out);
-  }
-  SKB_LAUNCH_CHECK();
+  skb::pool_by_index(rows, row_stride, idx, bag_offs, num_bags, reinterpret_cast<const skb::MemberDev*>(members_dev),
+                     num_members, any_sequential != 0, mode, (int)dim, out, skb::as_stream(stream));
   SKB_API_END
 }
 
@@ -2173,31 +2288,24 @@ int skb_fold_bags(const float* dpooled, int64_t dim, const uint32_t* idx, int64_
   Scratch bag(4 * n, s), skey(4 * n, s), sval(4 * n, s), cnt(16, s);
   const int64_t lcap = n / kLongRun + 1;
   Scratch longs(sizeof(LongRun) * lcap, s);
-  SKB_CUDA(cudaMemsetAsync(cnt.p, 0, 16, s));
-  k_bag_of<<<grid_for(num_bags > 0 ? num_bags : 1, 256), 256, 0, s>>>(bag_offs, num_bags, bag.as<uint32_t>());
-  SKB_LAUNCH_CHECK();
+  bag_of_positions(bag_offs, num_bags, bag.as<uint32_t>(), s);
   sort_pairs_u32(idx, skey.as<uint32_t>(), bag.as<uint32_t>(), sval.as<uint32_t>(), n,
                  bits_for((uint64_t)(max_index > 0 ? max_index : 1)), s);
-  const int64_t chunks = (n + 31) / 32;
-  AdamDev none{};
-  const bool v4 = D % 4 == 0 && (uintptr_t)dpooled % 16 == 0 && (uintptr_t)out % 16 == 0;
-  if (v4)
-    k_fused_adam<4, 1, 4, false><<<(unsigned)((chunks + 7) / 8), 256, 0, s>>>(
-        n, skey.as<uint32_t>(), sval.as<uint32_t>(), bag_offs, dpooled, mode, D, none, out, nullptr, -1,
-        cnt.as<int64_t>(), longs.as<LongRun>(), cnt.as<int64_t>() + 1, lcap);
-  else
-    k_fused_adam<1, 1, 4, false><<<(unsigned)((chunks + 7) / 8), 256, 0, s>>>(
-        n, skey.as<uint32_t>(), sval.as<uint32_t>(), bag_offs, dpooled, mode, D, none, out, nullptr, -1,
-        cnt.as<int64_t>(), nullptr, nullptr, 0);
-  SKB_LAUNCH_CHECK();
-  if (v4) {
-    const int64_t imgs = long_fold_pack_images(n, D);
-    Scratch prow(sizeof(float) * imgs * long_fold_stage_f(D), s), pl(sizeof(uint32_t) * lcap, s),
-        po(sizeof(uint32_t) * lcap, s), pc(sizeof(int64_t) * 2, s);
-    LongFoldPack pk{prow.as<float>(), imgs, pl.as<uint32_t>(), po.as<uint32_t>(), pc.as<int64_t>(), lcap};
-    launch_long_fold<false>(longs.as<LongRun>(), cnt.as<int64_t>() + 1, lcap, sval.as<uint32_t>(), dpooled, D,
-                            bag_offs, mode, none, out, nullptr, -1, s, nullptr, &pk);
-  }
+  const int64_t imgs = long_fold_pack_images(n, D);
+  Scratch prow(D % 4 == 0 ? sizeof(float) * imgs * long_fold_stage_f(D) : 16, s), pl(sizeof(uint32_t) * lcap, s),
+      po(sizeof(uint32_t) * lcap, s), pc(sizeof(int64_t) * 2, s);
+  LongFoldPack pk{prow.as<float>(), imgs, pl.as<uint32_t>(), po.as<uint32_t>(), pc.as<int64_t>(), lcap};
+  FoldWork w{longs.as<LongRun>(), lcap, cnt.as<int64_t>(), &pk};
+  fold_sorted(n, skey.as<uint32_t>(), sval.as<uint32_t>(), bag_offs, dpooled, mode, D, out, w, s);
+  SKB_API_END
+}
+
+int skb_fused_forward_send(skb_table_t h, const int64_t* recv_ids, int64_t n, int64_t step,
+                           const int64_t* recv_prefix, int32_t num_ranks, float* const* peer_windows,
+                           const int64_t* dst_base, void* stream) {
+  SKB_API_BEGIN
+  skb::fused_forward_send(skb::table_from(h), recv_ids, n, step, recv_prefix, num_ranks, peer_windows, dst_base,
+                          skb::as_stream(stream));
   SKB_API_END
 }
 

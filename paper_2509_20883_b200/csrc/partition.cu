@@ -331,7 +331,8 @@ __global__ void __launch_bounds__(kPartThreads) k_part_emit(const int64_t* __res
                                                             const uint32_t* __restrict__ lrank,
                                                             int64_t* __restrict__ uniq,
                                                             int64_t* __restrict__ inv_shard,
-                                                            int64_t* __restrict__ inv_pos) {
+                                                            int64_t* __restrict__ inv_pos,
+                                                            uint32_t* __restrict__ gidx) {
   constexpr int U = 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t b0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b0 < n; b0 += stride * U) {
@@ -359,8 +360,9 @@ __global__ void __launch_bounds__(kPartThreads) k_part_emit(const int64_t* __res
       const int64_t i = b0 + u * stride;
       if (i >= n) continue;
       const int64_t g = __ldg(&off[(int64_t)sh[u] * ntiles + f[u] / kPartTile]) + lr[u];
-      inv_pos[i] = g - __ldg(&off[(int64_t)sh[u] * ntiles]);
+      if (inv_pos) inv_pos[i] = g - __ldg(&off[(int64_t)sh[u] * ntiles]);
       if (inv_shard) inv_shard[i] = sh[u];
+      if (gidx) gidx[i] = (uint32_t)g;  // index into the owner-concatenated unique list
       if (f[u] == i) uniq[g] = key[u];
     }
   }
@@ -502,6 +504,57 @@ void dedup_first_occurrence(const int64_t* ids, int64_t n, DedupResult& r, cudaS
   }
 }
 
+// the split path's work arrays, carved from one buffer (persistent callers
+// keep it; unique_partition takes it from the stream-ordered pool)
+static size_t split_ws_layout(int64_t n, int64_t S, size_t* b_t, size_t* b_h, size_t* b_o) {
+  const int64_t cap = next_pow2(n * 2 > 64 ? n * 2 : 64);
+  const int64_t ntiles = (n + kPartTile - 1) / kPartTile;
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  *b_t = al(sizeof(HEntry) * (cap + 1));
+  *b_h = al(4 * (n > 0 ? n : 1));
+  *b_o = al(sizeof(int) * (ntiles > 0 ? ntiles : 1) * S);
+  return *b_t + 2 * *b_h + *b_o + 256;
+}
+
+size_t unique_partition_ws_bytes(int64_t n, int64_t S) {
+  size_t a, b, c;
+  return split_ws_layout(n, S, &a, &b, &c);
+}
+
+static void split_partition(const int64_t* ids, int64_t n, int64_t S, int64_t* uniq, int64_t* counts,
+                            int64_t* inv_shard, int64_t* inv_pos, uint32_t* gidx, void* ws, cudaStream_t s) {
+  const int64_t cap = next_pow2(n * 2 > 64 ? n * 2 : 64);
+  const int64_t ntiles = (n + kPartTile - 1) / kPartTile;
+  size_t b_t, b_h, b_o;
+  split_ws_layout(n, S, &b_t, &b_h, &b_o);
+  char* w = static_cast<char*>(ws);
+  HEntry* t = reinterpret_cast<HEntry*>(w);
+  uint32_t* hs = reinterpret_cast<uint32_t*>(w + b_t);
+  uint32_t* lr = reinterpret_cast<uint32_t*>(w + b_t + b_h);
+  int* off = reinterpret_cast<int*>(w + b_t + 2 * b_h);
+  unsigned long long* done = reinterpret_cast<unsigned long long*>(w + b_t + 2 * b_h + b_o);
+  k_part_init<<<grid_for(cap + 1, 256), 256, 0, s>>>(t, cap + 1, done, 1);
+  SKB_LAUNCH_CHECK();
+  k_part_insert<kPartU><<<grid_for((n + kPartU - 1) / kPartU, kPartThreads), kPartThreads, 0, s>>>(
+      ids, n, t, (uint64_t)(cap - 1), cap, hs);
+  SKB_LAUNCH_CHECK();
+  k_part_count<<<(unsigned)ntiles, kPartThreads, 0, s>>>(ids, n, t, hs, (int)S, ntiles, off, lr, done, counts);
+  SKB_LAUNCH_CHECK();
+  k_part_emit<<<grid_for((n + 3) / 4, kPartThreads), kPartThreads, 0, s>>>(
+      ids, n, t, hs, (int)S, ntiles, off, lr, uniq, inv_shard, inv_pos, gidx);
+  SKB_LAUNCH_CHECK();
+}
+
+void unique_partition_ws(const int64_t* ids, int64_t n, int64_t S, int64_t* uniq, int64_t* counts, uint32_t* gidx,
+                         void* ws, cudaStream_t s) {
+  if (n == 0) {
+    SKB_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * S, s));
+    return;
+  }
+  if (S > kSplitMaxS || n >= (1ll << 30)) raise(SKB_E_UNSUPPORTED, S, "persistent partition: S <= 256, n < 2^30");
+  split_partition(ids, n, S, uniq, counts, nullptr, nullptr, gidx, ws, s);
+}
+
 void unique_partition(const int64_t* ids, int64_t n, int64_t S, int64_t* uniq, int64_t* counts, int64_t* inv_shard,
                       int64_t* inv_pos, cudaStream_t s) {
   if (n == 0) {
@@ -509,27 +562,9 @@ void unique_partition(const int64_t* ids, int64_t n, int64_t S, int64_t* uniq, i
     return;
   }
   if (S <= kSplitMaxS && n < (1ll << 30)) {  // stable multi-split, no sort
-    const int64_t cap = next_pow2(n * 2 > 64 ? n * 2 : 64);
-    const int64_t ntiles = (n + kPartTile - 1) / kPartTile;
     // one stream-ordered allocation carved into the five work arrays
-    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    const size_t b_t = al(sizeof(HEntry) * (cap + 1)), b_h = al(4 * n), b_o = al(sizeof(int) * ntiles * S);
-    Scratch work(b_t + 2 * b_h + b_o + 256, s);
-    HEntry* t = work.as<HEntry>();
-    uint32_t* hs = reinterpret_cast<uint32_t*>(work.as<char>() + b_t);
-    uint32_t* lr = reinterpret_cast<uint32_t*>(work.as<char>() + b_t + b_h);
-    int* off = reinterpret_cast<int*>(work.as<char>() + b_t + 2 * b_h);
-    unsigned long long* done = reinterpret_cast<unsigned long long*>(work.as<char>() + b_t + 2 * b_h + b_o);
-    k_part_init<<<grid_for(cap + 1, 256), 256, 0, s>>>(t, cap + 1, done, 1);
-    SKB_LAUNCH_CHECK();
-    k_part_insert<kPartU><<<grid_for((n + kPartU - 1) / kPartU, kPartThreads), kPartThreads, 0, s>>>(
-        ids, n, t, (uint64_t)(cap - 1), cap, hs);
-    SKB_LAUNCH_CHECK();
-    k_part_count<<<(unsigned)ntiles, kPartThreads, 0, s>>>(ids, n, t, hs, (int)S, ntiles, off, lr, done, counts);
-    SKB_LAUNCH_CHECK();
-    k_part_emit<<<grid_for((n + 3) / 4, kPartThreads), kPartThreads, 0, s>>>(
-        ids, n, t, hs, (int)S, ntiles, off, lr, uniq, inv_shard, inv_pos);
-    SKB_LAUNCH_CHECK();
+    Scratch work(unique_partition_ws_bytes(n, S), s);
+    split_partition(ids, n, S, uniq, counts, inv_shard, inv_pos, nullptr, work.p, s);
     return;
   }
   DedupResult r;

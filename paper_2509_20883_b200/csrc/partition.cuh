@@ -22,6 +22,13 @@ bool has_duplicate(const int64_t* ids, int64_t n, cudaStream_t s);
 void unique_partition(const int64_t* ids, int64_t n, int64_t S, int64_t* uniq, int64_t* counts,
                       int64_t* inv_shard, int64_t* inv_pos, cudaStream_t s);
 
+// the split path with a caller-owned persistent workspace (no allocation),
+// emitting each position's index into the owner-concatenated unique list
+// (gidx) instead of (inv_shard, inv_pos); S <= 256, n < 2^30
+size_t unique_partition_ws_bytes(int64_t n, int64_t S);
+void unique_partition_ws(const int64_t* ids, int64_t n, int64_t S, int64_t* uniq, int64_t* counts, uint32_t* gidx,
+                         void* ws, cudaStream_t s);
+
 void grad_fold(const float* grads, int64_t n, int D, const int64_t* inverse, int64_t U, float* out,
                cudaStream_t s);
 

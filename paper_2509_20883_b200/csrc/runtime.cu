@@ -140,6 +140,12 @@ int64_t skb_last_error_arg(void) { return t_err_arg; }
 
 int64_t skb_launch_count(void) { return g_launches.load(); }
 
+int skb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  SKB_API_BEGIN
+  if (bytes > 0) SKB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, skb::as_stream(stream)));
+  SKB_API_END
+}
+
 int skb_device_sm_count(int device, int* out_host) {
   SKB_API_BEGIN
   int v = 0;

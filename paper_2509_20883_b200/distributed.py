@@ -30,6 +30,8 @@ gloo group and CUDA tensors the collectives are staged through host memory.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _native as N
@@ -214,25 +216,28 @@ def dist_grad_update(lt, ids_d, grads, cfg, step: int):
 
 class P2PWindows:
     """Receive windows in CUDA IPC memory that every peer maps: the producing
-    kernel stores rows straight into the consuming rank's window (NVLink P2P
+    kernel stores straight into the consuming rank's window (NVLink P2P
     stores between GPUs; ranks sharing one GPU in the tests).  Grown
     collectively: every rank takes the same decision from the all-gathered
-    count matrix, then handles are re-exchanged."""
+    count matrix (`ensure` gets every rank's need), then the IPC handles are
+    re-exchanged — the only host round trip besides the count matrix, and
+    only when a window grows."""
 
-    def __init__(self, comm: "Comm", dim: int):
-        self.comm, self.dim = comm, dim
+    def __init__(self, comm: "Comm"):
+        self.comm = comm
         self.cap, self.local, self.opened, self.peers_dev = {}, {}, {}, {}
+        self.grows = 0
 
-    def ensure(self, name: str, rows_per_rank) -> None:
-        need = max(rows_per_rank) if rows_per_rank else 0
+    def ensure(self, name: str, units_per_rank, unit_bytes: int) -> None:
+        need = max(units_per_rank) if units_per_rank else 0
         if need <= self.cap.get(name, 0) and name in self.local:
             return
         import ctypes as C
         import torch
-        cap = max(need, int(self.cap.get(name, 0) * 1.5), 1024)
+        cap = max(need + need // 4, int(self.cap.get(name, 0) * 1.5), 1024)
         self.close(name)
         ptr, handle = C.c_void_p(), (C.c_char * 64)()
-        N.call("skb_ipc_alloc", cap * self.dim * 4, C.byref(ptr), handle)
+        N.call("skb_ipc_alloc", cap * unit_bytes, C.byref(ptr), handle)
         handles = [None] * self.comm.size
         self.comm.dist.all_gather_object(handles, bytes(handle), group=self.comm.group)
         peers = []
@@ -246,10 +251,14 @@ class P2PWindows:
                 self.opened.setdefault(name, []).append(q.value)
         self.local[name], self.cap[name] = ptr.value, cap
         self.peers_dev[name] = torch.tensor(peers, dtype=torch.int64, device="cuda")
+        self.grows += 1
 
     def ptr(self, name: str):
         import ctypes as C
         return C.c_void_p(self.local[name])
+
+    def peers(self, name: str):
+        return N.ptr(self.peers_dev[name])
 
     def close(self, name: str) -> None:
         if name not in self.local:
@@ -274,127 +283,193 @@ def _prefix(xs):
     return out
 
 
-class DistSparseStep:
-    """Fused multi-GPU sparse step for one row-sharded logical table.
+class ExchangePlan:
+    """Every offset of one step's exchange, from the all-gathered count
+    matrix C[q][j] = unique ids rank q requests from owner j (sharding.py's
+    per-shard unique lists, rank q's batch).  Pure host arithmetic; every
+    rank derives the same windows from the same matrix.
 
-    forward : member keys (one launch) -> local dedup/partition -> counts +
-              ids all-to-all -> owner dedup (rank order) + admission + gather
-              -> rows all-to-all back -> pooling straight from the received
-              unique rows through the per-position index (no N x D restore).
-    backward: per-local-unique ordered fold of dpooled[bag] (/len) -> grads
-              all-to-all -> owner cross-rank fold in rank order -> AdamW.
+    requester `me`:  uniq list = owner segments send_pre[j]..send_pre[j+1];
+                     segment j goes to owner j's id / grad window at
+                     to_owner_base[j] (the ranks before me, rank order).
+    owner `me`:      received list = requester segments recv_pre[q]..; the
+                     row of received position i goes to requester q's row
+                     window at to_req_base[q] + i - recv_pre[q] (q's uniq
+                     index of that id: q's owners before me come first).
     """
 
-    def __init__(self, lt, comm: Comm | None = None, transport: str = "nccl"):
+    def __init__(self, cmat, me: int):
+        S = len(cmat)
+        self.S, self.me, self.cmat = S, me, [list(map(int, r)) for r in cmat]
+        c = self.cmat
+        self.send = c[me]
+        self.U = sum(self.send)
+        self.send_pre = _prefix(self.send)
+        self.recv = [c[q][me] for q in range(S)]
+        self.n_recv = sum(self.recv)
+        self.recv_pre = _prefix(self.recv)
+        self.to_owner_base = [sum(c[q][j] for q in range(me)) for j in range(S)]
+        self.to_req_base = [sum(c[q][:me]) for q in range(S)]
+        self.rows_need = [sum(c[q]) for q in range(S)]                       # requester q's row window
+        self.recv_need = [sum(c[q][j] for q in range(S)) for j in range(S)]  # owner j's id / grad window
+
+    def meta(self):
+        """int64 [4, S+1]: send_pre, to_owner_base, recv_pre, to_req_base."""
+        m = np.zeros((4, self.S + 1), np.int64)
+        m[0] = self.send_pre
+        m[1, :self.S] = self.to_owner_base
+        m[2] = self.recv_pre
+        m[3, :self.S] = self.to_req_base
+        return m
+
+
+class DistSparseStep:
+    """Fused multi-GPU sparse step for one row-sharded logical table
+    (reference sharding.py:222-297 driven by train.py:120-195).
+
+    forward : requester prepare (keys, dedup + owner split, sort; csrc/dist.cu)
+              -> count matrix (all-gather; the step's ONE host sync) -> ids
+              stored into the owners' id windows -> owner: the single-GPU
+              fused index phase on the received ids (admission in the
+              rank-ordered first-occurrence order = the oracle's slots) and a
+              row gather stored straight into each requester's row window ->
+              requester pools from its window.
+    backward: requester folds dpooled per local unique id (np.add.at order)
+              and stores the sums into the owners' grad windows -> owner:
+              the single-GPU fused fold+Adam (TMA ring / register kernels,
+              long-run fold) over the window, ranks' partial sums folded in
+              rank order.
+
+    Ordering between ranks is stream-ordered: a one-element NCCL all-reduce
+    after each round of peer stores (gloo: device sync + host barrier).
+    Results: slots and first-step rows exact vs the oracle fed the
+    rank-ordered concatenation; updates within tolerance (cross-rank partial
+    sums re-associate the fold).
+    """
+
+    def __init__(self, lt, comm: Comm | None = None):
         if not lt.dist:
             raise ValueError("DistSparseStep needs a LogicalTable built with dist=True")
-        if transport not in ("nccl", "p2p"):
-            raise ValueError(f"unknown transport {transport!r}")
+        import ctypes as C
+        import torch
         self.lt = lt
         self.comm = comm or Comm(lt.group)
-        self.ops = GpuOps()
-        self.transport = transport
-        self.win = P2PWindows(self.comm, lt.dim) if transport == "p2p" else None
-        self._ctx = None
+        self.S, self.me, self.D = self.comm.size, self.comm.rank, lt.dim
+        h = C.c_void_p()
+        N.call("skb_dist_create", self.D, self.S, C.byref(h))
+        self.h = h
+        self.win = P2PWindows(self.comm)
+        self.counts = torch.zeros(self.S, dtype=torch.int64, device="cuda")
+        # stream-ordered peer-memory barriers when the driver has stream memory
+        # operations (every B200 driver): then the step needs no collective at
+        # all — counts all-gathered by P2P stores, one readback of the matrix
+        ok = C.c_int32()
+        N.call("skb_p2p_memops_supported", C.byref(ok))
+        self.p2p_sync = bool(ok.value) and os.environ.get("SKB_DIST_BARRIER", "p2p") == "p2p"
+        self.epoch = 0
+        if self.p2p_sync:
+            S = self.S
+            self.win.ensure("flags", [S] * S, 8)
+            self.win.ensure("cmat", [S * S] * S, 8)
+            self._flag_ptrs = (C.c_int64 * S)(*self.win.peers_dev["flags"].cpu().tolist())
+        self.cmat_host = torch.zeros(self.S * self.S, dtype=torch.int64).pin_memory()
+        self.cmat_dev = torch.zeros(self.S * self.S, dtype=torch.int64, device="cuda")
+        self.syncs = 0  # host synchronisations of the step path (the count matrix readback)
+        self.plan = None
+        self._meta = None
+        self._mode = None
         self.last_counts = None
 
-    @staticmethod
-    def members_dev(batch):
-        """int64[F+1][4] {first position, first bag, salt, strategy} (C-ABI members_dev)."""
-        t = N.torch()
-        F = len(batch.members)
-        if getattr(batch, "_members_dev", None) is None:
-            m = np.zeros((F + 1, 4), np.int64)
-            m[:, 0] = batch.member_pos
-            m[:, 1] = batch.member_bag
-            m[:F, 2] = batch.salts.view(np.int64)
-            m[:F, 3] = batch.strategy
-            batch._members_dev = t.from_numpy(m).cuda()
-        return batch._members_dev
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                N.lib().skb_dist_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def _barrier(self):
+        """Order every rank's prior peer stores before any rank's later reads."""
+        if self.p2p_sync:
+            self.epoch += 1
+            N.call("skb_p2p_barrier", self._flag_ptrs, self.S, self.me, self.epoch, N.stream_ptr())
+        else:
+            self.comm.barrier_after_device_writes()
+
+    def _count_matrix(self):
+        """C[q][j] for all ranks: every rank stores its counts into row `rank`
+        of each peer's count window, barrier, one readback (the step's host
+        synchronisation).  Without stream memory operations: an all-gather."""
+        self.syncs += 1
+        if self.p2p_sync:
+            import torch
+            sp = N.stream_ptr()
+            N.call("skb_p2p_put_counts", N.ptr(self.counts), self.S, self.me, self.win.peers("cmat"), sp)
+            self._barrier()
+            N.call("skb_memcpy_async", self.cmat_host.data_ptr(), self.win.ptr("cmat"), 8 * self.S * self.S, sp)
+            torch.cuda.current_stream().synchronize()
+            flat = self.cmat_host.tolist()
+        elif self.comm.backend == "nccl":
+            self.comm.dist.all_gather_into_tensor(self.cmat_dev, self.counts, group=self.comm.group)
+            flat = self.cmat_dev.cpu().tolist()
+        else:
+            import torch
+            out = [torch.empty(self.S, dtype=torch.int64) for _ in range(self.S)]
+            self.comm.dist.all_gather(out, self.counts.cpu(), group=self.comm.group)
+            flat = [int(x) for t in out for x in t.tolist()]
+        return [flat[q * self.S:(q + 1) * self.S] for q in range(self.S)]
 
     def forward(self, batch, step: int, mode: str = "mean", out=None):
-        t = N.torch()
-        lt, comm, ops = self.lt, self.comm, self.ops
-        D, S, n, G = lt.dim, comm.size, batch.num_ids, batch.num_bags
+        import ctypes as C
+        from .fused import _MODES
+        if mode not in ("sum", "mean"):
+            raise ValueError(f"unknown mode {mode!r} (the multi-GPU step pools with sum or mean)")
+        lt, S, D = self.lt, self.S, self.D
         F = len(batch.members)
-        mdev = self.members_dev(batch)
-        if batch.namespaced:
-            keys = N.empty((n,), "int64")
-            if n:
-                N.call("skb_keys_members", N.ptr(batch.ids), n, N.ptr(mdev), F, N.ptr(keys), N.stream_ptr())
-        else:
-            keys = batch.ids
-        uniq, counts, inv_s, inv_p = ops.partition(keys, S)
-        gidx = ops.global_index(counts, inv_s, inv_p).to(t.int32)
-        cmat = None
-        if self.win is None:
-            recv_counts = comm.counts(counts)
-        else:
-            cmat = comm.count_matrix(counts)
-            recv_counts = [cmat[r][comm.rank] for r in range(S)]
-        recv_ids = comm.a2av(uniq, counts, recv_counts)
-        u2, inv2 = ops.dedup(recv_ids)
-        offs = ops.admit(lt.local_table, u2, step)
-        if self.win is None:
-            rows2 = ops.gather(lt.local_table, offs)
-            send_rows = ops.take_rows(rows2, inv2)
-            recv_rows = comm.a2av(send_rows, recv_counts, counts)
-            rows_ptr = N.ptr(recv_rows)
-        else:
-            # owner gathers each requested row straight into the requester's window
-            me = comm.rank
-            self.win.ensure("rows", [sum(cmat[j]) for j in range(S)])
-            nrecv = int(sum(recv_counts))
-            pre = N.to_dev(np.array(_prefix(recv_counts), np.int64), "int64")
-            base = N.to_dev(np.array([sum(cmat[j][:me]) for j in range(S)], np.int64), "int64")
-            if nrecv:
-                N.call("skb_p2p_send_rows", lt.local_table.handle, N.ptr(offs), N.ptr(inv2), nrecv, N.ptr(pre), S,
-                       N.ptr(self.win.peers_dev["rows"]), N.ptr(base), N.stream_ptr())
-            comm.barrier_after_device_writes()
-            rows_ptr = self.win.ptr("rows")
+        if batch._c_args is None:
+            batch._c_args = ((C.c_int64 * (F + 1))(*batch.member_pos.tolist()),
+                             (C.c_uint64 * max(F, 1))(*[int(x) for x in batch.salts]),
+                             (C.c_int64 * (F + 1))(*batch.member_bag.tolist()),
+                             (C.c_int32 * max(F, 1))(*batch.strategy.tolist()))
+        mp, sl, mb, st = batch._c_args
+        sp = N.stream_ptr()
+        N.call("skb_dist_prepare", self.h, N.ptr(batch.ids), batch.num_ids, mp, sl, F, 1 if batch.namespaced else 0,
+               N.ptr(batch.bag_offs), batch.num_bags, mb, st, N.ptr(self.counts), sp)
+        plan = ExchangePlan(self._count_matrix(), self.me)
+        self.win.ensure("ids", plan.recv_need, 8)
+        self.win.ensure("grads", plan.recv_need, 4 * D)
+        self.win.ensure("rows", plan.rows_need, 4 * D)
+        meta = N.to_dev(plan.meta(), "int64")
+        N.call("skb_dist_send_ids", self.h, plan.U, N.ptr(meta[0]), self.win.peers("ids"), N.ptr(meta[1]), sp)
+        self._barrier()
+        N.call("skb_fused_forward_send", lt.local_table.handle, self.win.ptr("ids"), plan.n_recv, int(step),
+               N.ptr(meta[2]), S, self.win.peers("rows"), N.ptr(meta[3]), sp)
+        self._barrier()
+        G = batch.num_bags
         pooled = out if out is not None else N.empty((G, D), "float32")
-        mcode = {"sum": 0, "mean": 1}[mode]
-        any_seq = int(bool((batch.strategy == 0).any()))
-        if G:
-            N.call("skb_pool_indexed", rows_ptr, D, N.ptr(gidx), N.ptr(batch.bag_offs), G, N.ptr(mdev), F,
-                   any_seq, mcode, D, N.ptr(pooled), N.stream_ptr())
-        self._ctx = dict(batch=batch, counts=counts, recv_counts=recv_counts, gidx=gidx, U=int(sum(counts)),
-                         inv2=inv2, u2=u2, offs=offs, mode=mcode, cmat=cmat)
-        self.last_counts = {"send": list(counts), "recv": list(recv_counts), "owner_unique": int(u2.numel())}
+        N.call("skb_dist_pool", self.h, self.win.ptr("rows"), _MODES[mode], N.ptr(pooled), sp)
+        self.plan, self._meta, self._mode = plan, meta, _MODES[mode]
+        self.last_counts = {"send": list(plan.send), "recv": list(plan.recv), "n_recv": plan.n_recv}
         return pooled
 
     def backward(self, dpooled, cfg, step: int):
-        c = self._ctx
-        if c is None:
+        from .optim import adam_scalars
+        import ctypes as C
+        if self.plan is None:
             raise ValueError("backward without a preceding forward")
-        lt, comm, ops = self.lt, self.comm, self.ops
-        D, b = lt.dim, c["batch"]
+        if step < 1:
+            raise ValueError("global step t must be >= 1")
+        plan, meta = self.plan, self._meta
         g = N.to_dev(dpooled, "float32")
-        agg = N.empty((max(c["U"], 1), D), "float32")
-        n = b.num_ids
-        if n:
-            N.call("skb_fold_bags", N.ptr(g), D, N.ptr(c["gidx"]), n, c["U"], N.ptr(b.bag_offs), b.num_bags,
-                   c["mode"], max(c["U"] - 1, 0), N.ptr(agg), N.stream_ptr())
-        if self.win is None:
-            recv_g = comm.a2av(agg[: c["U"]], c["counts"], c["recv_counts"])
-            g2 = ops.fold(recv_g, c["inv2"], c["u2"].numel())
-        else:
-            # requester stores its folded gradients straight into each owner's
-            # window, at the owner's rank-ordered receive offset
-            cmat, S, me = c["cmat"], comm.size, comm.rank
-            self.win.ensure("grads", [sum(cmat[r][s] for r in range(S)) for s in range(S)])
-            seg = N.to_dev(np.array(_prefix(c["counts"]), np.int64), "int64")
-            base = N.to_dev(np.array([sum(cmat[r][s] for r in range(me)) for s in range(S)], np.int64), "int64")
-            if c["U"]:
-                N.call("skb_p2p_send_grads", N.ptr(agg), D, c["U"], N.ptr(seg), S, N.ptr(self.win.peers_dev["grads"]),
-                       N.ptr(base), N.stream_ptr())
-            comm.barrier_after_device_writes()
-            nrecv = int(sum(c["recv_counts"]))
-            U2 = c["u2"].numel()
-            g2 = N.empty((max(U2, 1), D), "float32")
-            if nrecv or U2:
-                N.call("skb_grad_fold", self.win.ptr("grads"), nrecv, D, N.ptr(c["inv2"]), U2, N.ptr(g2),
-                       N.stream_ptr())
-            g2 = g2[:U2]
-        ops.adam(lt.local_table, c["offs"], g2, cfg, step)
-        self._ctx = None
+        sp = N.stream_ptr()
+        N.call("skb_dist_fold_send", self.h, N.ptr(g), self._mode, plan.U, N.ptr(meta[0]), self.win.peers("grads"),
+               N.ptr(meta[1]), sp)
+        self._barrier()
+        sc = adam_scalars(cfg, step)
+        N.call("skb_fused_backward", self.lt.local_table.handle, self.win.ptr("grads"), C.byref(sc), sp)
+        self.plan = None
+
+    def owner_unique(self) -> int:
+        """Rows this rank's shard touched in the last step (synchronizes)."""
+        from .fused import last_step_stats
+        return last_step_stats(self.lt)[0]

@@ -134,15 +134,37 @@ def lookup_pool(lt: LogicalTable, batch: PackedBatch, step: int, mode: str = "me
     return out
 
 
-def pool_grad_adam(lt: LogicalTable, dpooled, cfg: AdamConfig, step: int) -> None:
+def pool_grad_adam(lt: LogicalTable, dpooled, cfg: AdamConfig, step: int, prescaled: bool = False) -> None:
     """Backward of the last lookup_pool on `lt`: grad fold + Adam/AdamW on touched rows.
-    `dpooled` has the forward output's shape ([G, D], or [G, k*D] for tile)."""
+    `dpooled` has the forward output's shape ([G, D], or [G, k*D] for tile).
+
+    prescaled=True: `dpooled` already is each bag's per-position gradient —
+    train.py:181-186 builds float32(dpooled64 / len) in float64 — and is
+    folded as given, so the step is bit-exact with the reference's float64
+    expansion (the default divides a float32 dpooled by float32(len))."""
     telemetry.bump("fused.pool_grad_adam")
     if step < 1:
         raise ValueError("global step t must be >= 1")
     g = N.to_dev(dpooled, "float32")
     sc = adam_scalars(cfg, step)
-    N.call("skb_fused_backward", lt.local_table.handle, N.ptr(g), ctypes.byref(sc), N.stream_ptr())
+    N.call("skb_fused_backward_ex", lt.local_table.handle, N.ptr(g), ctypes.byref(sc), 1 if prescaled else 0,
+           N.stream_ptr())
+
+
+def step_load_stats(lt: LogicalTable, plan, out=None, sync: bool = True):
+    """load_stats (sharding.py:103-119) of the keys of the last prepared fused
+    batch for `plan` — train.py:223-228's per-step probe — from the step's
+    own sorted slots (one pass over the run heads on the device).
+    sync=False returns the device counts tensor (no host round trip)."""
+    from .sharding import LoadStats
+    S = plan.num_shards
+    counts = out if out is not None else N.empty((S,), "int64")
+    N.call("skb_fused_shard_counts", lt.local_table.handle, S, N.ptr(counts), N.stream_ptr())
+    if not sync:
+        return counts
+    c = counts.cpu().numpy()
+    total = int(c.sum())
+    return LoadStats(c, float(c.max()) / (total / S) if total else 1.0)
 
 
 def last_step_stats(lt: LogicalTable):

@@ -101,6 +101,9 @@ def segment_reduce(rows, segments, mode: str = "sum", strategy: str = "auto"):
     G = (offs.numel() if N.is_torch(offs) else len(offs)) - 1
     strategy = resolve_strategy(strategy, n, G)
     kind, dt, oname = _row_kind(rows)
+    if kind == "int" and strategy == "sequential":
+        # np.add.reduceat promotes integers narrower than int64 (numpy's reduce dtype rule)
+        oname = "uint64" if oname.startswith("uint") else "int64"
     if kind == "int" and mode == "mean":
         # segments.py:88-90 divides in place into the integer output
         raise TypeError(f"Cannot cast ufunc 'divide' output from dtype('float64') to dtype('{oname}') "

@@ -272,7 +272,7 @@ def table_edge_trace(tb, log):
     fl.append(3)                                              # the removed id's slot, reused next
     log("fl2", np.array(tb.idmap.free_list, np.int64))
     log("o3", tb.lookup_or_insert(np.array([100, 101, 102], np.int64), 5))
-    tb.idmap.put(200, 7)                                      # an entry sharing slot 7 with id 7
+    tb.idmap.put(200, 15)                                     # an entry on a never-allocated slot
     log("len2", np.array([len(tb.idmap)], np.int64))
     log("ex2", *tb.export_rows())
     log("ev2", np.array([tb.evict(9)], np.int64))

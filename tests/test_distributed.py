@@ -18,6 +18,8 @@ import torch.multiprocessing as mp
 
 from oracle import sparse_oracle as O
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
 S = 2
 DIM = 4
 STEPS = 4
@@ -174,8 +176,9 @@ def fused_inputs(rank, k):
     return ids, offs, dp
 
 
-def _fused_worker(rank, port, out_dir, transport="nccl"):
+def _fused_worker(rank, port, out_dir, barrier="p2p"):
     import torch.distributed as dist
+    os.environ["SKB_DIST_BARRIER"] = barrier
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=S)
@@ -183,7 +186,7 @@ def _fused_worker(rank, port, out_dir, transport="nccl"):
     from paper_2509_20883_b200.distributed import DistSparseStep
     torch.cuda.set_device(0)
     lt = skb.LogicalTable("dim4", DIM, S, seed=3, members=MEMBERS, namespaced=True, dist=True)
-    stepper = DistSparseStep(lt, transport=transport)
+    stepper = DistSparseStep(lt)
     cfg = skb.AdamConfig(lr=LR, weight_decay=0.01, variant="adamw")
     pooled = []
     for k in range(STEPS):
@@ -193,17 +196,23 @@ def _fused_worker(rank, port, out_dir, transport="nccl"):
         stepper.backward(torch.from_numpy(dp).cuda(), cfg, k + 1)
     ex = lt.local_table.export_rows()
     np.savez(os.path.join(out_dir, f"fused{rank}.npz"), *pooled, ids=ex[0], w=ex[1], m=ex[2], v=ex[3])
-    if stepper.win is not None:
-        stepper.win.close_all()
+    np.save(os.path.join(out_dir, f"grows{rank}.npy"), np.array([stepper.win.grows, stepper.syncs, stepper.p2p_sync]))
+    stepper.win.close_all()
     dist.barrier()
     dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-def test_dist_sparse_step_gpu(tmp_path, cuda):
-    """Fused multi-GPU step (2 ranks on one GPU, gloo staging) vs the oracle
-    train.py pipeline fed the rank-ordered concatenated batch with S = 2."""
-    mp.spawn(_fused_worker, args=(_free_port(), str(tmp_path)), nprocs=S, join=True)
+@pytest.mark.parametrize("barrier", ["p2p", "comm"])
+def test_dist_sparse_step_gpu(tmp_path, cuda, barrier):
+    """Fused multi-GPU step (2 ranks on one GPU) vs the oracle train.py
+    pipeline fed the rank-ordered concatenated batch with S = 2; ordering by
+    stream-ordered peer-memory barriers (default) or process-group barriers."""
+    mp.spawn(_fused_worker, args=(_free_port(), str(tmp_path), barrier), nprocs=S, join=True)
+    for r in range(S):
+        grows, syncs, p2p = np.load(os.path.join(tmp_path, f"grows{r}.npy")).tolist()
+        assert syncs == STEPS                      # one host sync per step: the count matrix
+        assert bool(p2p) == (barrier == "p2p")
     olt = O.OracleLogical("dim4", DIM, S, seed=3, members=MEMBERS, namespaced=True)
     for k in range(STEPS):
         ins = [fused_inputs(r, k) for r in range(S)]
@@ -235,23 +244,76 @@ def test_dist_sparse_step_gpu(tmp_path, cuda):
             np.testing.assert_allclose(z[key], ex[j], rtol=1e-5, atol=1e-6)
 
 
+@pytest.mark.parametrize("S", [1, 2, 3, 5, 8])
+def test_exchange_plan_places_every_row(S):
+    """CPU: the ExchangePlan offsets move every id, row and gradient to the
+    place the reference's per-shard lists define.  Simulated windows: each
+    rank's unique list split by owner, ids stored into owner windows, rows
+    stored back into requester windows, grads into owner windows."""
+    from paper_2509_20883_b200.distributed import ExchangePlan
+    rng = np.random.default_rng(S)
+    cmat = rng.integers(0, 7, (S, S)).tolist()
+    # rank q's unique list: owner-concatenated, each id tagged (q, owner, k)
+    uniq = {q: [(q, j, k) for j in range(S) for k in range(cmat[q][j])] for q in range(S)}
+    plans = [ExchangePlan(cmat, r) for r in range(S)]
+    id_win = {j: [None] * plans[0].recv_need[j] for j in range(S)}
+    for q in range(S):
+        p = plans[q]
+        for i, x in enumerate(uniq[q]):
+            j = next(j for j in range(S) if p.send_pre[j] <= i < p.send_pre[j + 1])
+            id_win[j][p.to_owner_base[j] + i - p.send_pre[j]] = x
+    for j in range(S):  # owner windows: rank-ordered segments, each in the requester's order
+        assert id_win[j] == [x for q in range(S) for x in uniq[q] if x[1] == j]
+        assert len(id_win[j]) == plans[j].n_recv
+    row_win = {q: [None] * plans[0].rows_need[q] for q in range(S)}
+    for j in range(S):  # owner j sends received position i's "row" (the id itself) back
+        p = plans[j]
+        for i, x in enumerate(id_win[j]):
+            q = next(q for q in range(S) if p.recv_pre[q] <= i < p.recv_pre[q + 1])
+            row_win[q][p.to_req_base[q] + i - p.recv_pre[q]] = x
+    for q in range(S):  # every requester gets its rows in its own unique order
+        assert row_win[q] == uniq[q]
+
+
 @pytest.mark.gpu
-def test_dist_sparse_step_p2p_transport(tmp_path, cuda):
-    """Peer-memory transport (rows gathered straight into the requester's IPC
-    window, folded grads stored straight into the owner's window) is
-    bit-identical to the all_to_all transport (2 ranks sharing one GPU)."""
-    a, b = tmp_path / "a2a", tmp_path / "p2p"
-    a.mkdir()
-    b.mkdir()
-    mp.spawn(_fused_worker, args=(_free_port(), str(a), "nccl"), nprocs=S, join=True)
-    mp.spawn(_fused_worker, args=(_free_port(), str(b), "p2p"), nprocs=S, join=True)
+def test_dist_sparse_step_one_host_sync(tmp_path, cuda):
+    """The fused multi-GPU step (2 ranks on one GPU): window growth happens
+    only when the batch outgrows the windows, and the step's host
+    synchronisation is the count matrix (table counter refreshes stay off
+    the steady-state path)."""
+    mp.spawn(_fused_worker, args=(_free_port(), str(tmp_path)), nprocs=S, join=True)
     for r in range(S):
-        za, zb = np.load(a / f"fused{r}.npz"), np.load(b / f"fused{r}.npz")
-        assert sorted(za.files) == sorted(zb.files)
-        for k in za.files:
-            assert np.array_equal(za[k].view(np.uint8), zb[k].view(np.uint8)), k
+        grows = int(np.load(os.path.join(tmp_path, f"grows{r}.npy"))[0])
+        assert grows <= 8, grows  # flags + counts once; 3 data windows created once, grown once for the 30x step
 
 
 @pytest.mark.gpu
 def test_exchange_protocol_gpu_kernels(tmp_path, cuda):
     _run(tmp_path, use_gpu=True)
+
+
+def test_bench_self_launch_command():
+    """`bench.py --gpus N` started without torchrun re-executes itself under
+    torch.distributed.run with N ranks on 127.0.0.1."""
+    import bench
+    cmd = bench.launch_cmd(["--gpus", "4", "--steps", "3"], 4, 29555)
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd and "--master-port=29555" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "3"] and cmd[-5].endswith("bench.py")
+
+
+def test_bench_gpus_n_fails_loudly_without_gpus():
+    """No silent single-GPU run for --gpus 2: with fewer visible GPUs the
+    launcher prints an error line and exits non-zero."""
+    import json
+    import subprocess
+    import sys
+    import torch
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("enough GPUs: the launcher would really run")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "BENCH_SHARED_GPU")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "1"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 2, (r.returncode, r.stderr[-2000:])
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and "needs 2 visible GPUs" in line["error"]

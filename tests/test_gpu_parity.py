@@ -841,3 +841,53 @@ def test_fused_graph_mode_equals_eager(skb, mode):
         assert np.array_equal(a.view(np.int32), b.view(np.int32))
     for x, y in zip(outs[0][1], outs[1][1]):
         assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
+
+
+def test_fused_prescaled_backward_matches_train_py(skb):
+    """train.py:181-186 builds each position's gradient in float64 as
+    float32(dpooled64 / len); pool_grad_adam(prescaled=True) folds exactly
+    those rows for mean bags -> bit-exact with the reference's expansion."""
+    import torch
+    rng = np.random.default_rng(17)
+    D, members = 16, ["u", "v"]
+    lt = skb.LogicalTable("dim16", D, 1, seed=2, members=members, namespaced=True)
+    olt = O.OracleLogical("dim16", D, 1, seed=2, members=members, namespaced=True)
+    cfg = skb.AdamConfig(lr=1e-2, weight_decay=0.01, variant="adamw")
+    for step in range(1, 4):
+        lens = [rng.integers(0, 7, 300) for _ in members]
+        offs = [np.concatenate([[0], np.cumsum(l)]).astype(np.int64) for l in lens]
+        ids = [rng.integers(0, 400, int(o[-1])) for o in offs]
+        batch = skb.PackedBatch(lt, members, ids, offs)
+        skb.lookup_pool(lt, batch, step, "mean")
+        dp64 = rng.standard_normal((600, D))  # float64, like train.py's dlogits * w
+        L = np.concatenate(lens).astype(np.float64)
+        g = (dp64 / np.maximum(L, 1.0)[:, None]).astype(np.float32)
+        skb.pool_grad_adam(lt, torch.from_numpy(g).cuda(), cfg, step, prescaled=True)
+        keys = np.concatenate([olt.keys_for(m, x) for m, x in zip(members, ids)])
+        O.lookup(olt, keys, step)
+        per_row = np.repeat(dp64 / np.maximum(L, 1.0)[:, None], L.astype(np.int64), axis=0).astype(np.float32)
+        O.grad_update(olt, keys, per_row, step, lr=1e-2, weight_decay=0.01, variant="adamw")
+    for a, b in zip(lt.local_table.export_rows(), olt.shards[0].export_rows()):
+        eq(a, b)
+
+
+@pytest.mark.parametrize("P", [1, 3, 8])
+def test_fused_step_load_stats(skb, P):
+    """load_stats of the step's keys (train.py:223-228) from the fused
+    step's sorted slots == the reference's load_stats on the same keys."""
+    rng = np.random.default_rng(P)
+    members = ["a", "b", "c"]
+    lt = skb.LogicalTable("dim8", 8, 1, seed=1, members=members, namespaced=True)
+    olt = O.OracleLogical("dim8", 8, 1, seed=1, members=members, namespaced=True)
+    for step in (1, 2):
+        ids = [rng.integers(0, 5000, 4000) for _ in members]
+        offs = [np.arange(4001, dtype=np.int64)] * 3
+        batch = skb.PackedBatch(lt, members, ids, offs)
+        skb.lookup_pool(lt, batch, step, "sum")
+        got = skb.step_load_stats(lt, skb.ShardPlan(P))
+        keys = np.concatenate([olt.keys_for(m, x) for m, x in zip(members, ids)])
+        counts, imbalance = O.shard_load(keys, P)
+        eq(got.counts, counts)
+        assert got.imbalance == imbalance
+        import torch
+        skb.pool_grad_adam(lt, torch.zeros((12000, 8), device="cuda"), skb.AdamConfig(), step)
