@@ -154,7 +154,10 @@ def c3(args):
     import paper_2509_20883_b200 as skb
     F, Bn, D = 26, 65536, 16
     mem = [f"C{f}" for f in range(F)]
-    lt = skb.LogicalTable("dim16", D, 1, seed=0, members=mem, namespaced=True)
+    # the IDMap is sized for the target up front (no rehash on the way); the
+    # row arena starts empty and grows copy-free (VMM) as rows are admitted
+    lt = skb.LogicalTable("dim16", D, 1, seed=0, members=mem, namespaced=True,
+                          capacity_hint=int(args.c3_rows * 1.05))
     offs = [np.arange(Bn + 1, dtype=np.int64)] * F
     P = 4
     base = []

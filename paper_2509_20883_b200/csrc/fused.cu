@@ -1606,7 +1606,9 @@ static void fused_prepare(Table* t, const BatchArgs& a, cudaStream_t s) {
   // growth moves the arena and side arrays: quiesce both streams before it and
   // finish the copies before any later main-stream kernel (e.g. the pending
   // fold+Adam of the previous step) can touch the new buffers (rare)
-  const bool grow = table_needs_growth(t, a.n);
+  // (VMM tables grow in place: rows never move and the IDMap rehash is
+  // stream-ordered on this stream, the only one that reads the IDMap)
+  const bool grow = table_needs_growth(t, a.n) && !t->vmm;
   if (grow) {
     SKB_CUDA(cudaStreamSynchronize(s));
     SKB_CUDA(cudaStreamSynchronize(x));

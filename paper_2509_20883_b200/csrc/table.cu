@@ -6,6 +6,7 @@
 // miss flags -> insert: the k-th unknown id (input order) gets
 // free_list[F-1-k] if k < F else allocated + k - F, so offsets are identical
 // to the reference's dict loop while every id is handled by its own thread.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -38,8 +39,34 @@ static void grow_array(T*& p, int64_t old_n, int64_t new_n, cudaStream_t s) {
   p = q;
 }
 
+// VMM growth: map more memory behind the six per-row arrays (rows never
+// move); VA is reserved for the capacity hint, else 8x the rows needed, and
+// re-reserved (remap, no copy) only when outgrown
+static void grow_arena_vmm(Table* t, int64_t new_rows, cudaStream_t s) {
+  const int64_t res_rows = std::max<int64_t>(t->rows_hint + t->rows_hint / 4, 8 * new_rows);
+  const size_t esz[6] = {sizeof(float) * (size_t)t->row_stride(), sizeof(int64_t), sizeof(uint8_t), sizeof(int64_t),
+                         sizeof(int64_t), sizeof(int64_t)};
+  bool moved = false;
+  for (int i = 0; i < 6; ++i) moved |= vmm_grow(t->va[i], esz[i] * (size_t)new_rows, esz[i] * (size_t)res_rows, s);
+  t->arena = reinterpret_cast<float*>(t->va[0].base);
+  t->last_step = reinterpret_cast<int64_t*>(t->va[1].base);
+  t->live = reinterpret_cast<uint8_t*>(t->va[2].base);
+  t->slot_key = reinterpret_cast<int64_t*>(t->va[3].base);
+  t->ins_seq = reinterpret_cast<int64_t*>(t->va[4].base);
+  t->free_list = reinterpret_cast<int64_t*>(t->va[5].base);
+  // mapped sizes are granularity-rounded: every array holds at least this many rows
+  int64_t rows = INT64_MAX;
+  for (int i = 0; i < 6; ++i) rows = std::min<int64_t>(rows, (int64_t)(t->va[i].mapped / esz[i]));
+  t->arena_rows = rows;
+  if (moved) t->gen++;  // only a re-reservation changes pointers (captured graphs re-prime)
+}
+
 static void grow_arena(Table* t, int64_t new_rows, cudaStream_t s) {
   if (new_rows <= t->arena_rows) return;
+  if (t->vmm) {
+    grow_arena_vmm(t, new_rows, s);
+    return;
+  }
   const int64_t old = t->arena_rows;
   grow_array(t->arena, old * t->row_stride(), new_rows * t->row_stride(), s);
   grow_array(t->last_step, old, new_rows, s);
@@ -138,7 +165,9 @@ void table_reserve(Table* t, int64_t n, cudaStream_t s) {
   int64_t need_alloc = t->known[C_ALLOC] + n;
   int64_t need_rows = t->known[C_ROWS] + n;
   if (need_alloc > t->arena_rows) {
-    int64_t nr = t->arena_rows + t->arena_rows / 2;
+    // copy-free (VMM) growth is cheap: 1/8 headroom keeps the mapped arena
+    // within ~1.1x of the rows; the copying fallback grows 1.5x
+    int64_t nr = t->arena_rows + (t->vmm ? t->arena_rows / 8 : t->arena_rows / 2);
     if (nr < need_alloc) nr = need_alloc;
     if (nr < 1024) nr = 1024;
     grow_arena(t, nr, s);
@@ -934,7 +963,11 @@ int skb_table_create(int64_t dim, int64_t seed, int64_t block_size, int64_t evic
   SKB_CUDA(cudaMemsetAsync(t->dflags, 0xFF, sizeof(unsigned long long) * 4, s));
   SKB_CUDA(cudaMallocHost(&t->hflags, sizeof(int64_t) * 4));
   int64_t rows = capacity_hint > 1024 ? capacity_hint : 1024;
-  grow_arena(t, rows, s);
+  t->vmm = vmm_available();
+  t->rows_hint = capacity_hint;
+  // VMM: VA for the hint is reserved now, memory is mapped as rows arrive;
+  // the IDMap is sized for the hint either way (no rehash while growing to it)
+  grow_arena(t, t->vmm ? 1024 : rows, s);
   rehash(t, next_pow2(rows * 2 > 2048 ? rows * 2 : 2048), s);
   SKB_CUDA(cudaStreamSynchronize(s));
   SKB_CUDA(cudaStreamDestroy(s));
@@ -949,12 +982,16 @@ int skb_table_destroy(skb_table_t h) {
     fprintf(stderr, "[skb] snapshot waits %lld, counter refreshes %lld (all tables so far)\n",
             (long long)g_snap_waits.load(), (long long)g_refreshes.load());
   SKB_CUDA(cudaDeviceSynchronize());
-  cudaFree(t->arena);
-  cudaFree(t->last_step);
-  cudaFree(t->live);
-  cudaFree(t->slot_key);
-  cudaFree(t->ins_seq);
-  cudaFree(t->free_list);
+  if (t->vmm) {
+    for (auto& a : t->va) vmm_free(a);
+  } else {
+    cudaFree(t->arena);
+    cudaFree(t->last_step);
+    cudaFree(t->live);
+    cudaFree(t->slot_key);
+    cudaFree(t->ins_seq);
+    cudaFree(t->free_list);
+  }
   cudaFree(t->idmap);
   cudaFree(t->counters);
   cudaFree(t->dflags);

@@ -17,6 +17,7 @@
 // Slot numbers are exactly the reference's offsets.
 #pragma once
 #include "common.cuh"
+#include "vmm.cuh"
 
 namespace skb {
 
@@ -42,6 +43,11 @@ struct Table {
   int64_t* slot_key = nullptr;
   int64_t* ins_seq = nullptr;
   int64_t* free_list = nullptr;
+  // copy-free growth: the six per-row arrays above live in reserved virtual
+  // address ranges and grow by mapping more memory (vmm.cuh); rows never move
+  bool vmm = false;
+  int64_t rows_hint = 0;  // capacity_hint: VA reserved for this many rows up front
+  VmmArray va[6];         // arena, last_step, live, slot_key, ins_seq, free_list
 
   HEntry* idmap = nullptr;
   int64_t idmap_cap = 0;

@@ -192,7 +192,8 @@ def _cross_pairs(pairs, sizes=None):
         stack = getattr(_DEFERRED, "stack", None)
         pending = [(flags[i:i + 1], f"cross_many: sizes[{i}] = {totals[i]} does not match the rows' product count")
                    for i in range(len(prep))]
-        if stack:
+        # host (numpy) results are read back here anyway: check them now
+        if stack and not any(r[0] for r in res):
             stack[-1].extend(pending)
         else:
             _raise_pending(pending)

@@ -231,9 +231,16 @@ def test_gpu_cross_many_sizes_checked(skb):
     ref = skb.cross(a, b)
     (ok,) = skb.cross_many([(a, b)], sizes=[true])
     assert np.array_equal(ok.values, ref.values)
+    import torch
+    ad = skb.RaggedTensor(torch.from_numpy(a.values).cuda(), torch.from_numpy(a.row_offsets).cuda())
+    bd = skb.RaggedTensor(torch.from_numpy(b.values).cuda(), torch.from_numpy(b.row_offsets).cuda())
     for bad in (true - 1, true + 5):
         with pytest.raises(ValueError, match="sizes"):
             skb.cross_many([(a, b)], sizes=[bad])
         with pytest.raises(ValueError, match="sizes"):
             with skb.deferred_checks():
                 skb.cross_many([(a, b)], sizes=[bad])
+        with pytest.raises(ValueError, match="sizes"):  # device results: raised at the context exit
+            with skb.deferred_checks():
+                (r,) = skb.cross_many([(ad, bd)], sizes=[bad])
+                assert r.values.numel() == bad
