@@ -697,6 +697,103 @@ def run_dist(args):
     dist.destroy_process_group()
 
 
+def run_threads(args):
+    """BENCH_SHARED_GPU=1 with --gpus N on one GPU: the N ranks of the
+    row-sharded step as N threads of this process (distributed.ThreadRanks),
+    each with its own stream, table shard, windows and batch — the full
+    multi-GPU protocol (P2P stores, stream-ordered peer barriers, one count
+    readback per step) with every rank's kernels sharing one device.  A
+    functional + protocol-overhead measurement, not an N-GPU number: the
+    line's n_gpus is 1 and `emulated_ranks` says N."""
+    import threading
+    import torch
+    import paper_2509_20883_b200 as skb
+    from paper_2509_20883_b200.distributed import DistSparseStep, ThreadRanks
+
+    W, B, mem = args.gpus, args.batch, members()
+    n_ids = F_FEATURES * B
+    world = ThreadRanks(W)
+    res = [None] * W
+    errs = []
+    start = threading.Barrier(W)
+    torch.cuda.set_device(0)
+
+    def body(rank):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                g = world.group(rank)
+                per_rank = (F_FEATURES * ID_SPACE) // W
+                lt = skb.LogicalTable("dim64", DIM, W, seed=0, members=mem, namespaced=True, dist=True, group=g,
+                                      capacity_hint=0 if args.cold else per_rank + per_rank // 10)
+                if not args.cold:
+                    all_ids = torch.arange(ID_SPACE, dtype=torch.int64, device="cuda")
+                    plan = skb.ShardPlan(W)
+                    for m in mem:
+                        keys = lt.keys_for(m, all_ids)
+                        lt.local_table._admit_unique(keys[plan.shard_of(keys) == rank].contiguous(), 0)
+                P = 4
+                offs = [np.arange(B + 1, dtype=np.int64)] * F_FEATURES
+                gen = torch.Generator(device="cuda")
+                gen.manual_seed(1234 + rank)
+                batches = [skb.PackedBatch(lt, mem, make_batch(rank, k, B), offs) for k in range(P)]
+                dps = [torch.empty((b.num_bags, DIM), device="cuda").normal_(0.0, 1e-2, generator=gen)
+                       for b in batches]
+                stepper = DistSparseStep(lt)
+                cfg = skb.AdamConfig(lr=1e-3, weight_decay=0.01, variant="adamw")
+                pooled = torch.empty((batches[0].num_bags, DIM), device="cuda")
+                step_no = [0]
+
+                def run(count):
+                    for k in range(count):
+                        step_no[0] += 1
+                        stepper.forward(batches[k % P], step_no[0], "sum", out=pooled)
+                        stepper.backward(dps[k % P], cfg, step_no[0])
+
+                run(args.warmup)
+                st.synchronize()
+                start.wait()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                syncs0 = stepper.syncs
+                w0 = time.perf_counter()
+                e0.record(st)
+                run(args.steps)
+                e1.record(st)
+                st.synchronize()
+                wall = time.perf_counter() - w0
+                res[rank] = {"ms": e0.elapsed_time(e1) / args.steps, "wall_ms": wall * 1e3 / args.steps,
+                             "syncs_per_step": (stepper.syncs - syncs0) / args.steps,
+                             "counts": stepper.last_counts, "owner_unique": stepper.owner_unique()}
+                stepper.win.close_all()
+        except BaseException as e:  # surface thread failures
+            errs.append(repr(e))
+            world._barrier.abort()
+            start.abort()
+
+    ths = [threading.Thread(target=body, args=(r,)) for r in range(W)]
+    clk = ClockSampler(0).__enter__()
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    clk.__exit__(None, None, None)
+    if errs:
+        raise RuntimeError("; ".join(errs))
+    ms = max(r["ms"] for r in res)
+    line = {"metric": METRIC, "value": W * n_ids / (ms / 1e3), "unit": "IDs/s", "n_gpus": 1, "emulated_ranks": W,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"C2 row-sharded over {W} ranks emulated on ONE GPU (threads of one process): "
+                                   "26 x dim64, uniform ids, bag length 1, sum, SparseAdamW, warm",
+                       "per_rank_batch": B, "features": F_FEATURES, "dim": DIM,
+                       "parallelism": f"row-sharded x{W} (ThreadRanks): P2P window stores, stream-ordered peer "
+                                      "barriers, owner side = fused step"},
+            "per_rank": res, "wall_ms_per_step": max(r["wall_ms"] for r in res),
+            "clocks": clk.summary(), "gpu_launches": None}
+    print(json.dumps(line), flush=True)
+
+
 def launch_cmd(args_argv, n: int, port: int):
     """The torchrun command `bench.py --gpus N` re-executes itself under when
     it was started as a plain process (one rank per GPU, 127.0.0.1)."""
@@ -711,6 +808,9 @@ def self_launch(args) -> int:
     import socket
     import torch
     shared = os.environ.get("BENCH_SHARED_GPU") == "1"
+    if shared and os.environ.get("BENCH_SHARED_PROCS") != "1":
+        run_threads(args)  # ranks as threads of this process on one GPU
+        return 0
     have = torch.cuda.device_count()
     if have < args.gpus and not shared:
         print(json.dumps({"metric": METRIC, "n_gpus": args.gpus, "error":

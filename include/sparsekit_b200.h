@@ -309,6 +309,22 @@ int skb_bucketize_multi_async(const float* values, const int64_t* col_offs, int6
 /* mod_transform / fused_mod features.py:56-62,180-189 (moduli > 0 checked on host) */
 int skb_mod_multi(const int64_t* values, const int64_t* col_offs, int64_t num_cols,
                   const int64_t* moduli, int64_t* out, int64_t n_total, void* stream);
+/* The same multi-column ops over a device table of per-column input
+ * pointers (col_ptrs[c] holds col_offs[c+1] - col_offs[c] values): no
+ * concatenation copy before the launch; the output stays concatenated.
+ * nan_flag (optional device word, caller sets ~0): deferred NaN check. */
+int skb_bucketize_cols(const float* const* col_ptrs, const int64_t* col_offs, int64_t num_cols,
+                       const float* edges_cat, const int64_t* edge_offs, int64_t* out, int64_t n_total,
+                       unsigned long long* nan_flag, void* stream);
+int skb_mod_cols(const int64_t* const* col_ptrs, const int64_t* col_offs, int64_t num_cols,
+                 const int64_t* moduli, int64_t* out, int64_t n_total, void* stream);
+/* PackedBatch for the fused step: members' ids concatenated into ids_out[N]
+ * and their bag offsets shifted by each member's first position into
+ * bag_offs_out[G+1], in one launch (device tables of per-member pointers and
+ * the member_pos / member_bag prefix arrays). */
+int skb_pack_members(const int64_t* const* ids_ptrs, const int64_t* const* offs_ptrs, const int64_t* member_pos,
+                     const int64_t* member_bag, int64_t num_members, int64_t n_total, int64_t num_bags,
+                     int64_t* ids_out, int64_t* bag_offs_out, void* stream);
 /* cross features.py:65-89: out_offs[rows+1] computed here; out sized by caller
  * from out_offs[rows] (use skb_cross_offsets first). */
 int skb_cross_offsets(const int64_t* a_offs, const int64_t* b_offs, int64_t rows,
@@ -347,6 +363,13 @@ int skb_ragged_pad_dense(const void* values, int64_t elem_bytes, int64_t width, 
  * -1 = the SKB_ADAM_VARIANT / SKB_POOL_VARIANT environment default.
  * last_variants: what the last backward / pool ran (adam 0 = TMA default,
  * -1 = generic-D kernel; pool -1 generic-D, 10 pairwise general). */
+/* Fold mode of the fused backward's long runs (ids with > 32 positions in a
+ * batch): 0 exact (default) — np.add.at's serial left fold, bit-exact with
+ * sharding.py:283-290; 1 tree (opt-in tolerance mode) — chunks of 256
+ * positions folded in parallel, then the chunk sums in order; error per
+ * column <= (256 + len/256) * 2^-24 * sum|g| (SURVEY §7.3-5's normwise
+ * bound).  Runs of <= 32 positions are exact in both modes. */
+int skb_fused_set_fold_mode(skb_table_t t, int32_t mode);
 int skb_fused_set_variants(skb_table_t t, int32_t adam_variant, int32_t pool_variant);
 int skb_fused_last_variants(skb_table_t t, int32_t* adam_host, int32_t* pool_host);
 int skb_fused_set_graphs(skb_table_t t, int32_t enable);

@@ -118,10 +118,14 @@ _SIGS = {
     "skb_bucketize_multi_async": ([_p, _p, _i64, _p, _p, _p, _i64, _p, _p], ctypes.c_int),
     "skb_mod_multi": ([_p, _p, _i64, _p, _p, _i64, _p], ctypes.c_int),
     "skb_cross_offsets": ([_p, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_bucketize_cols": ([_p, _p, _i64, _p, _p, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_mod_cols": ([_p, _p, _i64, _p, _p, _i64, _p], ctypes.c_int),
+    "skb_pack_members": ([_p, _p, _p, _p, _i64, _i64, _i64, _p, _p, _p], ctypes.c_int),
     "skb_cross": ([_p, _p, _p, _p, _i64, _p, _i64, _p, _p, _p], ctypes.c_int),
     "skb_ragged_truncate": ([_p, _i64, _i64, _i32, _p, _p, _p], ctypes.c_int),
     "skb_gather_elems": ([_p, _i64, _p, _i64, _p, _p], ctypes.c_int),
     "skb_ragged_pad_dense": ([_p, _i64, _i64, _p, _i64, _i64, _p, _p, _p, _p], ctypes.c_int),
+    "skb_fused_set_fold_mode": ([_p, _i32], ctypes.c_int),
     "skb_fused_set_variants": ([_p, _i32, _i32], ctypes.c_int),
     "skb_fused_last_variants": ([_p, ctypes.POINTER(_i32), ctypes.POINTER(_i32)], ctypes.c_int),
     "skb_fused_set_graphs": ([_p, ctypes.c_int32], ctypes.c_int),

@@ -111,6 +111,8 @@ struct FusedCtx {
   int last_adam = -1, last_pool = -1;
   int64_t* iota = nullptr;  // 0, 1, 2, ...: bag offsets of one-id bags (owner side of the multi-GPU step)
   int64_t iota_cap = 0;
+  bool tree = false;         // tolerance-mode long-run fold (set_fold_mode "tree")
+  TreeWork tw;
   bool graphs = false;  // replay each phase's device work as a CUDA graph
   cudaStream_t cap = nullptr;  // capture stream of graph mode
   // optional per-kernel CUDA-event profiling: kProf phases x (begin, end) x cap steps
@@ -164,6 +166,8 @@ void fused_ctx_destroy(FusedCtx* c) {
   if (c->cap) cudaStreamDestroy(c->cap);
   cudaFree(c->zrow);
   cudaFree(c->iota);
+  cudaFree(c->tw.chunk_off);
+  cudaFree(c->tw.partial);
   cudaFree(c->pack.images);
   if (c->lf_host) cudaFreeHost(c->lf_host);
   if (c->lf_ev) cudaEventDestroy(c->lf_ev);
@@ -1849,6 +1853,30 @@ static void pack_reserve(FusedCtx* c, int64_t rows, int64_t runs, int D, cudaStr
   c->pack_gen++;
 }
 
+static void tree_reserve(FusedCtx* c, int64_t n, int64_t runs_cap, int D, cudaStream_t s) {
+  const int64_t need = tree_chunk_cap(n, runs_cap);
+  if (need <= c->tw.chunk_cap) return;
+  SKB_CUDA(cudaStreamSynchronize(s));
+  cudaFree(c->tw.chunk_off);
+  cudaFree(c->tw.partial);
+  SKB_CUDA(cudaMalloc(&c->tw.chunk_off, sizeof(int64_t) * (runs_cap + 2)));
+  SKB_CUDA(cudaMalloc(&c->tw.partial, sizeof(float) * need * D));
+  c->tw.chunk_cap = need;
+  c->pack_gen++;
+}
+
+// the long-run pass of a backward: exact (serial np.add.at chain per column)
+// or, in tree mode, the two-level chunked reduction
+static void long_pass(FusedCtx* c, BatchCtx& B, const float* dpooled, int D, int mode, const AdamDev& a, Table* t,
+                      cudaStream_t st, bool deep, int budget = kLfSmemBudget) {
+  if (c->tree)
+    launch_long_fold_tree<true>(B.longs, B.dev + 3, B.longs_cap, B.sval, dpooled, D, B.bag_offs, mode, a, t->arena,
+                                t->last_step, B.step, st, c->zrow, c->tw);
+  else
+    launch_long_fold<true>(B.longs, B.dev + 3, B.longs_cap, B.sval, dpooled, D, B.bag_offs, mode, a, t->arena,
+                           t->last_step, B.step, st, c->zrow, &c->pack, deep, budget);
+}
+
 static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc, cudaStream_t s,
                            bool prescaled = false) {
   FusedCtx* c = t->fused;
@@ -1856,7 +1884,10 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
   BatchCtx& B = c->b[c->bwd_count % 2];
   const int64_t n = B.n;
   const int D = (int)t->dim;
-  if (n > 0 && D % 4 == 0) pack_reserve(c, n, B.longs_cap, D, s);
+  if (n > 0 && D % 4 == 0) {
+    if (c->tree) tree_reserve(c, n, B.longs_cap, D, s);
+    else pack_reserve(c, n, B.longs_cap, D, s);
+  }
   // long runs seen by a recent backward (no sync: the last completed readback)
   if (cudaEventQuery(c->lf_ev) == cudaSuccess) c->lf_last = *c->lf_host;
   else cudaGetLastError();
@@ -1899,9 +1930,7 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
       SKB_CUDA(cudaEventRecord(c->lf_fork, s));
       SKB_CUDA(cudaStreamWaitEvent(c->lf_stream, c->lf_fork, 0));
       static const int budget_env = env_int("SKB_LF_BUDGET", 0);
-      launch_long_fold<true>(B.longs, B.dev + 3, B.longs_cap, B.sval, dpooled, D, B.bag_offs, mode, a, t->arena,
-                             t->last_step, B.step, c->lf_stream, c->zrow, &c->pack, deep,
-                             budget_env > 0 ? budget_env * 1024 : kLfSmemBudget);
+      long_pass(c, B, dpooled, D, mode, a, t, c->lf_stream, deep, budget_env > 0 ? budget_env * 1024 : kLfSmemBudget);
       SKB_CUDA(cudaEventRecord(c->lf_join, c->lf_stream));
     }
     const int64_t lcap = overlap ? 0 : B.longs_cap;
@@ -1940,8 +1969,7 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     if (overlap)
       SKB_CUDA(cudaStreamWaitEvent(s, c->lf_join, 0));
     else if (v4)
-      launch_long_fold<true>(B.longs, B.dev + 3, B.longs_cap, B.sval, dpooled, D, B.bag_offs, mode, a, t->arena,
-                             t->last_step, B.step, s, c->zrow, &c->pack, deep);
+      long_pass(c, B, dpooled, D, mode, a, t, s, deep);
     prof_mark(c, P_ADAM, 1, s);
   }
   };
@@ -1949,7 +1977,8 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     GraphKey k;
     int64_t* v = k.v;
     v[0] = t->gen; v[1] = B.gen; v[2] = (int64_t)dpooled; v[3] = n; v[4] = (int64_t)B.bag_offs; v[5] = B.G;
-    v[6] = B.mode + (prescaled ? 8 : 0); v[7] = B.tile_k; v[8] = c->pack_gen; v[9] = deep;  // deep also picks the fold kernel
+    v[6] = B.mode + (prescaled ? 8 : 0); v[7] = B.tile_k; v[8] = c->pack_gen;
+    v[9] = deep + (c->tree ? 2 : 0);  // deep also picks the fold kernel
     B.g_bwd.run(k, s, c->cap, B.step, &a, work);
   } else {
     work(s);
@@ -2054,6 +2083,15 @@ int skb_fused_shard_counts(skb_table_t h, int64_t num_shards, int64_t* counts_ou
     k_head_shard_counts<<<grid_for(B.n, 256), 256, 0, s>>>(B.skey, B.n, t->slot_key, (int)num_shards,
                                                           reinterpret_cast<unsigned long long*>(counts_out));
   SKB_LAUNCH_CHECK();
+  SKB_API_END
+}
+
+int skb_fused_set_fold_mode(skb_table_t h, int32_t mode) {
+  SKB_API_BEGIN
+  if (mode != 0 && mode != 1) raise(SKB_E_VALUE, mode, "fold mode must be 0 (exact) or 1 (tree)");
+  FusedCtx* c = ctx_get(table_from(h));
+  if (c->prep_count > c->bwd_count) raise(SKB_E_VALUE, 0, "set_fold_mode while a fused step is in flight");
+  c->tree = mode == 1;
   SKB_API_END
 }
 

@@ -599,4 +599,174 @@ inline int64_t long_fold_pack_images(int64_t rows, int D) {
   return ng * (rows / tpi + rows / kMegaRunMin + 1);
 }
 
+// ---------------------------------------------------------------------------
+// Tolerance mode ("tree" fold, opt-in per table): a long run's gradients are
+// summed as chunks of kTreeChunk positions folded in parallel, then the
+// chunk partials folded in chunk order — a two-level reduction instead of
+// np.add.at's serial chain, so a hot id costs memory bandwidth, not one FADD
+// latency per position.  Error: |sum - exact| <= (kTreeChunk + n/kTreeChunk)
+// * 2^-24 * sum|x| per column (the serial fold's bound is n * 2^-24 * sum|x|),
+// the normwise tolerance SURVEY §7.3-5 allows; rows, slots and every run of
+// <= kLongRun positions stay bit-exact.
+// ---------------------------------------------------------------------------
+constexpr int kTreeChunk = 256;
+
+__device__ __forceinline__ float4 vdiv4(float4 x, float l) {
+  return make_float4(__fdiv_rn(x.x, l), __fdiv_rn(x.y, l), __fdiv_rn(x.z, l), __fdiv_rn(x.w, l));
+}
+
+struct TreeWork {
+  int64_t* chunk_off = nullptr;  // [cap + 1] first chunk of each run; [cap + ... ] total at [nruns]
+  float* partial = nullptr;      // [chunk_cap, D]
+  int64_t chunk_cap = 0;
+};
+
+inline int64_t tree_chunk_cap(int64_t n, int64_t runs_cap) { return n / kTreeChunk + runs_cap + 1; }
+
+// exclusive scan of the runs' chunk counts (one block; total at chunk_off[R])
+static __global__ void __launch_bounds__(1024) k_tree_plan(const LongRun* __restrict__ runs,
+                                                           const int64_t* __restrict__ nruns, int64_t cap,
+                                                           int64_t* __restrict__ chunk_off) {
+  __shared__ int64_t warp_sum[32];
+  __shared__ int64_t carry;
+  const int64_t R = *nruns < cap ? *nruns : cap;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t b0 = 0; b0 < R; b0 += blockDim.x) {
+    const int64_t r = b0 + threadIdx.x;
+    int64_t c = 0;
+    if (r < R) c = ((int64_t)runs[r].je - runs[r].jh + kTreeChunk - 1) / kTreeChunk;
+    int64_t inc = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) warp_sum[w] = inc;
+    __syncthreads();
+    int64_t base = carry;
+    for (int q = 0; q < w; ++q) base += warp_sum[q];
+    if (r < R) chunk_off[r] = base + inc - c;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = base + inc;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) chunk_off[R] = carry;
+}
+
+// one warp per (chunk, 128-column slice): fold the chunk's positions with four
+// interleaved accumulators (positions p, p+1, p+2, p+3 mod 4), then combine
+template <bool MEAN>
+static __global__ void __launch_bounds__(256) k_tree_partial(const LongRun* __restrict__ runs,
+                                                             const int64_t* __restrict__ nruns, int64_t cap,
+                                                             const int64_t* __restrict__ chunk_off,
+                                                             const uint32_t* __restrict__ ridx,
+                                                             const float* __restrict__ rows, int D,
+                                                             const int64_t* __restrict__ bag_offs,
+                                                             const float* __restrict__ zrow,
+                                                             float* __restrict__ partial, int64_t chunk_cap) {
+  const int64_t R = *nruns < cap ? *nruns : cap;
+  const int64_t total = chunk_off[R] < chunk_cap ? chunk_off[R] : chunk_cap;
+  const int slices = (D + 127) / 128;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t wu = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; wu < total * slices; wu += nw) {
+    const int64_t ch = wu / slices;
+    const int c = (int)(wu - ch * slices) * 128 + lane * 4;
+    int64_t lo = 0, hi = R;  // run r with chunk_off[r] <= ch < chunk_off[r + 1]
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(chunk_off + mid) <= ch) lo = mid; else hi = mid;
+    }
+    const LongRun run = runs[lo];
+    const int64_t p0 = run.jh + (ch - __ldg(chunk_off + lo)) * kTreeChunk;
+    const int64_t p1 = p0 + kTreeChunk < (int64_t)run.je ? p0 + kTreeChunk : (int64_t)run.je;
+    if (c >= D) continue;
+    float4 acc[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int64_t p = p0;
+    for (; p + 4 <= p1; p += 4) {
+      float4 x[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t g = __ldg(ridx + p + k);
+        x[k] = ldg4((g == 0xFFFFFFFFu ? zrow : rows + (int64_t)g * D) + c);
+        if (MEAN) x[k] = vdiv4(x[k], (float)(__ldg(bag_offs + g + 1) - __ldg(bag_offs + g)));
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k] = add4(acc[k], x[k]);
+    }
+    for (; p < p1; ++p) {
+      const uint32_t g = __ldg(ridx + p);
+      float4 x = ldg4((g == 0xFFFFFFFFu ? zrow : rows + (int64_t)g * D) + c);
+      if (MEAN) x = vdiv4(x, (float)(__ldg(bag_offs + g + 1) - __ldg(bag_offs + g)));
+      acc[0] = add4(acc[0], x);
+    }
+    st4(partial + ch * D + c, add4(add4(acc[0], acc[1]), add4(acc[2], acc[3])));
+  }
+}
+
+// one warp per (run, 128-column slice): fold the run's chunk partials in chunk
+// order, then Adam (ADAM) or write out[key]
+template <bool ADAM>
+static __global__ void __launch_bounds__(256) k_tree_final(const LongRun* __restrict__ runs,
+                                                           const int64_t* __restrict__ nruns, int64_t cap,
+                                                           const int64_t* __restrict__ chunk_off,
+                                                           const float* __restrict__ partial, int64_t chunk_cap,
+                                                           int D, AdamDev a, float* __restrict__ out,
+                                                           int64_t* __restrict__ last_step, int64_t step) {
+  const int64_t R = *nruns < cap ? *nruns : cap;
+  const int slices = (D + 127) / 128;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t wu = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; wu < R * slices; wu += nw) {
+    const int64_t r = wu / slices;
+    const int c = (int)(wu - r * slices) * 128 + lane * 4;
+    const LongRun run = runs[r];
+    if (c < D) {
+      const int64_t cb = __ldg(chunk_off + r), ce = __ldg(chunk_off + r + 1) < chunk_cap ? __ldg(chunk_off + r + 1)
+                                                                                       : chunk_cap;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int64_t ch = cb; ch < ce; ++ch) acc = add4(acc, ldg4(partial + ch * D + c));
+      if constexpr (ADAM) {
+        float* row = out + (int64_t)run.key * (3 * D);
+        float4 p = ldg4(row + c), m = ldg4(row + D + c), v = ldg4(row + 2 * D + c);
+        adam1(p.x, m.x, v.x, acc.x, a);
+        adam1(p.y, m.y, v.y, acc.y, a);
+        adam1(p.z, m.z, v.z, acc.z, a);
+        adam1(p.w, m.w, v.w, acc.w, a);
+        st4(row + c, p);
+        st4(row + D + c, m);
+        st4(row + 2 * D + c, v);
+      } else {
+        st4(out + (int64_t)run.key * D + c, acc);
+      }
+    }
+    if (ADAM && lane == 0 && wu % slices == 0 && step >= 0) last_step[run.key] = step;
+  }
+}
+
+// Tolerance-mode long-run pass (D % 4 == 0): plan, chunk partials, final fold.
+template <bool ADAM>
+inline void launch_long_fold_tree(LongRun* runs, const int64_t* nruns, int64_t cap, const uint32_t* ridx,
+                                  const float* rows, int D, const int64_t* bag_offs, int mode, AdamDev a, float* out,
+                                  int64_t* last_step, int64_t step, cudaStream_t s, const float* zrow,
+                                  const TreeWork& w) {
+  k_tree_plan<<<1, 1024, 0, s>>>(runs, nruns, cap, w.chunk_off);
+  SKB_LAUNCH_CHECK();
+  const int slices = (D + 127) / 128;
+  const unsigned grid = grid_for(w.chunk_cap * slices * 32, 256, 8);
+  if (mode == 1)
+    k_tree_partial<true><<<grid, 256, 0, s>>>(runs, nruns, cap, w.chunk_off, ridx, rows, D, bag_offs, zrow, w.partial,
+                                              w.chunk_cap);
+  else
+    k_tree_partial<false><<<grid, 256, 0, s>>>(runs, nruns, cap, w.chunk_off, ridx, rows, D, bag_offs, zrow,
+                                               w.partial, w.chunk_cap);
+  SKB_LAUNCH_CHECK();
+  k_tree_final<ADAM><<<grid_for((cap + 1) * slices * 32, 256, 4), 256, 0, s>>>(
+      runs, nruns, cap, w.chunk_off, w.partial, w.chunk_cap, D, a, out, last_step, step);
+  SKB_LAUNCH_CHECK();
+}
+
 }  // namespace skb

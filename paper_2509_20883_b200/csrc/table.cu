@@ -160,6 +160,14 @@ static bool bound_ok_after_snapshot(Table* t, int64_t n) {
 bool table_needs_growth(Table* t, int64_t n) { return !bound_ok_after_snapshot(t, n); }
 
 void table_reserve(Table* t, int64_t n, cudaStream_t s) {
+  if (t->vmm) {
+    // copy-free growth needs no exact counters: map more rows as soon as the
+    // no-sync upper bound comes within 1/8 of the arena, so the bound never
+    // fails and growth never drains the streams for a counter refresh
+    harvest_snapshot(t);
+    const int64_t ub = t->known[C_ALLOC] + t->pending_adds + n;
+    if (ub > t->arena_rows - t->arena_rows / 8) grow_arena(t, std::max<int64_t>(ub + ub / 8, 1024), s);
+  }
   if (bound_ok_after_snapshot(t, n)) return;
   table_refresh(t, s);
   int64_t need_alloc = t->known[C_ALLOC] + n;

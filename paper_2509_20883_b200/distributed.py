@@ -37,10 +37,56 @@ import numpy as np
 from . import _native as N
 
 
+class ThreadRanks:
+    """S ranks of one process, one thread each, sharing one GPU context —
+    the multi-GPU step's protocol run with every rank's kernels on its own
+    stream of one device (bench.py BENCH_SHARED_GPU=1 and tests).  Windows are
+    plain device memory exchanged by pointer; ordering uses the same
+    stream-ordered peer-memory barriers as separate processes on separate
+    GPUs.  `group(rank)` is the per-thread handle passed as `group=`."""
+
+    def __init__(self, size: int):
+        import threading
+        self.size = size
+        self._barrier = threading.Barrier(size)
+        self._slots = [None] * size
+
+    def group(self, rank: int) -> "ThreadRankGroup":
+        return ThreadRankGroup(self, rank)
+
+
+class ThreadRankGroup:
+    """One thread's view of a ThreadRanks world (the torch.distributed subset
+    the step uses: rank, size, barrier, all_gather_object, all_reduce of a
+    host integer)."""
+
+    def __init__(self, world: ThreadRanks, rank: int):
+        self.world, self.rank, self.size = world, rank, world.size
+
+    def barrier(self, group=None):
+        self.world._barrier.wait()
+
+    def all_gather_object(self, out, obj, group=None):
+        self.world._slots[self.rank] = obj
+        self.world._barrier.wait()
+        out[:] = list(self.world._slots)
+        self.world._barrier.wait()
+
+    def all_reduce_int(self, x: int) -> int:
+        vals = [None] * self.size
+        self.all_gather_object(vals, int(x))
+        return sum(vals)
+
+
 class Comm:
-    """all-to-all helpers on a process group (NCCL on GPUs, gloo on CPU)."""
+    """all-to-all helpers on a process group (NCCL on GPUs, gloo on CPU), or
+    on a ThreadRankGroup (backend "local": ranks are threads of one process)."""
 
     def __init__(self, group=None):
+        if isinstance(group, ThreadRankGroup):
+            self.dist, self.group = group, None
+            self.size, self.rank, self.backend = group.size, group.rank, "local"
+            return
         import torch.distributed as dist
         self.dist = dist
         self.group = group
@@ -238,12 +284,13 @@ class P2PWindows:
         self.close(name)
         ptr, handle = C.c_void_p(), (C.c_char * 64)()
         N.call("skb_ipc_alloc", cap * unit_bytes, C.byref(ptr), handle)
+        local = self.comm.backend == "local"  # ranks share this process: plain pointers
         handles = [None] * self.comm.size
-        self.comm.dist.all_gather_object(handles, bytes(handle), group=self.comm.group)
+        self.comm.dist.all_gather_object(handles, ptr.value if local else bytes(handle), group=self.comm.group)
         peers = []
         for j, h in enumerate(handles):
-            if j == self.comm.rank:
-                peers.append(ptr.value)
+            if j == self.comm.rank or local:
+                peers.append(ptr.value if j == self.comm.rank else h)
             else:
                 q = C.c_void_p()
                 N.call("skb_ipc_open", (C.c_char * 64).from_buffer_copy(h), C.byref(q))
@@ -267,6 +314,8 @@ class P2PWindows:
         import torch
         torch.cuda.synchronize()
         self.comm.dist.barrier(group=self.comm.group)  # nobody touches the old windows any more
+        if self.comm.backend == "local":
+            self.opened.pop(name, None)
         for q in self.opened.pop(name, []):
             N.call("skb_ipc_close", C.c_void_p(q))
         N.call("skb_ipc_free", C.c_void_p(self.local.pop(name)))

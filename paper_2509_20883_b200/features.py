@@ -7,6 +7,8 @@ that launch as its single dispatch (features.py:139-146).
 
 from __future__ import annotations
 
+import ctypes
+
 import threading
 
 import numpy as np
@@ -251,16 +253,17 @@ class FusedPlan:
                 self._dev = (N.to_dev(self.moduli, "int64"),)
         return self._dev
 
-    def _concat(self, columns, dtype: str):
+    def _columns(self, columns, dtype: str):
+        """Per-column device inputs + a device pointer table (no concatenation)."""
         if len(columns) != self.num_columns:
             raise ValueError(f"plan has {self.num_columns} columns, got {len(columns)}")
         parts = [N.to_dev(c.values, dtype).reshape(-1) for c in columns]
-        lens = np.array([p.numel() for p in parts], np.int64)
         co = np.zeros(len(parts) + 1, np.int64)
-        np.cumsum(lens, out=co[1:])
-        t = N.torch()
-        vals = t.cat(parts) if parts else N.empty((0,), dtype)
-        return vals.contiguous(), N.to_dev(co, "int64"), co
+        np.cumsum([p.numel() for p in parts], out=co[1:])
+        # empty columns still need a valid address (never dereferenced)
+        ptrs = np.array([p.data_ptr() for p in parts], np.int64) if parts else np.zeros(1, np.int64)
+        tab = N.to_dev(np.concatenate([ptrs, co]), "int64")
+        return parts, tab, co
 
 
 def _split(out, co, columns, as_np):
@@ -272,30 +275,44 @@ def _split(out, co, columns, as_np):
 
 
 def fused_bucketize(plan: FusedPlan, columns: list) -> list:
-    """Bucketize many columns in one kernel launch (features.py:165-177)."""
+    """Bucketize many columns in one kernel launch (features.py:165-177),
+    reading every column in place through a device pointer table."""
     telemetry.bump("features.fused_bucketize")
     if plan.kind != "bucketize":
         raise ValueError("plan is not a bucketize plan")
-    vals, co_d, co = plan._concat(columns, "float32")
+    parts, tab, co = plan._columns(columns, "float32")
     edges, eo = plan._params_dev()
-    out = _bucketize_flat(vals, co_d, plan.num_columns, edges, eo)
+    C, n = plan.num_columns, int(co[-1])
+    out = N.empty((n,), "int64")
+    if n:
+        ptrs, offs = ctypes.c_void_p(tab.data_ptr()), ctypes.c_void_p(tab.data_ptr() + 8 * max(C, 1))
+        stack = getattr(_DEFERRED, "stack", None)
+        if stack:
+            flag = N.torch().full((1,), -1, dtype=N.torch().int64, device=out.device)
+            N.call("skb_bucketize_cols", ptrs, offs, C, N.ptr(edges), N.ptr(eo), N.ptr(out), n, N.ptr(flag),
+                   N.stream_ptr())
+            stack[-1].append((flag, "bucketize input contains NaN"))
+        else:
+            N.call("skb_bucketize_cols", ptrs, offs, C, N.ptr(edges), N.ptr(eo), N.ptr(out), n, None,
+                   N.stream_ptr())
     plan._record_dispatch()
     as_np = bool(columns) and not N.is_torch(columns[0].values)
     return _split(out, co, columns, as_np)
 
 
 def fused_mod(plan: FusedPlan, columns: list) -> list:
-    """Modulus-reduce many columns in one kernel launch (features.py:180-189)."""
+    """Modulus-reduce many columns in one kernel launch (features.py:180-189),
+    reading every column in place through a device pointer table."""
     telemetry.bump("features.fused_mod")
     if plan.kind != "mod":
         raise ValueError("plan is not a mod plan")
-    vals, co_d, co = plan._concat(columns, "int64")
+    parts, tab, co = plan._columns(columns, "int64")
     (mods,) = plan._params_dev()
-    n = vals.numel()
+    C, n = plan.num_columns, int(co[-1])
     out = N.empty((n,), "int64")
     if n:
-        N.call("skb_mod_multi", N.ptr(vals), N.ptr(co_d), plan.num_columns, N.ptr(mods), N.ptr(out), n,
-               N.stream_ptr())
+        N.call("skb_mod_cols", ctypes.c_void_p(tab.data_ptr()), ctypes.c_void_p(tab.data_ptr() + 8 * max(C, 1)), C,
+               N.ptr(mods), N.ptr(out), n, N.stream_ptr())
     plan._record_dispatch()
     as_np = bool(columns) and not N.is_torch(columns[0].values)
     return _split(out, co, columns, as_np)

@@ -43,16 +43,21 @@ class PackedBatch:
         for f in range(F):
             self.member_pos[f + 1] = self.member_pos[f] + ids_d[f].numel()
             self.member_bag[f + 1] = self.member_bag[f] + offs_d[f].numel() - 1
-        self.ids = t.cat(ids_d).contiguous() if F > 1 else ids_d[0]
-        # members' bag offsets shifted by their first position, in three launches
-        # and no host round trip: cat(offs_f[:-1], 0) + repeat(member_pos, bags_f (+1))
         G = int(self.member_bag[F])
-        dev = self.ids.device
-        heads = t.cat([o[:-1] for o in offs_d] + [t.zeros(1, dtype=t.int64, device=dev)])
-        reps = np.append(np.diff(self.member_bag), 1).astype(np.int64)
-        shift = t.repeat_interleave(N.to_dev(self.member_pos, "int64", dev), N.to_dev(reps, "int64", dev),
-                                    output_size=G + 1)
-        self.bag_offs = (heads + shift).contiguous()
+        if F == 1:
+            self.ids, self.bag_offs = ids_d[0], offs_d[0]
+        else:
+            # one launch through per-member pointer tables (no cat / repeat_interleave)
+            dev = ids_d[0].device
+            tab = np.concatenate([[x.data_ptr() for x in ids_d], [o.data_ptr() for o in offs_d],
+                                  self.member_pos, self.member_bag]).astype(np.int64)
+            tab_d = N.to_dev(tab, "int64", dev)
+            self.ids = N.empty((self.num_ids,), "int64", dev)
+            self.bag_offs = N.empty((G + 1,), "int64", dev)
+            b = tab_d.data_ptr()
+            vp = ctypes.c_void_p
+            N.call("skb_pack_members", vp(b), vp(b + 8 * F), vp(b + 16 * F), vp(b + 16 * F + 8 * (F + 1)), F,
+                   self.num_ids, G, N.ptr(self.ids), N.ptr(self.bag_offs), N.stream_ptr())
         self.salts = np.array([lt.salt(m) if lt.namespaced else 0 for m in self.members], np.uint64)
         self.strategy = np.array(
             [0 if resolve_strategy(strategy, int(self.member_pos[f + 1] - self.member_pos[f]),
@@ -183,6 +188,20 @@ def use_graphs(lt: LogicalTable, enable: bool = True) -> None:
     mode; it removes the per-kernel launch cost that dominates small batches."""
     for t in lt.shards:
         N.call("skb_fused_set_graphs", t.handle, int(bool(enable)))
+
+
+def set_fold_mode(lt: LogicalTable, mode: str = "exact") -> None:
+    """How the fused backward folds the gradients of hot ids (runs of > 32
+    positions in one batch).  "exact" (default): np.add.at's serial left fold
+    (sharding.py:283-290), bit-exact with the reference.  "tree": opt-in
+    tolerance mode — chunks of 256 positions folded in parallel, then the
+    chunk sums in order; per column |error| <= (256 + len/256) * 2^-24 *
+    sum|g|, below the serial fold's own len * 2^-24 * sum|g| bound.  Hot
+    ids then cost memory bandwidth instead of one FADD latency per position."""
+    if mode not in ("exact", "tree"):
+        raise ValueError(f"unknown fold mode {mode!r}")
+    for t in lt.shards:
+        N.call("skb_fused_set_fold_mode", t.handle, 1 if mode == "tree" else 0)
 
 
 def set_variants(lt: LogicalTable, adam: int = -1, pool: int = -1) -> None:

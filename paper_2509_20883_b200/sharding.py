@@ -166,11 +166,14 @@ class LogicalTable:
         self.group = group
         self._num_shards = num_shards
         if dist:
-            import torch.distributed as tdist
-            ws = tdist.get_world_size(group)
+            from .distributed import ThreadRankGroup
+            if isinstance(group, ThreadRankGroup):
+                ws, self.rank = group.size, group.rank
+            else:
+                import torch.distributed as tdist
+                ws, self.rank = tdist.get_world_size(group), tdist.get_rank(group)
             if ws != num_shards:
                 raise ValueError(f"dist table needs num_shards == world size ({ws}), got {num_shards}")
-            self.rank = tdist.get_rank(group)
             self.shards = [EmbeddingTable(f"{name}/shard{self.rank}", dim, seed=seed, block_size=block_size,
                                           evict_threshold=evict_threshold, dtype=dtype, capacity_hint=capacity_hint)]
         else:
@@ -191,6 +194,8 @@ class LogicalTable:
     @property
     def num_rows(self) -> int:
         n = sum(t.num_rows for t in self.shards)
+        if self.dist and hasattr(self.group, "all_reduce_int"):
+            return self.group.all_reduce_int(n)
         if self.dist:
             import torch.distributed as tdist
             x = N.torch().tensor([n], dtype=N.torch().int64, device="cuda")
@@ -218,6 +223,8 @@ class LogicalTable:
 
     def evict(self, current_step: int) -> int:
         n = sum(t.evict(current_step) for t in self.shards)
+        if self.dist and hasattr(self.group, "all_reduce_int"):
+            return self.group.all_reduce_int(n)
         if self.dist:
             import torch.distributed as tdist
             x = N.torch().tensor([n], dtype=N.torch().int64, device="cuda")

@@ -213,14 +213,19 @@ def test_dist_sparse_step_gpu(tmp_path, cuda, barrier):
         grows, syncs, p2p = np.load(os.path.join(tmp_path, f"grows{r}.npy")).tolist()
         assert syncs == STEPS                      # one host sync per step: the count matrix
         assert bool(p2p) == (barrier == "p2p")
-    olt = O.OracleLogical("dim4", DIM, S, seed=3, members=MEMBERS, namespaced=True)
+    _check_fused_vs_oracle(S, lambda r: np.load(os.path.join(tmp_path, f"fused{r}.npz")))
+
+
+def _check_fused_vs_oracle(W, load):
+    """Every rank's pooled rows and table shard vs the oracle fed the
+    rank-ordered concatenation with W shards (first step exact)."""
+    olt = O.OracleLogical("dim4", DIM, W, seed=3, members=MEMBERS, namespaced=True)
     for k in range(STEPS):
-        ins = [fused_inputs(r, k) for r in range(S)]
-        # concatenation: rank 0's member-a ids, member-b ids, then rank 1's ...
-        keys = np.concatenate([olt.keys_for(m, ins[r][0][f]) for r in range(S) for f, m in enumerate(MEMBERS)])
+        ins = [fused_inputs(r, k) for r in range(W)]
+        keys = np.concatenate([olt.keys_for(m, ins[r][0][f]) for r in range(W) for f, m in enumerate(MEMBERS)])
         rows = O.lookup(olt, keys, k + 1)
         pos, grads = 0, []
-        for r in range(S):
+        for r in range(W):
             ref = []
             for f in range(len(MEMBERS)):
                 o = ins[r][1][f]
@@ -230,18 +235,64 @@ def test_dist_sparse_step_gpu(tmp_path, cuda, barrier):
                 g = ins[r][2][f * FB:(f + 1) * FB] / np.maximum(lens, 1).astype(np.float32)[:, None]
                 grads.append(np.repeat(g, lens, axis=0).astype(np.float32))
                 pos += n_f
-            got = np.load(os.path.join(tmp_path, f"fused{r}.npz"))[f"arr_{k}"]
+            got = load(r)[f"arr_{k}"]
             if k == 0:
                 assert np.array_equal(got.view(np.int32), np.concatenate(ref).view(np.int32))
             else:
                 np.testing.assert_allclose(got, np.concatenate(ref), rtol=1e-5, atol=1e-6)
         O.grad_update(olt, keys, np.concatenate(grads), k + 1, lr=LR, weight_decay=0.01, variant="adamw")
-    for r in range(S):
-        z = np.load(os.path.join(tmp_path, f"fused{r}.npz"))
+    for r in range(W):
+        z = load(r)
         ex = olt.shards[r].export_rows()
         assert np.array_equal(z["ids"], ex[0])
         for key, j in (("w", 1), ("m", 2), ("v", 3)):
             np.testing.assert_allclose(z[key], ex[j], rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W", [2, 3])
+def test_dist_sparse_step_thread_ranks(cuda, W):
+    """The multi-GPU protocol with W ranks as threads of one process on one
+    GPU (ThreadRanks: plain-pointer windows, stream-ordered peer barriers,
+    every rank on its own stream) vs the oracle."""
+    import threading
+    import paper_2509_20883_b200 as skb
+    from paper_2509_20883_b200.distributed import DistSparseStep, ThreadRanks
+    world = ThreadRanks(W)
+    out, errs = [None] * W, []
+
+    def body(rank):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                lt = skb.LogicalTable("dim4", DIM, W, seed=3, members=MEMBERS, namespaced=True, dist=True,
+                                      group=world.group(rank))
+                stepper = DistSparseStep(lt)
+                assert stepper.p2p_sync
+                cfg = skb.AdamConfig(lr=LR, weight_decay=0.01, variant="adamw")
+                res = {}
+                for k in range(STEPS):
+                    ids, offs, dp = fused_inputs(rank, k)
+                    batch = skb.PackedBatch(lt, MEMBERS, ids, offs)
+                    res[f"arr_{k}"] = stepper.forward(batch, k + 1, "mean").cpu().numpy()
+                    stepper.backward(torch.from_numpy(dp).cuda(), cfg, k + 1)
+                ex = lt.local_table.export_rows()
+                res.update(ids=ex[0], w=ex[1], m=ex[2], v=ex[3])
+                assert stepper.syncs == STEPS
+                stepper.win.close_all()
+                out[rank] = res
+        except BaseException as e:
+            errs.append(repr(e))
+            world._barrier.abort()
+
+    ths = [threading.Thread(target=body, args=(r,)) for r in range(W)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout=300)
+    assert not errs, errs
+    _check_fused_vs_oracle(W, lambda r: out[r])
 
 
 @pytest.mark.parametrize("S", [1, 2, 3, 5, 8])

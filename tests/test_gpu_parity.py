@@ -891,3 +891,48 @@ def test_fused_step_load_stats(skb, P):
         assert got.imbalance == imbalance
         import torch
         skb.pool_grad_adam(lt, torch.zeros((12000, 8), device="cuda"), skb.AdamConfig(), step)
+
+
+@pytest.mark.parametrize("mode,D", [("sum", 64), ("mean", 16), ("sum", 8)])
+def test_fused_tree_fold_within_normwise_bound(skb, mode, D):
+    """Opt-in tree fold for hot ids: ids / slots / pooled rows exact; the
+    folded gradient of every run within (256 + len/256) * 2^-24 * sum|g|
+    per column (checked through Adam's first moment at step 1, m = 0.1 g);
+    later steps stay within a stated relative tolerance of the exact oracle."""
+    import torch
+    rng = np.random.default_rng(77 + D)
+    members = ["h"]
+    lt = skb.LogicalTable(f"dim{D}", D, 1, seed=1, members=members, namespaced=True)
+    skb.set_fold_mode(lt, "tree")
+    olt = O.OracleLogical(f"dim{D}", D, 1, seed=1, members=members, namespaced=True)
+    cfg = skb.AdamConfig(lr=1e-2, weight_decay=0.01, variant="adamw")
+    nb = 24000
+    for step in (1, 2):
+        lens = rng.integers(1, 9, nb)
+        offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        ids = rng.integers(0, 5000, int(offs[-1]))
+        hot = rng.random(len(ids)) < 0.6
+        ids[hot] = rng.integers(0, 3, int(hot.sum()))
+        batch = skb.PackedBatch(lt, members, [ids], [offs])
+        pooled = skb.lookup_pool(lt, batch, step, mode)
+        dp = rng.standard_normal((nb, D)).astype(np.float32)
+        skb.pool_grad_adam(lt, torch.from_numpy(dp).cuda(), cfg, step)
+        keys = olt.keys_for("h", ids)
+        rows = O.lookup(olt, keys, step)
+        eq(pooled, O.pool(rows, offs, mode))
+        g = dp / lens.astype(np.float32)[:, None] if mode == "mean" else dp
+        per = np.repeat(g, lens, axis=0).astype(np.float32)
+        O.grad_update(olt, keys, per, step, lr=1e-2, weight_decay=0.01, variant="adamw")
+        got, want = lt.local_table.export_rows(), olt.shards[0].export_rows()
+        eq(got[0], want[0])
+        eq(got[4], want[4])
+        if step == 1:
+            u, inv = np.unique(keys, return_inverse=True)
+            order = np.searchsorted(u, want[0])
+            absum = np.zeros((len(u), D), np.float64)
+            np.add.at(absum, inv, np.abs(per).astype(np.float64))
+            cnt = np.bincount(inv, minlength=len(u))[order][:, None]
+            bound = 0.1 * (256 + cnt / 256.0) * 2.0 ** -24 * absum[order] + 1e-12
+            assert np.all(np.abs(got[2].astype(np.float64) - want[2]) <= bound)
+        np.testing.assert_allclose(got[1], want[1], rtol=1e-5, atol=1e-6)
+        np.testing.assert_allclose(got[3], want[3], rtol=1e-4, atol=1e-9)
