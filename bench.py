@@ -62,6 +62,9 @@ def parse():
     p.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
                    help="c2 (default) is the headline line; c1/c3/c4/c5 measure SURVEY §8d's other configs "
                         "on one GPU (their own JSON line each, not the headline)")
+    p.add_argument("--fold", default="exact", choices=["exact", "tree"],
+                   help="hot-id gradient fold: exact np.add.at order (default) or the opt-in tolerance-mode tree "
+                        "(c3/c4/c5 legs)")
     p.add_argument("--c3-rows", type=float, default=1.25e8,
                    help="c3: grow the shard to this many rows (1e9 rows / 8 GPUs per GPU)")
     return p.parse_args()
@@ -771,12 +774,14 @@ def run_threads(args):
             world._barrier.abort()
             start.abort()
 
-    ths = [threading.Thread(target=body, args=(r,)) for r in range(W)]
+    ths = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(W)]
     clk = ClockSampler(0).__enter__()
     for t in ths:
         t.start()
     for t in ths:
-        t.join()
+        t.join(timeout=600)
+    if any(t.is_alive() for t in ths):
+        errs.append("thread ranks did not finish within 600 s")
     clk.__exit__(None, None, None)
     if errs:
         raise RuntimeError("; ".join(errs))

@@ -55,6 +55,9 @@ def _line(args, workload, value, ms, ids_per_step, samples_per_step, algo_bytes,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
                      "peak_kind": peak_kind, "algorithmic_bytes": int(algo_bytes)},
         "cpu_baseline": cpu,
+        "fold": getattr(args, "fold", "exact") + (" (tolerance mode: hot-id runs > 32 positions reduced as a two-level "
+                                                  "tree, not bit-exact)" if getattr(args, "fold", "exact") == "tree"
+                                                  else " (bit-exact np.add.at order)"),
     }
     if extra:
         line.update(extra)
@@ -158,6 +161,7 @@ def c3(args):
     # row arena starts empty and grows copy-free (VMM) as rows are admitted
     lt = skb.LogicalTable("dim16", D, 1, seed=0, members=mem, namespaced=True,
                           capacity_hint=int(args.c3_rows * 1.05))
+    skb.set_fold_mode(lt, args.fold)
     offs = [np.arange(Bn + 1, dtype=np.int64)] * F
     P = 4
     base = []
@@ -260,6 +264,7 @@ def c4(args):
     # host's no-sync admission bound (every in-flight position a possible new
     # row); a tighter arena makes every step synchronise to refresh counters
     lt = skb.LogicalTable("seq", D, 1, seed=4, members=["seq"], namespaced=False, capacity_hint=2_400_000 + 3 * n)
+    skb.set_fold_mode(lt, args.fold)
     offs_d = torch.arange(0, n + 1, L, dtype=torch.int64, device="cuda")
     P = 2
     ids = [torch.from_numpy(np.random.Generator(np.random.PCG64(4 + k)).zipf(1.1, n).astype(np.int64)).cuda()
@@ -400,6 +405,8 @@ def c5(args):
     # with rows pre-reserved (no growth copies), admission in every step
     lts = {d: skb.LogicalTable(f"dim{d}", d, 1, seed=0, members=members[d], namespaced=True,
                                capacity_hint=24_000_000 if args.cold else 45_000_000) for d in DIMS5}
+    for lt_ in lts.values():
+        skb.set_fold_mode(lt_, args.fold)
     prepop_s = None
     if not args.cold:
         t0 = time.perf_counter()

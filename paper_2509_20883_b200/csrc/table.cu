@@ -43,11 +43,15 @@ static void grow_array(T*& p, int64_t old_n, int64_t new_n, cudaStream_t s) {
 // move); VA is reserved for the capacity hint, else 8x the rows needed, and
 // re-reserved (remap, no copy) only when outgrown
 static void grow_arena_vmm(Table* t, int64_t new_rows, cudaStream_t s) {
-  const int64_t res_rows = std::max<int64_t>(t->rows_hint + t->rows_hint / 4, 8 * new_rows);
+  const int64_t res_rows = std::max<int64_t>(t->rows_hint + t->rows_hint / 4, 64 * new_rows);
   const size_t esz[6] = {sizeof(float) * (size_t)t->row_stride(), sizeof(int64_t), sizeof(uint8_t), sizeof(int64_t),
                          sizeof(int64_t), sizeof(int64_t)};
   bool moved = false;
-  for (int i = 0; i < 6; ++i) moved |= vmm_grow(t->va[i], esz[i] * (size_t)new_rows, esz[i] * (size_t)res_rows, s);
+  for (int i = 0; i < 6; ++i) {
+    // VA is cheap: at least 16 GB per array (a re-reservation drains the device)
+    const size_t res = std::max<size_t>(esz[i] * (size_t)res_rows, (size_t)16 << 30);
+    moved |= vmm_grow(t->va[i], esz[i] * (size_t)new_rows, res, s);
+  }
   t->arena = reinterpret_cast<float*>(t->va[0].base);
   t->last_step = reinterpret_cast<int64_t*>(t->va[1].base);
   t->live = reinterpret_cast<uint8_t*>(t->va[2].base);

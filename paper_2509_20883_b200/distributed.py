@@ -439,7 +439,21 @@ class DistSparseStep:
 
     def _barrier(self):
         """Order every rank's prior peer stores before any rank's later reads."""
-        if self.p2p_sync:
+        if self.comm.backend == "local":
+            # ranks are threads of one process: every stream waits on events the
+            # others have ALREADY recorded — a wait on a not-yet-enqueued peer
+            # write (the memop barrier) could deadlock against any implicit
+            # device-wide synchronisation (cudaMalloc) of another rank's thread
+            import torch
+            ev = torch.cuda.Event()
+            ev.record()
+            evs = [None] * self.S
+            self.comm.dist.all_gather_object(evs, ev)
+            cur = torch.cuda.current_stream()
+            for j, e in enumerate(evs):
+                if j != self.me:
+                    cur.wait_event(e)
+        elif self.p2p_sync:
             self.epoch += 1
             N.call("skb_p2p_barrier", self._flag_ptrs, self.S, self.me, self.epoch, N.stream_ptr())
         else:

@@ -286,11 +286,12 @@ def test_dist_sparse_step_thread_ranks(cuda, W):
             errs.append(repr(e))
             world._barrier.abort()
 
-    ths = [threading.Thread(target=body, args=(r,)) for r in range(W)]
+    ths = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(W)]
     for t in ths:
         t.start()
     for t in ths:
         t.join(timeout=300)
+    assert not any(t.is_alive() for t in ths), "thread ranks did not finish (deadlock?)"
     assert not errs, errs
     _check_fused_vs_oracle(W, lambda r: out[r])
 
