@@ -1612,7 +1612,7 @@ static void fused_prepare(Table* t, const BatchArgs& a, cudaStream_t s) {
   // fold+Adam of the previous step) can touch the new buffers (rare)
   // (VMM tables grow in place: rows never move and the IDMap rehash is
   // stream-ordered on this stream, the only one that reads the IDMap)
-  const bool grow = table_needs_growth(t, a.n) && !t->vmm;
+  const bool grow = !t->vmm && table_needs_growth(t, a.n);
   if (grow) {
     SKB_CUDA(cudaStreamSynchronize(s));
     SKB_CUDA(cudaStreamSynchronize(x));

@@ -168,9 +168,19 @@ void table_reserve(Table* t, int64_t n, cudaStream_t s) {
     // copy-free growth needs no exact counters: map more rows as soon as the
     // no-sync upper bound comes within 1/8 of the arena, so the bound never
     // fails and growth never drains the streams for a counter refresh
+    // The bound counts every enqueued position as a possible new row, so a
+    // host running many steps ahead would map memory for rows that never
+    // come: before growing, wait for the in-flight snapshot (one index
+    // phase behind the host, not a drain) and re-check with its counts.
     harvest_snapshot(t);
-    const int64_t ub = t->known[C_ALLOC] + t->pending_adds + n;
-    if (ub > t->arena_rows - t->arena_rows / 8) grow_arena(t, std::max<int64_t>(ub + ub / 8, 1024), s);
+    int64_t ub = t->known[C_ALLOC] + t->pending_adds + n;
+    if (ub > t->arena_rows && t->snap_pending) {
+      g_snap_waits++;
+      SKB_CUDA(cudaEventSynchronize(t->snap_ev));
+      harvest_snapshot(t);
+      ub = t->known[C_ALLOC] + t->pending_adds + n;
+    }
+    if (ub > t->arena_rows) grow_arena(t, std::max<int64_t>(ub + ub / 8, 1024), s);
   }
   if (bound_ok_after_snapshot(t, n)) return;
   table_refresh(t, s);
