@@ -144,6 +144,24 @@ class ClockSampler:
 # algorithmic bytes (SURVEY §8d convention)
 # ---------------------------------------------------------------------------
 
+def maybe_trace(tag, fn):
+    """SKB_TRACE=<dir>: after the timed region, run fn() (a few more steps)
+    under torch.profiler (CUPTI kernel timeline) and write
+    <dir>/trace_<tag>.json (Chrome trace) for per-stream busy time and gaps
+    (scripts/trace_gaps.py).  Never part of a reported number."""
+    d = os.environ.get("SKB_TRACE")
+    if not d:
+        return
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    os.makedirs(d, exist_ok=True)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as p:
+        fn()
+        torch.cuda.synchronize()
+    p.export_chrome_trace(os.path.join(d, f"trace_{tag}.json"))
+
+
 def phase_bytes(n, g, u, unew, d, mode_mean=False):
     """Algorithmic minimum bytes per launch of each fused phase."""
     return {
@@ -452,6 +470,7 @@ def run_ours(args):
         vals = list(buf)[: cnt.value]
         phase_ms[name] = sum(vals) / len(vals) if vals else 0.0
     N.call("skb_fused_profile", table.handle, 0, N.stream_ptr())
+    maybe_trace("c2", lambda: run_steps(lambda k: (dev_batches[k % P], dps[k % P]), 6))
     u_touched, u_new = skb.last_step_stats(lt)
 
     # ---- e2e: public API with host buffers, H2D + result D2H inside ----------
@@ -765,6 +784,13 @@ def run_threads(args):
                 e1.record(st)
                 st.synchronize()
                 wall = time.perf_counter() - w0
+                if os.environ.get("SKB_TRACE"):  # every rank steps; rank 0 records the timeline
+                    start.wait()
+                    if rank == 0:
+                        maybe_trace(f"n{W}_shared", lambda: run(4))
+                    else:
+                        run(4)
+                        st.synchronize()
                 res[rank] = {"ms": e0.elapsed_time(e1) / args.steps, "wall_ms": wall * 1e3 / args.steps,
                              "syncs_per_step": (stepper.syncs - syncs0) / args.steps,
                              "counts": stepper.last_counts, "owner_unique": stepper.owner_unique()}

@@ -187,6 +187,32 @@ __host__ __device__ __forceinline__ int64_t next_pow2(int64_t x) {
 // ---------------------------------------------------------------------------
 // vector helpers
 // ---------------------------------------------------------------------------
+// segment of x in the ascending prefix array pre[0..S] (pre[S] = total)
+__device__ __forceinline__ int seg_of(const int64_t* __restrict__ pre, int S, int64_t x) {
+  int lo = 0, hi = S;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(pre + mid) <= x) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Destination of fold-only output row `key`: out + key*D, or (peers set) the
+// row's place in the receive window of the rank owning key's segment
+// (segments pre[j]..pre[j+1] go to peers[j] from row base[j]) — the
+// requester's folded gradients stored straight over NVLink, no staging copy.
+struct RowOut {
+  const int64_t* pre = nullptr;
+  int S = 0;
+  float* const* peers = nullptr;
+  const int64_t* base = nullptr;
+  __device__ __forceinline__ float* row(float* out, uint32_t key, int D) const {
+    if (!peers) return out + (int64_t)key * D;
+    const int j = seg_of(pre, S, key);
+    return peers[j] + (__ldg(base + j) + ((int64_t)key - __ldg(pre + j))) * D;
+  }
+};
+
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {

@@ -14,8 +14,9 @@
 //   pool      pooled[g] from the rows the owners stored into this rank's row
 //             window, through gidx (sum / mean, scatter or pairwise order).
 //   fold_send per local unique id, the in-order fold of dpooled[bag] (/len)
-//             — np.add.at order — stored straight into its owner's gradient
-//             window at this rank's rank-ordered offset.
+//             — np.add.at order — stored by the fold kernels themselves
+//             straight into its owner's gradient window at this rank's
+//             rank-ordered offset (no staging buffer, no copy kernel).
 // The owner side is the single-GPU fused step itself (fused.cu
 // skb_fused_forward_send / skb_fused_backward).  The only host
 // synchronisation of a step is the caller's read of the all-gathered count
@@ -45,7 +46,6 @@ struct DistCtx {
   size_t part_ws_bytes = 0;
   void* sort_ws = nullptr;
   size_t sort_ws_bytes = 0;
-  float* agg = nullptr;        // [cap_n, D] folded gradients per unique id
   LongRun* longs = nullptr;
   int64_t lcap = 0;
   int64_t* cnt = nullptr;      // [2]
@@ -86,7 +86,6 @@ static void dist_reserve(DistCtx* d, int64_t n, int F, cudaStream_t s) {
     grow_buf(d->bag, cap);
     grow_buf(d->skey, cap);
     grow_buf(d->sval, cap);
-    grow_buf(d->agg, cap * d->D);
     d->lcap = cap / kLongRun + 1;
     grow_buf(d->longs, d->lcap);
     d->part_ws_bytes = unique_partition_ws_bytes(cap, d->S);
@@ -190,7 +189,7 @@ int skb_dist_destroy(skb_dist_t h) {
   DistCtx* d = dist_from(h);
   SKB_CUDA(cudaDeviceSynchronize());
   for (void* p : {(void*)d->keys, (void*)d->uniq, (void*)d->counts, (void*)d->gidx, (void*)d->bag, (void*)d->skey,
-                  (void*)d->sval, d->part_ws, d->sort_ws, (void*)d->agg, (void*)d->longs, (void*)d->cnt,
+                  (void*)d->sval, d->part_ws, d->sort_ws, (void*)d->longs, (void*)d->cnt,
                   (void*)d->pack.images, (void*)d->pack.mlist, (void*)d->pack.moff, (void*)d->pack.morder,
                   (void*)d->pack.mcount, (void*)d->members})
     if (p) cudaFree(p);
@@ -238,8 +237,10 @@ int skb_dist_fold_send(skb_dist_t h, const float* dpooled, int32_t mode, int64_t
   if (!d->prepared) raise(SKB_E_VALUE, 0, "fold_send before prepare");
   if (num_unique < 0 || num_unique > d->n) raise(SKB_E_ARG, num_unique, "num_unique out of range");
   FoldWork w{d->longs, d->lcap, d->cnt, d->D % 4 == 0 ? &d->pack : nullptr};
-  fold_sorted(d->n, d->skey, d->sval, d->bag_offs, dpooled, mode, d->D, d->agg, w, s);
-  p2p_send_segments(d->agg, num_unique, d->D, seg_prefix, d->S, peer_windows, dst_base, s);
+  // each folded row is stored straight into its owner's gradient window
+  // (RowOut: segment of the unique index -> peer j, row base[j] + offset)
+  fold_sorted(d->n, d->skey, d->sval, d->bag_offs, dpooled, mode, d->D, nullptr, w, s,
+              RowOut{seg_prefix, d->S, peer_windows, dst_base});
   d->prepared = false;
   SKB_API_END
 }

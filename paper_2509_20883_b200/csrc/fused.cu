@@ -907,7 +907,8 @@ __global__ void __launch_bounds__(256, MINB) k_fused_adam(int64_t n, const uint3
                                                     float* __restrict__ arena, int64_t* __restrict__ last_step,
                                                     int64_t step, int64_t* __restrict__ dev_unique,
                                                     LongRun* __restrict__ longs, int64_t* __restrict__ nlong,
-                                                    int64_t longs_cap, const float* __restrict__ zrow = nullptr) {
+                                                    int64_t longs_cap, const float* __restrict__ zrow = nullptr,
+                                                    RowOut ro = RowOut{}) {
   using T = typename VecT<VEC>::T;
   __shared__ uint32_t s_bag[8][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -990,8 +991,8 @@ __global__ void __launch_bounds__(256, MINB) k_fused_adam(int64_t n, const uint3
             vstore<VEC>(row + c, p[r]);
             vstore<VEC>(row + D + c, m[r]);
             vstore<VEC>(row + 2 * D + c, v[r]);
-          } else {  // fold only: acc -> out[key] (arena is the [U, D] output)
-            vstore<VEC>(arena + (int64_t)slot[r] * D + c, acc[r]);
+          } else {  // fold only: acc -> out[key] (arena is the [U, D] output, or ro's peer rows)
+            vstore<VEC>(ro.row(arena, slot[r], D) + c, acc[r]);
           }
         }
       }
@@ -1002,6 +1003,7 @@ __global__ void __launch_bounds__(256, MINB) k_fused_adam(int64_t n, const uint3
     __syncwarp();
   }
   if (lane == 0 && heads_seen) atomicAdd(reinterpret_cast<unsigned long long*>(dev_unique), heads_seen);
+  if (!ADAM && ro.peers) __threadfence_system();  // peer stores before the stream's barrier write
 }
 
 // ---------------------------------------------------------------------------
@@ -1516,11 +1518,11 @@ static void register_param_kernels() {
   if (done) return;
   done = true;
   note_param_kernel((const void*)k_fused_admit, 24, -1, 14);  // step is argument 14 (ids, n, mt, F, ns, fpos, hslot, ...)
-  note_param_kernel((const void*)k_fused_adam<1, 1, 4>, 16, 7, 10);
-  note_param_kernel((const void*)k_fused_adam<4, 2, 4>, 16, 7, 10);
-  note_param_kernel((const void*)k_fused_adam<4, 1, 5>, 16, 7, 10);
-  note_param_kernel((const void*)k_fused_adam<4, 1, 4>, 16, 7, 10);
-  note_param_kernel((const void*)k_long_fold<true>, 18, 8, 11);  // (runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out, last_step, step, nst, zrow, packed, mlist, morder, mcount)
+  note_param_kernel((const void*)k_fused_adam<1, 1, 4>, 17, 7, 10);
+  note_param_kernel((const void*)k_fused_adam<4, 2, 4>, 17, 7, 10);
+  note_param_kernel((const void*)k_fused_adam<4, 1, 5>, 17, 7, 10);
+  note_param_kernel((const void*)k_fused_adam<4, 1, 4>, 17, 7, 10);
+  note_param_kernel((const void*)k_long_fold<true>, 20, 8, 11);  // (runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out, last_step, step, nst, zrow, packed, mlist, morder, mcount, ro, direct)
 }
 
 // graph mode is off while per-phase event profiling is on (events cannot be
@@ -2237,21 +2239,24 @@ void pool_by_index(const float* rows, int64_t stride, const uint32_t* idx, const
 }
 
 void fold_sorted(int64_t n, const uint32_t* skey, const uint32_t* sval, const int64_t* bag_offs,
-                 const float* dpooled, int mode, int D, float* out, const FoldWork& w, cudaStream_t s) {
+                 const float* dpooled, int mode, int D, float* out, const FoldWork& w, cudaStream_t s,
+                 const RowOut& ro) {
   SKB_CUDA(cudaMemsetAsync(w.cnt, 0, sizeof(int64_t) * 2, s));
   if (n <= 0) return;
   const int64_t chunks = (n + 31) / 32;
   AdamDev none{};
+  // peer windows (ro) hold D-float rows at 16-byte aligned bases
   const bool v4 = D % 4 == 0 && (uintptr_t)dpooled % 16 == 0 && (uintptr_t)out % 16 == 0;
   if (v4) {
     k_fused_adam<4, 1, 4, false><<<(unsigned)((chunks + 7) / 8), 256, 0, s>>>(
-        n, skey, sval, bag_offs, dpooled, mode, D, none, out, nullptr, -1, w.cnt, w.longs, w.cnt + 1, w.lcap);
+        n, skey, sval, bag_offs, dpooled, mode, D, none, out, nullptr, -1, w.cnt, w.longs, w.cnt + 1, w.lcap,
+        nullptr, ro);
     SKB_LAUNCH_CHECK();
     launch_long_fold<false>(w.longs, w.cnt + 1, w.lcap, sval, dpooled, D, bag_offs, mode, none, out, nullptr, -1, s,
-                            nullptr, w.pack);
+                            nullptr, w.pack, true, kLfSmemBudget, ro);
   } else {
     k_fused_adam<1, 1, 4, false><<<(unsigned)((chunks + 7) / 8), 256, 0, s>>>(
-        n, skey, sval, bag_offs, dpooled, mode, D, none, out, nullptr, -1, w.cnt, nullptr, nullptr, 0);
+        n, skey, sval, bag_offs, dpooled, mode, D, none, out, nullptr, -1, w.cnt, nullptr, nullptr, 0, nullptr, ro);
     SKB_LAUNCH_CHECK();
   }
 }

@@ -37,6 +37,7 @@ struct FoldWork {
 // the (key, bag) pairs sorted stably by key — np.add.at order.  Only keys
 // that occur are written.
 void fold_sorted(int64_t n, const uint32_t* skey, const uint32_t* sval, const int64_t* bag_offs,
-                 const float* dpooled, int mode, int D, float* out, const FoldWork& w, cudaStream_t s);
+                 const float* dpooled, int mode, int D, float* out, const FoldWork& w, cudaStream_t s,
+                 const RowOut& ro = RowOut{});
 
 }  // namespace skb

@@ -109,6 +109,12 @@ __host__ __device__ inline int long_fold_tpi(int D) {
   const int64_t t = ((long_fold_stage_f(D) / long_fold_img_w(D) - kLfPad) / 32) * 32;
   return (int)(t < 32 ? 32 : t);
 }
+// positions per direct column-group stage ([TPG][kLfGW] floats, row-major):
+// as many as the slot holds, a multiple of 32, at most the index buffer
+__host__ __device__ inline int long_fold_tpg(int D) {
+  const int64_t t = (long_fold_stage_f(D) / kLfGW) & ~31ll;
+  return (int)(t > kLfMaxTP ? kLfMaxTP : (t < 32 ? 32 : t));
+}
 constexpr int kLfMaxNC = 16;  // consumer warps
 constexpr int kLfCols = 4;    // columns per consumer lane: dims up to 32 * kLfMaxNC * kLfCols = 2048
 __host__ __device__ inline int long_fold_consumers(int D) {
@@ -129,10 +135,14 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+__device__ __forceinline__ float4 vdiv4(float4 x, float l) {
+  return make_float4(__fdiv_rn(x.x, l), __fdiv_rn(x.y, l), __fdiv_rn(x.z, l), __fdiv_rn(x.w, l));
+}
+
 // work unit wu -> (run, column group, packed?); false: nothing to do
 __device__ __forceinline__ bool long_fold_unit(int64_t wu, int64_t MU, int NCG, const LongRun* __restrict__ runs,
                                                const uint32_t* __restrict__ mlist,
-                                               const uint32_t* __restrict__ morder, const float* packed,
+                                               const uint32_t* __restrict__ morder, bool grouped,
                                                LongRun& run, int& cg, bool& img) {
   if (wu < MU) {  // column group of a mega run; unfitted mega runs come back as ordinary units
     const int64_t m = wu / NCG;
@@ -144,7 +154,7 @@ __device__ __forceinline__ bool long_fold_unit(int64_t wu, int64_t MU, int NCG, 
   run = runs[wu - MU];
   cg = 0;
   img = false;
-  return !(packed && run.pad != kNoPack);  // packed runs were covered by their groups
+  return !(grouped && run.pad != kNoPack);  // grouped runs were covered by their groups
 }
 
 template <bool ADAM>
@@ -154,7 +164,7 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
                             int64_t* __restrict__ last_step, int64_t step, int nst,
                             const float* __restrict__ zrow, const float* __restrict__ packed,
                             const uint32_t* __restrict__ mlist, const uint32_t* __restrict__ morder,
-                            const int64_t* __restrict__ mcount) {
+                            const int64_t* __restrict__ mcount, RowOut ro = RowOut{}, bool direct = false) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int TP = long_fold_tp(D);                // positions per row-major stage
   const int TPI = long_fold_tpi(D);              // positions per packed column-group image
@@ -171,7 +181,11 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
   // first (morder), so the hottest ids' chains start in the first wave on
   // distinct SMs; then one unit per ordinary run.  Producers and consumers
   // walk the same sequence.
-  const int64_t MU = packed ? (mcount[0] < R ? mcount[0] : R) * NCG : 0;
+  // direct: mega runs are column-group units too, but their producers gather
+  // the group's columns straight from the gradient rows (no packed images)
+  const bool grouped = packed != nullptr || direct;
+  const int TPG = long_fold_tpg(D);  // positions per direct group stage ([TPG][kLfGW] row-major)
+  const int64_t MU = grouped ? (mcount[0] < R ? mcount[0] : R) * NCG : 0;
   const int64_t units = MU + R;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -190,16 +204,66 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
       int cg;
       LongRun run;
       bool img;
-      if (!long_fold_unit(wu, MU, NCG, runs, mlist, morder, packed, run, cg, img)) continue;
+      if (!long_fold_unit(wu, MU, NCG, runs, mlist, morder, grouped, run, cg, img)) continue;
       const int ncol = D - kLfGW * cg < kLfGW ? D - kLfGW * cg : kLfGW;
-      const int step_p = img ? TPI : TP;
+      const int step_p = img ? (packed ? TPI : TPG) : TP;
       const int64_t nimg = img ? ((int64_t)run.je - run.jh + TPI - 1) / TPI : 0;  // images per column group
       for (int64_t p0 = run.jh; p0 < run.je; p0 += step_p, ++it) {
         if ((int)(it % (uint32_t)NPW) != pw) continue;
         const int s = (int)(it % (uint32_t)nst);
         const uint32_t ph = (it / (uint32_t)nst) & 1u;
-        const int np = (int)((int64_t)run.je - p0 < TP ? (int64_t)run.je - p0 : TP);
+        const int np = (int)((int64_t)run.je - p0 < step_p ? (int64_t)run.je - p0 : step_p);
         float* dst = buf + s * stage_f;
+        if (img && !packed) {  // direct group stage: [TPG][kLfGW] of this group's columns
+          const int cpg = ncol >> 2;  // 16-byte chunks per position (D % 4 == 0)
+          uint32_t* ix = idx + pw * kLfMaxTP;
+          {
+            uint32_t gi[kLfMaxTP / 32];  // all index loads in flight before the stores
+#pragma unroll
+            for (int k = 0; k < kLfMaxTP / 32; ++k) gi[k] = k * 32 + lane < np ? __ldg(ridx + p0 + k * 32 + lane) : 0u;
+#pragma unroll
+            for (int k = 0; k < kLfMaxTP / 32; ++k)
+              if (k * 32 + lane < np) ix[k * 32 + lane] = gi[k];
+          }
+          __syncwarp();
+          mbar_wait(&empty[s], ph ^ 1u);
+          const int items = np * cpg;
+          const int col0 = kLfGW * cg;
+          if (mode == 1) {
+            for (int b = lane; b < items; b += 4 * 32) {
+              float4 x[4];
+              float l[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int i = b + k * 32;
+                if (i < items) {
+                  const int row = i / cpg, ch = i - row * cpg;
+                  const uint32_t gg = ix[row];
+                  x[k] = ldg4((gg == 0xFFFFFFFFu ? zrow : rows + (int64_t)gg * D) + col0 + ch * 4);
+                  l[k] = (float)(__ldg(bag_offs + gg + 1) - __ldg(bag_offs + gg));
+                }
+              }
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int i = b + k * 32;
+                if (i < items) {
+                  const int row = i / cpg, ch = i - row * cpg;
+                  st4(dst + row * kLfGW + ch * 4, vdiv4(x[k], l[k]));
+                }
+              }
+            }
+            mbar_arrive(&full[s]);
+          } else {
+            for (int i = lane; i < items; i += 32) {
+              const int row = i / cpg, ch = i - row * cpg;
+              const uint32_t gg = ix[row];
+              cp_async16(dst + row * kLfGW + ch * 4, (gg == 0xFFFFFFFFu ? zrow : rows + (int64_t)gg * D) + col0 + ch * 4);
+            }
+            cp_async_arrive_noinc(&full[s]);
+          }
+          __syncwarp();  // ix is rewritten by this warp's next stage
+          continue;
+        }
         if (img) {  // one bulk copy: this column group's image of TPI positions
           const uint32_t bytes = (uint32_t)ncol * (uint32_t)PS * 4u;
           mbar_wait(&empty[s], ph ^ 1u);
@@ -281,9 +345,9 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
     int cg;
     LongRun run;
     bool img;
-    if (!long_fold_unit(wu, MU, NCG, runs, mlist, morder, packed, run, cg, img)) continue;
+    if (!long_fold_unit(wu, MU, NCG, runs, mlist, morder, grouped, run, cg, img)) continue;
     const int ncol = D - kLfGW * cg < kLfGW ? D - kLfGW * cg : kLfGW;
-    const int step_p = img ? TPI : TP;
+    const int step_p = img ? (packed ? TPI : TPG) : TP;
     float acc[kLfCols];
 #pragma unroll
     for (int q = 0; q < kLfCols; ++q) acc[q] = 0.f;
@@ -292,38 +356,55 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
       const uint32_t ph = (it / (uint32_t)nst) & 1u;
       const int np = (int)((int64_t)run.je - p0 < step_p ? (int64_t)run.je - p0 : step_p);
       mbar_wait(&full[s], ph);
-      if (img) {  // column-major image slice: four positions per 16-byte load,
+      if (img && !packed) {  // direct group stage: lane c folds column c, one position per LDS
+        if (warp == 0 && lane < ncol) {
+          const float* src = buf + s * stage_f + lane;
+#pragma unroll 16
+          for (int p = 0; p < np; ++p) acc[0] = __fadd_rn(acc[0], src[p * kLfGW]);
+        }
+      } else if (img) {  // column-major image slice: four positions per 16-byte load,
                   // the next 16 positions' loads issued before this 16's adds
         if (warp == 0 && lane < ncol) {
           const float* col = buf + s * stage_f + (int64_t)lane * PS;
           const float4* c4 = reinterpret_cast<const float4*>(col);
-          const int n16 = np & ~15;
-          if (n16) {
-            float4 x[4];
+          // two 16-position groups of loads in flight: every LDS.128 has a
+          // full 32-FADD iteration (~128 cycles) to land before its adds
+          const int n32 = np & ~31;
+          auto fold4 = [&](const float4& v) {
+            acc[0] = __fadd_rn(acc[0], v.x);
+            acc[0] = __fadd_rn(acc[0], v.y);
+            acc[0] = __fadd_rn(acc[0], v.z);
+            acc[0] = __fadd_rn(acc[0], v.w);
+          };
+          if (n32) {
+            float4 a[4], b[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) x[k] = c4[k];
-            for (int p = 16; p < n16; p += 16) {
-              float4 y[4];
+            for (int k = 0; k < 4; ++k) {
+              a[k] = c4[k];
+              b[k] = c4[4 + k];
+            }
+            for (int p = 32; p < n32; p += 32) {
+              float4 c[4], d[4];
 #pragma unroll
-              for (int k = 0; k < 4; ++k) y[k] = c4[(p >> 2) + k];
+              for (int k = 0; k < 4; ++k) c[k] = c4[(p >> 2) + k];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) fold4(a[k]);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) d[k] = c4[(p >> 2) + 4 + k];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) fold4(b[k]);
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
-                acc[0] = __fadd_rn(acc[0], x[k].x);
-                acc[0] = __fadd_rn(acc[0], x[k].y);
-                acc[0] = __fadd_rn(acc[0], x[k].z);
-                acc[0] = __fadd_rn(acc[0], x[k].w);
-                x[k] = y[k];
+                a[k] = c[k];
+                b[k] = d[k];
               }
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              acc[0] = __fadd_rn(acc[0], x[k].x);
-              acc[0] = __fadd_rn(acc[0], x[k].y);
-              acc[0] = __fadd_rn(acc[0], x[k].z);
-              acc[0] = __fadd_rn(acc[0], x[k].w);
-            }
+            for (int k = 0; k < 4; ++k) fold4(a[k]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) fold4(b[k]);
           }
-          for (int p = n16; p < np; ++p) acc[0] = __fadd_rn(acc[0], col[p]);
+          for (int p = n32; p < np; ++p) acc[0] = __fadd_rn(acc[0], col[p]);
         }
       } else {
 #pragma unroll
@@ -358,10 +439,11 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
         row[2 * D + c] = v;
         if (c == 0 && step >= 0) last_step[run.key] = step;
       } else {
-        out[(int64_t)run.key * D + c] = acc[q];
+        ro.row(out, run.key, D)[c] = acc[q];
       }
     }
   }
+  if (!ADAM && ro.peers) __threadfence_system();  // peer stores before the stream's barrier write
 }
 
 // ---------------------------------------------------------------------------
@@ -469,16 +551,18 @@ static __global__ void __launch_bounds__(1024) k_pack_plan(LongRun* runs, const 
   }
 }
 
-// one block per (mega run, stage k): the stage's TPI gradient rows are read
-// whole (coalesced 16-byte loads; / len for mean bags; zero row past a
-// tile's k) kPackSub positions at a time into shared memory, then written
-// out as contiguous column segments of all the run's column-group images at
-// once — every gradient byte is read once (a block per image re-read each row
-// per column group), every image byte written once.
-inline int pack_sub(int D) {
-  const int sp = 16384 / D;
+// one block per (mega run, stage k): the stage's TPI gradient rows are
+// gathered kPackSub positions at a time into shared memory by 16-byte
+// cp.async (double-buffered: sub-chunk i+1 in flight while sub-chunk i is
+// written out; zero row past a tile's k), then written out as contiguous
+// column segments of all the run's column-group images at once (/ len for
+// mean bags) — every gradient byte is read once, every image byte written
+// once, and a block always has a sub-chunk of loads outstanding.
+inline int pack_sub(int D) {  // 64 positions (measured: 128 at D=64 was slower, 630 vs 537 us in C4)
+  const int sp = 9000 / (D + 4);
   return sp > 64 ? 64 : (sp < 4 ? 4 : sp & ~3);
 }
+inline size_t pack_smem(int D) { return (size_t)2 * pack_sub(D) * ((D + 4) * sizeof(float) + sizeof(uint32_t)); }
 static __global__ void __launch_bounds__(256) k_pack_rows(const LongRun* __restrict__ runs,
                                                           const uint32_t* __restrict__ mlist,
                                                           const uint32_t* __restrict__ moff,
@@ -489,9 +573,12 @@ static __global__ void __launch_bounds__(256) k_pack_rows(const LongRun* __restr
                                                           const int64_t* __restrict__ bag_offs, int mode, int SP,
                                                           float* __restrict__ images) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float* tile = reinterpret_cast<float*>(smem_raw);  // [SP][D + 1]
-  const int TPI = long_fold_tpi(D), PS = TPI + kLfPad, NCG = long_fold_groups(D);
+  const int RS = D + 4;  // tile row stride (floats): 16-byte rows; LDS.128 of 8 consecutive rows hit distinct banks
+  float* tile = reinterpret_cast<float*>(smem_raw);                   // [2][SP][RS]
+  uint32_t* tgi = reinterpret_cast<uint32_t*>(tile + 2 * SP * RS);    // [2][SP] source row of each position
+  const int TPI = long_fold_tpi(D), PS = TPI + kLfPad;
   const int64_t stage_f = long_fold_stage_f(D);
+  const int NCG = long_fold_groups(D);
   const int64_t nm = mcount[0], npair = mcount[1] / NCG;  // (run, stage) pairs of the fitted runs
   const int cpr = D >> 2;
   for (int64_t q = blockIdx.x; q < npair; q += gridDim.x) {
@@ -506,29 +593,61 @@ static __global__ void __launch_bounds__(256) k_pack_rows(const LongRun* __restr
     const int64_t img0 = (int64_t)__ldg(moff + lo) + k;  // image of group g: img0 + g * per_group
     const int64_t j0 = (int64_t)run.jh + k * TPI;
     const int np = (int)((int64_t)run.je - j0 < TPI ? (int64_t)run.je - j0 : TPI);
-    for (int p0 = 0; p0 < np; p0 += SP) {
-      const int sp = np - p0 < SP ? np - p0 : SP;
-      __syncthreads();  // the previous sub-chunk has been written out
-      for (int t = threadIdx.x; t < sp * cpr; t += blockDim.x) {
-        const int p = t / cpr, c4 = t - p * cpr;
-        const uint32_t gi = __ldg(ridx + j0 + p0 + p);
-        float4 x = ldg4((gi == 0xFFFFFFFFu ? zrow : rows + (int64_t)gi * D) + c4 * 4);
-        if (mode == 1) {
-          const float l = (float)(__ldg(bag_offs + gi + 1) - __ldg(bag_offs + gi));
-          x = make_float4(__fdiv_rn(x.x, l), __fdiv_rn(x.y, l), __fdiv_rn(x.z, l), __fdiv_rn(x.w, l));
+    const int nsub = (np + SP - 1) / SP;
+    __syncthreads();  // the previous pair's last sub-chunk has been written out
+    auto issue = [&](int i) {  // cp.async of sub-chunk i into buffer i & 1
+      const int p0 = i * SP, sp = np - p0 < SP ? np - p0 : SP;
+      float* tb = tile + (i & 1) * SP * RS;
+      uint32_t* gb = tgi + (i & 1) * SP;
+      const int items = sp * cpr;
+      for (int t0 = threadIdx.x; t0 < items; t0 += 4 * blockDim.x) {
+        uint32_t gi[4];  // the four index loads in flight together
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int t = t0 + u * blockDim.x;
+          gi[u] = t < items ? __ldg(ridx + j0 + p0 + t / cpr) : 0u;
         }
-        float* dst = tile + p * (D + 1) + c4 * 4;
-        dst[0] = x.x;
-        dst[1] = x.y;
-        dst[2] = x.z;
-        dst[3] = x.w;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int t = t0 + u * blockDim.x;
+          if (t >= items) continue;
+          const int p = t / cpr, c4 = t - p * cpr;
+          if (c4 == 0) gb[p] = gi[u];
+          cp_async16(tb + p * RS + c4 * 4, (gi[u] == 0xFFFFFFFFu ? zrow : rows + (int64_t)gi[u] * D) + c4 * 4);
+        }
       }
-      __syncthreads();
-      for (int t = threadIdx.x; t < D * sp; t += blockDim.x) {
-        const int c = t / sp, p = t - c * sp;
-        const int g = c / kLfGW, cl = c - g * kLfGW;
-        images[(img0 + (int64_t)g * per_group) * stage_f + (int64_t)cl * PS + p0 + p] = tile[p * (D + 1) + c];
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    issue(0);
+    for (int i = 0; i < nsub; ++i) {
+      if (i + 1 < nsub) {
+        issue(i + 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
+      __syncthreads();  // sub-chunk i landed for every thread
+      const int p0 = i * SP, sp = np - p0 < SP ? np - p0 : SP;
+      const float* tb = tile + (i & 1) * SP * RS;
+      const uint32_t* gb = tgi + (i & 1) * SP;
+      // thread (position p, 4-column chunk c4): one LDS.128, four column
+      // stores — consecutive lanes take consecutive positions of one chunk,
+      // so each store instruction writes contiguous floats of one column
+      for (int t = threadIdx.x; t < sp * cpr; t += blockDim.x) {
+        const int c4 = t / sp, p = t - c4 * sp;
+        float4 x = *reinterpret_cast<const float4*>(tb + p * RS + c4 * 4);
+        if (mode == 1) {
+          const uint32_t gi = gb[p];
+          x = vdiv4(x, (float)(__ldg(bag_offs + gi + 1) - __ldg(bag_offs + gi)));
+        }
+        const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int c = c4 * 4 + e, g = c / kLfGW, cl = c - g * kLfGW;
+          images[(img0 + (int64_t)g * per_group) * stage_f + (int64_t)cl * PS + p0 + p] = xv[e];
+        }
+      }
+      __syncthreads();  // buffer i & 1 is refilled by issue(i + 2)
     }
   }
 }
@@ -546,7 +665,7 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
                              const float* rows, int D, const int64_t* bag_offs, int mode, AdamDev a, float* out,
                              int64_t* last_step, int64_t step, cudaStream_t s, const float* zrow = nullptr,
                              const LongFoldPack* pack = nullptr, bool expect_mega = true,
-                             int smem_budget = kLfSmemBudget) {
+                             int smem_budget = kLfSmemBudget, const RowOut& ro = RowOut{}) {
   if (D > 32 * kLfMaxNC * kLfCols) raise(SKB_E_UNSUPPORTED, D, "long-run fold: dim > %d", 32 * kLfMaxNC * kLfCols);
   const int nc = long_fold_consumers(D);
   static const int env_pw = getenv("SKB_LF_PW") ? atoi(getenv("SKB_LF_PW")) : 0;
@@ -563,16 +682,27 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
     set = sm;
   }
   const float* packed = nullptr;
+  bool direct = false;
+  // mega runs as column-group units: by default packed into stage images
+  // first (one TMA bulk copy per stage); SKB_LF_PACK=0: their producers
+  // gather the group's columns straight from the gradient rows instead (no
+  // pack pass, but a group CTA's random 32-byte gathers fall behind the
+  // chain: C4 5.25 vs 4.45 ms/step measured)
   static const bool env_pack = getenv("SKB_LF_PACK") ? atoi(getenv("SKB_LF_PACK")) != 0 : true;
-  // expect_mega: the caller saw long runs recently (else the two packing
-  // launches are skipped; mega runs then take the cp.async path, same result)
-  if (env_pack && expect_mega && pack && pack->images && pack->cap_runs >= cap) {
+  // expect_mega: the caller saw long runs recently (else the planning
+  // launches are skipped; mega runs then take the one-CTA path, same result)
+  if (!env_pack && expect_mega && pack && pack->mlist && pack->cap_runs >= cap) {
+    k_pack_plan<<<1, 1024, 0, s>>>(runs, nruns, cap, long_fold_tpg(D), long_fold_groups(D), mega_run_threshold(mode),
+                                   INT64_MAX / 4, pack->mlist, pack->moff, pack->mcount, pack->morder);
+    SKB_LAUNCH_CHECK();
+    direct = true;
+  } else if (env_pack && expect_mega && pack && pack->images && pack->cap_runs >= cap) {
     const int TPI = long_fold_tpi(D);
     k_pack_plan<<<1, 1024, 0, s>>>(runs, nruns, cap, TPI, long_fold_groups(D), mega_run_threshold(mode),
                                    pack->cap_images, pack->mlist, pack->moff, pack->mcount, pack->morder);
     SKB_LAUNCH_CHECK();
     const int sp = pack_sub(D);
-    const size_t psm = (size_t)sp * (D + 1) * sizeof(float);
+    const size_t psm = pack_smem(D);
     static size_t pset = 0;
     if (pset < psm && psm > 48 * 1024) {
       SKB_CUDA(cudaFuncSetAttribute(k_pack_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
@@ -587,9 +717,9 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
   if (grid < 1) grid = 1;
   k_long_fold<ADAM><<<(unsigned)grid, threads, sm, s>>>(runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out,
                                                         last_step, step, nst, zrow, packed,
-                                                        packed ? pack->mlist : nullptr,
-                                                        packed ? pack->morder : nullptr,
-                                                        packed ? pack->mcount : nullptr);
+                                                        (packed || direct) ? pack->mlist : nullptr,
+                                                        (packed || direct) ? pack->morder : nullptr,
+                                                        (packed || direct) ? pack->mcount : nullptr, ro, direct);
   SKB_LAUNCH_CHECK();
 }
 
@@ -610,10 +740,6 @@ inline int64_t long_fold_pack_images(int64_t rows, int D) {
 // <= kLongRun positions stay bit-exact.
 // ---------------------------------------------------------------------------
 constexpr int kTreeChunk = 256;
-
-__device__ __forceinline__ float4 vdiv4(float4 x, float l) {
-  return make_float4(__fdiv_rn(x.x, l), __fdiv_rn(x.y, l), __fdiv_rn(x.z, l), __fdiv_rn(x.w, l));
-}
 
 struct TreeWork {
   int64_t* chunk_off = nullptr;  // [cap + 1] first chunk of each run; [cap + ... ] total at [nruns]

@@ -25,16 +25,6 @@
 
 namespace skb {
 
-// segment of x in the ascending prefix array pre[0..S] (pre[S] = total)
-__device__ __forceinline__ int seg_of(const int64_t* __restrict__ pre, int S, int64_t x) {
-  int lo = 0, hi = S;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (__ldg(pre + mid) <= x) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
 // out row q (q-th id received, rank-ordered segments pre[j]..pre[j+1]) ->
 // peer window j at row base[j] + (q - pre[j]); source row = src[idx[q]] with
 // row stride sstride (arena rows through the slot list, or plain rows)
