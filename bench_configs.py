@@ -197,18 +197,22 @@ def c3(args):
     chunk = max(1, args.steps)
     t_start = time.perf_counter()
     while True:
-        e0, e1 = _events()
-        e0.record()
-        run(chunk)
-        e1.record()
+        # an event after every step: the slowest step of the chunk (a growth
+        # stall would show here, not only in the chunk's mean)
+        evs = [_events()[0] for _ in range(chunk + 1)]
+        evs[0].record()
+        for i in range(chunk):
+            run(1)
+            evs[i + 1].record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
+        steps_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(chunk)]
+        ms = sum(steps_ms)
         t_all += ms
         ids_all += chunk * n
         rows = lt.num_rows
         u, unew = skb.last_step_stats(lt)
-        curve.append({"rows": int(rows), "ms_per_step": ms / chunk, "ids_per_s": chunk * n / (ms / 1e3),
-                      "last_step_unique": u, "last_step_new": unew})
+        curve.append({"rows": int(rows), "ms_per_step": ms / chunk, "max_step_ms": max(steps_ms),
+                      "ids_per_s": chunk * n / (ms / 1e3), "last_step_unique": u, "last_step_new": unew})
         if rows >= target or time.perf_counter() - t_start > 240:
             break
     # steady state at the final size: same batches, new tails still admitted
@@ -243,11 +247,12 @@ def c3(args):
                          f"effective cores {cores}"}
     _line(args, "c3", n / (ms / 1e3), ms, n, Bn, sb, cpu,
           {"workload": "C3 per-GPU owner share: zipf(1.1) ids, 26 x dim16 merged namespaced table, batch "
-                       "65536, bag length 1, sum, SparseAdamW; table grown from empty (IDMap rehash + arena "
-                       "growth inside the timed steps)", "global_batch": Bn, "features": F, "dim": D,
+                       "65536, bag length 1, sum, SparseAdamW; table grown from empty inside the timed steps (IDMap "
+                       "sized from the capacity hint, row arena mapped copy-free as rows arrive)", "global_batch": Bn, "features": F, "dim": D,
            "target_rows": target, "parallelism": "single shard (one GPU's share of 8)",
            "l2": "inputs larger than L2 (table grows to GBs)"},
           {"growth_curve": curve, "table_rows": int(lt.num_rows), "growth_ids_per_s": ids_all / (t_all / 1e3),
+           "growth_max_step_ms": max(c["max_step_ms"] for c in curve),
            "unique_rows_per_step": u, "new_rows_per_step": unew})
 
 

@@ -359,10 +359,11 @@ int skb_ragged_pad_dense(const void* values, int64_t elem_bytes, int64_t width, 
 /* Kernel variant of the fused step, per table (tuning sweeps and tests):
  * adam 0 = auto (TMA ring <16,192,4> for sum batches of D >= 48 without
  * recent long runs, else the register kernel), 1-3 register shapes, 4-8 TMA
- * ring shapes; pool 0 = auto (staged one-hot gather when n == G), 1-4 forced;
- * -1 = the SKB_ADAM_VARIANT / SKB_POOL_VARIANT environment default.
+ * ring shapes; pool 0 = auto (staged one-hot gather when n == G, else the
+ * position-streaming kernel for 64 <= D <= 128), 1-5 forced register shapes
+ * / staged; -1 = the SKB_ADAM_VARIANT / SKB_POOL_VARIANT environment default.
  * last_variants: what the last backward / pool ran (adam 0 = TMA default,
- * -1 = generic-D kernel; pool -1 generic-D, 10 pairwise general). */
+ * -1 = generic-D kernel; pool -1 generic-D, 6 streaming, 10 pairwise general). */
 /* Fold mode of the fused backward's long runs (ids with > 32 positions in a
  * batch): 0 exact (default) — np.add.at's serial left fold, bit-exact with
  * sharding.py:283-290; 1 tree (opt-in tolerance mode) — chunks of 256

@@ -633,13 +633,106 @@ __device__ __forceinline__ void pool_chunk(const float* __restrict__ arena, cons
         acc[r] = vfill<VEC>(0.f);
         if (ok[r] && ee[r] > bb[r]) acc[r] = vadd<VEC>(acc[r], vload<VEC>(arena + (int64_t)ss[r] * D3 + c));
       }
+      // the rest of every bag, kPoolBatch positions at a time: all R bags'
+      // slot loads, then all their row loads, are in flight together before
+      // the adds (which stay in position order: the fold is bit-exact)
+      constexpr int kPoolBatch = R >= 4 ? 1 : 4 / R;  // R * kPoolBatch rows in flight per lane (no spills at MINB 4)
+      int64_t pr[R];
+      bool more = false;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        pr[r] = bb[r] + 1;
+        more |= ok[r] && pr[r] < ee[r];
+      }
+      while (more) {
+        uint32_t sl[R][kPoolBatch];
+        T v[R][kPoolBatch];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int u = 0; u < kPoolBatch; ++u)
+            sl[r][u] = (ok[r] && pr[r] + u < ee[r]) ? __ldg(slot + pr[r] + u) : 0xFFFFFFFFu;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int u = 0; u < kPoolBatch; ++u)
+            if (sl[r][u] != 0xFFFFFFFFu) v[r][u] = vload<VEC>(arena + (int64_t)sl[r][u] * D3 + c);
+        more = false;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+#pragma unroll
+          for (int u = 0; u < kPoolBatch; ++u)
+            if (sl[r][u] != 0xFFFFFFFFu) acc[r] = vadd<VEC>(acc[r], v[r][u]);
+          pr[r] += kPoolBatch;
+          more |= ok[r] && pr[r] < ee[r];
+        }
+      }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (!ok[r]) continue;
-        for (int64_t p = bb[r] + 1; p < ee[r]; ++p)
-          acc[r] = vadd<VEC>(acc[r], vload<VEC>(arena + (int64_t)__ldg(slot + p) * D3 + c));
         if (mode == 1 && ee[r] > bb[r]) acc[r] = vdiv<VEC>(acc[r], (float)(ee[r] - bb[r]));
         vstore<VEC>(out + (g0 + bi[r]) * D + c, acc[r]);
+      }
+    }
+  }
+}
+
+// Wide rows (one or two rows per warp instruction, D >= 64): a sub-group
+// owns a contiguous run of the chunk's bags, i.e. a contiguous range of
+// positions, and streams it K positions at a time — K slot loads, then K row
+// loads in flight, then the adds in position order, a bag's sum stored as
+// soon as its last position is added.  Bit-exact (same fold from +0, same
+// order); far more bytes in flight per warp than one bag at a time.
+template <int VEC, int K>
+__device__ __forceinline__ void pool_chunk_stream(const float* __restrict__ arena, const uint32_t* __restrict__ slot,
+                                                  int64_t g0, int nb, int64_t b, int64_t e, int lane, int mode,
+                                                  int D, int64_t D3, float* __restrict__ out, int64_t* s_e) {
+  using T = typename VecT<VEC>::T;
+  const int rowv = D / VEC;
+  const int L = rowv < 32 ? rowv : 32;
+  const int P = 32 / L;
+  const int sub = lane / L, sl = lane - sub * L;
+  const int per = (nb + P - 1) / P;
+  const int q0 = sub * per < nb ? sub * per : nb, q1 = q0 + per < nb ? q0 + per : nb;
+  __syncwarp();
+  if (lane < nb) s_e[lane] = e;
+  const int64_t bstart = __shfl_sync(0xffffffffu, b, q0 < 32 ? q0 : 31);
+  __syncwarp();
+  if (sub >= P || q0 >= q1) return;
+  const int64_t pend = s_e[q1 - 1];
+  for (int c = sl * VEC; c < D; c += L * VEC) {
+    int q = q0;
+    int64_t bq = bstart, eq = s_e[q];
+    while (q < q1 && eq == bq) {  // leading empty bags
+      vstore<VEC>(out + (g0 + q) * D + c, vfill<VEC>(0.f));
+      ++q;
+      eq = q < q1 ? s_e[q] : 0;
+    }
+    T acc = vfill<VEC>(0.f);
+    for (int64_t p = bstart; p < pend; p += K) {
+      uint32_t sv[K];
+      T v[K];
+#pragma unroll
+      for (int u = 0; u < K; ++u) sv[u] = p + u < pend ? __ldg(slot + p + u) : 0u;
+#pragma unroll
+      for (int u = 0; u < K; ++u)
+        if (p + u < pend) v[u] = vload<VEC>(arena + (int64_t)sv[u] * D3 + c);
+#pragma unroll
+      for (int u = 0; u < K; ++u) {
+        if (p + u >= pend) continue;
+        acc = vadd<VEC>(acc, v[u]);
+        if (p + u + 1 == eq) {  // bag q complete
+          vstore<VEC>(out + (g0 + q) * D + c, mode == 1 ? vdiv<VEC>(acc, (float)(eq - bq)) : acc);
+          acc = vfill<VEC>(0.f);
+          ++q;
+          bq = eq;
+          eq = q < q1 ? s_e[q] : 0;
+          while (q < q1 && eq == bq) {  // empty bags after it
+            vstore<VEC>(out + (g0 + q) * D + c, vfill<VEC>(0.f));
+            ++q;
+            eq = q < q1 ? s_e[q] : 0;
+          }
+        }
       }
     }
   }
@@ -665,6 +758,30 @@ __global__ void __launch_bounds__(256, MINB) k_fused_pool_scatter(const float* _
       if (e > b) s0 = __ldg(slot + b);
     }
     pool_chunk<VEC, R>(arena, slot, g0, nb, b, e, s0, lane, mode, D, stride, out);
+  }
+}
+
+// K6 for wide rows (VEC 4, 64 <= D <= 128): warps own chunks of 32 bags,
+// sub-groups stream their bags' positions (pool_chunk_stream)
+template <int K, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fused_pool_stream(const float* __restrict__ arena,
+                                                                 const uint32_t* __restrict__ slot,
+                                                                 const int64_t* __restrict__ bag_offs, int64_t G,
+                                                                 int mode, int D, int64_t stride,
+                                                                 float* __restrict__ out) {
+  __shared__ int64_t s_end[8][32];
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nchunks = (G + 31) / 32;
+  for (int64_t ch = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; ch < nchunks; ch += warps) {
+    const int64_t g0 = ch * 32;
+    const int nb = (int)(G - g0 < 32 ? G - g0 : 32);
+    int64_t b = 0, e = 0;
+    if (lane < nb) {
+      b = __ldg(bag_offs + g0 + lane);
+      e = __ldg(bag_offs + g0 + lane + 1);
+    }
+    pool_chunk_stream<4, K>(arena, slot, g0, nb, b, e, lane, mode, D, stride, out, s_end[threadIdx.x >> 5]);
   }
 }
 
@@ -1784,7 +1901,14 @@ static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStrea
           case 1: k_fused_pool_scatter<4, 1, 4><<<grid, 256, 0, s>>>(SKB_POOL_ARGS); break;
           case 2: k_fused_pool_scatter<4, 2, 1><<<grid, 256, 0, s>>>(SKB_POOL_ARGS); break;
           case 3: k_fused_pool_scatter<4, 4, 2><<<grid, 256, 0, s>>>(SKB_POOL_ARGS); break;
-          default: k_fused_pool_scatter<4, 2, 4><<<grid, 256, 0, s>>>(SKB_POOL_ARGS); break;
+          case 5: k_fused_pool_scatter<4, 2, 4><<<grid, 256, 0, s>>>(SKB_POOL_ARGS); break;
+          default:
+            if (D >= 64 && D <= 128) {  // wide rows: stream each sub-group's positions (C5: D=128 491 -> ? us)
+              c->last_pool = 6;
+              k_fused_pool_stream<8, 3><<<grid, 256, 0, s>>>(SKB_POOL_ARGS);
+            } else
+              k_fused_pool_scatter<4, 2, 4><<<grid, 256, 0, s>>>(SKB_POOL_ARGS);
+            break;
         }
 #undef SKB_POOL_ARGS
     } else if (v4) {
@@ -2099,7 +2223,7 @@ int skb_fused_set_fold_mode(skb_table_t h, int32_t mode) {
 
 int skb_fused_set_variants(skb_table_t h, int32_t adam_variant, int32_t pool_variant) {
   SKB_API_BEGIN
-  if (adam_variant > 8 || pool_variant > 4) raise(SKB_E_VALUE, 0, "adam variant must be <= 8, pool variant <= 4");
+  if (adam_variant > 8 || pool_variant > 5) raise(SKB_E_VALUE, 0, "adam variant must be <= 8, pool variant <= 5");
   FusedCtx* c = ctx_get(table_from(h));
   c->adam_var = adam_variant;
   c->pool_var = pool_variant;

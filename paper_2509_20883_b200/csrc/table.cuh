@@ -16,6 +16,8 @@
 //   counters  int64[4]                 {allocated, free_count, num_rows, seq}
 // Slot numbers are exactly the reference's offsets.
 #pragma once
+#include <thread>
+
 #include "common.cuh"
 #include "vmm.cuh"
 
@@ -48,6 +50,7 @@ struct Table {
   bool vmm = false;
   int64_t rows_hint = 0;  // capacity_hint: VA reserved for this many rows up front
   VmmArray va[6];         // arena, last_step, live, slot_key, ins_seq, free_list
+  std::thread va_prep;    // maps the next growth chunk of every array ahead of need
 
   HEntry* idmap = nullptr;
   int64_t idmap_cap = 0;

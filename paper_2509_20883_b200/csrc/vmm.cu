@@ -91,11 +91,38 @@ static void map_chunk(uint64_t va, size_t bytes, unsigned long long h) {
   check(A.access((CUdeviceptr)va, bytes, &d, 1), "cuMemSetAccess");
 }
 
+void vmm_prepare(VmmArray& a, size_t bytes, int device) {
+  Api& A = api();
+  if (!a.base || a.prep_bytes) return;
+  SKB_CUDA(cudaSetDevice(device));
+  const size_t g = vmm_granularity();
+  size_t add = round_up(bytes > 0 ? bytes : 1, g);
+  if (a.mapped + add > a.reserved) add = (a.reserved - a.mapped) / g * g;
+  if (!add) return;
+  CUmemAllocationProp p = prop_for_current();
+  CUmemGenericAllocationHandle h = 0;
+  if (A.create(&h, add, &p, 0) != CUDA_SUCCESS) {  // out of memory ahead of need: growth will retry (and raise)
+    cudaGetLastError();
+    return;
+  }
+  map_chunk(a.base + a.mapped, add, (unsigned long long)h);
+  a.prep_handle = (unsigned long long)h;
+  a.prep_bytes = add;
+}
+
 bool vmm_grow(VmmArray& a, size_t bytes, size_t reserve_hint, cudaStream_t s) {
   Api& A = api();
   const size_t g = vmm_granularity();
   const size_t want = round_up(bytes > 0 ? bytes : 1, g);
   if (want <= a.mapped) return false;
+  if (a.prep_bytes) {  // adopt the chunk prepared ahead: only the zero-fill is left
+    a.chunks.push_back(VmmArray::Chunk{a.prep_handle, a.mapped, a.prep_bytes});
+    SKB_CUDA(cudaMemsetAsync(reinterpret_cast<void*>(a.base + a.mapped), 0, a.prep_bytes, s));
+    a.mapped += a.prep_bytes;
+    a.prep_handle = 0;
+    a.prep_bytes = 0;
+    if (want <= a.mapped) return false;
+  }
   bool moved = false;
   if (want > a.reserved) {
     // (re)reserve: the requested hint, or 4x what is needed now
@@ -128,6 +155,10 @@ bool vmm_grow(VmmArray& a, size_t bytes, size_t reserve_hint, cudaStream_t s) {
 void vmm_free(VmmArray& a) {
   if (!a.base) return;
   Api& A = api();
+  if (a.prep_bytes) {
+    A.unmap((CUdeviceptr)(a.base + a.mapped), a.prep_bytes);
+    A.release((CUmemGenericAllocationHandle)a.prep_handle);
+  }
   for (const auto& c : a.chunks) {
     A.unmap((CUdeviceptr)(a.base + c.offset), c.bytes);
     A.release((CUmemGenericAllocationHandle)c.handle);

@@ -24,6 +24,10 @@ struct VmmArray {
     size_t offset, bytes;
   };
   std::vector<Chunk> chunks;
+  // a chunk created and mapped ahead of need at [mapped, mapped + prep_bytes)
+  // (by a background thread: growth then only zero-fills it on the stream)
+  unsigned long long prep_handle = 0;
+  size_t prep_bytes = 0;
 };
 
 // whether the driver exposes the VMM entry points (resolved once)
@@ -35,5 +39,11 @@ size_t vmm_granularity();
 // reserve this many times the needed bytes when (re)reserving VA.
 bool vmm_grow(VmmArray& a, size_t bytes, size_t reserve_hint, cudaStream_t s);
 void vmm_free(VmmArray& a);
+// Create and map (not zero) up to `bytes` more behind the mapped end, within
+// the reservation, for the next vmm_grow to adopt — the slow driver calls
+// (cuMemCreate / cuMemMap / cuMemSetAccess, ~0.3 ms per array) moved off the
+// step's host thread.  Safe from another thread while no vmm_grow / vmm_free
+// of the same array runs (the table joins its prepare thread before those).
+void vmm_prepare(VmmArray& a, size_t bytes, int device);
 
 }  // namespace skb

@@ -572,10 +572,21 @@ def test_fused_adam_variants_mean_hot(skb, variant):
                      check=_expect_adam(variant if variant else 2))
 
 
-@pytest.mark.parametrize("pool", [1, 2, 3, 4])
+@pytest.mark.parametrize("D,mode", [(64, "sum"), (64, "mean"), (96, "mean"), (128, "sum"), (128, "mean")])
+def test_fused_pool_stream(skb, D, mode):
+    """Default pool for wide rows (64 <= D <= 128, bags not all one-hot):
+    k_fused_pool_stream, sub-groups streaming their bags' positions in
+    batches — empty bags, long bags and chunk tails against the oracle."""
+    specs = [("a", 1000, lambda r, B: np.where(r.random(B) < 0.1, 0, r.geometric(0.25, B))),
+             ("b", 333, lambda r, B: r.integers(0, 13, B))]  # mean length < 16: every member pools with scatter
+    _fused_vs_oracle(skb, D, specs, steps=3, mode=mode, seed=90 + D,
+                     check=lambda step, lt: skb_last(lt)[1] == 6 or pytest.fail("stream pool"))
+
+
+@pytest.mark.parametrize("pool", [1, 2, 3, 4, 5])
 def test_fused_pool_variants(skb, pool):
-    """Forced pool kernels (1-3 register shapes, 4 staged one-hot gather with
-    its register fallback for mixed chunks) against the oracle."""
+    """Forced pool kernels (1-3 and 5 register shapes, 4 staged one-hot
+    gather with its register fallback for mixed chunks) against the oracle."""
     specs = [("a", 900, lambda r, B: np.where(r.random(B) < 0.8, 1, r.integers(0, 4, B)))]
     _fused_vs_oracle(skb, 64, specs, steps=3, mode="sum", seed=70 + pool, variants=(-1, pool),
                      check=lambda step, lt: skb_last(lt)[1] == pool or pytest.fail("pool variant"))
