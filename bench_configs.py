@@ -110,7 +110,9 @@ def c1(args):
     steps = max(args.steps, 200)  # ~50 us steps: time enough of them to amortise graph re-captures
     e0, e1 = _events()
     e0.record()
+    torch.cuda.nvtx.range_push("timed")
     run(steps)
+    torch.cuda.nvtx.range_pop()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
@@ -218,7 +220,9 @@ def c3(args):
     # steady state at the final size: same batches, new tails still admitted
     e0, e1 = _events()
     e0.record()
+    torch.cuda.nvtx.range_push("timed")
     run(args.steps)
+    torch.cuda.nvtx.range_pop()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
@@ -309,7 +313,9 @@ def c4(args):
         N.call("skb_fused_profile", lt.local_table.handle, args.steps, N.stream_ptr())
     e0, e1 = _events()
     e0.record()
+    torch.cuda.nvtx.range_push("timed")
     run(args.steps)
+    torch.cuda.nvtx.range_pop()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
@@ -536,8 +542,10 @@ def c5(args):
     e0, e1 = _events()
     with skb.deferred_checks():
         e0.record()
+        torch.cuda.nvtx.range_push("timed")
         w0 = time.perf_counter()
         run(args.steps)
+        torch.cuda.nvtx.range_pop()
         e1.record()
     torch.cuda.synchronize()
     wall = (time.perf_counter() - w0) / args.steps * 1e3
