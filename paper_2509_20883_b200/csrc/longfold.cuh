@@ -675,7 +675,17 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
   if (nst > long_fold_stages(D, smem_budget)) nst = long_fold_stages(D, smem_budget);
   if (npw > nst) npw = nst;  // a producer warp must never get a full ring lap ahead (parity waits)
   const int threads = 32 * (nc + npw);
-  const size_t sm = long_fold_smem(D, nst);
+  size_t sm = long_fold_smem(D, nst);
+  // SKB_LF_EXCLUSIVE=1: claim a whole SM's shared memory per CTA so no other
+  // kernel's blocks co-reside with a serial hot-id chain (issue-slot and L1
+  // contention stretch the ~4-cycle FADD chain)
+  static const int exclusive = getenv("SKB_LF_EXCLUSIVE") ? atoi(getenv("SKB_LF_EXCLUSIVE")) : 0;
+  if (exclusive) {
+    int dev = 0, optin = 0;
+    SKB_CUDA(cudaGetDevice(&dev));
+    SKB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if ((size_t)optin > sm) sm = (size_t)optin;
+  }
   static size_t set = 0;  // attribute raised to the largest size launched so far
   if (set < sm) {
     SKB_CUDA(cudaFuncSetAttribute(k_long_fold<ADAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));

@@ -19,7 +19,7 @@
 
 namespace skb {
 
-static std::atomic<int64_t> g_snap_waits{0}, g_refreshes{0};  // SKB_DEBUG_SYNC diagnostics
+static std::atomic<int64_t> g_snap_waits{0}, g_refreshes{0}, g_growths{0};  // SKB_DEBUG_SYNC diagnostics
 
 Table* table_from(skb_table_t h) {
   if (!h) raise(SKB_E_ARG, 0, "null table handle");
@@ -67,8 +67,13 @@ static void grow_arena_vmm(Table* t, int64_t new_rows, cudaStream_t s) {
   // the next growth step (1/8 of the rows) is created and mapped now on a
   // helper thread: the ~0.3 ms per array of driver calls leave the host
   // thread that feeds the step (measured: growth steps 2-3 ms vs 0.7 steady)
-  if (rows >= 65536) {
-    const int64_t inc = rows / 8;
+  size_t free_b = 0, total_b = 0;
+  SKB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  int64_t prep_bytes = 0;
+  for (int i = 0; i < 6; ++i) prep_bytes += (int64_t)esz[i] * (rows / 4);
+  // only with room to spare: a prepared chunk is memory held before it is needed
+  if (rows >= 65536 && (int64_t)free_b > 2 * prep_bytes + (8ll << 30)) {
+    const int64_t inc = rows / 4;  // the next geometric step
     const int dev = t->device;
     t->va_prep = std::thread([t, inc, dev, esz] {
       try {
@@ -81,6 +86,7 @@ static void grow_arena_vmm(Table* t, int64_t new_rows, cudaStream_t s) {
 
 static void grow_arena(Table* t, int64_t new_rows, cudaStream_t s) {
   if (new_rows <= t->arena_rows) return;
+  g_growths++;
   if (t->vmm) {
     grow_arena_vmm(t, new_rows, s);
     return;
@@ -179,24 +185,41 @@ bool table_needs_growth(Table* t, int64_t n) { return !bound_ok_after_snapshot(t
 
 void table_reserve(Table* t, int64_t n, cudaStream_t s) {
   if (t->vmm) {
-    // copy-free growth needs no exact counters: map more rows as soon as the
-    // no-sync upper bound comes within 1/8 of the arena, so the bound never
-    // fails and growth never drains the streams for a counter refresh
-    // The bound counts every enqueued position as a possible new row, so a
-    // host running many steps ahead would map memory for rows that never
-    // come: before growing, wait for the in-flight snapshot (one index
-    // phase behind the host, not a drain) and re-check with its counts.
-    // A few steps of slack (pending <= a quarter of the rows) is mapped
-    // without waiting: small tables / short steps keep the host ahead.
+    // Copy-free growth needs no exact counters: when the no-sync upper bound
+    // (every enqueued position a possible new row) passes the arena, map
+    // more rows — geometrically (1/4 of the arena, or the bound + 1/8), so
+    // a growing table maps O(log) chunks, each prepared ahead on a helper
+    // thread.  One exception: a large mapping (> 256 MB) for a table that
+    // is barely growing (its last snapshot interval admitted less than a
+    // quarter of the pending positions: a warm table whose bound is all
+    // hits) first waits for the in-flight snapshot — one index phase behind
+    // the host, not a drain — and re-checks with its counts, so a host
+    // running steps ahead never maps memory for rows that never come.
+    // A host more than 8 steps ahead of its last snapshot waits for that
+    // snapshot first (the device still has >= 8 steps queued, so this only
+    // throttles the host): the bound then never outruns the rows by more
+    // than 8 steps and a warm table settles on a fixed arena (C1: a host
+    // 200 graph-replayed steps ahead grew the arena ten times, 56 -> 105 us/step).
     harvest_snapshot(t);
-    int64_t ub = t->known[C_ALLOC] + t->pending_adds + n;
-    if (ub > t->arena_rows && t->snap_pending && t->pending_adds * 4 > t->known[C_ALLOC] + n) {
+    if (t->snap_pending && t->pending_adds > 8 * n) {
       g_snap_waits++;
       SKB_CUDA(cudaEventSynchronize(t->snap_ev));
       harvest_snapshot(t);
-      ub = t->known[C_ALLOC] + t->pending_adds + n;
     }
-    if (ub > t->arena_rows) grow_arena(t, std::max<int64_t>(ub + ub / 8, 1024), s);
+    int64_t ub = t->known[C_ALLOC] + t->pending_adds + n;
+    if (ub > t->arena_rows) {
+      const int64_t row_bytes = (int64_t)sizeof(float) * t->row_stride() + 4 * (int64_t)sizeof(int64_t) + 1;
+      const int64_t target = std::max<int64_t>(ub + ub / 8, t->arena_rows + t->arena_rows / 4);
+      const bool big = (target - t->arena_rows) * row_bytes > (256ll << 20);
+      if (big && t->snap_pending && t->recent_growth * 4 < t->pending_adds) {
+        g_snap_waits++;
+        SKB_CUDA(cudaEventSynchronize(t->snap_ev));
+        harvest_snapshot(t);
+        ub = t->known[C_ALLOC] + t->pending_adds + n;
+      }
+      if (ub > t->arena_rows)
+        grow_arena(t, std::max<int64_t>({ub + ub / 8, t->arena_rows + t->arena_rows / 4, (int64_t)1024}), s);
+    }
   }
   if (bound_ok_after_snapshot(t, n)) return;
   table_refresh(t, s);
@@ -1017,8 +1040,8 @@ int skb_table_destroy(skb_table_t h) {
   SKB_API_BEGIN
   Table* t = table_from(h);
   if (getenv("SKB_DEBUG_SYNC"))
-    fprintf(stderr, "[skb] snapshot waits %lld, counter refreshes %lld (all tables so far)\n",
-            (long long)g_snap_waits.load(), (long long)g_refreshes.load());
+    fprintf(stderr, "[skb] snapshot waits %lld, counter refreshes %lld, arena growths %lld (all tables so far)\n",
+            (long long)g_snap_waits.load(), (long long)g_refreshes.load(), (long long)g_growths.load());
   SKB_CUDA(cudaDeviceSynchronize());
   if (t->va_prep.joinable()) t->va_prep.join();
   if (t->vmm) {
