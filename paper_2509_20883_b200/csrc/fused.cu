@@ -97,6 +97,7 @@ struct FusedCtx {
   int64_t* lf_host = nullptr;   // pinned: long runs of a recent backward (async readback)
   cudaEvent_t lf_ev = nullptr;
   int64_t lf_last = 1;          // > 0: long runs seen recently (pack mega runs)
+  int64_t lf_maxlen = 0;        // longest run of a recent backward (exclusive long-fold SMs)
   cudaEvent_t ev_in = nullptr, ev_side_last = nullptr;
   // hot-id batches: the long-run fold runs on its own stream concurrently
   // with the main fold kernel (forked after the runs are listed, joined
@@ -210,8 +211,9 @@ static FusedCtx* ctx_get(Table* t) {
     }
     if (const char* g = getenv("SKB_FUSED_GRAPHS")) c->graphs = atoi(g) != 0;
     SKB_CUDA(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
-    SKB_CUDA(cudaMallocHost(&c->lf_host, sizeof(int64_t)));
-    *c->lf_host = 1;
+    SKB_CUDA(cudaMallocHost(&c->lf_host, 2 * sizeof(int64_t)));
+    c->lf_host[0] = 1;
+    c->lf_host[1] = 0;
     SKB_CUDA(cudaEventCreateWithFlags(&c->lf_ev, cudaEventDisableTiming));
     SKB_CUDA(cudaMalloc(&c->zrow, sizeof(float) * (t->dim + 4)));
     SKB_CUDA(cudaMemset(c->zrow, 0, sizeof(float) * (t->dim + 4)));
@@ -1972,7 +1974,10 @@ static void pack_reserve(FusedCtx* c, int64_t rows, int64_t runs, int D, cudaStr
     if (P.mlist) SKB_CUDA(cudaFree(P.mlist));
     if (P.moff) SKB_CUDA(cudaFree(P.moff));
     if (P.morder) SKB_CUDA(cudaFree(P.morder));
-    if (!P.mcount) SKB_CUDA(cudaMalloc(&P.mcount, sizeof(int64_t) * 2));
+    if (!P.mcount) {
+      SKB_CUDA(cudaMalloc(&P.mcount, sizeof(int64_t) * 3));
+      SKB_CUDA(cudaMemset(P.mcount, 0, sizeof(int64_t) * 3));
+    }
     SKB_CUDA(cudaMalloc(&P.mlist, sizeof(uint32_t) * runs));
     SKB_CUDA(cudaMalloc(&P.moff, sizeof(uint32_t) * runs));
     SKB_CUDA(cudaMalloc(&P.morder, sizeof(uint32_t) * runs));
@@ -2002,7 +2007,8 @@ static void long_pass(FusedCtx* c, BatchCtx& B, const float* dpooled, int D, int
                                 t->last_step, B.step, st, c->zrow, c->tw);
   else
     launch_long_fold<true>(B.longs, B.dev + 3, B.longs_cap, B.sval, dpooled, D, B.bag_offs, mode, a, t->arena,
-                           t->last_step, B.step, st, c->zrow, &c->pack, deep, budget);
+                           t->last_step, B.step, st, c->zrow, &c->pack, deep, budget, RowOut{},
+                           c->lf_maxlen >= kLfExclusiveRun);
 }
 
 static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc, cudaStream_t s,
@@ -2017,7 +2023,10 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     else pack_reserve(c, n, B.longs_cap, D, s);
   }
   // long runs seen by a recent backward (no sync: the last completed readback)
-  if (cudaEventQuery(c->lf_ev) == cudaSuccess) c->lf_last = *c->lf_host;
+  if (cudaEventQuery(c->lf_ev) == cudaSuccess) {
+    c->lf_last = c->lf_host[0];
+    c->lf_maxlen = c->lf_host[1];
+  }
   else cudaGetLastError();
   const bool deep = c->lf_last > 0;  // long runs recently: pack mega runs for TMA streaming
   const AdamDev a = to_dev(sc);
@@ -2106,7 +2115,7 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     int64_t* v = k.v;
     v[0] = t->gen; v[1] = B.gen; v[2] = (int64_t)dpooled; v[3] = n; v[4] = (int64_t)B.bag_offs; v[5] = B.G;
     v[6] = B.mode + (prescaled ? 8 : 0); v[7] = B.tile_k; v[8] = c->pack_gen;
-    v[9] = deep + (c->tree ? 2 : 0);  // deep also picks the fold kernel
+    v[9] = deep + (c->tree ? 2 : 0) + (c->lf_maxlen >= kLfExclusiveRun ? 4 : 0);  // deep also picks the fold kernel
     B.g_bwd.run(k, s, c->cap, B.step, &a, work);
   } else {
     work(s);
@@ -2114,6 +2123,8 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
   // sampled every 4th backward: a heuristic input, and small steps are launch-bound
   if (n > 0 && D % 4 == 0 && (c->bwd_count & 3) == 0 && cudaEventQuery(c->lf_ev) != cudaErrorNotReady) {
     SKB_CUDA(cudaMemcpyAsync(c->lf_host, B.dev + 3, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    if (c->pack.mcount)
+      SKB_CUDA(cudaMemcpyAsync(c->lf_host + 1, c->pack.mcount + 2, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     SKB_CUDA(cudaEventRecord(c->lf_ev, s));
   }
   cudaGetLastError();

@@ -100,6 +100,9 @@ __host__ __device__ inline int64_t long_fold_stage_f(int D) { return (int64_t)D 
 // are folded by ceil(D / kLfGW) CTAs in parallel, each streaming only its
 // columns (a 32-column group left the C4 hot run bound by one SM's stream).
 constexpr int kLfGW = 8;
+// a run this long (positions) keeps its column-group CTAs busy for >~0.5 ms:
+// the long fold then claims whole SMs (launch_long_fold `exclusive`)
+constexpr int64_t kLfExclusiveRun = 200000;
 __host__ __device__ inline int long_fold_groups(int D) { return (D + kLfGW - 1) / kLfGW; }
 // packed image of one column group (min(kLfGW, D) columns): the whole slot,
 // column-major with stride PS = TPI + kLfPad; TPI a multiple of 32 so PS is
@@ -455,7 +458,7 @@ struct LongFoldPack {
   int64_t cap_images = 0;
   uint32_t* mlist = nullptr;  // [cap_runs] run index of each mega run
   uint32_t* moff = nullptr;   // [cap_runs] first image of each mega run (ascending; kNoPack if it did not fit)
-  int64_t* mcount = nullptr;  // [2] mega runs, images in use
+  int64_t* mcount = nullptr;  // [3] mega runs, images in use, longest run (positions)
   int64_t cap_runs = 0;
   uint32_t* morder = nullptr; // [cap_runs] mega-list indices, longest run first
 };
@@ -472,17 +475,20 @@ static __global__ void __launch_bounds__(1024) k_pack_plan(LongRun* runs, const 
   __shared__ int64_t s_c[32], s_l[32];
   __shared__ int64_t s_cc, s_cl;
   __shared__ unsigned long long s_fit;  // images of the fitted runs (a prefix of the mega list)
+  __shared__ unsigned long long s_maxlen;  // longest run: mcount[2] (the host's hint for exclusive SMs)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
   const int64_t R = *nruns < cap ? *nruns : cap;
   if (threadIdx.x == 0) {
     s_cc = s_cl = 0;
     s_fit = 0;
+    s_maxlen = 0;
   }
   __syncthreads();
   for (int64_t b0 = 0; b0 < R; b0 += blockDim.x) {
     const int64_t r = b0 + threadIdx.x;
     int64_t len = 0;
     if (r < R) len = (int64_t)runs[r].je - runs[r].jh;
+    if (len > 0) atomicMax(&s_maxlen, (unsigned long long)len);
     const int64_t f = (r < R && len >= mega) ? 1 : 0, l = f ? NCG * ((len + TPI - 1) / TPI) : 0;
     int64_t ic = f, il = l;
     for (int o = 1; o < 32; o <<= 1) {
@@ -526,6 +532,7 @@ static __global__ void __launch_bounds__(1024) k_pack_plan(LongRun* runs, const 
   if (threadIdx.x == 0) {
     mcount[0] = s_cc;
     mcount[1] = (int64_t)s_fit;
+    mcount[2] = (int64_t)s_maxlen;
   }
   // longest-first order of the mega runs (rank by length, ties by list
   // position); beyond kSortMax mega runs: list order
@@ -665,7 +672,7 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
                              const float* rows, int D, const int64_t* bag_offs, int mode, AdamDev a, float* out,
                              int64_t* last_step, int64_t step, cudaStream_t s, const float* zrow = nullptr,
                              const LongFoldPack* pack = nullptr, bool expect_mega = true,
-                             int smem_budget = kLfSmemBudget, const RowOut& ro = RowOut{}) {
+                             int smem_budget = kLfSmemBudget, const RowOut& ro = RowOut{}, bool exclusive = false) {
   if (D > 32 * kLfMaxNC * kLfCols) raise(SKB_E_UNSUPPORTED, D, "long-run fold: dim > %d", 32 * kLfMaxNC * kLfCols);
   const int nc = long_fold_consumers(D);
   static const int env_pw = getenv("SKB_LF_PW") ? atoi(getenv("SKB_LF_PW")) : 0;
@@ -676,10 +683,14 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
   if (npw > nst) npw = nst;  // a producer warp must never get a full ring lap ahead (parity waits)
   const int threads = 32 * (nc + npw);
   size_t sm = long_fold_smem(D, nst);
-  // SKB_LF_EXCLUSIVE=1: claim a whole SM's shared memory per CTA so no other
-  // kernel's blocks co-reside with a serial hot-id chain (issue-slot and L1
-  // contention stretch the ~4-cycle FADD chain)
-  static const int exclusive = getenv("SKB_LF_EXCLUSIVE") ? atoi(getenv("SKB_LF_EXCLUSIVE")) : 0;
+  // exclusive: claim a whole SM's shared memory per CTA so no other kernel's
+  // blocks co-reside with a serial hot-id chain (issue-slot and L1
+  // contention stretch the ~4-cycle FADD chain).  The caller sets it when the
+  // longest run of a recent backward was long enough for the chain to bound
+  // the step (C4 4.26 -> 4.10 ms); with many short long runs (C5) it would
+  // only evict the main fold (6.7 -> 7.0-8.4 ms).  SKB_LF_EXCLUSIVE=0/1 forces.
+  static const int env_excl = getenv("SKB_LF_EXCLUSIVE") ? atoi(getenv("SKB_LF_EXCLUSIVE")) : -1;
+  if (env_excl >= 0) exclusive = env_excl != 0;
   if (exclusive) {
     int dev = 0, optin = 0;
     SKB_CUDA(cudaGetDevice(&dev));
