@@ -565,9 +565,13 @@ static __global__ void __launch_bounds__(1024) k_pack_plan(LongRun* runs, const 
 // column segments of all the run's column-group images at once (/ len for
 // mean bags) — every gradient byte is read once, every image byte written
 // once, and a block always has a sub-chunk of loads outstanding.
-inline int pack_sub(int D) {  // 64 positions (measured: 128 at D=64 was slower, 630 vs 537 us in C4)
-  const int sp = 9000 / (D + 4);
-  return sp > 64 ? 64 : (sp < 4 ? 4 : sp & ~3);
+// positions per sub-chunk: 64 for D >= 64 (128 at D=64 was slower in C4,
+// 630 vs 537 us); narrow rows take more per sub-chunk (4096 / D, up to 512:
+// a D=8 block otherwise walks its 512-position stage in 8 serial rounds)
+inline int pack_sub(int D) {
+  const int cap = 4096 / D > 64 ? (4096 / D > 512 ? 512 : 4096 / D) : 64;
+  const int sp = 9000 / (D + 4) > cap ? cap : 9000 / (D + 4);
+  return sp < 4 ? 4 : sp & ~3;
 }
 inline size_t pack_smem(int D) { return (size_t)2 * pack_sub(D) * ((D + 4) * sizeof(float) + sizeof(uint32_t)); }
 static __global__ void __launch_bounds__(256) k_pack_rows(const LongRun* __restrict__ runs,
