@@ -202,9 +202,12 @@ def c3(args):
         # an event after every step: the slowest step of the chunk (a growth
         # stall would show here, not only in the chunk's mean)
         evs = [_events()[0] for _ in range(chunk + 1)]
+        host_ms = []
         evs[0].record()
         for i in range(chunk):
+            h0 = time.perf_counter()
             run(1)
+            host_ms.append((time.perf_counter() - h0) * 1e3)
             evs[i + 1].record()
         torch.cuda.synchronize()
         steps_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(chunk)]
@@ -214,6 +217,7 @@ def c3(args):
         rows = lt.num_rows
         u, unew = skb.last_step_stats(lt)
         curve.append({"rows": int(rows), "ms_per_step": ms / chunk, "max_step_ms": max(steps_ms),
+                      "max_host_call_ms": max(host_ms),
                       "ids_per_s": chunk * n / (ms / 1e3), "last_step_unique": u, "last_step_new": unew})
         if rows >= target or time.perf_counter() - t_start > 240:
             break
