@@ -798,13 +798,15 @@ def test_fused_growth_under_async_snapshots(skb):
         eq(pooled[k], O.pool(O.lookup(olt, keys, k + 1), offs[0], "sum"))
 
 
+@pytest.mark.parametrize("D", [16, 64])
 @pytest.mark.parametrize("mode", ["sum", "mean"])
-def test_fused_graph_mode_equals_eager(skb, mode):
+def test_fused_graph_mode_equals_eager(skb, mode, D):
     """Graph-mode steps (capture on the 2nd call, replay with patched step /
     Adam scalars) leave bit-identical pooled rows and table state; table
-    growth and eviction between steps re-prime the graphs."""
+    growth and eviction between steps re-prime the graphs.  D=64 bags of 3
+    run the streaming pool kernel."""
     import torch
-    D, members, B = 16, ["a", "b"], 64
+    members, B = ["a", "b"], 64
     cfg = skb.AdamConfig(lr=1e-2, weight_decay=0.01, variant="adamw")
     rng = np.random.default_rng(8)
     specs = []
@@ -816,7 +818,7 @@ def test_fused_graph_mode_equals_eager(skb, mode):
         specs.append((ids, offs, rng.standard_normal((2 * B, D)).astype(np.float32)))
     outs = []
     for graphs in (False, True):
-        lt = skb.LogicalTable("dim16", D, 1, seed=4, members=members, namespaced=True, evict_threshold=3)
+        lt = skb.LogicalTable(f"dim{D}", D, 1, seed=4, members=members, namespaced=True, evict_threshold=3)
         skb.use_graphs(lt, graphs)
         # fixed device buffers refilled every step: the graph-replay contract
         bufs = [skb.PackedBatch(lt, members, specs[0][0], specs[0][1]) for _ in range(2)]
