@@ -104,8 +104,8 @@ static void dist_reserve(DistCtx* d, int64_t n, int F, cudaStream_t s) {
       grow_buf(d->pack.moff, d->lcap);
       grow_buf(d->pack.morder, d->lcap);
       if (!d->pack.mcount) {
-        SKB_CUDA(cudaMalloc(&d->pack.mcount, sizeof(int64_t) * 3));
-        SKB_CUDA(cudaMemset(d->pack.mcount, 0, sizeof(int64_t) * 3));
+        SKB_CUDA(cudaMalloc(&d->pack.mcount, sizeof(int64_t) * 4));
+        SKB_CUDA(cudaMemset(d->pack.mcount, 0, sizeof(int64_t) * 4));
       }
       d->pack.cap_runs = d->lcap;
     }

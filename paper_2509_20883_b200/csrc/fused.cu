@@ -176,6 +176,10 @@ void fused_ctx_destroy(FusedCtx* c) {
   cudaFree(c->pack.moff);
   cudaFree(c->pack.morder);
   cudaFree(c->pack.mcount);
+  cudaFree(c->pack.ready);
+  if (c->pack.pstream) cudaStreamDestroy(c->pack.pstream);
+  if (c->pack.ev_fork) cudaEventDestroy(c->pack.ev_fork);
+  if (c->pack.ev_join) cudaEventDestroy(c->pack.ev_join);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
   if (c->ev_side_last) cudaEventDestroy(c->ev_side_last);
   if (c->lf_stream) cudaStreamDestroy(c->lf_stream);
@@ -1643,7 +1647,7 @@ static void register_param_kernels() {
   note_param_kernel((const void*)k_fused_adam<4, 2, 4>, 17, 7, 10);
   note_param_kernel((const void*)k_fused_adam<4, 1, 5>, 17, 7, 10);
   note_param_kernel((const void*)k_fused_adam<4, 1, 4>, 17, 7, 10);
-  note_param_kernel((const void*)k_long_fold<true>, 20, 8, 11);  // (runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out, last_step, step, nst, zrow, packed, mlist, morder, mcount, ro, direct)
+  note_param_kernel((const void*)k_long_fold<true>, 21, 8, 11);  // (runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out, last_step, step, nst, zrow, packed, mlist, morder, mcount, ro, direct, ready)
 }
 
 // graph mode is off while per-phase event profiling is on (events cannot be
@@ -1969,14 +1973,26 @@ static void pack_reserve(FusedCtx* c, int64_t rows, int64_t runs, int D, cudaStr
     if (P.images) SKB_CUDA(cudaFree(P.images));
     SKB_CUDA(cudaMalloc(&P.images, sizeof(float) * imgs * long_fold_stage_f(D)));
     P.cap_images = imgs;
+    // per (run, stage) pair ready flags (epochs), zero = never written
+    if (P.ready) SKB_CUDA(cudaFree(P.ready));
+    const int64_t pairs = imgs / long_fold_groups(D) + 1;
+    SKB_CUDA(cudaMalloc(&P.ready, sizeof(uint32_t) * pairs));
+    SKB_CUDA(cudaMemset(P.ready, 0, sizeof(uint32_t) * pairs));
+  }
+  if (!P.pstream) {  // the pack's own stream: it runs beside the long fold (eager steps)
+    int lo = 0, hi = 0;
+    SKB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    SKB_CUDA(cudaStreamCreateWithPriority(&P.pstream, cudaStreamNonBlocking, hi));
+    SKB_CUDA(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming));
+    SKB_CUDA(cudaEventCreateWithFlags(&P.ev_join, cudaEventDisableTiming));
   }
   if (grow_runs) {
     if (P.mlist) SKB_CUDA(cudaFree(P.mlist));
     if (P.moff) SKB_CUDA(cudaFree(P.moff));
     if (P.morder) SKB_CUDA(cudaFree(P.morder));
     if (!P.mcount) {
-      SKB_CUDA(cudaMalloc(&P.mcount, sizeof(int64_t) * 3));
-      SKB_CUDA(cudaMemset(P.mcount, 0, sizeof(int64_t) * 3));
+      SKB_CUDA(cudaMalloc(&P.mcount, sizeof(int64_t) * 4));
+      SKB_CUDA(cudaMemset(P.mcount, 0, sizeof(int64_t) * 4));
     }
     SKB_CUDA(cudaMalloc(&P.mlist, sizeof(uint32_t) * runs));
     SKB_CUDA(cudaMalloc(&P.moff, sizeof(uint32_t) * runs));
@@ -2005,10 +2021,21 @@ static void long_pass(FusedCtx* c, BatchCtx& B, const float* dpooled, int D, int
   if (c->tree)
     launch_long_fold_tree<true>(B.longs, B.dev + 3, B.longs_cap, B.sval, dpooled, D, B.bag_offs, mode, a, t->arena,
                                 t->last_step, B.step, st, c->zrow, c->tw);
-  else
+  else {
+    // the pack runs beside the long fold (its own stream; the fold streams
+    // the images already packed and gathers the rest) only when a hot chain
+    // bounds the step — a recent longest run >= kLfExclusiveRun positions:
+    // C4 4.12 -> 3.83 ms; with many short mega runs (C5) the early direct
+    // gathers and the pack's high-priority blocks only slow the main fold
+    // (6.74 -> 7.34 ms).  Graph capture keeps the pack on the capturing stream.
+    LongFoldPack pk = c->pack;
+    static const int stream_pack = env_int("SKB_LF_STREAM_PACK", -1);
+    const bool hot = c->lf_maxlen >= kLfExclusiveRun;
+    if (graph_mode(c) || stream_pack == 0 || (stream_pack < 0 && !hot)) pk.pstream = nullptr;
     launch_long_fold<true>(B.longs, B.dev + 3, B.longs_cap, B.sval, dpooled, D, B.bag_offs, mode, a, t->arena,
-                           t->last_step, B.step, st, c->zrow, &c->pack, deep, budget, RowOut{},
+                           t->last_step, B.step, st, c->zrow, &pk, deep, budget, RowOut{},
                            c->lf_maxlen >= kLfExclusiveRun);
+  }
 }
 
 static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc, cudaStream_t s,

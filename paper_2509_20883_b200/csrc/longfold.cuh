@@ -160,6 +160,11 @@ __device__ __forceinline__ bool long_fold_unit(int64_t wu, int64_t MU, int NCG, 
   return !(grouped && run.pad != kNoPack);  // grouped runs were covered by their groups
 }
 
+// SKB_LF_MIX_TEST=1 (tests only): with streamed packs, treat every odd stage
+// as not yet packed, so one run mixes TMA image stages and gathered stages
+// deterministically
+__device__ int g_lf_mix_test = 0;
+
 template <bool ADAM>
 __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __restrict__ nruns, int64_t cap,
                             const uint32_t* __restrict__ ridx, const float* __restrict__ rows, int D,
@@ -167,8 +172,13 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
                             int64_t* __restrict__ last_step, int64_t step, int nst,
                             const float* __restrict__ zrow, const float* __restrict__ packed,
                             const uint32_t* __restrict__ mlist, const uint32_t* __restrict__ morder,
-                            const int64_t* __restrict__ mcount, RowOut ro = RowOut{}, bool direct = false) {
+                            const int64_t* __restrict__ mcount, RowOut ro = RowOut{}, bool direct = false,
+                            const uint32_t* __restrict__ ready = nullptr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  // stage layout (packed mode with ready flags): 0 = column-major image
+  // (TMA), 1 = row-major [positions][kLfGW] gathered directly because the
+  // pack had not reached that image yet
+  __shared__ int s_lay[kLfStages];
   const int TP = long_fold_tp(D);                // positions per row-major stage
   const int TPI = long_fold_tpi(D);              // positions per packed column-group image
   const int PS = TPI + kLfPad;                   // column stride of a packed image
@@ -187,6 +197,7 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
   // direct: mega runs are column-group units too, but their producers gather
   // the group's columns straight from the gradient rows (no packed images)
   const bool grouped = packed != nullptr || direct;
+  const uint32_t epoch = ready ? (uint32_t)mcount[3] : 0u;
   const int TPG = long_fold_tpg(D);  // positions per direct group stage ([TPG][kLfGW] row-major)
   const int64_t MU = grouped ? (mcount[0] < R ? mcount[0] : R) * NCG : 0;
   const int64_t units = MU + R;
@@ -267,9 +278,63 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
           __syncwarp();  // ix is rewritten by this warp's next stage
           continue;
         }
+        int gather = 0;  // packed mode: the pack has not written this image yet -> gather directly
+        if (img && ready) {
+          if (lane == 0) {
+            uint32_t f;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];"
+                         : "=r"(f) : "l"(ready + run.pad / NCG + (p0 - run.jh) / TPI) : "memory");
+            gather = f != epoch || (g_lf_mix_test && (((p0 - run.jh) / TPI) & 1));
+            if (!gather) asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA reads after the acquire
+          }
+          gather = __shfl_sync(0xffffffffu, gather, 0);
+        }
+        if (img && gather) {  // row-major [np][kLfGW] of this group's columns, 16-byte cp.async
+          const int cpg = ncol >> 2;
+          const int col0 = kLfGW * cg;
+          const int RS = long_fold_img_w(D);  // row stride: TPI rows of the group's columns fit the slot
+          uint32_t* ix = idx + pw * kLfMaxTP;
+          mbar_wait(&empty[s], ph ^ 1u);
+          if (lane == 0) s_lay[s] = 1;
+          for (int h0 = 0; h0 < np; h0 += kLfMaxTP) {  // index buffer holds kLfMaxTP positions
+            const int nh = np - h0 < kLfMaxTP ? np - h0 : kLfMaxTP;
+            __syncwarp();
+            {
+              uint32_t gi[kLfMaxTP / 32];
+#pragma unroll
+              for (int k = 0; k < kLfMaxTP / 32; ++k)
+                gi[k] = k * 32 + lane < nh ? __ldg(ridx + p0 + h0 + k * 32 + lane) : 0u;
+#pragma unroll
+              for (int k = 0; k < kLfMaxTP / 32; ++k)
+                if (k * 32 + lane < nh) ix[k * 32 + lane] = gi[k];
+            }
+            __syncwarp();
+            const int items = nh * cpg;
+            if (mode == 1) {
+              for (int i = lane; i < items; i += 32) {
+                const int row = i / cpg, ch = i - row * cpg;
+                const uint32_t gg = ix[row];
+                const float4 x = ldg4((gg == 0xFFFFFFFFu ? zrow : rows + (int64_t)gg * D) + col0 + ch * 4);
+                const float l = (float)(__ldg(bag_offs + gg + 1) - __ldg(bag_offs + gg));
+                st4(dst + (h0 + row) * RS + ch * 4, vdiv4(x, l));
+              }
+            } else {
+              for (int i = lane; i < items; i += 32) {
+                const int row = i / cpg, ch = i - row * cpg;
+                const uint32_t gg = ix[row];
+                cp_async16(dst + (h0 + row) * RS + ch * 4,
+                           (gg == 0xFFFFFFFFu ? zrow : rows + (int64_t)gg * D) + col0 + ch * 4);
+              }
+            }
+          }
+          if (mode == 1) mbar_arrive(&full[s]); else cp_async_arrive_noinc(&full[s]);
+          __syncwarp();
+          continue;
+        }
         if (img) {  // one bulk copy: this column group's image of TPI positions
           const uint32_t bytes = (uint32_t)ncol * (uint32_t)PS * 4u;
           mbar_wait(&empty[s], ph ^ 1u);
+          if (lane == 0) s_lay[s] = 0;
           if (lane == 0) {
             mbar_arrive_expect_tx(&full[s], bytes);
             const int64_t im = (int64_t)run.pad + (int64_t)cg * nimg + (p0 - run.jh) / TPI;
@@ -359,11 +424,12 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
       const uint32_t ph = (it / (uint32_t)nst) & 1u;
       const int np = (int)((int64_t)run.je - p0 < step_p ? (int64_t)run.je - p0 : step_p);
       mbar_wait(&full[s], ph);
-      if (img && !packed) {  // direct group stage: lane c folds column c, one position per LDS
+      if (img && (!packed || s_lay[s] == 1)) {  // direct group stage: lane c folds column c, one position per LDS
         if (warp == 0 && lane < ncol) {
           const float* src = buf + s * stage_f + lane;
+          const int rs = packed ? long_fold_img_w(D) : kLfGW;  // mixed stages: img_w-wide rows
 #pragma unroll 16
-          for (int p = 0; p < np; ++p) acc[0] = __fadd_rn(acc[0], src[p * kLfGW]);
+          for (int p = 0; p < np; ++p) acc[0] = __fadd_rn(acc[0], src[p * rs]);
         }
       } else if (img) {  // column-major image slice: four positions per 16-byte load,
                   // the next 16 positions' loads issued before this 16's adds
@@ -458,13 +524,21 @@ struct LongFoldPack {
   int64_t cap_images = 0;
   uint32_t* mlist = nullptr;  // [cap_runs] run index of each mega run
   uint32_t* moff = nullptr;   // [cap_runs] first image of each mega run (ascending; kNoPack if it did not fit)
-  int64_t* mcount = nullptr;  // [3] mega runs, images in use, longest run (positions)
+  int64_t* mcount = nullptr;  // [4] mega runs, images in use, longest run (positions), ready epoch
   int64_t cap_runs = 0;
   uint32_t* morder = nullptr; // [cap_runs] mega-list indices, longest run first
+  uint32_t* ready = nullptr;  // [cap_images / groups + 1] per (run, stage) pair: the epoch once its images are written
+  cudaStream_t pstream = nullptr;  // pack stream (eager steps): the pack runs beside the long fold
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
-// one block: exclusive scans of (is mega, stage images) over the run list;
-// run.pad = first image (kNoPack for ordinary runs or past capacity)
+// one block: the mega runs (>= `mega` positions) in list order -> mlist;
+// their longest-first order -> morder (rank by length, ties by list
+// position; beyond kSortMax mega runs: list order); stage images assigned in
+// morder order (so the hottest run's images come first and are packed first)
+// -> moff / run.pad (kNoPack past capacity); mcount = {mega runs, images in
+// use, longest run, epoch}: the epoch (bumped here) tags this pack's
+// per-pair ready flags
 static __global__ void __launch_bounds__(1024) k_pack_plan(LongRun* runs, const int64_t* __restrict__ nruns,
                                                            int64_t cap, int TPI, int NCG, int64_t mega,
                                                            int64_t cap_images,
@@ -472,71 +546,42 @@ static __global__ void __launch_bounds__(1024) k_pack_plan(LongRun* runs, const 
                                                            int64_t* __restrict__ mcount, uint32_t* __restrict__ morder) {
   constexpr int kSortMax = 2048;
   __shared__ uint32_t s_len[kSortMax];
-  __shared__ int64_t s_c[32], s_l[32];
-  __shared__ int64_t s_cc, s_cl;
-  __shared__ unsigned long long s_fit;  // images of the fitted runs (a prefix of the mega list)
+  __shared__ int64_t s_c[32];
+  __shared__ int64_t s_cc;
   __shared__ unsigned long long s_maxlen;  // longest run: mcount[2] (the host's hint for exclusive SMs)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
   const int64_t R = *nruns < cap ? *nruns : cap;
   if (threadIdx.x == 0) {
-    s_cc = s_cl = 0;
-    s_fit = 0;
+    s_cc = 0;
     s_maxlen = 0;
   }
   __syncthreads();
-  for (int64_t b0 = 0; b0 < R; b0 += blockDim.x) {
+  for (int64_t b0 = 0; b0 < R; b0 += blockDim.x) {  // compaction of the mega runs, list order
     const int64_t r = b0 + threadIdx.x;
     int64_t len = 0;
     if (r < R) len = (int64_t)runs[r].je - runs[r].jh;
     if (len > 0) atomicMax(&s_maxlen, (unsigned long long)len);
-    const int64_t f = (r < R && len >= mega) ? 1 : 0, l = f ? NCG * ((len + TPI - 1) / TPI) : 0;
-    int64_t ic = f, il = l;
+    const int64_t f = (r < R && len >= mega) ? 1 : 0;
+    int64_t ic = f;
     for (int o = 1; o < 32; o <<= 1) {
-      const int64_t yc = __shfl_up_sync(0xffffffffu, ic, o), yl = __shfl_up_sync(0xffffffffu, il, o);
-      if (lane >= o) {
-        ic += yc;
-        il += yl;
-      }
+      const int64_t yc = __shfl_up_sync(0xffffffffu, ic, o);
+      if (lane >= o) ic += yc;
     }
-    if (lane == 31) {
-      s_c[w] = ic;
-      s_l[w] = il;
-    }
+    if (lane == 31) s_c[w] = ic;
     __syncthreads();
-    int64_t bc = s_cc, bl = s_cl, tc = 0, tl = 0;
+    int64_t bc = s_cc, tc = 0;
     for (int q = 0; q < W; ++q) {
-      if (q < w) {
-        bc += s_c[q];
-        bl += s_l[q];
-      }
+      if (q < w) bc += s_c[q];
       tc += s_c[q];
-      tl += s_l[q];
     }
-    const int64_t xc = bc + ic - f, xl = bl + il - l;
     if (r < R) {
-      const bool fits = f && xl + l <= cap_images;
-      runs[r].pad = fits ? (uint32_t)xl : kNoPack;
-      if (fits) atomicMax(&s_fit, (unsigned long long)(xl + l));
-      if (f) {
-        mlist[xc] = (uint32_t)r;
-        moff[xc] = fits ? (uint32_t)xl : kNoPack;
-      }
+      runs[r].pad = kNoPack;
+      if (f) mlist[bc + ic - f] = (uint32_t)r;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      s_cc += tc;
-      s_cl += tl;
-    }
+    if (threadIdx.x == 0) s_cc += tc;
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    mcount[0] = s_cc;
-    mcount[1] = (int64_t)s_fit;
-    mcount[2] = (int64_t)s_maxlen;
-  }
-  // longest-first order of the mega runs (rank by length, ties by list
-  // position); beyond kSortMax mega runs: list order
-  __syncthreads();
   const int64_t M = s_cc;
   if (M <= kSortMax) {
     for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
@@ -555,6 +600,60 @@ static __global__ void __launch_bounds__(1024) k_pack_plan(LongRun* runs, const 
     }
   } else {
     for (int64_t i = threadIdx.x; i < M; i += blockDim.x) morder[i] = (uint32_t)i;
+  }
+  __threadfence_block();
+  __syncthreads();
+  // image offsets in morder order: exclusive scan of NCG * stages; a run fits
+  // while the running total stays within capacity (a prefix of morder)
+  __shared__ int64_t s_base;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  for (int64_t b0 = 0; b0 < M; b0 += blockDim.x) {
+    const int64_t rk = b0 + threadIdx.x;
+    int64_t l = 0, mi = 0;
+    if (rk < M) {
+      mi = morder[rk];
+      const LongRun ri = runs[mlist[mi]];
+      l = NCG * (((int64_t)ri.je - ri.jh + TPI - 1) / TPI);
+    }
+    int64_t il = l;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, il, o);
+      if (lane >= o) il += y;
+    }
+    if (lane == 31) s_c[w] = il;
+    __syncthreads();
+    int64_t bl = s_base, tl = 0;
+    for (int q = 0; q < W; ++q) {
+      if (q < w) bl += s_c[q];
+      tl += s_c[q];
+    }
+    if (rk < M) {
+      const int64_t xl = bl + il - l;
+      const bool fits = xl + l <= cap_images;
+      moff[mi] = fits ? (uint32_t)xl : kNoPack;
+      runs[mlist[mi]].pad = fits ? (uint32_t)xl : kNoPack;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base += tl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    mcount[0] = M;
+    mcount[1] = s_base <= cap_images ? s_base : 0;  // images in use (past capacity: the fitted prefix, below)
+    mcount[2] = (int64_t)s_maxlen;
+    mcount[3] += 1;  // epoch of this pack's ready flags
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && s_base > cap_images) {  // the fitted prefix ends before the first unfitted rank
+    int64_t used = 0;
+    for (int64_t rk = 0; rk < M; ++rk) {
+      const uint32_t o = moff[morder[rk]];
+      if (o == kNoPack) break;
+      const LongRun ri = runs[mlist[morder[rk]]];
+      used = (int64_t)o + NCG * (((int64_t)ri.je - ri.jh + TPI - 1) / TPI);
+    }
+    mcount[1] = used;
   }
 }
 
@@ -582,7 +681,9 @@ static __global__ void __launch_bounds__(256) k_pack_rows(const LongRun* __restr
                                                           const float* __restrict__ rows,
                                                           const float* __restrict__ zrow, int D,
                                                           const int64_t* __restrict__ bag_offs, int mode, int SP,
-                                                          float* __restrict__ images) {
+                                                          float* __restrict__ images,
+                                                          const uint32_t* __restrict__ morder,
+                                                          uint32_t* __restrict__ ready) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int RS = D + 4;  // tile row stride (floats): 16-byte rows; LDS.128 of 8 consecutive rows hit distinct banks
   float* tile = reinterpret_cast<float*>(smem_raw);                   // [2][SP][RS]
@@ -591,17 +692,21 @@ static __global__ void __launch_bounds__(256) k_pack_rows(const LongRun* __restr
   const int64_t stage_f = long_fold_stage_f(D);
   const int NCG = long_fold_groups(D);
   const int64_t nm = mcount[0], npair = mcount[1] / NCG;  // (run, stage) pairs of the fitted runs
+  const uint32_t epoch = (uint32_t)mcount[3];
   const int cpr = D >> 2;
+  // pairs in image order = morder order: the longest run's stages first, so
+  // a long fold streaming concurrently finds them ready soonest
   for (int64_t q = blockIdx.x; q < npair; q += gridDim.x) {
-    int64_t lo = 0, hi = nm;  // the mega run owning pair q (moff / NCG ascending; unfitted: kNoPack suffix)
+    int64_t lo = 0, hi = nm;  // rank owning pair q (moff[morder[.]] / NCG ascending; unfitted: kNoPack suffix)
     while (hi - lo > 1) {
       const int64_t mid = (lo + hi) >> 1;
-      if ((int64_t)__ldg(moff + mid) / NCG <= q) lo = mid; else hi = mid;
+      if ((int64_t)__ldg(moff + __ldg(morder + mid)) / NCG <= q) lo = mid; else hi = mid;
     }
-    const LongRun run = runs[__ldg(mlist + lo)];
+    const uint32_t mi = __ldg(morder + lo);
+    const LongRun run = runs[__ldg(mlist + mi)];
     const int64_t per_group = ((int64_t)run.je - run.jh + TPI - 1) / TPI;
-    const int64_t k = q - (int64_t)__ldg(moff + lo) / NCG;
-    const int64_t img0 = (int64_t)__ldg(moff + lo) + k;  // image of group g: img0 + g * per_group
+    const int64_t k = q - (int64_t)__ldg(moff + mi) / NCG;
+    const int64_t img0 = (int64_t)__ldg(moff + mi) + k;  // image of group g: img0 + g * per_group
     const int64_t j0 = (int64_t)run.jh + k * TPI;
     const int np = (int)((int64_t)run.je - j0 < TPI ? (int64_t)run.je - j0 : TPI);
     const int nsub = (np + SP - 1) / SP;
@@ -660,6 +765,10 @@ static __global__ void __launch_bounds__(256) k_pack_rows(const LongRun* __restr
       }
       __syncthreads();  // buffer i & 1 is refilled by issue(i + 2)
     }
+    if (ready && threadIdx.x == 0) {  // every group's image of pair q written (the barrier above)
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ready + q), "r"(epoch) : "memory");
+    }
   }
 }
 
@@ -699,7 +808,9 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
     int dev = 0, optin = 0;
     SKB_CUDA(cudaGetDevice(&dev));
     SKB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    if ((size_t)optin > sm) sm = (size_t)optin;
+    cudaFuncAttributes fa;
+    SKB_CUDA(cudaFuncGetAttributes(&fa, k_long_fold<ADAM>));
+    if ((size_t)optin - fa.sharedSizeBytes > sm) sm = (size_t)optin - fa.sharedSizeBytes;  // + static smem = the SM's all
   }
   static size_t set = 0;  // attribute raised to the largest size launched so far
   if (set < sm) {
@@ -707,6 +818,7 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
     set = sm;
   }
   const float* packed = nullptr;
+  const uint32_t* ready_flags = nullptr;
   bool direct = false;
   // mega runs as column-group units: by default packed into stage images
   // first (one TMA bulk copy per stage); SKB_LF_PACK=0: their producers
@@ -733,10 +845,29 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
       SKB_CUDA(cudaFuncSetAttribute(k_pack_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
       pset = psm;
     }
-    k_pack_rows<<<grid_for(pack->cap_images / long_fold_groups(D) * 256 + 256, 256, 4), 256, psm, s>>>(
-        runs, pack->mlist, pack->moff, pack->mcount, ridx, rows, zrow, D, bag_offs, mode, sp, pack->images);
+    // with a pack stream (eager steps) the pack runs beside the long fold:
+    // the fold streams every image the pack has already flagged and gathers
+    // the others itself, so the hottest chain starts at once instead of
+    // after the whole pack (C4: 0.54 ms off the critical path)
+    const bool fork = pack->pstream && pack->ready;
+    static bool mix_set = false;
+    if (fork && !mix_set) {
+      const int mix = getenv("SKB_LF_MIX_TEST") ? atoi(getenv("SKB_LF_MIX_TEST")) : 0;
+      SKB_CUDA(cudaMemcpyToSymbol(g_lf_mix_test, &mix, sizeof(int)));
+      mix_set = true;
+    }
+    cudaStream_t ps = s;
+    if (fork) {
+      SKB_CUDA(cudaEventRecord(pack->ev_fork, s));
+      SKB_CUDA(cudaStreamWaitEvent(pack->pstream, pack->ev_fork, 0));
+      ps = pack->pstream;
+    }
+    k_pack_rows<<<grid_for(pack->cap_images / long_fold_groups(D) * 256 + 256, 256, 4), 256, psm, ps>>>(
+        runs, pack->mlist, pack->moff, pack->mcount, ridx, rows, zrow, D, bag_offs, mode, sp, pack->images,
+        pack->morder, pack->ready);
     SKB_LAUNCH_CHECK();
     packed = pack->images;
+    ready_flags = fork ? pack->ready : nullptr;
   }
   int64_t grid = cap < (int64_t)sm_count() ? cap : (int64_t)sm_count();
   if (grid < 1) grid = 1;
@@ -744,8 +875,13 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
                                                         last_step, step, nst, zrow, packed,
                                                         (packed || direct) ? pack->mlist : nullptr,
                                                         (packed || direct) ? pack->morder : nullptr,
-                                                        (packed || direct) ? pack->mcount : nullptr, ro, direct);
+                                                        (packed || direct) ? pack->mcount : nullptr, ro, direct,
+                                                        ready_flags);
   SKB_LAUNCH_CHECK();
+  if (ready_flags) {  // later work on s (and the next pack plan) follows the pack
+    SKB_CUDA(cudaEventRecord(pack->ev_join, pack->pstream));
+    SKB_CUDA(cudaStreamWaitEvent(s, pack->ev_join, 0));
+  }
 }
 
 // stage images needed to pack up to `rows` positions of mega runs
