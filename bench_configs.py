@@ -296,12 +296,23 @@ def c4(args):
         tiles = torch.empty((G, L * D), device="cuda")
     plan = skb.ShardPlan(1)
 
+    pending = set()
+
     def run(count):
         for _ in range(count):
             step[0] += 1
             if fused:
-                skb.lookup_pool(lt, batches[step[0] % P], step[0], "tile", out=tiles, k=L, pad=0.0)
-                skb.pool_grad_adam(lt, dtile, cfg, step[0])
+                # cross-step pipeline: step k+1's index phase (probe,
+                # admission, sort of 8.2M positions) is issued before step
+                # k's backward and runs under its long fold
+                k = step[0]
+                if k not in pending:
+                    skb.prefetch(lt, batches[k % P], k, "tile", k=L, pad=0.0)
+                pending.discard(k)
+                skb.lookup_pool(lt, batches[k % P], k, "tile", out=tiles, k=L, pad=0.0)
+                skb.prefetch(lt, batches[(k + 1) % P], k + 1, "tile", k=L, pad=0.0)
+                pending.add(k + 1)
+                skb.pool_grad_adam(lt, dtile, cfg, k)
                 continue
             x = skb.RaggedTensor(ids[step[0] % P], offs_d).truncate(L, "tail")
             rows = skb.all_to_all_lookup(lt, x.values, plan, step[0])

@@ -177,6 +177,7 @@ void fused_ctx_destroy(FusedCtx* c) {
   cudaFree(c->pack.morder);
   cudaFree(c->pack.mcount);
   cudaFree(c->pack.ready);
+  cudaFree(c->pack.wctr);
   if (c->pack.pstream) cudaStreamDestroy(c->pack.pstream);
   if (c->pack.ev_fork) cudaEventDestroy(c->pack.ev_fork);
   if (c->pack.ev_join) cudaEventDestroy(c->pack.ev_join);
@@ -1647,7 +1648,7 @@ static void register_param_kernels() {
   note_param_kernel((const void*)k_fused_adam<4, 2, 4>, 17, 7, 10);
   note_param_kernel((const void*)k_fused_adam<4, 1, 5>, 17, 7, 10);
   note_param_kernel((const void*)k_fused_adam<4, 1, 4>, 17, 7, 10);
-  note_param_kernel((const void*)k_long_fold<true>, 21, 8, 11);  // (runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out, last_step, step, nst, zrow, packed, mlist, morder, mcount, ro, direct, ready)
+  note_param_kernel((const void*)k_long_fold<true>, 22, 8, 11);  // (runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out, last_step, step, nst, zrow, packed, mlist, morder, mcount, ro, direct, ready, wctr)
 }
 
 // graph mode is off while per-phase event profiling is on (events cannot be
@@ -1993,6 +1994,7 @@ static void pack_reserve(FusedCtx* c, int64_t rows, int64_t runs, int D, cudaStr
     if (!P.mcount) {
       SKB_CUDA(cudaMalloc(&P.mcount, sizeof(int64_t) * 4));
       SKB_CUDA(cudaMemset(P.mcount, 0, sizeof(int64_t) * 4));
+      SKB_CUDA(cudaMalloc(&P.wctr, sizeof(unsigned long long)));
     }
     SKB_CUDA(cudaMalloc(&P.mlist, sizeof(uint32_t) * runs));
     SKB_CUDA(cudaMalloc(&P.moff, sizeof(uint32_t) * runs));

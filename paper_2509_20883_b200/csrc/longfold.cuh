@@ -173,12 +173,20 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
                             const float* __restrict__ zrow, const float* __restrict__ packed,
                             const uint32_t* __restrict__ mlist, const uint32_t* __restrict__ morder,
                             const int64_t* __restrict__ mcount, RowOut ro = RowOut{}, bool direct = false,
-                            const uint32_t* __restrict__ ready = nullptr) {
+                            const uint32_t* __restrict__ ready = nullptr, unsigned long long* wctr = nullptr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // stage layout (packed mode with ready flags): 0 = column-major image
   // (TMA), 1 = row-major [positions][kLfGW] gathered directly because the
   // pack had not reached that image yet
   __shared__ int s_lay[kLfStages];
+  // dynamic unit scheduling (wctr): the k-th unit this CTA folds is fetched
+  // once, by the first producer warp, from the launch's counter and handed
+  // to every warp through a small ring — units are taken in walking order
+  // (the head id's column groups first), so the CTA that holds the longest
+  // chain takes nothing after it and short runs spread over the others
+  constexpr int kUnitRing = 64;
+  __shared__ long long s_wu[kUnitRing];
+  __shared__ int s_wseq[kUnitRing];
   const int TP = long_fold_tp(D);                // positions per row-major stage
   const int TPI = long_fold_tpi(D);              // positions per packed column-group image
   const int PS = TPI + kLfPad;                   // column stride of a packed image
@@ -209,12 +217,41 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  for (int i = threadIdx.x; i < kUnitRing; i += blockDim.x) s_wseq[i] = -1;
   __syncthreads();
+  // the unit of this CTA's k-th walk step (the same sequence in every warp);
+  // >= units ends the walk.  The fetcher skips units without work, so every
+  // ring entry holds at least one stage: no warp can fall a ring lap behind
+  // (the others trail the fetcher by at most the ring's nst stages)
+  auto unit_at = [&](int k) -> int64_t {
+    if (!wctr) return (int64_t)blockIdx.x + (int64_t)k * gridDim.x;
+    const int slot = k & (kUnitRing - 1);
+    if (warp == NC && lane == 0) {
+      long long u;
+      while (true) {
+        u = (long long)atomicAdd(wctr, 1ull);
+        if (u >= units) break;
+        int cg_;
+        LongRun r_;
+        bool im_;
+        if (long_fold_unit(u, MU, NCG, runs, mlist, morder, grouped, r_, cg_, im_)) break;
+      }
+      s_wu[slot] = u;
+      __threadfence_block();
+      *reinterpret_cast<volatile int*>(&s_wseq[slot]) = k;
+    }
+    while (*reinterpret_cast<volatile int*>(&s_wseq[slot]) != k) {
+    }
+    __threadfence_block();
+    return (int64_t)*reinterpret_cast<volatile long long*>(&s_wu[slot]);
+  };
   uint32_t it = 0;  // stage sequence number, identical in producers and consumers
   if (warp >= NC) {  // ---------------- producers: warp pw fills stages it = pw (mod NPW) ----------------
     const int pw = warp - NC, NPW = (int)(blockDim.x >> 5) - NC;
     const int cpr = D / 4;  // 16-byte chunks per row
-    for (int64_t wu = blockIdx.x; wu < units; wu += gridDim.x) {
+    for (int uk = 0;; ++uk) {
+      const int64_t wu = unit_at(uk);
+      if (wu >= units) break;
       int cg;
       LongRun run;
       bool img;
@@ -409,7 +446,9 @@ __global__ void k_long_fold(const LongRun* __restrict__ runs, const int64_t* __r
   // ceil(D/32) CTAs in parallel — each with its own serial chain per column
   const int c0 = warp * 32 + lane;
   const int cstep = 32 * NC;
-  for (int64_t wu = blockIdx.x; wu < units; wu += gridDim.x) {
+  for (int uk = 0;; ++uk) {
+    const int64_t wu = unit_at(uk);
+    if (wu >= units) break;
     int cg;
     LongRun run;
     bool img;
@@ -528,6 +567,7 @@ struct LongFoldPack {
   int64_t cap_runs = 0;
   uint32_t* morder = nullptr; // [cap_runs] mega-list indices, longest run first
   uint32_t* ready = nullptr;  // [cap_images / groups + 1] per (run, stage) pair: the epoch once its images are written
+  unsigned long long* wctr = nullptr;  // work-unit counter of one long-fold launch (dynamic unit scheduling)
   cudaStream_t pstream = nullptr;  // pack stream (eager steps): the pack runs beside the long fold
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
@@ -871,12 +911,13 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
   }
   int64_t grid = cap < (int64_t)sm_count() ? cap : (int64_t)sm_count();
   if (grid < 1) grid = 1;
+  if (pack && pack->wctr) SKB_CUDA(cudaMemsetAsync(pack->wctr, 0, sizeof(unsigned long long), s));
   k_long_fold<ADAM><<<(unsigned)grid, threads, sm, s>>>(runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out,
                                                         last_step, step, nst, zrow, packed,
                                                         (packed || direct) ? pack->mlist : nullptr,
                                                         (packed || direct) ? pack->morder : nullptr,
                                                         (packed || direct) ? pack->mcount : nullptr, ro, direct,
-                                                        ready_flags);
+                                                        ready_flags, pack ? pack->wctr : nullptr);
   SKB_LAUNCH_CHECK();
   if (ready_flags) {  // later work on s (and the next pack plan) follows the pack
     SKB_CUDA(cudaEventRecord(pack->ev_join, pack->pstream));
