@@ -713,7 +713,7 @@ inline int pack_sub(int D) {
   return sp < 4 ? 4 : sp & ~3;
 }
 inline size_t pack_smem(int D) { return (size_t)2 * pack_sub(D) * ((D + 4) * sizeof(float) + sizeof(uint32_t)); }
-static __global__ void __launch_bounds__(256) k_pack_rows(const LongRun* __restrict__ runs,
+static __global__ void __launch_bounds__(256, 5) k_pack_rows(const LongRun* __restrict__ runs,
                                                           const uint32_t* __restrict__ mlist,
                                                           const uint32_t* __restrict__ moff,
                                                           const int64_t* __restrict__ mcount,
@@ -842,7 +842,7 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
   // longest run of a recent backward was long enough for the chain to bound
   // the step (C4 4.26 -> 4.10 ms); with many short long runs (C5) it would
   // only evict the main fold (6.7 -> 7.0-8.4 ms).  SKB_LF_EXCLUSIVE=0/1 forces.
-  static const int env_excl = getenv("SKB_LF_EXCLUSIVE") ? atoi(getenv("SKB_LF_EXCLUSIVE")) : -1;
+  static const int env_excl = getenv("SKB_LF_EXCLUSIVE") ? atoi(getenv("SKB_LF_EXCLUSIVE")) : 0;
   if (env_excl >= 0) exclusive = env_excl != 0;
   if (exclusive) {
     int dev = 0, optin = 0;
@@ -855,6 +855,10 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
   static size_t set = 0;  // attribute raised to the largest size launched so far
   if (set < sm) {
     SKB_CUDA(cudaFuncSetAttribute(k_long_fold<ADAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    // an SM configures its shared-memory carveout for the blocks it holds:
+    // the maximum lets a pack block (or others) sit beside a long-fold CTA
+    static const int carve = getenv("SKB_LF_CARVEOUT") ? atoi(getenv("SKB_LF_CARVEOUT")) : 100;
+    SKB_CUDA(cudaFuncSetAttribute(k_long_fold<ADAM>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     set = sm;
   }
   const float* packed = nullptr;
@@ -909,7 +913,9 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
     packed = pack->images;
     ready_flags = fork ? pack->ready : nullptr;
   }
-  int64_t grid = cap < (int64_t)sm_count() ? cap : (int64_t)sm_count();
+  static const int64_t env_grid = getenv("SKB_LF_GRID") ? atoll(getenv("SKB_LF_GRID")) : 0;
+  const int64_t gmax = env_grid > 0 ? env_grid : (int64_t)sm_count();
+  int64_t grid = cap < gmax ? cap : gmax;
   if (grid < 1) grid = 1;
   if (pack && pack->wctr) SKB_CUDA(cudaMemsetAsync(pack->wctr, 0, sizeof(unsigned long long), s));
   k_long_fold<ADAM><<<(unsigned)grid, threads, sm, s>>>(runs, nruns, cap, ridx, rows, D, bag_offs, mode, a, out,
