@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import sys
 import threading
 
 import numpy as np
@@ -215,7 +216,7 @@ if os.environ.get("SKB_PROFILE_CALLS"):
     import collections
     import time as _time
 
-    _CALL_T = collections.defaultdict(lambda: [0, 0.0])
+    _CALL_T = collections.defaultdict(lambda: [0, 0.0, 0.0])
     _plain_call = call
 
     def call(name: str, *args) -> None:  # noqa: F811
@@ -224,13 +225,16 @@ if os.environ.get("SKB_PROFILE_CALLS"):
             _plain_call(name, *args)
         finally:
             rec = _CALL_T[name]
+            dt = _time.perf_counter() - t0
             rec[0] += 1
-            rec[1] += _time.perf_counter() - t0
+            rec[1] += dt
+            rec[2] = max(rec[2], dt)
 
     @atexit.register
     def _report_calls():
-        for k, (n, t) in sorted(_CALL_T.items(), key=lambda kv: -kv[1][1])[:20]:
-            print(f"[skb calls] {k:36s} {n:7d} calls {t * 1e3:10.2f} ms  {t / n * 1e6:8.1f} us/call")
+        for k, (n, t, mx) in sorted(_CALL_T.items(), key=lambda kv: -kv[1][1])[:20]:
+            print(f"[skb calls] {k:36s} {n:7d} calls {t * 1e3:10.2f} ms  {t / n * 1e6:8.1f} us/call  max {mx * 1e3:8.2f} ms",
+                  file=sys.stderr)
 
 
 # ---------------------------------------------------------------------------

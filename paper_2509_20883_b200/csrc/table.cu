@@ -72,7 +72,8 @@ static void grow_arena_vmm(Table* t, int64_t new_rows, cudaStream_t s) {
   int64_t prep_bytes = 0;
   for (int i = 0; i < 6; ++i) prep_bytes += (int64_t)esz[i] * (rows / 4);
   // only with room to spare: a prepared chunk is memory held before it is needed
-  if (rows >= 65536 && (int64_t)free_b > 2 * prep_bytes + (8ll << 30)) {
+  static const int prep_env = getenv("SKB_VMM_PREPARE") ? atoi(getenv("SKB_VMM_PREPARE")) : 1;
+  if (prep_env && rows >= 65536 && (int64_t)free_b > 2 * prep_bytes + (8ll << 30)) {
     const int64_t inc = rows / 4;  // the next geometric step
     const int dev = t->device;
     t->va_prep = std::thread([t, inc, dev, esz] {
@@ -1026,9 +1027,12 @@ int skb_table_create(int64_t dim, int64_t seed, int64_t block_size, int64_t evic
   int64_t rows = capacity_hint > 1024 ? capacity_hint : 1024;
   t->vmm = vmm_available();
   t->rows_hint = capacity_hint;
-  // VMM: VA for the hint is reserved now, memory is mapped as rows arrive;
-  // the IDMap is sized for the hint either way (no rehash while growing to it)
-  grow_arena(t, t->vmm ? 1024 : rows, s);
+  // The hint's rows are mapped (VMM) or allocated now: creating physical
+  // memory inside a step costs driver calls that can stall the process for
+  // 20-200 ms when the driver scrubs reused memory (C3 growth runs); past the
+  // hint the arena grows copy-free.  The IDMap is sized for the hint either
+  // way (no rehash while growing to it).
+  grow_arena(t, rows, s);
   rehash(t, next_pow2(rows * 2 > 2048 ? rows * 2 : 2048), s);
   SKB_CUDA(cudaStreamSynchronize(s));
   SKB_CUDA(cudaStreamDestroy(s));
