@@ -101,7 +101,7 @@ __host__ __device__ inline int64_t long_fold_stage_f(int D) { return (int64_t)D 
 // columns (a 32-column group left the C4 hot run bound by one SM's stream).
 constexpr int kLfGW = 8;
 // a run this long (positions) keeps its column-group CTAs busy for >~0.5 ms:
-// the long fold then claims whole SMs (launch_long_fold `exclusive`)
+// the long fold then runs as the step's critical path (launch_long_fold `hot_chain`)
 constexpr int64_t kLfExclusiveRun = 200000;
 __host__ __device__ inline int long_fold_groups(int D) { return (D + kLfGW - 1) / kLfGW; }
 // packed image of one column group (min(kLfGW, D) columns): the whole slot,
@@ -825,7 +825,7 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
                              const float* rows, int D, const int64_t* bag_offs, int mode, AdamDev a, float* out,
                              int64_t* last_step, int64_t step, cudaStream_t s, const float* zrow = nullptr,
                              const LongFoldPack* pack = nullptr, bool expect_mega = true,
-                             int smem_budget = kLfSmemBudget, const RowOut& ro = RowOut{}, bool exclusive = false) {
+                             int smem_budget = kLfSmemBudget, const RowOut& ro = RowOut{}, bool hot_chain = false) {
   if (D > 32 * kLfMaxNC * kLfCols) raise(SKB_E_UNSUPPORTED, D, "long-run fold: dim > %d", 32 * kLfMaxNC * kLfCols);
   const int nc = long_fold_consumers(D);
   static const int env_pw = getenv("SKB_LF_PW") ? atoi(getenv("SKB_LF_PW")) : 0;
@@ -836,15 +836,18 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
   if (npw > nst) npw = nst;  // a producer warp must never get a full ring lap ahead (parity waits)
   const int threads = 32 * (nc + npw);
   size_t sm = long_fold_smem(D, nst);
-  // exclusive: claim a whole SM's shared memory per CTA so no other kernel's
-  // blocks co-reside with a serial hot-id chain (issue-slot and L1
-  // contention stretch the ~4-cycle FADD chain).  The caller sets it when the
-  // longest run of a recent backward was long enough for the chain to bound
-  // the step (C4 4.26 -> 4.10 ms); with many short long runs (C5) it would
-  // only evict the main fold (6.7 -> 7.0-8.4 ms).  SKB_LF_EXCLUSIVE=0/1 forces.
+  // hot_chain (the caller saw a run >= kLfExclusiveRun positions recently:
+  // the chain bounds the step):
+  //  - the kernel asks for the maximum shared-memory carveout: an SM keeps
+  //    the carveout of the blocks it holds, and the maximum leaves room for
+  //    pack / index blocks beside a long-fold CTA (C4 3.26 -> 3.08 ms; on C5,
+  //    without a hot chain, it cost 1%: off there);
+  //  - SKB_LF_EXCLUSIVE=1 additionally claims a whole SM per CTA (no
+  //    co-resident blocks on a chain's SM; measured neutral to slightly worse
+  //    once units are scheduled dynamically, so off by default); 2 claims it
+  //    for every launch (tests).
   static const int env_excl = getenv("SKB_LF_EXCLUSIVE") ? atoi(getenv("SKB_LF_EXCLUSIVE")) : 0;
-  if (env_excl >= 0) exclusive = env_excl != 0;
-  if (exclusive) {
+  if ((env_excl == 1 && hot_chain) || env_excl > 1) {
     int dev = 0, optin = 0;
     SKB_CUDA(cudaGetDevice(&dev));
     SKB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -855,11 +858,16 @@ inline void launch_long_fold(LongRun* runs, const int64_t* nruns, int64_t cap, c
   static size_t set = 0;  // attribute raised to the largest size launched so far
   if (set < sm) {
     SKB_CUDA(cudaFuncSetAttribute(k_long_fold<ADAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    // an SM configures its shared-memory carveout for the blocks it holds:
-    // the maximum lets a pack block (or others) sit beside a long-fold CTA
-    static const int carve = getenv("SKB_LF_CARVEOUT") ? atoi(getenv("SKB_LF_CARVEOUT")) : 100;
-    SKB_CUDA(cudaFuncSetAttribute(k_long_fold<ADAM>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     set = sm;
+  }
+  {
+    static const int env_carve = getenv("SKB_LF_CARVEOUT") ? atoi(getenv("SKB_LF_CARVEOUT")) : -2;
+    const int want = env_carve != -2 ? env_carve : (hot_chain ? 100 : -1);
+    static int cur = -1;  // cudaSharedmemCarveoutDefault
+    if (want != cur) {
+      SKB_CUDA(cudaFuncSetAttribute(k_long_fold<ADAM>, cudaFuncAttributePreferredSharedMemoryCarveout, want));
+      cur = want;
+    }
   }
   const float* packed = nullptr;
   const uint32_t* ready_flags = nullptr;

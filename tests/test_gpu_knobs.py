@@ -4,7 +4,8 @@ the oracle with the same driver as test_gpu_parity._fused_vs_oracle:
 
 - SKB_LF_PACK=0: mega runs folded by column-group units whose producers
   gather the group's columns straight from the gradient rows (no pack pass);
-- SKB_LF_EXCLUSIVE=1 / 0: the long fold claiming whole SMs or not;
+- SKB_LF_EXCLUSIVE=2 / SKB_LF_CARVEOUT=100: the long fold claiming whole
+  SMs, or the maximum shared-memory carveout, on every launch;
 - SKB_POOL_VARIANT=5: the register pool shape that is not the default any more;
 - SKB_LF_STREAM_PACK=1 (+ SKB_LF_MIX_TEST=1): the pack on its own stream
   beside the long fold, whose producers stream the images already flagged
@@ -40,10 +41,10 @@ print("ok")
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", [{"SKB_LF_PACK": "0"}, {"SKB_LF_EXCLUSIVE": "1"}, {"SKB_LF_EXCLUSIVE": "0"},
+@pytest.mark.parametrize("env", [{"SKB_LF_PACK": "0"}, {"SKB_LF_EXCLUSIVE": "2"}, {"SKB_LF_CARVEOUT": "100"},
                                  {"SKB_POOL_VARIANT": "5"},
                                  {"SKB_LF_STREAM_PACK": "1", "SKB_LF_MIX_TEST": "1"},
-                                 {"SKB_LF_STREAM_PACK": "1", "SKB_LF_EXCLUSIVE": "1"}])
+                                 {"SKB_LF_STREAM_PACK": "1", "SKB_LF_EXCLUSIVE": "2"}])
 def test_knob_paths_vs_oracle(cuda, env):
     e = dict(os.environ)
     e.update(env)
