@@ -637,10 +637,18 @@ def run_dist(args):
     step_no = [0]
 
     def run(count):
+        # cross-step pipeline: step k+1's requester prepare + count exchange
+        # are enqueued between forward(k) and backward(k); the count readback
+        # (the step's one host sync) happens in forward(k+1), under backward(k)
         for k in range(count):
             step_no[0] += 1
-            stepper.forward(batches[k % P], step_no[0], "sum", out=pooled)
-            stepper.backward(dps[k % P], cfg, step_no[0])
+            t = step_no[0]
+            if stepper._pre is None:
+                stepper.prefetch(batches[t % P], t)
+            stepper.forward(batches[t % P], t, "sum", out=pooled)
+            if k + 1 < count:
+                stepper.prefetch(batches[(t + 1) % P], t + 1)
+            stepper.backward(dps[t % P], cfg, t)
 
     clk = ClockSampler(local).__enter__()
     run(args.warmup)
@@ -772,8 +780,13 @@ def run_threads(args):
                 def run(count):
                     for k in range(count):
                         step_no[0] += 1
-                        stepper.forward(batches[k % P], step_no[0], "sum", out=pooled)
-                        stepper.backward(dps[k % P], cfg, step_no[0])
+                        t = step_no[0]
+                        if stepper._pre is None:
+                            stepper.prefetch(batches[t % P], t)
+                        stepper.forward(batches[t % P], t, "sum", out=pooled)
+                        if k + 1 < count:
+                            stepper.prefetch(batches[(t + 1) % P], t + 1)
+                        stepper.backward(dps[t % P], cfg, t)
 
                 run(args.warmup)
                 st.synchronize()

@@ -404,11 +404,22 @@ class DistSparseStep:
         self.lt = lt
         self.comm = comm or Comm(lt.group)
         self.S, self.me, self.D = self.comm.size, self.comm.rank, lt.dim
-        h = C.c_void_p()
-        N.call("skb_dist_create", self.D, self.S, C.byref(h))
-        self.h = h
+        # two requester contexts (dedup / split / sort buffers), used by
+        # alternate steps, so step k+1's prepare can run (prefetch) while
+        # step k's backward still reads step k's
+        self.hs = []
+        for _ in range(2):
+            h = C.c_void_p()
+            N.call("skb_dist_create", self.D, self.S, C.byref(h))
+            self.hs.append(h)
+        self.h = self.hs[0]
+        self._next = 0  # context of the next prepare
+        self._free = [None, None]  # event after the backward that last read each context
+        self._pre = None  # prefetched (batch, step, context, plan)
+        self._side = None  # stream of prefetched prepares
         self.win = P2PWindows(self.comm)
-        self.counts = torch.zeros(self.S, dtype=torch.int64, device="cuda")
+        self.counts_h = [torch.zeros(self.S, dtype=torch.int64, device="cuda") for _ in range(2)]
+        self.counts = self.counts_h[0]
         # stream-ordered peer-memory barriers when the driver has stream memory
         # operations (every B200 driver): then the step needs no collective at
         # all — counts all-gathered by P2P stores, one readback of the matrix
@@ -416,11 +427,14 @@ class DistSparseStep:
         N.call("skb_p2p_memops_supported", C.byref(ok))
         self.p2p_sync = bool(ok.value) and os.environ.get("SKB_DIST_BARRIER", "p2p") == "p2p"
         self.epoch = 0
+        self.epoch2 = 0  # barrier channel of prefetched count exchanges (own flag words)
         if self.p2p_sync:
             S = self.S
             self.win.ensure("flags", [S] * S, 8)
+            self.win.ensure("flags2", [S] * S, 8)
             self.win.ensure("cmat", [S * S] * S, 8)
             self._flag_ptrs = (C.c_int64 * S)(*self.win.peers_dev["flags"].cpu().tolist())
+            self._flag_ptrs2 = (C.c_int64 * S)(*self.win.peers_dev["flags2"].cpu().tolist())
         self.cmat_host = torch.zeros(self.S * self.S, dtype=torch.int64).pin_memory()
         self.cmat_dev = torch.zeros(self.S * self.S, dtype=torch.int64, device="cuda")
         self.syncs = 0  # host synchronisations of the step path (the count matrix readback)
@@ -431,14 +445,16 @@ class DistSparseStep:
 
     def __del__(self):
         try:
-            if getattr(self, "h", None):
-                N.lib().skb_dist_destroy(self.h)
-                self.h = None
+            for h in getattr(self, "hs", []):
+                N.lib().skb_dist_destroy(h)
+            self.hs = []
         except Exception:
             pass
 
-    def _barrier(self):
-        """Order every rank's prior peer stores before any rank's later reads."""
+    def _barrier(self, channel: int = 1):
+        """Order every rank's prior peer stores before any rank's later reads
+        (channel 2: the prefetched count exchange, own flag words and epoch,
+        so it can run on a side stream while channel-1 barriers are pending)."""
         if self.comm.backend == "local":
             # ranks are threads of one process: every stream waits on events the
             # others have ALREADY recorded — a wait on a not-yet-enqueued peer
@@ -454,40 +470,55 @@ class DistSparseStep:
                 if j != self.me:
                     cur.wait_event(e)
         elif self.p2p_sync:
-            self.epoch += 1
-            N.call("skb_p2p_barrier", self._flag_ptrs, self.S, self.me, self.epoch, N.stream_ptr())
+            if channel == 2:
+                self.epoch2 += 1
+                N.call("skb_p2p_barrier", self._flag_ptrs2, self.S, self.me, self.epoch2, N.stream_ptr())
+            else:
+                self.epoch += 1
+                N.call("skb_p2p_barrier", self._flag_ptrs, self.S, self.me, self.epoch, N.stream_ptr())
         else:
             self.comm.barrier_after_device_writes()
 
-    def _count_matrix(self):
+    def _count_matrix(self, channel: int = 1, defer: bool = False, counts=None):
         """C[q][j] for all ranks: every rank stores its counts into row `rank`
         of each peer's count window, barrier, one readback (the step's host
-        synchronisation).  Without stream memory operations: an all-gather."""
+        synchronisation).  Without stream memory operations: an all-gather.
+        defer (peer-memory path): enqueue the readback and return an event;
+        `_matrix()` reads it once the event has completed."""
         self.syncs += 1
+        counts = self.counts if counts is None else counts
         if self.p2p_sync:
             import torch
             sp = N.stream_ptr()
-            N.call("skb_p2p_put_counts", N.ptr(self.counts), self.S, self.me, self.win.peers("cmat"), sp)
-            self._barrier()
+            N.call("skb_p2p_put_counts", N.ptr(counts), self.S, self.me, self.win.peers("cmat"), sp)
+            self._barrier(channel)
             N.call("skb_memcpy_async", self.cmat_host.data_ptr(), self.win.ptr("cmat"), 8 * self.S * self.S, sp)
+            if defer:
+                ev = torch.cuda.Event()
+                ev.record()
+                return ev
             torch.cuda.current_stream().synchronize()
-            flat = self.cmat_host.tolist()
-        elif self.comm.backend == "nccl":
-            self.comm.dist.all_gather_into_tensor(self.cmat_dev, self.counts, group=self.comm.group)
+            return self._matrix()
+        if self.comm.backend == "nccl":
+            self.comm.dist.all_gather_into_tensor(self.cmat_dev, counts, group=self.comm.group)
             flat = self.cmat_dev.cpu().tolist()
         else:
             import torch
             out = [torch.empty(self.S, dtype=torch.int64) for _ in range(self.S)]
-            self.comm.dist.all_gather(out, self.counts.cpu(), group=self.comm.group)
+            self.comm.dist.all_gather(out, counts.cpu(), group=self.comm.group)
             flat = [int(x) for t in out for x in t.tolist()]
         return [flat[q * self.S:(q + 1) * self.S] for q in range(self.S)]
 
-    def forward(self, batch, step: int, mode: str = "mean", out=None):
+    def _matrix(self):
+        flat = self.cmat_host.tolist()
+        return [flat[q * self.S:(q + 1) * self.S] for q in range(self.S)]
+
+    def _prepare(self, batch, channel: int, defer: bool = False):
+        """Requester prepare of `batch` into the next context + the count
+        exchange (the step's one host synchronisation) on the current stream;
+        returns (context index, count matrix, or the readback's event when
+        deferred)."""
         import ctypes as C
-        from .fused import _MODES
-        if mode not in ("sum", "mean"):
-            raise ValueError(f"unknown mode {mode!r} (the multi-GPU step pools with sum or mean)")
-        lt, S, D = self.lt, self.S, self.D
         F = len(batch.members)
         if batch._c_args is None:
             batch._c_args = ((C.c_int64 * (F + 1))(*batch.member_pos.tolist()),
@@ -495,10 +526,65 @@ class DistSparseStep:
                              (C.c_int64 * (F + 1))(*batch.member_bag.tolist()),
                              (C.c_int32 * max(F, 1))(*batch.strategy.tolist()))
         mp, sl, mb, st = batch._c_args
+        ci = self._next
+        self._next ^= 1
+        counts = self.counts_h[ci]
+        N.call("skb_dist_prepare", self.hs[ci], N.ptr(batch.ids), batch.num_ids, mp, sl, F,
+               1 if batch.namespaced else 0, N.ptr(batch.bag_offs), batch.num_bags, mb, st, N.ptr(counts),
+               N.stream_ptr())
+        return ci, self._count_matrix(channel, defer, counts)
+
+    def prefetch(self, batch, step: int) -> None:
+        """Prepare step `step`'s batch now (cross-step pipeline, like the
+        single-GPU `prefetch`): issue it between forward(k) and backward(k) for
+        step k+1.  The dedup / split / sort and the count exchange are only
+        enqueued (on a side stream, after the work already queued on the
+        caller's stream — forward(k) — and after the backward that last used
+        the context); the host reads the count matrix in forward(k+1), by when
+        backward(k) keeps the GPU busy.  Every rank must call it at the same
+        point of its step sequence."""
+        import torch
+        if self._pre is not None:
+            raise ValueError("a prefetched batch is already pending")
+        if self._side is None:
+            lo, hi = torch.cuda.Stream.priority_range()
+            self._side = torch.cuda.Stream(priority=hi)
+        cur = torch.cuda.current_stream()
+        side = self._side
+        side.wait_stream(cur)  # the batch's ids / offsets are ready
+        ev = self._free[self._next]
+        if ev is not None:
+            side.wait_event(ev)  # the backward that last read this context
+        with torch.cuda.stream(side):
+            ci, cm = self._prepare(batch, 2, defer=True)
+            done = torch.cuda.Event()
+            done.record(side)
+        self._pre = (batch, int(step), ci, cm, done)
+
+    def forward(self, batch, step: int, mode: str = "mean", out=None):
+        from .fused import _MODES
+        import torch
+        if mode not in ("sum", "mean"):
+            raise ValueError(f"unknown mode {mode!r} (the multi-GPU step pools with sum or mean)")
+        lt, S, D = self.lt, self.S, self.D
+        if self._pre is not None:
+            pb, pstep, ci, cm, done = self._pre
+            if pb is not batch or pstep != int(step):
+                raise ValueError("forward of a different batch / step than the pending prefetch")
+            self._pre = None
+            if isinstance(cm, torch.cuda.Event):
+                cm.synchronize()  # the step's one host synchronisation
+                cm = self._matrix()
+            torch.cuda.current_stream().wait_event(done)
+        else:
+            ev = self._free[self._next]
+            if ev is not None:
+                torch.cuda.current_stream().wait_event(ev)
+            ci, cm = self._prepare(batch, 1)
+        plan = ExchangePlan(cm, self.me)
+        self._ci = ci  # the context this step's pool and backward read
+        self.h, self.counts = self.hs[ci], self.counts_h[ci]
         sp = N.stream_ptr()
-        N.call("skb_dist_prepare", self.h, N.ptr(batch.ids), batch.num_ids, mp, sl, F, 1 if batch.namespaced else 0,
-               N.ptr(batch.bag_offs), batch.num_bags, mb, st, N.ptr(self.counts), sp)
-        plan = ExchangePlan(self._count_matrix(), self.me)
         self.win.ensure("ids", plan.recv_need, 8)
         self.win.ensure("grads", plan.recv_need, 4 * D)
         self.win.ensure("rows", plan.rows_need, 4 * D)
@@ -525,8 +611,12 @@ class DistSparseStep:
         plan, meta = self.plan, self._meta
         g = N.to_dev(dpooled, "float32")
         sp = N.stream_ptr()
-        N.call("skb_dist_fold_send", self.h, N.ptr(g), self._mode, plan.U, N.ptr(meta[0]), self.win.peers("grads"),
-               N.ptr(meta[1]), sp)
+        N.call("skb_dist_fold_send", self.hs[self._ci], N.ptr(g), self._mode, plan.U, N.ptr(meta[0]),
+               self.win.peers("grads"), N.ptr(meta[1]), sp)
+        import torch
+        ev = torch.cuda.Event()
+        ev.record()
+        self._free[self._ci] = ev  # this context may be prepared again after here
         self._barrier()
         sc = adam_scalars(cfg, step)
         N.call("skb_fused_backward", self.lt.local_table.handle, self.win.ptr("grads"), C.byref(sc), sp)

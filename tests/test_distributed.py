@@ -176,7 +176,21 @@ def fused_inputs(rank, k):
     return ids, offs, dp
 
 
-def _fused_worker(rank, port, out_dir, barrier="p2p"):
+def _fused_steps(skb, stepper, lt, rank, cfg, prefetch, sink):
+    """STEPS fused steps; prefetch: step k+1's prepare + count exchange issued
+    between forward(k) and backward(k) (the cross-step pipeline)."""
+    batches = [skb.PackedBatch(lt, MEMBERS, *fused_inputs(rank, k)[:2]) for k in range(STEPS)]
+    if prefetch:
+        stepper.prefetch(batches[0], 1)
+    for k in range(STEPS):
+        dp = fused_inputs(rank, k)[2]
+        sink(k, stepper.forward(batches[k], k + 1, "mean").cpu().numpy())
+        if prefetch and k + 1 < STEPS:
+            stepper.prefetch(batches[k + 1], k + 2)
+        stepper.backward(torch.from_numpy(dp).cuda(), cfg, k + 1)
+
+
+def _fused_worker(rank, port, out_dir, barrier="p2p", prefetch=False):
     import torch.distributed as dist
     os.environ["SKB_DIST_BARRIER"] = barrier
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -189,11 +203,7 @@ def _fused_worker(rank, port, out_dir, barrier="p2p"):
     stepper = DistSparseStep(lt)
     cfg = skb.AdamConfig(lr=LR, weight_decay=0.01, variant="adamw")
     pooled = []
-    for k in range(STEPS):
-        ids, offs, dp = fused_inputs(rank, k)
-        batch = skb.PackedBatch(lt, MEMBERS, ids, offs)
-        pooled.append(stepper.forward(batch, k + 1, "mean").cpu().numpy())
-        stepper.backward(torch.from_numpy(dp).cuda(), cfg, k + 1)
+    _fused_steps(skb, stepper, lt, rank, cfg, prefetch, lambda k, x: pooled.append(x))
     ex = lt.local_table.export_rows()
     np.savez(os.path.join(out_dir, f"fused{rank}.npz"), *pooled, ids=ex[0], w=ex[1], m=ex[2], v=ex[3])
     np.save(os.path.join(out_dir, f"grows{rank}.npy"), np.array([stepper.win.grows, stepper.syncs, stepper.p2p_sync]))
@@ -203,12 +213,14 @@ def _fused_worker(rank, port, out_dir, barrier="p2p"):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("prefetch", [False, True])
 @pytest.mark.parametrize("barrier", ["p2p", "comm"])
-def test_dist_sparse_step_gpu(tmp_path, cuda, barrier):
+def test_dist_sparse_step_gpu(tmp_path, cuda, barrier, prefetch):
     """Fused multi-GPU step (2 ranks on one GPU) vs the oracle train.py
     pipeline fed the rank-ordered concatenated batch with S = 2; ordering by
-    stream-ordered peer-memory barriers (default) or process-group barriers."""
-    mp.spawn(_fused_worker, args=(_free_port(), str(tmp_path), barrier), nprocs=S, join=True)
+    stream-ordered peer-memory barriers (default) or process-group barriers;
+    with and without the cross-step prefetch."""
+    mp.spawn(_fused_worker, args=(_free_port(), str(tmp_path), barrier, prefetch), nprocs=S, join=True)
     for r in range(S):
         grows, syncs, p2p = np.load(os.path.join(tmp_path, f"grows{r}.npy")).tolist()
         assert syncs == STEPS                      # one host sync per step: the count matrix
@@ -250,8 +262,9 @@ def _check_fused_vs_oracle(W, load):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("prefetch", [False, True])
 @pytest.mark.parametrize("W", [2, 3])
-def test_dist_sparse_step_thread_ranks(cuda, W):
+def test_dist_sparse_step_thread_ranks(cuda, W, prefetch):
     """The multi-GPU protocol with W ranks as threads of one process on one
     GPU (ThreadRanks: plain-pointer windows, stream-ordered peer barriers,
     every rank on its own stream) vs the oracle."""
@@ -272,11 +285,7 @@ def test_dist_sparse_step_thread_ranks(cuda, W):
                 assert stepper.p2p_sync
                 cfg = skb.AdamConfig(lr=LR, weight_decay=0.01, variant="adamw")
                 res = {}
-                for k in range(STEPS):
-                    ids, offs, dp = fused_inputs(rank, k)
-                    batch = skb.PackedBatch(lt, MEMBERS, ids, offs)
-                    res[f"arr_{k}"] = stepper.forward(batch, k + 1, "mean").cpu().numpy()
-                    stepper.backward(torch.from_numpy(dp).cuda(), cfg, k + 1)
+                _fused_steps(skb, stepper, lt, rank, cfg, prefetch, lambda k, x: res.__setitem__(f"arr_{k}", x))
                 ex = lt.local_table.export_rows()
                 res.update(ids=ex[0], w=ex[1], m=ex[2], v=ex[3])
                 assert stepper.syncs == STEPS
@@ -336,7 +345,7 @@ def test_dist_sparse_step_one_host_sync(tmp_path, cuda):
     mp.spawn(_fused_worker, args=(_free_port(), str(tmp_path)), nprocs=S, join=True)
     for r in range(S):
         grows = int(np.load(os.path.join(tmp_path, f"grows{r}.npy"))[0])
-        assert grows <= 8, grows  # flags + counts once; 3 data windows created once, grown once for the 30x step
+        assert grows <= 9, grows  # 2 flag windows + counts once; 3 data windows created once, grown once for the 30x step
 
 
 @pytest.mark.gpu
