@@ -2388,7 +2388,10 @@ void pool_by_index(const float* rows, int64_t stride, const uint32_t* idx, const
   const bool v4 = D % 4 == 0 && stride % 4 == 0 && (uintptr_t)out % 16 == 0 && (uintptr_t)rows % 16 == 0;
   if (!any_sequential) {
     const unsigned grid = grid_for(((G + 31) / 32) * 32, 256, 8);
-    if (v4)
+    static const int stream_env = env_int("SKB_POOL_BY_INDEX_STREAM", 1);
+    if (v4 && stream_env && D >= 64 && D <= 128)  // wide rows: stream positions (as the fused pool)
+      k_fused_pool_stream<8, 3><<<grid, 256, 0, s>>>(rows, idx, bag_offs, G, mode, D, stride, out);
+    else if (v4)
       k_fused_pool_scatter<4, 2, 4><<<grid, 256, 0, s>>>(rows, idx, bag_offs, G, mode, D, stride, out);
     else
       k_fused_pool_scatter<1, 1, 4><<<grid, 256, 0, s>>>(rows, idx, bag_offs, G, mode, D, stride, out);
@@ -2414,6 +2417,12 @@ void fold_sorted(int64_t n, const uint32_t* skey, const uint32_t* sval, const in
   // peer windows (ro) hold D-float rows at 16-byte aligned bases
   const bool v4 = D % 4 == 0 && (uintptr_t)dpooled % 16 == 0 && (uintptr_t)out % 16 == 0;
   if (v4) {
+    static const int fold_r = env_int("SKB_FOLD_ONLY_R", 2);  // rows per sub-group in flight (fold-only kernel)
+    if (fold_r == 2)
+      k_fused_adam<4, 2, 4, false><<<(unsigned)((chunks + 7) / 8), 256, 0, s>>>(
+          n, skey, sval, bag_offs, dpooled, mode, D, none, out, nullptr, -1, w.cnt, w.longs, w.cnt + 1, w.lcap,
+          nullptr, ro);
+    else
     k_fused_adam<4, 1, 4, false><<<(unsigned)((chunks + 7) / 8), 256, 0, s>>>(
         n, skey, sval, bag_offs, dpooled, mode, D, none, out, nullptr, -1, w.cnt, w.longs, w.cnt + 1, w.lcap,
         nullptr, ro);
