@@ -116,6 +116,7 @@ def c1(args):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
+    B.maybe_trace("c1", lambda: run(20))
     u, unew = skb.last_step_stats(lt)
     sb = B.step_bytes(Bn, Bn, u, unew, D)
 

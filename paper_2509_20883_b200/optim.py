@@ -40,16 +40,33 @@ class AdamConfig:
         return cls(**d)
 
 
+_SCALARS = {}
+
+
 def adam_scalars(cfg: AdamConfig, t: int) -> N.AdamScalars:
-    """float32 scalars of optim.py:69-75 (bias corrections via Python double pow)."""
-    f = np.float32
-    lr, b1, b2 = f(cfg.lr), f(cfg.beta1), f(cfg.beta2)
-    return N.AdamScalars(
-        lr=lr, beta1=b1, beta2=b2, eps=f(cfg.eps),
-        one_minus_beta1=f(f(1.0) - b1), one_minus_beta2=f(f(1.0) - b2),
-        bc1=f(1.0 - cfg.beta1 ** t), bc2=f(1.0 - cfg.beta2 ** t),
-        lr_wd=f(lr * f(cfg.weight_decay)),
-        decoupled_decay=1 if (cfg.variant == "adamw" and cfg.weight_decay != 0.0) else 0)
+    """float32 scalars of optim.py:69-75 (bias corrections via Python double pow).
+
+    The step-independent ones are computed once per configuration with numpy
+    float32 arithmetic; per call only bc1 / bc2 = float32(1 - beta**t) are
+    set — the double result rounded to float32 by the c_float field, the same
+    single rounding as np.float32(...) (the launch-bound C1 step calls this
+    every step; a dozen numpy scalar ops cost ~15 us)."""
+    key = (cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, cfg.variant)
+    base = _SCALARS.get(key)
+    if base is None:
+        f = np.float32
+        lr, b1, b2 = f(cfg.lr), f(cfg.beta1), f(cfg.beta2)
+        base = N.AdamScalars(
+            lr=lr, beta1=b1, beta2=b2, eps=f(cfg.eps),
+            one_minus_beta1=f(f(1.0) - b1), one_minus_beta2=f(f(1.0) - b2), bc1=0.0, bc2=0.0,
+            lr_wd=f(lr * f(cfg.weight_decay)),
+            decoupled_decay=1 if (cfg.variant == "adamw" and cfg.weight_decay != 0.0) else 0)
+        if len(_SCALARS) < 64:
+            _SCALARS[key] = base
+    sc = N.AdamScalars.from_buffer_copy(base)
+    sc.bc1 = 1.0 - cfg.beta1 ** t
+    sc.bc2 = 1.0 - cfg.beta2 ** t
+    return sc
 
 
 def sparse_adam_step(store, offsets, grads, cfg: AdamConfig, t: int) -> None:
