@@ -576,6 +576,9 @@ def run_ours(args):
             "kernels_ms": phase_ms,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "IDs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 32,
+                    "note": "each step's ids + bag offsets copied H2D from pinned host memory (copy stream, two "
+                            "steps ahead) and the step's stats D2H; pooled / dpooled stay on the device (the "
+                            "dense tower runs on the GPU)",
                     "h2d_ms_per_step": h2d_ms},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
