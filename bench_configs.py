@@ -531,6 +531,7 @@ def c5(args):
         return out
 
     pending = {}
+    side = torch.cuda.Stream()
 
     def run(count):
         # cross-step pipeline: step k's forward AND backward are enqueued first
@@ -558,10 +559,20 @@ def c5(args):
                 per[dd] = (batch.num_ids, batch.num_bags)
             for dd in DIMS5:
                 skb.pool_grad_adam(lts[dd], grads[(dd, cur[dd].num_bags)], cfg, k)
-            pending[k + 1] = build(k + 1)
-            for dd in DIMS5:
-                skb.prefetch(lts[dd], pending[k + 1][dd], k + 1, "mean")
+            # step k+1's feature engine and packed batches depend only on its
+            # inputs: on a side stream they run under step k's backward instead
+            # of queueing behind it (the prefetch orders itself after them)
+            main = torch.cuda.current_stream()
+            with torch.cuda.stream(side):
+                nxt = build(k + 1)
+                for b in nxt.values():  # read later on the compute stream
+                    b.ids.record_stream(main)
+                    b.bag_offs.record_stream(main)
+                for dd in DIMS5:
+                    skb.prefetch(lts[dd], nxt[dd], k + 1, "mean")
+            pending[k + 1] = nxt
             stats["per"] = per
+        torch.cuda.current_stream().wait_stream(side)  # the last step's build counts in the timed region
 
     # the feature engine's data checks (bucketize NaN) are read once per run
     # instead of once per call: no host synchronisation inside a step
