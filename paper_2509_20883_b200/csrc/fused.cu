@@ -1912,7 +1912,8 @@ static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStrea
           case 3: k_fused_pool_scatter<4, 4, 2><<<grid, 256, 0, s>>>(SKB_POOL_ARGS); break;
           case 5: k_fused_pool_scatter<4, 2, 4><<<grid, 256, 0, s>>>(SKB_POOL_ARGS); break;
           default:
-            if (D >= 64 && D <= 128) {  // wide rows: stream each sub-group's positions (C5: D=128 491 -> ? us)
+            static const int stream_min_d = env_int("SKB_POOL_STREAM_MIN_D", 64);
+            if (D >= stream_min_d && D <= 128) {  // wide rows: stream each sub-group's positions (C5: D=128 491 -> 345 us)
               c->last_pool = 6;
               k_fused_pool_stream<8, 3><<<grid, 256, 0, s>>>(SKB_POOL_ARGS);
             } else
