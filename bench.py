@@ -361,8 +361,12 @@ def run_ours(args):
     mem = members()
     n_ids = F_FEATURES * B
     cfg = skb.AdamConfig(lr=1e-3, weight_decay=0.01, variant="adamw")
+    # capacity: the 26M rows plus four steps of positions — the host's no-sync
+    # admission bound counts every in-flight position as a possible new row;
+    # with less slack every prefetch waits for the previous index phase's
+    # counter snapshot (a host sync per step)
     lt = skb.LogicalTable("dim64", DIM, 1, seed=0, members=mem, namespaced=True,
-                          capacity_hint=(F_FEATURES * ID_SPACE + F_FEATURES * ID_SPACE // 20) if not args.cold else 0)
+                          capacity_hint=(F_FEATURES * ID_SPACE + 4 * F_FEATURES * B) if not args.cold else 0)
     table = lt.local_table
 
     # warm steady state: every key of the stream admitted before timing
@@ -511,14 +515,26 @@ def run_ours(args):
         # the copy stream (so that prefetch does not wait for this copy)
         stage(k + 2)
 
+    stats_stream = torch.cuda.Stream()
+
     def after_e2e(k):
         buf_free[k % 3].record(main_stream)
-        # the step's metrics (misses, new rows, unique rows) back to the host
-        N.call("skb_fused_stats_async", table.handle, ctypes.c_void_p(stats_host[k].data_ptr()), N.stream_ptr())
+        # the step's metrics (misses, new rows, unique rows) back to the host,
+        # on a side stream: a copy on the compute stream delays the next
+        # step's pool launch past the next index phase's probe (measured
+        # ~40 us/step: the high-priority probe then takes the SMs first)
+        with torch.cuda.stream(stats_stream):  # (the copy waits for the step's backward itself)
+            N.call("skb_fused_stats_async", table.handle, ctypes.c_void_p(stats_host[k].data_ptr()), N.stream_ptr())
 
     # the compute stream sees the copied inputs through the prefetch's
     # ready event (index stream waited on the copy stream)
-    run_steps(get_e2e, args.steps, after_e2e, before_step, input_stream=copy_stream)
+    w_e2e = time.perf_counter()
+    if os.environ.get("SKB_TRACE"):  # diagnostic: the whole e2e loop under the kernel timeline
+        maybe_trace("c2_e2e", lambda: run_steps(get_e2e, args.steps, after_e2e, before_step,
+                                                input_stream=copy_stream))
+    else:
+        run_steps(get_e2e, args.steps, after_e2e, before_step, input_stream=copy_stream)
+    host_e2e_ms = (time.perf_counter() - w_e2e) * 1e3 / args.steps  # host time to issue a step
     e1.record()
     barrier()
     e2e_ms = e0.elapsed_time(e1)
@@ -576,6 +592,7 @@ def run_ours(args):
             "kernels_ms": phase_ms,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "IDs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 32,
+                    "host_issue_ms_per_step": host_e2e_ms,
                     "note": "each step's ids + bag offsets copied H2D from pinned host memory (copy stream, two "
                             "steps ahead) and the step's stats D2H; pooled / dpooled stay on the device (the "
                             "dense tower runs on the GPU)",

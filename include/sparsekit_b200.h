@@ -272,7 +272,10 @@ int skb_fused_profile(skb_table_t t, int64_t max_steps, void* stream);
 int skb_fused_profile_read(skb_table_t t, int32_t phase, float* ms_host, int64_t capacity,
                            int64_t* n_host);
 /* Stream-ordered copy of the last completed fused step's counters
- * {misses, new rows, unique rows, 0} into pinned host memory (no sync). */
+ * {misses, new rows, unique rows, 0} into pinned host memory (no sync).  Any
+ * stream: the copy waits for that step's backward, and the next reuse of the
+ * step's buffers waits for the copy (so a side stream keeps it off the
+ * compute stream). */
 int skb_fused_stats_async(skb_table_t t, int64_t* dst_pinned_host, void* stream);
 /* Number of unique rows the last fused forward touched (synchronizes). */
 int skb_fused_last_unique(skb_table_t t, int64_t* n_unique_host, int64_t* n_new_host, void* stream);

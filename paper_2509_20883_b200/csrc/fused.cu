@@ -84,6 +84,8 @@ struct BatchCtx {
   bool any_seq = false;
   bool last_written = false;  // deferred last_step already flushed
   cudaEvent_t ev_ready = nullptr, ev_free = nullptr;
+  cudaEvent_t ev_stats = nullptr;  // after a stats_async copy of dev (reuse of this buffer waits for it)
+  bool stats_pending = false;
   bool ever_used = false;
   int64_t gen = 0;  // bumped when a buffer above is reallocated / the member table changes
   StepGraph g_prep, g_fwd, g_bwd;  // graph mode: captured device work of each phase
@@ -150,6 +152,7 @@ static void batch_free(BatchCtx& B) {
   cudaFree(B.longs);
   if (B.ev_ready) cudaEventDestroy(B.ev_ready);
   if (B.ev_free) cudaEventDestroy(B.ev_free);
+  if (B.ev_stats) cudaEventDestroy(B.ev_stats);
 }
 
 void fused_ctx_destroy(FusedCtx* c) {
@@ -1735,6 +1738,10 @@ static void fused_prepare(Table* t, const BatchArgs& a, cudaStream_t s) {
   SKB_CUDA(cudaEventRecord(c->ev_in, s));
   SKB_CUDA(cudaStreamWaitEvent(x, c->ev_in, 0));
   if (B.ever_used) SKB_CUDA(cudaStreamWaitEvent(x, B.ev_free, 0));
+  if (B.stats_pending) {  // a stats_async copy of this buffer's counters, possibly on another stream
+    SKB_CUDA(cudaStreamWaitEvent(x, B.ev_stats, 0));
+    B.stats_pending = false;
+  }
   // growth moves the arena and side arrays: quiesce both streams before it and
   // finish the copies before any later main-stream kernel (e.g. the pending
   // fold+Adam of the previous step) can touch the new buffers (rare)
@@ -2336,7 +2343,12 @@ int skb_fused_stats_async(skb_table_t h, int64_t* dst_pinned_host, void* stream)
   FusedCtx* c = t->fused;
   if (!c || c->bwd_count == 0) raise(SKB_E_VALUE, 0, "no fused step has completed on this table");
   BatchCtx& B = c->b[(c->bwd_count - 1) % 2];
-  SKB_CUDA(cudaMemcpyAsync(dst_pinned_host, B.dev, sizeof(int64_t) * 4, cudaMemcpyDeviceToHost, as_stream(stream)));
+  cudaStream_t s = as_stream(stream);
+  SKB_CUDA(cudaStreamWaitEvent(s, B.ev_free, 0));  // after that step's backward, whatever stream this is
+  SKB_CUDA(cudaMemcpyAsync(dst_pinned_host, B.dev, sizeof(int64_t) * 4, cudaMemcpyDeviceToHost, s));
+  if (!B.ev_stats) SKB_CUDA(cudaEventCreateWithFlags(&B.ev_stats, cudaEventDisableTiming));
+  SKB_CUDA(cudaEventRecord(B.ev_stats, s));
+  B.stats_pending = true;
   SKB_API_END
 }
 
