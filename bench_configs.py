@@ -244,6 +244,7 @@ def c3(args):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
+    B.maybe_trace("c3", lambda: run(6))
     u, unew = skb.last_step_stats(lt)
     sb = B.step_bytes(n, n, u, unew, D)
 

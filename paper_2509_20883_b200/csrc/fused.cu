@@ -33,6 +33,7 @@
 #include "fused.cuh"
 #include "graph.cuh"
 #include "p2p.cuh"
+#include "partition.cuh"
 #include "longfold.cuh"
 #include "tma.cuh"
 #include "pool.cuh"
@@ -424,20 +425,10 @@ __global__ void __launch_bounds__(256) k_miss_insert(const int64_t* __restrict__
     int64_t h;
     if (key == kEmptyKey) {
       h = cap;
-    } else {
-      h = (int64_t)(bucket_hash((uint64_t)key) & mask);
-      while (true) {
-        long long k = *reinterpret_cast<volatile long long*>(&t[h].key);
-        if (k == key) break;
-        if (k == kEmptyKey) {
-          long long prev = (long long)atomicCAS(reinterpret_cast<unsigned long long*>(&t[h].key),
-                                                (unsigned long long)kEmptyKey, (unsigned long long)key);
-          if (prev == kEmptyKey || prev == key) break;
-        }
-        h = (int64_t)(((uint64_t)h + 1) & mask);
-      }
+      if (*reinterpret_cast<volatile long long*>(&t[h].val) > i) atomicMin(&t[h].val, (long long)i);
+    } else {  // one 128-bit CAS claims the bucket with this position, or lowers it (none if already lower)
+      h = (int64_t)insert_or_lower(t, bucket_hash((uint64_t)key) & mask, mask, key, (long long)i);
     }
-    if (*reinterpret_cast<volatile long long*>(&t[h].val) > i) atomicMin(&t[h].val, (long long)i);
     hslot[i] = (int32_t)h;
   }
 }
@@ -1681,7 +1672,11 @@ static bool admit_coop(Table* t) {
 static void launch_admission_phased(const AdmitArgs& A, size_t msm, cudaStream_t x) {
   const int64_t n = A.n;
   const int64_t ntiles = (n + kRankTile - 1) / kRankTile;
-  const unsigned wide = grid_for(n, 256, 4);
+  // the phased chain runs when a table is growing (its index phase then is
+  // the step's critical path: C3): full occupancy for the latency-bound
+  // insert / admit passes (SKB_ADMIT_WAVES, blocks per SM)
+  static const int waves = env_int("SKB_ADMIT_WAVES", 8);
+  const unsigned wide = grid_for(n, 256, waves);
   k_fill_scratch<<<wide, 256, 0, x>>>(A.scratch, A.dev);
   SKB_LAUNCH_CHECK();
   k_miss_insert<<<wide, 256, msm, x>>>(A.ids, n, A.mt, A.F, A.namespaced, A.miss, A.scratch, A.dev, A.hslot);
@@ -1694,7 +1689,7 @@ static void launch_admission_phased(const AdmitArgs& A, size_t msm, cudaStream_t
   k_rank_fresh<<<tiles, 256, 0, x>>>(n, A.fresh, A.tile_cnt, A.dev, A.rank, A.fpos);
   SKB_LAUNCH_CHECK();
   const int chunks = (A.D + 3) / 4;
-  k_fused_admit<<<grid_for(n * chunks, 256, 4), 256, msm, x>>>(
+  k_fused_admit<<<grid_for(n * chunks, 256, waves), 256, msm, x>>>(
       A.ids, n, A.mt, A.F, A.namespaced, A.fpos, A.hslot, A.scratch, A.dev, A.counters, A.free_list, A.map,
       A.mask, A.cap, A.step, A.D, A.seed_mix, A.scale, A.arena, A.last_step, A.live, A.slot_key, A.ins_seq,
       A.arena_rows);

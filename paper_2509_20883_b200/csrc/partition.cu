@@ -141,47 +141,6 @@ __global__ void k_part_init(HEntry* t, int64_t count, unsigned long long* status
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nstatus; i += stride) status[i] = 0ull;
 }
 
-// 128-bit CAS on a whole {key, first position} entry (sm_90+ atom.cas.b128)
-__device__ __forceinline__ void cas_entry(HEntry* p, long long ck, long long cv, long long nk, long long nv,
-                                          long long& ok, long long& ov) {
-  asm volatile("{\n\t.reg .b128 c, n, o;\n\t"
-               "mov.b128 c, {%2, %3};\n\t"
-               "mov.b128 n, {%4, %5};\n\t"
-               "atom.global.cas.b128 o, [%6], c, n;\n\t"
-               "mov.b128 {%0, %1}, o;\n\t}"
-               : "=l"(ok), "=l"(ov)
-               : "l"(ck), "l"(cv), "l"(nk), "l"(nv), "l"(p)
-               : "memory");
-}
-
-// insert-or-lower: the bucket ends as {key, min position}.  The bucket is
-// read first (L2, no atomic): a bucket already holding the key at an earlier
-// position needs no atomic at all — hot keys (zipf) would otherwise serialise
-// every occurrence on one address — and a foreign key moves on to the next
-// bucket (keys are never removed).  Otherwise one 128-bit CAS claims an empty
-// bucket or lowers a later position; a failed CAS re-examines the bucket
-// with the value it returned.
-__device__ __forceinline__ uint64_t insert_or_lower(HEntry* t, uint64_t slot, uint64_t mask, long long key,
-                                                    long long i) {
-  constexpr long long kMaxPos = 0x7FFFFFFFFFFFFFFFll;
-  longlong2 e = __ldcg(reinterpret_cast<const longlong2*>(&t[slot]));
-  while (true) {
-    if (e.x == key) {
-      if (e.y <= i) return slot;
-    } else if (e.x != kEmptyKey) {
-      slot = (slot + 1) & mask;
-      e = __ldcg(reinterpret_cast<const longlong2*>(&t[slot]));
-      continue;
-    } else {
-      e.y = kMaxPos;  // an empty bucket always holds {EMPTY, max}
-    }
-    long long ok, ov;
-    cas_entry(&t[slot], e.x, e.y, key, i, ok, ov);
-    if (ok == e.x && ov == e.y) return slot;
-    e = make_longlong2(ok, ov);
-  }
-}
-
 template <int kPartU>
 __global__ void __launch_bounds__(kPartThreads) k_part_insert(const int64_t* __restrict__ ids, int64_t n, HEntry* t,
                                                               uint64_t mask, int64_t cap,
