@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes
+import gc
 import json
 import os
 import statistics
@@ -138,6 +139,53 @@ class ClockSampler:
                         reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# Python garbage-collector pauses in the timed region
+# ---------------------------------------------------------------------------
+
+class GcPauses:
+    """Records every collector pass (generation, ms) while active.  A full
+    (generation 2) pass walks every live container object — with torch
+    imported that is ~0.5M objects, tens of ms — and the host issuing the
+    step stops for that long, so the device drains its queue and idles.
+    `freeze()` (the default; SKB_BENCH_GC_FREEZE=0 turns it off) does what a
+    long-running trainer does once its setup is done: one full collection,
+    then gc.freeze() moves the survivors to the permanent generation, so
+    later passes only walk the step's own short-lived objects."""
+
+    def __init__(self):
+        self.passes = []
+        self._t0 = None
+
+    def _cb(self, phase, info):
+        if phase == "start":
+            self._t0 = time.perf_counter()
+        elif self._t0 is not None:
+            self.passes.append((info.get("generation", -1), (time.perf_counter() - self._t0) * 1e3))
+            self._t0 = None
+
+    def __enter__(self):
+        gc.callbacks.append(self._cb)
+        return self
+
+    def __exit__(self, *a):
+        gc.callbacks.remove(self._cb)
+
+    @staticmethod
+    def freeze() -> bool:
+        if os.environ.get("SKB_BENCH_GC_FREEZE", "1") == "0":
+            return False
+        gc.collect()
+        gc.freeze()
+        return True
+
+    def summary(self):
+        return {"frozen": gc.get_freeze_count() > 0, "passes": len(self.passes),
+                "full_passes": sum(1 for g, _ in self.passes if g == 2),
+                "max_ms": round(max((d for _, d in self.passes), default=0.0), 3),
+                "total_ms": round(sum(d for _, d in self.passes), 3)}
 
 
 # ---------------------------------------------------------------------------

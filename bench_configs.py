@@ -28,6 +28,7 @@ bounded sample of the same workload on this host's cores.
 from __future__ import annotations
 
 import json
+import os
 import statistics
 import time
 
@@ -43,6 +44,107 @@ def _events():
     return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
 
+_CLK = {"summary": None, "gc": None}
+
+
+def _timed(run, steps):
+    """The timed region every config shares: CUDA events on the current
+    stream around `run(steps)`, an NVTX "timed" range (ncu/CUPTI filters),
+    and nvidia-smi clocks sampled while it runs (the sampler starts before
+    e0 so the first samples land inside the region).  Returns ms per step."""
+    import torch
+    e0, e1 = _events()
+    B.GcPauses.freeze()
+    with B.ClockSampler(torch.cuda.current_device()) as clk, B.GcPauses() as gcp:
+        time.sleep(0.25)  # the sampler's first rows
+        e0.record()
+        torch.cuda.nvtx.range_push("timed")
+        run(steps)
+        torch.cuda.nvtx.range_pop()
+        e1.record()
+        torch.cuda.synchronize()
+    _CLK["summary"] = clk.summary()
+    _CLK["gc"] = gcp.summary()
+    return e0.elapsed_time(e1) / steps
+
+
+class _Watch:
+    """Diagnostics (SKB_C5_WATCH=1): a thread samples the main thread's Python
+    stack every ms while a watched block runs; blocks longer than 10 ms print
+    the stacks seen after the 10 ms mark (and the sampling gaps: a gap means
+    the main thread held the GIL inside a C call)."""
+
+    def __init__(self):
+        import sys
+        import threading
+        import traceback
+        self.sys, self.tb = sys, traceback
+        self.main = threading.get_ident()
+        self.t0 = None
+        self.samples = []
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+
+    def _run(self):
+        while True:
+            time.sleep(0.001)
+            t0 = self.t0
+            if t0 is not None:
+                dt = time.perf_counter() - t0
+                if dt > 0.010:
+                    f = self.sys._current_frames().get(self.main)
+                    st = "".join(self.tb.format_stack(f, limit=6)[-4:]) if f else "?"
+                    self.samples.append((round(dt * 1e3, 2), st))
+
+    def __enter__(self):
+        self.samples = []
+        self.t0 = time.perf_counter()
+
+    def __exit__(self, *a):
+        dt = time.perf_counter() - self.t0
+        self.t0 = None
+        if dt > 0.010:
+            import sys
+            print(f"[watch] block {dt * 1e3:.1f} ms; {len(self.samples)} samples", file=sys.stderr)
+            last = None
+            for t, st in self.samples:
+                if st != last:
+                    print(f"[watch] t={t} ms\n{st}", file=sys.stderr)
+                    last = st
+
+
+def _settle(run, warmup: int, chunk: int = 10, cap: int = 300) -> int:
+    """Warm-up until the torch caching allocator stops growing: `warmup`
+    steps, then chunks of `chunk` steps until two chunks in a row make no new
+    device allocation (at most `cap` extra steps).  Blocks the step's tensors pin
+    across streams (record_stream) are freed late, so the pool keeps adding
+    segments for a few dozen steps; each addition is a cudaMalloc, which in
+    a process holding ~150 GB of mapped tables took 20-100 ms at random on
+    the host — long enough for the device to drain its queue and idle.
+    Returns the warm-up steps run."""
+    import torch
+    run(warmup)
+    done, clean = warmup, 0
+    while done < warmup + cap and clean < 2:
+        a0 = torch.cuda.memory_stats().get("num_device_alloc", 0)
+        run(chunk)
+        done += chunk
+        clean = clean + 1 if torch.cuda.memory_stats().get("num_device_alloc", 0) == a0 else 0
+    return done
+
+
+def _worst(steps_ms, host_t):
+    """The slowest timed step: its device ms and the host ms of each phase
+    of it and of the step before (a host stall shows up in one of those)."""
+    i = max(range(len(steps_ms)), key=steps_ms.__getitem__)
+    ph = ("forward", "backward", "build", "prefetch")
+    out = {"index": i, "ms": round(steps_ms[i], 3)}
+    for j, tag in ((i - 1, "host_prev"), (i, "host")):
+        if 0 <= j < len(host_t):
+            out[tag] = {nm: round(host_t[j][q] * 1e3, 3) for q, nm in enumerate(ph)}
+    return out
+
+
 def _line(args, workload, value, ms, ids_per_step, samples_per_step, algo_bytes, cpu, config, extra=None):
     peak, peak_kind = B.load_peaks()
     achieved = algo_bytes / (ms / 1e3) / 1e9
@@ -54,7 +156,7 @@ def _line(args, workload, value, ms, ids_per_step, samples_per_step, algo_bytes,
         "roofline": {"bound": "hbm", "kernel": "whole step (SURVEY §8d B_step)", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
                      "peak_kind": peak_kind, "algorithmic_bytes": int(algo_bytes)},
-        "cpu_baseline": cpu,
+        "cpu_baseline": cpu, "clocks": _CLK["summary"], "gc_in_timed": _CLK["gc"],
         "fold": getattr(args, "fold", "exact") + (" (tolerance mode: hot-id runs > 32 positions reduced as a two-level "
                                                   "tree, not bit-exact)" if getattr(args, "fold", "exact") == "tree"
                                                   else " (bit-exact np.add.at order)"),
@@ -108,14 +210,7 @@ def c1(args):
     run(max(args.warmup, 3) + 20)  # admits the id space; graphs captured on the 2nd call
     torch.cuda.synchronize()
     steps = max(args.steps, 200)  # ~50 us steps: time enough of them to amortise graph re-captures
-    e0, e1 = _events()
-    e0.record()
-    torch.cuda.nvtx.range_push("timed")
-    run(steps)
-    torch.cuda.nvtx.range_pop()
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
+    ms = _timed(run, steps)
     B.maybe_trace("c1", lambda: run(20))
     u, unew = skb.last_step_stats(lt)
     sb = B.step_bytes(Bn, Bn, u, unew, D)
@@ -236,14 +331,7 @@ def c3(args):
         if rows >= target or time.perf_counter() - t_start > 240:
             break
     # steady state at the final size: same batches, new tails still admitted
-    e0, e1 = _events()
-    e0.record()
-    torch.cuda.nvtx.range_push("timed")
-    run(args.steps)
-    torch.cuda.nvtx.range_pop()
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = _timed(run, args.steps)
     B.maybe_trace("c3", lambda: run(6))
     u, unew = skb.last_step_stats(lt)
     sb = B.step_bytes(n, n, u, unew, D)
@@ -335,20 +423,13 @@ def c4(args):
             # every kept position maps to one tile row: its gradient is that row
             skb.all_to_all_grad_update(lt, x.values, dtile.view(n, D), plan, cfg, step[0])
 
-    run(max(args.warmup, 3))
+    _settle(run, max(args.warmup, 3))
     torch.cuda.synchronize()
     import ctypes
     from paper_2509_20883_b200 import _native as N
     if fused:
         N.call("skb_fused_profile", lt.local_table.handle, args.steps, N.stream_ptr())
-    e0, e1 = _events()
-    e0.record()
-    torch.cuda.nvtx.range_push("timed")
-    run(args.steps)
-    torch.cuda.nvtx.range_pop()
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = _timed(run, args.steps)
     phase_ms = {}
     if fused:
         buf = (ctypes.c_float * args.steps)()
@@ -446,7 +527,7 @@ def c5(args):
     # --cold: tables start empty
     # with rows pre-reserved (no growth copies), admission in every step
     lts = {d: skb.LogicalTable(f"dim{d}", d, 1, seed=0, members=members[d], namespaced=True,
-                               capacity_hint=24_000_000 if args.cold else 45_000_000) for d in DIMS5}
+                               capacity_hint=24_000_000 if args.cold else int(os.environ.get("SKB_C5_HINT", 45_000_000))) for d in DIMS5}
     for lt_ in lts.values():
         skb.set_fold_mode(lt_, args.fold)
     prepop_s = None
@@ -533,8 +614,16 @@ def c5(args):
 
     pending = {}
     side = torch.cuda.Stream()
+    watch = _Watch() if os.environ.get("SKB_C5_WATCH") else None
+    if watch:
+        _build = build
 
-    def run(count):
+        def build(k):  # noqa: F811
+            with watch:
+                return _build(k)
+    host_t = []  # host seconds per step: (forward calls, backward calls, build, prefetch)
+
+    def run(count, marks=None):
         # cross-step pipeline: step k's forward AND backward are enqueued first
         # (several ms of device work), then the host builds step k+1 (feature
         # engine launches, packed batches) and issues its index phase (probe,
@@ -549,56 +638,85 @@ def c5(args):
         for _ in range(count):
             step[0] += 1
             k = step[0]
+            tp = time.perf_counter()
             cur = pending.pop(k)
             per = {}
+            main = torch.cuda.current_stream()
             for dd in DIMS5:
                 batch = cur[dd]
-                skb.lookup_pool(lts[dd], batch, k, "mean")
                 key = (dd, batch.num_bags)
                 if key not in grads:
                     grads[key] = torch.randn((batch.num_bags, dd), device="cuda") * 1e-2
                 per[dd] = (batch.num_ids, batch.num_bags)
+                skb.lookup_pool(lts[dd], batch, k, "mean")
+            tf = time.perf_counter()
             for dd in DIMS5:
                 skb.pool_grad_adam(lts[dd], grads[(dd, cur[dd].num_bags)], cfg, k)
+            tb = time.perf_counter()
+            if marks is not None:
+                marks.append(_events()[0])
+                marks[-1].record()
             # step k+1's feature engine and packed batches depend only on its
             # inputs: on a side stream they run under step k's backward instead
             # of queueing behind it (the prefetch orders itself after them)
-            main = torch.cuda.current_stream()
             with torch.cuda.stream(side):
                 nxt = build(k + 1)
                 for b in nxt.values():  # read later on the compute stream
                     b.ids.record_stream(main)
                     b.bag_offs.record_stream(main)
+                tn = time.perf_counter()
                 for dd in DIMS5:
                     skb.prefetch(lts[dd], nxt[dd], k + 1, "mean")
             pending[k + 1] = nxt
+            host_t.append((tf - tp, tb - tf, tn - tb, time.perf_counter() - tn))
             stats["per"] = per
         torch.cuda.current_stream().wait_stream(side)  # the last step's build counts in the timed region
 
     # the feature engine's data checks (bucketize NaN) are read once per run
     # instead of once per call: no host synchronisation inside a step
     with skb.deferred_checks():
-        run(max(args.warmup, 3))
+        warm_run = _settle(run, max(args.warmup, 3))
     torch.cuda.synchronize()
-    e0, e1 = _events()
-    with skb.deferred_checks():
-        e0.record()
-        torch.cuda.nvtx.range_push("timed")
+    marks = []
+
+    def timed_run(count):
+        # one event per step boundary on the compute stream: the per-step
+        # spread (a slow step shows as an outlier, not as a shifted mean)
+        marks.append(_events()[0])
+        marks[-1].record()
+        run(count, marks)
+
+    wall_s = []
+
+    def timed_run(count, _inner=timed_run):
         w0 = time.perf_counter()
-        run(args.steps)
-        torch.cuda.nvtx.range_pop()
-        e1.record()
-    torch.cuda.synchronize()
-    wall = (time.perf_counter() - w0) / args.steps * 1e3
+        _inner(count)
+        torch.cuda.synchronize()
+        wall_s.append(time.perf_counter() - w0)
+
+    m0 = torch.cuda.memory_stats()
+    with skb.deferred_checks():
+        ms = _timed(timed_run, args.steps)
+    wall = wall_s[0] / args.steps * 1e3
+    m1 = torch.cuda.memory_stats()
+    alloc = {k: m1.get(k, 0) - m0.get(k, 0) for k in ("num_alloc_retries", "num_device_alloc", "num_device_free",
+                                                      "num_sync_all_streams")}
+    alloc["reserved_gb"] = m1.get("reserved_bytes.all.current", 0) / 2**30
+    alloc["free_gb"] = torch.cuda.mem_get_info()[0] / 2**30
+    steps_ms = [a.elapsed_time(b) for a, b in zip(marks[:-1], marks[1:])]
+    ht = host_t[-args.steps:]
+    host_ms = {nm: statistics.median(x[i] for x in ht) * 1e3 for i, nm in enumerate(("forward", "backward", "build",
+                                                                                        "prefetch"))}
     with skb.deferred_checks():
         B.maybe_trace("c5", lambda: run(3))
-    ms = e0.elapsed_time(e1) / args.steps
     per = stats["per"]
     n, g = sum(v[0] for v in per.values()), sum(v[1] for v in per.values())
     sb = 0
+    per_table = {}
     for dd in DIMS5:
         u, unew = skb.last_step_stats(lts[dd])
         sb += B.step_bytes(per[dd][0], per[dd][1], u, unew, dd)
+        per_table[f"dim{dd}"] = {"ids": per[dd][0], "bags": per[dd][1], "unique": u, "new": unew}
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -651,6 +769,9 @@ def c5(args):
            "global_batch": Bn, "features": 200, "dims": list(DIMS5), "parallelism": "single shard",
            "l2": "inputs larger than L2"},
           {"bags_per_step": g, "host_wall_ms_per_step": wall, "host_batch_gen_s": gen_s,
+           "step_ms": {"median": statistics.median(steps_ms), "min": min(steps_ms), "max": max(steps_ms)},
+           "host_issue_ms": host_ms, "torch_alloc_in_timed": alloc, "warmup_steps_run": warm_run,
+           "worst_step": _worst(steps_ms, ht),
            "table_rows": {f"dim{d}": int(lts[d].num_rows) for d in DIMS5}, "prepopulate_s": prepop_s,
            "arena_rows": {f"dim{d}": int(lts[d].local_table._h.stats()[4]) for d in DIMS5},
            "state": "cold (growing)" if args.cold else "warm (all stream keys admitted)"})
