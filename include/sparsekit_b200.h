@@ -133,6 +133,17 @@ int skb_table_gather(skb_table_t t, const int64_t* offsets, int64_t n, float* ro
 /* scatter_update embedding.py:240-250 (distinct -> SKB_E_VALUE, live -> SKB_E_INDEX) */
 int skb_table_scatter_update(skb_table_t t, const int64_t* offsets, int64_t n, const float* rows,
                              void* stream);
+/* The same two checked operators with the check recorded on the device
+ * instead of read back (deferred_checks(), no synchronization): flags_dev is
+ * a caller-owned int64[4] preset to -1 (all ones); the first failing input
+ * index is atomically lowered into it — gather: [0] = not a live slot;
+ * scatter_update: [0] = duplicate, [1] = not live / out of range, [2] = an
+ * out-of-range offset (distinctness then re-checked by the caller).  The
+ * scatter writes nothing unless every check passed (read on the device). */
+int skb_table_gather_deferred(skb_table_t t, const int64_t* offsets, int64_t n, float* rows_out,
+                              int64_t* flags_dev, void* stream);
+int skb_table_scatter_update_deferred(skb_table_t t, const int64_t* offsets, int64_t n, const float* rows,
+                                      int64_t* flags_dev, void* stream);
 /* evict embedding.py:252-274: stale slots join the free list in insertion order */
 int skb_table_evict(skb_table_t t, int64_t current_step, int64_t* n_evicted_host, void* stream);
 /* export_rows embedding.py:276-284 into caller buffers of >= num_rows entries,

@@ -159,6 +159,19 @@ def main():
     sec = timed(lambda: N.call("skb_table_scatter_update", table.handle, N.ptr(sidx), R, N.ptr(newr),
                                N.stream_ptr()))
     report("scatter", traffic("scatter", n=R, d=D), sec, "1M x 16 (distinct + liveness checked)")
+    # the same checked operators inside deferred_checks(): every check still
+    # runs (on the device) and raises at the context's exit; the call itself
+    # neither synchronises nor reads back
+    # (the C-ABI entries EmbeddingTable.gather / scatter_update call there,
+    # with a caller-owned flag array, like the other rows of this table)
+    dflags = torch.full((4,), -1, dtype=torch.int64, device="cuda")
+    sec = timed(lambda: N.call("skb_table_gather_deferred", table.handle, N.ptr(gidx), R, N.ptr(gout), N.ptr(dflags),
+                               N.stream_ptr()))
+    report("gather", traffic("gather", n=R, d=D), sec, "1M x 16 (liveness-checked, deferred check)")
+    sec = timed(lambda: N.call("skb_table_scatter_update_deferred", table.handle, N.ptr(sidx), R, N.ptr(newr),
+                               N.ptr(dflags), N.stream_ptr()))
+    report("scatter", traffic("scatter", n=R, d=D), sec, "1M x 16 (distinct + liveness checked, deferred check)")
+    assert dflags.cpu().tolist() == [-1] * 4, "deferred checks flagged valid inputs"
     # the same two operators without the reference's per-call validation
     # (callers that own the offsets, e.g. the fused step / the exchange)
     sec = timed(lambda: N.call("skb_table_gather_unchecked", table.handle, N.ptr(gidx), R, N.ptr(gout),

@@ -57,6 +57,8 @@ _SIGS = {
     "skb_table_gather_unchecked": ([_p, _p, _i64, _p, _p], ctypes.c_int),
     "skb_sparse_adam_step_unchecked": ([_p, _p, _i64, _p, ctypes.POINTER(AdamScalars), _p], ctypes.c_int),
     "skb_table_scatter_update": ([_p, _p, _i64, _p, _p], ctypes.c_int),
+    "skb_table_gather_deferred": ([_p, _p, _i64, _p, _p, _p], ctypes.c_int),
+    "skb_table_scatter_update_deferred": ([_p, _p, _i64, _p, _p, _p], ctypes.c_int),
     "skb_table_evict": ([_p, _i64, ctypes.POINTER(_i64), _p], ctypes.c_int),
     "skb_table_export": ([_p, _p, _p, _p, _p, _p, _i64, ctypes.POINTER(_i64), _p], ctypes.c_int),
     "skb_table_restore": ([_p, _p, _i64, _p, _p, _p, _p, _p], ctypes.c_int),

@@ -112,10 +112,10 @@ __global__ void k_inverse(const int64_t* __restrict__ ids, const int64_t* __rest
 // ---------------------------------------------------------------------------
 // Stable multi-split for S <= kSplitMaxS in four launches, no sort, no
 // look-back spinning and no host round trip:
-//   k_part_init    table {EMPTY, INT64_MAX} + zeroed tile-done counter
-//   k_part_insert  every position claims its key's bucket and lowers the
-//                  bucket's position to its own index (one 128-bit CAS in the
-//                  common case) -> the bucket holds the key's first occurrence
+//   k_part_init    position table all kNoPos + zeroed tile-done counter
+//   k_part_insert  every position claims its key's bucket (one 32-bit CAS)
+//                  or lowers the bucket's position to its own index -> the
+//                  bucket holds the key's first occurrence
 //   k_part_count   tile of kPartTile positions per block: first occurrences
 //                  ranked per owner shard inside the tile (__match_any_sync +
 //                  per-warp running counts) -> lrank[i]; per-(shard, tile)
@@ -130,24 +130,39 @@ constexpr int kSplitMaxS = 256;
 constexpr int kPartThreads = 256;
 constexpr int kPartRounds = 4;                             // 32-position rounds per warp
 constexpr int kPartTile = kPartThreads * kPartRounds;      // 1024 positions per tile
-constexpr int kPartU = 1;                                  // insert chains per thread
+constexpr int kPartU = 1;  // insert chains per thread (4 in flight measured slower: 30.6 vs 24.4 us, L2 atomics)
 constexpr int kScanSmem = 8192;                            // int32 staging of the tile-count scan
 
-// table fill + zeroed counters, one launch
-__global__ void k_part_init(HEntry* t, int64_t count, unsigned long long* status, int64_t nstatus) {
+// The split path's table holds ONE uint32 per bucket: the first position of
+// the key that owns it (the key itself is read back through ids[], which is
+// L2-resident).  4 B per bucket instead of a 16-B {key, first} entry: the
+// table of 1M positions is 8 MB instead of 32 MB, a claim is one 32-bit CAS,
+// and no key value has to be reserved as "empty".
+constexpr uint32_t kNoPos = 0xFFFFFFFFu;
+
+// table fill + zeroed counters, one launch (cap is a power of two >= 64)
+__global__ void k_part_init(uint32_t* t, int64_t cap, unsigned long long* status, int64_t nstatus) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += stride)
-    reinterpret_cast<longlong2*>(t)[i] = make_longlong2(kEmptyKey, 0x7FFFFFFFFFFFFFFFll);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cap / 4; i += stride)
+    reinterpret_cast<uint4*>(t)[i] = make_uint4(kNoPos, kNoPos, kNoPos, kNoPos);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nstatus; i += stride) status[i] = 0ull;
 }
 
+// every position claims its key's bucket (CAS from kNoPos) or, finding the
+// key there, lowers the bucket to its own position: the bucket ends holding
+// the key's first occurrence.  The first CAS of each of a thread's kPartU
+// positions is issued before any result is used (kPartU round trips in
+// flight); CAS first, no plain load before it: most positions of a batch
+// carry a key not seen yet, and for them the CAS is the only round trip.
 template <int kPartU>
-__global__ void __launch_bounds__(kPartThreads) k_part_insert(const int64_t* __restrict__ ids, int64_t n, HEntry* t,
-                                                              uint64_t mask, int64_t cap,
+__global__ void __launch_bounds__(kPartThreads) k_part_insert(const int64_t* __restrict__ ids, int64_t n,
+                                                              uint32_t* t, uint64_t mask,
                                                               uint32_t* __restrict__ hslot) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < n; base += stride * kPartU) {
     long long key[kPartU];
+    uint64_t h[kPartU];
+    uint32_t v[kPartU];
 #pragma unroll
     for (int u = 0; u < kPartU; ++u) {
       const int64_t i = base + u * stride;
@@ -156,21 +171,29 @@ __global__ void __launch_bounds__(kPartThreads) k_part_insert(const int64_t* __r
 #pragma unroll
     for (int u = 0; u < kPartU; ++u) {
       const int64_t i = base + u * stride;
+      h[u] = bucket_hash((uint64_t)key[u]) & mask;
+      v[u] = i < n ? atomicCAS(t + h[u], kNoPos, (uint32_t)i) : kNoPos;
+    }
+#pragma unroll
+    for (int u = 0; u < kPartU; ++u) {
+      const int64_t i = base + u * stride;
       if (i >= n) continue;
-      uint64_t slot;
-      if (key[u] == kEmptyKey) {  // side entry: only the position is contended
-        slot = (uint64_t)cap;
-        if (__ldcg(&t[cap].val) > i) atomicMin(&t[cap].val, (long long)i);
-      } else {
-        slot = insert_or_lower(t, bucket_hash((uint64_t)key[u]) & mask, mask, key[u], (long long)i);
+      const uint32_t me = (uint32_t)i;
+      while (v[u] != kNoPos) {  // kNoPos: claimed, this position is the first so far
+        if (__ldg(ids + v[u]) == key[u]) {  // the key's bucket: keep the smaller position
+          if (v[u] > me) atomicMin(t + h[u], me);
+          break;
+        }
+        h[u] = (h[u] + 1) & mask;
+        v[u] = atomicCAS(t + h[u], kNoPos, me);
       }
-      hslot[i] = (uint32_t)slot;
+      hslot[i] = (uint32_t)h[u];
     }
   }
 }
 
 __global__ void __launch_bounds__(kPartThreads) k_part_count(const int64_t* __restrict__ ids, int64_t n,
-                                                             const HEntry* __restrict__ t,
+                                                             const uint32_t* __restrict__ t,
                                                              const uint32_t* __restrict__ hslot, int S,
                                                              int64_t ntiles, int* __restrict__ off,
                                                              uint32_t* __restrict__ lrank_out,
@@ -195,7 +218,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_count(const int64_t* __re
   for (int r = 0; r < kPartRounds; ++r) {
     fv[r] = -1;
     if (i0 + r * 32 < n) {
-      fv[r] = t[hs[r]].val;
+      fv[r] = (long long)t[hs[r]];
       key[r] = ids[i0 + r * 32];
     }
   }
@@ -284,7 +307,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_count(const int64_t* __re
 }
 
 __global__ void __launch_bounds__(kPartThreads) k_part_emit(const int64_t* __restrict__ ids, int64_t n,
-                                                            const HEntry* __restrict__ t,
+                                                            const uint32_t* __restrict__ t,
                                                             const uint32_t* __restrict__ hslot, int S,
                                                             int64_t ntiles, const int* __restrict__ off,
                                                             const uint32_t* __restrict__ lrank,
@@ -301,7 +324,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_emit(const int64_t* __res
       const int64_t i = b0 + u * stride;
       if (i < n) {
         key[u] = ids[i];
-        f[u] = t[hslot[i]].val;
+        f[u] = (long long)t[hslot[i]];
       }
     }
     uint32_t lr[U];
@@ -469,7 +492,7 @@ static size_t split_ws_layout(int64_t n, int64_t S, size_t* b_t, size_t* b_h, si
   const int64_t cap = next_pow2(n * 2 > 64 ? n * 2 : 64);
   const int64_t ntiles = (n + kPartTile - 1) / kPartTile;
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-  *b_t = al(sizeof(HEntry) * (cap + 1));
+  *b_t = al(sizeof(uint32_t) * cap);
   *b_h = al(4 * (n > 0 ? n : 1));
   *b_o = al(sizeof(int) * (ntiles > 0 ? ntiles : 1) * S);
   return *b_t + 2 * *b_h + *b_o + 256;
@@ -487,15 +510,15 @@ static void split_partition(const int64_t* ids, int64_t n, int64_t S, int64_t* u
   size_t b_t, b_h, b_o;
   split_ws_layout(n, S, &b_t, &b_h, &b_o);
   char* w = static_cast<char*>(ws);
-  HEntry* t = reinterpret_cast<HEntry*>(w);
+  uint32_t* t = reinterpret_cast<uint32_t*>(w);
   uint32_t* hs = reinterpret_cast<uint32_t*>(w + b_t);
   uint32_t* lr = reinterpret_cast<uint32_t*>(w + b_t + b_h);
   int* off = reinterpret_cast<int*>(w + b_t + 2 * b_h);
   unsigned long long* done = reinterpret_cast<unsigned long long*>(w + b_t + 2 * b_h + b_o);
-  k_part_init<<<grid_for(cap + 1, 256), 256, 0, s>>>(t, cap + 1, done, 1);
+  k_part_init<<<grid_for(cap / 4, 256), 256, 0, s>>>(t, cap, done, 1);
   SKB_LAUNCH_CHECK();
   k_part_insert<kPartU><<<grid_for((n + kPartU - 1) / kPartU, kPartThreads), kPartThreads, 0, s>>>(
-      ids, n, t, (uint64_t)(cap - 1), cap, hs);
+      ids, n, t, (uint64_t)(cap - 1), hs);
   SKB_LAUNCH_CHECK();
   k_part_count<<<(unsigned)ntiles, kPartThreads, 0, s>>>(ids, n, t, hs, (int)S, ntiles, off, lr, done, counts);
   SKB_LAUNCH_CHECK();

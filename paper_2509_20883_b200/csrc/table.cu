@@ -464,15 +464,18 @@ __global__ void __launch_bounds__(256) k_write_rows_if_clear(const int64_t* __re
   }
 }
 
+// flags: the table's own (read back by the caller right after) or a
+// caller-owned device array (deferred checks)
 template <int VEC, int MODE>
 static void launch_checked_scatter(Table* t, const int64_t* offs, int64_t n, const float* src, float* dst,
-                                   cudaStream_t s) {
+                                   cudaStream_t s, unsigned long long* flags = nullptr) {
+  if (!flags) flags = t->dflags;
   k_check_rows<MODE><<<grid_for(n, 256), 256, 0, s>>>(offs, n, t->live, t->counters, t->ensured_slots,
-                                                      t->block_size, t->arena_rows, t->bitmap, t->dflags);
+                                                      t->block_size, t->arena_rows, t->bitmap, flags);
   SKB_LAUNCH_CHECK();
   const int D = (int)t->dim;
   k_write_rows_if_clear<VEC, MODE><<<grid_for((n * (D / VEC) + kRowsUnroll - 1) / kRowsUnroll, 256), 256, 0, s>>>(
-      offs, n, src, D, dst, 3 * t->dim, t->arena_rows, t->bitmap, t->dflags);
+      offs, n, src, D, dst, 3 * t->dim, t->arena_rows, t->bitmap, flags);
   SKB_LAUNCH_CHECK();
 }
 
@@ -1133,6 +1136,34 @@ int skb_table_gather(skb_table_t h, const int64_t* offsets, int64_t n, float* ro
     const int64_t o = read_i64(offsets + bad, s);
     raise(SKB_E_INDEX, o, "gather: offset %lld is not a live slot", (long long)o);
   }
+  SKB_API_END
+}
+
+int skb_table_gather_deferred(skb_table_t h, const int64_t* offsets, int64_t n, float* rows_out, int64_t* flags_dev,
+                              void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  if (!flags_dev) raise(SKB_E_ARG, 0, "gather_deferred: flags_dev is null");
+  if (n <= 0) return SKB_OK;
+  const int D = (int)t->dim;
+  launch_rows_gather_checked(IdxArray{offsets}, t->arena, 3 * D, rows_out, D, n, D, t->live, t->arena_rows,
+                             reinterpret_cast<unsigned long long*>(flags_dev), as_stream(stream));
+  SKB_API_END
+}
+
+int skb_table_scatter_update_deferred(skb_table_t h, const int64_t* offsets, int64_t n, const float* rows,
+                                      int64_t* flags_dev, void* stream) {
+  SKB_API_BEGIN
+  Table* t = table_from(h);
+  cudaStream_t s = as_stream(stream);
+  if (!flags_dev) raise(SKB_E_ARG, 0, "scatter_update_deferred: flags_dev is null");
+  if (n <= 0) return SKB_OK;
+  fused_require_quiet(t, true, "scatter_update");
+  ensure_bitmap(t, s);
+  auto* f = reinterpret_cast<unsigned long long*>(flags_dev);
+  const bool v4 = t->dim % 4 == 0 && (uintptr_t)rows % 16 == 0;
+  if (v4) launch_checked_scatter<4, 0>(t, offsets, n, rows, t->arena, s, f);
+  else launch_checked_scatter<1, 0>(t, offsets, n, rows, t->arena, s, f);
   SKB_API_END
 }
 

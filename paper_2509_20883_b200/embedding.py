@@ -18,6 +18,7 @@ import numpy as np
 
 from . import _native as N
 from . import telemetry
+from .features import _deferred_stack
 
 DEFAULT_BLOCK_SIZE = 65536
 
@@ -284,7 +285,15 @@ class EmbeddingTable:
         o = N.to_dev(offsets, "int64").reshape(-1)
         out = N.empty((o.numel(), self.dim), "float32")
         if o.numel():
-            N.call("skb_table_gather", self._h.h, N.ptr(o), o.numel(), N.ptr(out), N.stream_ptr())
+            pending = None if as_np else _deferred_stack()
+            if pending is None:
+                N.call("skb_table_gather", self._h.h, N.ptr(o), o.numel(), N.ptr(out), N.stream_ptr())
+            else:  # deferred_checks(): the liveness check is read at the context's exit
+                flags = N.torch().full((4,), -1, dtype=N.torch().int64, device=o.device)
+                N.call("skb_table_gather_deferred", self._h.h, N.ptr(o), o.numel(), N.ptr(out), N.ptr(flags),
+                       N.stream_ptr())
+                pending.append((flags, lambda v, o=o: None if v[0] == -1 else IndexError(
+                    f"gather: offset {int(o[v[0]])} is not a live slot")))
         return N.out_like(out, as_np)
 
     def scatter_update(self, offsets, rows) -> None:
@@ -297,7 +306,28 @@ class EmbeddingTable:
         if not o.numel():
             return
         r = N.to_dev(rows, "float32")
-        N.call("skb_table_scatter_update", self._h.h, N.ptr(o), o.numel(), N.ptr(r), N.stream_ptr())
+        pending = _deferred_stack()
+        if pending is None:
+            N.call("skb_table_scatter_update", self._h.h, N.ptr(o), o.numel(), N.ptr(r), N.stream_ptr())
+            return
+        # deferred_checks(): checked and written on the device (nothing is
+        # written unless every check passes); the verdict is read at the exit
+        flags = N.torch().full((4,), -1, dtype=N.torch().int64, device=o.device)
+        N.call("skb_table_scatter_update_deferred", self._h.h, N.ptr(o), o.numel(), N.ptr(r), N.ptr(flags),
+               N.stream_ptr())
+
+        def verdict(v, o=o):
+            if v[0] == -1 and v[1] == -1:
+                return None
+            # duplicates (ValueError) before liveness (IndexError), as the
+            # eager path; out-of-range offsets are outside the bitmap, so
+            # their distinctness is decided here
+            dup = v[0] != -1 if v[2] == -1 else int(N.torch().unique(o).numel()) != o.numel()
+            if dup:
+                return ValueError("scatter_update requires distinct offsets")
+            return IndexError(f"scatter_update: offset {int(o[v[1]])} is not a live slot")
+
+        pending.append((flags, verdict))
 
     def evict(self, current_step: int) -> int:
         """Drop slots idle for more than evict_threshold steps (embedding.py:252-274)."""

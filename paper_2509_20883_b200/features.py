@@ -85,13 +85,30 @@ def check_deferred() -> None:
 
 
 def _raise_pending(flags):
+    """Read every recorded flag array in one copy and raise the first
+    failure.  An entry is (int64 device flags, message): ValueError(message)
+    when flags[0] != -1 (~0: nothing flagged); or (flags, fn): fn(list of the
+    flag values) returns the exception to raise, or None."""
     if not flags:
         return
     t = N.torch()
-    vals = t.cat([f for f, _ in flags]).cpu().tolist()
-    for v, (_, msg) in zip(vals, flags):
-        if v != -1:  # ~0 as int64: nothing flagged
+    vals = t.cat([f.reshape(-1) for f, _ in flags]).cpu().tolist()
+    k = 0
+    for f, msg in flags:
+        v = vals[k:k + f.numel()]
+        k += f.numel()
+        if callable(msg):
+            exc = msg(v)
+            if exc is not None:
+                raise exc
+        elif v[0] != -1:
             raise ValueError(msg)
+
+
+def _deferred_stack():
+    """The innermost deferred_checks() record list, or None outside one."""
+    stack = getattr(_DEFERRED, "stack", None)
+    return stack[-1] if stack else None
 
 
 def _bucketize_flat(vals_d, col_offs_d, C, edges_d, edge_offs_d):

@@ -226,6 +226,55 @@ def test_checked_row_ops_leave_table_untouched_and_rearm(skb, D):
     eq(t.gather(o[:3]), np.ones((3, D), np.float32))
 
 
+@pytest.mark.parametrize("D", [3, 16])
+def test_deferred_gather_scatter(skb, D):
+    """gather / scatter_update inside deferred_checks(): same results as the
+    eager calls, nothing read back per call, and the eager path's exception
+    (type, message, duplicate-before-liveness order) raised at the context's
+    exit — with the table untouched by a failing scatter."""
+    import torch
+    rng = np.random.default_rng(D + 1)
+    n = 50_000
+    t = skb.EmbeddingTable("d", D, seed=2)
+    o = torch.from_numpy(t.lookup_or_insert(np.arange(n, dtype=np.int64) * 5 + 1, 1)).cuda()
+    perm = torch.from_numpy(rng.permutation(n)).cuda()
+    rows = torch.from_numpy(rng.standard_normal((n, D)).astype(np.float32)).cuda()
+    before = t.gather(o).clone()
+    with skb.deferred_checks():
+        g = t.gather(o[perm])
+        t.scatter_update(o[perm], rows)
+        g2 = t.gather(o[perm])
+    eq(g.cpu().numpy(), before[perm].cpu().numpy())
+    eq(g2.cpu().numpy(), rows.cpu().numpy())
+    snap = t.gather(o).clone()
+    cases = [
+        (lambda x: x.__setitem__(n - 1, x[17]), ValueError, "requires distinct"),
+        (lambda x: x.__setitem__(5, n + 10), IndexError, f"scatter_update: offset {n + 10} is not a live slot"),
+        # a duplicate AND a dead slot: the duplicate wins, as in the eager path
+        (lambda x: (x.__setitem__(3, n + 20), x.__setitem__(9, x[2])), ValueError, "requires distinct"),
+        # two equal out-of-range offsets: distinctness decided on the host
+        (lambda x: (x.__setitem__(4, -7), x.__setitem__(8, -7)), ValueError, "requires distinct"),
+        (lambda x: x.__setitem__(6, -7), IndexError, "scatter_update: offset -7 is not a live slot"),
+    ]
+    for mutate, exc, msg in cases:
+        bad = o[perm].clone()
+        mutate(bad)
+        with pytest.raises(exc, match=msg):
+            with skb.deferred_checks():
+                t.scatter_update(bad, rows * 2)
+        eq(t.gather(o).cpu().numpy(), snap.cpu().numpy())
+    with pytest.raises(IndexError, match=f"gather: offset {n + 3} is not a live slot"):
+        with skb.deferred_checks():
+            x = o.clone()
+            x[11] = n + 3
+            t.gather(x)
+    # the same failures eagerly: identical messages
+    bad = o[perm].clone()
+    bad[5] = n + 10
+    with pytest.raises(IndexError, match=f"scatter_update: offset {n + 10} is not a live slot"):
+        t.scatter_update(bad, rows)
+
+
 @pytest.mark.parametrize("name", ["short", "long", "len1", "empty_all"])
 @pytest.mark.parametrize("D", [1, 3, 16])
 def test_segments(skb, golden, name, D):
