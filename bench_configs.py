@@ -613,6 +613,9 @@ def c5(args):
         return out
 
     pending = {}
+    # default priority: at high priority (like the tables' index streams) the
+    # feature engine of step k+1 ran under step k's fold+Adam, but the step
+    # was no faster (6.36 vs 6.28 ms): the kernels it overlapped slowed down
     side = torch.cuda.Stream()
     watch = _Watch() if os.environ.get("SKB_C5_WATCH") else None
     if watch:
@@ -771,6 +774,7 @@ def c5(args):
           {"bags_per_step": g, "host_wall_ms_per_step": wall, "host_batch_gen_s": gen_s,
            "step_ms": {"median": statistics.median(steps_ms), "min": min(steps_ms), "max": max(steps_ms)},
            "host_issue_ms": host_ms, "torch_alloc_in_timed": alloc, "warmup_steps_run": warm_run,
+           "per_table": per_table,
            "worst_step": _worst(steps_ms, ht),
            "table_rows": {f"dim{d}": int(lts[d].num_rows) for d in DIMS5}, "prepopulate_s": prepop_s,
            "arena_rows": {f"dim{d}": int(lts[d].local_table._h.stats()[4]) for d in DIMS5},

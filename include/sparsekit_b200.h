@@ -346,6 +346,16 @@ int skb_cross_offsets(const int64_t* a_offs, const int64_t* b_offs, int64_t rows
 int skb_cross(const int64_t* a_vals, const int64_t* a_offs, const int64_t* b_vals,
               const int64_t* b_offs, int64_t rows, const int64_t* out_offs, int64_t total, int64_t* out,
               int64_t* size_flag, void* stream);
+/* cross over many column pairs (features.cross_many) in two launches.
+ * descs_dev: device array of npairs 80-byte descriptors
+ *   { a_vals, a_offs, b_vals, b_offs, rows, out_offs[rows+1], total, out_base,
+ *     size_flag (optional, caller sets -1), pad }  (all 8-byte fields);
+ * skb_cross_offsets_many fills every pair's out_offs (and size_flag, as
+ * skb_cross does); skb_cross_many writes every pair's products to
+ * out[out_base .. out_base + total) (total = sum of the pairs' totals, <= 1024
+ * pairs per launch). */
+int skb_cross_offsets_many(const void* descs_dev, int64_t npairs, void* stream);
+int skb_cross_many(const void* descs_dev, int64_t npairs, int64_t total, int64_t* out, void* stream);
 /* size_flag (optional device int64, caller sets -1): set to the true product
  * count when `total` (a caller-supplied size, features.cross_many(sizes=))
  * differs from out_offs[rows]; positions past the true count are zeroed and

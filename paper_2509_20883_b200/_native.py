@@ -125,6 +125,8 @@ _SIGS = {
     "skb_mod_cols": ([_p, _p, _i64, _p, _p, _i64, _p], ctypes.c_int),
     "skb_pack_members": ([_p, _p, _p, _p, _i64, _i64, _i64, _p, _p, _p], ctypes.c_int),
     "skb_cross": ([_p, _p, _p, _p, _i64, _p, _i64, _p, _p, _p], ctypes.c_int),
+    "skb_cross_offsets_many": ([_p, _i64, _p], ctypes.c_int),
+    "skb_cross_many": ([_p, _i64, _i64, _p, _p], ctypes.c_int),
     "skb_ragged_truncate": ([_p, _i64, _i64, _i32, _p, _p, _p], ctypes.c_int),
     "skb_gather_elems": ([_p, _i64, _p, _i64, _p, _p], ctypes.c_int),
     "skb_ragged_pad_dense": ([_p, _i64, _i64, _p, _i64, _i64, _p, _p, _p, _p], ctypes.c_int),

@@ -1017,6 +1017,8 @@ __global__ void __launch_bounds__(256) k_fused_tile(const float* __restrict__ ar
 // each per pass: both rows' w, m, v and first dpooled loads are in flight
 // before any arithmetic.  A run continuing past its chunk is finished by the
 // warp owning its head (the next chunk sees no head there).
+constexpr int kFoldBatch = 2;  // gradient rows in flight per run in k_fused_adam's fold
+
 template <int VEC, int R, int MINB, bool ADAM = true>
 __global__ void __launch_bounds__(256, MINB) k_fused_adam(int64_t n, const uint32_t* __restrict__ skey,
                                                     const uint32_t* __restrict__ sval,
@@ -1097,7 +1099,28 @@ __global__ void __launch_bounds__(256, MINB) k_fused_adam(int64_t n, const uint3
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (h[r] < 0) continue;
-          for (int64_t jj = j0 + h[r] + 1; jj < e[r]; ++jj) {
+          int64_t jj = j0 + h[r] + 1;
+          // runs of up to kLongRun positions: kFoldBatch gradient rows in
+          // flight per step of the chain (their loads do not depend on the
+          // accumulator), added strictly in position order — the same FADD
+          // sequence as one row at a time, so still bit-exact
+          for (; jj + kFoldBatch <= e[r]; jj += kFoldBatch) {
+            uint32_t g[kFoldBatch];
+            T x[kFoldBatch];
+#pragma unroll
+            for (int q = 0; q < kFoldBatch; ++q)
+              g[q] = jj + q < j0 + 32 ? s_bag[wib][jj + q - j0] : __ldg(sval + jj + q);
+#pragma unroll
+            for (int q = 0; q < kFoldBatch; ++q) x[q] = vload<VEC>(grad_row(dpooled, zrow, g[q], D) + c);
+            if (mode == 1) {
+#pragma unroll
+              for (int q = 0; q < kFoldBatch; ++q)
+                x[q] = vdiv<VEC>(x[q], (float)(__ldg(bag_offs + g[q] + 1) - __ldg(bag_offs + g[q])));
+            }
+#pragma unroll
+            for (int q = 0; q < kFoldBatch; ++q) acc[r] = vadd<VEC>(acc[r], x[q]);
+          }
+          for (; jj < e[r]; ++jj) {
             const uint32_t g = jj < j0 + 32 ? s_bag[wib][jj - j0] : __ldg(sval + jj);
             T x = vload<VEC>(grad_row(dpooled, zrow, g, D) + c);
             if (mode == 1) x = vdiv<VEC>(x, (float)(__ldg(bag_offs + g + 1) - __ldg(bag_offs + g)));

@@ -79,6 +79,115 @@ __global__ void k_cross_lens(const int64_t* __restrict__ aoff, const int64_t* __
     lens[r] = (aoff[r + 1] - aoff[r]) * (boff[r + 1] - boff[r]);
 }
 
+// ---------------------------------------------------------------------------
+// cross_many: every column pair of a step in two launches (features.py:65-89
+// per pair).  One descriptor per pair; outputs of all pairs share one buffer
+// (out_base = the pair's first output).  Launch 1: one CTA per pair scans its
+// row products into out_offs and checks the caller's size; launch 2: one
+// thread per output element of all pairs (pair by binary search over the
+// descriptors' out_base, row by binary search over the pair's out_offs).
+// ---------------------------------------------------------------------------
+struct CrossDesc {
+  const int64_t* a;
+  const int64_t* ao;
+  const int64_t* b;
+  const int64_t* bo;
+  int64_t rows;
+  int64_t* oo;       // [rows + 1]
+  int64_t total;     // caller size of this pair's output (or the true one)
+  int64_t out_base;  // first output of this pair in the shared buffer
+  int64_t* flag;     // optional: true product count when it differs from total
+  int64_t pad;
+};
+static_assert(sizeof(CrossDesc) == 80, "descriptor layout is shared with features.py");
+
+constexpr int kCrossScanThreads = 1024;
+constexpr int kCrossScanItems = 8;
+
+__global__ void __launch_bounds__(kCrossScanThreads) k_cross_offsets_many(const CrossDesc* __restrict__ descs) {
+  const CrossDesc d = descs[blockIdx.x];
+  constexpr int W = kCrossScanThreads / 32;
+  __shared__ int64_t s_warp[W];
+  __shared__ int64_t s_carry;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  constexpr int64_t kChunk = (int64_t)kCrossScanThreads * kCrossScanItems;
+  for (int64_t c0 = 0; c0 < d.rows; c0 += kChunk) {
+    int64_t v[kCrossScanItems];
+    int64_t loc = 0;
+    const int64_t r0 = c0 + (int64_t)threadIdx.x * kCrossScanItems;
+#pragma unroll
+    for (int q = 0; q < kCrossScanItems; ++q) {
+      const int64_t r = r0 + q;
+      v[q] = r < d.rows ? (d.ao[r + 1] - d.ao[r]) * (d.bo[r + 1] - d.bo[r]) : 0;
+      loc += v[q];
+    }
+    int64_t inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_warp[w] = inc;
+    __syncthreads();
+    int64_t before = s_carry, tot = 0;
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      const int64_t x = s_warp[q];
+      if (q < w) before += x;
+      tot += x;
+    }
+    int64_t run = before + inc - loc;
+#pragma unroll
+    for (int q = 0; q < kCrossScanItems; ++q) {
+      const int64_t r = r0 + q;
+      if (r < d.rows) d.oo[r] = run;
+      run += v[q];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    d.oo[d.rows] = s_carry;
+    if (d.flag && s_carry != d.total) *d.flag = s_carry;
+  }
+}
+
+constexpr int kCrossMaxPairs = 1024;
+
+__global__ void __launch_bounds__(256) k_cross_many(const CrossDesc* __restrict__ descs, int npairs, int64_t T,
+                                                    int64_t* __restrict__ out) {
+  __shared__ int64_t s_base[kCrossMaxPairs + 1];
+  for (int k = threadIdx.x; k < npairs; k += blockDim.x) s_base[k] = descs[k].out_base;
+  if (threadIdx.x == 0) s_base[npairs] = T;
+  __syncthreads();
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = npairs;  // pair p with s_base[p] <= t < s_base[p+1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_base[mid] <= t) lo = mid; else hi = mid;
+    }
+    const CrossDesc& d = descs[lo];
+    const int64_t tl = t - s_base[lo];
+    const int64_t true_total = __ldg(d.oo + d.rows);
+    if (tl >= true_total) {  // a caller-supplied size larger than the products: never read past the inputs
+      out[t] = 0;
+      continue;
+    }
+    int64_t a = 0, b = d.rows;  // row r with oo[r] <= tl < oo[r+1]
+    while (b - a > 1) {
+      const int64_t mid = (a + b) >> 1;
+      if (__ldg(d.oo + mid) <= tl) a = mid; else b = mid;
+    }
+    const int64_t within = tl - __ldg(d.oo + a);
+    const int64_t lb = __ldg(d.bo + a + 1) - __ldg(d.bo + a);
+    const int64_t i = within / lb, j = within - i * lb;
+    out[t] = (int64_t)fnv_pair((uint64_t)__ldg(d.a + __ldg(d.ao + a) + i), (uint64_t)__ldg(d.b + __ldg(d.bo + a) + j));
+  }
+}
+
 }  // namespace skb
 
 using namespace skb;
@@ -144,6 +253,27 @@ int skb_cross_offsets(const int64_t* a_offs, const int64_t* b_offs, int64_t rows
   k_cross_lens<<<grid_for(rows, 256), 256, 0, s>>>(a_offs, b_offs, rows, lens.as<int64_t>());
   SKB_LAUNCH_CHECK();
   scan_exclusive_i64(lens.as<int64_t>(), out_offs, rows, out_offs + rows, s);
+  SKB_API_END
+}
+
+int skb_cross_offsets_many(const void* descs_dev, int64_t npairs, void* stream) {
+  SKB_API_BEGIN
+  if (npairs < 0) raise(SKB_E_ARG, npairs, "cross_many: negative pair count");
+  if (npairs == 0) return SKB_OK;
+  k_cross_offsets_many<<<(unsigned)npairs, kCrossScanThreads, 0, as_stream(stream)>>>(
+      static_cast<const CrossDesc*>(descs_dev));
+  SKB_LAUNCH_CHECK();
+  SKB_API_END
+}
+
+int skb_cross_many(const void* descs_dev, int64_t npairs, int64_t total, int64_t* out, void* stream) {
+  SKB_API_BEGIN
+  if (npairs < 0 || npairs > kCrossMaxPairs) raise(SKB_E_ARG, npairs, "cross_many: 0..1024 pairs per launch");
+  if (total < 0) raise(SKB_E_VALUE, total, "cross: negative output size");
+  if (npairs == 0 || total == 0) return SKB_OK;
+  k_cross_many<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(static_cast<const CrossDesc*>(descs_dev),
+                                                                     (int)npairs, total, out);
+  SKB_LAUNCH_CHECK();
   SKB_API_END
 }
 

@@ -172,7 +172,19 @@ def cross_many(pairs, sizes=None) -> list:
     return _cross_pairs(list(pairs), sizes)
 
 
+_CROSS_MAX_PAIRS = 1024  # pairs per skb_cross_many launch
+
+
 def _cross_pairs(pairs, sizes=None):
+    """All pairs in two launches (csrc/hashing.cu k_cross_offsets_many +
+    k_cross_many): one 80-byte descriptor per pair, every pair's offsets in
+    one buffer and every pair's products in another (the results are views)."""
+    if len(pairs) > _CROSS_MAX_PAIRS:
+        k = _CROSS_MAX_PAIRS
+        if sizes is not None and len(sizes) != len(pairs):
+            raise ValueError(f"{len(sizes)} sizes for {len(pairs)} column pairs")
+        return _cross_pairs(pairs[:k], None if sizes is None else sizes[:k]) + \
+            _cross_pairs(pairs[k:], None if sizes is None else sizes[k:])
     t = N.torch()
     prep = []
     for a, b in pairs:
@@ -181,36 +193,51 @@ def _cross_pairs(pairs, sizes=None):
         as_np = not N.is_torch(a.values)
         av, bv = N.to_dev(a.values, "int64").reshape(-1), N.to_dev(b.values, "int64").reshape(-1)
         ao, bo = N.to_dev(a.row_offsets, "int64"), N.to_dev(b.row_offsets, "int64")
-        rows = a.num_rows
-        oo = N.empty((rows + 1,), "int64")
-        N.call("skb_cross_offsets", N.ptr(ao), N.ptr(bo), rows, N.ptr(oo), N.stream_ptr())
-        prep.append((as_np, av, ao, bv, bo, rows, oo))
+        prep.append((as_np, av, ao, bv, bo, a.num_rows))
     if not prep:
         return []
-    flags = None
+    P = len(prep)
+    totals = None
     if sizes is not None:
-        if len(sizes) != len(prep):
-            raise ValueError(f"{len(sizes)} sizes for {len(prep)} column pairs")
+        if len(sizes) != P:
+            raise ValueError(f"{len(sizes)} sizes for {P} column pairs")
         totals = [int(x) for x in sizes]
         if any(x < 0 for x in totals):
             raise ValueError("cross sizes must be >= 0")
-        # caller-supplied sizes are checked against the device totals: inside
-        # deferred_checks() at its exit, otherwise right here (one sync)
-        flags = t.full((len(prep),), -1, dtype=t.int64, device=prep[0][1].device)
-    else:
-        totals = t.stack([p[6][-1] for p in prep]).cpu().tolist()  # the single synchronisation
-    res = []
-    for i, ((as_np, av, ao, bv, bo, rows, oo), total) in enumerate(zip(prep, totals)):
-        out = N.empty((int(total),), "int64")
-        if total or flags is not None:
-            N.call("skb_cross", N.ptr(av), N.ptr(ao), N.ptr(bv), N.ptr(bo), rows, N.ptr(oo), int(total), N.ptr(out),
-                   N.ptr(flags[i:i + 1]) if flags is not None else None, N.stream_ptr())
-        # offsets come from the validated inputs by construction: carried as trusted
-        res.append((as_np, out, oo))
+    dev = prep[0][1].device
+    oo_start = np.zeros(P + 1, np.int64)
+    np.cumsum([r + 1 for *_, r in prep], out=oo_start[1:])
+    oo_all = N.empty((int(oo_start[-1]),), "int64", dev)
+    # caller-supplied sizes are checked against the device totals: inside
+    # deferred_checks() at its exit, otherwise right here (one sync)
+    flags = t.full((P,), -1, dtype=t.int64, device=dev) if totals is not None else None
+    desc = np.zeros((P, 10), np.int64)
+    oo_ptr, fl_ptr = oo_all.data_ptr(), flags.data_ptr() if flags is not None else 0
+    for i, (_, av, ao, bv, bo, rows) in enumerate(prep):
+        desc[i, :6] = (av.data_ptr(), ao.data_ptr(), bv.data_ptr(), bo.data_ptr(), rows, oo_ptr + 8 * oo_start[i])
+        desc[i, 8] = fl_ptr + 8 * i if fl_ptr else 0
+    if totals is not None:
+        desc[:, 6] = totals
+    desc_d = N.to_dev(desc, "int64", dev)
+    N.call("skb_cross_offsets_many", N.ptr(desc_d), P, N.stream_ptr())
+    if totals is None:  # the single synchronisation: every pair's total in one read
+        ends = t.from_numpy(oo_start[1:] - 1).to(dev)
+        totals = [int(x) for x in oo_all[ends].cpu().tolist()]
+        desc[:, 6] = totals
+    base = np.zeros(P + 1, np.int64)
+    np.cumsum(totals, out=base[1:])
+    desc[:, 7] = base[:-1]
+    T = int(base[-1])
+    out_all = N.empty((T,), "int64", dev)
+    if T:
+        desc_d = N.to_dev(desc, "int64", dev)
+        N.call("skb_cross_many", N.ptr(desc_d), P, T, N.ptr(out_all), N.stream_ptr())
+    # offsets come from the validated inputs by construction: carried as trusted
+    res = [(p[0], out_all[base[i]:base[i + 1]], oo_all[oo_start[i]:oo_start[i + 1]]) for i, p in enumerate(prep)]
     if flags is not None:
         stack = getattr(_DEFERRED, "stack", None)
         pending = [(flags[i:i + 1], f"cross_many: sizes[{i}] = {totals[i]} does not match the rows' product count")
-                   for i in range(len(prep))]
+                   for i in range(P)]
         # host (numpy) results are read back here anyway: check them now
         if stack and not any(r[0] for r in res):
             stack[-1].extend(pending)
