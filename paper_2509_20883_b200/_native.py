@@ -14,7 +14,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsparsekit_b200.so")
+# SKB_LIB_PATH: another build of the same library (same-box A/B of kernel variants)
+LIB_PATH = os.environ.get("SKB_LIB_PATH") or os.path.join(_HERE, "libsparsekit_b200.so")
 
 SKB_OK, SKB_E_VALUE, SKB_E_INDEX, SKB_E_KEY, SKB_E_CUDA, SKB_E_NOMEM, SKB_E_ARG, SKB_E_UNSUPPORTED = range(8)
 SKB_E_IO = 8

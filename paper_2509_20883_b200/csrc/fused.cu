@@ -1017,7 +1017,7 @@ __global__ void __launch_bounds__(256) k_fused_tile(const float* __restrict__ ar
 // each per pass: both rows' w, m, v and first dpooled loads are in flight
 // before any arithmetic.  A run continuing past its chunk is finished by the
 // warp owning its head (the next chunk sees no head there).
-constexpr int kFoldBatch = 2;  // gradient rows in flight per run in k_fused_adam's fold
+constexpr int kFoldBatch = 2;  // gradient rows in flight per run in k_fused_adam's fold (same-box A/B: 1, 3, 4 slower)
 
 template <int VEC, int R, int MINB, bool ADAM = true>
 __global__ void __launch_bounds__(256, MINB) k_fused_adam(int64_t n, const uint32_t* __restrict__ skey,
