@@ -2140,7 +2140,9 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
       // hot-id batches (extra gradient rows per run): C5's five tables 6.1 ->
       // 3.4 ms, C3 1.13 -> 0.91 ms, C4 7.99 -> 7.76 ms (B200)
       const int forced = c->adam_var >= 0 ? c->adam_var : adam_variant();
-      const int var = forced ? forced : (adam_tma_fits(mode, D, c->lf_last) ? 0 : 2);
+      // register kernel <4,1,4> with the 2-row fold batch (same-box A/B:
+      // C4 3.07 -> 3.02, C5 6.25 -> 6.21 ms vs <4,1,5>; C1/C3 equal)
+      const int var = forced ? forced : (adam_tma_fits(mode, D, c->lf_last) ? 0 : 3);
       c->last_adam = var;
       switch (var) {
         case 1: k_fused_adam<4, 2, 4><<<grid, 256, 0, s>>>(SKB_ADAM_ARGS); break;

@@ -612,13 +612,13 @@ def test_fused_adam_variants_onehot_sum(skb, variant, D):
                      check=_expect_adam(variant), id_hi=2500)
 
 
-@pytest.mark.parametrize("variant", [0, 2, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("variant", [0, 2, 3, 4, 5, 6, 7, 8])
 def test_fused_adam_variants_mean_hot(skb, variant):
     """Forced fold+Adam variants with mean bags, empty bags and zipf hot ids
     (runs > 32 positions leave the ring for the long fold)."""
     specs = [("a", 700, lambda r, B: r.integers(0, 5, B)), ("zb", 400, lambda r, B: r.integers(1, 9, B))]
     _fused_vs_oracle(skb, 64, specs, steps=4, mode="mean", seed=50 + variant, variants=(variant, -1),
-                     check=_expect_adam(variant if variant else 2))
+                     check=_expect_adam(variant if variant else 3))
 
 
 @pytest.mark.parametrize("D,mode", [(64, "sum"), (64, "mean"), (96, "mean"), (128, "sum"), (128, "mean")])
