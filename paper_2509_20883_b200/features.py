@@ -173,6 +173,59 @@ def cross_many(pairs, sizes=None) -> list:
 
 
 _CROSS_MAX_PAIRS = 1024  # pairs per skb_cross_many launch
+_CROSS_BATCH_MAX_ROWS = 1 << 16  # rows one scanning CTA of k_cross_offsets_many takes in stride
+
+
+def _cross_pairs_each(pairs, sizes=None):
+    """Per-pair launches (multi-CTA scan of each pair's row products): for a
+    single pair or pairs too long for one scanning CTA."""
+    t = N.torch()
+    prep = []
+    for a, b in pairs:
+        if a.num_rows != b.num_rows:
+            raise ValueError(f"row-count mismatch: {a.num_rows} vs {b.num_rows}")
+        as_np = not N.is_torch(a.values)
+        av, bv = N.to_dev(a.values, "int64").reshape(-1), N.to_dev(b.values, "int64").reshape(-1)
+        ao, bo = N.to_dev(a.row_offsets, "int64"), N.to_dev(b.row_offsets, "int64")
+        rows = a.num_rows
+        oo = N.empty((rows + 1,), "int64")
+        N.call("skb_cross_offsets", N.ptr(ao), N.ptr(bo), rows, N.ptr(oo), N.stream_ptr())
+        prep.append((as_np, av, ao, bv, bo, rows, oo))
+    if not prep:
+        return []
+    flags = None
+    if sizes is not None:
+        if len(sizes) != len(prep):
+            raise ValueError(f"{len(sizes)} sizes for {len(prep)} column pairs")
+        totals = [int(x) for x in sizes]
+        if any(x < 0 for x in totals):
+            raise ValueError("cross sizes must be >= 0")
+        # caller-supplied sizes are checked against the device totals: inside
+        # deferred_checks() at its exit, otherwise right here (one sync)
+        flags = t.full((len(prep),), -1, dtype=t.int64, device=prep[0][1].device)
+    else:
+        totals = t.stack([p[6][-1] for p in prep]).cpu().tolist()  # the single synchronisation
+    res = []
+    for i, ((as_np, av, ao, bv, bo, rows, oo), total) in enumerate(zip(prep, totals)):
+        out = N.empty((int(total),), "int64")
+        if total or flags is not None:
+            N.call("skb_cross", N.ptr(av), N.ptr(ao), N.ptr(bv), N.ptr(bo), rows, N.ptr(oo), int(total), N.ptr(out),
+                   N.ptr(flags[i:i + 1]) if flags is not None else None, N.stream_ptr())
+        # offsets come from the validated inputs by construction: carried as trusted
+        res.append((as_np, out, oo))
+    if flags is not None:
+        stack = getattr(_DEFERRED, "stack", None)
+        pending = [(flags[i:i + 1], f"cross_many: sizes[{i}] = {totals[i]} does not match the rows' product count")
+                   for i in range(len(prep))]
+        # host (numpy) results are read back here anyway: check them now
+        if stack and not any(r[0] for r in res):
+            stack[-1].extend(pending)
+        else:
+            _raise_pending(pending)
+    return [RaggedTensor(out.cpu().numpy(), oo.cpu().numpy()) if as_np else RaggedTensor._trusted(out, oo)
+            for as_np, out, oo in res]
+
+
 
 
 def _cross_pairs(pairs, sizes=None):
@@ -185,6 +238,8 @@ def _cross_pairs(pairs, sizes=None):
             raise ValueError(f"{len(sizes)} sizes for {len(pairs)} column pairs")
         return _cross_pairs(pairs[:k], None if sizes is None else sizes[:k]) + \
             _cross_pairs(pairs[k:], None if sizes is None else sizes[k:])
+    if len(pairs) <= 1 or max(a.num_rows for a, _ in pairs) > _CROSS_BATCH_MAX_ROWS:
+        return _cross_pairs_each(pairs, sizes)
     t = N.torch()
     prep = []
     for a, b in pairs:

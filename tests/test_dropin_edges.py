@@ -218,6 +218,55 @@ def test_gpu_counters_after_prefetch(skb):
     assert len(lt.local_table.export_rows()[0]) == 4 * B
 
 
+def test_deferred_verdicts_in_record_order():
+    """CPU: deferred_checks' read-back raises the first recorded failure —
+    plain flags (ValueError with the message) and verdict callables (their
+    exception, or None) in one read, in recording order."""
+    import torch
+    from paper_2509_20883_b200 import features as F
+    ok = torch.full((4,), -1, dtype=torch.int64)
+    seen = []
+    recs = [(torch.tensor([-1]), "never"),
+            (ok, lambda v: seen.append(v) or None),
+            (torch.tensor([-1, 7, -1, -1]), lambda v: IndexError(f"bad {v[1]}")),
+            (torch.tensor([3]), "later")]
+    with pytest.raises(IndexError, match="bad 7"):
+        F._raise_pending(recs)
+    assert seen == [[-1, -1, -1, -1]]
+    with pytest.raises(ValueError, match="later"):
+        F._raise_pending(recs[:2] + recs[3:])
+    F._raise_pending([])
+
+
+@pytest.mark.gpu
+def test_gpu_cross_many_batched(skb):
+    """cross_many's two-launch path (per-pair descriptors) against the
+    oracle pair by pair: empty rows, empty pairs, zero-row pairs, mixed
+    sizes, and more pairs than one launch takes (chunked)."""
+    import torch
+    from oracle import sparse_oracle as O
+    rng = np.random.default_rng(9)
+    pairs, host = [], []
+    for p in range(1100):
+        rows = 0 if p % 97 == 5 else int(rng.integers(1, 40))
+        la = rng.integers(0, 4, rows) * (p % 13 != 3)
+        lb = rng.integers(0, 5, rows)
+        oa, ob = np.concatenate([[0], np.cumsum(la)]), np.concatenate([[0], np.cumsum(lb)])
+        a = rng.integers(-2**62, 2**62, int(oa[-1]))
+        b = rng.integers(-2**62, 2**62, int(ob[-1]))
+        host.append((a, oa, b, ob))
+        dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+        pairs.append((skb.RaggedTensor(dev(a), dev(oa)), skb.RaggedTensor(dev(b), dev(ob))))
+    sizes = [int((np.diff(oa) * np.diff(ob)).sum()) for _, oa, _, ob in host]
+    for kw in ({}, {"sizes": sizes}):
+        with skb.deferred_checks():
+            got = skb.cross_many(pairs, **kw)
+        assert len(got) == len(pairs)
+        for r, (a, oa, b, ob) in zip(got, host):
+            v, o = O.cross_rows(a, oa, b, ob)
+            assert np.array_equal(r.values.cpu().numpy(), v) and np.array_equal(r.row_offsets.cpu().numpy(), o)
+
+
 @pytest.mark.gpu
 def test_gpu_cross_many_sizes_checked(skb):
     """cross_many(sizes=...) trusts nothing: a wrong size raises ValueError
