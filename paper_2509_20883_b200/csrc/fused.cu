@@ -1937,8 +1937,11 @@ static void fused_forward(Table* t, const BatchArgs& a, float* pooled, cudaStrea
           case 3: k_fused_pool_scatter<4, 4, 2><<<grid, 256, 0, s>>>(SKB_POOL_ARGS); break;
           case 5: k_fused_pool_scatter<4, 2, 4><<<grid, 256, 0, s>>>(SKB_POOL_ARGS); break;
           default:
-            static const int stream_min_d = env_int("SKB_POOL_STREAM_MIN_D", 64);
-            if (D >= stream_min_d && D <= 128) {  // wide rows: stream each sub-group's positions (C5: D=128 491 -> 345 us)
+            // stream each sub-group's positions (C5: D=128 491 -> 345 us; and for
+            // the narrow tables too: D=8/16/32 140/183/244 -> 127/140/177 us,
+            // C5 6.20 -> 6.04-6.09 ms same-box)
+            static const int stream_min_d = env_int("SKB_POOL_STREAM_MIN_D", 8);
+            if (D >= stream_min_d && D <= 128) {
               c->last_pool = 6;
               k_fused_pool_stream<8, 3><<<grid, 256, 0, s>>>(SKB_POOL_ARGS);
             } else

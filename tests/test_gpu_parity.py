@@ -621,9 +621,10 @@ def test_fused_adam_variants_mean_hot(skb, variant):
                      check=_expect_adam(variant if variant else 3))
 
 
-@pytest.mark.parametrize("D,mode", [(64, "sum"), (64, "mean"), (96, "mean"), (128, "sum"), (128, "mean")])
+@pytest.mark.parametrize("D,mode", [(8, "mean"), (12, "sum"), (16, "mean"), (32, "sum"), (64, "sum"), (64, "mean"),
+                                    (96, "mean"), (128, "sum"), (128, "mean")])
 def test_fused_pool_stream(skb, D, mode):
-    """Default pool for wide rows (64 <= D <= 128, bags not all one-hot):
+    """Default pool for rows of 8 <= D <= 128 (D % 4 == 0, bags not all one-hot):
     k_fused_pool_stream, sub-groups streaming their bags' positions in
     batches — empty bags, long bags and chunk tails against the oracle."""
     specs = [("a", 1000, lambda r, B: np.where(r.random(B) < 0.1, 0, r.geometric(0.25, B))),
