@@ -2101,7 +2101,8 @@ static void fused_backward(Table* t, const float* dpooled, const skb_adam_t& sc,
     // rows already are the per-position gradients
     int mode = (B.mode == 2 || prescaled) ? 0 : B.mode;
     Scratch scaled;
-    if (mode == 1 && v4 && n >= 8 * B.G) {
+    static const int prescale_ratio = env_int("SKB_PRESCALE_RATIO", 8);
+    if (mode == 1 && v4 && n >= prescale_ratio * B.G) {
       scaled = Scratch(sizeof(float) * B.G * D, s);
       k_scale_bags<<<grid_for(B.G * (D / 4), 256), 256, 0, s>>>(dpooled, B.bag_offs, B.G, D, scaled.as<float>());
       SKB_LAUNCH_CHECK();
