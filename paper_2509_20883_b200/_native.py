@@ -357,6 +357,13 @@ def _staging() -> _H2DStaging:
     return _STAGING
 
 
+def neg_ones(n: int, device=None):
+    """int64[n] of -1 on the device (deferred-check flag arrays): uploaded
+    through the pinned staging ring — a host-to-device copy, not a fill
+    kernel launched into the step."""
+    return to_dev(np.full(n, -1, np.int64), "int64", device)
+
+
 def empty(shape, dtype: str, device=None):
     t = torch()
     dev = t.device("cuda", t.cuda.current_device()) if device is None else t.device(device)

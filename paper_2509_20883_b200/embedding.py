@@ -289,7 +289,7 @@ class EmbeddingTable:
             if pending is None:
                 N.call("skb_table_gather", self._h.h, N.ptr(o), o.numel(), N.ptr(out), N.stream_ptr())
             else:  # deferred_checks(): the liveness check is read at the context's exit
-                flags = N.torch().full((4,), -1, dtype=N.torch().int64, device=o.device)
+                flags = N.neg_ones(4, o.device)
                 N.call("skb_table_gather_deferred", self._h.h, N.ptr(o), o.numel(), N.ptr(out), N.ptr(flags),
                        N.stream_ptr())
                 pending.append((flags, lambda v, o=o: None if v[0] == -1 else IndexError(
@@ -312,7 +312,7 @@ class EmbeddingTable:
             return
         # deferred_checks(): checked and written on the device (nothing is
         # written unless every check passes); the verdict is read at the exit
-        flags = N.torch().full((4,), -1, dtype=N.torch().int64, device=o.device)
+        flags = N.neg_ones(4, o.device)
         N.call("skb_table_scatter_update_deferred", self._h.h, N.ptr(o), o.numel(), N.ptr(r), N.ptr(flags),
                N.stream_ptr())
 

@@ -117,7 +117,7 @@ def _bucketize_flat(vals_d, col_offs_d, C, edges_d, edge_offs_d):
     if n:
         stack = getattr(_DEFERRED, "stack", None)
         if stack:
-            flag = N.torch().full((1,), -1, dtype=N.torch().int64, device=vals_d.device)
+            flag = N.neg_ones(1, vals_d.device)
             N.call("skb_bucketize_multi_async", N.ptr(vals_d), N.ptr(col_offs_d), C, N.ptr(edges_d),
                    N.ptr(edge_offs_d), N.ptr(out), n, N.ptr(flag), N.stream_ptr())
             stack[-1].append((flag, "bucketize input contains NaN"))
@@ -202,7 +202,7 @@ def _cross_pairs_each(pairs, sizes=None):
             raise ValueError("cross sizes must be >= 0")
         # caller-supplied sizes are checked against the device totals: inside
         # deferred_checks() at its exit, otherwise right here (one sync)
-        flags = t.full((len(prep),), -1, dtype=t.int64, device=prep[0][1].device)
+        flags = N.neg_ones(len(prep), prep[0][1].device)
     else:
         totals = t.stack([p[6][-1] for p in prep]).cpu().tolist()  # the single synchronisation
     res = []
@@ -265,7 +265,7 @@ def _cross_pairs(pairs, sizes=None):
     oo_all = N.empty((int(oo_start[-1]),), "int64", dev)
     # caller-supplied sizes are checked against the device totals: inside
     # deferred_checks() at its exit, otherwise right here (one sync)
-    flags = t.full((P,), -1, dtype=t.int64, device=dev) if totals is not None else None
+    flags = N.neg_ones(P, dev) if totals is not None else None
     desc = np.zeros((P, 10), np.int64)
     oo_ptr, fl_ptr = oo_all.data_ptr(), flags.data_ptr() if flags is not None else 0
     for i, (_, av, ao, bv, bo, rows) in enumerate(prep):
@@ -387,7 +387,7 @@ def fused_bucketize(plan: FusedPlan, columns: list) -> list:
         ptrs, offs = ctypes.c_void_p(tab.data_ptr()), ctypes.c_void_p(tab.data_ptr() + 8 * max(C, 1))
         stack = getattr(_DEFERRED, "stack", None)
         if stack:
-            flag = N.torch().full((1,), -1, dtype=N.torch().int64, device=out.device)
+            flag = N.neg_ones(1, out.device)
             N.call("skb_bucketize_cols", ptrs, offs, C, N.ptr(edges), N.ptr(eo), N.ptr(out), n, N.ptr(flag),
                    N.stream_ptr())
             stack[-1].append((flag, "bucketize input contains NaN"))
