@@ -1308,7 +1308,21 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) k_fused_adam_tma(int64_t n,
           float4 x = *reinterpret_cast<const float4*>(sdp + c);
           if (mode == 1) x = vdiv<4>(x, (float)(__ldg(bag_offs + d.bag + 1) - __ldg(bag_offs + d.bag)));
           float4 acc = add4(make_float4(0.f, 0.f, 0.f, 0.f), x);
-          for (uint32_t jj = d.jh + 1; jj < d.je; ++jj) {
+          uint32_t jj = d.jh + 1;
+          // two gradient rows in flight per step of the run, added in
+          // position order (the same FADD sequence: bit-exact)
+          for (; jj + 2 <= d.je; jj += 2) {
+            const uint32_t g0 = __ldg(sval + jj), g1 = __ldg(sval + jj + 1);
+            float4 y0 = ldg4(grad_row(dpooled, zrow, g0, D) + c);
+            float4 y1 = ldg4(grad_row(dpooled, zrow, g1, D) + c);
+            if (mode == 1) {
+              y0 = vdiv<4>(y0, (float)(__ldg(bag_offs + g0 + 1) - __ldg(bag_offs + g0)));
+              y1 = vdiv<4>(y1, (float)(__ldg(bag_offs + g1 + 1) - __ldg(bag_offs + g1)));
+            }
+            acc = add4(acc, y0);
+            acc = add4(acc, y1);
+          }
+          for (; jj < d.je; ++jj) {
             const uint32_t g = __ldg(sval + jj);
             float4 y = ldg4(grad_row(dpooled, zrow, g, D) + c);
             if (mode == 1) y = vdiv<4>(y, (float)(__ldg(bag_offs + g + 1) - __ldg(bag_offs + g)));
@@ -1634,7 +1648,14 @@ static int adam_variant() {
   return v;
 }
 static bool adam_tma_fits(int mode, int D, int64_t recent_long_runs) {
-  return mode == 0 && D >= 48 && recent_long_runs == 0;
+  // SKB_TMA_MEAN_MIN_D: narrowest row width whose mean batches also take the
+  // TMA ring (0: mean batches always take the register kernel)
+  static const int mean_min_d = env_int("SKB_TMA_MEAN_MIN_D", 0);
+  // SKB_TMA_HOT=1: also for batches with recent long runs (the ring defers
+  // them to the long fold like the register kernel)
+  static const int hot = env_int("SKB_TMA_HOT", 0);
+  const bool mode_ok = mode == 0 || (mode == 1 && mean_min_d > 0 && D >= mean_min_d);
+  return mode_ok && D >= 48 && (hot || recent_long_runs == 0);
 }
 static int pool_variant() {
   static int v = env_int("SKB_POOL_VARIANT", 0);
