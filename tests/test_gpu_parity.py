@@ -525,11 +525,14 @@ def test_ragged(skb, golden):
 
 
 def _fused_vs_oracle(skb, D, member_specs, steps, mode, seed=0, evict_every=0, thr=None, cfg=None, k=None, pad=0.0,
-                     variants=None, check=None, id_hi=500):
+                     variants=None, check=None, id_hi=500, mid_export_every=0):
     """Drive the fused step and the oracle pipeline side by side (mode "tile":
     oracle = segment_tile + per-position tile gradients, zero past k).
     variants=(adam, pool) forces the fused kernels; check(step, lt) runs
-    after every backward (e.g. to assert which kernel ran)."""
+    after every backward (e.g. to assert which kernel ran); mid_export_every:
+    every that many steps the rows are exported and compared between a
+    backward and the next forward (a deferred long fold must be joined);
+    mode may be a function of the step."""
     import torch
     rng = np.random.default_rng(seed)
     members = [m for m, _, _ in member_specs]
@@ -538,7 +541,9 @@ def _fused_vs_oracle(skb, D, member_specs, steps, mode, seed=0, evict_every=0, t
         skb.set_variants(lt, *variants)
     olt = O.OracleLogical(f"dim{D}", D, 1, seed=seed, members=members, namespaced=True, evict_threshold=thr)
     cfg = cfg or skb.AdamConfig(lr=1e-2, weight_decay=0.01, variant="adamw")
+    mode_of = mode if callable(mode) else (lambda _step: mode)  # mode per step (a table may switch)
     for step in range(1, steps + 1):
+        mode = mode_of(step)
         ids, offs = [], []
         for m, B, gen in member_specs:
             lens = gen(rng, B)
@@ -580,6 +585,9 @@ def _fused_vs_oracle(skb, D, member_specs, steps, mode, seed=0, evict_every=0, t
                       eps=cfg.eps, weight_decay=cfg.weight_decay, variant=cfg.variant)
         if evict_every and step % evict_every == 0:
             assert lt.evict(step) == olt.evict(step)
+        if mid_export_every and step % mid_export_every == 0 and step < steps:
+            for a, b in zip(lt.local_table.export_rows(), olt.shards[0].export_rows()):
+                eq(a, b)
     for a, b in zip(lt.local_table.export_rows(), olt.shards[0].export_rows()):
         eq(a, b)
     eq(lt.local_table.idmap.free_list, olt.shards[0].free)
@@ -720,6 +728,17 @@ def test_fused_tile_mega_runs_past_k(skb):
     ids' mega runs fold the zero row (packed images included)."""
     specs = [("zlong", 160, lambda r, B: r.integers(100, 300, B))]
     _fused_vs_oracle(skb, 32, specs, steps=2, mode="tile", seed=7, k=40, pad=0.5)
+
+
+def test_fused_tile_hot_rows_mid_export_and_mode_switch(skb):
+    """C4 in miniature over 7 steps with the rows exported between a backward
+    and the next forward every 3rd step (the long-run fold of the hot ids
+    runs on its own stream: every reader must see it joined), then a table
+    switching from tile to mean bags and back."""
+    _fused_vs_oracle(skb, 64, [("zseq", 120, lambda r, B: np.full(B, 400, np.int64))], steps=7, mode="tile", k=400,
+                     seed=11, mid_export_every=3)
+    _fused_vs_oracle(skb, 16, [("zt", 90, lambda r, B: r.integers(100, 300, B))], steps=6,
+                     mode=lambda st: "mean" if st == 4 else "tile", k=40, seed=13, mid_export_every=2)
 
 
 def test_fused_generic_dim(skb):
