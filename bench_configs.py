@@ -530,6 +530,10 @@ def c5(args):
                                capacity_hint=24_000_000 if args.cold else int(os.environ.get("SKB_C5_HINT", 45_000_000))) for d in DIMS5}
     for lt_ in lts.values():
         skb.set_fold_mode(lt_, args.fold)
+    # per-table kernel overrides for A/B runs: SKB_C5_VARIANTS="8:1:-1/16:2:-1" (dim:adam:pool)
+    for spec in filter(None, os.environ.get("SKB_C5_VARIANTS", "").split("/")):
+        d_, a_, p_ = (int(x) for x in spec.split(":"))
+        skb.set_variants(lts[d_], a_, p_)
     prepop_s = None
     if not args.cold:
         t0 = time.perf_counter()
