@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(256) k_write_rows_if_clear(const int64_t* __re
         row[u] = pow2 ? (t >> sh) : t / per_row;  // no 64-bit division for power-of-two row widths
         col[u] = (int)(t - row[u] * per_row) * VEC;
         r[u] = offs[row[u]];
-        if (MODE == 0 && col[u] == 0 && r[u] >= 0 && r[u] < rows) bitmap[r[u] >> 5] = 0u;
+        if (MODE == 0 && bitmap && col[u] == 0 && r[u] >= 0 && r[u] < rows) bitmap[r[u] >> 5] = 0u;
         if (ok) v[u] = vload<VEC>(src + row[u] * (int64_t)D + col[u]);
       }
     }
@@ -474,9 +474,15 @@ static void launch_checked_scatter(Table* t, const int64_t* offs, int64_t n, con
                                                       t->block_size, t->arena_rows, t->bitmap, flags);
   SKB_LAUNCH_CHECK();
   const int D = (int)t->dim;
+  // the distinctness bitmap back to all-clear: one memset when the whole
+  // bitmap is smaller than the rows' scattered sector writes would be (1M
+  // rows over a 1M-row table: 128 KB instead of 1M random 32-byte sector
+  // writes inside the write kernel), per row otherwise (few rows, big table)
+  const bool memset_clear = MODE == 0 && t->bitmap_words * (int64_t)sizeof(uint32_t) <= n * 32;
   k_write_rows_if_clear<VEC, MODE><<<grid_for((n * (D / VEC) + kRowsUnroll - 1) / kRowsUnroll, 256), 256, 0, s>>>(
-      offs, n, src, D, dst, 3 * t->dim, t->arena_rows, t->bitmap, flags);
+      offs, n, src, D, dst, 3 * t->dim, t->arena_rows, memset_clear ? nullptr : t->bitmap, flags);
   SKB_LAUNCH_CHECK();
+  if (memset_clear) SKB_CUDA(cudaMemsetAsync(t->bitmap, 0, sizeof(uint32_t) * t->bitmap_words, s));
 }
 
 // pinned readback of the persistent flags (synchronizes)
@@ -523,7 +529,10 @@ static void check_adam_offsets(Table* t, const int64_t* offs, int64_t n, cudaStr
   k_check_rows<2><<<grid_for(n, 256), 256, 0, s>>>(offs, n, t->live, t->counters, t->ensured_slots, t->block_size,
                                                   t->arena_rows, t->bitmap, t->dflags);
   SKB_LAUNCH_CHECK();
-  k_clear_bits<<<grid_for(n, 256), 256, 0, s>>>(offs, n, t->arena_rows, t->bitmap);
+  if (t->bitmap_words * (int64_t)sizeof(uint32_t) <= n * 32)  // as launch_checked_scatter: memset when cheaper
+    SKB_CUDA(cudaMemsetAsync(t->bitmap, 0, sizeof(uint32_t) * t->bitmap_words, s));
+  else
+    k_clear_bits<<<grid_for(n, 256), 256, 0, s>>>(offs, n, t->arena_rows, t->bitmap);
   SKB_LAUNCH_CHECK();
   const int64_t* f = flags_fetch(t, s);
   const unsigned long long f0 = (uint64_t)f[0], f1 = (uint64_t)f[1], f2 = (uint64_t)f[2];
